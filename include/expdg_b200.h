@@ -1,0 +1,180 @@
+/* expdg_b200 — C ABI of the B200-native exponential-DG hot path.
+ *
+ * Drop-in boundary for the reference library `expdg` (/root/reference/proj,
+ * arXiv 2011.01316).  The reference is a C++20/Eigen library whose plugin
+ * boundary is the split operator
+ *     SplitOperator{dim, LinearAction linear, nonlinear}      proj/include/expdg/split_operator.hpp:12-20
+ *     LinearAction = std::function<VectorXd(const VectorXd&)> proj/include/expdg/phi.hpp:11
+ * produced by burgers_split_operator / euler_split_operator
+ * (proj/include/expdg/burgers.hpp:94-96, proj/include/expdg/euler.hpp:105-107),
+ * consumed by phi_combination (proj/include/expdg/phi.hpp:44-71), step_epi2
+ * (proj/include/expdg/integrators.hpp:29-31) and integrate (:81-82).
+ * Each entry point below replaces one of those; the C++ mirror of the
+ * reference signatures lives in include/expdg_b200.hpp.
+ *
+ * Conventions: plain pointers and sizes; *_dev pointers are CUDA device
+ * pointers (fp64), *_host pointers are host memory; `stream` is a cudaStream_t
+ * (NULL = the context's stream).  Every call returns a status code; the
+ * message of the last failure on the calling thread is expdg_last_error().
+ * A context is not internally synchronised: one host thread per context.
+ */
+#ifndef EXPDG_B200_H
+#define EXPDG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: the reference's exception types (SURVEY.md §8b "Errors"). */
+#define EXPDG_OK 0
+#define EXPDG_E_INVALID 1     /* std::invalid_argument  (e.g. proj/src/burgers.cpp:24-35)      */
+#define EXPDG_E_DOMAIN 2      /* std::domain_error      (proj/src/euler.cpp:27-28, :210-211)    */
+#define EXPDG_E_KRYLOV 3      /* KrylovError            (proj/include/expdg/phi.hpp:61-66)      */
+#define EXPDG_E_CUDA 4        /* device / runtime failure (no reference analogue)             */
+#define EXPDG_E_UNSUPPORTED 5 /* valid for the reference, not on the device path (e.g. over-integration) */
+
+/* Operator kinds. */
+#define EXPDG_BURGERS1D 1 /* BurgersOperator (proj/src/burgers.cpp)                         */
+#define EXPDG_BURGERS2D 2 /* extension: tensor-product LDG Burgers (config C3)               */
+#define EXPDG_EULER2D 3   /* EulerOperator (proj/src/euler.cpp), Lax-Friedrichs split        */
+#define EXPDG_EULER3D 4   /* extension: 3D Lax-Friedrichs Euler (config C5)                  */
+#define EXPDG_DENSE 5     /* dense matrix LinearAction (the test fakes of proj/tests/test_phi.cpp) */
+
+/* Integrator kinds: IntegratorKind (proj/include/expdg/integrators.hpp:15). */
+#define EXPDG_EXP_EULER 0
+#define EXPDG_EPI2 1
+
+typedef struct expdg_ctx expdg_ctx;
+typedef struct expdg_op expdg_op;
+
+/* Mesh + physics of one operator.  Mirrors build_interval_mesh / build_quad_mesh
+ * (proj/include/expdg/mesh.hpp:47-54, uniform breakpoints), BurgersConfig
+ * (proj/include/expdg/burgers.hpp:16-23) and EulerConfig (proj/include/expdg/euler.hpp:33-37). */
+typedef struct {
+  int kind;            /* EXPDG_BURGERS1D .. EXPDG_EULER3D */
+  int order;           /* LGL degree k (device: 1..8) */
+  int nx, ny, nz;      /* elements per axis */
+  double x0, x1, y0, y1, z0, z1;
+  int periodic;        /* 1 periodic, 0 zero-Dirichlet (Burgers 1D/2D only) */
+  double kappa;        /* BurgersConfig::kappa */
+  int flux;            /* Burgers: 0 lax_friedrichs, 1 entropy */
+  double sigma;        /* entropy-flux jump penalty */
+  int sigma_adaptive;
+  int over_integrate;  /* must be 0 on the device path (EXPDG_E_UNSUPPORTED) */
+  double gamma;        /* Euler */
+  int euler_flux;      /* 0 roe (EXPDG_E_UNSUPPORTED on the device path), 1 lax_friedrichs */
+} expdg_op_desc;
+
+/* KrylovSettings (proj/include/expdg/integrators.hpp:20-24) + the two
+ * PhiCombinationProblem knobs it does not expose (proj/include/expdg/phi.hpp:52-53);
+ * 0 selects the reference default for initial_basis (16) / max_substeps (40). */
+typedef struct {
+  double tol;
+  int max_basis;
+  int orth_length;
+  int initial_basis;
+  int max_substeps;
+} expdg_krylov_cfg;
+
+/* KrylovStats (proj/include/expdg/phi.hpp:25-28) + KrylovError::last_estimate. */
+typedef struct {
+  long long iterations;
+  int substeps;
+  double last_estimate;
+} expdg_krylov_stats;
+
+/* TimeLoopConfig (proj/include/expdg/integrators.hpp:58-63). */
+typedef struct {
+  int integrator; /* EXPDG_EPI2 or EXPDG_EXP_EULER */
+  double dt;
+  double t_final;
+  expdg_krylov_cfg krylov;
+  int use_graph;  /* 1: device-resident control in CUDA-graph WHILE nodes; 0: host-stepped control */
+} expdg_time_cfg;
+
+/* IntegrationResult (proj/include/expdg/integrators.hpp:66-74), minus u (in place). */
+typedef struct {
+  double t;
+  int status; /* 0 completed, 1 blew_up (RunStatus) */
+  int steps;
+  long long krylov_iterations;
+  int blow_up_step;
+  double max_abs;
+} expdg_integration_result;
+
+const char* expdg_last_error(void);
+
+/* Context: one device, one stream, the phi-engine workspace. */
+int expdg_ctx_create(int device, expdg_ctx** out);
+int expdg_ctx_destroy(expdg_ctx* ctx);
+void* expdg_ctx_stream(expdg_ctx* ctx);
+int expdg_ctx_synchronize(expdg_ctx* ctx);
+
+/* Operator factory: replaces BurgersOperator / EulerOperator construction
+ * (proj/src/burgers.cpp:20-93, proj/src/euler.cpp:186-244) minus the frozen
+ * state, which expdg_op_linearize supplies. */
+int expdg_op_create(expdg_ctx* ctx, const expdg_op_desc* desc, expdg_op** out);
+/* Dense LinearAction y = A x (row-major n x n, host memory): the dense fakes of
+ * proj/tests/test_phi.cpp:16-29 and proj/tests/test_integrators.cpp:15-23. */
+int expdg_dense_op_create(expdg_ctx* ctx, int n, const double* a_host, expdg_op** out);
+int expdg_op_destroy(expdg_op* op);
+long long expdg_op_dim(const expdg_op* op);
+
+/* Freeze the reference state u~ (copied): burgers_split_operator / euler_split_operator
+ * (proj/src/burgers.cpp:309-320, proj/src/euler.cpp:390-401).  EXPDG_E_DOMAIN on an
+ * inadmissible Euler state (proj/src/euler.cpp:210-211). */
+int expdg_op_linearize(expdg_op* op, const double* ref_dev);
+/* SplitOperator::linear — the JVP (proj/src/burgers.cpp:146-180, proj/src/euler.cpp:299-341). */
+int expdg_op_apply_linear(expdg_op* op, const double* x_dev, double* y_dev, void* stream);
+/* SplitOperator::nonlinear (proj/src/burgers.cpp:182-215, proj/src/euler.cpp:343-388). */
+int expdg_op_apply_nonlinear(expdg_op* op, const double* x_dev, double* y_dev, void* stream);
+/* burgers_full_rhs / euler_full_rhs (proj/include/expdg/burgers.hpp:99-101, euler.hpp:110-111). */
+int expdg_op_full_rhs(expdg_op* op, const double* x_dev, double* y_dev, void* stream);
+
+/* phi_combination (proj/src/phi.cpp:133-260): out = sum_i dt^i phi_i(dt L) b_i with
+ * L the op's linear action at its frozen state; b_dev[0..p], NULL entries are zero
+ * vectors.  Synchronous; EXPDG_E_KRYLOV maps KrylovError (stats->last_estimate set). */
+int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_dev, int p, double dt,
+                          const expdg_krylov_cfg* cfg, double* out_dev, expdg_krylov_stats* stats);
+
+/* step_epi2 (proj/src/integrators.cpp:76-83) with the op linearised at u:
+ * u <- u + phi_combination({0, L u + N u}).  Synchronous. */
+int expdg_step_epi2(expdg_ctx* ctx, expdg_op* op, double* u_dev, double dt, const expdg_krylov_cfg* cfg,
+                    expdg_krylov_stats* stats);
+
+/* integrate (proj/src/integrators.cpp:140-201) for EPI2 (relinearised each step) and
+ * exp_euler (frozen at u0).  u_dev updated in place.  Optional per-step outputs
+ * (capacity `cap`): cumulative Krylov iterations and max|u| (the on_step payload,
+ * proj/include/expdg/integrators.hpp:62).  Blow-up is reported, not returned as an error. */
+int expdg_integrate(expdg_ctx* ctx, expdg_op* op, double* u_dev, const expdg_time_cfg* cfg,
+                    expdg_integration_result* res, long long* iters_per_step, double* amax_per_step, int cap);
+/* Same from/to HOST memory (the H2D / D2H copies are part of the call). */
+int expdg_integrate_host(expdg_ctx* ctx, expdg_op* op, double* u_host, const expdg_time_cfg* cfg,
+                         expdg_integration_result* res, long long* iters_per_step, double* amax_per_step,
+                         int cap);
+
+/* Device matrix exponential (the controller's Higham 2005 expm, one CTA),
+ * n <= 130, row-major host in/out: the Eigen MatrixFunctions exp() call site
+ * proj/src/phi.cpp:40. */
+int expdg_expm(expdg_ctx* ctx, int n, const double* a_host, double* out_host);
+/* Controller state of the last phi call (16 doubles, for diagnostics). */
+int expdg_debug_state(expdg_ctx* ctx, double* out16);
+/* Hessenberg matrix of the last phi call, (129 x 128) row-major (diagnostics). */
+int expdg_debug_hessenberg(expdg_ctx* ctx, double* out);
+
+/* Setup helpers. */
+int expdg_lgl_basis(int order, double* nodes, double* weights, double* diff_rowmajor);
+/* Seeded synthetic inputs of BASELINE.json configs 1..5. */
+int expdg_initial_condition(int config, int nx, int order, uint64_t seed, double noise, double* out_host);
+/* Number of device kernels launched by this context since creation (instrumentation). */
+long long expdg_ctx_kernel_launches(expdg_ctx* ctx);
+/* Device-event time (ms) of the last expdg_integrate call's step loop. */
+double expdg_ctx_last_loop_ms(expdg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EXPDG_B200_H */

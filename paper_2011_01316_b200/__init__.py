@@ -1,0 +1,405 @@
+"""paper_2011_01316_b200 — B200-native exponential-DG hot path.
+
+Python mirror of the reference library's operator API (/root/reference/proj,
+`expdg`): split-operator factory + linearize (burgers_split_operator /
+euler_split_operator), the JVP `apply_linear`, `apply_nonlinear`,
+`full_rhs`, `phi_combination`, `step_epi2` and `integrate`, all executed by
+the sm_100a CUDA library `_build/libexpdg_b200.so` through its C ABI
+(include/expdg_b200.h).  There is no CPU fallback: without the built library
+and a CUDA device every call raises.
+
+PyTorch is plumbing only (device memory and streams).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_build", "libexpdg_b200.so")
+
+EXPDG_OK, EXPDG_E_INVALID, EXPDG_E_DOMAIN, EXPDG_E_KRYLOV, EXPDG_E_CUDA, EXPDG_E_UNSUPPORTED = range(6)
+BURGERS1D, BURGERS2D, EULER2D, EULER3D, DENSE = 1, 2, 3, 4, 5
+INTEGRATORS = {"exp_euler": 0, "epi2": 1}
+
+
+class KrylovError(RuntimeError):
+    """proj/include/expdg/phi.hpp:61-66 — carries the last error estimate."""
+
+    def __init__(self, msg, last_estimate=0.0):
+        super().__init__(msg)
+        self.last_estimate = last_estimate
+
+
+class DeviceError(RuntimeError):
+    pass
+
+
+class UnsupportedError(ValueError):
+    pass
+
+
+class OpDesc(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int), ("order", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+        ("x0", C.c_double), ("x1", C.c_double), ("y0", C.c_double), ("y1", C.c_double),
+        ("z0", C.c_double), ("z1", C.c_double), ("periodic", C.c_int), ("kappa", C.c_double),
+        ("flux", C.c_int), ("sigma", C.c_double), ("sigma_adaptive", C.c_int),
+        ("over_integrate", C.c_int), ("gamma", C.c_double), ("euler_flux", C.c_int),
+    ]
+
+
+class KrylovCfg(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_basis", C.c_int), ("orth_length", C.c_int),
+                ("initial_basis", C.c_int), ("max_substeps", C.c_int)]
+
+
+class KrylovStatsC(C.Structure):
+    _fields_ = [("iterations", C.c_longlong), ("substeps", C.c_int), ("last_estimate", C.c_double)]
+
+
+class TimeCfg(C.Structure):
+    _fields_ = [("integrator", C.c_int), ("dt", C.c_double), ("t_final", C.c_double),
+                ("krylov", KrylovCfg), ("use_graph", C.c_int)]
+
+
+class IntegrationResultC(C.Structure):
+    _fields_ = [("t", C.c_double), ("status", C.c_int), ("steps", C.c_int),
+                ("krylov_iterations", C.c_longlong), ("blow_up_step", C.c_int), ("max_abs", C.c_double)]
+
+
+# symbols declared in include/expdg_b200.h (checked by tests/test_abi.py)
+EXPORTS = [
+    "expdg_last_error", "expdg_ctx_create", "expdg_ctx_destroy", "expdg_ctx_stream", "expdg_ctx_synchronize",
+    "expdg_op_create", "expdg_dense_op_create", "expdg_op_destroy", "expdg_op_dim", "expdg_op_linearize",
+    "expdg_op_apply_linear", "expdg_op_apply_nonlinear", "expdg_op_full_rhs", "expdg_phi_combination",
+    "expdg_step_epi2", "expdg_integrate", "expdg_integrate_host", "expdg_lgl_basis",
+    "expdg_initial_condition", "expdg_ctx_kernel_launches", "expdg_ctx_last_loop_ms", "expdg_expm",
+    "expdg_debug_state", "expdg_debug_hessenberg",
+]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    from . import _build
+    return _build.build(force=force)
+
+
+def lib():
+    """Loads the CUDA library; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(f"expdg CUDA library missing: {LIB_PATH} (run paper_2011_01316_b200._build)")
+    L = C.CDLL(LIB_PATH)
+    vp, dp, i64 = C.c_void_p, C.POINTER(C.c_double), C.c_longlong
+    L.expdg_last_error.restype = C.c_char_p
+    L.expdg_ctx_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.expdg_ctx_destroy.argtypes = [vp]
+    L.expdg_ctx_stream.restype = vp
+    L.expdg_ctx_stream.argtypes = [vp]
+    L.expdg_ctx_synchronize.argtypes = [vp]
+    L.expdg_ctx_kernel_launches.restype = i64
+    L.expdg_ctx_kernel_launches.argtypes = [vp]
+    L.expdg_ctx_last_loop_ms.restype = C.c_double
+    L.expdg_ctx_last_loop_ms.argtypes = [vp]
+    L.expdg_op_create.argtypes = [vp, C.POINTER(OpDesc), C.POINTER(vp)]
+    L.expdg_dense_op_create.argtypes = [vp, C.c_int, dp, C.POINTER(vp)]
+    L.expdg_op_destroy.argtypes = [vp]
+    L.expdg_op_dim.restype = i64
+    L.expdg_op_dim.argtypes = [vp]
+    L.expdg_op_linearize.argtypes = [vp, vp]
+    for f in ("expdg_op_apply_linear", "expdg_op_apply_nonlinear", "expdg_op_full_rhs"):
+        getattr(L, f).argtypes = [vp, vp, vp, vp]
+    L.expdg_phi_combination.argtypes = [vp, vp, C.POINTER(vp), C.c_int, C.c_double, C.POINTER(KrylovCfg), vp,
+                                        C.POINTER(KrylovStatsC)]
+    L.expdg_step_epi2.argtypes = [vp, vp, vp, C.c_double, C.POINTER(KrylovCfg), C.POINTER(KrylovStatsC)]
+    L.expdg_integrate.argtypes = [vp, vp, vp, C.POINTER(TimeCfg), C.POINTER(IntegrationResultC),
+                                  C.POINTER(i64), dp, C.c_int]
+    L.expdg_integrate_host.argtypes = [vp, vp, dp, C.POINTER(TimeCfg), C.POINTER(IntegrationResultC),
+                                       C.POINTER(i64), dp, C.c_int]
+    L.expdg_lgl_basis.argtypes = [C.c_int, dp, dp, dp]
+    L.expdg_expm.argtypes = [vp, C.c_int, dp, dp]
+    L.expdg_debug_state.argtypes = [vp, dp]
+    L.expdg_debug_hessenberg.argtypes = [vp, dp]
+    L.expdg_initial_condition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, dp]
+    _lib = L
+    return L
+
+
+def _check(rc, stats: Optional[KrylovStatsC] = None):
+    if rc == EXPDG_OK:
+        return
+    msg = lib().expdg_last_error().decode()
+    if rc == EXPDG_E_INVALID:
+        raise ValueError(msg)
+    if rc == EXPDG_E_DOMAIN:
+        raise ArithmeticError(msg)
+    if rc == EXPDG_E_KRYLOV:
+        raise KrylovError(msg, stats.last_estimate if stats is not None else 0.0)
+    if rc == EXPDG_E_UNSUPPORTED:
+        raise UnsupportedError(msg)
+    raise DeviceError(msg)
+
+
+def _dptr(t) -> int:
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    return t.data_ptr()
+
+
+def _np_ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+# ---------------------------------------------------------------- setup helpers
+def lgl_basis(order: int):
+    """proj/src/basis.cpp:35-85 (host setup of the device constants)."""
+    n = order + 1
+    x, w, D = np.empty(n), np.empty(n), np.empty((n, n))
+    _check(lib().expdg_lgl_basis(order, _np_ptr(x), _np_ptr(w), _np_ptr(D)))
+    return x, w, D
+
+
+def initial_condition(config: int, nx: int, order: int, seed: int, noise: float = 1e-6) -> np.ndarray:
+    """Seeded synthetic input of BASELINE.json config C<config>."""
+    if config not in (1, 2, 3, 4, 5):
+        raise ValueError("initial_condition: config must be 1..5")
+    comps = {1: 1, 2: 1, 3: 1, 4: 4, 5: 5}[config]
+    npe = {1: order + 1, 2: order + 1, 3: (order + 1) ** 2, 4: (order + 1) ** 2, 5: (order + 1) ** 3}[config]
+    ne = {1: nx, 2: nx, 3: nx * nx, 4: nx * nx, 5: nx ** 3}[config]
+    out = np.empty(ne * npe * comps)
+    _check(lib().expdg_initial_condition(config, nx, order, seed, noise, _np_ptr(out)))
+    return out
+
+
+# ---------------------------------------------------------------- context / operators
+class Context:
+    def __init__(self, device: int = 0):
+        import torch
+        torch.cuda.init()
+        self.device = device
+        h = C.c_void_p()
+        _check(lib().expdg_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().expdg_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def kernel_launches(self) -> int:
+        return lib().expdg_ctx_kernel_launches(self.h)
+
+    @property
+    def last_loop_ms(self) -> float:
+        return lib().expdg_ctx_last_loop_ms(self.h)
+
+    def expm(self, a: np.ndarray) -> np.ndarray:
+        """The device controller's expm (proj/src/phi.cpp:40 restated, Higham 2005)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        out = np.empty_like(a)
+        _check(lib().expdg_expm(self.h, a.shape[0], _np_ptr(a), _np_ptr(out)))
+        return out
+
+    def debug_state(self) -> dict:
+        v = np.zeros(16)
+        _check(lib().expdg_debug_state(self.h, _np_ptr(v)))
+        keys = ["mc", "h", "t", "beta", "avnorm", "last_estimate", "substeps", "iterations", "breakdown",
+                "status", "mmax", "grow_cap", "full_orth", "cycles", "pre_norm", "m"]
+        return dict(zip(keys, v.tolist()))
+
+    def debug_hessenberg(self) -> np.ndarray:
+        h = np.zeros((129, 128))
+        _check(lib().expdg_debug_hessenberg(self.h, _np_ptr(h)))
+        return h
+
+    def synchronize(self):
+        _check(lib().expdg_ctx_synchronize(self.h))
+
+
+@dataclass
+class OperatorSpec:
+    kind: str  # burgers1d | burgers2d | euler2d | euler3d
+    order: int
+    nx: int
+    ny: int = 1
+    nz: int = 1
+    box: tuple = (0.0, 1.0, 0.0, 1.0, 0.0, 1.0)
+    periodic: bool = True
+    kappa: float = 0.03
+    flux: str = "lf"
+    sigma: float = 0.0
+    sigma_adaptive: bool = False
+    over_integrate: bool = False
+    gamma: float = 1.4
+    euler_flux: str = "lf"
+
+    def desc(self) -> OpDesc:
+        d = OpDesc()
+        d.kind = {"burgers1d": BURGERS1D, "burgers2d": BURGERS2D, "euler2d": EULER2D, "euler3d": EULER3D}[self.kind]
+        d.order, d.nx, d.ny, d.nz = self.order, self.nx, self.ny, self.nz
+        d.x0, d.x1, d.y0, d.y1, d.z0, d.z1 = self.box
+        d.periodic = int(self.periodic)
+        d.kappa, d.flux, d.sigma = self.kappa, (1 if self.flux in ("ef", "entropy") else 0), self.sigma
+        d.sigma_adaptive, d.over_integrate = int(self.sigma_adaptive), int(self.over_integrate)
+        d.gamma, d.euler_flux = self.gamma, (0 if self.euler_flux == "roe" else 1)
+        return d
+
+    @property
+    def components(self) -> int:
+        return {"burgers1d": 1, "burgers2d": 1, "euler2d": 4, "euler3d": 5}[self.kind]
+
+
+class Operator:
+    """A DG operator on the device; `linearize(ref)` freezes u~ like the
+    reference split-operator factories (proj/src/burgers.cpp:309-320)."""
+
+    def __init__(self, ctx: Context, spec: Optional[OperatorSpec] = None, dense=None):
+        self.ctx = ctx
+        self.spec = spec
+        h = C.c_void_p()
+        if dense is not None:
+            a = np.ascontiguousarray(dense, dtype=np.float64)
+            _check(lib().expdg_dense_op_create(ctx.h, a.shape[0], _np_ptr(a), C.byref(h)))
+        else:
+            d = spec.desc()
+            _check(lib().expdg_op_create(ctx.h, C.byref(d), C.byref(h)))
+        self.h = h
+        self.dim = lib().expdg_op_dim(h)
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().expdg_op_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def linearize(self, ref):
+        import torch
+        torch.cuda.current_stream().synchronize()
+        _check(lib().expdg_op_linearize(self.h, _dptr(ref)))
+        return self
+
+    def _apply(self, fn, x, out=None):
+        import torch
+        out = torch.empty_like(x) if out is None else out
+        stream = torch.cuda.current_stream().cuda_stream
+        _check(getattr(lib(), fn)(self.h, _dptr(x), _dptr(out), C.c_void_p(stream)))
+        return out
+
+    def apply_linear(self, x, out=None):
+        """SplitOperator::linear — the JVP (proj/src/burgers.cpp:146-180, euler.cpp:299-341)."""
+        return self._apply("expdg_op_apply_linear", x, out)
+
+    def apply_nonlinear(self, x, out=None):
+        return self._apply("expdg_op_apply_nonlinear", x, out)
+
+    def full_rhs(self, x, out=None):
+        return self._apply("expdg_op_full_rhs", x, out)
+
+
+def _kcfg(tol, max_basis, orth_length, initial_basis=0, max_substeps=0) -> KrylovCfg:
+    k = KrylovCfg()
+    k.tol, k.max_basis, k.orth_length = tol, max_basis, orth_length
+    k.initial_basis, k.max_substeps = initial_basis, max_substeps
+    return k
+
+
+@dataclass
+class KrylovStats:
+    iterations: int = 0
+    substeps: int = 0
+    last_estimate: float = 0.0
+
+
+def phi_combination(ctx: Context, op: Operator, b: Sequence, dt: float, tol: float = 1e-12,
+                    max_basis: int = 128, orth_length: int = 128, initial_basis: int = 16,
+                    max_substeps: int = 40, out=None):
+    """proj/src/phi.cpp:133-260: sum_i dt^i phi_i(dt L) b_i; entries of b may be None (zero)."""
+    import torch
+    if len(b) == 0:
+        raise ValueError("phi_combination: empty b list")
+    torch.cuda.current_stream().synchronize()
+    ptrs = (C.c_void_p * len(b))(*[C.c_void_p(_dptr(x) if x is not None else 0) for x in b])
+    if out is None:
+        out = torch.empty(op.dim, dtype=torch.float64, device=f"cuda:{ctx.device}")
+    st = KrylovStatsC()
+    cfg = _kcfg(tol, max_basis, orth_length, initial_basis, max_substeps)
+    rc = lib().expdg_phi_combination(ctx.h, op.h, ptrs, len(b) - 1, dt, C.byref(cfg), C.c_void_p(_dptr(out)),
+                                     C.byref(st))
+    _check(rc, st)
+    return out, KrylovStats(st.iterations, st.substeps, st.last_estimate)
+
+
+def step_epi2(ctx: Context, op: Operator, u, dt: float, tol=1e-12, max_basis=128, orth_length=128):
+    """proj/src/integrators.cpp:76-83 (u updated in place and returned)."""
+    import torch
+    torch.cuda.current_stream().synchronize()
+    st = KrylovStatsC()
+    cfg = _kcfg(tol, max_basis, orth_length)
+    _check(lib().expdg_step_epi2(ctx.h, op.h, C.c_void_p(_dptr(u)), dt, C.byref(cfg), C.byref(st)), st)
+    return u, KrylovStats(st.iterations, st.substeps, st.last_estimate)
+
+
+@dataclass
+class IntegrationResult:
+    """proj/include/expdg/integrators.hpp:66-74."""
+    u: object
+    t: float
+    status: str
+    steps: int
+    krylov_iterations: int
+    blow_up_step: int
+    max_abs: float
+    iters_per_step: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.int64))
+    amax_per_step: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    loop_ms: float = 0.0
+
+
+def integrate(ctx: Context, op: Operator, u0, integrator: str, dt: float, t_final: float, tol=1e-12,
+              max_basis=128, orth_length=128, use_graph: bool = True) -> IntegrationResult:
+    """proj/src/integrators.cpp:140-201 on the device.  `u0` may be a CUDA
+    tensor (updated in place) or a host numpy array (copied in/out inside the call)."""
+    import torch
+    cfg = TimeCfg()
+    cfg.integrator = INTEGRATORS[integrator]
+    cfg.dt, cfg.t_final = dt, t_final
+    cfg.krylov = _kcfg(tol, max_basis, orth_length)
+    cfg.use_graph = int(use_graph)
+    cap = int(math.ceil(t_final / dt + 1e-9)) + 2
+    iters = np.zeros(cap, dtype=np.int64)
+    amax = np.zeros(cap)
+    res = IntegrationResultC()
+    if isinstance(u0, np.ndarray):
+        u = np.ascontiguousarray(u0, dtype=np.float64)
+        _check(lib().expdg_integrate_host(ctx.h, op.h, _np_ptr(u), C.byref(cfg), C.byref(res),
+                                          iters.ctypes.data_as(C.POINTER(C.c_longlong)), _np_ptr(amax), cap))
+    else:
+        u = u0
+        torch.cuda.current_stream().synchronize()
+        _check(lib().expdg_integrate(ctx.h, op.h, C.c_void_p(_dptr(u)), C.byref(cfg), C.byref(res),
+                                     iters.ctypes.data_as(C.POINTER(C.c_longlong)), _np_ptr(amax), cap))
+    n_ok = res.steps if res.status == 0 else res.steps - 1
+    return IntegrationResult(u, res.t, "completed" if res.status == 0 else "blew_up", res.steps,
+                             res.krylov_iterations, res.blow_up_step, res.max_abs, iters[:n_ok].copy(),
+                             amax[:n_ok].copy(), ctx.last_loop_ms)
+
+
+from . import configs  # noqa: E402,F401

@@ -1,0 +1,559 @@
+// C ABI of the B200 exponential-DG hot path (include/expdg_b200.h).
+// Maps the reference's exception types onto status codes.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "krylov.cuh"
+
+namespace expdg {
+void host_initial_condition(int cfg, int nx, int order, uint64_t seed, double noise, double* out);
+void launch_step_begin(cudaStream_t s, PhiState* st, const double* dt_seq);
+void launch_step_finish(cudaStream_t s, PhiState* st, double* u, const double* w, int mode, StepRecord* rec,
+                        double* partials, int grid);
+void launch_absmax(cudaStream_t s, const double* u, long long n, double* out2, int grid);
+int op_check_ref(OpDevice& op, cudaStream_t s, const double* ref);  // 0 ok, 1 not finite, 2 inadmissible
+void device_expm(cudaStream_t s, double* work, int N, double* out);
+
+struct Unsupported : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct KrylovFailure : std::runtime_error {
+  double estimate;
+  KrylovFailure(const std::string& w, double e) : std::runtime_error(w), estimate(e) {}
+};
+}  // namespace expdg
+
+using namespace expdg;
+
+struct expdg_ctx {
+  std::unique_ptr<Engine> eng;
+  long long launches = 0;
+  double last_loop_ms = 0.0;
+  double* udev = nullptr;  // staging for expdg_integrate_host
+  long long udev_len = 0;
+  double* work2 = nullptr;  // small reduction buffer
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+struct expdg_op {
+  expdg_ctx* ctx = nullptr;
+  std::unique_ptr<OpDevice> dev;
+  double* ref_owned = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return EXPDG_OK;
+  } catch (const Unsupported& e) {
+    g_err = e.what();
+    return EXPDG_E_UNSUPPORTED;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return EXPDG_E_INVALID;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return EXPDG_E_DOMAIN;
+  } catch (const KrylovFailure& e) {
+    g_err = e.what();
+    return EXPDG_E_KRYLOV;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return EXPDG_E_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return EXPDG_E_CUDA;
+  }
+}
+
+cudaStream_t pick(expdg_op* op, void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : op->ctx->eng->stream;
+}
+
+bool use_graph_default() {
+  const char* e = std::getenv("EXPDG_HOST_CONTROL");
+  return !(e && e[0] == '1');
+}
+
+void validate_desc(const expdg_op_desc& d) {
+  if (d.kind < EXPDG_BURGERS1D || d.kind > EXPDG_EULER3D) throw std::invalid_argument("unknown operator kind");
+  if (d.order < 1 || d.order > 20) throw std::invalid_argument("lgl_basis: order must be in [1, 20]");
+  if (d.order > 8) throw Unsupported("device operators support orders 1..8");
+  if (d.nx < 1 || ((d.kind == EXPDG_BURGERS2D || d.kind == EXPDG_EULER2D) && d.ny < 1) ||
+      (d.kind == EXPDG_EULER3D && (d.ny < 1 || d.nz < 1)))
+    throw std::invalid_argument("need at least one element per axis");
+  if (!(d.x0 < d.x1)) throw std::invalid_argument("degenerate interval");
+  if (d.kind == EXPDG_BURGERS1D || d.kind == EXPDG_BURGERS2D) {
+    if (!(d.kappa > 0.0)) throw std::invalid_argument("BurgersOperator: kappa must be positive");
+    if (d.sigma < 0.0) throw std::invalid_argument("BurgersOperator: sigma must be nonnegative");
+    if (d.over_integrate) throw Unsupported("over-integrated Burgers is not on the device path");
+  } else {
+    if (!d.periodic) throw std::invalid_argument("EulerOperator: periodic boundaries only");
+    if (d.euler_flux != 1) throw Unsupported("Roe flux is not on the device path (lax_friedrichs only)");
+  }
+}
+
+void map_phi_status(const PhiState& s) {
+  switch (s.status) {
+    case PHI_OK: return;
+    case PHI_ERR_BUDGET: throw KrylovFailure("phi_combination: no convergence within substep budget", s.last_estimate);
+    case PHI_ERR_NONFINITE: throw KrylovFailure("phi_combination: non-finite input", s.last_estimate);
+    case PHI_ERR_UNDERFLOW: throw KrylovFailure("phi_combination: substep underflow", s.last_estimate);
+    case PHI_ERR_DOMAIN: throw std::domain_error("EulerOperator: inadmissible reference state");
+    default: throw CudaError("phi engine: controller did not finish (status " + std::to_string(s.status) + ")");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* expdg_last_error(void) { return g_err.c_str(); }
+
+int expdg_ctx_create(int device, expdg_ctx** out) {
+  return guard([&] {
+    auto c = std::make_unique<expdg_ctx>();
+    c->eng = std::make_unique<Engine>(device);
+    EXPDG_CUDA(cudaMalloc(&c->work2, sizeof(double) * 2 * 4096));
+    EXPDG_CUDA(cudaEventCreate(&c->ev0));
+    EXPDG_CUDA(cudaEventCreate(&c->ev1));
+    *out = c.release();
+  });
+}
+
+int expdg_ctx_destroy(expdg_ctx* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaStreamSynchronize(ctx->eng->stream);
+    cudaFree(ctx->udev);
+    cudaFree(ctx->work2);
+    cudaEventDestroy(ctx->ev0);
+    cudaEventDestroy(ctx->ev1);
+    delete ctx;
+  });
+}
+
+void* expdg_ctx_stream(expdg_ctx* ctx) { return ctx ? (void*)ctx->eng->stream : nullptr; }
+
+int expdg_ctx_synchronize(expdg_ctx* ctx) {
+  return guard([&] { EXPDG_CUDA(cudaStreamSynchronize(ctx->eng->stream)); });
+}
+
+long long expdg_ctx_kernel_launches(expdg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+double expdg_ctx_last_loop_ms(expdg_ctx* ctx) { return ctx ? ctx->last_loop_ms : 0.0; }
+
+int expdg_op_create(expdg_ctx* ctx, const expdg_op_desc* desc, expdg_op** out) {
+  return guard([&] {
+    if (!ctx || !desc) throw std::invalid_argument("null argument");
+    validate_desc(*desc);
+    EXPDG_CUDA(cudaSetDevice(ctx->eng->device));
+    auto op = std::make_unique<expdg_op>();
+    op->ctx = ctx;
+    switch (desc->kind) {
+      case EXPDG_BURGERS1D: op->dev = make_burgers1d(*desc); break;
+      case EXPDG_BURGERS2D: op->dev = make_burgers2d(*desc); break;
+      case EXPDG_EULER2D: op->dev = make_euler2d(*desc); break;
+      case EXPDG_EULER3D: op->dev = make_euler3d(*desc); break;
+    }
+    *out = op.release();
+  });
+}
+
+int expdg_dense_op_create(expdg_ctx* ctx, int n, const double* a_host, expdg_op** out) {
+  return guard([&] {
+    if (!ctx || !a_host || n < 1) throw std::invalid_argument("dense op: bad arguments");
+    auto op = std::make_unique<expdg_op>();
+    op->ctx = ctx;
+    op->dev = make_dense(n, a_host);
+    *out = op.release();
+  });
+}
+
+int expdg_op_destroy(expdg_op* op) {
+  return guard([&] {
+    if (!op) return;
+    cudaFree(op->ref_owned);
+    delete op;
+  });
+}
+
+long long expdg_op_dim(const expdg_op* op) { return op ? op->dev->n : 0; }
+
+int expdg_op_linearize(expdg_op* op, const double* ref_dev) {
+  return guard([&] {
+    if (!op || !ref_dev) throw std::invalid_argument("null argument");
+    cudaStream_t s = op->ctx->eng->stream;
+    const int chk = op_check_ref(*op->dev, s, ref_dev);
+    if (chk == 1) throw std::invalid_argument("reference state not finite");
+    if (chk == 2) throw std::domain_error("EulerOperator: inadmissible reference state");
+    if (!op->ref_owned) EXPDG_CUDA(cudaMalloc(&op->ref_owned, sizeof(double) * op->dev->n));
+    EXPDG_CUDA(cudaMemcpyAsync(op->ref_owned, ref_dev, sizeof(double) * op->dev->n, cudaMemcpyDeviceToDevice, s));
+    op->dev->ref = op->ref_owned;
+  });
+}
+
+static int apply_common(expdg_op* op, int which, const double* x, double* y, void* stream) {
+  return guard([&] {
+    if (!op || !x || !y) throw std::invalid_argument("null argument");
+    if (which != 2 && !op->dev->ref && op->dev->desc.kind != EXPDG_DENSE)
+      throw std::invalid_argument("operator not linearized (call expdg_op_linearize)");
+    cudaStream_t s = pick(op, stream);
+    if (stream) EXPDG_CUDA(cudaStreamSynchronize(op->ctx->eng->stream));
+    op->dev->launch_apply(s, which, x, y);
+    op->ctx->launches++;
+    EXPDG_CUDA(cudaGetLastError());
+  });
+}
+
+int expdg_op_apply_linear(expdg_op* op, const double* x_dev, double* y_dev, void* stream) {
+  return apply_common(op, 0, x_dev, y_dev, stream);
+}
+int expdg_op_apply_nonlinear(expdg_op* op, const double* x_dev, double* y_dev, void* stream) {
+  return apply_common(op, 1, x_dev, y_dev, stream);
+}
+int expdg_op_full_rhs(expdg_op* op, const double* x_dev, double* y_dev, void* stream) {
+  return apply_common(op, 2, x_dev, y_dev, stream);
+}
+
+int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_dev, int p, double dt,
+                          const expdg_krylov_cfg* cfg, double* out_dev, expdg_krylov_stats* stats) {
+  return guard([&] {
+    if (!ctx || !op || !b_dev || !cfg || !out_dev) throw std::invalid_argument("null argument");
+    if (p < 0) throw std::invalid_argument("phi_combination: empty b list");
+    if (p > kMaxP) throw Unsupported("phi_combination: p > 4");
+    if (!(dt > 0.0)) throw std::invalid_argument("phi_combination: dt must be positive");
+    if (cfg->max_basis > kMaxBasis) throw Unsupported("phi_combination: max_basis > 128");
+    if (cfg->max_basis < 1) throw std::invalid_argument("phi_combination: max_basis must be positive");
+    if (!op->dev->ref && op->dev->desc.kind != EXPDG_DENSE)
+      throw std::invalid_argument("operator not linearized (call expdg_op_linearize)");
+    Engine& e = *ctx->eng;
+    const long long n = op->dev->n;
+    PhiState c = e.config(n, p, dt, *cfg);
+    e.ensure(n + p, c.mmax);
+    c = e.config(n, p, dt, *cfg);
+    c.max_steps = 1;
+    e.upload_config(c, e.stream);
+    BArgs b{};
+    b.p = p;
+    for (int i = 0; i <= p; ++i) b.b[i] = b_dev[i];
+    e.run_phi(*op->dev, b, use_graph_default() ? 1 : 0);
+    EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
+    const PhiState& s = *e.st_host;
+    ctx->launches += 2 + s.body_runs * (op->dev->fused_dots() ? 5 : 6);
+    if (stats) {
+      stats->iterations = s.iterations;
+      stats->substeps = s.substeps;
+      stats->last_estimate = s.last_estimate;
+    }
+    map_phi_status(s);
+    EXPDG_CUDA(cudaMemcpyAsync(out_dev, e.slot(0), sizeof(double) * n, cudaMemcpyDeviceToDevice, e.stream));
+    EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int expdg_step_epi2(expdg_ctx* ctx, expdg_op* op, double* u_dev, double dt, const expdg_krylov_cfg* cfg,
+                    expdg_krylov_stats* stats) {
+  return guard([&] {
+    if (!ctx || !op || !u_dev || !cfg) throw std::invalid_argument("null argument");
+    Engine& e = *ctx->eng;
+    const long long n = op->dev->n;
+    if (!op->dev->ref && op->dev->desc.kind != EXPDG_DENSE) {
+      if (expdg_op_linearize(op, u_dev) != EXPDG_OK) {
+        const std::string m = g_err;
+        if (m.find("inadmissible") != std::string::npos) throw std::domain_error(m);
+        throw std::invalid_argument(m);
+      }
+    }
+    e.ensure_scratch(n, 2);
+    double* r = e.scratch;
+    double* t = e.scratch + e.scratch_ld;
+    // r = L u + N u (proj/src/integrators.cpp:79)
+    op->dev->launch_apply(e.stream, 0, u_dev, r);
+    if (op->dev->desc.kind != EXPDG_DENSE) {
+      op->dev->launch_apply(e.stream, 1, u_dev, t);
+      launch_axpy_into(e.stream, r, t, n);
+    }
+    ctx->launches += 3;
+    const double* b[2] = {nullptr, r};
+    expdg_krylov_stats st{};
+    const int rc = expdg_phi_combination(ctx, op, b, 1, dt, cfg, t, &st);
+    if (stats) *stats = st;
+    if (rc == EXPDG_E_KRYLOV) throw KrylovFailure(g_err, st.last_estimate);
+    if (rc != EXPDG_OK) throw CudaError(g_err);
+    launch_axpy_into(e.stream, u_dev, t, n);
+    ctx->launches++;
+    EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+  });
+}
+
+static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_time_cfg* cfg,
+                           expdg_integration_result* res, long long* iters, double* amaxs, int cap) {
+  if (!ctx || !op || !u || !cfg || !res) throw std::invalid_argument("null argument");
+  if (!(cfg->dt > 0.0)) throw std::invalid_argument("integrate: dt must be positive");
+  if (cfg->t_final < cfg->dt) throw std::invalid_argument("integrate: t_final must be at least dt");
+  if (cfg->integrator != EXPDG_EPI2 && cfg->integrator != EXPDG_EXP_EULER)
+    throw Unsupported("integrate: device integrators are epi2 and exp_euler");
+  if (cfg->krylov.max_basis > kMaxBasis) throw Unsupported("max_basis > 128");
+  Engine& e = *ctx->eng;
+  OpDevice& dev = *op->dev;
+  const long long n = dev.n;
+  const int mode = cfg->integrator == EXPDG_EPI2 ? 0 : 1;
+  // dt sequence of proj/src/integrators.cpp:155-157
+  std::vector<double> dts;
+  {
+    double t = 0.0;
+    const double t_end = cfg->t_final * (1.0 - 1e-14);
+    while (t < t_end) {
+      const double dt = std::min(cfg->dt, cfg->t_final - t);
+      dts.push_back(dt);
+      t += dt;
+    }
+  }
+  const int S = (int)dts.size();
+  const int p = 1;
+  PhiState c = e.config(n, p, cfg->dt, cfg->krylov);
+  e.ensure(n + p, c.mmax);
+  e.ensure_scratch(n, 2);
+  double* rbuf = e.scratch;              // EPI2: R ; exp_euler: N(u)
+  double* refbuf = e.scratch + e.scratch_ld;  // exp_euler: frozen u0
+  // max|u0| -> blow-up scale (proj/src/integrators.cpp:148-149)
+  const int rgrid = std::min(4096, std::max(1, (int)std::min<long long>(e.num_sms * 4, (n + 255) / 256)));
+  launch_absmax(e.stream, u, n, ctx->work2, rgrid);
+  std::vector<double> h2(2 * rgrid);
+  EXPDG_CUDA(cudaMemcpyAsync(h2.data(), ctx->work2, sizeof(double) * 2 * rgrid, cudaMemcpyDeviceToHost, e.stream));
+  EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+  double max0 = 0.0;
+  for (int i = 0; i < rgrid; ++i) max0 = std::max(max0, h2[2 * i]);
+  if (mode == 1) {
+    const int chk = op_check_ref(dev, e.stream, u);
+    if (chk == 2) throw std::domain_error("EulerOperator: inadmissible reference state");
+    EXPDG_CUDA(cudaMemcpyAsync(refbuf, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, e.stream));
+  }
+  c = e.config(n, p, cfg->dt, cfg->krylov);
+  c.max_steps = S;
+  c.blow_up_scale = 1e10 * (1.0 + max0);
+  e.upload_config(c, e.stream);
+  double* dts_dev = nullptr;
+  StepRecord* rec_dev = nullptr;
+  EXPDG_CUDA(cudaMalloc(&dts_dev, sizeof(double) * S));
+  EXPDG_CUDA(cudaMalloc(&rec_dev, sizeof(StepRecord) * S));
+  EXPDG_CUDA(cudaMemcpyAsync(dts_dev, dts.data(), sizeof(double) * S, cudaMemcpyHostToDevice, e.stream));
+  const double* saved_ref = dev.ref;
+  dev.ref = mode == 0 ? u : refbuf;
+  BArgs b{};
+  b.p = 1;
+  b.b[0] = mode == 0 ? nullptr : u;
+  b.b[1] = rbuf;
+  const int fgrid = std::min(2048, std::max(1, (int)std::min<long long>(e.num_sms * 4, (n + 255) / 256)));
+  auto pre = [&](cudaStream_t s) {
+    launch_step_begin(s, e.st, dts_dev);
+    if (mode == 0) dev.launch_residual(s, u, rbuf, e.st, e.partials);
+    else dev.launch_apply(s, 1, u, rbuf);
+    e.launch_phi_init(s, b);
+  };
+  auto post = [&](cudaStream_t s) { launch_step_finish(s, e.st, u, e.slot(0), mode, rec_dev, e.partials, fgrid); };
+  const int per_step = 5;
+  const int body_k = dev.fused_dots() ? 5 : 6;
+  cudaGraphExec_t ex = nullptr;
+  const bool graph = cfg->use_graph != 0;
+  int launched = 0;
+  try {
+    if (graph) {
+      cudaGraph_t g;
+      EXPDG_CUDA(cudaGraphCreate(&g, 0));
+      cudaStream_t cs;
+      EXPDG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+      EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      pre(cs);
+      cudaGraphConditionalHandle h;
+      EXPDG_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+      cudaStreamCaptureStatus cst;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      cudaGraph_t cg;
+      EXPDG_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &ndeps));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = h;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cnode;
+      EXPDG_CUDA(cudaGraphAddNode(&cnode, g, deps, ndeps, &cp));
+      EXPDG_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
+      post(cs);
+      EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      e.launch_body(cs, dev, b, h, 1);
+      EXPDG_CUDA(cudaStreamEndCapture(cs, &body));
+      EXPDG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+      cudaGraphDestroy(g);
+      cudaStreamDestroy(cs);
+    }
+    // lagged early-exit check: launch in chunks, look at `stopped` of the chunk before
+    int* stop_host = nullptr;
+    EXPDG_CUDA(cudaMallocHost(&stop_host, sizeof(int) * 2));
+    stop_host[0] = stop_host[1] = 0;
+    cudaEvent_t chunk_ev;
+    EXPDG_CUDA(cudaEventCreateWithFlags(&chunk_ev, cudaEventDisableTiming));
+    EXPDG_CUDA(cudaEventRecord(ctx->ev0, e.stream));
+    const int chunk = 32;
+    bool pending = false;
+    while (launched < S) {
+      const int cnt = std::min(chunk, S - launched);
+      for (int i = 0; i < cnt; ++i) {
+        if (graph) {
+          EXPDG_CUDA(cudaGraphLaunch(ex, e.stream));
+        } else {
+          pre(e.stream);
+          for (int cyc = 0;; ++cyc) {
+            e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0);
+            EXPDG_CUDA(cudaMemcpyAsync(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost, e.stream));
+            EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+            if (e.st_host->action == ACT_DONE || e.st_host->action == ACT_NONE || e.st_host->stopped) break;
+            if (cyc > 10000000) throw CudaError("host-stepped phi did not terminate");
+          }
+          post(e.stream);
+        }
+      }
+      launched += cnt;
+      if (pending) {
+        EXPDG_CUDA(cudaEventSynchronize(chunk_ev));
+        if (stop_host[0]) break;
+      }
+      EXPDG_CUDA(cudaMemcpyAsync(stop_host, &e.st->stopped, sizeof(int), cudaMemcpyDeviceToHost, e.stream));
+      EXPDG_CUDA(cudaEventRecord(chunk_ev, e.stream));
+      pending = true;
+    }
+    EXPDG_CUDA(cudaEventRecord(ctx->ev1, e.stream));
+    EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+    float ms = 0.f;
+    EXPDG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    ctx->last_loop_ms = ms;
+    cudaEventDestroy(chunk_ev);
+    cudaFreeHost(stop_host);
+  } catch (...) {
+    if (ex) cudaGraphExecDestroy(ex);
+    dev.ref = saved_ref;
+    cudaFree(dts_dev);
+    cudaFree(rec_dev);
+    throw;
+  }
+  if (ex) cudaGraphExecDestroy(ex);
+  dev.ref = saved_ref;
+  EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
+  const PhiState st = *e.st_host;
+  ctx->launches += (long long)launched * per_step + st.body_runs * body_k;
+  std::vector<StepRecord> rec(std::max(1, st.step));
+  if (st.step > 0)
+    EXPDG_CUDA(cudaMemcpy(rec.data(), rec_dev, sizeof(StepRecord) * st.step, cudaMemcpyDeviceToHost));
+  cudaFree(dts_dev);
+  cudaFree(rec_dev);
+  res->steps = st.step;
+  res->status = 0;
+  res->blow_up_step = -1;
+  res->max_abs = max0;
+  res->t = 0.0;
+  for (int i = 0; i < st.step; ++i) res->t += dts[i];
+  for (int i = 0; i < st.step; ++i) {
+    if (rec[i].status) {
+      res->status = 1;
+      res->blow_up_step = i + 1;
+      break;
+    }
+    res->max_abs = std::max(res->max_abs, rec[i].amax);
+    if (i < cap) {
+      if (iters) iters[i] = rec[i].iterations_cum;
+      if (amaxs) amaxs[i] = rec[i].amax;
+    }
+  }
+  res->krylov_iterations = st.iterations_total;
+}
+
+int expdg_integrate(expdg_ctx* ctx, expdg_op* op, double* u_dev, const expdg_time_cfg* cfg,
+                    expdg_integration_result* res, long long* iters_per_step, double* amax_per_step, int cap) {
+  return guard([&] { integrate_impl(ctx, op, u_dev, cfg, res, iters_per_step, amax_per_step, cap); });
+}
+
+int expdg_integrate_host(expdg_ctx* ctx, expdg_op* op, double* u_host, const expdg_time_cfg* cfg,
+                         expdg_integration_result* res, long long* iters_per_step, double* amax_per_step,
+                         int cap) {
+  return guard([&] {
+    if (!ctx || !op || !u_host) throw std::invalid_argument("null argument");
+    Engine& e = *ctx->eng;
+    const long long n = op->dev->n;
+    if (ctx->udev_len < n) {
+      cudaFree(ctx->udev);
+      ctx->udev = nullptr;
+      EXPDG_CUDA(cudaMalloc(&ctx->udev, sizeof(double) * n));
+      ctx->udev_len = n;
+    }
+    EXPDG_CUDA(cudaMemcpyAsync(ctx->udev, u_host, sizeof(double) * n, cudaMemcpyHostToDevice, e.stream));
+    integrate_impl(ctx, op, ctx->udev, cfg, res, iters_per_step, amax_per_step, cap);
+    EXPDG_CUDA(cudaMemcpyAsync(u_host, ctx->udev, sizeof(double) * n, cudaMemcpyDeviceToHost, e.stream));
+    EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+  });
+}
+
+int expdg_expm(expdg_ctx* ctx, int n, const double* a_host, double* out_host) {
+  return guard([&] {
+    if (!ctx || n < 1 || n > kMaxBasis + 2) throw std::invalid_argument("expm: 1 <= n <= 130");
+    Engine& e = *ctx->eng;
+    double* out = nullptr;
+    EXPDG_CUDA(cudaMalloc(&out, sizeof(double) * n * n));
+    EXPDG_CUDA(cudaMemcpyAsync(e.ework, a_host, sizeof(double) * n * n, cudaMemcpyHostToDevice, e.stream));
+    device_expm(e.stream, e.ework, n, out);
+    ctx->launches++;
+    EXPDG_CUDA(cudaMemcpyAsync(out_host, out, sizeof(double) * n * n, cudaMemcpyDeviceToHost, e.stream));
+    EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+    cudaFree(out);
+  });
+}
+
+int expdg_debug_state(expdg_ctx* ctx, double* out16) {
+  return guard([&] {
+    Engine& e = *ctx->eng;
+    EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
+    const PhiState& s = *e.st_host;
+    const double v[16] = {(double)s.mc, s.h, s.t, s.beta, s.avnorm, s.last_estimate, (double)s.substeps,
+                          (double)s.iterations, (double)s.breakdown, (double)s.status, (double)s.mmax,
+                          (double)s.grow_cap, (double)s.full_orth, (double)s.cycles, s.pre_norm, (double)s.m};
+    std::memcpy(out16, v, sizeof(v));
+  });
+}
+
+int expdg_debug_hessenberg(expdg_ctx* ctx, double* out /* (kMaxBasis+1) x kMaxBasis */) {
+  return guard([&] {
+    Engine& e = *ctx->eng;
+    EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
+    std::memcpy(out, e.st_host->H, sizeof(e.st_host->H));
+  });
+}
+
+int expdg_lgl_basis(int order, double* nodes, double* weights, double* diff) {
+  return guard([&] {
+    const HostBasis b = host_lgl_basis(order);
+    const int n = order + 1;
+    std::memcpy(nodes, b.nodes.data(), sizeof(double) * n);
+    std::memcpy(weights, b.weights.data(), sizeof(double) * n);
+    std::memcpy(diff, b.D.data(), sizeof(double) * n * n);
+  });
+}
+
+int expdg_initial_condition(int config, int nx, int order, uint64_t seed, double noise, double* out_host) {
+  return guard([&] {
+    if (nx < 1 || !out_host) throw std::invalid_argument("initial_condition: bad arguments");
+    host_initial_condition(config, nx, order, seed, noise, out_host);
+  });
+}
+
+}  // extern "C"

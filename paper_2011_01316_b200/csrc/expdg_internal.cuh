@@ -1,0 +1,229 @@
+// Internal device/host definitions of the B200 exponential-DG engine.
+//
+// Layout in HBM:
+//   * fields: element-major, then component, then node (x fastest), exactly the
+//     reference FieldState layout (proj/include/expdg/mesh.hpp:61-80);
+//   * Krylov basis: (mmax + 2) slots of `ld` doubles, slot 0 doubles as the
+//     running phi vector w (proj/src/phi.cpp:160-165, :227-237), slot i >= 1 holds
+//     V_i UNNORMALISED with a per-slot scale s_i (V_i = s_i * slot_i), so no
+//     normalisation pass is ever streamed; `ld` is padded to a multiple of
+//     kLdAlign with zeros so every tall-skinny tile is a full TMA bulk copy;
+//   * the p augmentation scalars of the phi vector sit at [n, n+p) of every slot.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "expdg_b200.h"
+
+namespace expdg {
+
+constexpr int kMaxBasis = 128;            // proj/include/expdg/phi.hpp:47 default
+constexpr int kMaxSlots = kMaxBasis + 2;  // V_0..V_mmax plus one scratch slot
+constexpr int kMaxP = 4;                  // b_0..b_4 (integrators use p <= 3)
+constexpr int kTailPad = 8;               // [n, n+8) is the tail region of a slot
+constexpr long long kLdAlign = 2048;      // largest tall-skinny tile (doubles)
+constexpr int kTsThreads = 256;
+constexpr int kMaxPartials = 2048;        // max CTAs contributing partial sums
+
+enum Action : int {
+  ACT_NONE = 0,
+  ACT_START = 1,    // phi vector initialised: controller computes beta and resets
+  ACT_EXTEND = 2,   // Arnoldi column j: y = A V_j, orthogonalise (CGS2 / IOP)
+  ACT_AVNORM = 3,   // ||A V_mc|| (proj/src/phi.cpp:195-199)
+  ACT_COMBINE = 4,  // w = V_{0:mc} (beta f(0:mc, 0))  (proj/src/phi.cpp:227)
+  ACT_DONE = 5,
+};
+
+enum Phase : int { PH_SUBSTEP = 0, PH_POST = 1, PH_DECIDE = 2, PH_DONE = 3, PH_EXTEND = 4 };
+
+enum PhiStatus : int {
+  PHI_RUNNING = 0,
+  PHI_OK = 1,
+  PHI_ERR_BUDGET = 2,     // proj/src/phi.cpp:186-188
+  PHI_ERR_NONFINITE = 3,  // proj/src/phi.cpp:191-192
+  PHI_ERR_UNDERFLOW = 4,  // proj/src/phi.cpp:252-253
+  PHI_ERR_DOMAIN = 5,     // inadmissible Euler state (proj/src/euler.cpp:210-211)
+  PHI_ERR_CYCLES = 6,     // safety valve: controller cycle budget exhausted
+};
+
+// Device-resident state of one phi_combination call (and of the step around it).
+struct PhiState {
+  // ---- configuration (host-written at call setup)
+  long long n;       // local head length
+  long long len;     // n + p on the rank holding the tail, else n
+  long long ld;      // slot stride
+  int p;
+  int tail_here;
+  double dt;
+  double tol;
+  int mmax, window, grow_cap, max_substeps, full_orth, initial_basis;
+  int max_cycles;
+  // ---- dynamic control
+  int action, phase, j, j0, k;
+  int target, m, mc, breakdown, status;
+  long long iterations;  // this call
+  int substeps;          // this call
+  int cycles;
+  double beta, avnorm, t, h, last_estimate, pre_norm;
+  // ---- reduced results of the last kernels (raw sums over the local rank)
+  double red_nrmA;  // ||y||^2 after the operator
+  double red_nrmC;  // ||y||^2 after pass C
+  double red_w2;    // ||w_head||^2 after combine / init
+  double red_dotA[kMaxSlots];
+  double red_dotB[kMaxSlots];
+  double bnorm2[kMaxP + 1];
+  // ---- per-slot scale and combine coefficients
+  double scale[kMaxSlots];
+  double comb[kMaxSlots];
+  double tailw[kMaxP];
+  // ---- Hessenberg (mmax+1) x mmax, row stride kMaxBasis
+  double H[(kMaxBasis + 1) * kMaxBasis];
+  // ---- last-block reduction tickets, one per reducing kernel kind
+  unsigned int ticket[16];
+  // ---- step-level bookkeeping (integrate)
+  int stopped;        // a previous step blew up / finished: every kernel no-ops
+  int step;           // steps completed
+  int max_steps;
+  int domain_flag;    // set by operator kernels on inadmissible states
+  int any_b;          // some b_i nonzero
+  long long iterations_total;
+  long long body_runs;  // controller invocations (one per engine cycle)
+  double blow_up_scale;
+  double amax_step;
+};
+
+// One record per integrate step, read back by the host at the end.
+struct StepRecord {
+  double t, dt, amax;
+  long long iterations_cum;
+  int status;  // 0 ok, 1 blew up (KrylovError / domain / non-finite / > scale)
+  int substeps;
+  int phi_status;
+  int pad;
+};
+
+// ---------------------------------------------------------------- errors
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define EXPDG_CUDA(call)                                                                  \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw ::expdg::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Deterministic block sum (fixed tree order).  `buf` needs blockDim/32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* buf) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) buf[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    s = lane < nw ? buf[lane] : 0.0;
+    s = warp_sum(s);
+  }
+  return s;  // valid in thread 0
+}
+
+__device__ __forceinline__ double block_max(double v, double* buf) {
+  v = warp_max(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) buf[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    s = lane < nw ? buf[lane] : 0.0;
+    s = warp_max(s);
+  }
+  return s;
+}
+
+// Last-block deterministic grid reduction: every CTA stores `cnt` partial sums
+// at partials[blockIdx.x * stride + i]; the CTA that arrives last sums them in
+// block order and calls `sink(i, total)`.  Returns true in the last CTA.
+template <class Sink>
+__device__ __forceinline__ bool grid_reduce_last(const double* mine, int cnt, double* partials,
+                                                 int stride, unsigned int* ticket, Sink sink) {
+  __shared__ bool s_last;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) partials[(size_t)blockIdx.x * stride + i] = mine[i];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(ticket, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    double s = 0.0;
+    for (unsigned int b = 0; b < gridDim.x; ++b) s += __ldcg(&partials[(size_t)b * stride + i]);
+    sink(i, s);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ticket = 0u;
+  return true;
+}
+
+// ---------------------------------------------------------------- TMA bulk copy (1D)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__host__ __device__ inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
+}  // namespace expdg

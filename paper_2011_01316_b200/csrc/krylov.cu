@@ -1,0 +1,795 @@
+// Device-resident adaptive Krylov phi engine (the B200 replacement of
+// proj/src/phi.cpp:133-260 and the Arnoldi loop of proj/src/phi.cpp:84-112).
+//
+// One "cycle" of the engine is a fixed sequence of six kernels:
+//   [operator apply] -> [pass A dots] -> [pass B update+dots] -> [pass C update+norm]
+//   -> [combine] -> [controller]
+// Each kernel reads the action chosen by the previous controller from device
+// memory and no-ops when it is not its turn, so the sequence is captured once
+// into the body of a CUDA-graph WHILE node; the controller (one CTA) runs the
+// Higham expm of the small augmented Hessenberg matrix, the reference error
+// estimator and the accept / grow / halve rules, and clears the WHILE
+// condition when the call is done.  No host round-trip per step.
+//
+// Orthogonalisation is classical Gram-Schmidt with one reorthogonalisation
+// (CGS2) instead of the reference's two-pass MGS (proj/src/phi.cpp:94-100): the
+// same projector in exact arithmetic, three streaming passes over V per column
+// instead of 2(k+1) sequential ones.  IOP windows use one pass (reference: one
+// MGS pass over the window).
+#include <algorithm>
+#include <cstring>
+
+#include "krylov.cuh"
+
+namespace expdg {
+
+enum TsMode { TS_DOTS = 0, TS_UPD_DOTS = 1, TS_UPD_NORM = 2, TS_COMBINE = 3 };
+enum Ticket { TK_DOTS = 0, TK_UPD_DOTS = 1, TK_UPD_NORM = 2, TK_COMBINE = 3, TK_APPLY = 4, TK_INIT = 5,
+              TK_RES = 6, TK_FINISH = 7, TK_MAX = 8 };
+
+constexpr int kTsSmemBytes = 196608;  // 2 stages of (k + 1) x T doubles
+constexpr int kAccPerLane = (kMaxSlots + 7) / 8;
+
+// ------------------------------------------------------------------ tall-skinny passes
+// Streams the k active basis tiles (and y) through shared memory with 1D TMA
+// bulk copies, double buffered on mbarriers; T adapts to k so a stage is
+// ~96 KB in flight per SM.
+template <int MODE>
+__global__ void __launch_bounds__(kTsThreads) k_ts(PhiState* st, double* base, double* partials) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ uint64_t bars[2];
+  __shared__ int s_active, s_i0, s_k, s_y, s_T;
+  __shared__ long long s_ld, s_n;
+  __shared__ double s_coef[kMaxSlots];
+  __shared__ double s_red[kMaxSlots + 1];
+  __shared__ double s_buf[kTsThreads / 32];
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int active = 0, i0 = 0, k = 0, y = 0;
+    if (!st->stopped) {
+      const int a = st->action;
+      if (MODE == TS_DOTS) active = a == ACT_EXTEND;
+      else if (MODE == TS_UPD_DOTS) active = a == ACT_EXTEND && st->full_orth;
+      else if (MODE == TS_UPD_NORM) active = a == ACT_EXTEND;
+      else active = a == ACT_COMBINE;
+    }
+    if (active) {
+      if (MODE == TS_COMBINE) { i0 = 0; k = st->mc; y = 0; }
+      else { i0 = st->j0; k = st->j - st->j0 + 1; y = st->j + 1; }
+    }
+    const int nst = k + (MODE == TS_COMBINE ? 0 : 1);
+    int T = 2048;
+    while (T > 64 && 2 * nst * T * 8 > kTsSmemBytes) T >>= 1;
+    s_active = active; s_i0 = i0; s_k = k; s_y = y; s_T = T;
+    s_ld = st->ld; s_n = st->n;
+    if (active) {
+      mbar_init(&bars[0], 1);
+      mbar_init(&bars[1], 1);
+      fence_mbar_init();
+    }
+  }
+  __syncthreads();
+  if (!s_active) return;
+  const int i0 = s_i0, k = s_k, T = s_T;
+  const long long ld = s_ld, n = s_n;
+  for (int i = tid; i < k; i += blockDim.x) {
+    const int slot = i0 + i;
+    const double s = st->scale[slot];
+    double c;
+    if (MODE == TS_DOTS) c = 0.0;
+    else if (MODE == TS_UPD_DOTS) c = s * s * st->red_dotA[slot];
+    else if (MODE == TS_UPD_NORM) c = s * s * (st->full_orth ? st->red_dotB[slot] : st->red_dotA[slot]);
+    else c = s * st->comb[slot];
+    s_coef[i] = c;
+  }
+  const bool hasY = MODE != TS_COMBINE;
+  const int nst = k + (hasY ? 1 : 0);
+  double* ybase = base + (size_t)s_y * ld;
+  const long long ntiles = ld / T;
+  double* stage[2] = {smem, smem + (size_t)nst * T};
+  const uint32_t tile_bytes = (uint32_t)T * 8u;
+
+  auto issue = [&](long long tl, int s) {
+    if (tid == 0 && tl < ntiles) {
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&bars[s], tile_bytes * (uint32_t)nst);
+      for (int q = 0; q < k; ++q)
+        bulk_g2s(stage[s] + (size_t)q * T, base + (size_t)(i0 + q) * ld + tl * T, tile_bytes, &bars[s]);
+      if (hasY) bulk_g2s(stage[s] + (size_t)k * T, ybase + tl * T, tile_bytes, &bars[s]);
+    }
+  };
+  __syncthreads();
+  issue(blockIdx.x, 0);
+  issue((long long)blockIdx.x + gridDim.x, 1);
+
+  double acc[kAccPerLane];
+#pragma unroll
+  for (int v = 0; v < kAccPerLane; ++v) acc[v] = 0.0;
+  double nacc = 0.0;
+  const int lane = tid & 31, wid = tid >> 5;
+  int it = 0;
+  for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x, ++it) {
+    const int s = it & 1;
+    mbar_wait(&bars[s], (it >> 1) & 1);
+    double* V = stage[s];
+    double* Y = stage[s] + (size_t)k * T;
+    const long long g0 = tl * T;
+    if (MODE == TS_UPD_DOTS || MODE == TS_UPD_NORM) {
+      for (int d = tid; d < T; d += blockDim.x) {
+        double yv = Y[d];
+        for (int i = 0; i < k; ++i) yv = fma(-s_coef[i], V[(size_t)i * T + d], yv);
+        Y[d] = yv;
+        ybase[g0 + d] = yv;
+        if (MODE == TS_UPD_NORM) nacc = fma(yv, yv, nacc);
+      }
+      if (MODE == TS_UPD_DOTS) __syncthreads();
+    } else if (MODE == TS_COMBINE) {
+      for (int d = tid; d < T; d += blockDim.x) {
+        double wv = 0.0;
+        for (int i = 0; i < k; ++i) wv = fma(s_coef[i], V[(size_t)i * T + d], wv);
+        base[g0 + d] = wv;  // slot 0, in place (this tile already staged)
+        if (g0 + d < n) nacc = fma(wv, wv, nacc);
+      }
+    }
+    if (MODE == TS_DOTS || MODE == TS_UPD_DOTS) {
+#pragma unroll
+      for (int v = 0; v < kAccPerLane; ++v) {
+        const int i = wid + 8 * v;
+        if (i < k) {
+          const double* Vi = V + (size_t)i * T;
+          double a = acc[v];
+          for (int d = lane; d < T; d += 32) a = fma(Vi[d], Y[d], a);
+          acc[v] = a;
+        }
+      }
+    }
+    __syncthreads();
+    issue(tl + 2LL * gridDim.x, s);
+  }
+
+  // ---- deterministic reductions
+  if (MODE == TS_DOTS || MODE == TS_UPD_DOTS) {
+#pragma unroll
+    for (int v = 0; v < kAccPerLane; ++v) {
+      const int i = wid + 8 * v;
+      const double r = warp_sum(acc[v]);
+      if (i < k && lane == 0) s_red[i] = r;
+    }
+    __syncthreads();
+    double* dst = MODE == TS_DOTS ? st->red_dotA : st->red_dotB;
+    grid_reduce_last(s_red, k, partials, kMaxSlots, &st->ticket[MODE == TS_DOTS ? TK_DOTS : TK_UPD_DOTS],
+                     [&](int i, double v) { dst[i0 + i] = v; });
+  } else {
+    const double tot = block_sum(nacc, s_buf);
+    if (tid == 0) s_red[0] = tot;
+    __syncthreads();
+    grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[MODE == TS_COMBINE ? TK_COMBINE : TK_UPD_NORM],
+                     [&](int, double v) {
+                       if (MODE == TS_COMBINE) st->red_w2 = v;
+                       else st->red_nrmC = v;
+                     });
+  }
+}
+
+// ------------------------------------------------------------------ phi init
+// w = [b_0; 0 ... 0, 1] (proj/src/phi.cpp:160-165); ||b_i||^2 for the all-zero
+// early exit (proj/src/phi.cpp:141-145) and ||w_head||^2 for beta.
+__global__ void __launch_bounds__(256) k_phi_init(PhiState* st, double* slot0, BArgs b, double* partials) {
+  __shared__ double s_buf[8];
+  __shared__ double s_red[kMaxP + 2];
+  if (st->stopped) return;
+  const long long n = st->n;
+  double acc[kMaxP + 1];
+#pragma unroll
+  for (int i = 0; i <= kMaxP; ++i) acc[i] = 0.0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long d = (long long)blockIdx.x * blockDim.x + threadIdx.x; d < n; d += stride) {
+    const double w0 = b.b[0] ? b.b[0][d] : 0.0;
+    slot0[d] = w0;
+#pragma unroll
+    for (int i = 0; i <= kMaxP; ++i)
+      if (i <= b.p && b.b[i]) {
+        const double v = b.b[i][d];
+        acc[i] = fma(v, v, acc[i]);
+      }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here)
+    slot0[n + threadIdx.x] = (b.p > 0 && (int)threadIdx.x == b.p - 1) ? 1.0 : 0.0;
+#pragma unroll
+  for (int i = 0; i <= kMaxP; ++i) {
+    const double t = block_sum(acc[i], s_buf);
+    if (threadIdx.x == 0) s_red[i] = t;
+  }
+  __syncthreads();
+  grid_reduce_last(s_red, kMaxP + 1, partials, kMaxSlots, &st->ticket[TK_INIT], [&](int i, double v) {
+    st->bnorm2[i] = v;
+  });
+}
+
+// ------------------------------------------------------------------ block dense linear algebra
+__device__ void blk_matmul(double* C, const double* A, const double* B, int N) {
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    const int i = idx / N, j = idx - i * N;
+    double s = 0.0;
+    for (int k = 0; k < N; ++k) s = fma(A[i * N + k], B[k * N + j], s);
+    C[idx] = s;
+  }
+  __syncthreads();
+}
+
+// out = sum c_m M_m + ident * I
+__device__ void blk_lincomb(double* out, int N, int cnt, const double* c, const double* const* M, double ident) {
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    double s = 0.0;
+    for (int m = 0; m < cnt; ++m) s += c[m] * M[m][idx];
+    if (idx / N == idx % N) s += ident;
+    out[idx] = s;
+  }
+  __syncthreads();
+}
+
+// Solves A X = B (partial pivoting, first maximal pivot), B overwritten.
+__device__ void blk_lu_solve(double* A, double* B, int N) {
+  __shared__ int s_piv;
+  const int tid = threadIdx.x;
+  for (int k = 0; k < N; ++k) {
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = k;
+      for (int i = k + tid; i < N; i += 32) {
+        const double v = fabs(A[i * N + k]);
+        if (v > best) { best = v; bi = i; }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (tid == 0) s_piv = bi;
+    }
+    __syncthreads();
+    const int p = s_piv;
+    if (p != k) {
+      for (int j = tid; j < N; j += blockDim.x) {
+        double t = A[k * N + j]; A[k * N + j] = A[p * N + j]; A[p * N + j] = t;
+        t = B[k * N + j]; B[k * N + j] = B[p * N + j]; B[p * N + j] = t;
+      }
+      __syncthreads();
+    }
+    const double d = A[k * N + k];
+    for (int i = k + 1 + tid; i < N; i += blockDim.x) A[i * N + k] = A[i * N + k] / d;
+    __syncthreads();
+    const int rows = N - k - 1;
+    for (int idx = tid; idx < rows * N; idx += blockDim.x) {
+      const int i = k + 1 + idx / N, j = idx % N;
+      const double l = A[i * N + k];
+      if (j > k) A[i * N + j] -= l * A[k * N + j];
+      B[i * N + j] -= l * B[k * N + j];
+    }
+    __syncthreads();
+  }
+  for (int j = tid; j < N; j += blockDim.x) {
+    for (int i = N - 1; i >= 0; --i) {
+      double s = B[i * N + j];
+      for (int kk = i + 1; kk < N; ++kk) s -= A[i * N + kk] * B[kk * N + j];
+      B[i * N + j] = s / A[i * N + i];
+    }
+  }
+  __syncthreads();
+}
+
+// Higham (2005) scaling and squaring, the algorithm of Eigen's MatrixFunctions
+// exp() (proj/src/phi.cpp:40).  A (N x N) in W[0]; result in *out (one of W's).
+__device__ double* blk_expm(double* W, int N) {
+  __shared__ double s_l1;
+  __shared__ int s_sq;
+  __shared__ double s_buf[32];
+  const size_t NN = (size_t)N * N;
+  double* A = W;
+  double* A2 = W + NN;
+  double* A4 = W + 2 * NN;
+  double* A6 = W + 3 * NN;
+  double* A8 = W + 4 * NN;
+  double* U = W + 5 * NN;
+  double* V = W + 6 * NN;
+  double* T1 = W + 7 * NN;
+  double* T2 = W + 8 * NN;
+  // 1-norm
+  double colmax = 0.0;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < N; ++i) s += fabs(A[i * N + j]);
+    colmax = fmax(colmax, s);
+  }
+  const double l1 = block_max(colmax, s_buf);
+  if (threadIdx.x == 0) s_l1 = l1;
+  __syncthreads();
+  const double nrm = s_l1;
+  int deg;
+  if (nrm < 1.495585217958292e-002) deg = 3;
+  else if (nrm < 2.539398330063230e-001) deg = 5;
+  else if (nrm < 9.504178996162932e-001) deg = 7;
+  else if (nrm < 2.097847961257068e+000) deg = 9;
+  else deg = 13;
+  if (deg == 13) {
+    if (threadIdx.x == 0) {
+      int e;
+      frexp(nrm / 5.371920351148152, &e);
+      s_sq = e < 0 ? 0 : e;
+    }
+    __syncthreads();
+    const int sq = s_sq;
+    for (size_t idx = threadIdx.x; idx < NN; idx += blockDim.x) A[idx] = ldexp(A[idx], -sq);
+    __syncthreads();
+  } else if (threadIdx.x == 0) {
+    s_sq = 0;
+  }
+  __syncthreads();
+  blk_matmul(A2, A, A, N);
+  if (deg == 3) {
+    const double b[] = {120.0, 60.0, 12.0, 1.0};
+    { const double c[] = {b[3]}; const double* M[] = {A2}; blk_lincomb(T1, N, 1, c, M, b[1]); }
+    blk_matmul(U, A, T1, N);
+    { const double c[] = {b[2]}; const double* M[] = {A2}; blk_lincomb(V, N, 1, c, M, b[0]); }
+  } else if (deg == 5) {
+    const double b[] = {30240.0, 15120.0, 3360.0, 420.0, 30.0, 1.0};
+    blk_matmul(A4, A2, A2, N);
+    { const double c[] = {b[5], b[3]}; const double* M[] = {A4, A2}; blk_lincomb(T1, N, 2, c, M, b[1]); }
+    blk_matmul(U, A, T1, N);
+    { const double c[] = {b[4], b[2]}; const double* M[] = {A4, A2}; blk_lincomb(V, N, 2, c, M, b[0]); }
+  } else if (deg == 7) {
+    const double b[] = {17297280.0, 8648640.0, 1995840.0, 277200.0, 25200.0, 1512.0, 56.0, 1.0};
+    blk_matmul(A4, A2, A2, N);
+    blk_matmul(A6, A4, A2, N);
+    { const double c[] = {b[7], b[5], b[3]}; const double* M[] = {A6, A4, A2}; blk_lincomb(T1, N, 3, c, M, b[1]); }
+    blk_matmul(U, A, T1, N);
+    { const double c[] = {b[6], b[4], b[2]}; const double* M[] = {A6, A4, A2}; blk_lincomb(V, N, 3, c, M, b[0]); }
+  } else if (deg == 9) {
+    const double b[] = {17643225600.0, 8821612800.0, 2075673600.0, 302702400.0, 30270240.0,
+                        2162160.0,     110880.0,     3960.0,       90.0,        1.0};
+    blk_matmul(A4, A2, A2, N);
+    blk_matmul(A6, A4, A2, N);
+    blk_matmul(A8, A6, A2, N);
+    { const double c[] = {b[9], b[7], b[5], b[3]}; const double* M[] = {A8, A6, A4, A2}; blk_lincomb(T1, N, 4, c, M, b[1]); }
+    blk_matmul(U, A, T1, N);
+    { const double c[] = {b[8], b[6], b[4], b[2]}; const double* M[] = {A8, A6, A4, A2}; blk_lincomb(V, N, 4, c, M, b[0]); }
+  } else {
+    const double b[] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
+                        1187353796428800.0,  129060195264000.0,   10559470521600.0,
+                        670442572800.0,      33522128640.0,       1323241920.0,
+                        40840800.0,          960960.0,            16380.0,
+                        182.0,               1.0};
+    blk_matmul(A4, A2, A2, N);
+    blk_matmul(A6, A4, A2, N);
+    { const double c[] = {b[13], b[11], b[9]}; const double* M[] = {A6, A4, A2}; blk_lincomb(T1, N, 3, c, M, 0.0); }
+    blk_matmul(T2, A6, T1, N);
+    { const double c[] = {1.0, b[7], b[5], b[3]}; const double* M[] = {T2, A6, A4, A2}; blk_lincomb(T1, N, 4, c, M, b[1]); }
+    blk_matmul(U, A, T1, N);
+    { const double c[] = {b[12], b[10], b[8]}; const double* M[] = {A6, A4, A2}; blk_lincomb(T1, N, 3, c, M, 0.0); }
+    blk_matmul(T2, A6, T1, N);
+    { const double c[] = {1.0, b[6], b[4], b[2]}; const double* M[] = {T2, A6, A4, A2}; blk_lincomb(V, N, 4, c, M, b[0]); }
+  }
+  // numer = U + V -> T1 ; denom = V - U -> T2 ; solve denom X = numer
+  { const double c[] = {1.0, 1.0}; const double* M[] = {U, V}; blk_lincomb(T1, N, 2, c, M, 0.0); }
+  { const double c[] = {-1.0, 1.0}; const double* M[] = {U, V}; blk_lincomb(T2, N, 2, c, M, 0.0); }
+  blk_lu_solve(T2, T1, N);
+  double* cur = T1;
+  double* oth = A2;
+  for (int i = 0; i < s_sq; ++i) {
+    blk_matmul(oth, cur, cur, N);
+    double* t = cur; cur = oth; oth = t;
+  }
+  return cur;
+}
+
+// Standalone device expm (one CTA) of an N x N matrix in W[0..N*N); result copied to out.
+__global__ void __launch_bounds__(256) k_expm(double* W, int N, double* out) {
+  const double* F = blk_expm(W, N);
+  for (int i = threadIdx.x; i < N * N; i += blockDim.x) out[i] = F[i];
+}
+
+void device_expm(cudaStream_t s, double* work, int N, double* out) { k_expm<<<1, 256, 0, s>>>(work, N, out); }
+
+// ------------------------------------------------------------------ controller
+__device__ __forceinline__ void set_window(PhiState* st, int j) {
+  st->j = j;
+  st->j0 = st->full_orth ? 0 : max(0, j + 1 - st->window);
+  st->k = j - st->j0 + 1;
+}
+
+__global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double* W,
+                                             cudaGraphConditionalHandle cond, int use_graph) {
+  __shared__ int s_phase, s_exit, s_zeroH, s_done;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    st->body_runs++;
+    s_exit = 0; s_zeroH = 0; s_done = 0;
+    if (st->stopped || st->action == ACT_DONE || st->action == ACT_NONE) {
+      s_done = 1;
+    } else {
+      st->cycles++;
+      int phase = st->phase;
+      switch (st->action) {
+        case ACT_START:
+          phase = PH_SUBSTEP;
+          break;
+        case ACT_EXTEND: {
+          const int j = st->j;
+          const double* sc = st->scale;
+          for (int i = st->j0; i <= j; ++i) {
+            const double h1 = sc[i] * st->red_dotA[i];
+            const double h2 = st->full_orth ? sc[i] * st->red_dotB[i] : 0.0;
+            st->H[i * kMaxBasis + j] = st->full_orth ? (h1 + h2) : h1;
+          }
+          const double pre_norm = sqrt(st->red_nrmA);
+          const double hnext = sqrt(st->red_nrmC);
+          st->pre_norm = pre_norm;
+          st->H[(j + 1) * kMaxBasis + j] = hnext;
+          const int mc = j + 1;
+          st->mc = mc;
+          st->iterations++;
+          if (hnext <= 1e-14 * fmax(pre_norm, 1e-300)) {
+            st->H[mc * kMaxBasis + (mc - 1)] = 0.0;
+            st->breakdown = 1;
+            phase = PH_POST;
+          } else {
+            st->scale[mc] = 1.0 / hnext;
+            if (mc < st->target) {
+              set_window(st, mc);
+              st->action = ACT_EXTEND;
+              s_exit = 1;
+            } else {
+              phase = PH_POST;
+            }
+          }
+          break;
+        }
+        case ACT_AVNORM:
+          st->avnorm = sqrt(st->red_nrmA);
+          phase = PH_DECIDE;
+          break;
+        case ACT_COMBINE: {
+          double w2 = st->red_w2;
+          if (st->tail_here)
+            for (int j = 0; j < st->p; ++j) slot0[st->n + j] = st->tailw[j];
+          for (int j = 0; j < st->p; ++j) w2 += st->tailw[j] * st->tailw[j];
+          st->red_w2 = w2;
+          phase = st->t < 1.0 - 1e-14 ? PH_SUBSTEP : PH_DONE;
+          break;
+        }
+        default:
+          break;
+      }
+      if (st->cycles > st->max_cycles) {
+        st->status = PHI_ERR_CYCLES;
+        phase = PH_DONE;
+        s_exit = 0;
+      }
+      s_phase = phase;
+    }
+  }
+  __syncthreads();
+  if (s_done) {
+    if (tid == 0 && use_graph) cudaGraphSetConditional(cond, 0u);
+    return;
+  }
+  while (!s_exit) {
+    const int phase = s_phase;
+    if (phase == PH_DECIDE) {
+      // hbar (mc+2)^2 = [H(0:mc, 0:mc-1) 0; 0 .. 1 0], scaled by h (proj/src/phi.cpp:208-211)
+      const int mc = st->mc, N = mc + 2;
+      const double h = st->h;
+      for (int idx = tid; idx < N * N; idx += blockDim.x) {
+        const int i = idx / N, j = idx % N;
+        double v = 0.0;
+        if (i <= mc && j < mc) v = st->H[i * kMaxBasis + j];
+        if (i == mc + 1 && j == mc) v = 1.0;
+        W[idx] = h * v;
+      }
+      __syncthreads();
+      const double* F = blk_expm(W, N);
+      if (tid == 0) {
+        const double beta = st->beta;
+        double err = 0.0;
+        if (!st->breakdown) {
+          const double p1 = fabs(beta * F[mc * N]);
+          const double p2 = fabs(beta * F[(mc + 1) * N]) * st->avnorm;
+          if (p1 > 10.0 * p2) err = p2;
+          else if (p1 > p2) err = p1 * p2 / (p1 - p2);
+          else err = p1;
+        }
+        st->last_estimate = err;
+        const double tol = st->tol;
+        if (st->breakdown || err <= 0.5 * tol * beta * h) {
+          for (int i = 0; i < mc; ++i) st->comb[i] = beta * F[i * N];
+          const double t = st->t + h;
+          st->t = t;
+          st->substeps++;
+          for (int j = 0; j < st->p; ++j) {
+            double v = 1.0;
+            for (int q = 1; q <= st->p - 1 - j; ++q) v *= st->dt * t / q;
+            st->tailw[j] = v;
+          }
+          double hn = h;
+          if (err < 1e-3 * tol * beta * h) hn *= 2.0;
+          st->h = fmin(hn, 1.0 - t);
+          st->action = ACT_COMBINE;
+          s_exit = 1;
+        } else if (mc < st->grow_cap) {
+          const int m = min(st->grow_cap, max(mc + 1, (3 * mc) / 2));
+          st->m = m;
+          st->target = m;
+          set_window(st, mc);
+          st->action = ACT_EXTEND;
+          s_exit = 1;
+        } else {
+          st->h = h * 0.5;
+          if (st->h < 1e-12) {
+            st->status = PHI_ERR_UNDERFLOW;
+            s_phase = PH_DONE;
+          }
+        }
+      }
+      __syncthreads();
+      continue;
+    }
+    if (tid == 0) {
+      if (phase == PH_SUBSTEP) {
+        if (st->substeps >= st->max_substeps) {
+          st->status = PHI_ERR_BUDGET;
+          s_phase = PH_DONE;
+        } else {
+          const double beta = sqrt(st->red_w2);
+          if (beta == 0.0) {
+            s_phase = PH_DONE;
+          } else if (!isfinite(beta)) {
+            st->status = PHI_ERR_NONFINITE;
+            st->last_estimate = beta;
+            s_phase = PH_DONE;
+          } else {
+            st->beta = beta;
+            st->mc = 0;
+            st->breakdown = 0;
+            st->scale[0] = 1.0 / beta;
+            st->target = st->m;
+            set_window(st, 0);
+            st->action = ACT_EXTEND;
+            s_zeroH = 1;
+            s_exit = 1;
+          }
+        }
+      } else if (phase == PH_POST) {
+        if (!st->breakdown) {
+          st->j = st->mc;
+          st->action = ACT_AVNORM;
+          st->iterations++;
+          s_exit = 1;
+        } else {
+          st->avnorm = 0.0;
+          s_phase = PH_DECIDE;
+        }
+      } else if (phase == PH_DONE) {
+        if (st->status == PHI_RUNNING) st->status = PHI_OK;
+        st->action = ACT_DONE;
+        s_done = 1;
+        s_exit = 1;
+      }
+    }
+    __syncthreads();
+  }
+  if (s_zeroH) {
+    const int rows = st->mmax + 1;
+    for (int idx = tid; idx < rows * kMaxBasis; idx += blockDim.x) st->H[idx] = 0.0;
+  }
+  if (tid == 0) st->phase = s_phase;
+  if (tid == 0 && s_done && use_graph) cudaGraphSetConditional(cond, 0u);
+}
+
+// Sets action = START / DONE after the init reduction (separate tiny kernel so the
+// decision sees the fully reduced norms).
+__global__ void k_phi_start(PhiState* st) {
+  if (st->stopped) return;
+  int any = 0;
+  for (int i = 0; i <= st->p; ++i) any |= st->bnorm2[i] > 0.0;
+  st->any_b = any;
+  st->iterations = 0;
+  st->substeps = 0;
+  st->cycles = 0;
+  st->t = 0.0;
+  st->h = 1.0;
+  st->m = min(st->initial_basis, st->mmax);
+  st->mc = 0;
+  st->breakdown = 0;
+  st->last_estimate = 0.0;
+  st->red_w2 = st->bnorm2[0] + (st->p > 0 ? 1.0 : 0.0);
+  for (int j = 0; j < kMaxP; ++j) st->tailw[j] = (j == st->p - 1) ? 1.0 : 0.0;
+  if (st->domain_flag) {
+    st->status = PHI_ERR_DOMAIN;
+    st->action = ACT_DONE;
+  } else if (!any) {
+    st->status = PHI_OK;
+    st->action = ACT_DONE;
+  } else {
+    st->status = PHI_RUNNING;
+    st->action = ACT_START;
+  }
+  st->phase = PH_SUBSTEP;
+}
+
+// ------------------------------------------------------------------ host side
+Engine::Engine(int dev) : device(dev) {
+  EXPDG_CUDA(cudaSetDevice(dev));
+  EXPDG_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  EXPDG_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  EXPDG_CUDA(cudaMalloc(&st, sizeof(PhiState)));
+  EXPDG_CUDA(cudaMemset(st, 0, sizeof(PhiState)));
+  EXPDG_CUDA(cudaMallocHost(&st_host, sizeof(PhiState)));
+  EXPDG_CUDA(cudaMalloc(&partials, sizeof(double) * kMaxPartials * kMaxSlots));
+  ework_doubles = size_t(9) * (kMaxBasis + 2) * (kMaxBasis + 2);
+  EXPDG_CUDA(cudaMalloc(&ework, sizeof(double) * ework_doubles));
+  EXPDG_CUDA(cudaFuncSetAttribute(k_ts<TS_DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes));
+  EXPDG_CUDA(cudaFuncSetAttribute(k_ts<TS_UPD_DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes));
+  EXPDG_CUDA(cudaFuncSetAttribute(k_ts<TS_UPD_NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes));
+  EXPDG_CUDA(cudaFuncSetAttribute(k_ts<TS_COMBINE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTsSmemBytes));
+}
+
+Engine::~Engine() {
+  cudaFree(base);
+  cudaFree(st);
+  cudaFreeHost(st_host);
+  cudaFree(partials);
+  cudaFree(ework);
+  cudaFree(scratch);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void Engine::ensure(long long len, int mmax) {
+  const long long need_ld = round_up(len + kTailPad, kLdAlign);
+  const int need_slots = mmax + 2;
+  if (base && need_ld == ld && need_slots <= slots) {
+    // the zero padding beyond [0, len) must hold for every slot: clear stale
+    // data from a previous call with a longer vector
+    if (len != cur_len) EXPDG_CUDA(cudaMemsetAsync(base, 0, sizeof(double) * (size_t)ld * slots, stream));
+    cur_len = len;
+    return;
+  }
+  cur_len = len;
+  if (base) EXPDG_CUDA(cudaFree(base));
+  base = nullptr;
+  ld = need_ld;
+  slots = need_slots;
+  EXPDG_CUDA(cudaMalloc(&base, sizeof(double) * (size_t)ld * slots));
+  EXPDG_CUDA(cudaMemset(base, 0, sizeof(double) * (size_t)ld * slots));
+}
+
+void Engine::ensure_scratch(long long len, int count) {
+  const long long need = round_up(len + kTailPad, kLdAlign);
+  if (scratch && scratch_ld >= need) return;
+  if (scratch) EXPDG_CUDA(cudaFree(scratch));
+  scratch_ld = need;
+  EXPDG_CUDA(cudaMalloc(&scratch, sizeof(double) * (size_t)need * count));
+  EXPDG_CUDA(cudaMemset(scratch, 0, sizeof(double) * (size_t)need * count));
+}
+
+PhiState Engine::config(long long n, int p, double dt, const expdg_krylov_cfg& kc) const {
+  PhiState c;
+  std::memset(&c, 0, sizeof(c));
+  c.n = n;
+  c.p = p;
+  c.tail_here = 1;
+  c.len = n + p;
+  c.ld = ld;
+  c.dt = dt;
+  c.tol = std::max(kc.tol, 5e-15);  // proj/src/phi.cpp:167
+  const long long dim = n + p;
+  c.mmax = (int)std::min<long long>(kc.max_basis, dim);  // :168
+  c.initial_basis = kc.initial_basis > 0 ? kc.initial_basis : 16;
+  c.max_substeps = kc.max_substeps > 0 ? kc.max_substeps : 40;
+  const int orth = kc.orth_length;
+  c.full_orth = (orth >= c.mmax || dim <= std::max(c.initial_basis, 16)) ? 1 : 0;  // :171-173
+  c.window = c.full_orth ? c.mmax : orth;
+  c.grow_cap = c.full_orth ? c.mmax : std::min(c.mmax, 32);  // :177
+  c.max_cycles = 200000;
+  c.action = ACT_NONE;
+  return c;
+}
+
+// Uploads only the configuration prefix of PhiState (dynamic fields are reset on device).
+void Engine::upload_config(const PhiState& c, cudaStream_t s) {
+  std::memcpy(st_host, &c, sizeof(PhiState));
+  EXPDG_CUDA(cudaMemcpyAsync(st, st_host, sizeof(PhiState), cudaMemcpyHostToDevice, s));
+}
+
+void Engine::launch_phi_init(cudaStream_t s, const BArgs& b) {
+  const int grid = num_sms * 2;
+  k_phi_init<<<grid, 256, 0, s>>>(st, slot(0), b, partials);
+  k_phi_start<<<1, 1, 0, s>>>(st);
+}
+
+static int ts_grid(const Engine& e) {
+  const long long tiles = e.ld / 256;
+  return (int)std::max<long long>(1, std::min<long long>(e.num_sms, tiles));
+}
+
+void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
+                         int use_graph) {
+  const int g = ts_grid(*this);
+  op.launch_phi_apply(s, st, base, partials, b);
+  if (!op.fused_dots()) k_ts<TS_DOTS><<<g, kTsThreads, kTsSmemBytes, s>>>(st, base, partials);
+  k_ts<TS_UPD_DOTS><<<g, kTsThreads, kTsSmemBytes, s>>>(st, base, partials);
+  k_ts<TS_UPD_NORM><<<g, kTsThreads, kTsSmemBytes, s>>>(st, base, partials);
+  k_ts<TS_COMBINE><<<g, kTsThreads, kTsSmemBytes, s>>>(st, base, partials);
+  k_ctl<<<1, 256, 0, s>>>(st, slot(0), ework, h, use_graph);
+}
+
+void Engine::run_phi(OpDevice& op, const BArgs& b, int use_graph) {
+  if (use_graph) {
+    cudaGraphExec_t ex = build_phi_graph(op, b);
+    EXPDG_CUDA(cudaGraphLaunch(ex, stream));
+    EXPDG_CUDA(cudaStreamSynchronize(stream));
+    cudaGraphExecDestroy(ex);
+    return;
+  }
+  launch_phi_init(stream, b);
+  for (int cyc = 0; cyc < 1000000; ++cyc) {
+    launch_body(stream, op, b, cudaGraphConditionalHandle{}, 0);
+    EXPDG_CUDA(cudaMemcpyAsync(st_host, st, sizeof(PhiState), cudaMemcpyDeviceToHost, stream));
+    EXPDG_CUDA(cudaStreamSynchronize(stream));
+    if (st_host->action == ACT_DONE || st_host->action == ACT_NONE || st_host->stopped) return;
+  }
+  throw std::runtime_error("phi host loop did not terminate");
+}
+
+cudaGraphExec_t Engine::build_phi_graph(OpDevice& op, const BArgs& b) {
+  cudaGraph_t g;
+  EXPDG_CUDA(cudaGraphCreate(&g, 0));
+  cudaStream_t cs;
+  EXPDG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  // init part
+  EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  launch_phi_init(cs, b);
+  cudaGraphConditionalHandle h;
+  EXPDG_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  cudaGraph_t cg;
+  EXPDG_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &ndeps));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode;
+  EXPDG_CUDA(cudaGraphAddNode(&cnode, g, deps, ndeps, &cp));
+  EXPDG_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
+  EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  launch_body(cs, op, b, h, 1);
+  EXPDG_CUDA(cudaStreamEndCapture(cs, &body));
+  cudaGraphExec_t ex;
+  EXPDG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+  cudaGraphDestroy(g);
+  cudaStreamDestroy(cs);
+  return ex;
+}
+
+// ------------------------------------------------------------------ utilities
+__global__ void k_axpy_into(double* u, const double* w, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) u[i] += w[i];
+}
+__global__ void k_copy(double* d, const double* s, long long n) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) d[i] = s[i];
+}
+void launch_axpy_into(cudaStream_t s, double* u, const double* w, long long n) {
+  k_axpy_into<<<592, 256, 0, s>>>(u, w, n);
+}
+void launch_copy(cudaStream_t s, double* dst, const double* src, long long n) {
+  k_copy<<<592, 256, 0, s>>>(dst, src, n);
+}
+
+}  // namespace expdg

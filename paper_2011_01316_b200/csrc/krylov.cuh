@@ -1,0 +1,96 @@
+// Host-side interface of the device-resident phi engine (krylov.cu) and of the
+// operator kernels (ops_*.cu).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "expdg_internal.cuh"
+
+namespace expdg {
+
+// Vectors b_1..b_p that the augmented operator adds (proj/src/phi.cpp:151-158).
+struct BArgs {
+  const double* b[kMaxP + 1];  // b[0] .. b[p]; nullptr = zero vector
+  int p;
+};
+
+// Device operator: one DG operator frozen at a reference state (ũ pointer).
+class OpDevice {
+ public:
+  virtual ~OpDevice() = default;
+  expdg_op_desc desc{};
+  long long n = 0;        // local DOF count
+  int comps = 1;
+  const double* ref = nullptr;  // ũ (device), not owned
+  // Cycle apply: y = dt * aug(s_j V_j) into slot j+1 plus ||y||^2 (action EXTEND/AVNORM).
+  virtual void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials,
+                                const BArgs& b) = 0;
+  // Standalone: which 0 = L x (at ref), 1 = N x (at ref), 2 = full rhs (no ref).
+  virtual void launch_apply(cudaStream_t s, int which, const double* x, double* y) = 0;
+  // Step residual R = L u + N u at ref = u, with ||R||^2 -> st->bnorm2[1] and the
+  // inadmissibility flag -> st->domain_flag.  Skipped when st->stopped.
+  virtual void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st,
+                               double* partials) = 0;
+  // Whether the apply kernel also writes pass-A dots (else the generic kernel runs).
+  virtual bool fused_dots() const { return false; }
+};
+
+std::unique_ptr<OpDevice> make_burgers1d(const expdg_op_desc& d);
+std::unique_ptr<OpDevice> make_burgers2d(const expdg_op_desc& d);
+std::unique_ptr<OpDevice> make_euler2d(const expdg_op_desc& d);
+std::unique_ptr<OpDevice> make_euler3d(const expdg_op_desc& d);
+std::unique_ptr<OpDevice> make_dense(int n, const double* a_host);
+
+// Host-side LGL basis (same arithmetic as proj/src/basis.cpp:35-85).
+struct HostBasis {
+  int order = 0;
+  std::vector<double> nodes, weights, D;  // D row-major
+};
+HostBasis host_lgl_basis(int order);
+
+// Device workspace + launch helpers of the phi engine.
+class Engine {
+ public:
+  explicit Engine(int device);
+  ~Engine();
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t stream = nullptr;
+
+  // workspace
+  long long ld = 0;
+  int slots = 0;
+  long long cur_len = -1;
+  double* base = nullptr;      // slots * ld
+  PhiState* st = nullptr;
+  PhiState* st_host = nullptr;  // pinned mirror
+  double* partials = nullptr;
+  double* ework = nullptr;     // expm workspace
+  size_t ework_doubles = 0;
+  double* scratch = nullptr;   // 2 vectors of ld: R and a spare
+  long long scratch_ld = 0;
+
+  void ensure(long long len, int mmax);
+  void ensure_scratch(long long len, int count);
+  double* slot(int i) const { return base + (size_t)i * ld; }
+
+  // Host-computed configuration for a phi call (proj/src/phi.cpp:133-183).
+  PhiState config(long long n, int p, double dt, const expdg_krylov_cfg& kc) const;
+  void upload_config(const PhiState& cfg, cudaStream_t s);
+
+  // Kernel sequences.
+  void launch_phi_init(cudaStream_t s, const BArgs& b);
+  void launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
+                   int use_graph);
+  // Runs one phi call to completion; host-stepped or graph-driven control.
+  void run_phi(OpDevice& op, const BArgs& b, int use_graph);
+  // Builds a while-node graph around launch_body; caller owns the exec.
+  cudaGraphExec_t build_phi_graph(OpDevice& op, const BArgs& b);
+};
+
+// Small utility kernels.
+void launch_axpy_into(cudaStream_t s, double* u, const double* w, long long n);  // u += w
+void launch_copy(cudaStream_t s, double* dst, const double* src, long long n);
+
+}  // namespace expdg

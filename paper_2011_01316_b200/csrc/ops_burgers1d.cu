@@ -1,0 +1,453 @@
+// 1D viscous Burgers LDG operators on sm_100a: the JVP L x
+// (proj/src/burgers.cpp:146-180), N x (:182-215) and the full RHS (:217-265),
+// collocated LGL (over_integrate = false), periodic or zero-Dirichlet.
+//
+// One thread per element over a CTA tile of 128 elements staged (with a
+// one-element halo each side) in shared memory by coalesced loads; the LDG
+// gradient of the two neighbours is recomputed at the shared face node instead
+// of being written to HBM, so L x streams x, u~ and (in the phi cycle) b_1 once
+// and writes y once: 32 B/DOF (SURVEY.md §8d canonical JVP bytes).
+#include <algorithm>
+
+#include "krylov.cuh"
+
+namespace expdg {
+
+namespace {
+
+constexpr int kB1Threads = 128;
+
+template <int NP>
+struct B1P {
+  int ne;
+  int periodic;
+  double a, b;
+  double kappa, sigma;
+  int entropy, sigma_adaptive;
+  double w[NP];
+  double G[NP * NP];   // grad_vol(i,j) = w_i D(i,j)      (proj/src/burgers.cpp:49)
+  double Lv[NP * NP];  // lift_vol(i,j) = D(j,i) w_j      (proj/src/burgers.cpp:50)
+  const double* ut;
+  long long n;
+};
+
+// x_e of the uniform breakpoints (proj/src/mesh.cpp:11-16)
+__device__ __forceinline__ double b1_break(double a, double b, int i, int ne) {
+  return i == ne ? b : a + (b - a) * i / ne;
+}
+
+template <int NP>
+__device__ __forceinline__ double b1_face_flux(const B1P<NP>& P, int mode, double um, double up, double utm,
+                                               double utp, double qstar, double h) {
+  const double jump = um - up;  // normal = +1 on every face this helper sees
+  double lin = 0.0;
+  if (mode != 2) {
+    const double diss = 0.5 * fmax(fabs(utm), fabs(utp));
+    lin = 0.5 * (utm * um + utp * up) + diss * jump;
+  }
+  if (mode == 0) return P.kappa * qstar - lin;
+  double nl;
+  if (!P.entropy) {
+    const double ahs = 0.25 * (um * um + up * up);
+    nl = ahs + 0.5 * fmax(fabs(um), fabs(up)) * jump;
+  } else {
+    double soh;
+    if (mode == 1) {
+      const double sig = P.sigma_adaptive ? P.kappa / 100.0 + h * fmax(fabs(utm), fabs(utp)) : P.sigma;
+      soh = sig * (1.0 / h);
+    } else {
+      soh = P.sigma_adaptive ? P.kappa / (100.0 * h) + fmax(fabs(um), fabs(up)) : P.sigma / h;
+    }
+    const double ahs = 0.25 * (um * um + up * up);
+    const double avg = 0.5 * (um + up);
+    nl = (ahs + avg * avg) / 3.0 + soh * jump;
+  }
+  if (mode == 1) return lin - nl;
+  return P.kappa * qstar - nl;
+}
+
+// Element e of the operator; x*/u* point at NP values of the left / centre /
+// right elements (left/right ignored when the face is a Dirichlet boundary).
+template <int NP>
+__device__ __forceinline__ void b1_element(const B1P<NP>& P, int mode, int e, const double* xL,
+                                           const double* xC, const double* xR, const double* uL,
+                                           const double* uC, const double* uR, double* out) {
+  constexpr int N = NP - 1;
+  const bool hasL = P.periodic || e > 0;
+  const bool hasR = P.periodic || e < P.ne - 1;
+  const int eL = e == 0 ? P.ne - 1 : e - 1;
+  const int eR = e == P.ne - 1 ? 0 : e + 1;
+  const double hC = b1_break(P.a, P.b, e + 1, P.ne) - b1_break(P.a, P.b, e, P.ne);
+  const double hL = b1_break(P.a, P.b, eL + 1, P.ne) - b1_break(P.a, P.b, eL, P.ne);
+  const double hR = b1_break(P.a, P.b, eR + 1, P.ne) - b1_break(P.a, P.b, eR, P.ne);
+  double q[NP], qLN = 0.0, qR0 = 0.0;
+  if (mode != 1) {
+    // LDG gradient (proj/src/burgers.cpp:105-130)
+    double r[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) s = fma(P.G[i * NP + j], xC[j], s);
+      r[i] = s;
+    }
+    if (hasL) {
+      const double us = 0.5 * (xL[N] + xC[0]);
+      r[0] -= (us - xC[0]);
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) s = fma(P.G[N * NP + j], xL[j], s);
+      s += (us - xL[N]);
+      qLN = (2.0 / hL) * (s / P.w[N]);
+    } else {
+      r[0] += -1.0 * (0.0 - xC[0]);
+    }
+    if (hasR) {
+      const double us = 0.5 * (xC[N] + xR[0]);
+      r[N] += (us - xC[N]);
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) s = fma(P.G[j], xR[j], s);
+      s -= (us - xR[0]);
+      qR0 = (2.0 / hR) * (s / P.w[0]);
+    } else {
+      r[N] += (0.0 - xC[N]);
+    }
+    const double c = 2.0 / hC;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) q[i] = c * (r[i] / P.w[i]);
+  }
+  // volume: gq = kappa q - u~ x | u~ x - x^2/2 | kappa q - x^2/2 ; r = -lift gq
+  double gq[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    const double x = xC[p];
+    if (mode == 0) gq[p] = fma(-uC[p], x, P.kappa * q[p]);
+    else if (mode == 1) gq[p] = uC[p] * x - 0.5 * (x * x);
+    else gq[p] = P.kappa * q[p] - 0.5 * (x * x);
+  }
+  double r[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) s = fma(P.Lv[i * NP + p], gq[p], s);
+    r[i] = -s;
+  }
+  // faces (proj/src/burgers.cpp:159-173)
+  if (hasL) {
+    const double f = b1_face_flux(P, mode, xL[N], xC[0], mode == 2 ? 0.0 : uL[N], mode == 2 ? 0.0 : uC[0],
+                                  0.5 * (qLN + q[0]), hL);
+    r[0] -= f;
+  } else {
+    // boundary face: owner e, node 0, normal -1, ghost 0; q** one-sided
+    const double um = xC[0];
+    const double jump = -um;
+    double f;
+    const double utm = mode == 2 ? 0.0 : uC[0];
+    const double lin = 0.5 * (utm * um + 0.0) + 0.5 * fmax(fabs(utm), 0.0) * jump;
+    if (mode == 0) {
+      f = P.kappa * q[0] - lin;
+    } else {
+      double nl;
+      if (!P.entropy) {
+        nl = 0.25 * (um * um) + 0.5 * fabs(um) * jump;
+      } else {
+        double soh;
+        if (mode == 1) soh = (P.sigma_adaptive ? P.kappa / 100.0 + hC * fabs(utm) : P.sigma) * (1.0 / hC);
+        else soh = P.sigma_adaptive ? P.kappa / (100.0 * hC) + fabs(um) : P.sigma / hC;
+        const double avg = 0.5 * um;
+        nl = (0.25 * (um * um) + avg * avg) / 3.0 + soh * jump;
+      }
+      f = mode == 1 ? lin - nl : P.kappa * q[0] - nl;
+    }
+    r[0] += -1.0 * f;
+  }
+  if (hasR) {
+    const double f = b1_face_flux(P, mode, xC[N], xR[0], mode == 2 ? 0.0 : uC[N], mode == 2 ? 0.0 : uR[0],
+                                  0.5 * (q[N] + qR0), hC);
+    r[N] += f;
+  } else {
+    const double um = xC[N];
+    const double jump = um;
+    const double utm = mode == 2 ? 0.0 : uC[N];
+    const double lin = 0.5 * (utm * um + 0.0) + 0.5 * fmax(fabs(utm), 0.0) * jump;
+    double f;
+    if (mode == 0) {
+      f = P.kappa * q[N] - lin;
+    } else {
+      double nl;
+      if (!P.entropy) {
+        nl = 0.25 * (um * um) + 0.5 * fabs(um) * jump;
+      } else {
+        double soh;
+        if (mode == 1) soh = (P.sigma_adaptive ? P.kappa / 100.0 + hC * fabs(utm) : P.sigma) * (1.0 / hC);
+        else soh = P.sigma_adaptive ? P.kappa / (100.0 * hC) + fabs(um) : P.sigma / hC;
+        const double avg = 0.5 * um;
+        nl = (0.25 * (um * um) + avg * avg) / 3.0 + soh * jump;
+      }
+      f = mode == 1 ? lin - nl : P.kappa * q[N] - nl;
+    }
+    r[N] += f;
+  }
+  const double c = 2.0 / hC;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) out[i] = c * (r[i] / P.w[i]);
+}
+
+// Stage [e0-1, e0+E] of x (scaled by xs) and u~ into shared memory.
+template <int NP>
+__device__ __forceinline__ void b1_stage(const B1P<NP>& P, long long e0, int E, const double* x, double xs,
+                                         bool want_ut, double* sx, double* su) {
+  const int cnt = (E + 2) * NP;
+  for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+    long long ge = e0 - 1 + idx / NP;
+    const int node = idx % NP;
+    double xv = 0.0, uv = 0.0;
+    if (ge < 0 || ge >= P.ne) {
+      if (P.periodic) {
+        ge = (ge + P.ne) % P.ne;
+        xv = x[ge * NP + node] * xs;
+        if (want_ut) uv = P.ut[ge * NP + node];
+      }
+    } else {
+      xv = x[ge * NP + node] * xs;
+      if (want_ut) uv = P.ut[ge * NP + node];
+    }
+    sx[idx] = xv;
+    su[idx] = uv;
+  }
+}
+
+// Standalone apply: y = L x | N x | rhs(x).
+template <int NP>
+__global__ void __launch_bounds__(kB1Threads) k_b1_apply(B1P<NP> P, int mode, const double* __restrict__ x,
+                                                         double* __restrict__ y, const PhiState* st) {
+  __shared__ double sx[(kB1Threads + 2) * NP], su[(kB1Threads + 2) * NP], sy[kB1Threads * NP];
+  if (st && st->stopped) return;
+  const int ntiles = (P.ne + kB1Threads - 1) / kB1Threads;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = (long long)tile * kB1Threads;
+    const int E = (int)(P.ne - e0 < kB1Threads ? P.ne - e0 : kB1Threads);
+    __syncthreads();
+    b1_stage(P, e0, E, x, 1.0, mode != 2, sx, su);
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < E) {
+      double out[NP];
+      b1_element<NP>(P, mode, (int)(e0 + t), sx + t * NP, sx + (t + 1) * NP, sx + (t + 2) * NP, su + t * NP,
+                     su + (t + 1) * NP, su + (t + 2) * NP, out);
+#pragma unroll
+      for (int i = 0; i < NP; ++i) sy[t * NP + i] = out[i];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < E * NP; idx += blockDim.x) y[e0 * NP + idx] = sy[idx];
+  }
+}
+
+// Phi-cycle apply: y = dt (L s_j V_j + sum_i x_tail[i] b_{p-i}) into slot j+1
+// (proj/src/phi.cpp:151-158) and ||y||^2 (pre_norm / avnorm).
+template <int NP>
+__global__ void __launch_bounds__(kB1Threads) k_b1_phi(B1P<NP> P, PhiState* st, double* base, double* partials,
+                                                       BArgs b) {
+  __shared__ double sx[(kB1Threads + 2) * NP], su[(kB1Threads + 2) * NP], sy[kB1Threads * NP];
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[kB1Threads / 32];
+  __shared__ double s_red[1];
+  if (threadIdx.x == 0) {
+    const int a = st->action;
+    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    if (s_go) {
+      s_j = st->j;
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[P.n + i] * s_xs : 0.0;
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  double nacc = 0.0;
+  const int ntiles = (P.ne + kB1Threads - 1) / kB1Threads;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = (long long)tile * kB1Threads;
+    const int E = (int)(P.ne - e0 < kB1Threads ? P.ne - e0 : kB1Threads);
+    __syncthreads();
+    b1_stage(P, e0, E, x, xs, true, sx, su);
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < E) {
+      double out[NP];
+      b1_element<NP>(P, 0, (int)(e0 + t), sx + t * NP, sx + (t + 1) * NP, sx + (t + 2) * NP, su + t * NP,
+                     su + (t + 1) * NP, su + (t + 2) * NP, out);
+#pragma unroll
+      for (int i = 0; i < NP; ++i) sy[t * NP + i] = out[i];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < E * NP; idx += blockDim.x) {
+      const long long g = e0 * NP + idx;
+      double v = sy[idx];
+      for (int i = 0; i < b.p; ++i)
+        if (b.b[b.p - i]) v = fma(s_xt[i], b.b[b.p - i][g], v);
+      v = dt * v;
+      y[g] = v;
+      nacc = fma(v, v, nacc);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here) {
+    const int i = threadIdx.x;
+    const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
+    y[P.n + i] = v;
+    nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (threadIdx.x == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+}
+
+template <int NP>
+class Burgers1D : public OpDevice {
+ public:
+  B1P<NP> P{};
+  int grid = 1;
+  explicit Burgers1D(const expdg_op_desc& d) {
+    desc = d;
+    const HostBasis hb = host_lgl_basis(d.order);
+    P.ne = d.nx;
+    P.periodic = d.periodic;
+    P.a = d.x0;
+    P.b = d.x1;
+    P.kappa = d.kappa;
+    P.sigma = d.sigma;
+    P.entropy = d.flux == 1;
+    P.sigma_adaptive = d.sigma_adaptive;
+    for (int i = 0; i < NP; ++i) {
+      P.w[i] = hb.weights[i];
+      for (int j = 0; j < NP; ++j) {
+        P.G[i * NP + j] = hb.weights[i] * hb.D[i * NP + j];
+        P.Lv[i * NP + j] = hb.D[j * NP + i] * hb.weights[j];
+      }
+    }
+    n = (long long)d.nx * NP;
+    P.n = n;
+    comps = 1;
+    const int ntiles = (d.nx + kB1Threads - 1) / kB1Threads;
+    grid = std::max(1, std::min(ntiles, 148 * 8));
+  }
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+    B1P<NP> p = P;
+    p.ut = ref;
+    k_b1_phi<NP><<<grid, kB1Threads, 0, s>>>(p, st, base, partials, b);
+  }
+  void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
+    B1P<NP> p = P;
+    p.ut = ref;
+    k_b1_apply<NP><<<grid, kB1Threads, 0, s>>>(p, which, x, y, nullptr);
+  }
+  void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
+    B1P<NP> p = P;
+    p.ut = u;
+    k_b1_apply<NP><<<grid, kB1Threads, 0, s>>>(p, 2, u, r, st);
+  }
+};
+
+// ---------------------------------------------------------------- dense (test operator)
+__global__ void k_dense_apply(int n, const double* __restrict__ A, const double* __restrict__ x, double xs,
+                              double* __restrict__ y) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  double s = 0.0;
+  for (int c = lane; c < n; c += 32) s = fma(A[(size_t)row * n + c], x[c] * xs, s);
+  s = warp_sum(s);
+  if (lane == 0) y[row] = s;
+}
+
+// y = dt (A s_j V_j + aug) into slot j+1, ||y||^2 -> red_nrmA (single CTA, test sizes)
+__global__ void k_dense_phi(int n, const double* __restrict__ A, PhiState* st, double* base, BArgs b) {
+  __shared__ double s_buf[32];
+  __shared__ double s_xt[kMaxP];
+  if (st->stopped) return;
+  const int a = st->action;
+  if (!(a == ACT_EXTEND || a == ACT_AVNORM)) return;
+  const int j = st->j;
+  const double xs = st->scale[j], dt = st->dt;
+  const long long ld = st->ld;
+  const double* x = base + (size_t)j * ld;
+  double* y = base + (size_t)(j + 1) * ld;
+  if (threadIdx.x < kMaxP) s_xt[threadIdx.x] = (threadIdx.x < b.p) ? x[n + threadIdx.x] * xs : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double nacc = 0.0;
+  for (int row = wid; row < n; row += nw) {
+    double s = 0.0;
+    for (int c = lane; c < n; c += 32) s = fma(A[(size_t)row * n + c], x[c] * xs, s);
+    s = warp_sum(s);
+    if (lane == 0) {
+      double v = s;
+      for (int i = 0; i < b.p; ++i)
+        if (b.b[b.p - i]) v = fma(s_xt[i], b.b[b.p - i][row], v);
+      v = dt * v;
+      y[row] = v;
+      nacc = fma(v, v, nacc);
+    }
+  }
+  if (threadIdx.x < kTailPad) {
+    const int i = threadIdx.x;
+    const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
+    y[n + i] = v;
+    nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (threadIdx.x == 0) st->red_nrmA = tot;
+}
+
+class DenseOp : public OpDevice {
+ public:
+  double* A = nullptr;
+  DenseOp(int nn, const double* a_host) {
+    n = nn;
+    desc.kind = EXPDG_DENSE;
+    EXPDG_CUDA(cudaMalloc(&A, sizeof(double) * (size_t)nn * nn));
+    EXPDG_CUDA(cudaMemcpy(A, a_host, sizeof(double) * (size_t)nn * nn, cudaMemcpyHostToDevice));
+  }
+  ~DenseOp() override { cudaFree(A); }
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double*, const BArgs& b) override {
+    k_dense_phi<<<1, 1024, 0, s>>>((int)n, A, st, base, b);
+  }
+  void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
+    if (which != 0) throw std::invalid_argument("dense operator: only the linear action exists");
+    k_dense_apply<<<(unsigned)((n + 7) / 8), 256, 0, s>>>((int)n, A, x, 1.0, y);
+  }
+  void launch_residual(cudaStream_t s, const double* u, double* r, PhiState*, double*) override {
+    k_dense_apply<<<(unsigned)((n + 7) / 8), 256, 0, s>>>((int)n, A, u, 1.0, r);
+  }
+};
+
+}  // namespace
+
+std::unique_ptr<OpDevice> make_burgers1d(const expdg_op_desc& d) {
+  if (d.over_integrate) throw std::invalid_argument("burgers1d: over_integrate is not on the device path");
+  switch (d.order + 1) {
+    case 2: return std::make_unique<Burgers1D<2>>(d);
+    case 3: return std::make_unique<Burgers1D<3>>(d);
+    case 4: return std::make_unique<Burgers1D<4>>(d);
+    case 5: return std::make_unique<Burgers1D<5>>(d);
+    case 6: return std::make_unique<Burgers1D<6>>(d);
+    case 7: return std::make_unique<Burgers1D<7>>(d);
+    case 8: return std::make_unique<Burgers1D<8>>(d);
+    case 9: return std::make_unique<Burgers1D<9>>(d);
+  }
+  throw std::invalid_argument("burgers1d: device orders are 1..8");
+}
+
+std::unique_ptr<OpDevice> make_dense(int n, const double* a_host) { return std::make_unique<DenseOp>(n, a_host); }
+
+}  // namespace expdg
