@@ -1,0 +1,275 @@
+"""bench.py — exponential-DG step throughput on B200 (BASELINE.json metric).
+
+Workload (N=1): config C4 of BASELINE.json — 2D compressible Euler, strength-5
+isentropic vortex on [0,10]^2, 1024 x 1024 quads, N = 4 LGL (104,857,600 DOF),
+Lax-Friedrichs, EPI2 at Cr_a = 5, Krylov tol 1e-10, max dim 40 — the largest
+configuration of the reference's own physics that fits one GPU (configs[1], C2,
+fails in the reference algorithm itself: KrylovError -> blew_up at step 1, see
+DESIGN.md).  One "step" = one EPI2 step (relinearise, R, phi_1 by the adaptive
+augmented Krylov engine, u update).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Prints one JSON line (rank 0).  value = DOF-steps/s with the state resident in
+HBM (device CUDA events around the step loop); e2e = the same metric through the
+public API with host buffers (H2D + D2H of u inside every step); roofline = the
+JVP + Arnoldi phi engine's canonical algorithmic bytes over the
+step time against the measured HBM copy peak; cpu_baseline = the oracle (CPU
+restatement of the reference, single-threaded like the reference) on a bounded
+sample of the same physics.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        smax = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": smax, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    return world, rank, local
+
+
+def cpu_sample(workload, steps: int = 1, nx: int = 128, warmup: int = 0):
+    """The oracle (CPU restatement of the reference) on a bounded sample of the
+    same physics: same config, Courant rule and Krylov settings on nx x nx."""
+    import oracle
+    from paper_2011_01316_b200 import configs
+    w = configs.scaled(workload, nx, steps=steps)
+    spec = w.spec()
+    u0 = oracle.initial_condition(w.config, w.nx, w.order, configs.SEEDS[w.config], w.noise)
+    dt = w.time_step(u0)
+    P = oracle.Problem(spec.kind, spec.order, spec.nx, spec.ny, spec.nz, box=spec.box, periodic=spec.periodic,
+                       kappa=spec.kappa, flux=spec.flux, sigma=spec.sigma, euler_flux=spec.euler_flux)
+    u = u0
+    if warmup:
+        u = P.integrate("epi2", u, dt, warmup * dt, tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis).u
+    r = P.integrate("epi2", u, dt, steps * dt, tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    dofs = P.dim
+    return {"value": dofs * r.steps / r.seconds, "seconds": r.seconds, "steps": r.steps, "dofs": dofs,
+            "nx": nx, "iterations": r.krylov_iterations}
+
+
+def run_reference(args, workload):
+    """--impl reference: the reference's CPU path (oracle port; the reference
+    itself cannot be built here) on the host cores, bounded samples per step."""
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    nx = args.ref_nx
+    s = cpu_sample(workload, steps=args.steps, nx=nx, warmup=args.warmup)
+    line = {
+        "impl": "reference", "metric": "DOF-steps/s per exponential-DG step", "value": s["value"],
+        "unit": "DOF-steps/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * s["seconds"] / max(1, s["steps"]), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload.name, "sample": f"{nx}x{nx} elements (same physics/Courant/Krylov)",
+                   "dofs": s["dofs"]},
+        "cpu_baseline": {"value": s["value"], "unit": "DOF-steps/s", "cores": 1, "kind": "port",
+                         "sample": f"oracle EPI2, {workload.name} physics on {nx}x{nx} elements, "
+                                   f"{args.steps} timed steps after {args.warmup} warm-up; single-threaded "
+                                   f"like the reference (proj/README.md:43-45)"},
+        "e2e": {"value": s["value"], "unit": "DOF-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--ref-nx", type=int, default=96)
+    ap.add_argument("--cpu-nx", type=int, default=128)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    from paper_2011_01316_b200 import configs
+    workload = configs.ALL[args.config]
+    if args.impl == "reference":
+        run_reference(args, workload)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2011_01316_b200 as pkg
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    ctx = pkg.Context(local)
+    w = workload
+    u0 = w.initial_condition()
+    dt = w.time_step(u0) if w.dt is None else w.dt
+    op = pkg.Operator(ctx, w.spec())
+    n = op.dim
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    u = torch.tensor(u0, device=f"cuda:{local}")
+
+    # warm-up steps (untimed)
+    rw = pkg.integrate(ctx, op, u, "epi2", dt, args.warmup * dt, **kw)
+    if rw.status != "completed":
+        raise RuntimeError(f"warm-up blew up at step {rw.blow_up_step}")
+
+    # timed region: barrier + synchronize on both sides, device events inside the library
+    clocks = ClockSampler(local)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    l0 = ctx.kernel_launches
+    r = pkg.integrate(ctx, op, u, "epi2", dt, args.steps * dt, **kw)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    launches = ctx.kernel_launches - l0
+    traffic = ctx.traffic()
+    if r.status != "completed" or r.steps != args.steps:
+        raise RuntimeError(f"timed run: {r.status} after {r.steps} steps")
+    loop_s = r.loop_ms / 1e3
+    if world > 1:
+        t = torch.tensor([loop_s], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        loop_s = float(t.item())
+    value = world * n * args.steps / loop_s
+    peak, peak_kind = hbm_peak()
+    achieved = traffic["alg_bytes"] / (r.loop_ms / 1e3) / 1e9
+    iters_per_step = np.diff(np.concatenate([[0], r.iters_per_step])) if len(r.iters_per_step) else []
+
+    # e2e: public API with host buffers, H2D + D2H of u inside every step
+    e2e = None
+    if not args.no_e2e:
+        uh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        uh.copy_(u.cpu())
+        uh_np = uh.numpy()
+        if world > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            re = pkg.integrate(ctx, op, uh_np, "epi2", dt, dt, **kw)
+            if re.status != "completed":
+                raise RuntimeError("e2e step blew up")
+        t1 = time.perf_counter()
+        e_s = t1 - t0
+        if world > 1:
+            tt = torch.tensor([e_s], device=f"cuda:{local}")
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            e_s = float(tt.item())
+        e2e = {"value": world * n * args.steps / e_s, "unit": "DOF-steps/s", "h2d_bytes_per_step": 8 * n,
+               "d2h_bytes_per_step": 8 * n, "seconds": e_s}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s = cpu_sample(w, steps=1, nx=args.cpu_nx)
+        cpu = {"value": s["value"], "unit": "DOF-steps/s", "cores": 1, "kind": "port",
+               "sample": f"oracle EPI2 (CPU restatement of the reference, single-threaded), {w.name} physics "
+                         f"on {args.cpu_nx}x{args.cpu_nx} elements ({s['dofs']} DOF), 1 step, "
+                         f"{s['seconds']:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": "DOF-steps/s per exponential-DG step", "value": value, "unit": "DOF-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * loop_s / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded strength-5 isentropic vortex + 1e-6 N(0,1) density noise)",
+            "config": {"workload": w.name, "dofs": n, "elements": f"{w.nx}x{w.ny}", "order": w.order,
+                       "dt": dt, "cr_a": w.cfl, "krylov": {"tol": w.tol, "max_basis": w.max_basis,
+                                                           "orth_length": w.max_basis},
+                       "integrator": "epi2", "l2": "inputs larger than L2 (Krylov workspace "
+                       f"{(w.max_basis + 2) * 8 * n / 1e9:.1f} GB vs 126 MB L2)",
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                       "krylov_iters_per_step": [int(v) for v in iters_per_step]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "phi engine cycle (operator apply + CGS2 passes + combine + controller), "
+                                   "canonical algorithmic bytes of the realised trajectory / step-loop time",
+                         "peak_kind": peak_kind, "alg_bytes_per_step": traffic["alg_bytes"] / args.steps,
+                         "columns": traffic["columns"], "avnorms": traffic["avnorms"],
+                         "combines": traffic["combines"]},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

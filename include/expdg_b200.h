@@ -172,6 +172,10 @@ int expdg_initial_condition(int config, int nx, int order, uint64_t seed, double
 long long expdg_ctx_kernel_launches(expdg_ctx* ctx);
 /* Device-event time (ms) of the last expdg_integrate call's step loop. */
 double expdg_ctx_last_loop_ms(expdg_ctx* ctx);
+/* Canonical algorithmic HBM bytes of the last integrate / phi call's
+ * realised trajectory, and its counts of Arnoldi columns, avnorm applications and
+ * accepted substeps: out4 = {bytes, columns, avnorms, combines}. */
+int expdg_ctx_traffic(expdg_ctx* ctx, double* out4);
 
 #ifdef __cplusplus
 }

@@ -80,7 +80,7 @@ EXPORTS = [
     "expdg_op_apply_linear", "expdg_op_apply_nonlinear", "expdg_op_full_rhs", "expdg_phi_combination",
     "expdg_step_epi2", "expdg_integrate", "expdg_integrate_host", "expdg_lgl_basis",
     "expdg_initial_condition", "expdg_ctx_kernel_launches", "expdg_ctx_last_loop_ms", "expdg_expm",
-    "expdg_debug_state", "expdg_debug_hessenberg",
+    "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic",
 ]
 
 _lib = None
@@ -129,6 +129,7 @@ def lib():
     L.expdg_expm.argtypes = [vp, C.c_int, dp, dp]
     L.expdg_debug_state.argtypes = [vp, dp]
     L.expdg_debug_hessenberg.argtypes = [vp, dp]
+    L.expdg_ctx_traffic.argtypes = [vp, dp]
     L.expdg_initial_condition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, dp]
     _lib = L
     return L
@@ -223,6 +224,12 @@ class Context:
         keys = ["mc", "h", "t", "beta", "avnorm", "last_estimate", "substeps", "iterations", "breakdown",
                 "status", "mmax", "grow_cap", "full_orth", "cycles", "pre_norm", "m"]
         return dict(zip(keys, v.tolist()))
+
+    def traffic(self) -> dict:
+        """Canonical algorithmic bytes of the last call's realised trajectory."""
+        v = np.zeros(4)
+        _check(lib().expdg_ctx_traffic(self.h, _np_ptr(v)))
+        return {"alg_bytes": v[0], "columns": int(v[1]), "avnorms": int(v[2]), "combines": int(v[3])}
 
     def debug_hessenberg(self) -> np.ndarray:
         h = np.zeros((129, 128))

@@ -531,6 +531,18 @@ int expdg_debug_state(expdg_ctx* ctx, double* out16) {
   });
 }
 
+int expdg_ctx_traffic(expdg_ctx* ctx, double* out4) {
+  return guard([&] {
+    Engine& e = *ctx->eng;
+    EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
+    const PhiState& s = *e.st_host;
+    out4[0] = s.alg_bytes;
+    out4[1] = (double)s.extend_cols;
+    out4[2] = (double)s.avnorms;
+    out4[3] = (double)s.combines;
+  });
+}
+
 int expdg_debug_hessenberg(expdg_ctx* ctx, double* out /* (kMaxBasis+1) x kMaxBasis */) {
   return guard([&] {
     Engine& e = *ctx->eng;

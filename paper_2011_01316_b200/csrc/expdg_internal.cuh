@@ -94,6 +94,11 @@ struct PhiState {
   int any_b;          // some b_i nonzero
   long long iterations_total;
   long long body_runs;  // controller invocations (one per engine cycle)
+  // canonical algorithmic HBM bytes of the realised trajectory:
+  // JVP 32 n per operator application, CGS2 8 n (3k + 6) per column against k
+  // vectors, combine 8 n (m + 1) per accepted substep, 40 n per step.
+  double alg_bytes;
+  long long extend_cols, avnorms, combines;
   double blow_up_scale;
   double amax_step;
 };

@@ -422,6 +422,11 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
             const double h2 = st->full_orth ? sc[i] * st->red_dotB[i] : 0.0;
             st->H[i * kMaxBasis + j] = st->full_orth ? (h1 + h2) : h1;
           }
+          {
+            const double nd = (double)st->n, kk = (double)(j - st->j0 + 1);
+            st->alg_bytes += 32.0 * nd + 8.0 * nd * (st->full_orth ? 3.0 * kk + 6.0 : 2.0 * kk + 4.0);
+            st->extend_cols++;
+          }
           const double pre_norm = sqrt(st->red_nrmA);
           const double hnext = sqrt(st->red_nrmC);
           st->pre_norm = pre_norm;
@@ -446,10 +451,14 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
           break;
         }
         case ACT_AVNORM:
+          st->alg_bytes += 32.0 * (double)st->n;
+          st->avnorms++;
           st->avnorm = sqrt(st->red_nrmA);
           phase = PH_DECIDE;
           break;
         case ACT_COMBINE: {
+          st->alg_bytes += 8.0 * (double)st->n * (double)(st->mc + 1);
+          st->combines++;
           double w2 = st->red_w2;
           if (st->tail_here)
             for (int j = 0; j < st->p; ++j) slot0[st->n + j] = st->tailw[j];

@@ -1,0 +1,416 @@
+// 2D compressible Euler DG operators on sm_100a, Lax-Friedrichs split:
+// the JVP L q = frozen-Jacobian volume + linearised LF faces
+// (proj/src/euler.cpp:299-341, rhs_faces :260-297, inverse mass :246-258),
+// N q (:343-388) and the full RHS (:403-408).
+//
+// No frozen arrays: the reference stores 2 x 16 doubles of A(q~) per node and
+// 3 x 16 per face node (proj/src/euler.cpp:207-243); here A(q~) is recomputed
+// from q~ (32 B/node) in registers, so the JVP streams x, q~, b_1 and y only.
+// One thread per LGL node, a CTA tile of floor(256 / NP^2) consecutive elements
+// staged in shared memory; face neighbours come from the tile when present,
+// else from L2.
+#include <algorithm>
+
+#include "krylov.cuh"
+
+namespace expdg {
+
+namespace {
+
+
+template <int NP>
+struct E2P {
+  int nx, ny;
+  double x0, x1, y0, y1;
+  double gamma;
+  double w[NP];
+  double WD[NP * NP];  // WD(a, b) = w_a D(a, b)
+  const double* ut;
+  long long n;
+};
+
+struct Prim {
+  double rho, u, v, p, a, H;
+};
+
+// proj/src/euler.cpp:15-24
+__device__ __forceinline__ Prim prim_of(const double q[4], double gamma) {
+  Prim pr;
+  pr.rho = q[0];
+  pr.u = q[1] / q[0];
+  pr.v = q[2] / q[0];
+  pr.p = (gamma - 1.0) * (q[3] - 0.5 * pr.rho * (pr.u * pr.u + pr.v * pr.v));
+  pr.a = sqrt(gamma * pr.p / pr.rho);
+  pr.H = (q[3] + pr.p) / pr.rho;
+  return pr;
+}
+
+__device__ __forceinline__ bool admissible4(const double q[4], double gamma) {
+  if (!(q[0] > 0.0)) return false;
+  const double p = (gamma - 1.0) * (q[3] - 0.5 * (q[1] * q[1] + q[2] * q[2]) / q[0]);
+  return p > 0.0;
+}
+
+// out = A(pr, n) x for n = e_x (dir 0) or e_y (dir 1), entries of
+// jacobian_from_primitives (proj/src/euler.cpp:44-73) with n substituted.
+__device__ __forceinline__ void jac_apply(const Prim& pr, int dir, double gamma, const double x[4], double out[4]) {
+  const double gm1 = gamma - 1.0;
+  const double u = pr.u, v = pr.v, H = pr.H;
+  const double phi = 0.5 * gm1 * (u * u + v * v);
+  if (dir == 0) {
+    const double un = u;
+    out[0] = x[1];
+    out[1] = (phi - u * un) * x[0] + (u - gm1 * u + un) * x[1] + (-gm1 * v) * x[2] + gm1 * x[3];
+    out[2] = (-v * un) * x[0] + v * x[1] + un * x[2];
+    out[3] = ((phi - H) * un) * x[0] + (H - gm1 * u * un) * x[1] + (-gm1 * v * un) * x[2] + (gamma * un) * x[3];
+  } else {
+    const double un = v;
+    out[0] = x[2];
+    out[1] = (-u * un) * x[0] + un * x[1] + u * x[2];
+    out[2] = (phi - v * un) * x[0] + (-gm1 * u) * x[1] + (v - gm1 * v + un) * x[2] + gm1 * x[3];
+    out[3] = ((phi - H) * un) * x[0] + (-gm1 * u * un) * x[1] + (H - gm1 * v * un) * x[2] + (gamma * un) * x[3];
+  }
+}
+
+// physical flux F(q) . e_dir (proj/src/euler.cpp:26-40)
+__device__ __forceinline__ void flux_dir(const double q[4], const Prim& pr, int dir, double f[4]) {
+  if (dir == 0) {
+    f[0] = q[1];
+    f[1] = q[1] * pr.u + pr.p;
+    f[2] = q[2] * pr.u;
+    f[3] = q[0] * pr.u * pr.H;
+  } else {
+    f[0] = q[2];
+    f[1] = q[1] * pr.v;
+    f[2] = q[2] * pr.v + pr.p;
+    f[3] = q[0] * pr.v * pr.H;
+  }
+}
+
+// Numerical normal flux on a face with n = +e_dir between owner (qm, utm) and
+// neighbour (qp, utp):  mode 0 linearised LF, 1 full LF - linearised, 2 full LF.
+__device__ __forceinline__ void face_flux(int mode, int dir, double gamma, const double qm[4], const double qp[4],
+                                          const double utm[4], const double utp[4], double f[4], bool& bad) {
+  double lin[4] = {0, 0, 0, 0};
+  if (mode != 2) {
+    const Prim tm = prim_of(utm, gamma), tp = prim_of(utp, gamma);
+    double am[4], ap[4];
+    jac_apply(tm, dir, gamma, qm, am);
+    jac_apply(tp, dir, gamma, qp, ap);
+    const double cm = fabs(dir == 0 ? tm.u : tm.v) + tm.a;
+    const double cp = fabs(dir == 0 ? tp.u : tp.v) + tp.a;
+    const double lam = fmax(cm, cp);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) lin[c] = 0.5 * (am[c] + ap[c]) + 0.5 * (lam * (qm[c] - qp[c]));
+  }
+  if (mode == 0) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) f[c] = lin[c];
+    return;
+  }
+  // euler_lax_friedrichs_flux (proj/src/euler.cpp:147-158)
+  if (!admissible4(qm, gamma) || !admissible4(qp, gamma)) bad = true;
+  const Prim pm = prim_of(qm, gamma), pp = prim_of(qp, gamma);
+  double fm[4], fp[4];
+  flux_dir(qm, pm, dir, fm);
+  flux_dir(qp, pp, dir, fp);
+  const double cm = fabs(dir == 0 ? pm.u : pm.v) + pm.a;
+  const double cp = fabs(dir == 0 ? pp.u : pp.v) + pp.a;
+  const double s = 0.5 * fmax(cm, cp);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double full = 0.5 * (fm[c] + fp[c]) + s * (qm[c] - qp[c]);
+    f[c] = mode == 1 ? full - lin[c] : full;
+  }
+}
+
+__device__ __forceinline__ double brk(double a, double b, int i, int n) { return i == n ? b : a + (b - a) * i / n; }
+
+template <int NP>
+struct E2Tile {
+  static constexpr int NN = NP * NP;
+  static constexpr int TE = 256 / NN;  // elements per CTA tile
+  static constexpr int VALS = TE * 4 * NN;
+};
+
+// Loads node `node` of element `e` (4 comps) of x (scaled) / ut, from the staged
+// tile when e is in it, else from global memory.
+template <int NP>
+__device__ __forceinline__ void load_node(const double* sx, const double* su, long long e0, int te, long long e,
+                                          int node, const double* x, double xs, const double* ut, double q[4],
+                                          double t[4], bool need_ut) {
+  constexpr int NN = NP * NP;
+  const long long le = e - e0;
+  if (le >= 0 && le < te) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      q[c] = sx[(le * 4 + c) * NN + node];
+      t[c] = need_ut ? su[(le * 4 + c) * NN + node] : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      q[c] = x[(e * 4 + c) * NN + node] * xs;
+      t[c] = need_ut ? ut[(e * 4 + c) * NN + node] : 0.0;
+    }
+  }
+}
+
+// Computes the operator for every node of a tile; result per thread in out[4]
+// (valid when the thread maps to a node of the tile).
+template <int NP>
+__device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, long long e0, int te, const double* x, double xs,
+                                        double* sx, double* su, double* sf, double out[4], bool& bad) {
+  constexpr int NN = NP * NP;
+  constexpr int N = NP - 1;
+  const int t = threadIdx.x;
+  const int le = t / NN, node = t % NN;
+  const int i = node % NP, j = node / NP;
+  const bool active = le < te;
+  const bool need_ut = mode != 2;
+  // stage x, ut of the tile (coalesced: the tile is contiguous)
+  const int cnt = te * 4 * NN;
+  for (int idx = t; idx < cnt; idx += blockDim.x) {
+    sx[idx] = x[e0 * 4 * NN + idx] * xs;
+    if (need_ut) su[idx] = P.ut[e0 * 4 * NN + idx];
+  }
+  __syncthreads();
+  double q[4], ut[4];
+  long long e = e0 + le;
+  int ie = 0, je = 0;
+  if (active) {
+    ie = (int)(e % P.nx);
+    je = (int)(e / P.nx);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      q[c] = sx[(le * 4 + c) * NN + node];
+      ut[c] = need_ut ? su[(le * 4 + c) * NN + node] : 0.0;
+    }
+    // volume fluxes: fx, fy (linear: A(ut) q; nonlinear: F(q) - A(ut) q; full: F(q))
+    double fx[4], fy[4];
+    if (mode != 2) {
+      const Prim tp = prim_of(ut, P.gamma);
+      jac_apply(tp, 0, P.gamma, q, fx);
+      jac_apply(tp, 1, P.gamma, q, fy);
+    }
+    if (mode != 0) {
+      if (!admissible4(q, P.gamma)) bad = true;
+      const Prim pq = prim_of(q, P.gamma);
+      double Fx[4], Fy[4];
+      flux_dir(q, pq, 0, Fx);
+      flux_dir(q, pq, 1, Fy);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        fx[c] = mode == 1 ? Fx[c] - fx[c] : Fx[c];
+        fy[c] = mode == 1 ? Fy[c] - fy[c] : Fy[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      sf[((le * 2 + 0) * 4 + c) * NN + node] = fx[c];
+      sf[((le * 2 + 1) * 4 + c) * NN + node] = fy[c];
+    }
+  }
+  __syncthreads();
+  if (!active) return;
+  const double hx = brk(P.x0, P.x1, ie + 1, P.nx) - brk(P.x0, P.x1, ie, P.nx);
+  const double hy = brk(P.y0, P.y1, je + 1, P.ny) - brk(P.y0, P.y1, je, P.ny);
+  const double sy = 0.5 * hy * P.w[j];
+  const double sxs = 0.5 * hx * P.w[i];
+  double r[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double* fxr = sf + ((le * 2 + 0) * 4 + c) * NN + j * NP;  // row j
+    const double* fyc = sf + ((le * 2 + 1) * 4 + c) * NN + i;       // column i
+    double ax = 0.0, ay = 0.0;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      ax = fma(P.WD[k * NP + i], fxr[k], ax);
+      ay = fma(P.WD[k * NP + j], fyc[k * NP], ay);
+    }
+    r[c] = sy * ax;
+    r[c] += sxs * ay;
+  }
+  // x-faces (owner on the low side, normal +e_x, periodic)
+  if (i == N || i == 0) {
+    const bool owner = i == N;
+    const int ie2 = owner ? (ie + 1 == P.nx ? 0 : ie + 1) : (ie == 0 ? P.nx - 1 : ie - 1);
+    const long long e2 = (long long)je * P.nx + ie2;
+    const int node2 = j * NP + (owner ? 0 : N);
+    double q2[4], u2[4], f[4];
+    load_node<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
+    if (owner) face_flux(mode, 0, P.gamma, q, q2, ut, u2, f, bad);
+    else face_flux(mode, 0, P.gamma, q2, q, u2, ut, f, bad);
+    // half edge length of the owner element (uniform breaks along y)
+    const double fw = 0.5 * hy * P.w[j];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) r[c] = owner ? r[c] - fw * f[c] : r[c] + fw * f[c];
+  }
+  if (j == N || j == 0) {
+    const bool owner = j == N;
+    const int je2 = owner ? (je + 1 == P.ny ? 0 : je + 1) : (je == 0 ? P.ny - 1 : je - 1);
+    const long long e2 = (long long)je2 * P.nx + ie;
+    const int node2 = (owner ? 0 : N) * NP + i;
+    double q2[4], u2[4], f[4];
+    load_node<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
+    if (owner) face_flux(mode, 1, P.gamma, q, q2, ut, u2, f, bad);
+    else face_flux(mode, 1, P.gamma, q2, q, u2, ut, f, bad);
+    const double fw = 0.5 * hx * P.w[i];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) r[c] = owner ? r[c] - fw * f[c] : r[c] + fw * f[c];
+  }
+  const double scale = 4.0 / (hx * hy);
+  const double im = scale / (P.w[i] * P.w[j]);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) out[c] = r[c] * im;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256) k_e2_apply(E2P<NP> P, int mode, const double* __restrict__ x,
+                                                  double* __restrict__ y, PhiState* st) {
+  constexpr int NN = NP * NP, TE = E2Tile<NP>::TE;
+  __shared__ double sx[E2Tile<NP>::VALS], su[E2Tile<NP>::VALS], sf[2 * E2Tile<NP>::VALS];
+  if (st && st->stopped) return;
+  const long long ne = (long long)P.nx * P.ny;
+  const long long ntiles = (ne + TE - 1) / TE;
+  bool bad = false;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = tile * TE;
+    const int te = (int)(ne - e0 < TE ? ne - e0 : TE);
+    __syncthreads();
+    double out[4];
+    e2_tile<NP>(P, mode, e0, te, x, 1.0, sx, su, sf, out, bad);
+    const int t = threadIdx.x, le = t / NN, node = t % NN;
+    if (le < te) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) y[((e0 + le) * 4 + c) * NN + node] = out[c];
+    }
+  }
+  if (bad && st) st->domain_flag = 1;
+}
+
+// phi-cycle apply: y = dt (L s_j V_j + aug) into slot j+1, ||y||^2 -> red_nrmA
+template <int NP>
+__global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
+  constexpr int NN = NP * NP, TE = E2Tile<NP>::TE;
+  __shared__ double sx[E2Tile<NP>::VALS], su[E2Tile<NP>::VALS], sf[2 * E2Tile<NP>::VALS];
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[8];
+  __shared__ double s_red[1];
+  if (threadIdx.x == 0) {
+    const int a = st->action;
+    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    if (s_go) {
+      s_j = st->j;
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[P.n + i] * s_xs : 0.0;
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  const long long ne = (long long)P.nx * P.ny;
+  const long long ntiles = (ne + TE - 1) / TE;
+  double nacc = 0.0;
+  bool bad = false;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = tile * TE;
+    const int te = (int)(ne - e0 < TE ? ne - e0 : TE);
+    __syncthreads();
+    double out[4];
+    e2_tile<NP>(P, 0, e0, te, x, xs, sx, su, sf, out, bad);
+    const int t = threadIdx.x, le = t / NN, node = t % NN;
+    __syncthreads();
+    if (le < te) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sx[(le * 4 + c) * NN + node] = out[c];
+    }
+    __syncthreads();
+    for (int idx = t; idx < te * 4 * NN; idx += blockDim.x) {
+      const long long g = e0 * 4 * NN + idx;
+      double v = sx[idx];
+      for (int k = 0; k < b.p; ++k)
+        if (b.b[b.p - k]) v = fma(s_xt[k], b.b[b.p - k][g], v);
+      v = dt * v;
+      y[g] = v;
+      nacc = fma(v, v, nacc);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here) {
+    const int i = threadIdx.x;
+    const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
+    y[P.n + i] = v;
+    nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (threadIdx.x == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+}
+
+template <int NP>
+class Euler2D : public OpDevice {
+ public:
+  E2P<NP> P{};
+  int grid = 1;
+  explicit Euler2D(const expdg_op_desc& d) {
+    desc = d;
+    const HostBasis hb = host_lgl_basis(d.order);
+    P.nx = d.nx;
+    P.ny = d.ny;
+    P.x0 = d.x0;
+    P.x1 = d.x1;
+    P.y0 = d.y0;
+    P.y1 = d.y1;
+    P.gamma = d.gamma;
+    for (int a = 0; a < NP; ++a) {
+      P.w[a] = hb.weights[a];
+      for (int b2 = 0; b2 < NP; ++b2) P.WD[a * NP + b2] = hb.weights[a] * hb.D[a * NP + b2];
+    }
+    n = (long long)d.nx * d.ny * NP * NP * 4;
+    P.n = n;
+    comps = 4;
+    const long long ntiles = ((long long)d.nx * d.ny + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
+    grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
+  }
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+    E2P<NP> p = P;
+    p.ut = ref;
+    k_e2_phi<NP><<<grid, 256, 0, s>>>(p, st, base, partials, b);
+  }
+  void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
+    E2P<NP> p = P;
+    p.ut = ref;
+    k_e2_apply<NP><<<grid, 256, 0, s>>>(p, which, x, y, nullptr);
+  }
+  void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
+    E2P<NP> p = P;
+    p.ut = u;
+    k_e2_apply<NP><<<grid, 256, 0, s>>>(p, 2, u, r, st);
+  }
+};
+
+}  // namespace
+
+std::unique_ptr<OpDevice> make_euler2d(const expdg_op_desc& d) {
+  switch (d.order + 1) {
+    case 2: return std::make_unique<Euler2D<2>>(d);
+    case 3: return std::make_unique<Euler2D<3>>(d);
+    case 4: return std::make_unique<Euler2D<4>>(d);
+    case 5: return std::make_unique<Euler2D<5>>(d);
+    case 6: return std::make_unique<Euler2D<6>>(d);
+    case 7: return std::make_unique<Euler2D<7>>(d);
+    case 8: return std::make_unique<Euler2D<8>>(d);
+    case 9: return std::make_unique<Euler2D<9>>(d);
+  }
+  throw std::invalid_argument("euler2d: device orders are 1..8");
+}
+
+}  // namespace expdg

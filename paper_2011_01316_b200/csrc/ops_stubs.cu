@@ -1,6 +1,5 @@
 #include "krylov.cuh"
 namespace expdg {
 std::unique_ptr<OpDevice> make_burgers2d(const expdg_op_desc&) { throw std::invalid_argument("burgers2d: not built yet"); }
-std::unique_ptr<OpDevice> make_euler2d(const expdg_op_desc&) { throw std::invalid_argument("euler2d: not built yet"); }
 std::unique_ptr<OpDevice> make_euler3d(const expdg_op_desc&) { throw std::invalid_argument("euler3d: not built yet"); }
 }

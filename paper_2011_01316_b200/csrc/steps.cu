@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(256) k_step_finish(PhiState* st, double* u, co
     const bool failed = st->status != PHI_OK;
     const double am = bad > 0.0 ? INFINITY : mx;
     if (!failed) st->iterations_total += st->iterations;  // KrylovError drops the call's stats
+    st->alg_bytes += 40.0 * (double)st->n;
     StepRecord r;
     r.dt = st->dt;
     r.t = 0.0;
