@@ -155,6 +155,9 @@ def main():
     ap.add_argument("--cpu-nx", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--host-control", action="store_true",
+                    help="host-stepped controller (same kernels, no graph WHILE nodes): for ncu, which "
+                         "cannot profile kernel nodes of graphs with conditional nodes")
     args = ap.parse_args()
 
     from paper_2011_01316_b200 import configs
@@ -176,7 +179,7 @@ def main():
     dt = w.time_step(u0) if w.dt is None else w.dt
     op = pkg.Operator(ctx, w.spec())
     n = op.dim
-    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis, use_graph=not args.host_control)
     u = torch.tensor(u0, device=f"cuda:{local}")
 
     # warm-up steps (untimed)

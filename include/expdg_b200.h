@@ -161,6 +161,9 @@ int expdg_integrate_host(expdg_ctx* ctx, expdg_op* op, double* u_host, const exp
 int expdg_expm(expdg_ctx* ctx, int n, const double* a_host, double* out_host);
 /* Controller state of the last phi call (16 doubles, for diagnostics). */
 int expdg_debug_state(expdg_ctx* ctx, double* out16);
+/* Micro-benchmark of one CGS2 streaming pass (mode 0 dots, 1 update+dots,
+ * 2 update+norm, 3 combine) against k basis vectors of length n; avg ms. */
+int expdg_bench_ts(expdg_ctx* ctx, long long n, int k, int mode, int reps, double* ms);
 /* Hessenberg matrix of the last phi call, (129 x 128) row-major (diagnostics). */
 int expdg_debug_hessenberg(expdg_ctx* ctx, double* out);
 

@@ -80,7 +80,7 @@ EXPORTS = [
     "expdg_op_apply_linear", "expdg_op_apply_nonlinear", "expdg_op_full_rhs", "expdg_phi_combination",
     "expdg_step_epi2", "expdg_integrate", "expdg_integrate_host", "expdg_lgl_basis",
     "expdg_initial_condition", "expdg_ctx_kernel_launches", "expdg_ctx_last_loop_ms", "expdg_expm",
-    "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic",
+    "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts",
 ]
 
 _lib = None
@@ -130,6 +130,7 @@ def lib():
     L.expdg_debug_state.argtypes = [vp, dp]
     L.expdg_debug_hessenberg.argtypes = [vp, dp]
     L.expdg_ctx_traffic.argtypes = [vp, dp]
+    L.expdg_bench_ts.argtypes = [vp, C.c_longlong, C.c_int, C.c_int, C.c_int, dp]
     L.expdg_initial_condition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, dp]
     _lib = L
     return L
@@ -230,6 +231,12 @@ class Context:
         v = np.zeros(4)
         _check(lib().expdg_ctx_traffic(self.h, _np_ptr(v)))
         return {"alg_bytes": v[0], "columns": int(v[1]), "avnorms": int(v[2]), "combines": int(v[3])}
+
+    def bench_ts(self, n: int, k: int, mode: int, reps: int = 5) -> float:
+        """avg ms of one CGS2 streaming pass (0 dots, 1 update+dots, 2 update+norm, 3 combine)."""
+        ms = C.c_double()
+        _check(lib().expdg_bench_ts(self.h, n, k, mode, reps, C.byref(ms)))
+        return ms.value
 
     def debug_hessenberg(self) -> np.ndarray:
         h = np.zeros((129, 128))

@@ -197,7 +197,7 @@ int expdg_op_linearize(expdg_op* op, const double* ref_dev) {
     if (chk == 2) throw std::domain_error("EulerOperator: inadmissible reference state");
     if (!op->ref_owned) EXPDG_CUDA(cudaMalloc(&op->ref_owned, sizeof(double) * op->dev->n));
     EXPDG_CUDA(cudaMemcpyAsync(op->ref_owned, ref_dev, sizeof(double) * op->dev->n, cudaMemcpyDeviceToDevice, s));
-    op->dev->ref = op->ref_owned;
+    op->dev->freeze(s, op->ref_owned);
   });
 }
 
@@ -295,6 +295,11 @@ int expdg_step_epi2(expdg_ctx* ctx, expdg_op* op, double* u_dev, double dt, cons
   });
 }
 
+static void restore_ref(OpDevice& dev, cudaStream_t s, const double* saved) {
+  if (saved) dev.freeze(s, saved);
+  else dev.ref = nullptr;
+}
+
 static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_time_cfg* cfg,
                            expdg_integration_result* res, long long* iters, double* amaxs, int cap) {
   if (!ctx || !op || !u || !cfg || !res) throw std::invalid_argument("null argument");
@@ -348,7 +353,8 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   EXPDG_CUDA(cudaMalloc(&rec_dev, sizeof(StepRecord) * S));
   EXPDG_CUDA(cudaMemcpyAsync(dts_dev, dts.data(), sizeof(double) * S, cudaMemcpyHostToDevice, e.stream));
   const double* saved_ref = dev.ref;
-  dev.ref = mode == 0 ? u : refbuf;
+  if (mode == 0) dev.ref = u;  // EPI2: re-frozen at u^n by the residual kernel every step
+  else dev.freeze(e.stream, refbuf);
   BArgs b{};
   b.p = 1;
   b.b[0] = mode == 0 ? nullptr : u;
@@ -443,13 +449,13 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     cudaFreeHost(stop_host);
   } catch (...) {
     if (ex) cudaGraphExecDestroy(ex);
-    dev.ref = saved_ref;
+    restore_ref(dev, e.stream, saved_ref);
     cudaFree(dts_dev);
     cudaFree(rec_dev);
     throw;
   }
   if (ex) cudaGraphExecDestroy(ex);
-  dev.ref = saved_ref;
+  restore_ref(dev, e.stream, saved_ref);
   EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
   const PhiState st = *e.st_host;
   ctx->launches += (long long)launched * per_step + st.body_runs * body_k;
@@ -540,6 +546,13 @@ int expdg_ctx_traffic(expdg_ctx* ctx, double* out4) {
     out4[1] = (double)s.extend_cols;
     out4[2] = (double)s.avnorms;
     out4[3] = (double)s.combines;
+  });
+}
+
+int expdg_bench_ts(expdg_ctx* ctx, long long n, int k, int mode, int reps, double* ms) {
+  return guard([&] {
+    if (k < 1 || k > kMaxBasis) throw std::invalid_argument("bench_ts: 1 <= k <= 128");
+    *ms = ctx->eng->bench_ts(n, k, mode, reps);
   });
 }
 

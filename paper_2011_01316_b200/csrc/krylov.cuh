@@ -34,6 +34,9 @@ class OpDevice {
                                double* partials) = 0;
   // Whether the apply kernel also writes pass-A dots (else the generic kernel runs).
   virtual bool fused_dots() const { return false; }
+  // Freeze the reference state (proj/src/burgers.cpp:53-78, proj/src/euler.cpp:198-243):
+  // operators that keep derived frozen data compute it here.
+  virtual void freeze(cudaStream_t s, const double* r) { ref = r; }
 };
 
 std::unique_ptr<OpDevice> make_burgers1d(const expdg_op_desc& d);
@@ -50,8 +53,16 @@ struct HostBasis {
 HostBasis host_lgl_basis(int order);
 
 // Device workspace + launch helpers of the phi engine.
+struct TsTuning {
+  int budget = 196608;  // dynamic smem per CTA of the tall-skinny passes
+  int stages = 2;       // pipeline depth cap
+  int min_T = 64;       // smallest tile (doubles) before giving up stages
+};
+
 class Engine {
  public:
+  TsTuning ts_tuning;
+  int ld_odd = 1;
   explicit Engine(int device);
   ~Engine();
   int device = 0;
@@ -81,6 +92,8 @@ class Engine {
 
   // Kernel sequences.
   void launch_phi_init(cudaStream_t s, const BArgs& b);
+  void launch_ts(cudaStream_t s, int mode);
+  double bench_ts(long long n, int k, int mode, int reps);
   void launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
                    int use_graph);
   // Runs one phi call to completion; host-stepped or graph-driven control.

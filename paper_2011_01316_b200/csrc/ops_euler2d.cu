@@ -10,6 +10,7 @@
 // staged in shared memory; face neighbours come from the tile when present,
 // else from L2.
 #include <algorithm>
+#include <vector>
 
 #include "krylov.cuh"
 
@@ -21,11 +22,12 @@ namespace {
 template <int NP>
 struct E2P {
   int nx, ny;
-  double x0, x1, y0, y1;
   double gamma;
   double w[NP];
   double WD[NP * NP];  // WD(a, b) = w_a D(a, b)
-  const double* ut;
+  const double* ut;    // frozen primitives (u, v, H, a) of q~ per node, state layout
+  const double* hx;    // element widths per column (uniform breakpoints, proj/src/mesh.cpp:11-16)
+  const double* hy;    // element heights per row
   long long n;
 };
 
@@ -42,6 +44,18 @@ __device__ __forceinline__ Prim prim_of(const double q[4], double gamma) {
   pr.p = (gamma - 1.0) * (q[3] - 0.5 * pr.rho * (pr.u * pr.u + pr.v * pr.v));
   pr.a = sqrt(gamma * pr.p / pr.rho);
   pr.H = (q[3] + pr.p) / pr.rho;
+  return pr;
+}
+
+// frozen (u, v, H, a) -> the primitives the linearised flux reads (rho, p unused)
+__device__ __forceinline__ Prim prim_frozen(const double t[4]) {
+  Prim pr;
+  pr.rho = 0.0;
+  pr.p = 0.0;
+  pr.u = t[0];
+  pr.v = t[1];
+  pr.H = t[2];
+  pr.a = t[3];
   return pr;
 }
 
@@ -93,7 +107,7 @@ __device__ __forceinline__ void face_flux(int mode, int dir, double gamma, const
                                           const double utm[4], const double utp[4], double f[4], bool& bad) {
   double lin[4] = {0, 0, 0, 0};
   if (mode != 2) {
-    const Prim tm = prim_of(utm, gamma), tp = prim_of(utp, gamma);
+    const Prim tm = prim_frozen(utm), tp = prim_frozen(utp);
     double am[4], ap[4];
     jac_apply(tm, dir, gamma, qm, am);
     jac_apply(tp, dir, gamma, qp, ap);
@@ -124,7 +138,6 @@ __device__ __forceinline__ void face_flux(int mode, int dir, double gamma, const
   }
 }
 
-__device__ __forceinline__ double brk(double a, double b, int i, int n) { return i == n ? b : a + (b - a) * i / n; }
 
 template <int NP>
 struct E2Tile {
@@ -136,11 +149,11 @@ struct E2Tile {
 // Loads node `node` of element `e` (4 comps) of x (scaled) / ut, from the staged
 // tile when e is in it, else from global memory.
 template <int NP>
-__device__ __forceinline__ void load_node(const double* sx, const double* su, long long e0, int te, long long e,
-                                          int node, const double* x, double xs, const double* ut, double q[4],
-                                          double t[4], bool need_ut) {
+__device__ __forceinline__ void load_node(const double* sx, const double* su, int e0, int te, int e, int node,
+                                          const double* x, double xs, const double* ut, double q[4], double t[4],
+                                          bool need_ut) {
   constexpr int NN = NP * NP;
-  const long long le = e - e0;
+  const int le = e - e0;
   if (le >= 0 && le < te) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -150,8 +163,9 @@ __device__ __forceinline__ void load_node(const double* sx, const double* su, lo
   } else {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      q[c] = x[(e * 4 + c) * NN + node] * xs;
-      t[c] = need_ut ? ut[(e * 4 + c) * NN + node] : 0.0;
+      const size_t g = ((size_t)e * 4 + c) * NN + node;
+      q[c] = x[g] * xs;
+      t[c] = need_ut ? ut[g] : 0.0;
     }
   }
 }
@@ -159,7 +173,7 @@ __device__ __forceinline__ void load_node(const double* sx, const double* su, lo
 // Computes the operator for every node of a tile; result per thread in out[4]
 // (valid when the thread maps to a node of the tile).
 template <int NP>
-__device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, long long e0, int te, const double* x, double xs,
+__device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, int e0, int te, const double* x, double xs,
                                         double* sx, double* su, double* sf, double out[4], bool& bad) {
   constexpr int NN = NP * NP;
   constexpr int N = NP - 1;
@@ -170,17 +184,18 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, long long e0
   const bool need_ut = mode != 2;
   // stage x, ut of the tile (coalesced: the tile is contiguous)
   const int cnt = te * 4 * NN;
+  const size_t gbase = (size_t)e0 * 4 * NN;
   for (int idx = t; idx < cnt; idx += blockDim.x) {
-    sx[idx] = x[e0 * 4 * NN + idx] * xs;
-    if (need_ut) su[idx] = P.ut[e0 * 4 * NN + idx];
+    sx[idx] = x[gbase + idx] * xs;
+    if (need_ut) su[idx] = P.ut[gbase + idx];
   }
   __syncthreads();
   double q[4], ut[4];
-  long long e = e0 + le;
+  const int e = e0 + le;
   int ie = 0, je = 0;
   if (active) {
-    ie = (int)(e % P.nx);
-    je = (int)(e / P.nx);
+    je = e / P.nx;
+    ie = e - je * P.nx;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
       q[c] = sx[(le * 4 + c) * NN + node];
@@ -189,7 +204,7 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, long long e0
     // volume fluxes: fx, fy (linear: A(ut) q; nonlinear: F(q) - A(ut) q; full: F(q))
     double fx[4], fy[4];
     if (mode != 2) {
-      const Prim tp = prim_of(ut, P.gamma);
+      const Prim tp = prim_frozen(ut);
       jac_apply(tp, 0, P.gamma, q, fx);
       jac_apply(tp, 1, P.gamma, q, fy);
     }
@@ -213,8 +228,8 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, long long e0
   }
   __syncthreads();
   if (!active) return;
-  const double hx = brk(P.x0, P.x1, ie + 1, P.nx) - brk(P.x0, P.x1, ie, P.nx);
-  const double hy = brk(P.y0, P.y1, je + 1, P.ny) - brk(P.y0, P.y1, je, P.ny);
+  const double hx = __ldg(P.hx + ie);
+  const double hy = __ldg(P.hy + je);
   const double sy = 0.5 * hy * P.w[j];
   const double sxs = 0.5 * hx * P.w[i];
   double r[4];
@@ -235,7 +250,7 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, long long e0
   if (i == N || i == 0) {
     const bool owner = i == N;
     const int ie2 = owner ? (ie + 1 == P.nx ? 0 : ie + 1) : (ie == 0 ? P.nx - 1 : ie - 1);
-    const long long e2 = (long long)je * P.nx + ie2;
+    const int e2 = je * P.nx + ie2;
     const int node2 = j * NP + (owner ? 0 : N);
     double q2[4], u2[4], f[4];
     load_node<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
@@ -249,7 +264,7 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, long long e0
   if (j == N || j == 0) {
     const bool owner = j == N;
     const int je2 = owner ? (je + 1 == P.ny ? 0 : je + 1) : (je == 0 ? P.ny - 1 : je - 1);
-    const long long e2 = (long long)je2 * P.nx + ie;
+    const int e2 = je2 * P.nx + ie;
     const int node2 = (owner ? 0 : N) * NP + i;
     double q2[4], u2[4], f[4];
     load_node<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
@@ -267,23 +282,34 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, long long e0
 
 template <int NP>
 __global__ void __launch_bounds__(256) k_e2_apply(E2P<NP> P, int mode, const double* __restrict__ x,
-                                                  double* __restrict__ y, PhiState* st) {
+                                                  double* __restrict__ y, PhiState* st, double* frozen) {
   constexpr int NN = NP * NP, TE = E2Tile<NP>::TE;
   __shared__ double sx[E2Tile<NP>::VALS], su[E2Tile<NP>::VALS], sf[2 * E2Tile<NP>::VALS];
   if (st && st->stopped) return;
-  const long long ne = (long long)P.nx * P.ny;
-  const long long ntiles = (ne + TE - 1) / TE;
+  const int ne = P.nx * P.ny;
+  const int ntiles = (ne + TE - 1) / TE;
   bool bad = false;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long long e0 = tile * TE;
-    const int te = (int)(ne - e0 < TE ? ne - e0 : TE);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int e0 = tile * TE;
+    const int te = ne - e0 < TE ? ne - e0 : TE;
     __syncthreads();
     double out[4];
     e2_tile<NP>(P, mode, e0, te, x, 1.0, sx, su, sf, out, bad);
     const int t = threadIdx.x, le = t / NN, node = t % NN;
     if (le < te) {
+      const int e = e0 + le;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) y[((e0 + le) * 4 + c) * NN + node] = out[c];
+      for (int c = 0; c < 4; ++c) y[((size_t)e * 4 + c) * NN + node] = out[c];
+      if (frozen && mode == 2) {
+        // freeze (u, v, H, a) of the state for the JVPs of this step (ref = x)
+        double qn[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) qn[c] = x[((size_t)e * 4 + c) * NN + node];
+        const Prim pr = prim_of(qn, P.gamma);
+        const double fv[4] = {pr.u, pr.v, pr.H, pr.a};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) frozen[((size_t)e * 4 + c) * NN + node] = fv[c];
+      }
     }
   }
   if (bad && st) st->domain_flag = 1;
@@ -316,13 +342,13 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
   const double* x = base + (size_t)s_j * s_ld;
   double* y = base + (size_t)(s_j + 1) * s_ld;
   const double xs = s_xs, dt = s_dt;
-  const long long ne = (long long)P.nx * P.ny;
-  const long long ntiles = (ne + TE - 1) / TE;
+  const int ne = P.nx * P.ny;
+  const int ntiles = (ne + TE - 1) / TE;
   double nacc = 0.0;
   bool bad = false;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long long e0 = tile * TE;
-    const int te = (int)(ne - e0 < TE ? ne - e0 : TE);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int e0 = tile * TE;
+    const int te = ne - e0 < TE ? ne - e0 : TE;
     __syncthreads();
     double out[4];
     e2_tile<NP>(P, 0, e0, te, x, xs, sx, su, sf, out, bad);
@@ -334,7 +360,7 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
     }
     __syncthreads();
     for (int idx = t; idx < te * 4 * NN; idx += blockDim.x) {
-      const long long g = e0 * 4 * NN + idx;
+      const size_t g = (size_t)e0 * 4 * NN + idx;
       double v = sx[idx];
       for (int k = 0; k < b.p; ++k)
         if (b.b[b.p - k]) v = fma(s_xt[k], b.b[b.p - k][g], v);
@@ -355,21 +381,53 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
   grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
 }
 
+// (u, v, H, a) of q~ per node (proj/src/euler.cpp:15-24): the frozen data of
+// the linearised operator, 32 B/node like q~ itself.
+__global__ void k_e2_freeze(const double* __restrict__ q, long long nelem, int nn, double gamma,
+                            double* __restrict__ frozen) {
+  const long long nodes = nelem * nn;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < nodes; g += stride) {
+    const long long e = g / nn;
+    const int node = (int)(g - e * nn);
+    double qn[4];
+    for (int c = 0; c < 4; ++c) qn[c] = q[(e * 4 + c) * nn + node];
+    const Prim pr = prim_of(qn, gamma);
+    const double fv[4] = {pr.u, pr.v, pr.H, pr.a};
+    for (int c = 0; c < 4; ++c) frozen[(e * 4 + c) * nn + node] = fv[c];
+  }
+}
+
+double ubreak(double a, double b, int i, int n) { return i == n ? b : a + (b - a) * i / n; }
+
 template <int NP>
 class Euler2D : public OpDevice {
  public:
   E2P<NP> P{};
   int grid = 1;
+  double* frozen = nullptr;
+  double* hbuf = nullptr;
+  ~Euler2D() override {
+    cudaFree(frozen);
+    cudaFree(hbuf);
+  }
+  void freeze(cudaStream_t s, const double* r) override {
+    ref = r;
+    k_e2_freeze<<<1184, 256, 0, s>>>(r, (long long)P.nx * P.ny, NP * NP, P.gamma, frozen);
+  }
   explicit Euler2D(const expdg_op_desc& d) {
     desc = d;
     const HostBasis hb = host_lgl_basis(d.order);
     P.nx = d.nx;
     P.ny = d.ny;
-    P.x0 = d.x0;
-    P.x1 = d.x1;
-    P.y0 = d.y0;
-    P.y1 = d.y1;
     P.gamma = d.gamma;
+    std::vector<double> hs(d.nx + d.ny);
+    for (int i = 0; i < d.nx; ++i) hs[i] = ubreak(d.x0, d.x1, i + 1, d.nx) - ubreak(d.x0, d.x1, i, d.nx);
+    for (int j = 0; j < d.ny; ++j) hs[d.nx + j] = ubreak(d.y0, d.y1, j + 1, d.ny) - ubreak(d.y0, d.y1, j, d.ny);
+    EXPDG_CUDA(cudaMalloc(&hbuf, sizeof(double) * hs.size()));
+    EXPDG_CUDA(cudaMemcpy(hbuf, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice));
+    P.hx = hbuf;
+    P.hy = hbuf + d.nx;
     for (int a = 0; a < NP; ++a) {
       P.w[a] = hb.weights[a];
       for (int b2 = 0; b2 < NP; ++b2) P.WD[a * NP + b2] = hb.weights[a] * hb.D[a * NP + b2];
@@ -377,23 +435,25 @@ class Euler2D : public OpDevice {
     n = (long long)d.nx * d.ny * NP * NP * 4;
     P.n = n;
     comps = 4;
+    EXPDG_CUDA(cudaMalloc(&frozen, sizeof(double) * n));
     const long long ntiles = ((long long)d.nx * d.ny + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
   }
   void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
     E2P<NP> p = P;
-    p.ut = ref;
+    p.ut = frozen;
     k_e2_phi<NP><<<grid, 256, 0, s>>>(p, st, base, partials, b);
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
     E2P<NP> p = P;
-    p.ut = ref;
-    k_e2_apply<NP><<<grid, 256, 0, s>>>(p, which, x, y, nullptr);
+    p.ut = frozen;
+    k_e2_apply<NP><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
   }
+  // R = full rhs(u) and, as a side product, the frozen primitives of u (ref = u)
   void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
     E2P<NP> p = P;
-    p.ut = u;
-    k_e2_apply<NP><<<grid, 256, 0, s>>>(p, 2, u, r, st);
+    p.ut = nullptr;
+    k_e2_apply<NP><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
   }
 };
 
