@@ -13,8 +13,9 @@
  * reference signatures lives in include/expdg_b200.hpp.
  *
  * Conventions: plain pointers and sizes; *_dev pointers are CUDA device
- * pointers (fp64), *_host pointers are host memory; `stream` is a cudaStream_t
- * (NULL = the context's stream).  Every call returns a status code; the
+ * pointers (fp64), *_host pointers are host memory; `stream` is a cudaStream_t:
+ * a non-NULL stream makes the call asynchronous on it; NULL runs on the
+ * context's stream and returns when the work is complete.  Every call returns a status code; the
  * message of the last failure on the calling thread is expdg_last_error().
  * A context is not internally synchronised: one host thread per context.
  */

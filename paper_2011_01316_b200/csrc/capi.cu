@@ -198,6 +198,8 @@ int expdg_op_linearize(expdg_op* op, const double* ref_dev) {
     if (!op->ref_owned) EXPDG_CUDA(cudaMalloc(&op->ref_owned, sizeof(double) * op->dev->n));
     EXPDG_CUDA(cudaMemcpyAsync(op->ref_owned, ref_dev, sizeof(double) * op->dev->n, cudaMemcpyDeviceToDevice, s));
     op->dev->freeze(s, op->ref_owned);
+    // the caller may release ref_dev on return: finish reading it
+    EXPDG_CUDA(cudaStreamSynchronize(s));
   });
 }
 
@@ -207,10 +209,14 @@ static int apply_common(expdg_op* op, int which, const double* x, double* y, voi
     if (which != 2 && !op->dev->ref && op->dev->desc.kind != EXPDG_DENSE)
       throw std::invalid_argument("operator not linearized (call expdg_op_linearize)");
     cudaStream_t s = pick(op, stream);
+    // work queued on the context stream (linearize) precedes the caller's stream
     if (stream) EXPDG_CUDA(cudaStreamSynchronize(op->ctx->eng->stream));
     op->dev->launch_apply(s, which, x, y);
     op->ctx->launches++;
     EXPDG_CUDA(cudaGetLastError());
+    // NULL stream: the context stream, completed before return (no ordering with
+    // the caller's streams is implied otherwise)
+    if (!stream) EXPDG_CUDA(cudaStreamSynchronize(s));
   });
 }
 

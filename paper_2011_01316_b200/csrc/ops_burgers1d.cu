@@ -9,191 +9,14 @@
 // and writes y once: 32 B/DOF (SURVEY.md §8d canonical JVP bytes).
 #include <algorithm>
 
-#include "krylov.cuh"
+#include "burgers_common.cuh"
 
 namespace expdg {
 
 namespace {
 
+using namespace burgers;
 constexpr int kB1Threads = 128;
-
-template <int NP>
-struct B1P {
-  int ne;
-  int periodic;
-  double a, b;
-  double kappa, sigma;
-  int entropy, sigma_adaptive;
-  double w[NP];
-  double G[NP * NP];   // grad_vol(i,j) = w_i D(i,j)      (proj/src/burgers.cpp:49)
-  double Lv[NP * NP];  // lift_vol(i,j) = D(j,i) w_j      (proj/src/burgers.cpp:50)
-  const double* ut;
-  long long n;
-};
-
-// x_e of the uniform breakpoints (proj/src/mesh.cpp:11-16)
-__device__ __forceinline__ double b1_break(double a, double b, int i, int ne) {
-  return i == ne ? b : a + (b - a) * i / ne;
-}
-
-template <int NP>
-__device__ __forceinline__ double b1_face_flux(const B1P<NP>& P, int mode, double um, double up, double utm,
-                                               double utp, double qstar, double h) {
-  const double jump = um - up;  // normal = +1 on every face this helper sees
-  double lin = 0.0;
-  if (mode != 2) {
-    const double diss = 0.5 * fmax(fabs(utm), fabs(utp));
-    lin = 0.5 * (utm * um + utp * up) + diss * jump;
-  }
-  if (mode == 0) return P.kappa * qstar - lin;
-  double nl;
-  if (!P.entropy) {
-    const double ahs = 0.25 * (um * um + up * up);
-    nl = ahs + 0.5 * fmax(fabs(um), fabs(up)) * jump;
-  } else {
-    double soh;
-    if (mode == 1) {
-      const double sig = P.sigma_adaptive ? P.kappa / 100.0 + h * fmax(fabs(utm), fabs(utp)) : P.sigma;
-      soh = sig * (1.0 / h);
-    } else {
-      soh = P.sigma_adaptive ? P.kappa / (100.0 * h) + fmax(fabs(um), fabs(up)) : P.sigma / h;
-    }
-    const double ahs = 0.25 * (um * um + up * up);
-    const double avg = 0.5 * (um + up);
-    nl = (ahs + avg * avg) / 3.0 + soh * jump;
-  }
-  if (mode == 1) return lin - nl;
-  return P.kappa * qstar - nl;
-}
-
-// Element e of the operator; x*/u* point at NP values of the left / centre /
-// right elements (left/right ignored when the face is a Dirichlet boundary).
-template <int NP>
-__device__ __forceinline__ void b1_element(const B1P<NP>& P, int mode, int e, const double* xL,
-                                           const double* xC, const double* xR, const double* uL,
-                                           const double* uC, const double* uR, double* out) {
-  constexpr int N = NP - 1;
-  const bool hasL = P.periodic || e > 0;
-  const bool hasR = P.periodic || e < P.ne - 1;
-  const int eL = e == 0 ? P.ne - 1 : e - 1;
-  const int eR = e == P.ne - 1 ? 0 : e + 1;
-  const double hC = b1_break(P.a, P.b, e + 1, P.ne) - b1_break(P.a, P.b, e, P.ne);
-  const double hL = b1_break(P.a, P.b, eL + 1, P.ne) - b1_break(P.a, P.b, eL, P.ne);
-  const double hR = b1_break(P.a, P.b, eR + 1, P.ne) - b1_break(P.a, P.b, eR, P.ne);
-  double q[NP], qLN = 0.0, qR0 = 0.0;
-  if (mode != 1) {
-    // LDG gradient (proj/src/burgers.cpp:105-130)
-    double r[NP];
-#pragma unroll
-    for (int i = 0; i < NP; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < NP; ++j) s = fma(P.G[i * NP + j], xC[j], s);
-      r[i] = s;
-    }
-    if (hasL) {
-      const double us = 0.5 * (xL[N] + xC[0]);
-      r[0] -= (us - xC[0]);
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < NP; ++j) s = fma(P.G[N * NP + j], xL[j], s);
-      s += (us - xL[N]);
-      qLN = (2.0 / hL) * (s / P.w[N]);
-    } else {
-      r[0] += -1.0 * (0.0 - xC[0]);
-    }
-    if (hasR) {
-      const double us = 0.5 * (xC[N] + xR[0]);
-      r[N] += (us - xC[N]);
-      double s = 0.0;
-#pragma unroll
-      for (int j = 0; j < NP; ++j) s = fma(P.G[j], xR[j], s);
-      s -= (us - xR[0]);
-      qR0 = (2.0 / hR) * (s / P.w[0]);
-    } else {
-      r[N] += (0.0 - xC[N]);
-    }
-    const double c = 2.0 / hC;
-#pragma unroll
-    for (int i = 0; i < NP; ++i) q[i] = c * (r[i] / P.w[i]);
-  }
-  // volume: gq = kappa q - u~ x | u~ x - x^2/2 | kappa q - x^2/2 ; r = -lift gq
-  double gq[NP];
-#pragma unroll
-  for (int p = 0; p < NP; ++p) {
-    const double x = xC[p];
-    if (mode == 0) gq[p] = fma(-uC[p], x, P.kappa * q[p]);
-    else if (mode == 1) gq[p] = uC[p] * x - 0.5 * (x * x);
-    else gq[p] = P.kappa * q[p] - 0.5 * (x * x);
-  }
-  double r[NP];
-#pragma unroll
-  for (int i = 0; i < NP; ++i) {
-    double s = 0.0;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) s = fma(P.Lv[i * NP + p], gq[p], s);
-    r[i] = -s;
-  }
-  // faces (proj/src/burgers.cpp:159-173)
-  if (hasL) {
-    const double f = b1_face_flux(P, mode, xL[N], xC[0], mode == 2 ? 0.0 : uL[N], mode == 2 ? 0.0 : uC[0],
-                                  0.5 * (qLN + q[0]), hL);
-    r[0] -= f;
-  } else {
-    // boundary face: owner e, node 0, normal -1, ghost 0; q** one-sided
-    const double um = xC[0];
-    const double jump = -um;
-    double f;
-    const double utm = mode == 2 ? 0.0 : uC[0];
-    const double lin = 0.5 * (utm * um + 0.0) + 0.5 * fmax(fabs(utm), 0.0) * jump;
-    if (mode == 0) {
-      f = P.kappa * q[0] - lin;
-    } else {
-      double nl;
-      if (!P.entropy) {
-        nl = 0.25 * (um * um) + 0.5 * fabs(um) * jump;
-      } else {
-        double soh;
-        if (mode == 1) soh = (P.sigma_adaptive ? P.kappa / 100.0 + hC * fabs(utm) : P.sigma) * (1.0 / hC);
-        else soh = P.sigma_adaptive ? P.kappa / (100.0 * hC) + fabs(um) : P.sigma / hC;
-        const double avg = 0.5 * um;
-        nl = (0.25 * (um * um) + avg * avg) / 3.0 + soh * jump;
-      }
-      f = mode == 1 ? lin - nl : P.kappa * q[0] - nl;
-    }
-    r[0] += -1.0 * f;
-  }
-  if (hasR) {
-    const double f = b1_face_flux(P, mode, xC[N], xR[0], mode == 2 ? 0.0 : uC[N], mode == 2 ? 0.0 : uR[0],
-                                  0.5 * (q[N] + qR0), hC);
-    r[N] += f;
-  } else {
-    const double um = xC[N];
-    const double jump = um;
-    const double utm = mode == 2 ? 0.0 : uC[N];
-    const double lin = 0.5 * (utm * um + 0.0) + 0.5 * fmax(fabs(utm), 0.0) * jump;
-    double f;
-    if (mode == 0) {
-      f = P.kappa * q[N] - lin;
-    } else {
-      double nl;
-      if (!P.entropy) {
-        nl = 0.25 * (um * um) + 0.5 * fabs(um) * jump;
-      } else {
-        double soh;
-        if (mode == 1) soh = (P.sigma_adaptive ? P.kappa / 100.0 + hC * fabs(utm) : P.sigma) * (1.0 / hC);
-        else soh = P.sigma_adaptive ? P.kappa / (100.0 * hC) + fabs(um) : P.sigma / hC;
-        const double avg = 0.5 * um;
-        nl = (0.25 * (um * um) + avg * avg) / 3.0 + soh * jump;
-      }
-      f = mode == 1 ? lin - nl : P.kappa * q[N] - nl;
-    }
-    r[N] += f;
-  }
-  const double c = 2.0 / hC;
-#pragma unroll
-  for (int i = 0; i < NP; ++i) out[i] = c * (r[i] / P.w[i]);
-}
 
 // Stage [e0-1, e0+E] of x (scaled by xs) and u~ into shared memory.
 template <int NP>

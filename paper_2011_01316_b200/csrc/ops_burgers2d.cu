@@ -1,0 +1,226 @@
+// 2D viscous Burgers (config C3, an extension: BurgersOperator is 1D only,
+// proj/src/burgers.cpp:24-25).  Collocated tensor-product LDG on a Cartesian
+// quad mesh = the reference 1D LDG operator applied along every element x-line
+// plus along every y-line (see oracle/src/burgers.cpp, Burgers2DOperator), so a
+// y-invariant field reproduces the 1D operator exactly.
+//
+// CTA tile of floor(256 / NP) elements; phase 1: one thread per (element, row)
+// runs the 1D element kernel along x; phase 2: one thread per (element, column)
+// along y and adds.  Line neighbours come from L2.
+#include <algorithm>
+
+#include "burgers_common.cuh"
+
+namespace expdg {
+
+namespace {
+
+using namespace burgers;
+
+template <int NP>
+struct B2Tile {
+  static constexpr int TE = 256 / NP;
+};
+
+// line of NP values: x-line (row j) or y-line (column i) of element e
+__device__ __forceinline__ void gather(const double* v, double s, long long e, int NP_, int line, bool xdir,
+                                       double* out) {
+  const int NN = NP_ * NP_;
+  for (int t = 0; t < NP_; ++t) out[t] = v[e * NN + (xdir ? line * NP_ + t : t * NP_ + line)] * s;
+}
+
+template <int NP>
+__device__ __forceinline__ void b2_tile(const B1P<NP>& Px, const B1P<NP>& Py, int nx, int ny, int mode, long long e0,
+                                        int te, const double* x, double xs, double* sout) {
+  constexpr int NN = NP * NP;
+  const int t = threadIdx.x;
+  const int le = t / NP, line = t % NP;
+  const bool active = le < te;
+  const bool need_ut = mode != 2;
+  double xL[NP], xC[NP], xR[NP], uL[NP], uC[NP], uR[NP], out[NP];
+  long long e = 0;
+  int ie = 0, je = 0;
+  if (active) {
+    e = e0 + le;
+    je = (int)(e / nx);
+    ie = (int)(e - (long long)je * nx);
+    // x-line (row `line`)
+    const long long eW = (long long)je * nx + (ie == 0 ? nx - 1 : ie - 1);
+    const long long eE = (long long)je * nx + (ie == nx - 1 ? 0 : ie + 1);
+    gather(x, xs, eW, NP, line, true, xL);
+    gather(x, xs, e, NP, line, true, xC);
+    gather(x, xs, eE, NP, line, true, xR);
+    if (need_ut) {
+      gather(Px.ut, 1.0, eW, NP, line, true, uL);
+      gather(Px.ut, 1.0, e, NP, line, true, uC);
+      gather(Px.ut, 1.0, eE, NP, line, true, uR);
+    }
+    b1_element<NP>(Px, mode, ie, xL, xC, xR, uL, uC, uR, out);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) sout[le * NN + line * NP + i] = out[i];
+  }
+  __syncthreads();
+  if (active) {
+    // y-line (column `line`)
+    const long long eS = (long long)(je == 0 ? ny - 1 : je - 1) * nx + ie;
+    const long long eN = (long long)(je == ny - 1 ? 0 : je + 1) * nx + ie;
+    gather(x, xs, eS, NP, line, false, xL);
+    gather(x, xs, e, NP, line, false, xC);
+    gather(x, xs, eN, NP, line, false, xR);
+    if (need_ut) {
+      gather(Py.ut, 1.0, eS, NP, line, false, uL);
+      gather(Py.ut, 1.0, e, NP, line, false, uC);
+      gather(Py.ut, 1.0, eN, NP, line, false, uR);
+    }
+    b1_element<NP>(Py, mode, je, xL, xC, xR, uL, uC, uR, out);
+#pragma unroll
+    for (int j = 0; j < NP; ++j) sout[le * NN + j * NP + line] += out[j];
+  }
+  __syncthreads();
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256) k_b2_apply(B1P<NP> Px, B1P<NP> Py, int nx, int ny, int mode,
+                                                  const double* __restrict__ x, double* __restrict__ y,
+                                                  const PhiState* st) {
+  constexpr int NN = NP * NP, TE = B2Tile<NP>::TE;
+  __shared__ double sout[TE * NN];
+  if (st && st->stopped) return;
+  const long long ne = (long long)nx * ny;
+  const long long ntiles = (ne + TE - 1) / TE;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = tile * TE;
+    const int te = (int)(ne - e0 < TE ? ne - e0 : TE);
+    b2_tile<NP>(Px, Py, nx, ny, mode, e0, te, x, 1.0, sout);
+    for (int idx = threadIdx.x; idx < te * NN; idx += blockDim.x) y[e0 * NN + idx] = sout[idx];
+    __syncthreads();
+  }
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256) k_b2_phi(B1P<NP> Px, B1P<NP> Py, int nx, int ny, PhiState* st, double* base,
+                                                double* partials, BArgs b) {
+  constexpr int NN = NP * NP, TE = B2Tile<NP>::TE;
+  __shared__ double sout[TE * NN];
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[8];
+  __shared__ double s_red[1];
+  if (threadIdx.x == 0) {
+    const int a = st->action;
+    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    if (s_go) {
+      s_j = st->j;
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[Px.n + i] * s_xs : 0.0;
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  const long long ne = (long long)nx * ny;
+  const long long ntiles = (ne + TE - 1) / TE;
+  double nacc = 0.0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = tile * TE;
+    const int te = (int)(ne - e0 < TE ? ne - e0 : TE);
+    b2_tile<NP>(Px, Py, nx, ny, 0, e0, te, x, xs, sout);
+    for (int idx = threadIdx.x; idx < te * NN; idx += blockDim.x) {
+      const long long g = e0 * NN + idx;
+      double v = sout[idx];
+      for (int k = 0; k < b.p; ++k)
+        if (b.b[b.p - k]) v = fma(s_xt[k], b.b[b.p - k][g], v);
+      v = dt * v;
+      y[g] = v;
+      nacc = fma(v, v, nacc);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here) {
+    const int i = threadIdx.x;
+    const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
+    y[Px.n + i] = v;
+    nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (threadIdx.x == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+}
+
+template <int NP>
+class Burgers2D : public OpDevice {
+ public:
+  B1P<NP> Px{}, Py{};
+  int nx = 0, ny = 0, grid = 1;
+  explicit Burgers2D(const expdg_op_desc& d) {
+    desc = d;
+    const HostBasis hb = host_lgl_basis(d.order);
+    nx = d.nx;
+    ny = d.ny;
+    for (B1P<NP>* P : {&Px, &Py}) {
+      P->periodic = d.periodic;
+      P->kappa = d.kappa;
+      P->sigma = d.sigma;
+      P->entropy = d.flux == 1;
+      P->sigma_adaptive = d.sigma_adaptive;
+      for (int i = 0; i < NP; ++i) {
+        P->w[i] = hb.weights[i];
+        for (int j = 0; j < NP; ++j) {
+          P->G[i * NP + j] = hb.weights[i] * hb.D[i * NP + j];
+          P->Lv[i * NP + j] = hb.D[j * NP + i] * hb.weights[j];
+        }
+      }
+    }
+    Px.ne = d.nx;
+    Px.a = d.x0;
+    Px.b = d.x1;
+    Py.ne = d.ny;
+    Py.a = d.y0;
+    Py.b = d.y1;
+    n = (long long)d.nx * d.ny * NP * NP;
+    Px.n = Py.n = n;
+    comps = 1;
+    const long long ntiles = ((long long)d.nx * d.ny + B2Tile<NP>::TE - 1) / B2Tile<NP>::TE;
+    grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
+  }
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+    B1P<NP> px = Px, py = Py;
+    px.ut = py.ut = ref;
+    k_b2_phi<NP><<<grid, 256, 0, s>>>(px, py, nx, ny, st, base, partials, b);
+  }
+  void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
+    B1P<NP> px = Px, py = Py;
+    px.ut = py.ut = ref;
+    k_b2_apply<NP><<<grid, 256, 0, s>>>(px, py, nx, ny, which, x, y, nullptr);
+  }
+  void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
+    B1P<NP> px = Px, py = Py;
+    px.ut = py.ut = u;
+    k_b2_apply<NP><<<grid, 256, 0, s>>>(px, py, nx, ny, 2, u, r, st);
+  }
+};
+
+}  // namespace
+
+std::unique_ptr<OpDevice> make_burgers2d(const expdg_op_desc& d) {
+  switch (d.order + 1) {
+    case 2: return std::make_unique<Burgers2D<2>>(d);
+    case 3: return std::make_unique<Burgers2D<3>>(d);
+    case 4: return std::make_unique<Burgers2D<4>>(d);
+    case 5: return std::make_unique<Burgers2D<5>>(d);
+    case 6: return std::make_unique<Burgers2D<6>>(d);
+    case 7: return std::make_unique<Burgers2D<7>>(d);
+    case 8: return std::make_unique<Burgers2D<8>>(d);
+    case 9: return std::make_unique<Burgers2D<9>>(d);
+  }
+  throw std::invalid_argument("burgers2d: device orders are 1..8");
+}
+
+}  // namespace expdg

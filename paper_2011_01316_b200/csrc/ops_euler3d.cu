@@ -1,0 +1,454 @@
+// 3D compressible Euler, Lax-Friedrichs split (config C5, an extension of the
+// reference's 2D EulerOperator, proj/src/euler.cpp:186-388, to hexahedra and
+// five conserved variables; the CPU definition is oracle/src/euler.cpp,
+// Euler3DOperator).  A z-invariant state with w = 0 reproduces the 2D operator.
+//
+// One thread per LGL node; CTA tile of floor(256 / NP^3) elements; the frozen
+// data are the per-node primitives (u, v, w, H, a) of q~ (40 B/node, the size
+// of q~ itself) written once per step by the residual kernel.
+#include <algorithm>
+#include <vector>
+
+#include "krylov.cuh"
+
+namespace expdg {
+
+namespace {
+
+template <int NP>
+struct E3P {
+  int nx, ny, nz;
+  double gamma;
+  double w[NP];
+  double WD[NP * NP];
+  const double* ut;  // frozen (u, v, w, H, a) per node
+  const double* hx;
+  const double* hy;
+  const double* hz;
+  long long n;
+};
+
+struct Prim3 {
+  double u[3], H, a, p;
+};
+
+__device__ __forceinline__ Prim3 prim3_of(const double q[5], double gamma) {
+  Prim3 pr;
+  const double rho = q[0];
+  pr.u[0] = q[1] / rho;
+  pr.u[1] = q[2] / rho;
+  pr.u[2] = q[3] / rho;
+  pr.p = (gamma - 1.0) * (q[4] - 0.5 * rho * (pr.u[0] * pr.u[0] + pr.u[1] * pr.u[1] + pr.u[2] * pr.u[2]));
+  pr.a = sqrt(gamma * pr.p / rho);
+  pr.H = (q[4] + pr.p) / rho;
+  return pr;
+}
+
+__device__ __forceinline__ Prim3 prim3_frozen(const double t[5]) {
+  Prim3 pr;
+  pr.u[0] = t[0];
+  pr.u[1] = t[1];
+  pr.u[2] = t[2];
+  pr.H = t[3];
+  pr.a = t[4];
+  pr.p = 0.0;
+  return pr;
+}
+
+__device__ __forceinline__ bool admissible5(const double q[5], double gamma) {
+  if (!(q[0] > 0.0)) return false;
+  const double p = (gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / q[0]);
+  return p > 0.0;
+}
+
+// out = A(pr, e_dir) x  (rows of the 3D flux Jacobian, oracle jac3)
+__device__ __forceinline__ void jac3_apply(const Prim3& pr, int dir, double gamma, const double x[5],
+                                           double out[5]) {
+  const double gm1 = gamma - 1.0;
+  const double un = pr.u[dir];
+  const double phi = 0.5 * gm1 * (pr.u[0] * pr.u[0] + pr.u[1] * pr.u[1] + pr.u[2] * pr.u[2]);
+  out[0] = x[1 + dir];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const double nr = r == dir ? 1.0 : 0.0;
+    double s = (phi * nr - pr.u[r] * un) * x[0];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double nc = c == dir ? 1.0 : 0.0;
+      double a = pr.u[r] * nc - gm1 * nr * pr.u[c];
+      if (c == r) a += un;
+      s = fma(a, x[1 + c], s);
+    }
+    out[1 + r] = fma(gm1 * nr, x[4], s);
+  }
+  double s = ((phi - pr.H) * un) * x[0];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) s = fma((c == dir ? pr.H : 0.0) - gm1 * pr.u[c] * un, x[1 + c], s);
+  out[4] = fma(gamma * un, x[4], s);
+}
+
+__device__ __forceinline__ void flux3_dir(const double q[5], const Prim3& pr, int dir, double f[5]) {
+  const double vn = pr.u[dir];
+  f[0] = q[dir + 1];
+  f[1] = q[1] * vn;
+  f[2] = q[2] * vn;
+  f[3] = q[3] * vn;
+  f[dir + 1] += pr.p;
+  f[4] = q[0] * vn * pr.H;
+}
+
+// face normal +e_dir between owner (m) and neighbour (p): 0 linear LF, 1 full - linear, 2 full
+__device__ __forceinline__ void face3(int mode, int dir, double gamma, const double qm[5], const double qp[5],
+                                      const double tm_[5], const double tp_[5], double f[5], bool& bad) {
+  double lin[5] = {0, 0, 0, 0, 0};
+  if (mode != 2) {
+    const Prim3 tm = prim3_frozen(tm_), tp = prim3_frozen(tp_);
+    double am[5], ap[5];
+    jac3_apply(tm, dir, gamma, qm, am);
+    jac3_apply(tp, dir, gamma, qp, ap);
+    const double lam = fmax(fabs(tm.u[dir]) + tm.a, fabs(tp.u[dir]) + tp.a);
+#pragma unroll
+    for (int c = 0; c < 5; ++c) lin[c] = 0.5 * (am[c] + ap[c]) + 0.5 * (lam * (qm[c] - qp[c]));
+  }
+  if (mode == 0) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) f[c] = lin[c];
+    return;
+  }
+  if (!admissible5(qm, gamma) || !admissible5(qp, gamma)) bad = true;
+  const Prim3 pm = prim3_of(qm, gamma), pp = prim3_of(qp, gamma);
+  double fm[5], fp[5];
+  flux3_dir(qm, pm, dir, fm);
+  flux3_dir(qp, pp, dir, fp);
+  const double s = 0.5 * fmax(fabs(pm.u[dir]) + pm.a, fabs(pp.u[dir]) + pp.a);
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    const double full = 0.5 * (fm[c] + fp[c]) + s * (qm[c] - qp[c]);
+    f[c] = mode == 1 ? full - lin[c] : full;
+  }
+}
+
+template <int NP>
+struct E3Tile {
+  static constexpr int NN = NP * NP * NP;
+  static constexpr int TE = 256 / NN > 0 ? 256 / NN : 1;
+  static constexpr int VALS = TE * 5 * NN;
+};
+
+template <int NP>
+__device__ __forceinline__ void load5(const double* sx, const double* su, long long e0, int te, long long e, int node,
+                                      const double* x, double xs, const double* ut, double q[5], double t[5],
+                                      bool need_ut) {
+  constexpr int NN = NP * NP * NP;
+  const long long le = e - e0;
+  if (le >= 0 && le < te) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      q[c] = sx[(le * 5 + c) * NN + node];
+      t[c] = need_ut ? ut[((size_t)e * 5 + c) * NN + node] : 0.0;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      const size_t g = ((size_t)e * 5 + c) * NN + node;
+      q[c] = x[g] * xs;
+      t[c] = need_ut ? ut[g] : 0.0;
+    }
+  }
+}
+
+template <int NP>
+__device__ __forceinline__ void e3_tile(const E3P<NP>& P, int mode, long long e0, int te, const double* x, double xs,
+                                        double* sx, double* su, double* sf, double out[5], bool& bad) {
+  constexpr int NN = NP * NP * NP;
+  constexpr int N = NP - 1;
+  const int t = threadIdx.x;
+  const int le = t / NN, node = t % NN;
+  const int i = node % NP, j = (node / NP) % NP, k = node / (NP * NP);
+  const bool active = le < te;
+  const bool need_ut = mode != 2;
+  const int cnt = te * 5 * NN;
+  const size_t gbase = (size_t)e0 * 5 * NN;
+  for (int idx = t; idx < cnt; idx += blockDim.x) sx[idx] = x[gbase + idx] * xs;
+  __syncthreads();
+  double q[5], ut[5];
+  const long long e = e0 + le;
+  int ix = 0, iy = 0, iz = 0;
+  if (active) {
+    const long long exy = (long long)P.nx * P.ny;
+    iz = (int)(e / exy);
+    const long long r = e - (long long)iz * exy;
+    iy = (int)(r / P.nx);
+    ix = (int)(r - (long long)iy * P.nx);
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      q[c] = sx[(le * 5 + c) * NN + node];
+      ut[c] = need_ut ? P.ut[gbase + (le * 5 + c) * NN + node] : 0.0;
+    }
+    double fl[3][5];
+    if (mode != 2) {
+      const Prim3 tp = prim3_frozen(ut);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) jac3_apply(tp, d, P.gamma, q, fl[d]);
+    }
+    if (mode != 0) {
+      if (!admissible5(q, P.gamma)) bad = true;
+      const Prim3 pq = prim3_of(q, P.gamma);
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        double F[5];
+        flux3_dir(q, pq, d, F);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) fl[d][c] = mode == 1 ? F[c] - fl[d][c] : F[c];
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+#pragma unroll
+      for (int c = 0; c < 5; ++c) sf[((le * 3 + d) * 5 + c) * NN + node] = fl[d][c];
+  }
+  __syncthreads();
+  if (!active) return;
+  const double hx = __ldg(P.hx + ix), hy = __ldg(P.hy + iy), hz = __ldg(P.hz + iz);
+  const double sxv = (0.25 * hy * hz) * P.w[j] * P.w[k];
+  const double syv = (0.25 * hz * hx) * P.w[i] * P.w[k];
+  const double szv = (0.25 * hx * hy) * P.w[i] * P.w[j];
+  double r[5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    const double* fx = sf + ((le * 3 + 0) * 5 + c) * NN + (k * NP + j) * NP;
+    const double* fy = sf + ((le * 3 + 1) * 5 + c) * NN + k * NP * NP + i;
+    const double* fz = sf + ((le * 3 + 2) * 5 + c) * NN + j * NP + i;
+    double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+    for (int m = 0; m < NP; ++m) {
+      ax = fma(P.WD[m * NP + i], fx[m], ax);
+      ay = fma(P.WD[m * NP + j], fy[m * NP], ay);
+      az = fma(P.WD[m * NP + k], fz[m * NP * NP], az);
+    }
+    r[c] = sxv * ax;
+    r[c] += syv * ay;
+    r[c] += szv * az;
+  }
+  // faces: x, y, z (oracle face order), owner on the low side, periodic
+  const int idx3[3] = {i, j, k};
+  const int nel[3] = {P.nx, P.ny, P.nz};
+  const int pos[3] = {ix, iy, iz};
+  const double area[3] = {0.25 * (hy * hz), 0.25 * (hx * hz), 0.25 * (hx * hy)};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int a = idx3[d];
+    if (a != 0 && a != N) continue;
+    const bool owner = a == N;
+    int p2[3] = {pos[0], pos[1], pos[2]};
+    p2[d] = owner ? (pos[d] + 1 == nel[d] ? 0 : pos[d] + 1) : (pos[d] == 0 ? nel[d] - 1 : pos[d] - 1);
+    const long long e2 = ((long long)p2[2] * P.ny + p2[1]) * P.nx + p2[0];
+    int n2[3] = {i, j, k};
+    n2[d] = owner ? 0 : N;
+    const int node2 = (n2[2] * NP + n2[1]) * NP + n2[0];
+    double q2[5], u2[5], f[5];
+    load5<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
+    if (owner) face3(mode, d, P.gamma, q, q2, ut, u2, f, bad);
+    else face3(mode, d, P.gamma, q2, q, u2, ut, f, bad);
+    // face quadrature weight (1/4 area) w_t1 w_t2 with (t1, t2) the two tangential node indices
+    const int t1 = d == 0 ? j : i;
+    const int t2 = d == 2 ? j : k;
+    const double fw = area[d] * P.w[t1] * P.w[t2];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) r[c] = owner ? r[c] - fw * f[c] : r[c] + fw * f[c];
+  }
+  const double scale = 8.0 / (hx * hy * hz);
+  const double im = scale / (P.w[i] * P.w[j] * P.w[k]);
+#pragma unroll
+  for (int c = 0; c < 5; ++c) out[c] = r[c] * im;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256) k_e3_apply(E3P<NP> P, int mode, const double* __restrict__ x,
+                                                  double* __restrict__ y, PhiState* st, double* frozen) {
+  constexpr int NN = NP * NP * NP, TE = E3Tile<NP>::TE;
+  __shared__ double sx[E3Tile<NP>::VALS], sf[3 * E3Tile<NP>::VALS];
+  double* su = nullptr;
+  if (st && st->stopped) return;
+  const long long ne = (long long)P.nx * P.ny * P.nz;
+  const long long ntiles = (ne + TE - 1) / TE;
+  bool bad = false;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = tile * TE;
+    const int te = (int)(ne - e0 < TE ? ne - e0 : TE);
+    __syncthreads();
+    double out[5];
+    e3_tile<NP>(P, mode, e0, te, x, 1.0, sx, su, sf, out, bad);
+    const int t = threadIdx.x, le = t / NN, node = t % NN;
+    if (le < te) {
+      const long long e = e0 + le;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) y[((size_t)e * 5 + c) * NN + node] = out[c];
+      if (frozen && mode == 2) {
+        double qn[5];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) qn[c] = x[((size_t)e * 5 + c) * NN + node];
+        const Prim3 pr = prim3_of(qn, P.gamma);
+        const double fv[5] = {pr.u[0], pr.u[1], pr.u[2], pr.H, pr.a};
+#pragma unroll
+        for (int c = 0; c < 5; ++c) frozen[((size_t)e * 5 + c) * NN + node] = fv[c];
+      }
+    }
+  }
+  if (bad && st) st->domain_flag = 1;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256) k_e3_phi(E3P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
+  constexpr int NN = NP * NP * NP, TE = E3Tile<NP>::TE;
+  __shared__ double sx[E3Tile<NP>::VALS], sf[3 * E3Tile<NP>::VALS];
+  double* su = nullptr;
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[8];
+  __shared__ double s_red[1];
+  if (threadIdx.x == 0) {
+    const int a = st->action;
+    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    if (s_go) {
+      s_j = st->j;
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[P.n + i] * s_xs : 0.0;
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  const long long ne = (long long)P.nx * P.ny * P.nz;
+  const long long ntiles = (ne + TE - 1) / TE;
+  double nacc = 0.0;
+  bool bad = false;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = tile * TE;
+    const int te = (int)(ne - e0 < TE ? ne - e0 : TE);
+    __syncthreads();
+    double out[5];
+    e3_tile<NP>(P, 0, e0, te, x, xs, sx, su, sf, out, bad);
+    const int t = threadIdx.x, le = t / NN, node = t % NN;
+    __syncthreads();
+    if (le < te) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) sx[(le * 5 + c) * NN + node] = out[c];
+    }
+    __syncthreads();
+    for (int idx = t; idx < te * 5 * NN; idx += blockDim.x) {
+      const size_t g = (size_t)e0 * 5 * NN + idx;
+      double v = sx[idx];
+      for (int q = 0; q < b.p; ++q)
+        if (b.b[b.p - q]) v = fma(s_xt[q], b.b[b.p - q][g], v);
+      v = dt * v;
+      y[g] = v;
+      nacc = fma(v, v, nacc);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here) {
+    const int i = threadIdx.x;
+    const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
+    y[P.n + i] = v;
+    nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (threadIdx.x == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+}
+
+__global__ void k_e3_freeze(const double* __restrict__ q, long long nelem, int nn, double gamma,
+                            double* __restrict__ frozen) {
+  const long long nodes = nelem * nn;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < nodes; g += stride) {
+    const long long e = g / nn;
+    const int node = (int)(g - e * nn);
+    double qn[5];
+    for (int c = 0; c < 5; ++c) qn[c] = q[(e * 5 + c) * nn + node];
+    const Prim3 pr = prim3_of(qn, gamma);
+    const double fv[5] = {pr.u[0], pr.u[1], pr.u[2], pr.H, pr.a};
+    for (int c = 0; c < 5; ++c) frozen[(e * 5 + c) * nn + node] = fv[c];
+  }
+}
+
+double ub3(double a, double b, int i, int n) { return i == n ? b : a + (b - a) * i / n; }
+
+template <int NP>
+class Euler3D : public OpDevice {
+ public:
+  E3P<NP> P{};
+  int grid = 1;
+  double* frozen = nullptr;
+  double* hbuf = nullptr;
+  ~Euler3D() override {
+    cudaFree(frozen);
+    cudaFree(hbuf);
+  }
+  explicit Euler3D(const expdg_op_desc& d) {
+    desc = d;
+    const HostBasis hb = host_lgl_basis(d.order);
+    P.nx = d.nx;
+    P.ny = d.ny;
+    P.nz = d.nz;
+    P.gamma = d.gamma;
+    std::vector<double> hs(d.nx + d.ny + d.nz);
+    for (int i = 0; i < d.nx; ++i) hs[i] = ub3(d.x0, d.x1, i + 1, d.nx) - ub3(d.x0, d.x1, i, d.nx);
+    for (int j = 0; j < d.ny; ++j) hs[d.nx + j] = ub3(d.y0, d.y1, j + 1, d.ny) - ub3(d.y0, d.y1, j, d.ny);
+    for (int k = 0; k < d.nz; ++k) hs[d.nx + d.ny + k] = ub3(d.z0, d.z1, k + 1, d.nz) - ub3(d.z0, d.z1, k, d.nz);
+    EXPDG_CUDA(cudaMalloc(&hbuf, sizeof(double) * hs.size()));
+    EXPDG_CUDA(cudaMemcpy(hbuf, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice));
+    P.hx = hbuf;
+    P.hy = hbuf + d.nx;
+    P.hz = hbuf + d.nx + d.ny;
+    for (int a = 0; a < NP; ++a) {
+      P.w[a] = hb.weights[a];
+      for (int b2 = 0; b2 < NP; ++b2) P.WD[a * NP + b2] = hb.weights[a] * hb.D[a * NP + b2];
+    }
+    n = (long long)d.nx * d.ny * d.nz * NP * NP * NP * 5;
+    P.n = n;
+    comps = 5;
+    EXPDG_CUDA(cudaMalloc(&frozen, sizeof(double) * n));
+    const long long ntiles = ((long long)d.nx * d.ny * d.nz + E3Tile<NP>::TE - 1) / E3Tile<NP>::TE;
+    grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
+  }
+  void freeze(cudaStream_t s, const double* r) override {
+    ref = r;
+    k_e3_freeze<<<1184, 256, 0, s>>>(r, (long long)P.nx * P.ny * P.nz, NP * NP * NP, P.gamma, frozen);
+  }
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+    E3P<NP> p = P;
+    p.ut = frozen;
+    k_e3_phi<NP><<<grid, 256, 0, s>>>(p, st, base, partials, b);
+  }
+  void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
+    E3P<NP> p = P;
+    p.ut = frozen;
+    k_e3_apply<NP><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
+  }
+  void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
+    E3P<NP> p = P;
+    p.ut = nullptr;
+    k_e3_apply<NP><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
+  }
+};
+
+}  // namespace
+
+std::unique_ptr<OpDevice> make_euler3d(const expdg_op_desc& d) {
+  switch (d.order + 1) {
+    case 2: return std::make_unique<Euler3D<2>>(d);
+    case 3: return std::make_unique<Euler3D<3>>(d);
+    case 4: return std::make_unique<Euler3D<4>>(d);
+  }
+  throw std::invalid_argument("euler3d: device orders are 1..3");
+}
+
+}  // namespace expdg

@@ -1,0 +1,229 @@
+"""GPU parity for the configs outside the reference's dimensionality:
+C3 (2D tensor-product LDG Burgers) and C5 (3D Lax-Friedrichs Euler).  Each is
+checked against its oracle definition, reduces to the reference-matched lower-
+dimensional device operator, and (C5) converges at design order on the exact
+isentropic vortex."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2011_01316_b200 as pkg
+from paper_2011_01316_b200 import configs
+from tests.gpu_util import oracle_problem, rel, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return pkg.Context(0)
+
+
+# ------------------------------------------------------------------ 2D Burgers
+@pytest.mark.parametrize("order,nx,ny,periodic,flux,sigma", [
+    (4, 6, 5, True, "lf", 0.0),
+    (3, 4, 7, False, "ef", 1e-3),
+    (2, 5, 5, True, "ef", 0.5),
+    (7, 3, 2, True, "lf", 0.0),
+])
+def test_burgers2d_apply_matches_oracle(ctx, order, nx, ny, periodic, flux, sigma):
+    rng = np.random.default_rng(order + 10 * nx)
+    spec = pkg.OperatorSpec("burgers2d", order, nx, ny, box=(0, 1, 0, 2, 0, 1), periodic=periodic, kappa=1e-2,
+                            flux=flux, sigma=sigma)
+    op = pkg.Operator(ctx, spec)
+    orc = oracle_problem(spec)
+    ref, x = rng.standard_normal(op.dim), rng.standard_normal(op.dim)
+    op.linearize(to_dev(ref))
+    assert rel(to_host(op.apply_linear(to_dev(x))), orc.apply_linear(ref, x)) < 1e-13
+    assert rel(to_host(op.apply_nonlinear(to_dev(x))), orc.apply_nonlinear(ref, x)) < 1e-13
+    assert rel(to_host(op.full_rhs(to_dev(x))), orc.full_rhs(x)) < 1e-13
+
+
+def test_burgers2d_y_invariant_reduces_to_1d(ctx):
+    # a y-invariant field: the 2D operator equals the reference-matched 1D operator on every line
+    order, nx, ny = 4, 16, 3
+    rng = np.random.default_rng(3)
+    s1 = pkg.OperatorSpec("burgers1d", order, nx, box=(0, 2 * math.pi, 0, 1, 0, 1), kappa=1e-2, flux="ef", sigma=0.3)
+    s2 = pkg.OperatorSpec("burgers2d", order, nx, ny, box=(0, 2 * math.pi, 0, 1, 0, 1), kappa=1e-2, flux="ef",
+                          sigma=0.3)
+    op1, op2 = pkg.Operator(ctx, s1), pkg.Operator(ctx, s2)
+    np1 = order + 1
+    u1, x1 = rng.standard_normal(op1.dim), rng.standard_normal(op1.dim)
+
+    def extrude(v):
+        out = np.empty(op2.dim)
+        blk = out.reshape(ny, nx, np1, np1)  # [je][ie][j][i]
+        blk[:] = v.reshape(nx, np1)[None, :, None, :]
+        return out
+
+    op1.linearize(to_dev(u1))
+    op2.linearize(to_dev(extrude(u1)))
+    for f1, f2 in ((op1.apply_linear, op2.apply_linear), (op1.apply_nonlinear, op2.apply_nonlinear),
+                   (op1.full_rhs, op2.full_rhs)):
+        y1 = to_host(f1(to_dev(x1)))
+        y2 = to_host(f2(to_dev(extrude(x1))))
+        assert np.abs(y2 - extrude(y1)).max() <= 1e-12 * np.abs(y1).max()
+
+
+def test_c3_reduced_mesh_epi2_parity(ctx):
+    w = configs.scaled(configs.C3, 16, steps=3)
+    u0 = w.initial_condition()
+    orc = oracle_problem(w.spec()).integrate("epi2", u0, w.dt, w.steps * w.dt, tol=w.tol, max_basis=w.max_basis,
+                                             orth_length=w.max_basis)
+    op = pkg.Operator(ctx, w.spec())
+    r = pkg.integrate(ctx, op, to_dev(u0), "epi2", w.dt, w.steps * w.dt, tol=w.tol, max_basis=w.max_basis,
+                      orth_length=w.max_basis)
+    assert r.status == orc.status == "completed"
+    assert rel(to_host(r.u), orc.u) <= 1e-9
+    d_dev = np.diff(np.concatenate([[0], r.iters_per_step]))
+    d_orc = np.diff(np.concatenate([[0], orc.iters_per_step]))
+    assert np.max(np.abs(d_dev - d_orc)) <= 1
+
+
+# ------------------------------------------------------------------ 3D Euler
+def random_state5(rng, ne, npe):
+    q = np.empty(ne * 5 * npe)
+    for e in range(ne):
+        rho = rng.uniform(0.5, 2.0, npe)
+        vel = [rng.uniform(-1, 1, npe) for _ in range(3)]
+        p = rng.uniform(0.5, 2.0, npe)
+        blk = q[e * 5 * npe:(e + 1) * 5 * npe].reshape(5, npe)
+        blk[0] = rho
+        for d in range(3):
+            blk[1 + d] = rho * vel[d]
+        blk[4] = p / 0.4 + 0.5 * rho * sum(v * v for v in vel)
+    return q
+
+
+@pytest.mark.parametrize("order,n", [(1, 3), (2, 3), (3, 2)])
+def test_euler3d_apply_matches_oracle(ctx, order, n):
+    rng = np.random.default_rng(order)
+    spec = pkg.OperatorSpec("euler3d", order, n, n + 1, n, box=(0, 1, 0, 2, 0, 1.5), euler_flux="lf")
+    op = pkg.Operator(ctx, spec)
+    orc = oracle_problem(spec)
+    npe = (order + 1) ** 3
+    ne = n * (n + 1) * n
+    ref, q = random_state5(rng, ne, npe), random_state5(rng, ne, npe)
+    x = rng.standard_normal(op.dim)
+    op.linearize(to_dev(ref))
+    assert rel(to_host(op.apply_linear(to_dev(x))), orc.apply_linear(ref, x)) < 1e-13
+    assert rel(to_host(op.apply_nonlinear(to_dev(q))), orc.apply_nonlinear(ref, q)) < 1e-13
+    assert rel(to_host(op.full_rhs(to_dev(q))), orc.full_rhs(q)) < 1e-12
+
+
+def test_euler3d_z_invariant_reduces_to_2d(ctx):
+    order, nx, ny, nz = 3, 4, 3, 2
+    rng = np.random.default_rng(5)
+    s2 = pkg.OperatorSpec("euler2d", order, nx, ny, box=(0, 10, 0, 6, 0, 1), euler_flux="lf")
+    s3 = pkg.OperatorSpec("euler3d", order, nx, ny, nz, box=(0, 10, 0, 6, 0, 2), euler_flux="lf")
+    op2, op3 = pkg.Operator(ctx, s2), pkg.Operator(ctx, s3)
+    np1 = order + 1
+    n2 = np1 * np1
+
+    def state2(rng):
+        q = np.empty(nx * ny * 4 * n2)
+        for e in range(nx * ny):
+            rho, u, v, p = (rng.uniform(0.5, 2, n2), rng.uniform(-1, 1, n2), rng.uniform(-1, 1, n2),
+                            rng.uniform(0.5, 2, n2))
+            blk = q[e * 4 * n2:(e + 1) * 4 * n2].reshape(4, n2)
+            blk[0], blk[1], blk[2], blk[3] = rho, rho * u, rho * v, p / 0.4 + 0.5 * rho * (u * u + v * v)
+        return q
+
+    def extrude(q2, zero_w=True):
+        out = np.zeros(op3.dim)
+        b3 = out.reshape(nz, ny, nx, 5, np1, np1, np1)  # [kz][jy][ix][c][k][j][i]
+        b2 = q2.reshape(ny, nx, 4, np1, np1)
+        for c2, c3 in ((0, 0), (1, 1), (2, 2), (3, 4)):
+            b3[:, :, :, c3] = b2[None, :, :, c2, None, :, :]
+        return out
+
+    def project(y3):  # 3D result restricted to the 2D components of the kz=0, k=0 plane
+        b3 = y3.reshape(nz, ny, nx, 5, np1, np1, np1)
+        out = np.empty((ny, nx, 4, np1, np1))
+        for c2, c3 in ((0, 0), (1, 1), (2, 2), (3, 4)):
+            out[:, :, c2] = b3[0, :, :, c3, 0]
+        return out.reshape(-1), b3[:, :, :, 3]
+
+    ref, x, q = state2(rng), rng.standard_normal(op2.dim), state2(rng)
+    op2.linearize(to_dev(ref))
+    op3.linearize(to_dev(extrude(ref)))
+    for name in ("apply_linear", "apply_nonlinear", "full_rhs"):
+        arg2 = x if name == "apply_linear" else q
+        y2 = to_host(getattr(op2, name)(to_dev(arg2)))
+        y3 = to_host(getattr(op3, name)(to_dev(extrude(arg2))))
+        proj, wmom = project(y3)
+        scale = np.abs(y2).max()
+        assert np.abs(proj - y2).max() <= 1e-12 * scale, name
+        assert np.abs(wmom).max() <= 1e-12 * scale, name
+
+
+def test_c5_reduced_mesh_epi2_parity(ctx):
+    w = configs.scaled(configs.C5, 4, steps=2)
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    orc = oracle_problem(w.spec()).integrate("epi2", u0, dt, w.steps * dt, tol=w.tol, max_basis=w.max_basis,
+                                             orth_length=w.max_basis)
+    op = pkg.Operator(ctx, w.spec())
+    r = pkg.integrate(ctx, op, to_dev(u0), "epi2", dt, w.steps * dt, tol=w.tol, max_basis=w.max_basis,
+                      orth_length=w.max_basis)
+    assert r.status == orc.status == "completed"
+    assert rel(to_host(r.u), orc.u) <= 1e-9
+    d_dev = np.diff(np.concatenate([[0], r.iters_per_step]))
+    d_orc = np.diff(np.concatenate([[0], orc.iters_per_step]))
+    assert np.max(np.abs(d_dev - d_orc)) <= 1
+
+
+def _vortex(x, y, t, lam=0.05, alpha=2.0, uinf=0.2, xc=5.0, yc=0.0, gamma=1.4):
+    # proj/src/euler.cpp:160-184 with the reference default VortexParams
+    cp = gamma / (gamma - 1.0)
+    xt = x - xc - uinf * t
+    yt = y - yc
+    xt = xt - 10.0 * np.round(xt / 10.0)
+    yt = yt - 10.0 * np.round(yt / 10.0)
+    r2 = xt * xt + yt * yt
+    s = lam / (2 * math.pi)
+    e1 = np.exp(0.5 * alpha * (1 - r2))
+    u = uinf - s * yt * e1
+    v = s * xt * e1
+    T = 1.0 - s * s / (2 * alpha * cp) * np.exp(alpha * (1 - r2))
+    rho = T ** (1 / (gamma - 1))
+    p = T ** (gamma / (gamma - 1))
+    return rho, u, v, p
+
+
+def test_c5_extruded_vortex_converges_at_design_order(ctx):
+    # 3D operator on a z-extruded exact isentropic vortex: L2 error at t = 0.5 decays at
+    # (about) the design order k+1 under h-refinement (k = 3, dt small).
+    order = 3
+    np1 = order + 1
+    x_lgl, w_lgl, _ = pkg.lgl_basis(order)
+    errs = []
+    hs = []
+    for n in (4, 8):
+        nz = 1
+        spec = pkg.OperatorSpec("euler3d", order, n, n, nz, box=(0, 10, -5, 5, 0, 1), euler_flux="lf")
+        op = pkg.Operator(ctx, spec)
+        h = 10.0 / n
+        xe = (np.arange(n)[:, None] + 0.5 * (x_lgl[None, :] + 1)) * h        # [ie][i]
+        ye = -5 + (np.arange(n)[:, None] + 0.5 * (x_lgl[None, :] + 1)) * h   # [je][j]
+        X = xe[None, :, None, :]  # [je][ie][j][i]
+        Y = ye[:, None, :, None]
+
+        def state(t):
+            rho, u, v, p = _vortex(np.broadcast_to(X, (n, n, np1, np1)), np.broadcast_to(Y, (n, n, np1, np1)), t)
+            q = np.zeros((nz, n, n, 5, np1, np1, np1))
+            comps = [rho, rho * u, rho * v, 0 * rho, p / 0.4 + 0.5 * rho * (u * u + v * v)]
+            for c in range(5):
+                q[:, :, :, c] = comps[c].transpose(0, 1, 2, 3)[None, :, :, None, :, :]
+            return q.reshape(-1)
+
+        t_end, dt = 0.5, 0.05
+        r = pkg.integrate(ctx, op, to_dev(state(0.0)), "epi2", dt, t_end, tol=1e-12, max_basis=40, orth_length=40)
+        assert r.status == "completed"
+        d = (to_host(r.u) - state(t_end)).reshape(nz, n, n, 5, np1, np1, np1)[:, :, :, 0]
+        wq = (w_lgl[:, None, None] * w_lgl[None, :, None] * w_lgl[None, None, :]) * (h * h * 1.0) / 8.0
+        errs.append(math.sqrt(float(np.sum(d * d * wq[None, None, None]))))
+        hs.append(h)
+    order_obs = math.log(errs[0] / errs[1]) / math.log(hs[0] / hs[1])
+    assert order_obs >= order + 0.5, (errs, order_obs)
