@@ -1,0 +1,214 @@
+// expdg_b200.hpp — header-only C++ mirror of the reference `expdg` hot-path API
+// (/root/reference/proj/include/expdg/{split_operator,phi,integrators}.hpp) on
+// top of the C ABI in expdg_b200.h.  Same names, argument meaning and
+// exception types as the reference; vectors are std::vector<double> on the
+// host (the reference uses Eigen::VectorXd, absent in this image) or raw device
+// pointers.
+//
+//   reference                                         here
+//   ------------------------------------------------  -----------------------------------------
+//   burgers_split_operator(mesh, basis, cfg, u~)      SplitOperator(ctx, desc).linearize(u~)
+//   euler_split_operator(...)   (proj/src/euler.cpp:390-401)
+//   SplitOperator::linear / nonlinear                 SplitOperator::linear / nonlinear
+//   phi_combination(PhiCombinationProblem)            phi_combination(ctx, op, b, dt, settings)
+//   step_epi2(op, u, dt, ks, stats)                   step_epi2(ctx, op, u, dt, ks, stats)
+//   integrate(problem, kind, u0, TimeLoopConfig)      integrate(ctx, op, kind, u0, TimeLoopConfig)
+//   KrylovError{last_estimate}                        KrylovError{last_estimate}
+//   std::invalid_argument / std::domain_error         same types
+#pragma once
+
+#include <cstddef>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "expdg_b200.h"
+
+namespace expdg {
+namespace b200 {
+
+// proj/include/expdg/phi.hpp:61-66
+class KrylovError : public std::runtime_error {
+ public:
+  KrylovError(const std::string& what, double estimate) : std::runtime_error(what), last_estimate(estimate) {}
+  double last_estimate;
+};
+
+class DeviceError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc, double estimate = 0.0) {
+  if (rc == EXPDG_OK) return;
+  const std::string msg = expdg_last_error();
+  switch (rc) {
+    case EXPDG_E_INVALID: throw std::invalid_argument(msg);
+    case EXPDG_E_DOMAIN: throw std::domain_error(msg);
+    case EXPDG_E_KRYLOV: throw KrylovError(msg, estimate);
+    case EXPDG_E_UNSUPPORTED: throw std::invalid_argument("unsupported on the device path: " + msg);
+    default: throw DeviceError(msg);
+  }
+}
+
+// proj/include/expdg/phi.hpp:25-28
+struct KrylovStats {
+  long iterations = 0;
+  int substeps = 0;
+};
+
+// proj/include/expdg/integrators.hpp:20-24
+struct KrylovSettings {
+  double tol = 1e-12;
+  int max_basis = 128;
+  int orth_length = 128;
+};
+
+enum class IntegratorKind { exp_euler, epi2 };
+enum class RunStatus { completed, blew_up };
+
+// proj/include/expdg/integrators.hpp:58-63 (on_step is called after the run, in
+// step order, with the same payload: step, t, max|u|, cumulative iterations)
+struct TimeLoopConfig {
+  double dt = 0.1;
+  double t_final = 1.0;
+  KrylovSettings krylov;
+  bool device_control = true;  // CUDA-graph WHILE-node controller (no host round-trip)
+  void (*on_step)(int, double, double, long, void*) = nullptr;
+  void* on_step_user = nullptr;
+};
+
+// proj/include/expdg/integrators.hpp:66-74
+struct IntegrationResult {
+  std::vector<double> u;
+  double t = 0.0;
+  RunStatus status = RunStatus::completed;
+  int steps = 0;
+  long krylov_iterations = 0;
+  int blow_up_step = -1;
+  double max_abs = 0.0;
+};
+
+class Context {
+ public:
+  explicit Context(int device = 0) { check(expdg_ctx_create(device, &h_)); }
+  ~Context() { expdg_ctx_destroy(h_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+  expdg_ctx* get() const { return h_; }
+  void synchronize() { check(expdg_ctx_synchronize(h_)); }
+
+ private:
+  expdg_ctx* h_ = nullptr;
+};
+
+// The split operator (proj/include/expdg/split_operator.hpp:12-20), frozen at
+// the state passed to linearize (device pointer).  linear/nonlinear act on
+// device pointers; the host-vector overloads copy in and out.
+class SplitOperator {
+ public:
+  SplitOperator(Context& ctx, const expdg_op_desc& desc) : ctx_(&ctx) { check(expdg_op_create(ctx.get(), &desc, &h_)); }
+  SplitOperator(Context& ctx, int n, const double* dense_rowmajor) : ctx_(&ctx) {
+    check(expdg_dense_op_create(ctx.get(), n, dense_rowmajor, &h_));
+  }
+  ~SplitOperator() { expdg_op_destroy(h_); }
+  SplitOperator(const SplitOperator&) = delete;
+  SplitOperator& operator=(const SplitOperator&) = delete;
+
+  long long dim() const { return expdg_op_dim(h_); }
+  expdg_op* get() const { return h_; }
+  Context& context() const { return *ctx_; }
+  SplitOperator& linearize(const double* ref_dev) {
+    check(expdg_op_linearize(h_, ref_dev));
+    return *this;
+  }
+  void linear(const double* x_dev, double* y_dev, void* stream = nullptr) const {
+    check(expdg_op_apply_linear(h_, x_dev, y_dev, stream));
+  }
+  void nonlinear(const double* x_dev, double* y_dev, void* stream = nullptr) const {
+    check(expdg_op_apply_nonlinear(h_, x_dev, y_dev, stream));
+  }
+  void full_rhs(const double* x_dev, double* y_dev, void* stream = nullptr) const {
+    check(expdg_op_full_rhs(h_, x_dev, y_dev, stream));
+  }
+
+ private:
+  Context* ctx_;
+  expdg_op* h_ = nullptr;
+};
+
+// proj/src/phi.cpp:133-260: out = sum_i dt^i phi_i(dt L) b_i (device pointers, b[i] may be null)
+inline KrylovStats phi_combination(Context& ctx, SplitOperator& op, const std::vector<const double*>& b_dev,
+                                   double dt, const KrylovSettings& ks, double* out_dev, int initial_basis = 16,
+                                   int max_substeps = 40) {
+  if (b_dev.empty()) throw std::invalid_argument("phi_combination: empty b list");
+  expdg_krylov_cfg c{ks.tol, ks.max_basis, ks.orth_length, initial_basis, max_substeps};
+  expdg_krylov_stats s{};
+  const int rc = expdg_phi_combination(ctx.get(), op.get(), b_dev.data(), (int)b_dev.size() - 1, dt, &c, out_dev, &s);
+  check(rc, s.last_estimate);
+  return KrylovStats{(long)s.iterations, s.substeps};
+}
+
+// proj/src/integrators.cpp:76-83 (u updated in place on the device)
+inline void step_epi2(Context& ctx, SplitOperator& op, double* u_dev, double dt, const KrylovSettings& ks,
+                      KrylovStats* stats = nullptr) {
+  expdg_krylov_cfg c{ks.tol, ks.max_basis, ks.orth_length, 0, 0};
+  expdg_krylov_stats s{};
+  const int rc = expdg_step_epi2(ctx.get(), op.get(), u_dev, dt, &c, &s);
+  check(rc, s.last_estimate);
+  if (stats) {
+    stats->iterations += (long)s.iterations;
+    stats->substeps += s.substeps;
+  }
+}
+
+// proj/src/integrators.cpp:140-201 from a HOST initial state (copied in/out).
+inline IntegrationResult integrate(Context& ctx, SplitOperator& op, IntegratorKind kind, std::vector<double> u0,
+                                   const TimeLoopConfig& cfg) {
+  expdg_time_cfg t{};
+  t.integrator = kind == IntegratorKind::epi2 ? EXPDG_EPI2 : EXPDG_EXP_EULER;
+  t.dt = cfg.dt;
+  t.t_final = cfg.t_final;
+  t.krylov = expdg_krylov_cfg{cfg.krylov.tol, cfg.krylov.max_basis, cfg.krylov.orth_length, 0, 0};
+  t.use_graph = cfg.device_control ? 1 : 0;
+  const int cap = (int)(cfg.t_final / cfg.dt + 2.5);
+  std::vector<long long> iters(cap > 0 ? cap : 1);
+  std::vector<double> amax(cap > 0 ? cap : 1);
+  expdg_integration_result r{};
+  check(expdg_integrate_host(ctx.get(), op.get(), u0.data(), &t, &r, iters.data(), amax.data(), cap));
+  IntegrationResult out;
+  out.u = std::move(u0);
+  out.t = r.t;
+  out.status = r.status == 0 ? RunStatus::completed : RunStatus::blew_up;
+  out.steps = r.steps;
+  out.krylov_iterations = (long)r.krylov_iterations;
+  out.blow_up_step = r.blow_up_step;
+  out.max_abs = r.max_abs;
+  if (cfg.on_step) {
+    const int ok = out.status == RunStatus::completed ? out.steps : out.steps - 1;
+    double tt = 0.0;
+    for (int s = 0; s < ok && s < cap; ++s) {
+      tt += cfg.dt < cfg.t_final - tt ? cfg.dt : cfg.t_final - tt;  // proj/src/integrators.cpp:157
+      cfg.on_step(s + 1, tt, amax[s], (long)iters[s], cfg.on_step_user);
+    }
+  }
+  return out;
+}
+
+// proj/src/basis.cpp:35-85
+struct NodalBasis {
+  int order = 0;
+  std::vector<double> nodes, weights, diff_matrix;  // diff row-major
+};
+inline NodalBasis lgl_basis(int order) {
+  NodalBasis b;
+  b.order = order;
+  b.nodes.resize(order + 1);
+  b.weights.resize(order + 1);
+  b.diff_matrix.resize((size_t)(order + 1) * (order + 1));
+  check(expdg_lgl_basis(order, b.nodes.data(), b.weights.data(), b.diff_matrix.data()));
+  return b;
+}
+
+}  // namespace b200
+}  // namespace expdg
