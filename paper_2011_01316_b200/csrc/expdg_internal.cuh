@@ -229,6 +229,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       : "memory");
 }
 
+// named barrier over the 256 consumer threads of a warp-specialised CTA
+__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __host__ __device__ inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
 
 }  // namespace expdg

@@ -43,10 +43,6 @@ constexpr int kTsBlock = kTsConsumers + 32;
 constexpr int kTsMaxT = 2048;
 constexpr int kTsChunk = 512;
 
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 template <int MODE>
 __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, double* partials, int budget,

@@ -10,6 +10,7 @@
 // staged in shared memory; face neighbours come from the tile when present,
 // else from L2.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "krylov.cuh"
@@ -381,6 +382,237 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
   grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
 }
 
+// ---------------------------------------------------------------- 2.5D strip JVP (phi cycle)
+// A CTA owns a strip of W element columns and marches up a chunk of element
+// rows.  Warp 8 streams whole element rows (x = slot j and the frozen
+// primitives, each with its E/W halo element) by 1D TMA bulk copies into a
+// 4-row smem ring (full/empty mbarriers); warps 0-7 compute row r from the
+// ring rows r-1, r, r+1, so every byte of x and q~ comes from HBM once per JVP.
+template <int NP>
+struct E2Strip {
+  static constexpr int NN = NP * NP;
+  static constexpr int W = 256 / NN;          // elements per strip
+  static constexpr int BLK = 4 * NN;          // doubles per element
+  static constexpr int ROWD = (W + 2) * BLK;  // doubles per array per row (with halo)
+  static constexpr int BUFD = 2 * ROWD + W * BLK;  // x + frozen (with halo) + b_1
+  static constexpr int NBUF = 4;
+  static constexpr int ROWS_PER_UNIT = 64;
+  static constexpr int SMEM = (NBUF * BUFD + 2 * W * BLK) * 8;  // ring + sf
+};
+
+template <int NP>
+__global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st, double* base, double* partials,
+                                                         BArgs b) {
+  using S = E2Strip<NP>;
+  constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
+  extern __shared__ __align__(128) double smem[];
+  double* ring = smem;
+  double* sf = smem + NBUF * S::BUFD;
+  __shared__ uint64_t full[NBUF], empty[NBUF];
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[9];
+  __shared__ double s_red[1];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    const int a = st->action;
+    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    if (s_go) {
+      s_j = st->j;
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[P.n + i] * s_xs : 0.0;
+      for (int q = 0; q < NBUF; ++q) {
+        mbar_init(&full[q], 1);
+        mbar_init(&empty[q], 1);
+      }
+      fence_mbar_init();
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  const int nx = P.nx, ny = P.ny;
+  const int nstrips = (nx + W - 1) / W;
+  const int nchunks = (ny + S::ROWS_PER_UNIT - 1) / S::ROWS_PER_UNIT;
+  const int nunits = nstrips * nchunks;
+  // p == 1 (EPI2, exp_euler): the single aug vector b_1 rides in the TMA ring too
+  const double* b1 = (b.p == 1) ? b.b[1] : nullptr;
+  double nacc = 0.0;
+
+  if (wid == 8) {
+    // ---------------- producer
+    if (lane == 0) {
+      long long seq = 0;
+      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int strip = u % nstrips, chunk = u / nstrips;
+        const int ie0 = strip * W, w = min(W, nx - ie0);
+        const int r0 = chunk * S::ROWS_PER_UNIT, r1 = min(ny, r0 + S::ROWS_PER_UNIT);
+        for (int q = 0; q < r1 - r0 + 2; ++q) {
+          int row = r0 - 1 + q;
+          row = row < 0 ? row + ny : (row >= ny ? row - ny : row);
+          const int sl = (int)(seq % NBUF);
+          const int use = (int)(seq / NBUF);
+          mbar_wait(&empty[sl], (use & 1) ^ 1);
+          double* dst = ring + (size_t)sl * S::BUFD;
+          const uint32_t eb = BLK * 8;
+          const bool with_b = b1 && q >= 1 && q <= r1 - r0;  // only the computed rows need b_1
+          mbar_arrive_expect_tx(&full[sl], 2u * (uint32_t)(w + 2) * eb + (with_b ? (uint32_t)w * eb : 0u));
+          const size_t rbase = (size_t)row * nx;
+          const int left = ie0 == 0 ? nx - 1 : ie0 - 1;
+          const int right = ie0 + w == nx ? 0 : ie0 + w;
+          for (int arr = 0; arr < 2; ++arr) {
+            const double* src = arr == 0 ? x : P.ut;
+            double* d = dst + arr * S::ROWD;
+            if (ie0 >= 1 && ie0 + w < nx) {
+              bulk_g2s(d, src + (rbase + left) * BLK, (uint32_t)(w + 2) * eb, &full[sl]);
+            } else {
+              bulk_g2s(d, src + (rbase + left) * BLK, eb, &full[sl]);
+              bulk_g2s(d + BLK, src + (rbase + ie0) * BLK, (uint32_t)w * eb, &full[sl]);
+              bulk_g2s(d + (size_t)(w + 1) * BLK, src + (rbase + right) * BLK, eb, &full[sl]);
+            }
+          }
+          if (with_b) bulk_g2s(dst + 2 * S::ROWD, b1 + (rbase + ie0) * BLK, (uint32_t)w * eb, &full[sl]);
+          ++seq;
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers: one thread per node of the strip row
+    const int le = tid / NN, node = tid % NN;
+    const int i = node % NP, j = node / NP;
+    long long seq = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int strip = u % nstrips, chunk = u / nstrips;
+      const int ie0 = strip * W, w = min(W, nx - ie0);
+      const int r0 = chunk * S::ROWS_PER_UNIT, r1 = min(ny, r0 + S::ROWS_PER_UNIT);
+      const bool active = le < w;
+      const int ie = ie0 + le;
+      const double hx = active ? __ldg(P.hx + ie) : 1.0;
+      auto slot = [&](long long q) { return ring + (size_t)((seq + q) % NBUF) * S::BUFD; };
+      auto wait_row = [&](long long q) { mbar_wait(&full[(seq + q) % NBUF], (int)(((seq + q) / NBUF) & 1)); };
+      wait_row(0);
+      wait_row(1);
+      for (int r = r0; r < r1; ++r) {
+        const long long q = r - r0 + 1;  // ring index of row r
+        wait_row(q + 1);
+        const double* cur = slot(q);
+        const double* lo = slot(q - 1);
+        const double* hi = slot(q + 1);
+        const double hy = __ldg(P.hy + r);
+        double qv[4], tv[4];
+        if (active) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            qv[c] = cur[(le + 1) * BLK + c * NN + node] * xs;
+            tv[c] = cur[S::ROWD + (le + 1) * BLK + c * NN + node];
+          }
+          const Prim tp = prim_frozen(tv);
+          double fx[4], fy[4];
+          jac_apply(tp, 0, P.gamma, qv, fx);
+          jac_apply(tp, 1, P.gamma, qv, fy);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            sf[((le * 2 + 0) * 4 + c) * NN + node] = fx[c];
+            sf[((le * 2 + 1) * 4 + c) * NN + node] = fy[c];
+          }
+        }
+        consumer_sync();
+        if (active) {
+          const double sy = 0.5 * hy * P.w[j];
+          const double sxs = 0.5 * hx * P.w[i];
+          double rr[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double* fxr = sf + ((le * 2 + 0) * 4 + c) * NN + j * NP;
+            const double* fyc = sf + ((le * 2 + 1) * 4 + c) * NN + i;
+            double ax = 0.0, ay = 0.0;
+#pragma unroll
+            for (int k = 0; k < NP; ++k) {
+              ax = fma(P.WD[k * NP + i], fxr[k], ax);
+              ay = fma(P.WD[k * NP + j], fyc[k * NP], ay);
+            }
+            rr[c] = sy * ax;
+            rr[c] += sxs * ay;
+          }
+          bool bad = false;
+          if (i == N || i == 0) {
+            const bool owner = i == N;
+            const int pos = owner ? le + 2 : le;  // E / W neighbour in the row buffer
+            const int node2 = j * NP + (owner ? 0 : N);
+            double q2[4], u2[4], f[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              q2[c] = cur[pos * BLK + c * NN + node2] * xs;
+              u2[c] = cur[S::ROWD + pos * BLK + c * NN + node2];
+            }
+            if (owner) face_flux(0, 0, P.gamma, qv, q2, tv, u2, f, bad);
+            else face_flux(0, 0, P.gamma, q2, qv, u2, tv, f, bad);
+            const double fw = 0.5 * hy * P.w[j];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) rr[c] = owner ? rr[c] - fw * f[c] : rr[c] + fw * f[c];
+          }
+          if (j == N || j == 0) {
+            const bool owner = j == N;
+            const double* nb = owner ? hi : lo;
+            const int node2 = (owner ? 0 : N) * NP + i;
+            double q2[4], u2[4], f[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              q2[c] = nb[(le + 1) * BLK + c * NN + node2] * xs;
+              u2[c] = nb[S::ROWD + (le + 1) * BLK + c * NN + node2];
+            }
+            if (owner) face_flux(0, 1, P.gamma, qv, q2, tv, u2, f, bad);
+            else face_flux(0, 1, P.gamma, q2, qv, u2, tv, f, bad);
+            const double fw = 0.5 * hx * P.w[i];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) rr[c] = owner ? rr[c] - fw * f[c] : rr[c] + fw * f[c];
+          }
+          const double scale = 4.0 / (hx * hy);
+          const double im = scale / (P.w[i] * P.w[j]);
+          const size_t e = (size_t)r * nx + ie;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const size_t g = (e * 4 + c) * NN + node;
+            double v = rr[c] * im;
+            if (b1) {
+              v = fma(s_xt[0], cur[2 * S::ROWD + le * BLK + c * NN + node], v);
+            } else {
+              for (int k = 0; k < b.p; ++k)
+                if (b.b[b.p - k]) v = fma(s_xt[k], b.b[b.p - k][g], v);
+            }
+            v = dt * v;
+            y[g] = v;
+            nacc = fma(v, v, nacc);
+          }
+        }
+        consumer_sync();  // rows r-1 .. r fully consumed, sf free
+        if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);
+      }
+      if (tid == 0) {
+        mbar_arrive(&empty[(seq + (r1 - r0)) % NBUF]);      // row r1 - 1
+        mbar_arrive(&empty[(seq + (r1 - r0) + 1) % NBUF]);  // row r1 (upper halo)
+      }
+      seq += r1 - r0 + 2;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid < kTailPad && st->tail_here) {
+    const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
+    y[P.n + tid] = v;
+    nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (tid == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+}
+
 // (u, v, H, a) of q~ per node (proj/src/euler.cpp:15-24): the frozen data of
 // the linearised operator, 32 B/node like q~ itself.
 __global__ void k_e2_freeze(const double* __restrict__ q, long long nelem, int nn, double gamma,
@@ -407,6 +639,7 @@ class Euler2D : public OpDevice {
   int grid = 1;
   double* frozen = nullptr;
   double* hbuf = nullptr;
+  bool use_strip = true;
   ~Euler2D() override {
     cudaFree(frozen);
     cudaFree(hbuf);
@@ -436,13 +669,23 @@ class Euler2D : public OpDevice {
     P.n = n;
     comps = 4;
     EXPDG_CUDA(cudaMalloc(&frozen, sizeof(double) * n));
+    use_strip = !(std::getenv("EXPDG_E2_TILE") && std::getenv("EXPDG_E2_TILE")[0] == '1');
+    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    E2Strip<NP>::SMEM));
     const long long ntiles = ((long long)d.nx * d.ny + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
   }
   void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
     E2P<NP> p = P;
     p.ut = frozen;
-    k_e2_phi<NP><<<grid, 256, 0, s>>>(p, st, base, partials, b);
+    if (use_strip) {
+      using SS = E2Strip<NP>;
+      const int units = ((P.nx + SS::W - 1) / SS::W) * ((P.ny + SS::ROWS_PER_UNIT - 1) / SS::ROWS_PER_UNIT);
+      const int g = std::max(1, std::min(units, 2 * 148));
+      k_e2_phi_strip<NP><<<g, 288, SS::SMEM, s>>>(p, st, base, partials, b);
+    } else {
+      k_e2_phi<NP><<<grid, 256, 0, s>>>(p, st, base, partials, b);
+    }
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
     E2P<NP> p = P;
