@@ -46,6 +46,8 @@ extern "C" {
 /* Integrator kinds: IntegratorKind (proj/include/expdg/integrators.hpp:15). */
 #define EXPDG_EXP_EULER 0
 #define EXPDG_EPI2 1
+#define EXPDG_EXPRB32 2 /* step_exprb32 (proj/src/integrators.cpp:85-98): two phi calls (p = 1, p = 3) */
+#define EXPDG_EXPRB42 3 /* step_exprb42 (proj/src/integrators.cpp:100-113) */
 
 typedef struct expdg_ctx expdg_ctx;
 typedef struct expdg_op expdg_op;
@@ -88,7 +90,7 @@ typedef struct {
 
 /* TimeLoopConfig (proj/include/expdg/integrators.hpp:58-63). */
 typedef struct {
-  int integrator; /* EXPDG_EPI2 or EXPDG_EXP_EULER */
+  int integrator; /* EXPDG_EXP_EULER, EXPDG_EPI2, EXPDG_EXPRB32, EXPDG_EXPRB42 */
   double dt;
   double t_final;
   expdg_krylov_cfg krylov;
@@ -145,8 +147,8 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
 int expdg_step_epi2(expdg_ctx* ctx, expdg_op* op, double* u_dev, double dt, const expdg_krylov_cfg* cfg,
                     expdg_krylov_stats* stats);
 
-/* integrate (proj/src/integrators.cpp:140-201) for EPI2 (relinearised each step) and
- * exp_euler (frozen at u0).  u_dev updated in place.  Optional per-step outputs
+/* integrate (proj/src/integrators.cpp:140-201) for EPI2 / EXPRB32 / EXPRB42 (relinearised
+ * each step) and exp_euler (frozen at u0).  u_dev updated in place.  Optional per-step outputs
  * (capacity `cap`): cumulative Krylov iterations and max|u| (the on_step payload,
  * proj/include/expdg/integrators.hpp:62).  Blow-up is reported, not returned as an error. */
 int expdg_integrate(expdg_ctx* ctx, expdg_op* op, double* u_dev, const expdg_time_cfg* cfg,

@@ -64,7 +64,7 @@ struct KrylovSettings {
   int orth_length = 128;
 };
 
-enum class IntegratorKind { exp_euler, epi2 };
+enum class IntegratorKind { exp_euler, epi2, exprb32, exprb42 };
 enum class RunStatus { completed, blew_up };
 
 // proj/include/expdg/integrators.hpp:58-63 (on_step is called after the run, in
@@ -166,7 +166,10 @@ inline void step_epi2(Context& ctx, SplitOperator& op, double* u_dev, double dt,
 inline IntegrationResult integrate(Context& ctx, SplitOperator& op, IntegratorKind kind, std::vector<double> u0,
                                    const TimeLoopConfig& cfg) {
   expdg_time_cfg t{};
-  t.integrator = kind == IntegratorKind::epi2 ? EXPDG_EPI2 : EXPDG_EXP_EULER;
+  t.integrator = kind == IntegratorKind::epi2      ? EXPDG_EPI2
+                 : kind == IntegratorKind::exprb32 ? EXPDG_EXPRB32
+                 : kind == IntegratorKind::exprb42 ? EXPDG_EXPRB42
+                                                   : EXPDG_EXP_EULER;
   t.dt = cfg.dt;
   t.t_final = cfg.t_final;
   t.krylov = expdg_krylov_cfg{cfg.krylov.tol, cfg.krylov.max_basis, cfg.krylov.orth_length, 0, 0};

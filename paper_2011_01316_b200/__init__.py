@@ -25,7 +25,7 @@ LIB_PATH = os.path.join(_PKG, "_build", "libexpdg_b200.so")
 
 EXPDG_OK, EXPDG_E_INVALID, EXPDG_E_DOMAIN, EXPDG_E_KRYLOV, EXPDG_E_CUDA, EXPDG_E_UNSUPPORTED = range(6)
 BURGERS1D, BURGERS2D, EULER2D, EULER3D, DENSE = 1, 2, 3, 4, 5
-INTEGRATORS = {"exp_euler": 0, "epi2": 1}
+INTEGRATORS = {"exp_euler": 0, "epi2": 1, "exprb32": 2, "exprb42": 3}
 
 
 class KrylovError(RuntimeError):

@@ -15,6 +15,11 @@ void launch_step_begin(cudaStream_t s, PhiState* st, const double* dt_seq);
 void launch_step_finish(cudaStream_t s, PhiState* st, double* u, const double* w, int mode, StepRecord* rec,
                         double* partials, int grid);
 void launch_absmax(cudaStream_t s, const double* u, long long n, double* out2, int grid);
+void launch_phi_config(cudaStream_t s, PhiState* st, const double* dt_seq, int p, double mult, int mmax,
+                       int full_orth, int window, int grow_cap);
+void launch_vec_add(cudaStream_t s, const PhiState* st, double* out, const double* u, const double* w, long long n);
+void launch_exprb_d2(cudaStream_t s, const PhiState* st, const double* dt_seq, double* d, const double* a,
+                     const double* b, double c, long long n);
 int op_check_ref(OpDevice& op, cudaStream_t s, const double* ref);  // 0 ok, 1 not finite, 2 inadmissible
 void device_expm(cudaStream_t s, double* work, int N, double* out);
 
@@ -311,13 +316,14 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   if (!ctx || !op || !u || !cfg || !res) throw std::invalid_argument("null argument");
   if (!(cfg->dt > 0.0)) throw std::invalid_argument("integrate: dt must be positive");
   if (cfg->t_final < cfg->dt) throw std::invalid_argument("integrate: t_final must be at least dt");
-  if (cfg->integrator != EXPDG_EPI2 && cfg->integrator != EXPDG_EXP_EULER)
-    throw Unsupported("integrate: device integrators are epi2 and exp_euler");
+  const int kind = cfg->integrator;
+  if (kind < EXPDG_EXP_EULER || kind > EXPDG_EXPRB42) throw Unsupported("integrate: device integrators are "
+                                                                        "exp_euler, epi2, exprb32, exprb42");
   if (cfg->krylov.max_basis > kMaxBasis) throw Unsupported("max_basis > 128");
   Engine& e = *ctx->eng;
   OpDevice& dev = *op->dev;
   const long long n = dev.n;
-  const int mode = cfg->integrator == EXPDG_EPI2 ? 0 : 1;
+  const bool exprb = kind == EXPDG_EXPRB32 || kind == EXPDG_EXPRB42;
   // dt sequence of proj/src/integrators.cpp:155-157
   std::vector<double> dts;
   {
@@ -330,12 +336,18 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     }
   }
   const int S = (int)dts.size();
-  const int p = 1;
-  PhiState c = e.config(n, p, cfg->dt, cfg->krylov);
-  e.ensure(n + p, c.mmax);
-  e.ensure_scratch(n, 2);
-  double* rbuf = e.scratch;              // EPI2: R ; exp_euler: N(u)
-  double* refbuf = e.scratch + e.scratch_ld;  // exp_euler: frozen u0
+  const int pmax = exprb ? 3 : 1;
+  e.ensure(n + pmax, std::max(e.config(n, 1, cfg->dt, cfg->krylov).mmax, e.config(n, pmax, cfg->dt, cfg->krylov).mmax));
+  const PhiState c1 = e.config(n, 1, cfg->dt, cfg->krylov);  // after ensure: carries the slot stride
+  e.ensure_scratch(n, 6);
+  double* sb[6];
+  for (int i = 0; i < 6; ++i) sb[i] = e.scratch + (size_t)i * e.scratch_ld;
+  double* rbuf = sb[0];    // R (EPI2 / EXPRB) or N(u) (exp_euler)
+  double* refbuf = sb[1];  // exp_euler: frozen u0
+  double* nu = sb[2];      // EXPRB: N(u)
+  double* stage = sb[3];   // EXPRB: u + w1
+  double* ns = sb[4];      // EXPRB: N(u + w1)
+  double* d2 = sb[5];      // EXPRB: c/dt^2 (N(u + w1) - N(u))
   // max|u0| -> blow-up scale (proj/src/integrators.cpp:148-149)
   const int rgrid = std::min(4096, std::max(1, (int)std::min<long long>(e.num_sms * 4, (n + 255) / 256)));
   launch_absmax(e.stream, u, n, ctx->work2, rgrid);
@@ -344,12 +356,12 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   EXPDG_CUDA(cudaStreamSynchronize(e.stream));
   double max0 = 0.0;
   for (int i = 0; i < rgrid; ++i) max0 = std::max(max0, h2[2 * i]);
-  if (mode == 1) {
+  if (kind == EXPDG_EXP_EULER) {
     const int chk = op_check_ref(dev, e.stream, u);
     if (chk == 2) throw std::domain_error("EulerOperator: inadmissible reference state");
     EXPDG_CUDA(cudaMemcpyAsync(refbuf, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, e.stream));
   }
-  c = e.config(n, p, cfg->dt, cfg->krylov);
+  PhiState c = c1;
   c.max_steps = S;
   c.blow_up_scale = 1e10 * (1.0 + max0);
   e.upload_config(c, e.stream);
@@ -359,25 +371,79 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   EXPDG_CUDA(cudaMalloc(&rec_dev, sizeof(StepRecord) * S));
   EXPDG_CUDA(cudaMemcpyAsync(dts_dev, dts.data(), sizeof(double) * S, cudaMemcpyHostToDevice, e.stream));
   const double* saved_ref = dev.ref;
-  if (mode == 0) dev.ref = u;  // EPI2: re-frozen at u^n by the residual kernel every step
-  else dev.freeze(e.stream, refbuf);
-  BArgs b{};
-  b.p = 1;
-  b.b[0] = mode == 0 ? nullptr : u;
-  b.b[1] = rbuf;
-  const int fgrid = std::min(2048, std::max(1, (int)std::min<long long>(e.num_sms * 4, (n + 255) / 256)));
+  if (kind == EXPDG_EXP_EULER) dev.freeze(e.stream, refbuf);
+  else dev.ref = u;  // re-frozen at u^n by the residual kernel every step
+
+  // ---- the step as segments: pre, {phi, mid}..., post
+  BArgs b1{}, b2{};
+  b1.p = 1;
+  b1.b[0] = kind == EXPDG_EXP_EULER ? u : nullptr;
+  b1.b[1] = rbuf;
+  b2.p = 3;
+  b2.b[1] = rbuf;
+  b2.b[3] = d2;
+  const PhiState c3 = e.config(n, 3, cfg->dt, cfg->krylov);
+  const double mult1 = kind == EXPDG_EXPRB42 ? 0.75 : 1.0;         // proj/src/integrators.cpp:106
+  const double dcoef = kind == EXPDG_EXPRB42 ? 32.0 / 9.0 : 2.0;  // :97 / :111
+  const int vgrid = 1184;
   auto pre = [&](cudaStream_t s) {
     launch_step_begin(s, e.st, dts_dev);
-    if (mode == 0) dev.launch_residual(s, u, rbuf, e.st, e.partials);
-    else dev.launch_apply(s, 1, u, rbuf);
-    e.launch_phi_init(s, b);
+    if (kind == EXPDG_EXP_EULER) {
+      dev.launch_apply(s, 1, u, rbuf);  // N(u) at the frozen u0 (proj/src/integrators.cpp:71)
+    } else {
+      dev.launch_residual(s, u, rbuf, e.st, e.partials);  // R = L u + N u at u~ = u
+      if (exprb) {
+        dev.launch_apply(s, 1, u, nu);
+        launch_phi_config(s, e.st, dts_dev, 1, mult1, c1.mmax, c1.full_orth, c1.window, c1.grow_cap);
+      }
+    }
+    e.launch_phi_init(s, b1);
   };
-  auto post = [&](cudaStream_t s) { launch_step_finish(s, e.st, u, e.slot(0), mode, rec_dev, e.partials, fgrid); };
-  const int per_step = 5;
+  auto mid = [&](cudaStream_t s) {
+    launch_vec_add(s, e.st, stage, u, e.slot(0), n);
+    dev.launch_apply(s, 1, stage, ns);
+    launch_exprb_d2(s, e.st, dts_dev, d2, ns, nu, dcoef, n);
+    launch_phi_config(s, e.st, dts_dev, 3, 1.0, c3.mmax, c3.full_orth, c3.window, c3.grow_cap);
+    e.launch_phi_init(s, b2);
+  };
+  const int fgrid = std::min(2048, std::max(1, (int)std::min<long long>(e.num_sms * 4, (n + 255) / 256)));
+  auto post = [&](cudaStream_t s) {
+    launch_step_finish(s, e.st, u, e.slot(0), kind == EXPDG_EXP_EULER ? 1 : 0, rec_dev, e.partials, fgrid);
+  };
+  (void)vgrid;
+  const int per_step = exprb ? 13 : 5;
   const int body_k = dev.fused_dots() ? 5 : 6;
   cudaGraphExec_t ex = nullptr;
   const bool graph = cfg->use_graph != 0;
   int launched = 0;
+
+  // Adds a WHILE node after the current capture position; returns its body graph.
+  auto add_while = [&](cudaStream_t cs, cudaGraph_t g, cudaGraphConditionalHandle* h) {
+    EXPDG_CUDA(cudaGraphConditionalHandleCreate(h, g, 1, cudaGraphCondAssignDefault));
+    cudaStreamCaptureStatus cst;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    cudaGraph_t cg;
+    EXPDG_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &ndeps));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = *h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    EXPDG_CUDA(cudaGraphAddNode(&cnode, g, deps, ndeps, &cp));
+    EXPDG_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
+    return cp.conditional.phGraph_out[0];
+  };
+  auto host_loop = [&](const BArgs& b) {
+    for (long long cyc = 0;; ++cyc) {
+      e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0);
+      EXPDG_CUDA(cudaMemcpyAsync(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost, e.stream));
+      EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+      if (e.st_host->action == ACT_DONE || e.st_host->action == ACT_NONE || e.st_host->stopped) break;
+      if (cyc > 10000000) throw CudaError("host-stepped phi did not terminate");
+    }
+  };
   try {
     if (graph) {
       cudaGraph_t g;
@@ -386,27 +452,22 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
       EXPDG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
       pre(cs);
-      cudaGraphConditionalHandle h;
-      EXPDG_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
-      cudaStreamCaptureStatus cst;
-      const cudaGraphNode_t* deps = nullptr;
-      size_t ndeps = 0;
-      cudaGraph_t cg;
-      EXPDG_CUDA(cudaStreamGetCaptureInfo(cs, &cst, nullptr, &cg, &deps, &ndeps));
-      cudaGraphNodeParams cp = {};
-      cp.type = cudaGraphNodeTypeConditional;
-      cp.conditional.handle = h;
-      cp.conditional.type = cudaGraphCondTypeWhile;
-      cp.conditional.size = 1;
-      cudaGraphNode_t cnode;
-      EXPDG_CUDA(cudaGraphAddNode(&cnode, g, deps, ndeps, &cp));
-      EXPDG_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
+      cudaGraphConditionalHandle h1, h2;
+      cudaGraph_t body1 = add_while(cs, g, &h1), body2 = nullptr;
+      if (exprb) {
+        mid(cs);
+        body2 = add_while(cs, g, &h2);
+      }
       post(cs);
       EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
-      cudaGraph_t body = cp.conditional.phGraph_out[0];
-      EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-      e.launch_body(cs, dev, b, h, 1);
-      EXPDG_CUDA(cudaStreamEndCapture(cs, &body));
+      EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body1, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      e.launch_body(cs, dev, b1, h1, 1);
+      EXPDG_CUDA(cudaStreamEndCapture(cs, &body1));
+      if (exprb) {
+        EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body2, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        e.launch_body(cs, dev, b2, h2, 1);
+        EXPDG_CUDA(cudaStreamEndCapture(cs, &body2));
+      }
       EXPDG_CUDA(cudaGraphInstantiate(&ex, g, 0));
       cudaGraphDestroy(g);
       cudaStreamDestroy(cs);
@@ -427,12 +488,10 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
           EXPDG_CUDA(cudaGraphLaunch(ex, e.stream));
         } else {
           pre(e.stream);
-          for (int cyc = 0;; ++cyc) {
-            e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0);
-            EXPDG_CUDA(cudaMemcpyAsync(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost, e.stream));
-            EXPDG_CUDA(cudaStreamSynchronize(e.stream));
-            if (e.st_host->action == ACT_DONE || e.st_host->action == ACT_NONE || e.st_host->stopped) break;
-            if (cyc > 10000000) throw CudaError("host-stepped phi did not terminate");
+          host_loop(b1);
+          if (exprb) {
+            mid(e.stream);
+            host_loop(b2);
           }
           post(e.stream);
         }

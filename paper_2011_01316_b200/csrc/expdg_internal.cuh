@@ -91,6 +91,7 @@ struct PhiState {
   int step;           // steps completed
   int max_steps;
   int domain_flag;    // set by operator kernels on inadmissible states
+  int step_failed;    // a phi call of this step failed (KrylovError / domain): skip the rest
   int any_b;          // some b_i nonzero
   long long iterations_total;
   long long body_runs;  // controller invocations (one per engine cycle)

@@ -628,6 +628,10 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
         }
       } else if (phase == PH_DONE) {
         if (st->status == PHI_RUNNING) st->status = PHI_OK;
+        // stats of a call that returned are kept (add_stats, proj/src/integrators.cpp:59-65);
+        // a KrylovError drops them and fails the step
+        if (st->status == PHI_OK) st->iterations_total += st->iterations;
+        else st->step_failed = 1;
         st->action = ACT_DONE;
         s_done = 1;
         s_exit = 1;
@@ -647,6 +651,10 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
 // decision sees the fully reduced norms).
 __global__ void k_phi_start(PhiState* st) {
   if (st->stopped) return;
+  if (st->step_failed) {  // an earlier phi call of this step failed: skip this one
+    st->action = ACT_DONE;
+    return;
+  }
   int any = 0;
   for (int i = 0; i <= st->p; ++i) any |= st->bnorm2[i] > 0.0;
   st->any_b = any;
@@ -663,6 +671,7 @@ __global__ void k_phi_start(PhiState* st) {
   for (int j = 0; j < kMaxP; ++j) st->tailw[j] = (j == st->p - 1) ? 1.0 : 0.0;
   if (st->domain_flag) {
     st->status = PHI_ERR_DOMAIN;
+    st->step_failed = 1;
     st->action = ACT_DONE;
   } else if (!any) {
     st->status = PHI_OK;
@@ -740,9 +749,10 @@ void Engine::ensure(long long len, int mmax) {
 
 void Engine::ensure_scratch(long long len, int count) {
   const long long need = round_up(len + kTailPad, kLdAlign);
-  if (scratch && scratch_ld >= need) return;
+  if (scratch && scratch_ld >= need && scratch_count >= count) return;
   if (scratch) EXPDG_CUDA(cudaFree(scratch));
   scratch_ld = need;
+  scratch_count = count;
   EXPDG_CUDA(cudaMalloc(&scratch, sizeof(double) * (size_t)need * count));
   EXPDG_CUDA(cudaMemset(scratch, 0, sizeof(double) * (size_t)need * count));
 }

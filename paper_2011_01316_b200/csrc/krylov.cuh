@@ -81,6 +81,7 @@ class Engine {
   size_t ework_doubles = 0;
   double* scratch = nullptr;   // 2 vectors of ld: R and a spare
   long long scratch_ld = 0;
+  int scratch_count = 0;
 
   void ensure(long long len, int mmax);
   void ensure_scratch(long long len, int count);

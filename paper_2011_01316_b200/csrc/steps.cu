@@ -9,6 +9,38 @@ __global__ void k_step_begin(PhiState* st, const double* dt_seq) {
   if (st->stopped) return;
   st->dt = dt_seq[st->step];
   st->domain_flag = 0;
+  st->step_failed = 0;
+}
+
+// Per-call configuration of the phi calls of an EXPRB step (p and the dt factor
+// differ between the two calls, proj/src/integrators.cpp:85-113).
+__global__ void k_phi_config(PhiState* st, const double* dt_seq, int p, double mult, int mmax, int full_orth,
+                             int window, int grow_cap) {
+  if (st->stopped) return;
+  st->p = p;
+  st->len = st->n + p;
+  st->dt = dt_seq[st->step] * mult;
+  st->mmax = mmax;
+  st->full_orth = full_orth;
+  st->window = window;
+  st->grow_cap = grow_cap;
+}
+
+// S = u + w (the EXPRB internal stage, proj/src/integrators.cpp:93 / :108)
+__global__ void k_vec_add(const PhiState* st, double* s, const double* u, const double* w, long long n) {
+  if (st->stopped || st->step_failed) return;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) s[i] = u[i] + w[i];
+}
+
+// d = (c / (dt*dt)) * (a - b) with dt the step's dt (2/dt^2 for EXPRB32, 32/9/dt^2 for EXPRB42)
+__global__ void k_exprb_d2(const PhiState* st, const double* dt_seq, double* d, const double* a, const double* b,
+                           double c, long long n) {
+  if (st->stopped || st->step_failed) return;
+  const double dt = dt_seq[st->step];
+  const double f = c / (dt * dt);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) d[i] = f * (a[i] - b[i]);
 }
 
 // mode 0 (EPI2): u <- u + w ; mode 1 (exp_euler): u <- w.  Then max|u|, finiteness,
@@ -19,7 +51,7 @@ __global__ void __launch_bounds__(256) k_step_finish(PhiState* st, double* u, co
   __shared__ double s_red[2];
   __shared__ int s_ok;
   if (st->stopped) return;
-  if (threadIdx.x == 0) s_ok = st->status == PHI_OK;
+  if (threadIdx.x == 0) s_ok = st->status == PHI_OK && !st->step_failed;
   __syncthreads();
   const bool ok = s_ok;
   const long long n = st->n;
@@ -55,9 +87,8 @@ __global__ void __launch_bounds__(256) k_step_finish(PhiState* st, double* u, co
     }
     st->ticket[7] = 0u;
     const int step = st->step;
-    const bool failed = st->status != PHI_OK;
+    const bool failed = st->step_failed || st->status != PHI_OK;
     const double am = bad > 0.0 ? INFINITY : mx;
-    if (!failed) st->iterations_total += st->iterations;  // KrylovError drops the call's stats
     st->alg_bytes += 40.0 * (double)st->n;
     StepRecord r;
     r.dt = st->dt;
@@ -98,6 +129,17 @@ void launch_step_begin(cudaStream_t s, PhiState* st, const double* dt_seq) { k_s
 void launch_step_finish(cudaStream_t s, PhiState* st, double* u, const double* w, int mode, StepRecord* rec,
                         double* partials, int grid) {
   k_step_finish<<<grid, 256, 0, s>>>(st, u, w, mode, rec, partials);
+}
+void launch_phi_config(cudaStream_t s, PhiState* st, const double* dt_seq, int p, double mult, int mmax,
+                       int full_orth, int window, int grow_cap) {
+  k_phi_config<<<1, 1, 0, s>>>(st, dt_seq, p, mult, mmax, full_orth, window, grow_cap);
+}
+void launch_vec_add(cudaStream_t s, const PhiState* st, double* out, const double* u, const double* w, long long n) {
+  k_vec_add<<<1184, 256, 0, s>>>(st, out, u, w, n);
+}
+void launch_exprb_d2(cudaStream_t s, const PhiState* st, const double* dt_seq, double* d, const double* a,
+                     const double* b, double c, long long n) {
+  k_exprb_d2<<<1184, 256, 0, s>>>(st, dt_seq, d, a, b, c, n);
 }
 void launch_absmax(cudaStream_t s, const double* u, long long n, double* out2, int grid) {
   k_absmax<<<grid, 256, 0, s>>>(u, n, out2);

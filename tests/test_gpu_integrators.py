@@ -84,3 +84,23 @@ def test_step_epi2_euler_matches_one_step_integrate(ctx):
     u, st = pkg.step_epi2(ctx, op, u, dt, tol=w.tol, max_basis=40, orth_length=40)
     assert rel(to_host(u), to_host(r.u)) < 1e-12
     assert st.iterations == r.krylov_iterations
+
+
+@pytest.mark.parametrize("integ", ["exprb32", "exprb42"])
+@pytest.mark.parametrize("kind", ["burgers1d", "euler2d"])
+def test_exprb_matches_oracle(ctx, kind, integ):
+    # proj/src/integrators.cpp:85-113: two phi calls per step (p = 1 then p = 3)
+    if kind == "burgers1d":
+        w = configs.scaled(configs.C1_S3E4, 64, steps=4)
+    else:
+        w = configs.scaled(configs.C4, 10, steps=2)
+    u0 = w.initial_condition()
+    dt = w.time_step(u0) if w.dt is None else w.dt
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    orc = oracle_problem(w.spec()).integrate(integ, u0, dt, w.steps * dt, **kw)
+    op = pkg.Operator(ctx, w.spec())
+    for use_graph in (True, False):
+        r = pkg.integrate(ctx, op, to_dev(u0), integ, dt, w.steps * dt, use_graph=use_graph, **kw)
+        assert r.status == orc.status == "completed"
+        assert rel(to_host(r.u), orc.u) <= 1e-9
+        assert np.max(np.abs(_dims(r) - _dims(orc))) <= 2  # two phi calls per step, +-1 each
