@@ -65,7 +65,7 @@ typedef struct {
   int flux;            /* Burgers: 0 lax_friedrichs, 1 entropy */
   double sigma;        /* entropy-flux jump penalty */
   int sigma_adaptive;
-  int over_integrate;  /* must be 0 on the device path (EXPDG_E_UNSUPPORTED) */
+  int over_integrate;  /* 1D Burgers: Gauss rule of (3k+3)/2 points + consistent mass (proj/src/burgers.cpp:39-51) */
   double gamma;        /* Euler */
   int euler_flux;      /* 0 roe (EXPDG_E_UNSUPPORTED on the device path), 1 lax_friedrichs */
 } expdg_op_desc;
@@ -129,6 +129,14 @@ long long expdg_op_dim(const expdg_op* op);
  * (proj/src/burgers.cpp:309-320, proj/src/euler.cpp:390-401).  EXPDG_E_DOMAIN on an
  * inadmissible Euler state (proj/src/euler.cpp:210-211). */
 int expdg_op_linearize(expdg_op* op, const double* ref_dev);
+/* Steady weak source of BurgersConfig::source (proj/src/burgers.cpp:80-92): the per-element
+ * load vector 0.5 h_e I^T (W s) in state layout (n doubles, device, copied), added to N and
+ * the full RHS.  1D Burgers only. */
+int expdg_op_set_source(expdg_op* op, const double* weak_source_dev);
+/* Same, from the source function itself (BurgersConfig::source, proj/include/expdg/burgers.hpp:22):
+ * the library evaluates source(x, user) at the operator's quadrature points and builds the
+ * weak load exactly as proj/src/burgers.cpp:80-92. */
+int expdg_op_set_source_fn(expdg_op* op, double (*source)(double x, void* user), void* user);
 /* SplitOperator::linear — the JVP (proj/src/burgers.cpp:146-180, proj/src/euler.cpp:299-341). */
 int expdg_op_apply_linear(expdg_op* op, const double* x_dev, double* y_dev, void* stream);
 /* SplitOperator::nonlinear (proj/src/burgers.cpp:182-215, proj/src/euler.cpp:343-388). */

@@ -20,6 +20,7 @@
 #include <cstddef>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "expdg_b200.h"
@@ -120,6 +121,17 @@ class SplitOperator {
   Context& context() const { return *ctx_; }
   SplitOperator& linearize(const double* ref_dev) {
     check(expdg_op_linearize(h_, ref_dev));
+    return *this;
+  }
+  // BurgersConfig::source (proj/include/expdg/burgers.hpp:22), as a weak load already on the
+  // device or as the function itself (evaluated on the operator's quadrature).
+  SplitOperator& set_source(const double* weak_source_dev) {
+    check(expdg_op_set_source(h_, weak_source_dev));
+    return *this;
+  }
+  SplitOperator& set_source(const std::function<double(double)>& s) {
+    auto tramp = [](double x, void* u) { return (*static_cast<const std::function<double(double)>*>(u))(x); };
+    check(expdg_op_set_source_fn(h_, tramp, const_cast<std::function<double(double)>*>(&s)));
     return *this;
   }
   void linear(const double* x_dev, double* y_dev, void* stream = nullptr) const {

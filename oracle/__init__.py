@@ -86,6 +86,16 @@ def lib():
         L.oracle_acc_ode_order.restype = C.c_double
         L.oracle_acc_ode_order.argtypes = [C.c_int]
         L.oracle_acc_exp_euler_joint.argtypes = [dp]
+        L.oracle_harness_burgers.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_double, C.c_int,
+                                             C.c_int, C.c_double, dp, dp, dp]
+        L.oracle_l2_error_exact.restype = C.c_double
+        L.oracle_mms_source.restype = C.c_double
+        L.oracle_mms_source.argtypes = [C.c_double, C.c_double]
+        L.oracle_l2_error_exact.argtypes = [C.c_char_p, C.c_int, C.c_int, dp, C.c_double]
+        L.oracle_rk4_reference.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_double,
+                                           C.c_double, dp]
+        L.oracle_l2_error_discrete.restype = C.c_double
+        L.oracle_l2_error_discrete.argtypes = [C.c_char_p, C.c_int, C.c_int, dp, C.c_int, C.c_int, dp]
         _lib = L
     return _lib
 
@@ -302,3 +312,38 @@ def burgers_diag(problem: Problem, ref, u):
     _check(lib().oracle_burgers_diag(problem.h, _p(ref), _p(u), _p(q),
                                      *[C.byref(v) for v in vals]))
     return q, tuple(v.value for v in vals)
+
+
+# ---------------------------------------------------------------- harness helpers (checker side)
+def harness_burgers(problem, ne, k, flux="", sigma=0.0, sigma_adaptive=False, over_integrate=-1, kappa=-1.0):
+    """u0, weak source and effective config of make_problem (proj/src/harness.cpp:48-142)."""
+    n = ne * (k + 1)
+    u0, src, cfg = np.empty(n), np.empty(n), np.empty(5)
+    rc = lib().oracle_harness_burgers(problem.encode(), ne, k, flux.encode(), sigma, int(sigma_adaptive),
+                                      over_integrate, kappa, _p(u0), _p(src), _p(cfg))
+    if rc:
+        raise ValueError("harness problem")
+    return u0, src, {"kappa": cfg[0], "flux": "ef" if cfg[1] else "lf", "sigma": cfg[2],
+                     "sigma_adaptive": bool(cfg[3]), "over_integrate": bool(cfg[4])}
+
+
+def mms_source(x, kappa):
+    """burgers-mms forcing (proj/src/harness.cpp:97-104)."""
+    return lib().oracle_mms_source(float(x), float(kappa))
+
+
+def l2_error_exact(problem, ne, k, u, t):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    return lib().oracle_l2_error_exact(problem.encode(), ne, k, _p(u), t)
+
+
+def rk4_reference(problem, ne, k, flux, over_integrate, dt, t_final):
+    out = np.empty(ne * (k + 1))
+    _check(lib().oracle_rk4_reference(problem.encode(), ne, k, flux.encode(), over_integrate, dt, t_final, _p(out)))
+    return out
+
+
+def l2_error_discrete(problem, ne, k, u, ref_ne, ref_k, uref):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    uref = np.ascontiguousarray(uref, dtype=np.float64)
+    return lib().oracle_l2_error_discrete(problem.encode(), ne, k, _p(u), ref_ne, ref_k, _p(uref))

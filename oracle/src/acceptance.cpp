@@ -1,6 +1,7 @@
 // ORACLE (test infrastructure): restatement of the reference acceptance
 // criteria that print digits (proj/tests/acceptance.cpp:110-527), used to pin
 // this oracle against proj/test_output.txt:18-28.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -230,3 +231,100 @@ int oracle_acc_exp_euler_joint(double* errors /*3*/) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- checker helpers for the
+// device replays of the acceptance criteria (tests/test_gpu_acceptance.py)
+extern "C" {
+
+// make_problem (proj/src/harness.cpp:48-142) for the Burgers problems: u0, the weak
+// source load vector (zeros when none) and the effective BurgersConfig.
+// out_cfg = {kappa, flux(0 lf/1 ef), sigma, sigma_adaptive, over_integrate}
+int oracle_harness_burgers(const char* problem, int ne, int k, const char* flux, double sigma, int sigma_adaptive,
+                           int over_integrate, double kappa, double* u0, double* src_weak, double* out_cfg) {
+  try {
+    ExperimentConfig cfg;
+    cfg.problem = problem;
+    cfg.flux = flux;
+    cfg.sigma = sigma;
+    cfg.sigma_adaptive = sigma_adaptive != 0;
+    cfg.over_integrate = over_integrate;
+    cfg.kappa = kappa;
+    ProblemContext ctx = make_problem(cfg, ne, k);
+    std::memcpy(u0, ctx.u0.data(), sizeof(double) * ctx.u0.size());
+    const BurgersConfig& bc = ctx.burgers;
+    const int np = k + 1;
+    std::fill(src_weak, src_weak + (size_t)ne * np, 0.0);
+    if (bc.source) {
+      // proj/src/burgers.cpp:80-92
+      const QuadratureRule quad = bc.over_integrate ? gauss_quadrature((3 * k + 2 + 1) / 2) : lgl_quadrature(*ctx.basis);
+      const Mat interp = bc.over_integrate ? interpolation_matrix(*ctx.basis, quad.points) : Mat::identity(np);
+      const int nq = int(quad.points.size());
+      for (int e = 0; e < ne; ++e) {
+        const Element& el = ctx.mesh->elements[e];
+        const double s = 0.5 * el.hx;
+        for (int i = 0; i < np; ++i) {
+          double acc = 0.0;
+          for (int q = 0; q < nq; ++q)
+            acc += (s * interp(q, i)) * (quad.weights[q] * bc.source(el.x0 + 0.5 * (quad.points[q] + 1.0) * el.hx));
+          src_weak[(size_t)e * np + i] = acc;
+        }
+      }
+    }
+    out_cfg[0] = bc.kappa;
+    out_cfg[1] = bc.flux == FluxKind::entropy ? 1.0 : 0.0;
+    out_cfg[2] = bc.sigma;
+    out_cfg[3] = bc.sigma_adaptive ? 1.0 : 0.0;
+    out_cfg[4] = bc.over_integrate ? 1.0 : 0.0;
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// L2 error of a Burgers harness state against the exact solution (burgers-mms) at time t
+double oracle_l2_error_exact(const char* problem, int ne, int k, const double* u, double t) {
+  ExperimentConfig cfg;
+  cfg.problem = problem;
+  ProblemContext ctx = make_problem(cfg, ne, k);
+  auto exact = ctx.exact;
+  return l2_error(Vec(u, u + ctx.u0.size()), 1, *ctx.mesh, *ctx.basis,
+                  [&](double x, double y, int c) { return exact(x, y, t, c); })[0];
+}
+
+// rk4 reference of a Burgers harness problem (generate_reference, proj/src/harness.cpp:364-386)
+int oracle_rk4_reference(const char* problem, int ne, int k, const char* flux, int over_integrate, double dt,
+                         double t_final, double* u_out) {
+  ExperimentConfig cfg;
+  cfg.problem = problem;
+  cfg.flux = flux;
+  cfg.over_integrate = over_integrate;
+  ProblemContext ctx = make_problem(cfg, ne, k);
+  TimeLoopConfig tl;
+  tl.dt = dt;
+  tl.t_final = t_final;
+  const IntegrationResult r = integrate(ctx.split, IntegratorKind::rk4, ctx.u0, tl);
+  std::memcpy(u_out, r.u.data(), sizeof(double) * r.u.size());
+  return r.status == RunStatus::completed ? 0 : 1;
+}
+
+// discrete L2 error (proj/src/harness.cpp:190-199) of u (ne, k) against uref (ref_ne, ref_k)
+// on the harness mesh of `problem`
+double oracle_l2_error_discrete(const char* problem, int ne, int k, const double* u, int ref_ne, int ref_k,
+                                const double* uref) {
+  ExperimentConfig cfg;
+  cfg.problem = problem;
+  ProblemContext a = make_problem(cfg, ne, k);
+  ProblemContext b = make_problem(cfg, ref_ne, ref_k);
+  const Vec ur(uref, uref + b.u0.size());
+  return l2_error(Vec(u, u + a.u0.size()), 1, *a.mesh, *a.basis,
+                  [&](double x, double, int) { return evaluate_1d(ur, *b.mesh, *b.basis, x); })[0];
+}
+
+}  // extern "C"
+
+namespace oracle {
+double mms_source(double x, double kappa);
+}  // namespace oracle
+
+// the burgers-mms forcing s(x) = u u_x - kappa u_xx (proj/src/harness.cpp:97-104)
+extern "C" double oracle_mms_source(double x, double kappa) { return oracle::mms_source(x, kappa); }

@@ -185,6 +185,9 @@ double mms_solution_dxx(double x) {
   const double s = std::sin(x * x), c = std::cos(x * x);
   return 2.0 * c * (x * x - x) - 4.0 * x * x * s * (x * x - x) + 4.0 * x * c * (2.0 * x - 1.0) + 2.0 * s;
 }
+}  // namespace
+double mms_source(double x, double kappa) { return mms_solution(x) * mms_solution_dx(x) - kappa * mms_solution_dxx(x); }
+namespace {
 double smooth_initial(double x) {
   const double s = std::sin(2.0 * M_PI * x);
   return s * s * s * std::pow(1.0 - x, 1.5);

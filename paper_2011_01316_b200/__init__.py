@@ -80,10 +80,12 @@ EXPORTS = [
     "expdg_op_apply_linear", "expdg_op_apply_nonlinear", "expdg_op_full_rhs", "expdg_phi_combination",
     "expdg_step_epi2", "expdg_integrate", "expdg_integrate_host", "expdg_lgl_basis",
     "expdg_initial_condition", "expdg_ctx_kernel_launches", "expdg_ctx_last_loop_ms", "expdg_expm",
-    "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts",
+    "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts", "expdg_op_set_source",
+    "expdg_op_set_source_fn",
 ]
 
 _lib = None
+SOURCE_FN = C.CFUNCTYPE(C.c_double, C.c_double, C.c_void_p)
 
 
 def build(force: bool = False) -> str:
@@ -116,6 +118,8 @@ def lib():
     L.expdg_op_dim.restype = i64
     L.expdg_op_dim.argtypes = [vp]
     L.expdg_op_linearize.argtypes = [vp, vp]
+    L.expdg_op_set_source.argtypes = [vp, vp]
+    L.expdg_op_set_source_fn.argtypes = [vp, SOURCE_FN, vp]
     for f in ("expdg_op_apply_linear", "expdg_op_apply_nonlinear", "expdg_op_full_rhs"):
         getattr(L, f).argtypes = [vp, vp, vp, vp]
     L.expdg_phi_combination.argtypes = [vp, vp, C.POINTER(vp), C.c_int, C.c_double, C.POINTER(KrylovCfg), vp,
@@ -309,6 +313,20 @@ class Operator:
         import torch
         torch.cuda.current_stream().synchronize()
         _check(lib().expdg_op_linearize(self.h, _dptr(ref)))
+        return self
+
+    def set_source(self, weak_source):
+        """BurgersConfig::source as its weak load vector (proj/src/burgers.cpp:80-92)."""
+        import torch
+        torch.cuda.current_stream().synchronize()
+        _check(lib().expdg_op_set_source(self.h, _dptr(weak_source)))
+        return self
+
+    def set_source_function(self, source):
+        """BurgersConfig::source given as a callable s(x) (proj/include/expdg/burgers.hpp:22);
+        the library builds the weak load on its own quadrature (proj/src/burgers.cpp:80-92)."""
+        cb = SOURCE_FN(lambda x, _user: float(source(x)))
+        _check(lib().expdg_op_set_source_fn(self.h, cb, None))
         return self
 
     def _apply(self, fn, x, out=None):

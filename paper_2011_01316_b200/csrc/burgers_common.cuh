@@ -20,6 +20,7 @@ struct B1P {
   double G[NP * NP];   // grad_vol(i,j) = w_i D(i,j)      (proj/src/burgers.cpp:49)
   double Lv[NP * NP];  // lift_vol(i,j) = D(j,i) w_j      (proj/src/burgers.cpp:50)
   const double* ut;
+  const double* src;   // weak source (proj/src/burgers.cpp:80-92), may be null
   long long n;
 };
 
@@ -126,6 +127,10 @@ __device__ __forceinline__ void b1_element(const B1P<NP>& P, int mode, int e, co
     for (int p = 0; p < NP; ++p) s = fma(P.Lv[i * NP + p], gq[p], s);
     r[i] = -s;
   }
+  if (mode != 0 && P.src) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) r[i] += P.src[(long long)e * NP + i];
+  }
   // faces (proj/src/burgers.cpp:159-173)
   if (hasL) {
     const double f = b1_face_flux(P, mode, xL[N], xC[0], mode == 2 ? 0.0 : uL[N], mode == 2 ? 0.0 : uC[0],
@@ -185,6 +190,181 @@ __device__ __forceinline__ void b1_element(const B1P<NP>& P, int mode, int e, co
   const double c = 2.0 / hC;
 #pragma unroll
   for (int i = 0; i < NP; ++i) out[i] = c * (r[i] / P.w[i]);
+}
+
+}  // namespace burgers
+}  // namespace expdg
+
+namespace expdg {
+namespace burgers {
+
+// Over-integrated variant (BurgersConfig::over_integrate, proj/src/burgers.cpp:39-51):
+// Gauss rule of NQ = (3k+3)/2 points, interp I (NQ x NP), consistent mass M (dense,
+// applied as M^-1, the reference's LDLT solve), grad_vol = I^T W I D, lift_vol = (I D)^T W.
+template <int NP, int NQ>
+struct B1OP {
+  int ne;
+  int periodic;
+  double a, b;
+  double kappa, sigma;
+  int entropy, sigma_adaptive;
+  double G[NP * NP];    // grad_vol
+  double Lv[NP * NQ];   // lift_vol (NP x NQ)
+  double I[NQ * NP];    // interp
+  double Mi[NP * NP];   // M^-1
+  const double* ut;
+  const double* src;    // weak source (proj/src/burgers.cpp:80-92), may be null
+  long long n;
+};
+
+// r of one element's LDG gradient system before the mass solve (proj/src/burgers.cpp:105-123):
+// xL2/xR2 are the end values of the elements two away (needed for the face terms of the
+// neighbours), has* flags as in b1_element.
+template <int NP, int NQ>
+__device__ __forceinline__ void b1oi_grad_r(const B1OP<NP, NQ>& P, const double* xm, const double* xc,
+                                            const double* xp, bool hasL, bool hasR, double* r) {
+  constexpr int N = NP - 1;
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) s = fma(P.G[i * NP + j], xc[j], s);
+    r[i] = s;
+  }
+  if (hasL) r[0] -= (0.5 * (xm[N] + xc[0]) - xc[0]);
+  else r[0] += -1.0 * (0.0 - xc[0]);
+  if (hasR) r[N] += (0.5 * (xc[N] + xp[0]) - xc[N]);
+  else r[N] += (0.0 - xc[N]);
+}
+
+template <int NP, int NQ>
+__device__ __forceinline__ void b1oi_minv(const B1OP<NP, NQ>& P, double c, const double* r, double* q) {
+#pragma unroll
+  for (int i = 0; i < NP; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) s = fma(P.Mi[i * NP + j], r[j], s);
+    q[i] = c * s;
+  }
+}
+
+// Element e; x*/u* point at NP values of elements e-2 .. e+2 (only the end values of
+// the outer two are used).
+template <int NP, int NQ>
+__device__ __forceinline__ void b1oi_element(const B1OP<NP, NQ>& P, int mode, int e, const double* xLL,
+                                             const double* xL, const double* xC, const double* xR,
+                                             const double* xRR, const double* uL, const double* uC,
+                                             const double* uR, double* out) {
+  constexpr int N = NP - 1;
+  const int ne = P.ne;
+  const bool hasL = P.periodic || e > 0;
+  const bool hasR = P.periodic || e < ne - 1;
+  const int eL = e == 0 ? ne - 1 : e - 1;
+  const int eR = e == ne - 1 ? 0 : e + 1;
+  const double hC = b1_break(P.a, P.b, e + 1, ne) - b1_break(P.a, P.b, e, ne);
+  const double hL = b1_break(P.a, P.b, eL + 1, ne) - b1_break(P.a, P.b, eL, ne);
+  const double hR = b1_break(P.a, P.b, eR + 1, ne) - b1_break(P.a, P.b, eR, ne);
+  double q[NP], qLN = 0.0, qR0 = 0.0;
+  if (mode != 1) {
+    double r[NP], t[NP];
+    b1oi_grad_r(P, xL, xC, xR, hasL, hasR, r);
+    b1oi_minv(P, 2.0 / hC, r, q);
+    if (hasL) {
+      const bool hLL = P.periodic || eL > 0;
+      b1oi_grad_r(P, xLL, xL, xC, hLL, true, r);
+      b1oi_minv(P, 2.0 / hL, r, t);
+      qLN = t[N];
+    }
+    if (hasR) {
+      const bool hRR = P.periodic || eR < ne - 1;
+      b1oi_grad_r(P, xC, xR, xRR, true, hRR, r);
+      b1oi_minv(P, 2.0 / hR, r, t);
+      qR0 = t[0];
+    }
+  }
+  // volume at the Gauss points (proj/src/burgers.cpp:152-157, :187-193, :223-230)
+  double r[NP];
+#pragma unroll
+  for (int i = 0; i < NP; ++i) r[i] = 0.0;
+#pragma unroll
+  for (int p = 0; p < NQ; ++p) {
+    double xq = 0.0, uq = 0.0, qq = 0.0;
+#pragma unroll
+    for (int j = 0; j < NP; ++j) {
+      xq = fma(P.I[p * NP + j], xC[j], xq);
+      if (mode != 2) uq = fma(P.I[p * NP + j], uC[j], uq);
+      if (mode != 1) qq = fma(P.I[p * NP + j], q[j], qq);
+    }
+    double g;
+    if (mode == 0) g = fma(-uq, xq, P.kappa * qq);
+    else if (mode == 1) g = uq * xq - 0.5 * (xq * xq);
+    else g = P.kappa * qq - 0.5 * (xq * xq);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) r[i] = fma(P.Lv[i * NQ + p], g, r[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < NP; ++i) r[i] = -r[i];
+  if (mode != 0 && P.src) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) r[i] += P.src[(long long)e * NP + i];
+  }
+  // faces: identical to the collocated operator (traces are nodal end values)
+  B1P<NP> F{};
+  F.kappa = P.kappa;
+  F.sigma = P.sigma;
+  F.entropy = P.entropy;
+  F.sigma_adaptive = P.sigma_adaptive;
+  if (hasL) {
+    r[0] -= b1_face_flux(F, mode, xL[N], xC[0], mode == 2 ? 0.0 : uL[N], mode == 2 ? 0.0 : uC[0],
+                         0.5 * (qLN + q[0]), hL);
+  } else {
+    const double um = xC[0], jump = -um;
+    const double utm = mode == 2 ? 0.0 : uC[0];
+    const double lin = 0.5 * (utm * um + 0.0) + 0.5 * fmax(fabs(utm), 0.0) * jump;
+    double f;
+    if (mode == 0) {
+      f = P.kappa * q[0] - lin;
+    } else {
+      double nl;
+      if (!P.entropy) {
+        nl = 0.25 * (um * um) + 0.5 * fabs(um) * jump;
+      } else {
+        double soh;
+        if (mode == 1) soh = (P.sigma_adaptive ? P.kappa / 100.0 + hC * fabs(utm) : P.sigma) * (1.0 / hC);
+        else soh = P.sigma_adaptive ? P.kappa / (100.0 * hC) + fabs(um) : P.sigma / hC;
+        const double avg = 0.5 * um;
+        nl = (0.25 * (um * um) + avg * avg) / 3.0 + soh * jump;
+      }
+      f = mode == 1 ? lin - nl : P.kappa * q[0] - nl;
+    }
+    r[0] += -1.0 * f;
+  }
+  if (hasR) {
+    r[N] += b1_face_flux(F, mode, xC[N], xR[0], mode == 2 ? 0.0 : uC[N], mode == 2 ? 0.0 : uR[0],
+                         0.5 * (q[N] + qR0), hC);
+  } else {
+    const double um = xC[N], jump = um;
+    const double utm = mode == 2 ? 0.0 : uC[N];
+    const double lin = 0.5 * (utm * um + 0.0) + 0.5 * fmax(fabs(utm), 0.0) * jump;
+    double f;
+    if (mode == 0) {
+      f = P.kappa * q[N] - lin;
+    } else {
+      double nl;
+      if (!P.entropy) {
+        nl = 0.25 * (um * um) + 0.5 * fabs(um) * jump;
+      } else {
+        double soh;
+        if (mode == 1) soh = (P.sigma_adaptive ? P.kappa / 100.0 + hC * fabs(utm) : P.sigma) * (1.0 / hC);
+        else soh = P.sigma_adaptive ? P.kappa / (100.0 * hC) + fabs(um) : P.sigma / hC;
+        const double avg = 0.5 * um;
+        nl = (0.25 * (um * um) + avg * avg) / 3.0 + soh * jump;
+      }
+      f = mode == 1 ? lin - nl : P.kappa * q[N] - nl;
+    }
+    r[N] += f;
+  }
+  b1oi_minv(P, 2.0 / hC, r, out);
 }
 
 }  // namespace burgers

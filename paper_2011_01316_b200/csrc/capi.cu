@@ -100,7 +100,8 @@ void validate_desc(const expdg_op_desc& d) {
   if (d.kind == EXPDG_BURGERS1D || d.kind == EXPDG_BURGERS2D) {
     if (!(d.kappa > 0.0)) throw std::invalid_argument("BurgersOperator: kappa must be positive");
     if (d.sigma < 0.0) throw std::invalid_argument("BurgersOperator: sigma must be nonnegative");
-    if (d.over_integrate) throw Unsupported("over-integrated Burgers is not on the device path");
+    if (d.over_integrate && d.kind == EXPDG_BURGERS2D)
+      throw Unsupported("over-integrated 2D Burgers is not on the device path");
   } else {
     if (!d.periodic) throw std::invalid_argument("EulerOperator: periodic boundaries only");
     if (d.euler_flux != 1) throw Unsupported("Roe flux is not on the device path (lax_friedrichs only)");
@@ -204,6 +205,31 @@ int expdg_op_linearize(expdg_op* op, const double* ref_dev) {
     EXPDG_CUDA(cudaMemcpyAsync(op->ref_owned, ref_dev, sizeof(double) * op->dev->n, cudaMemcpyDeviceToDevice, s));
     op->dev->freeze(s, op->ref_owned);
     // the caller may release ref_dev on return: finish reading it
+    EXPDG_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int expdg_op_set_source(expdg_op* op, const double* weak_source_dev) {
+  return guard([&] {
+    if (!op || !weak_source_dev) throw std::invalid_argument("null argument");
+    op->dev->set_source(op->ctx->eng->stream, weak_source_dev);
+    EXPDG_CUDA(cudaStreamSynchronize(op->ctx->eng->stream));
+  });
+}
+
+int expdg_op_set_source_fn(expdg_op* op, double (*source)(double x, void* user), void* user) {
+  return guard([&] {
+    if (!op || !source) throw std::invalid_argument("null argument");
+    const expdg_op_desc& d = op->dev->desc;
+    if (d.kind != EXPDG_BURGERS1D) throw std::invalid_argument("source terms are 1D Burgers only");
+    std::vector<double> w((size_t)op->dev->n);
+    host_burgers_source(d.order, d.nx, d.x0, d.x1, d.over_integrate != 0, source, user, w.data());
+    cudaStream_t s = op->ctx->eng->stream;
+    double* tmp = nullptr;
+    EXPDG_CUDA(cudaMallocAsync(&tmp, sizeof(double) * w.size(), s));
+    EXPDG_CUDA(cudaMemcpyAsync(tmp, w.data(), sizeof(double) * w.size(), cudaMemcpyHostToDevice, s));
+    op->dev->set_source(s, tmp);
+    EXPDG_CUDA(cudaFreeAsync(tmp, s));
     EXPDG_CUDA(cudaStreamSynchronize(s));
   });
 }

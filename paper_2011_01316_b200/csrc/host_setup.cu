@@ -225,6 +225,87 @@ HostBasis host_lgl_basis(int order) {
   return b;
 }
 
+// Over-integration matrices of BurgersOperator (proj/src/burgers.cpp:39-51), built
+// with the same products as the reference; M^-1 by LDLT solves of the unit vectors.
+HostOI host_burgers_oi(int order) {
+  const HostBasis b = host_lgl_basis(order);
+  const int np = order + 1;
+  const Rule quad = gauss((3 * order + 2 + 1) / 2);
+  const int nq = (int)quad.p.size();
+  HostOI o;
+  o.nq = nq;
+  o.I.assign((size_t)nq * np, 0.0);
+  for (int q = 0; q < nq; ++q) {
+    const std::vector<double> v = lagrange(b, quad.p[q]);
+    for (int j = 0; j < np; ++j) o.I[(size_t)q * np + j] = v[j];
+  }
+  std::vector<double> dI((size_t)nq * np, 0.0);  // dinterp = I D
+  for (int q = 0; q < nq; ++q)
+    for (int k = 0; k < np; ++k)
+      for (int j = 0; j < np; ++j) dI[(size_t)q * np + j] += o.I[(size_t)q * np + k] * b.D[(size_t)k * np + j];
+  o.G.assign((size_t)np * np, 0.0);  // (I^T W) dI
+  for (int i = 0; i < np; ++i)
+    for (int q = 0; q < nq; ++q) {
+      const double a = o.I[(size_t)q * np + i] * quad.w[q];
+      for (int j = 0; j < np; ++j) o.G[(size_t)i * np + j] += a * dI[(size_t)q * np + j];
+    }
+  o.Lv.assign((size_t)np * nq, 0.0);  // dI^T W
+  for (int i = 0; i < np; ++i)
+    for (int q = 0; q < nq; ++q) o.Lv[(size_t)i * nq + q] = dI[(size_t)q * np + i] * quad.w[q];
+  std::vector<double> M((size_t)np * np, 0.0);  // (I^T W) I
+  for (int i = 0; i < np; ++i)
+    for (int q = 0; q < nq; ++q) {
+      const double a = o.I[(size_t)q * np + i] * quad.w[q];
+      for (int j = 0; j < np; ++j) M[(size_t)i * np + j] += a * o.I[(size_t)q * np + j];
+    }
+  Ldlt l;
+  l.compute(M, np);
+  o.Mi.assign((size_t)np * np, 0.0);
+  for (int j = 0; j < np; ++j) {
+    std::vector<double> e(np, 0.0);
+    e[j] = 1.0;
+    const std::vector<double> c = l.solve(e);
+    for (int i = 0; i < np; ++i) o.Mi[(size_t)i * np + j] = c[i];
+  }
+  return o;
+}
+
+// Weak load of BurgersConfig::source (proj/src/burgers.cpp:80-92): per element
+// 0.5 h_e I^T (W s(x_q)) on the operator's quadrature (Gauss (3k+3)/2 points when
+// over-integrated, the LGL nodes otherwise).
+void host_burgers_source(int order, int ne, double a, double b, bool over_integrate,
+                         double (*fn)(double, void*), void* user, double* out) {
+  const HostBasis basis = host_lgl_basis(order);
+  const int np = order + 1;
+  std::vector<double> pts, wts, I;
+  if (over_integrate) {
+    const Rule quad = gauss((3 * order + 2 + 1) / 2);
+    pts = quad.p;
+    wts = quad.w;
+    I.assign(pts.size() * np, 0.0);
+    for (size_t q = 0; q < pts.size(); ++q) {
+      const std::vector<double> v = lagrange(basis, pts[q]);
+      for (int j = 0; j < np; ++j) I[q * np + j] = v[j];
+    }
+  } else {
+    pts = basis.nodes;
+    wts = basis.weights;
+    I.assign((size_t)np * np, 0.0);
+    for (int j = 0; j < np; ++j) I[(size_t)j * np + j] = 1.0;
+  }
+  const int nq = (int)pts.size();
+  std::vector<double> ws(nq);
+  for (int e = 0; e < ne; ++e) {
+    const double x0 = ubreak(a, b, e, ne), hx = ubreak(a, b, e + 1, ne) - x0;
+    for (int q = 0; q < nq; ++q) ws[q] = wts[q] * fn(x0 + 0.5 * (pts[q] + 1.0) * hx, user);
+    for (int i = 0; i < np; ++i) {
+      double acc = 0.0;
+      for (int q = 0; q < nq; ++q) acc += I[(size_t)q * np + i] * ws[q];
+      out[(size_t)e * np + i] = 0.5 * hx * acc;
+    }
+  }
+}
+
 // Seeded inputs (identical generator and formulas to the oracle's inputs.cpp).
 void host_initial_condition(int cfg, int nx, int order, uint64_t seed, double noise, double* out) {
   const HostBasis b = host_lgl_basis(order);

@@ -37,6 +37,11 @@ class OpDevice {
   // Freeze the reference state (proj/src/burgers.cpp:53-78, proj/src/euler.cpp:198-243):
   // operators that keep derived frozen data compute it here.
   virtual void freeze(cudaStream_t s, const double* r) { ref = r; }
+  // Weak steady source added to N and the full RHS (BurgersConfig::source,
+  // proj/src/burgers.cpp:80-92): per element (s, l_j) values, state layout.
+  virtual void set_source(cudaStream_t, const double*) {
+    throw std::invalid_argument("this operator has no source term");
+  }
 };
 
 std::unique_ptr<OpDevice> make_burgers1d(const expdg_op_desc& d);
@@ -51,6 +56,13 @@ struct HostBasis {
   std::vector<double> nodes, weights, D;  // D row-major
 };
 HostBasis host_lgl_basis(int order);
+struct HostOI {
+  int nq = 0;
+  std::vector<double> I, G, Lv, Mi;  // interp (nq x np), grad_vol, lift_vol (np x nq), M^-1
+};
+HostOI host_burgers_oi(int order);
+void host_burgers_source(int order, int ne, double a, double b, bool over_integrate,
+                         double (*fn)(double, void*), void* user, double* out);
 
 // Device workspace + launch helpers of the phi engine.
 struct TsTuning {

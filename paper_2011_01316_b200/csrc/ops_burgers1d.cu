@@ -140,6 +140,13 @@ class Burgers1D : public OpDevice {
  public:
   B1P<NP> P{};
   int grid = 1;
+  double* src = nullptr;
+  ~Burgers1D() override { cudaFree(src); }
+  void set_source(cudaStream_t s, const double* weak) override {
+    if (!src) EXPDG_CUDA(cudaMalloc(&src, sizeof(double) * n));
+    EXPDG_CUDA(cudaMemcpyAsync(src, weak, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    P.src = src;
+  }
   explicit Burgers1D(const expdg_op_desc& d) {
     desc = d;
     const HostBasis hb = host_lgl_basis(d.order);
@@ -178,6 +185,181 @@ class Burgers1D : public OpDevice {
     B1P<NP> p = P;
     p.ut = u;
     k_b1_apply<NP><<<grid, kB1Threads, 0, s>>>(p, 2, u, r, st);
+  }
+};
+
+// ---------------------------------------------------------------- over-integrated 1D Burgers
+// Stage [e0-2, e0+E+1] (two-element halo: the dense consistent-mass solve makes
+// a neighbour's face q depend on its other face).
+template <int NP, int NQ>
+__device__ __forceinline__ void b1oi_stage(const B1OP<NP, NQ>& P, long long e0, int E, const double* x, double xs,
+                                           bool want_ut, double* sx, double* su) {
+  const int cnt = (E + 4) * NP;
+  for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+    long long ge = e0 - 2 + idx / NP;
+    const int node = idx % NP;
+    double xv = 0.0, uv = 0.0;
+    if (ge < 0 || ge >= P.ne) {
+      if (P.periodic) {
+        ge = ((ge % P.ne) + P.ne) % P.ne;
+        xv = x[ge * NP + node] * xs;
+        if (want_ut) uv = P.ut[ge * NP + node];
+      }
+    } else {
+      xv = x[ge * NP + node] * xs;
+      if (want_ut) uv = P.ut[ge * NP + node];
+    }
+    sx[idx] = xv;
+    su[idx] = uv;
+  }
+}
+
+template <int NP, int NQ>
+__global__ void __launch_bounds__(kB1Threads) k_b1oi_apply(B1OP<NP, NQ> P, int mode, const double* __restrict__ x,
+                                                           double* __restrict__ y, const PhiState* st) {
+  __shared__ double sx[(kB1Threads + 4) * NP], su[(kB1Threads + 4) * NP], sy[kB1Threads * NP];
+  if (st && st->stopped) return;
+  const int ntiles = (P.ne + kB1Threads - 1) / kB1Threads;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = (long long)tile * kB1Threads;
+    const int E = (int)(P.ne - e0 < kB1Threads ? P.ne - e0 : kB1Threads);
+    __syncthreads();
+    b1oi_stage(P, e0, E, x, 1.0, mode != 2, sx, su);
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < E) {
+      double out[NP];
+      const double* b = sx + (t + 2) * NP;
+      const double* ub = su + (t + 2) * NP;
+      b1oi_element<NP, NQ>(P, mode, (int)(e0 + t), b - 2 * NP, b - NP, b, b + NP, b + 2 * NP, ub - NP, ub, ub + NP,
+                           out);
+#pragma unroll
+      for (int i = 0; i < NP; ++i) sy[t * NP + i] = out[i];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < E * NP; idx += blockDim.x) y[e0 * NP + idx] = sy[idx];
+  }
+}
+
+template <int NP, int NQ>
+__global__ void __launch_bounds__(kB1Threads) k_b1oi_phi(B1OP<NP, NQ> P, PhiState* st, double* base,
+                                                         double* partials, BArgs b) {
+  __shared__ double sx[(kB1Threads + 4) * NP], su[(kB1Threads + 4) * NP], sy[kB1Threads * NP];
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[kB1Threads / 32];
+  __shared__ double s_red[1];
+  if (threadIdx.x == 0) {
+    const int a = st->action;
+    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    if (s_go) {
+      s_j = st->j;
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[P.n + i] * s_xs : 0.0;
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  double nacc = 0.0;
+  const int ntiles = (P.ne + kB1Threads - 1) / kB1Threads;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long e0 = (long long)tile * kB1Threads;
+    const int E = (int)(P.ne - e0 < kB1Threads ? P.ne - e0 : kB1Threads);
+    __syncthreads();
+    b1oi_stage(P, e0, E, x, xs, true, sx, su);
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < E) {
+      double out[NP];
+      const double* bb = sx + (t + 2) * NP;
+      const double* ub = su + (t + 2) * NP;
+      b1oi_element<NP, NQ>(P, 0, (int)(e0 + t), bb - 2 * NP, bb - NP, bb, bb + NP, bb + 2 * NP, ub - NP, ub,
+                           ub + NP, out);
+#pragma unroll
+      for (int i = 0; i < NP; ++i) sy[t * NP + i] = out[i];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < E * NP; idx += blockDim.x) {
+      const long long g = e0 * NP + idx;
+      double v = sy[idx];
+      for (int i = 0; i < b.p; ++i)
+        if (b.b[b.p - i]) v = fma(s_xt[i], b.b[b.p - i][g], v);
+      v = dt * v;
+      y[g] = v;
+      nacc = fma(v, v, nacc);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here) {
+    const int i = threadIdx.x;
+    const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
+    y[P.n + i] = v;
+    nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (threadIdx.x == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+}
+
+template <int NP, int NQ>
+class Burgers1DOI : public OpDevice {
+ public:
+  B1OP<NP, NQ> P{};
+  int grid = 1;
+  double* src = nullptr;
+  ~Burgers1DOI() override { cudaFree(src); }
+  explicit Burgers1DOI(const expdg_op_desc& d) {
+    desc = d;
+    const HostOI o = host_burgers_oi(d.order);
+    if (o.nq != NQ) throw std::invalid_argument("burgers1d: over-integration rule mismatch");
+    P.ne = d.nx;
+    P.periodic = d.periodic;
+    P.a = d.x0;
+    P.b = d.x1;
+    P.kappa = d.kappa;
+    P.sigma = d.sigma;
+    P.entropy = d.flux == 1;
+    P.sigma_adaptive = d.sigma_adaptive;
+    for (int i = 0; i < NP * NP; ++i) {
+      P.G[i] = o.G[i];
+      P.Mi[i] = o.Mi[i];
+    }
+    for (int i = 0; i < NP * NQ; ++i) {
+      P.Lv[i] = o.Lv[i];
+      P.I[i] = o.I[i];
+    }
+    n = (long long)d.nx * NP;
+    P.n = n;
+    comps = 1;
+    const int ntiles = (d.nx + kB1Threads - 1) / kB1Threads;
+    grid = std::max(1, std::min(ntiles, 148 * 8));
+  }
+  void set_source(cudaStream_t s, const double* weak) override {
+    if (!src) EXPDG_CUDA(cudaMalloc(&src, sizeof(double) * n));
+    EXPDG_CUDA(cudaMemcpyAsync(src, weak, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    P.src = src;
+  }
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+    B1OP<NP, NQ> p = P;
+    p.ut = ref;
+    k_b1oi_phi<NP, NQ><<<grid, kB1Threads, 0, s>>>(p, st, base, partials, b);
+  }
+  void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
+    B1OP<NP, NQ> p = P;
+    p.ut = ref;
+    k_b1oi_apply<NP, NQ><<<grid, kB1Threads, 0, s>>>(p, which, x, y, nullptr);
+  }
+  void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
+    B1OP<NP, NQ> p = P;
+    p.ut = u;
+    k_b1oi_apply<NP, NQ><<<grid, kB1Threads, 0, s>>>(p, 2, u, r, st);
   }
 };
 
@@ -257,7 +439,19 @@ class DenseOp : public OpDevice {
 }  // namespace
 
 std::unique_ptr<OpDevice> make_burgers1d(const expdg_op_desc& d) {
-  if (d.over_integrate) throw std::invalid_argument("burgers1d: over_integrate is not on the device path");
+  if (d.over_integrate) {
+    switch (d.order) {  // NQ = (3k + 3) / 2 Gauss points (proj/src/burgers.cpp:41)
+      case 1: return std::make_unique<Burgers1DOI<2, 3>>(d);
+      case 2: return std::make_unique<Burgers1DOI<3, 4>>(d);
+      case 3: return std::make_unique<Burgers1DOI<4, 6>>(d);
+      case 4: return std::make_unique<Burgers1DOI<5, 7>>(d);
+      case 5: return std::make_unique<Burgers1DOI<6, 9>>(d);
+      case 6: return std::make_unique<Burgers1DOI<7, 10>>(d);
+      case 7: return std::make_unique<Burgers1DOI<8, 12>>(d);
+      case 8: return std::make_unique<Burgers1DOI<9, 13>>(d);
+    }
+    throw std::invalid_argument("burgers1d: device orders are 1..8");
+  }
   switch (d.order + 1) {
     case 2: return std::make_unique<Burgers1D<2>>(d);
     case 3: return std::make_unique<Burgers1D<3>>(d);

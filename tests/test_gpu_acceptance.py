@@ -1,0 +1,127 @@
+"""The reference's own acceptance criteria replayed on the DEVICE path.
+
+The device integrates the harness problems of proj/src/harness.cpp:48-142
+(over-integrated LDG Burgers on (0,1) with zero Dirichlet data, optional MMS
+source) with exactly the reference's settings (proj/tests/acceptance.cpp), and
+must reproduce the digits the reference printed in proj/test_output.txt:18-28.
+The oracle only supplies initial states / reference solutions / error norms
+(checker side).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2011_01316_b200 as pkg
+from tests.gpu_util import to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+KRYLOV = dict(tol=1e-12, max_basis=128, orth_length=128)  # ExperimentConfig defaults
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return pkg.Context(0)
+
+
+def device_problem(ctx, problem, ne, k, flux="", sigma=0.0):
+    u0, src, cfg = oracle.harness_burgers(problem, ne, k, flux, sigma)
+    spec = pkg.OperatorSpec("burgers1d", k, ne, box=(0.0, 1.0, 0, 1, 0, 1), periodic=False, kappa=cfg["kappa"],
+                            flux=cfg["flux"], sigma=cfg["sigma"], sigma_adaptive=cfg["sigma_adaptive"],
+                            over_integrate=cfg["over_integrate"])
+    op = pkg.Operator(ctx, spec)
+    if np.any(src != 0.0):
+        op.set_source(to_dev(src))
+    return op, u0
+
+
+def test_over_integrated_operator_matches_oracle(ctx):
+    rng = np.random.default_rng(3)
+    for k in range(1, 9):
+        for periodic in (True, False):
+            spec = pkg.OperatorSpec("burgers1d", k, 9, box=(0, 1, 0, 1, 0, 1), periodic=periodic, kappa=0.04,
+                                    flux="ef", sigma=2e-3, over_integrate=True)
+            op = pkg.Operator(ctx, spec)
+            orc = oracle.Problem("burgers1d", k, 9, box=(0, 1, 0, 1, 0, 1), periodic=periodic, kappa=0.04,
+                                 flux="ef", sigma=2e-3, over_integrate=True)
+            ref, x = rng.standard_normal(op.dim), rng.standard_normal(op.dim)
+            op.linearize(to_dev(ref))
+            for dev_f, orc_f in ((op.apply_linear, lambda v: orc.apply_linear(ref, v)),
+                                 (op.apply_nonlinear, lambda v: orc.apply_nonlinear(ref, v)),
+                                 (op.full_rhs, orc.full_rhs)):
+                a, b = to_host(dev_f(to_dev(x))), orc_f(x)
+                assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(b), (k, periodic)
+
+
+def test_criterion_5_large_courant_epi2(ctx):
+    # proj/test_output.txt:22 — "Cr_d=161.0, EPI2 completed with max|u| ratio 1.0000"
+    op, u0 = device_problem(ctx, "burgers-smooth", 40, 4, "ef", 3e-4)
+    r = pkg.integrate(ctx, op, to_dev(u0), "epi2", 0.1, 1.0, **KRYLOV)
+    assert r.status == "completed" and r.steps == 10
+    assert f"{r.max_abs / np.abs(u0).max():.4f}" == "1.0000"
+
+
+def test_criterion_4_temporal_orders(ctx):
+    # proj/test_output.txt:21 — EPI2 orders 1.974 2.044 2.037 (err@0.01 4.942e-06),
+    # EXPRB32 orders 2.641 2.881 3.001
+    uref = oracle.rk4_reference("burgers-smooth", 40, 4, "lf", 1, 1e-5, 1.0)
+    dts = [0.5, 0.25, 0.1, 0.05, 0.01]
+    for integ, want in (("epi2", ["1.974", "2.044", "2.037"]), ("exprb32", ["2.641", "2.881", "3.001"])):
+        errs = []
+        for dt in dts:
+            op, u0 = device_problem(ctx, "burgers-smooth", 40, 4, "lf")
+            r = pkg.integrate(ctx, op, to_dev(u0), integ, dt, 1.0, **KRYLOV)
+            assert r.status == "completed"
+            errs.append(oracle.l2_error_discrete("burgers-smooth", 40, 4, to_host(r.u), 40, 4, uref))
+        orders = [f"{math.log(errs[i - 1] / errs[i]) / math.log(dts[i - 1] / dts[i]):.3f}" for i in (2, 3, 4)]
+        assert orders == want, (integ, orders)
+        if integ == "epi2":
+            assert f"{errs[4]:.3e}" == "4.942e-06"
+
+
+@pytest.mark.parametrize("k,flux,errs_want,orders_want", [
+    (2, "lf", ["2.455e-06", "3.051e-07", "3.807e-08", "4.755e-09"], ["3.008", "3.003", "3.001"]),
+    (4, "lf", None, ["5.003", "5.001", "5.000"]),
+    (3, "ef", None, ["3.077", "3.019", "3.005"]),
+])
+def test_criteria_2_3_manufactured_solution(ctx, k, flux, errs_want, orders_want):
+    # proj/test_output.txt:19-20 — exprb32, dt 5e-5, t 0.01, MMS source term on the device
+    errs = []
+    for ne in (20, 40, 80, 160):
+        op, u0 = device_problem(ctx, "burgers-mms", ne, k, flux, 0.0)
+        r = pkg.integrate(ctx, op, to_dev(u0), "exprb32", 5e-5, 0.01, **KRYLOV)
+        assert r.status == "completed"
+        errs.append(oracle.l2_error_exact("burgers-mms", ne, k, to_host(r.u), 0.01))
+    if errs_want:
+        assert [f"{e:.3e}" for e in errs] == errs_want
+    assert [f"{math.log2(errs[i - 1] / errs[i]):.3f}" for i in (1, 2, 3)] == orders_want
+
+
+def test_criterion_9_burgers_orders(ctx):
+    # proj/test_output.txt:26 — "Burgers orders 1.04/2.04/2.88/3.70"
+    uref = oracle.rk4_reference("burgers-smooth", 20, 3, "lf", 1, 1e-5, 1.0)
+    got = []
+    for integ in ("exp_euler", "epi2", "exprb32", "exprb42"):
+        e = []
+        for dt in (0.1, 0.05):
+            op, u0 = device_problem(ctx, "burgers-smooth", 20, 3, "lf")
+            r = pkg.integrate(ctx, op, to_dev(u0), integ, dt, 1.0, **KRYLOV)
+            e.append(oracle.l2_error_discrete("burgers-smooth", 20, 3, to_host(r.u), 20, 3, uref))
+        got.append(f"{math.log(e[0] / e[1]) / math.log(2.0):.2f}")
+    assert got == ["1.04", "2.04", "2.88", "3.70"]
+
+
+@pytest.mark.parametrize("over_integrate", [True, False])
+def test_source_function_matches_weak_load(ctx, over_integrate):
+    # expdg_op_set_source_fn builds (s, l_j) itself (proj/src/burgers.cpp:80-92)
+    u0, src, cfg = oracle.harness_burgers("burgers-mms", 20, 3, "lf", 0.0, over_integrate=over_integrate)
+    spec = pkg.OperatorSpec("burgers1d", 3, 20, box=(0.0, 1.0, 0, 1, 0, 1), periodic=False, kappa=cfg["kappa"],
+                            flux=cfg["flux"], over_integrate=over_integrate)
+    a, b = pkg.Operator(ctx, spec), pkg.Operator(ctx, spec)
+    a.set_source(to_dev(src))
+    b.set_source_function(lambda x: oracle.mms_source(x, cfg["kappa"]))
+    x = to_dev(u0)
+    ya, yb = to_host(a.full_rhs(x)), to_host(b.full_rhs(x))
+    assert np.linalg.norm(ya - yb) <= 1e-13 * np.linalg.norm(ya)
