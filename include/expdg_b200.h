@@ -67,7 +67,7 @@ typedef struct {
   int sigma_adaptive;
   int over_integrate;  /* 1D Burgers: Gauss rule of (3k+3)/2 points + consistent mass (proj/src/burgers.cpp:39-51) */
   double gamma;        /* Euler */
-  int euler_flux;      /* 0 roe (EXPDG_E_UNSUPPORTED on the device path), 1 lax_friedrichs */
+  int euler_flux;      /* 0 roe (2D only, proj/src/euler.cpp:114-145), 1 lax_friedrichs */
 } expdg_op_desc;
 
 /* KrylovSettings (proj/include/expdg/integrators.hpp:20-24) + the two

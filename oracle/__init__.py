@@ -91,7 +91,9 @@ def lib():
         L.oracle_l2_error_exact.restype = C.c_double
         L.oracle_mms_source.restype = C.c_double
         L.oracle_mms_source.argtypes = [C.c_double, C.c_double]
-        L.oracle_l2_error_exact.argtypes = [C.c_char_p, C.c_int, C.c_int, dp, C.c_double]
+        L.oracle_l2_error_exact.argtypes = [C.c_char_p, C.c_int, C.c_int, dp, C.c_double, C.c_int]
+        L.oracle_harness_u0.restype = C.c_long
+        L.oracle_harness_u0.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_void_p]
         L.oracle_rk4_reference.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_double,
                                            C.c_double, dp]
         L.oracle_l2_error_discrete.restype = C.c_double
@@ -332,9 +334,19 @@ def mms_source(x, kappa):
     return lib().oracle_mms_source(float(x), float(kappa))
 
 
-def l2_error_exact(problem, ne, k, u, t):
+def l2_error_exact(problem, ne, k, u, t, comp=0):
     u = np.ascontiguousarray(u, dtype=np.float64)
-    return lib().oracle_l2_error_exact(problem.encode(), ne, k, _p(u), t)
+    return lib().oracle_l2_error_exact(problem.encode(), ne, k, _p(u), t, comp)
+
+
+def harness_u0(problem, ne, k):
+    """u0 of make_problem (proj/src/harness.cpp:48-142)."""
+    n = lib().oracle_harness_u0(problem.encode(), ne, k, None)
+    if n < 0:
+        raise ValueError("harness problem")
+    out = np.empty(n)
+    lib().oracle_harness_u0(problem.encode(), ne, k, _p(out))
+    return out
 
 
 def rk4_reference(problem, ne, k, flux, over_integrate, dt, t_final):

@@ -281,14 +281,29 @@ int oracle_harness_burgers(const char* problem, int ne, int k, const char* flux,
   }
 }
 
-// L2 error of a Burgers harness state against the exact solution (burgers-mms) at time t
-double oracle_l2_error_exact(const char* problem, int ne, int k, const double* u, double t) {
+// L2 error (component comp) of a harness state against the problem's exact solution at
+// time t (burgers-mms, euler-vortex; proj/src/harness.cpp:418-440)
+double oracle_l2_error_exact(const char* problem, int ne, int k, const double* u, double t, int comp) {
   ExperimentConfig cfg;
   cfg.problem = problem;
   ProblemContext ctx = make_problem(cfg, ne, k);
   auto exact = ctx.exact;
-  return l2_error(Vec(u, u + ctx.u0.size()), 1, *ctx.mesh, *ctx.basis,
-                  [&](double x, double y, int c) { return exact(x, y, t, c); })[0];
+  return l2_error(Vec(u, u + ctx.u0.size()), ctx.components, *ctx.mesh, *ctx.basis,
+                  [&](double x, double y, int c) { return exact(x, y, t, c); })[comp];
+}
+
+// u0 of any harness problem (make_problem, proj/src/harness.cpp:48-142); returns the
+// dimension, writes u0 when out is non-null
+long oracle_harness_u0(const char* problem, int ne, int k, double* out) {
+  try {
+    ExperimentConfig cfg;
+    cfg.problem = problem;
+    ProblemContext ctx = make_problem(cfg, ne, k);
+    if (out) std::memcpy(out, ctx.u0.data(), sizeof(double) * ctx.u0.size());
+    return (long)ctx.u0.size();
+  } catch (const std::exception&) {
+    return -1;
+  }
 }
 
 // rk4 reference of a Burgers harness problem (generate_reference, proj/src/harness.cpp:364-386)

@@ -104,7 +104,8 @@ void validate_desc(const expdg_op_desc& d) {
       throw Unsupported("over-integrated 2D Burgers is not on the device path");
   } else {
     if (!d.periodic) throw std::invalid_argument("EulerOperator: periodic boundaries only");
-    if (d.euler_flux != 1) throw Unsupported("Roe flux is not on the device path (lax_friedrichs only)");
+    if (d.euler_flux != 1 && d.kind == EXPDG_EULER3D)
+      throw Unsupported("3D Euler: Lax-Friedrichs flux only (the Roe flux is 2D, proj/src/euler.cpp:114-145)");
   }
 }
 

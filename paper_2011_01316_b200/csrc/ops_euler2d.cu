@@ -1,4 +1,4 @@
-// 2D compressible Euler DG operators on sm_100a, Lax-Friedrichs split:
+// 2D compressible Euler DG operators on sm_100a, Lax-Friedrichs or Roe split:
 // the JVP L q = frozen-Jacobian volume + linearised LF faces
 // (proj/src/euler.cpp:299-341, rhs_faces :260-297, inverse mass :246-258),
 // N q (:343-388) and the full RHS (:403-408).
@@ -102,41 +102,113 @@ __device__ __forceinline__ void flux_dir(const double q[4], const Prim& pr, int 
   }
 }
 
+// |A(avg, e_dir)| dq = R |Lambda| R^-1 dq at a Roe state (abs_jacobian_from,
+// proj/src/euler.cpp:75-103), applied to the vector without forming the matrix.
+__device__ __forceinline__ void roe_abs_apply(int dir, double gamma, double rho, double u, double v, double H,
+                                              double a, const double dq[4], double out[4]) {
+  const double gm1 = gamma - 1.0;
+  const double n0 = dir == 0 ? 1.0 : 0.0, n1 = dir == 0 ? 0.0 : 1.0;
+  const double un = dir == 0 ? u : v;
+  const double ut = dir == 0 ? v : -u;
+  const double phi = 0.5 * gm1 * (u * u + v * v);
+  const double a2 = a * a;
+  const double dp = phi * dq[0] - gm1 * u * dq[1] - gm1 * v * dq[2] + gm1 * dq[3];
+  const double dun = (-un * dq[0] + n0 * dq[1] + n1 * dq[2]) / rho;
+  const double dut = (-ut * dq[0] - n1 * dq[1] + n0 * dq[2]) / rho;
+  const double w0 = fabs(un - a) * ((dp - rho * a * dun) / (2.0 * a2));
+  const double w1 = fabs(un) * (dq[0] - dp / a2);
+  const double w2 = fabs(un) * (rho * dut);
+  const double w3 = fabs(un + a) * ((dp + rho * a * dun) / (2.0 * a2));
+  out[0] = w0 + w1 + w3;
+  out[1] = (u - a * n0) * w0 + u * w1 - n1 * w2 + (u + a * n0) * w3;
+  out[2] = (v - a * n1) * w0 + v * w1 + n0 * w2 + (v + a * n1) * w3;
+  out[3] = (H - a * un) * w0 + 0.5 * (u * u + v * v) * w1 + ut * w2 + (H + a * un) * w3;
+}
+
+// roe_average (proj/src/euler.cpp:114-131) from (u, v, H) and sqrt(rho) of both sides;
+// false when the averaged sound speed is not real.
+__device__ __forceinline__ bool roe_avg(double sm, double um, double vm, double Hm, double sp, double up, double vp,
+                                        double Hp, double gamma, double& rho, double& u, double& v, double& H,
+                                        double& a) {
+  rho = sm * sp;
+  u = (sm * um + sp * up) / (sm + sp);
+  v = (sm * vm + sp * vp) / (sm + sp);
+  H = (sm * Hm + sp * Hp) / (sm + sp);
+  const double a2 = (gamma - 1.0) * (H - 0.5 * (u * u + v * v));
+  a = sqrt(a2);
+  return a2 > 0.0;
+}
+
 // Numerical normal flux on a face with n = +e_dir between owner (qm, utm) and
-// neighbour (qp, utp):  mode 0 linearised LF, 1 full LF - linearised, 2 full LF.
+// neighbour (qp, utp):  mode 0 linearised, 1 full - linearised, 2 full.
+// ROE: Roe flux (frozen |A| at the Roe average of q~, proj/src/euler.cpp:232-236,
+// roe_flux :138-145); else Lax-Friedrichs (:237-241, :147-158).  The frozen
+// slot 3 holds sqrt(rho~) for Roe, a~ for LF.
+template <bool ROE>
 __device__ __forceinline__ void face_flux(int mode, int dir, double gamma, const double qm[4], const double qp[4],
                                           const double utm[4], const double utp[4], double f[4], bool& bad) {
   double lin[4] = {0, 0, 0, 0};
   if (mode != 2) {
     const Prim tm = prim_frozen(utm), tp = prim_frozen(utp);
-    double am[4], ap[4];
+    double am[4], ap[4], dq[4], dis[4];
     jac_apply(tm, dir, gamma, qm, am);
     jac_apply(tp, dir, gamma, qp, ap);
-    const double cm = fabs(dir == 0 ? tm.u : tm.v) + tm.a;
-    const double cp = fabs(dir == 0 ? tp.u : tp.v) + tp.a;
-    const double lam = fmax(cm, cp);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) lin[c] = 0.5 * (am[c] + ap[c]) + 0.5 * (lam * (qm[c] - qp[c]));
+    for (int c = 0; c < 4; ++c) dq[c] = qm[c] - qp[c];
+    if (ROE) {
+      double rho, u, v, H, a;
+      roe_avg(utm[3], tm.u, tm.v, tm.H, utp[3], tp.u, tp.v, tp.H, gamma, rho, u, v, H, a);
+      roe_abs_apply(dir, gamma, rho, u, v, H, a, dq, dis);
+    } else {
+      const double cm = fabs(dir == 0 ? tm.u : tm.v) + tm.a;
+      const double cp = fabs(dir == 0 ? tp.u : tp.v) + tp.a;
+      const double lam = fmax(cm, cp);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dis[c] = lam * dq[c];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) lin[c] = 0.5 * (am[c] + ap[c]) + 0.5 * dis[c];
   }
   if (mode == 0) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) f[c] = lin[c];
     return;
   }
-  // euler_lax_friedrichs_flux (proj/src/euler.cpp:147-158)
   if (!admissible4(qm, gamma) || !admissible4(qp, gamma)) bad = true;
   const Prim pm = prim_of(qm, gamma), pp = prim_of(qp, gamma);
-  double fm[4], fp[4];
+  double fm[4], fp[4], dis[4];
   flux_dir(qm, pm, dir, fm);
   flux_dir(qp, pp, dir, fp);
-  const double cm = fabs(dir == 0 ? pm.u : pm.v) + pm.a;
-  const double cp = fabs(dir == 0 ? pp.u : pp.v) + pp.a;
-  const double s = 0.5 * fmax(cm, cp);
+  if (ROE) {
+    double dq[4], rho, u, v, H, a;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dq[c] = qm[c] - qp[c];
+    if (!roe_avg(sqrt(pm.rho), pm.u, pm.v, pm.H, sqrt(pp.rho), pp.u, pp.v, pp.H, gamma, rho, u, v, H, a)) bad = true;
+    roe_abs_apply(dir, gamma, rho, u, v, H, a, dq, dis);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dis[c] *= 0.5;
+  } else {
+    const double cm = fabs(dir == 0 ? pm.u : pm.v) + pm.a;
+    const double cp = fabs(dir == 0 ? pp.u : pp.v) + pp.a;
+    const double sc = 0.5 * fmax(cm, cp);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) dis[c] = sc * (qm[c] - qp[c]);
+  }
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    const double full = 0.5 * (fm[c] + fp[c]) + s * (qm[c] - qp[c]);
+    const double full = 0.5 * (fm[c] + fp[c]) + dis[c];
     f[c] = mode == 1 ? full - lin[c] : full;
   }
+}
+
+// frozen data per node: (u, v, H, a) for LF, (u, v, H, sqrt(rho)) for Roe
+template <bool ROE>
+__device__ __forceinline__ void frozen_of(const double q[4], double gamma, double fv[4]) {
+  const Prim pr = prim_of(q, gamma);
+  fv[0] = pr.u;
+  fv[1] = pr.v;
+  fv[2] = pr.H;
+  fv[3] = ROE ? sqrt(pr.rho) : pr.a;
 }
 
 
@@ -173,7 +245,7 @@ __device__ __forceinline__ void load_node(const double* sx, const double* su, in
 
 // Computes the operator for every node of a tile; result per thread in out[4]
 // (valid when the thread maps to a node of the tile).
-template <int NP>
+template <int NP, bool ROE>
 __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, int e0, int te, const double* x, double xs,
                                         double* sx, double* su, double* sf, double out[4], bool& bad) {
   constexpr int NN = NP * NP;
@@ -255,8 +327,8 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, int e0, int 
     const int node2 = j * NP + (owner ? 0 : N);
     double q2[4], u2[4], f[4];
     load_node<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
-    if (owner) face_flux(mode, 0, P.gamma, q, q2, ut, u2, f, bad);
-    else face_flux(mode, 0, P.gamma, q2, q, u2, ut, f, bad);
+    if (owner) face_flux<ROE>(mode, 0, P.gamma, q, q2, ut, u2, f, bad);
+    else face_flux<ROE>(mode, 0, P.gamma, q2, q, u2, ut, f, bad);
     // half edge length of the owner element (uniform breaks along y)
     const double fw = 0.5 * hy * P.w[j];
 #pragma unroll
@@ -269,8 +341,8 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, int e0, int 
     const int node2 = (owner ? 0 : N) * NP + i;
     double q2[4], u2[4], f[4];
     load_node<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
-    if (owner) face_flux(mode, 1, P.gamma, q, q2, ut, u2, f, bad);
-    else face_flux(mode, 1, P.gamma, q2, q, u2, ut, f, bad);
+    if (owner) face_flux<ROE>(mode, 1, P.gamma, q, q2, ut, u2, f, bad);
+    else face_flux<ROE>(mode, 1, P.gamma, q2, q, u2, ut, f, bad);
     const double fw = 0.5 * hx * P.w[i];
 #pragma unroll
     for (int c = 0; c < 4; ++c) r[c] = owner ? r[c] - fw * f[c] : r[c] + fw * f[c];
@@ -281,7 +353,7 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, int e0, int 
   for (int c = 0; c < 4; ++c) out[c] = r[c] * im;
 }
 
-template <int NP>
+template <int NP, bool ROE>
 __global__ void __launch_bounds__(256) k_e2_apply(E2P<NP> P, int mode, const double* __restrict__ x,
                                                   double* __restrict__ y, PhiState* st, double* frozen) {
   constexpr int NN = NP * NP, TE = E2Tile<NP>::TE;
@@ -295,7 +367,7 @@ __global__ void __launch_bounds__(256) k_e2_apply(E2P<NP> P, int mode, const dou
     const int te = ne - e0 < TE ? ne - e0 : TE;
     __syncthreads();
     double out[4];
-    e2_tile<NP>(P, mode, e0, te, x, 1.0, sx, su, sf, out, bad);
+    e2_tile<NP, ROE>(P, mode, e0, te, x, 1.0, sx, su, sf, out, bad);
     const int t = threadIdx.x, le = t / NN, node = t % NN;
     if (le < te) {
       const int e = e0 + le;
@@ -306,8 +378,8 @@ __global__ void __launch_bounds__(256) k_e2_apply(E2P<NP> P, int mode, const dou
         double qn[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) qn[c] = x[((size_t)e * 4 + c) * NN + node];
-        const Prim pr = prim_of(qn, P.gamma);
-        const double fv[4] = {pr.u, pr.v, pr.H, pr.a};
+        double fv[4];
+        frozen_of<ROE>(qn, P.gamma, fv);
 #pragma unroll
         for (int c = 0; c < 4; ++c) frozen[((size_t)e * 4 + c) * NN + node] = fv[c];
       }
@@ -317,7 +389,7 @@ __global__ void __launch_bounds__(256) k_e2_apply(E2P<NP> P, int mode, const dou
 }
 
 // phi-cycle apply: y = dt (L s_j V_j + aug) into slot j+1, ||y||^2 -> red_nrmA
-template <int NP>
+template <int NP, bool ROE>
 __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
   constexpr int NN = NP * NP, TE = E2Tile<NP>::TE;
   __shared__ double sx[E2Tile<NP>::VALS], su[E2Tile<NP>::VALS], sf[2 * E2Tile<NP>::VALS];
@@ -352,7 +424,7 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
     const int te = ne - e0 < TE ? ne - e0 : TE;
     __syncthreads();
     double out[4];
-    e2_tile<NP>(P, 0, e0, te, x, xs, sx, su, sf, out, bad);
+    e2_tile<NP, ROE>(P, 0, e0, te, x, xs, sx, su, sf, out, bad);
     const int t = threadIdx.x, le = t / NN, node = t % NN;
     __syncthreads();
     if (le < te) {
@@ -400,7 +472,7 @@ struct E2Strip {
   static constexpr int SMEM = (NBUF * BUFD + 2 * W * BLK) * 8;  // ring + sf
 };
 
-template <int NP>
+template <int NP, bool ROE>
 __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st, double* base, double* partials,
                                                          BArgs b) {
   using S = E2Strip<NP>;
@@ -551,8 +623,8 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
               q2[c] = cur[pos * BLK + c * NN + node2] * xs;
               u2[c] = cur[S::ROWD + pos * BLK + c * NN + node2];
             }
-            if (owner) face_flux(0, 0, P.gamma, qv, q2, tv, u2, f, bad);
-            else face_flux(0, 0, P.gamma, q2, qv, u2, tv, f, bad);
+            if (owner) face_flux<ROE>(0, 0, P.gamma, qv, q2, tv, u2, f, bad);
+            else face_flux<ROE>(0, 0, P.gamma, q2, qv, u2, tv, f, bad);
             const double fw = 0.5 * hy * P.w[j];
 #pragma unroll
             for (int c = 0; c < 4; ++c) rr[c] = owner ? rr[c] - fw * f[c] : rr[c] + fw * f[c];
@@ -567,8 +639,8 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
               q2[c] = nb[(le + 1) * BLK + c * NN + node2] * xs;
               u2[c] = nb[S::ROWD + (le + 1) * BLK + c * NN + node2];
             }
-            if (owner) face_flux(0, 1, P.gamma, qv, q2, tv, u2, f, bad);
-            else face_flux(0, 1, P.gamma, q2, qv, u2, tv, f, bad);
+            if (owner) face_flux<ROE>(0, 1, P.gamma, qv, q2, tv, u2, f, bad);
+            else face_flux<ROE>(0, 1, P.gamma, q2, qv, u2, tv, f, bad);
             const double fw = 0.5 * hx * P.w[i];
 #pragma unroll
             for (int c = 0; c < 4; ++c) rr[c] = owner ? rr[c] - fw * f[c] : rr[c] + fw * f[c];
@@ -613,8 +685,9 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
   grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
 }
 
-// (u, v, H, a) of q~ per node (proj/src/euler.cpp:15-24): the frozen data of
-// the linearised operator, 32 B/node like q~ itself.
+// (u, v, H, a | sqrt(rho)) of q~ per node (proj/src/euler.cpp:15-24): the frozen
+// data of the linearised operator, 32 B/node like q~ itself.
+template <bool ROE>
 __global__ void k_e2_freeze(const double* __restrict__ q, long long nelem, int nn, double gamma,
                             double* __restrict__ frozen) {
   const long long nodes = nelem * nn;
@@ -624,8 +697,8 @@ __global__ void k_e2_freeze(const double* __restrict__ q, long long nelem, int n
     const int node = (int)(g - e * nn);
     double qn[4];
     for (int c = 0; c < 4; ++c) qn[c] = q[(e * 4 + c) * nn + node];
-    const Prim pr = prim_of(qn, gamma);
-    const double fv[4] = {pr.u, pr.v, pr.H, pr.a};
+    double fv[4];
+    frozen_of<ROE>(qn, gamma, fv);
     for (int c = 0; c < 4; ++c) frozen[(e * 4 + c) * nn + node] = fv[c];
   }
 }
@@ -640,13 +713,15 @@ class Euler2D : public OpDevice {
   double* frozen = nullptr;
   double* hbuf = nullptr;
   bool use_strip = true;
+  bool roe = false;
   ~Euler2D() override {
     cudaFree(frozen);
     cudaFree(hbuf);
   }
   void freeze(cudaStream_t s, const double* r) override {
     ref = r;
-    k_e2_freeze<<<1184, 256, 0, s>>>(r, (long long)P.nx * P.ny, NP * NP, P.gamma, frozen);
+    if (roe) k_e2_freeze<true><<<1184, 256, 0, s>>>(r, (long long)P.nx * P.ny, NP * NP, P.gamma, frozen);
+    else k_e2_freeze<false><<<1184, 256, 0, s>>>(r, (long long)P.nx * P.ny, NP * NP, P.gamma, frozen);
   }
   explicit Euler2D(const expdg_op_desc& d) {
     desc = d;
@@ -670,7 +745,10 @@ class Euler2D : public OpDevice {
     comps = 4;
     EXPDG_CUDA(cudaMalloc(&frozen, sizeof(double) * n));
     use_strip = !(std::getenv("EXPDG_E2_TILE") && std::getenv("EXPDG_E2_TILE")[0] == '1');
-    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    roe = d.euler_flux == 0;
+    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    E2Strip<NP>::SMEM));
+    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     E2Strip<NP>::SMEM));
     const long long ntiles = ((long long)d.nx * d.ny + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
@@ -682,21 +760,25 @@ class Euler2D : public OpDevice {
       using SS = E2Strip<NP>;
       const int units = ((P.nx + SS::W - 1) / SS::W) * ((P.ny + SS::ROWS_PER_UNIT - 1) / SS::ROWS_PER_UNIT);
       const int g = std::max(1, std::min(units, 2 * 148));
-      k_e2_phi_strip<NP><<<g, 288, SS::SMEM, s>>>(p, st, base, partials, b);
+      if (roe) k_e2_phi_strip<NP, true><<<g, 288, SS::SMEM, s>>>(p, st, base, partials, b);
+      else k_e2_phi_strip<NP, false><<<g, 288, SS::SMEM, s>>>(p, st, base, partials, b);
     } else {
-      k_e2_phi<NP><<<grid, 256, 0, s>>>(p, st, base, partials, b);
+      if (roe) k_e2_phi<NP, true><<<grid, 256, 0, s>>>(p, st, base, partials, b);
+      else k_e2_phi<NP, false><<<grid, 256, 0, s>>>(p, st, base, partials, b);
     }
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
     E2P<NP> p = P;
     p.ut = frozen;
-    k_e2_apply<NP><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
+    if (roe) k_e2_apply<NP, true><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
+    else k_e2_apply<NP, false><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
   }
   // R = full rhs(u) and, as a side product, the frozen primitives of u (ref = u)
   void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
     E2P<NP> p = P;
     p.ut = nullptr;
-    k_e2_apply<NP><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
+    if (roe) k_e2_apply<NP, true><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
+    else k_e2_apply<NP, false><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
   }
 };
 

@@ -27,4 +27,5 @@ def oracle_problem(spec):
     import oracle
     return oracle.Problem(spec.kind, spec.order, spec.nx, spec.ny, spec.nz, box=spec.box, periodic=spec.periodic,
                           kappa=spec.kappa, flux=spec.flux, sigma=spec.sigma, sigma_adaptive=spec.sigma_adaptive,
-                          gamma=spec.gamma, euler_flux=spec.euler_flux)
+                          gamma=spec.gamma, euler_flux=spec.euler_flux,
+                          over_integrate=spec.over_integrate)

@@ -125,3 +125,22 @@ def test_source_function_matches_weak_load(ctx, over_integrate):
     x = to_dev(u0)
     ya, yb = to_host(a.full_rhs(x)), to_host(b.full_rhs(x))
     assert np.linalg.norm(ya - yb) <= 1e-13 * np.linalg.norm(ya)
+
+
+def test_criterion_8_vortex_orders_roe(ctx):
+    # proj/test_output.txt:25 — euler-vortex (harness default flux = Roe), exprb42,
+    # ne {256, 1024}, dt 0.01, t 1: k=1 rho order 1.725; k=2 2.709 (err 1.486e-05); k=3 3.781
+    want = {1: "1.725", 2: "2.709", 3: "3.781"}
+    for k in (1, 2, 3):
+        errs = []
+        for ne in (256, 1024):
+            nx = int(round(math.sqrt(ne)))
+            u0 = oracle.harness_u0("euler-vortex", ne, k)
+            op = pkg.Operator(ctx, pkg.OperatorSpec("euler2d", k, nx, nx, box=(0.0, 10.0, -5.0, 5.0, 0, 1),
+                                                    euler_flux="roe"))
+            r = pkg.integrate(ctx, op, to_dev(u0), "exprb42", 0.01, 1.0, **KRYLOV)
+            assert r.status == "completed" and r.steps == 100
+            errs.append(oracle.l2_error_exact("euler-vortex", ne, k, to_host(r.u), 1.0, 0))
+        assert f"{math.log2(errs[0] / errs[1]):.3f}" == want[k]
+        if k == 2:
+            assert f"{errs[1]:.3e}" == "1.486e-05"

@@ -1,4 +1,4 @@
-"""GPU parity: 2D Euler Lax-Friedrichs split operator (proj/src/euler.cpp) vs the oracle."""
+"""GPU parity: 2D Euler split operator, Lax-Friedrichs and Roe fluxes (proj/src/euler.cpp), vs the oracle."""
 import numpy as np
 import pytest
 
@@ -28,6 +28,7 @@ def random_state(rng, ne, np_):
     return q
 
 
+@pytest.mark.parametrize("flux", ["lf", "roe"])
 @pytest.mark.parametrize("order,nx,ny,box", [
     (1, 3, 3, (0, 10, -5, 5, 0, 1)),
     (2, 4, 3, (0, 10, -5, 5, 0, 1)),
@@ -36,9 +37,9 @@ def random_state(rng, ne, np_):
     (4, 33, 2, (0, 10, 0, 10, 0, 1)),
     (7, 3, 4, (0, 3, 1, 2, 0, 1)),
 ])
-def test_apply_matches_oracle(ctx, order, nx, ny, box):
+def test_apply_matches_oracle(ctx, order, nx, ny, box, flux):
     rng = np.random.default_rng(order * 100 + nx)
-    spec = pkg.OperatorSpec("euler2d", order, nx, ny, box=box, euler_flux="lf")
+    spec = pkg.OperatorSpec("euler2d", order, nx, ny, box=box, euler_flux=flux)
     op = pkg.Operator(ctx, spec)
     orc = oracle_problem(spec)
     npe = (order + 1) ** 2
@@ -51,9 +52,10 @@ def test_apply_matches_oracle(ctx, order, nx, ny, box):
     assert rel(to_host(op.full_rhs(to_dev(q))), orc.full_rhs(q)) < 1e-12
 
 
-def test_uniform_flow_is_steady(ctx):
+@pytest.mark.parametrize("flux", ["lf", "roe"])
+def test_uniform_flow_is_steady(ctx, flux):
     # proj/tests/test_euler.cpp:225-239
-    spec = pkg.OperatorSpec("euler2d", 2, 4, 4, box=(0, 10, -5, 5, 0, 1), euler_flux="lf")
+    spec = pkg.OperatorSpec("euler2d", 2, 4, 4, box=(0, 10, -5, 5, 0, 1), euler_flux=flux)
     op = pkg.Operator(ctx, spec)
     mean = np.array([1.0, 0.2, 0.0, 1.0 / 0.4 + 0.5 * 0.04])
     q = np.concatenate([np.repeat(mean[c], 9) for c in range(4)] * 16)
@@ -70,7 +72,7 @@ def test_inadmissible_reference_is_domain_error(ctx):
     with pytest.raises(ArithmeticError):
         op.linearize(to_dev(q))
     with pytest.raises(pkg.UnsupportedError):
-        pkg.Operator(ctx, pkg.OperatorSpec("euler2d", 2, 2, 2, euler_flux="roe"))
+        pkg.Operator(ctx, pkg.OperatorSpec("euler3d", 2, 2, 2, 2, euler_flux="roe"))
 
 
 @pytest.mark.parametrize("nx", [16, 32])
@@ -100,3 +102,23 @@ def test_inadmissible_state_blows_up_like_reference(ctx):
     r = pkg.integrate(ctx, op, to_dev(q), "epi2", 0.01, 0.05, tol=1e-10, max_basis=20, orth_length=20)
     orc = oracle_problem(spec).integrate("epi2", q, 0.01, 0.05, tol=1e-10, max_basis=20, orth_length=20)
     assert r.status == orc.status == "blew_up" and r.blow_up_step == orc.blow_up_step == 1
+
+
+@pytest.mark.parametrize("integ", ["epi2", "exprb42"])
+def test_roe_vortex_parity(ctx, integ):
+    # the harness default flux (EulerConfig{} = Roe, proj/src/harness.cpp:62-66) on the
+    # strength-5 C4 vortex, reduced mesh
+    w = configs.scaled(configs.C4, 12, steps=3)
+    spec = w.spec()
+    spec.euler_flux = "roe"
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    orc = oracle_problem(spec).integrate(integ, u0, dt, w.steps * dt, **kw)
+    op = pkg.Operator(ctx, spec)
+    r = pkg.integrate(ctx, op, to_dev(u0), integ, dt, w.steps * dt, **kw)
+    assert r.status == orc.status == "completed"
+    assert rel(to_host(r.u), orc.u) <= 1e-9
+    d_dev = np.diff(np.concatenate([[0], r.iters_per_step]))
+    d_orc = np.diff(np.concatenate([[0], orc.iters_per_step]))
+    assert np.max(np.abs(d_dev - d_orc)) <= 2
