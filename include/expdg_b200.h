@@ -68,6 +68,11 @@ typedef struct {
   int over_integrate;  /* 1D Burgers: Gauss rule of (3k+3)/2 points + consistent mass (proj/src/burgers.cpp:39-51) */
   double gamma;        /* Euler */
   int euler_flux;      /* 0 roe (2D only, proj/src/euler.cpp:114-145), 1 lax_friedrichs */
+  /* Slab partition (0, 0 = the whole mesh): this rank owns the element
+   * rows [part_begin, part_end) of a 2D Euler mesh.  The global mesh stays nx x ny; the
+   * operator's state holds only the owned rows and exchanges one halo row with its
+   * periodic neighbours (rank -+ 1) through the context's communicator. */
+  int part_begin, part_end;
 } expdg_op_desc;
 
 /* KrylovSettings (proj/include/expdg/integrators.hpp:20-24) + the two
@@ -114,6 +119,23 @@ int expdg_ctx_create(int device, expdg_ctx** out);
 int expdg_ctx_destroy(expdg_ctx* ctx);
 void* expdg_ctx_stream(expdg_ctx* ctx);
 int expdg_ctx_synchronize(expdg_ctx* ctx);
+
+/* Multi-GPU (slab partition, one process per GPU): the reference is single-threaded
+ * and has no distributed layer; these add the two collectives the partitioned path
+ * needs (sum/max allreduce of the reduced Gram-Schmidt dots and norms, neighbour
+ * halo exchange).  Attach the communicator before creating partitioned operators;
+ * a context with a communicator runs its control host-stepped.
+ *   NCCL: rank 0 calls expdg_nccl_unique_id, broadcasts the 128 bytes, every rank
+ *         calls expdg_ctx_attach_nccl (collective, like ncclCommInitRank).
+ *   Local group: several ranks driven by threads of one process (host-staged
+ *         exchange; single-GPU tests of the partitioned algorithm). */
+typedef struct expdg_local_group expdg_local_group;
+int expdg_nccl_unique_id(unsigned char out[128]);
+int expdg_ctx_attach_nccl(expdg_ctx* ctx, const unsigned char unique_id[128], int rank, int size);
+int expdg_local_group_create(int size, expdg_local_group** out);
+int expdg_local_group_destroy(expdg_local_group* g);
+int expdg_ctx_attach_local(expdg_ctx* ctx, expdg_local_group* g, int rank);
+int expdg_ctx_comm(const expdg_ctx* ctx, int* rank, int* size); /* 0, 1 without a communicator */
 
 /* Operator factory: replaces BurgersOperator / EulerOperator construction
  * (proj/src/burgers.cpp:20-93, proj/src/euler.cpp:186-244) minus the frozen

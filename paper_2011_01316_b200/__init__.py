@@ -51,6 +51,7 @@ class OpDesc(C.Structure):
         ("z0", C.c_double), ("z1", C.c_double), ("periodic", C.c_int), ("kappa", C.c_double),
         ("flux", C.c_int), ("sigma", C.c_double), ("sigma_adaptive", C.c_int),
         ("over_integrate", C.c_int), ("gamma", C.c_double), ("euler_flux", C.c_int),
+        ("part_begin", C.c_int), ("part_end", C.c_int),
     ]
 
 
@@ -81,7 +82,8 @@ EXPORTS = [
     "expdg_step_epi2", "expdg_integrate", "expdg_integrate_host", "expdg_lgl_basis",
     "expdg_initial_condition", "expdg_ctx_kernel_launches", "expdg_ctx_last_loop_ms", "expdg_expm",
     "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts", "expdg_op_set_source",
-    "expdg_op_set_source_fn",
+    "expdg_op_set_source_fn", "expdg_nccl_unique_id", "expdg_ctx_attach_nccl", "expdg_local_group_create",
+    "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm",
 ]
 
 _lib = None
@@ -136,6 +138,12 @@ def lib():
     L.expdg_ctx_traffic.argtypes = [vp, dp]
     L.expdg_bench_ts.argtypes = [vp, C.c_longlong, C.c_int, C.c_int, C.c_int, dp]
     L.expdg_initial_condition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, dp]
+    L.expdg_nccl_unique_id.argtypes = [C.c_char_p]
+    L.expdg_ctx_attach_nccl.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
+    L.expdg_local_group_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.expdg_local_group_destroy.argtypes = [vp]
+    L.expdg_ctx_attach_local.argtypes = [vp, vp, C.c_int]
+    L.expdg_ctx_comm.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     _lib = L
     return L
 
@@ -250,6 +258,48 @@ class Context:
     def synchronize(self):
         _check(lib().expdg_ctx_synchronize(self.h))
 
+    # ---- multi-GPU slab partition
+    def attach_nccl(self, unique_id: bytes, rank: int, size: int):
+        """Collective over the `size` ranks (ncclCommInitRank); unique_id from nccl_unique_id()."""
+        _check(lib().expdg_ctx_attach_nccl(self.h, bytes(unique_id), rank, size))
+        return self
+
+    def attach_local(self, group: "LocalGroup", rank: int):
+        """Rank `rank` of a host-staged group driven by threads of this process."""
+        self._group = group  # keep the group alive as long as the context
+        _check(lib().expdg_ctx_attach_local(self.h, group.h, rank))
+        return self
+
+    @property
+    def comm(self) -> tuple:
+        r, n = C.c_int(), C.c_int()
+        _check(lib().expdg_ctx_comm(self.h, C.byref(r), C.byref(n)))
+        return r.value, n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().expdg_nccl_unique_id(buf))
+    return buf.raw
+
+
+class LocalGroup:
+    """Host-staged communicator group for several ranks in one process (single-GPU tests)."""
+
+    def __init__(self, size: int):
+        h = C.c_void_p()
+        _check(lib().expdg_local_group_create(size, C.byref(h)))
+        self.h = h
+        self.size = size
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().expdg_local_group_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
 
 @dataclass
 class OperatorSpec:
@@ -267,6 +317,7 @@ class OperatorSpec:
     over_integrate: bool = False
     gamma: float = 1.4
     euler_flux: str = "lf"
+    part: tuple = (0, 0)  # owned element rows [begin, end) of a slab-partitioned 2D Euler mesh
 
     def desc(self) -> OpDesc:
         d = OpDesc()
@@ -277,6 +328,7 @@ class OperatorSpec:
         d.kappa, d.flux, d.sigma = self.kappa, (1 if self.flux in ("ef", "entropy") else 0), self.sigma
         d.sigma_adaptive, d.over_integrate = int(self.sigma_adaptive), int(self.over_integrate)
         d.gamma, d.euler_flux = self.gamma, (0 if self.euler_flux == "roe" else 1)
+        d.part_begin, d.part_end = self.part
         return d
 
     @property

@@ -40,8 +40,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OUT, exist_ok=True)
     objs = []
 
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+    newest_header = max((os.path.getmtime(h) for h in headers), default=0.0)
+
     def compile_one(src):
         obj = os.path.join(OUT, os.path.basename(src) + ".o")
+        if (not force and os.path.exists(obj) and os.path.getmtime(obj) > os.path.getmtime(src)
+                and os.path.getmtime(obj) > newest_header):
+            return obj
         cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, *FLAGS, "-x", "c++", "-c", src, "-o", obj]

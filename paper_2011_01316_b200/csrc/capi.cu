@@ -15,6 +15,7 @@ void launch_step_begin(cudaStream_t s, PhiState* st, const double* dt_seq);
 void launch_step_finish(cudaStream_t s, PhiState* st, double* u, const double* w, int mode, StepRecord* rec,
                         double* partials, int grid);
 void launch_absmax(cudaStream_t s, const double* u, long long n, double* out2, int grid);
+void launch_step_decide(cudaStream_t s, PhiState* st, StepRecord* rec);
 void launch_phi_config(cudaStream_t s, PhiState* st, const double* dt_seq, int p, double mult, int mmax,
                        int full_orth, int window, int grow_cap);
 void launch_vec_add(cudaStream_t s, const PhiState* st, double* out, const double* u, const double* w, long long n);
@@ -34,7 +35,12 @@ struct KrylovFailure : std::runtime_error {
 
 using namespace expdg;
 
+struct expdg_local_group {
+  std::shared_ptr<LocalGroup> g;
+};
+
 struct expdg_ctx {
+  std::unique_ptr<Comm> comm;  // declared before eng: destroyed after it
   std::unique_ptr<Engine> eng;
   long long launches = 0;
   double last_loop_ms = 0.0;
@@ -104,6 +110,12 @@ void validate_desc(const expdg_op_desc& d) {
       throw Unsupported("over-integrated 2D Burgers is not on the device path");
   } else {
     if (!d.periodic) throw std::invalid_argument("EulerOperator: periodic boundaries only");
+    if (d.part_end > d.part_begin) {
+      if (d.kind != EXPDG_EULER2D) throw Unsupported("slab partition: 2D Euler only");
+      if (d.part_begin < 0 || d.part_end > d.ny) throw std::invalid_argument("slab partition: rows out of range");
+    } else if (d.part_begin != 0 || d.part_end != 0) {
+      throw std::invalid_argument("slab partition: empty row range");
+    }
     if (d.euler_flux != 1 && d.kind == EXPDG_EULER3D)
       throw Unsupported("3D Euler: Lax-Friedrichs flux only (the Roe flux is 2D, proj/src/euler.cpp:114-145)");
   }
@@ -158,10 +170,59 @@ int expdg_ctx_synchronize(expdg_ctx* ctx) {
 long long expdg_ctx_kernel_launches(expdg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 double expdg_ctx_last_loop_ms(expdg_ctx* ctx) { return ctx ? ctx->last_loop_ms : 0.0; }
 
+int expdg_nccl_unique_id(unsigned char out[128]) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null argument");
+    nccl_unique_id(out);
+  });
+}
+
+int expdg_ctx_attach_nccl(expdg_ctx* ctx, const unsigned char unique_id[128], int rank, int size) {
+  return guard([&] {
+    if (!ctx || !unique_id) throw std::invalid_argument("null argument");
+    if (ctx->comm) throw std::invalid_argument("context already has a communicator");
+    EXPDG_CUDA(cudaSetDevice(ctx->eng->device));
+    ctx->comm = make_nccl_comm(unique_id, rank, size);
+    ctx->eng->comm = ctx->comm.get();
+  });
+}
+
+int expdg_local_group_create(int size, expdg_local_group** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null argument");
+    auto g = std::make_unique<expdg_local_group>();
+    g->g = make_local_group(size);
+    *out = g.release();
+  });
+}
+
+int expdg_local_group_destroy(expdg_local_group* g) {
+  return guard([&] { delete g; });
+}
+
+int expdg_ctx_attach_local(expdg_ctx* ctx, expdg_local_group* g, int rank) {
+  return guard([&] {
+    if (!ctx || !g) throw std::invalid_argument("null argument");
+    if (ctx->comm) throw std::invalid_argument("context already has a communicator");
+    ctx->comm = make_local_comm(g->g, rank);
+    ctx->eng->comm = ctx->comm.get();
+  });
+}
+
+int expdg_ctx_comm(const expdg_ctx* ctx, int* rank, int* size) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null argument");
+    if (rank) *rank = ctx->comm ? ctx->comm->rank : 0;
+    if (size) *size = ctx->comm ? ctx->comm->size : 1;
+  });
+}
+
 int expdg_op_create(expdg_ctx* ctx, const expdg_op_desc* desc, expdg_op** out) {
   return guard([&] {
     if (!ctx || !desc) throw std::invalid_argument("null argument");
     validate_desc(*desc);
+    if (desc->part_end > desc->part_begin && !ctx->comm)
+      throw std::invalid_argument("partitioned operator: attach a communicator to the context first");
     EXPDG_CUDA(cudaSetDevice(ctx->eng->device));
     auto op = std::make_unique<expdg_op>();
     op->ctx = ctx;
@@ -171,6 +232,7 @@ int expdg_op_create(expdg_ctx* ctx, const expdg_op_desc* desc, expdg_op** out) {
       case EXPDG_EULER2D: op->dev = make_euler2d(*desc); break;
       case EXPDG_EULER3D: op->dev = make_euler3d(*desc); break;
     }
+    op->dev->comm = ctx->comm.get();
     *out = op.release();
   });
 }
@@ -195,11 +257,25 @@ int expdg_op_destroy(expdg_op* op) {
 
 long long expdg_op_dim(const expdg_op* op) { return op ? op->dev->n : 0; }
 
+// op_check_ref, max-reduced over the ranks of a partitioned operator (every rank
+// then throws or proceeds to the collective freeze together)
+static int check_ref(expdg_op* op, cudaStream_t s, const double* ref) {
+  int chk = op_check_ref(*op->dev, s, ref);
+  if (op->dev->partitioned()) {
+    int* d = reinterpret_cast<int*>(op->ctx->work2);
+    EXPDG_CUDA(cudaMemcpyAsync(d, &chk, sizeof(int), cudaMemcpyHostToDevice, s));
+    op->ctx->comm->allreduce(d, d, 1, COMM_I32, COMM_MAX, s);
+    EXPDG_CUDA(cudaMemcpyAsync(&chk, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+    EXPDG_CUDA(cudaStreamSynchronize(s));
+  }
+  return chk;
+}
+
 int expdg_op_linearize(expdg_op* op, const double* ref_dev) {
   return guard([&] {
     if (!op || !ref_dev) throw std::invalid_argument("null argument");
     cudaStream_t s = op->ctx->eng->stream;
-    const int chk = op_check_ref(*op->dev, s, ref_dev);
+    const int chk = check_ref(op, s, ref_dev);
     if (chk == 1) throw std::invalid_argument("reference state not finite");
     if (chk == 2) throw std::domain_error("EulerOperator: inadmissible reference state");
     if (!op->ref_owned) EXPDG_CUDA(cudaMalloc(&op->ref_owned, sizeof(double) * op->dev->n));
@@ -383,8 +459,18 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   EXPDG_CUDA(cudaStreamSynchronize(e.stream));
   double max0 = 0.0;
   for (int i = 0; i < rgrid; ++i) max0 = std::max(max0, h2[2 * i]);
+  // partitioned: max over ranks (host value staged through a device double)
+  auto global_max = [&](double v) {
+    if (!e.comm) return v;
+    EXPDG_CUDA(cudaMemcpyAsync(ctx->work2, &v, sizeof(double), cudaMemcpyHostToDevice, e.stream));
+    e.comm->allreduce(ctx->work2, ctx->work2, 1, COMM_F64, COMM_MAX, e.stream);
+    EXPDG_CUDA(cudaMemcpyAsync(&v, ctx->work2, sizeof(double), cudaMemcpyDeviceToHost, e.stream));
+    EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+    return v;
+  };
+  max0 = global_max(max0);
   if (kind == EXPDG_EXP_EULER) {
-    const int chk = op_check_ref(dev, e.stream, u);
+    const int chk = (int)global_max((double)op_check_ref(dev, e.stream, u));
     if (chk == 2) throw std::domain_error("EulerOperator: inadmissible reference state");
     EXPDG_CUDA(cudaMemcpyAsync(refbuf, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, e.stream));
   }
@@ -419,6 +505,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
       dev.launch_apply(s, 1, u, rbuf);  // N(u) at the frozen u0 (proj/src/integrators.cpp:71)
     } else {
       dev.launch_residual(s, u, rbuf, e.st, e.partials);  // R = L u + N u at u~ = u
+      if (e.comm) e.comm->allreduce(&e.st->domain_flag, &e.st->domain_flag, 1, COMM_I32, COMM_MAX, s);
       if (exprb) {
         dev.launch_apply(s, 1, u, nu);
         launch_phi_config(s, e.st, dts_dev, 1, mult1, c1.mmax, c1.full_orth, c1.window, c1.grow_cap);
@@ -436,12 +523,16 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   const int fgrid = std::min(2048, std::max(1, (int)std::min<long long>(e.num_sms * 4, (n + 255) / 256)));
   auto post = [&](cudaStream_t s) {
     launch_step_finish(s, e.st, u, e.slot(0), kind == EXPDG_EXP_EULER ? 1 : 0, rec_dev, e.partials, fgrid);
+    if (e.comm) {  // blow-up test on the max over ranks
+      e.comm->allreduce(e.st->mx, e.st->mx, 2, COMM_F64, COMM_MAX, s);
+      launch_step_decide(s, e.st, rec_dev);
+    }
   };
   (void)vgrid;
-  const int per_step = exprb ? 13 : 5;
+  const int per_step = (exprb ? 13 : 5) + (e.comm ? 1 : 0);
   const int body_k = dev.fused_dots() ? 5 : 6;
   cudaGraphExec_t ex = nullptr;
-  const bool graph = cfg->use_graph != 0;
+  const bool graph = cfg->use_graph != 0 && !e.comm;  // partitioned: host-stepped control
   int launched = 0;
 
   // Adds a WHILE node after the current capture position; returns its body graph.

@@ -56,10 +56,10 @@ enum PhiStatus : int {
 struct PhiState {
   // ---- configuration (host-written at call setup)
   long long n;       // local head length
-  long long len;     // n + p on the rank holding the tail, else n
+  long long len;     // n + p (the p-scalar tail is replicated on every rank)
   long long ld;      // slot stride
   int p;
-  int tail_here;
+  int tail_here;     // this rank counts the tail in reductions (rank 0)
   double dt;
   double tol;
   int mmax, window, grow_cap, max_substeps, full_orth, initial_basis;
@@ -71,13 +71,26 @@ struct PhiState {
   int substeps;          // this call
   int cycles;
   double beta, avnorm, t, h, last_estimate, pre_norm;
-  // ---- reduced results of the last kernels (raw sums over the local rank)
-  double red_nrmA;  // ||y||^2 after the operator
-  double red_nrmC;  // ||y||^2 after pass C
-  double red_w2;    // ||w_head||^2 after combine / init
-  double red_dotA[kMaxSlots];
-  double red_dotB[kMaxSlots];
-  double bnorm2[kMaxP + 1];
+  // ---- reduced results of the last kernels.  Single rank: the kernels' grid
+  // reductions land in `red` directly.  Slab-partitioned (multi = 1): they land
+  // in `loc` (this rank's partial sums) and the host enqueues a sum-allreduce
+  // loc -> red after every reducing kernel (idempotent when a kernel no-ops).
+  struct Red {
+    double nrmA;  // ||y||^2 after the operator
+    double nrmC;  // ||y||^2 after pass C
+    double w2;    // ||w_head||^2 after combine / init
+    double dotA[kMaxSlots];
+    double dotB[kMaxSlots];
+    double bnorm2[kMaxP + 1];
+  };
+  Red red;
+  Red loc;
+  int multi;
+  int pad_multi;
+  double mx[2];  // per-step max reductions (max|u|, non-finite flag), allreduced in place
+#ifdef __CUDACC__
+  __device__ __forceinline__ Red& rs() { return multi ? loc : red; }
+#endif
   // ---- per-slot scale and combine coefficients
   double scale[kMaxSlots];
   double comb[kMaxSlots];

@@ -17,6 +17,7 @@
 // instead of 2(k+1) sequential ones.  IOP windows use one pass (reference: one
 // MGS pass over the window).
 #include <algorithm>
+#include <cstddef>
 #include <cstdlib>
 #include <cstring>
 
@@ -50,7 +51,7 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
   extern __shared__ __align__(128) double smem[];
   __shared__ uint64_t full[kTsMaxStages], empty[kTsMaxStages];
   __shared__ int s_active, s_i0, s_k, s_y, s_T, s_S;
-  __shared__ long long s_ld, s_n;
+  __shared__ long long s_ld, s_n, s_ndot;
   __shared__ double s_coef[kMaxSlots];
   __shared__ double s_red[kMaxSlots + 1];
   __shared__ double s_buf[kTsBlock / 32];
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
     S = S > max_stages ? max_stages : S;
     s_active = active; s_i0 = i0; s_k = k; s_y = y; s_T = T; s_S = S;
     s_ld = st->ld; s_n = st->n;
+    s_ndot = st->tail_here ? st->ld : st->n;  // the replicated tail counts on rank 0 only
     if (active) {
       for (int q = 0; q < S; ++q) {
         mbar_init(&full[q], 1);
@@ -92,14 +94,14 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
   __syncthreads();
   if (!s_active) return;
   const int i0 = s_i0, k = s_k, T = s_T, S = s_S;
-  const long long ld = s_ld, n = s_n;
+  const long long ld = s_ld, n = s_n, ndot = s_ndot;
   for (int i = tid; i < k; i += blockDim.x) {
     const int slot = i0 + i;
     const double sc = st->scale[slot];
     double c;
     if (MODE == TS_DOTS) c = 0.0;
-    else if (MODE == TS_UPD_DOTS) c = sc * sc * st->red_dotA[slot];
-    else if (MODE == TS_UPD_NORM) c = sc * sc * (st->full_orth ? st->red_dotB[slot] : st->red_dotA[slot]);
+    else if (MODE == TS_UPD_DOTS) c = sc * sc * st->red.dotA[slot];
+    else if (MODE == TS_UPD_NORM) c = sc * sc * (st->full_orth ? st->red.dotB[slot] : st->red.dotA[slot]);
     else c = sc * st->comb[slot];
     s_coef[i] = c;
   }
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
           const double yv = y0 + y1;
           Y[d] = yv;
           ybase[g0 + d] = yv;
-          if (MODE == TS_UPD_NORM) nacc = fma(yv, yv, nacc);
+          if (MODE == TS_UPD_NORM && g0 + d < ndot) nacc = fma(yv, yv, nacc);
         }
         if (MODE == TS_UPD_DOTS) consumer_sync();
       } else if (MODE == TS_COMBINE) {
@@ -170,9 +172,10 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
         // y chunk of 512 cached in registers (lane owns d = c0 + lane + 32 m)
         for (int c0 = 0; c0 < T; c0 += kTsChunk) {
           const int per = min(T - c0, kTsChunk) >> 5;  // T >= 32
+          const long long lim = ndot - g0 - c0 - lane;
           double yr[kTsChunk / 32];
 #pragma unroll
-          for (int m = 0; m < kTsChunk / 32; ++m) yr[m] = m < per ? Y[c0 + lane + 32 * m] : 0.0;
+          for (int m = 0; m < kTsChunk / 32; ++m) yr[m] = (m < per && 32 * m < lim) ? Y[c0 + lane + 32 * m] : 0.0;
 #pragma unroll
           for (int v = 0; v < kAccPerLane; ++v) {
             const int i = wid + 8 * v;
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
       if (wid < kTsConsumers / 32 && i < k && lane == 0) s_red[i] = r;
     }
     __syncthreads();
-    double* dst = MODE == TS_DOTS ? st->red_dotA : st->red_dotB;
+    double* dst = MODE == TS_DOTS ? st->rs().dotA : st->rs().dotB;
     grid_reduce_last(s_red, k, partials, kMaxSlots, &st->ticket[MODE == TS_DOTS ? TK_DOTS : TK_UPD_DOTS],
                      [&](int i, double v) { dst[i0 + i] = v; });
   } else {
@@ -214,8 +217,8 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
     __syncthreads();
     grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[MODE == TS_COMBINE ? TK_COMBINE : TK_UPD_NORM],
                      [&](int, double v) {
-                       if (MODE == TS_COMBINE) st->red_w2 = v;
-                       else st->red_nrmC = v;
+                       if (MODE == TS_COMBINE) st->rs().w2 = v;
+                       else st->rs().nrmC = v;
                      });
   }
 }
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(256) k_phi_init(PhiState* st, double* slot0, B
         acc[i] = fma(v, v, acc[i]);
       }
   }
-  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here)
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad)
     slot0[n + threadIdx.x] = (b.p > 0 && (int)threadIdx.x == b.p - 1) ? 1.0 : 0.0;
 #pragma unroll
   for (int i = 0; i <= kMaxP; ++i) {
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(256) k_phi_init(PhiState* st, double* slot0, B
   }
   __syncthreads();
   grid_reduce_last(s_red, kMaxP + 1, partials, kMaxSlots, &st->ticket[TK_INIT], [&](int i, double v) {
-    st->bnorm2[i] = v;
+    st->rs().bnorm2[i] = v;
   });
 }
 
@@ -466,8 +469,8 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
           const int j = st->j;
           const double* sc = st->scale;
           for (int i = st->j0; i <= j; ++i) {
-            const double h1 = sc[i] * st->red_dotA[i];
-            const double h2 = st->full_orth ? sc[i] * st->red_dotB[i] : 0.0;
+            const double h1 = sc[i] * st->red.dotA[i];
+            const double h2 = st->full_orth ? sc[i] * st->red.dotB[i] : 0.0;
             st->H[i * kMaxBasis + j] = st->full_orth ? (h1 + h2) : h1;
           }
           {
@@ -475,8 +478,8 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
             st->alg_bytes += 32.0 * nd + 8.0 * nd * (st->full_orth ? 3.0 * kk + 6.0 : 2.0 * kk + 4.0);
             st->extend_cols++;
           }
-          const double pre_norm = sqrt(st->red_nrmA);
-          const double hnext = sqrt(st->red_nrmC);
+          const double pre_norm = sqrt(st->red.nrmA);
+          const double hnext = sqrt(st->red.nrmC);
           st->pre_norm = pre_norm;
           st->H[(j + 1) * kMaxBasis + j] = hnext;
           const int mc = j + 1;
@@ -501,17 +504,16 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
         case ACT_AVNORM:
           st->alg_bytes += 32.0 * (double)st->n;
           st->avnorms++;
-          st->avnorm = sqrt(st->red_nrmA);
+          st->avnorm = sqrt(st->red.nrmA);
           phase = PH_DECIDE;
           break;
         case ACT_COMBINE: {
           st->alg_bytes += 8.0 * (double)st->n * (double)(st->mc + 1);
           st->combines++;
-          double w2 = st->red_w2;
-          if (st->tail_here)
-            for (int j = 0; j < st->p; ++j) slot0[st->n + j] = st->tailw[j];
+          double w2 = st->red.w2;
+          for (int j = 0; j < st->p; ++j) slot0[st->n + j] = st->tailw[j];  // replicated tail
           for (int j = 0; j < st->p; ++j) w2 += st->tailw[j] * st->tailw[j];
-          st->red_w2 = w2;
+          st->red.w2 = w2;
           phase = st->t < 1.0 - 1e-14 ? PH_SUBSTEP : PH_DONE;
           break;
         }
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
           st->status = PHI_ERR_BUDGET;
           s_phase = PH_DONE;
         } else {
-          const double beta = sqrt(st->red_w2);
+          const double beta = sqrt(st->red.w2);
           if (beta == 0.0) {
             s_phase = PH_DONE;
           } else if (!isfinite(beta)) {
@@ -656,7 +658,7 @@ __global__ void k_phi_start(PhiState* st) {
     return;
   }
   int any = 0;
-  for (int i = 0; i <= st->p; ++i) any |= st->bnorm2[i] > 0.0;
+  for (int i = 0; i <= st->p; ++i) any |= st->red.bnorm2[i] > 0.0;
   st->any_b = any;
   st->iterations = 0;
   st->substeps = 0;
@@ -667,7 +669,9 @@ __global__ void k_phi_start(PhiState* st) {
   st->mc = 0;
   st->breakdown = 0;
   st->last_estimate = 0.0;
-  st->red_w2 = st->bnorm2[0] + (st->p > 0 ? 1.0 : 0.0);
+  st->red.w2 = st->red.bnorm2[0] + (st->p > 0 ? 1.0 : 0.0);
+  // partitioned: the body's allreduces rebuild red from loc before the controller reads it
+  if (st->multi) st->loc.w2 = st->loc.bnorm2[0] + ((st->p > 0 && st->tail_here) ? 1.0 : 0.0);
   for (int j = 0; j < kMaxP; ++j) st->tailw[j] = (j == st->p - 1) ? 1.0 : 0.0;
   if (st->domain_flag) {
     st->status = PHI_ERR_DOMAIN;
@@ -762,7 +766,8 @@ PhiState Engine::config(long long n, int p, double dt, const expdg_krylov_cfg& k
   std::memset(&c, 0, sizeof(c));
   c.n = n;
   c.p = p;
-  c.tail_here = 1;
+  c.tail_here = comm ? (comm->rank == 0 ? 1 : 0) : 1;
+  c.multi = comm ? 1 : 0;
   c.len = n + p;
   c.ld = ld;
   c.dt = dt;
@@ -786,9 +791,18 @@ void Engine::upload_config(const PhiState& c, cudaStream_t s) {
   EXPDG_CUDA(cudaMemcpyAsync(st, st_host, sizeof(PhiState), cudaMemcpyHostToDevice, s));
 }
 
+void Engine::reduce(cudaStream_t s) {
+  if (!comm) return;
+  constexpr long long cnt = sizeof(PhiState::Red) / sizeof(double);
+  const char* p = reinterpret_cast<const char*>(st);
+  comm->allreduce(p + offsetof(PhiState, loc), const_cast<char*>(p) + offsetof(PhiState, red), cnt, COMM_F64,
+                  COMM_SUM, s);
+}
+
 void Engine::launch_phi_init(cudaStream_t s, const BArgs& b) {
   const int grid = num_sms * 2;
   k_phi_init<<<grid, 256, 0, s>>>(st, slot(0), b, partials);
+  reduce(s);
   k_phi_start<<<1, 1, 0, s>>>(st);
 }
 
@@ -812,10 +826,17 @@ void Engine::launch_ts(cudaStream_t s, int mode) {
 void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
                          int use_graph) {
   op.launch_phi_apply(s, st, base, partials, b);
-  if (!op.fused_dots()) launch_ts(s, TS_DOTS);
+  reduce(s);
+  if (!op.fused_dots()) {
+    launch_ts(s, TS_DOTS);
+    reduce(s);
+  }
   launch_ts(s, TS_UPD_DOTS);
+  reduce(s);
   launch_ts(s, TS_UPD_NORM);
+  reduce(s);
   launch_ts(s, TS_COMBINE);
+  reduce(s);
   k_ctl<<<1, 256, 0, s>>>(st, slot(0), ework, h, use_graph);
 }
 
@@ -837,8 +858,8 @@ double Engine::bench_ts(long long n, int k, int mode, int reps) {
   c.mc = k;
   for (int i = 0; i < kMaxSlots; ++i) {
     c.scale[i] = 1.0;
-    c.red_dotA[i] = 1e-3;
-    c.red_dotB[i] = 1e-3;
+    c.red.dotA[i] = 1e-3;
+    c.red.dotB[i] = 1e-3;
     c.comb[i] = 1e-3;
   }
   upload_config(c, stream);
@@ -859,7 +880,7 @@ double Engine::bench_ts(long long n, int k, int mode, int reps) {
 }
 
 void Engine::run_phi(OpDevice& op, const BArgs& b, int use_graph) {
-  if (use_graph) {
+  if (use_graph && !comm) {
     cudaGraphExec_t ex = build_phi_graph(op, b);
     EXPDG_CUDA(cudaGraphLaunch(ex, stream));
     EXPDG_CUDA(cudaStreamSynchronize(stream));

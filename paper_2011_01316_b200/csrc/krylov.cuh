@@ -5,6 +5,7 @@
 #include <memory>
 #include <vector>
 
+#include "comm.cuh"
 #include "expdg_internal.cuh"
 
 namespace expdg {
@@ -23,12 +24,16 @@ class OpDevice {
   long long n = 0;        // local DOF count
   int comps = 1;
   const double* ref = nullptr;  // ũ (device), not owned
+  // Slab-partitioned operators (desc.part_end > desc.part_begin) hold only their
+  // element rows and exchange one halo row per application through `comm`.
+  Comm* comm = nullptr;
+  bool partitioned() const { return desc.part_end > desc.part_begin; }
   // Cycle apply: y = dt * aug(s_j V_j) into slot j+1 plus ||y||^2 (action EXTEND/AVNORM).
   virtual void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials,
                                 const BArgs& b) = 0;
   // Standalone: which 0 = L x (at ref), 1 = N x (at ref), 2 = full rhs (no ref).
   virtual void launch_apply(cudaStream_t s, int which, const double* x, double* y) = 0;
-  // Step residual R = L u + N u at ref = u, with ||R||^2 -> st->bnorm2[1] and the
+  // Step residual R = L u + N u at ref = u, with ||R||^2 -> st->red.bnorm2[1] and the
   // inadmissibility flag -> st->domain_flag.  Skipped when st->stopped.
   virtual void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st,
                                double* partials) = 0;
@@ -75,6 +80,11 @@ class Engine {
  public:
   TsTuning ts_tuning;
   int ld_odd = 1;
+  // Set when the context belongs to a slab-partitioned group: every reducing
+  // kernel is followed by a sum-allreduce of PhiState::loc -> PhiState::red,
+  // and the control runs host-stepped (no CUDA graphs).
+  Comm* comm = nullptr;
+  void reduce(cudaStream_t s);
   explicit Engine(int device);
   ~Engine();
   int device = 0;

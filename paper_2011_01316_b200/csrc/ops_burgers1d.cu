@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kB1Threads) k_b1_phi(B1P<NP> P, PhiState* st, 
       s_dt = st->dt;
       s_ld = st->ld;
       const double* xslot = base + (size_t)s_j * st->ld;
-      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[P.n + i] * s_xs : 0.0;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
     }
   }
   __syncthreads();
@@ -123,16 +123,17 @@ __global__ void __launch_bounds__(kB1Threads) k_b1_phi(B1P<NP> P, PhiState* st, 
       nacc = fma(v, v, nacc);
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here) {
+  // the p-scalar tail is replicated on every rank; rank 0 counts it
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad) {
     const int i = threadIdx.x;
     const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
     y[P.n + i] = v;
-    nacc = fma(v, v, nacc);
+    if (st->tail_here) nacc = fma(v, v, nacc);
   }
   const double tot = block_sum(nacc, s_buf);
   if (threadIdx.x == 0) s_red[0] = tot;
   __syncthreads();
-  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
 template <int NP>
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(kB1Threads) k_b1oi_phi(B1OP<NP, NQ> P, PhiStat
       s_dt = st->dt;
       s_ld = st->ld;
       const double* xslot = base + (size_t)s_j * st->ld;
-      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[P.n + i] * s_xs : 0.0;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
     }
   }
   __syncthreads();
@@ -296,16 +297,17 @@ __global__ void __launch_bounds__(kB1Threads) k_b1oi_phi(B1OP<NP, NQ> P, PhiStat
       nacc = fma(v, v, nacc);
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here) {
+  // the p-scalar tail is replicated on every rank; rank 0 counts it
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad) {
     const int i = threadIdx.x;
     const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
     y[P.n + i] = v;
-    nacc = fma(v, v, nacc);
+    if (st->tail_here) nacc = fma(v, v, nacc);
   }
   const double tot = block_sum(nacc, s_buf);
   if (threadIdx.x == 0) s_red[0] = tot;
   __syncthreads();
-  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
 template <int NP, int NQ>
@@ -375,7 +377,7 @@ __global__ void k_dense_apply(int n, const double* __restrict__ A, const double*
   if (lane == 0) y[row] = s;
 }
 
-// y = dt (A s_j V_j + aug) into slot j+1, ||y||^2 -> red_nrmA (single CTA, test sizes)
+// y = dt (A s_j V_j + aug) into slot j+1, ||y||^2 -> red.nrmA (single CTA, test sizes)
 __global__ void k_dense_phi(int n, const double* __restrict__ A, PhiState* st, double* base, BArgs b) {
   __shared__ double s_buf[32];
   __shared__ double s_xt[kMaxP];
@@ -411,7 +413,7 @@ __global__ void k_dense_phi(int n, const double* __restrict__ A, PhiState* st, d
     nacc = fma(v, v, nacc);
   }
   const double tot = block_sum(nacc, s_buf);
-  if (threadIdx.x == 0) st->red_nrmA = tot;
+  if (threadIdx.x == 0) st->rs().nrmA = tot;
 }
 
 class DenseOp : public OpDevice {

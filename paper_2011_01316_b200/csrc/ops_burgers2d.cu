@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(256) k_b2_phi(B1P<NP> Px, B1P<NP> Py, int nx, 
       s_dt = st->dt;
       s_ld = st->ld;
       const double* xslot = base + (size_t)s_j * st->ld;
-      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[Px.n + i] * s_xs : 0.0;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[Px.n + i] * s_xs : 0.0;
     }
   }
   __syncthreads();
@@ -142,16 +142,17 @@ __global__ void __launch_bounds__(256) k_b2_phi(B1P<NP> Px, B1P<NP> Py, int nx, 
     }
     __syncthreads();
   }
-  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here) {
+  // the p-scalar tail is replicated on every rank; rank 0 counts it
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad) {
     const int i = threadIdx.x;
     const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
     y[Px.n + i] = v;
-    nacc = fma(v, v, nacc);
+    if (st->tail_here) nacc = fma(v, v, nacc);
   }
   const double tot = block_sum(nacc, s_buf);
   if (threadIdx.x == 0) s_red[0] = tot;
   __syncthreads();
-  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
 template <int NP>

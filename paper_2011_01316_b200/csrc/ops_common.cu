@@ -42,6 +42,7 @@ int op_check_ref(OpDevice& op, cudaStream_t s, const double* ref) {
   if (d.kind == EXPDG_BURGERS2D) { np = np1 * np1; ne = (long long)d.nx * d.ny; }
   if (d.kind == EXPDG_EULER2D) { np = np1 * np1; ne = (long long)d.nx * d.ny; comps = 4; edim = 2; }
   if (d.kind == EXPDG_EULER3D) { np = np1 * np1 * np1; ne = (long long)d.nx * d.ny * d.nz; comps = 5; edim = 3; }
+  ne = op.n / ((long long)comps * np);  // the owned elements (slab-partitioned operators)
   k_check_ref<<<592, 256, 0, s>>>(ref, ne, comps, np, edim, flag);
   int h = 0;
   EXPDG_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));

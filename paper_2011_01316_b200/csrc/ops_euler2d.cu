@@ -30,6 +30,13 @@ struct E2P {
   const double* hx;    // element widths per column (uniform breakpoints, proj/src/mesh.cpp:11-16)
   const double* hy;    // element heights per row
   long long n;
+  // slab partition: rows -1 and ny are the neighbours' halo rows (raw values of the
+  // applied vector / the frozen primitives), exchanged before the kernel runs
+  int part;
+  const double* gx_lo;
+  const double* gx_hi;
+  const double* gt_lo;
+  const double* gt_hi;
 };
 
 struct Prim {
@@ -336,11 +343,22 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, int e0, int 
   }
   if (j == N || j == 0) {
     const bool owner = j == N;
-    const int je2 = owner ? (je + 1 == P.ny ? 0 : je + 1) : (je == 0 ? P.ny - 1 : je - 1);
-    const int e2 = je2 * P.nx + ie;
+    const int jn = owner ? je + 1 : je - 1;
     const int node2 = (owner ? 0 : N) * NP + i;
     double q2[4], u2[4], f[4];
-    load_node<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
+    if (P.part && (jn < 0 || jn >= P.ny)) {  // halo row of the neighbouring rank
+      const double* gx = jn < 0 ? P.gx_lo : P.gx_hi;
+      const double* gt = jn < 0 ? P.gt_lo : P.gt_hi;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const size_t g = ((size_t)ie * 4 + c) * NN + node2;
+        q2[c] = gx[g] * xs;
+        u2[c] = need_ut ? gt[g] : 0.0;
+      }
+    } else {
+      const int je2 = jn < 0 ? P.ny - 1 : (jn >= P.ny ? 0 : jn);
+      load_node<NP>(sx, su, e0, te, je2 * P.nx + ie, node2, x, xs, P.ut, q2, u2, need_ut);
+    }
     if (owner) face_flux<ROE>(mode, 1, P.gamma, q, q2, ut, u2, f, bad);
     else face_flux<ROE>(mode, 1, P.gamma, q2, q, u2, ut, f, bad);
     const double fw = 0.5 * hx * P.w[i];
@@ -388,7 +406,7 @@ __global__ void __launch_bounds__(256) k_e2_apply(E2P<NP> P, int mode, const dou
   if (bad && st) st->domain_flag = 1;
 }
 
-// phi-cycle apply: y = dt (L s_j V_j + aug) into slot j+1, ||y||^2 -> red_nrmA
+// phi-cycle apply: y = dt (L s_j V_j + aug) into slot j+1, ||y||^2 -> red.nrmA
 template <int NP, bool ROE>
 __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
   constexpr int NN = NP * NP, TE = E2Tile<NP>::TE;
@@ -407,7 +425,7 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
       s_dt = st->dt;
       s_ld = st->ld;
       const double* xslot = base + (size_t)s_j * st->ld;
-      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[P.n + i] * s_xs : 0.0;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
     }
   }
   __syncthreads();
@@ -442,16 +460,17 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
       nacc = fma(v, v, nacc);
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x < kTailPad && st->tail_here) {
+  // the p-scalar tail is replicated on every rank; rank 0 counts it
+  if (blockIdx.x == 0 && threadIdx.x < kTailPad) {
     const int i = threadIdx.x;
     const double v = (i + 1 < b.p) ? dt * s_xt[i + 1] : 0.0;
     y[P.n + i] = v;
-    nacc = fma(v, v, nacc);
+    if (st->tail_here) nacc = fma(v, v, nacc);
   }
   const double tot = block_sum(nacc, s_buf);
   if (threadIdx.x == 0) s_red[0] = tot;
   __syncthreads();
-  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
 // ---------------------------------------------------------------- 2.5D strip JVP (phi cycle)
@@ -496,7 +515,7 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
       s_dt = st->dt;
       s_ld = st->ld;
       const double* xslot = base + (size_t)s_j * st->ld;
-      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p && st->tail_here) ? xslot[P.n + i] * s_xs : 0.0;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
       for (int q = 0; q < NBUF; ++q) {
         mbar_init(&full[q], 1);
         mbar_init(&empty[q], 1);
@@ -527,7 +546,15 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
         const int r0 = chunk * S::ROWS_PER_UNIT, r1 = min(ny, r0 + S::ROWS_PER_UNIT);
         for (int q = 0; q < r1 - r0 + 2; ++q) {
           int row = r0 - 1 + q;
-          row = row < 0 ? row + ny : (row >= ny ? row - ny : row);
+          const double* srcx = x;
+          const double* srct = P.ut;
+          if (P.part && (row < 0 || row >= ny)) {  // halo row of the neighbouring rank
+            srcx = row < 0 ? P.gx_lo : P.gx_hi;
+            srct = row < 0 ? P.gt_lo : P.gt_hi;
+            row = 0;
+          } else {
+            row = row < 0 ? row + ny : (row >= ny ? row - ny : row);
+          }
           const int sl = (int)(seq % NBUF);
           const int use = (int)(seq / NBUF);
           mbar_wait(&empty[sl], (use & 1) ^ 1);
@@ -536,10 +563,11 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
           const bool with_b = b1 && q >= 1 && q <= r1 - r0;  // only the computed rows need b_1
           mbar_arrive_expect_tx(&full[sl], 2u * (uint32_t)(w + 2) * eb + (with_b ? (uint32_t)w * eb : 0u));
           const size_t rbase = (size_t)row * nx;
+          const size_t brbase = (size_t)(r0 - 1 + q) * nx;  // b_1 rows are always owned rows
           const int left = ie0 == 0 ? nx - 1 : ie0 - 1;
           const int right = ie0 + w == nx ? 0 : ie0 + w;
           for (int arr = 0; arr < 2; ++arr) {
-            const double* src = arr == 0 ? x : P.ut;
+            const double* src = arr == 0 ? srcx : srct;
             double* d = dst + arr * S::ROWD;
             if (ie0 >= 1 && ie0 + w < nx) {
               bulk_g2s(d, src + (rbase + left) * BLK, (uint32_t)(w + 2) * eb, &full[sl]);
@@ -549,7 +577,7 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
               bulk_g2s(d + (size_t)(w + 1) * BLK, src + (rbase + right) * BLK, eb, &full[sl]);
             }
           }
-          if (with_b) bulk_g2s(dst + 2 * S::ROWD, b1 + (rbase + ie0) * BLK, (uint32_t)w * eb, &full[sl]);
+          if (with_b) bulk_g2s(dst + 2 * S::ROWD, b1 + (brbase + ie0) * BLK, (uint32_t)w * eb, &full[sl]);
           ++seq;
         }
       }
@@ -674,15 +702,15 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
     }
   }
   __syncthreads();
-  if (blockIdx.x == 0 && tid < kTailPad && st->tail_here) {
+  if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
     const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
     y[P.n + tid] = v;
-    nacc = fma(v, v, nacc);
+    if (st->tail_here) nacc = fma(v, v, nacc);
   }
   const double tot = block_sum(nacc, s_buf);
   if (tid == 0) s_red[0] = tot;
   __syncthreads();
-  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->red_nrmA = v; });
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
 // (u, v, H, a | sqrt(rho)) of q~ per node (proj/src/euler.cpp:15-24): the frozen
@@ -703,6 +731,20 @@ __global__ void k_e2_freeze(const double* __restrict__ q, long long nelem, int n
   }
 }
 
+// First / last owned element row of Krylov slot j (the vector the next phi-cycle
+// apply reads) into the halo send buffers; no-op unless this cycle applies the operator.
+__global__ void k_e2_pack_rows(const PhiState* st, const double* base, long long rowd, long long last,
+                               double* __restrict__ lo, double* __restrict__ hi) {
+  const int a = st->action;
+  if (st->stopped || !(a == ACT_EXTEND || a == ACT_AVNORM)) return;
+  const double* x = base + (size_t)st->j * st->ld;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rowd; i += stride) {
+    lo[i] = x[i];
+    hi[i] = x[last + i];
+  }
+}
+
 double ubreak(double a, double b, int i, int n) { return i == n ? b : a + (b - a) * i / n; }
 
 template <int NP>
@@ -714,24 +756,55 @@ class Euler2D : public OpDevice {
   double* hbuf = nullptr;
   bool use_strip = true;
   bool roe = false;
+  // slab partition: halo rows (x lo/hi, frozen lo/hi) and send staging (lo/hi)
+  double* halo = nullptr;
+  long long rowd = 0;  // doubles per element row
   ~Euler2D() override {
     cudaFree(frozen);
     cudaFree(hbuf);
+    cudaFree(halo);
+  }
+  double* hx_lo() const { return halo; }
+  double* hx_hi() const { return halo + rowd; }
+  double* ht_lo() const { return halo + 2 * rowd; }
+  double* ht_hi() const { return halo + 3 * rowd; }
+  double* sb_lo() const { return halo + 4 * rowd; }
+  double* sb_hi() const { return halo + 5 * rowd; }
+  // neighbour rows of a state-layout vector v -> (lo, hi) halo buffers
+  void exchange(cudaStream_t s, const double* v, double* lo, double* hi) {
+    comm->halo(v, v + (size_t)(P.ny - 1) * rowd, lo, hi, rowd, s);
+  }
+  E2P<NP> params(const double* ut) const {
+    E2P<NP> p = P;
+    p.ut = ut;
+    if (p.part) {
+      p.gx_lo = hx_lo();
+      p.gx_hi = hx_hi();
+      p.gt_lo = ht_lo();
+      p.gt_hi = ht_hi();
+    }
+    return p;
   }
   void freeze(cudaStream_t s, const double* r) override {
     ref = r;
     if (roe) k_e2_freeze<true><<<1184, 256, 0, s>>>(r, (long long)P.nx * P.ny, NP * NP, P.gamma, frozen);
     else k_e2_freeze<false><<<1184, 256, 0, s>>>(r, (long long)P.nx * P.ny, NP * NP, P.gamma, frozen);
+    if (P.part) exchange(s, frozen, ht_lo(), ht_hi());
   }
   explicit Euler2D(const expdg_op_desc& d) {
     desc = d;
     const HostBasis hb = host_lgl_basis(d.order);
+    const bool part = d.part_end > d.part_begin;
+    const int row0 = part ? d.part_begin : 0;
+    const int nyl = part ? d.part_end - d.part_begin : d.ny;
     P.nx = d.nx;
-    P.ny = d.ny;
+    P.ny = nyl;
+    P.part = part ? 1 : 0;
     P.gamma = d.gamma;
-    std::vector<double> hs(d.nx + d.ny);
+    std::vector<double> hs(d.nx + nyl);
     for (int i = 0; i < d.nx; ++i) hs[i] = ubreak(d.x0, d.x1, i + 1, d.nx) - ubreak(d.x0, d.x1, i, d.nx);
-    for (int j = 0; j < d.ny; ++j) hs[d.nx + j] = ubreak(d.y0, d.y1, j + 1, d.ny) - ubreak(d.y0, d.y1, j, d.ny);
+    for (int j = 0; j < nyl; ++j)
+      hs[d.nx + j] = ubreak(d.y0, d.y1, row0 + j + 1, d.ny) - ubreak(d.y0, d.y1, row0 + j, d.ny);
     EXPDG_CUDA(cudaMalloc(&hbuf, sizeof(double) * hs.size()));
     EXPDG_CUDA(cudaMemcpy(hbuf, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice));
     P.hx = hbuf;
@@ -740,22 +813,30 @@ class Euler2D : public OpDevice {
       P.w[a] = hb.weights[a];
       for (int b2 = 0; b2 < NP; ++b2) P.WD[a * NP + b2] = hb.weights[a] * hb.D[a * NP + b2];
     }
-    n = (long long)d.nx * d.ny * NP * NP * 4;
+    n = (long long)d.nx * nyl * NP * NP * 4;
     P.n = n;
     comps = 4;
+    rowd = (long long)d.nx * NP * NP * 4;
     EXPDG_CUDA(cudaMalloc(&frozen, sizeof(double) * n));
+    if (part) {
+      EXPDG_CUDA(cudaMalloc(&halo, sizeof(double) * 6 * rowd));
+      EXPDG_CUDA(cudaMemset(halo, 0, sizeof(double) * 6 * rowd));
+    }
     use_strip = !(std::getenv("EXPDG_E2_TILE") && std::getenv("EXPDG_E2_TILE")[0] == '1');
     roe = d.euler_flux == 0;
     EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     E2Strip<NP>::SMEM));
     EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     E2Strip<NP>::SMEM));
-    const long long ntiles = ((long long)d.nx * d.ny + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
+    const long long ntiles = ((long long)d.nx * nyl + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
   }
   void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
-    E2P<NP> p = P;
-    p.ut = frozen;
+    if (P.part) {  // halo rows of the slot this cycle applies the operator to
+      k_e2_pack_rows<<<296, 256, 0, s>>>(st, base, rowd, (long long)(P.ny - 1) * rowd, sb_lo(), sb_hi());
+      comm->halo(sb_lo(), sb_hi(), hx_lo(), hx_hi(), rowd, s);
+    }
+    const E2P<NP> p = params(frozen);
     if (use_strip) {
       using SS = E2Strip<NP>;
       const int units = ((P.nx + SS::W - 1) / SS::W) * ((P.ny + SS::ROWS_PER_UNIT - 1) / SS::ROWS_PER_UNIT);
@@ -768,17 +849,18 @@ class Euler2D : public OpDevice {
     }
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
-    E2P<NP> p = P;
-    p.ut = frozen;
+    if (P.part) exchange(s, x, hx_lo(), hx_hi());
+    const E2P<NP> p = params(frozen);
     if (roe) k_e2_apply<NP, true><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
     else k_e2_apply<NP, false><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
   }
   // R = full rhs(u) and, as a side product, the frozen primitives of u (ref = u)
   void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
-    E2P<NP> p = P;
-    p.ut = nullptr;
+    if (P.part) exchange(s, u, hx_lo(), hx_hi());
+    const E2P<NP> p = params(nullptr);
     if (roe) k_e2_apply<NP, true><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
     else k_e2_apply<NP, false><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
+    if (P.part) exchange(s, frozen, ht_lo(), ht_hi());  // frozen halo for this step's JVPs
   }
 };
 

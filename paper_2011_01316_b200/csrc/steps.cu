@@ -43,6 +43,30 @@ __global__ void k_exprb_d2(const PhiState* st, const double* dt_seq, double* d, 
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) d[i] = f * (a[i] - b[i]);
 }
 
+__device__ void step_decide(PhiState* st, StepRecord* rec, double mx, double bad) {
+  const int step = st->step;
+  const bool failed = st->step_failed || st->status != PHI_OK;
+  const double am = bad > 0.0 ? INFINITY : mx;
+  st->alg_bytes += 40.0 * (double)st->n;
+  StepRecord r;
+  r.dt = st->dt;
+  r.t = 0.0;
+  r.amax = am;
+  r.iterations_cum = st->iterations_total;
+  r.substeps = st->substeps;
+  r.phi_status = st->status;
+  r.pad = 0;
+  if (failed || !isfinite(am) || am > st->blow_up_scale) {
+    r.status = 1;
+    st->stopped = 1;
+  } else {
+    r.status = 0;
+  }
+  rec[step] = r;
+  st->step = step + 1;
+  if (st->step >= st->max_steps) st->stopped = 1;
+}
+
 // mode 0 (EPI2): u <- u + w ; mode 1 (exp_euler): u <- w.  Then max|u|, finiteness,
 // blow-up test against 1e10 (1 + max|u0|) (proj/src/integrators.cpp:149, :186-193).
 __global__ void __launch_bounds__(256) k_step_finish(PhiState* st, double* u, const double* w, int mode,
@@ -86,28 +110,19 @@ __global__ void __launch_bounds__(256) k_step_finish(PhiState* st, double* u, co
       bad = fmax(bad, __ldcg(&partials[(size_t)b * kMaxSlots + 1]));
     }
     st->ticket[7] = 0u;
-    const int step = st->step;
-    const bool failed = st->step_failed || st->status != PHI_OK;
-    const double am = bad > 0.0 ? INFINITY : mx;
-    st->alg_bytes += 40.0 * (double)st->n;
-    StepRecord r;
-    r.dt = st->dt;
-    r.t = 0.0;
-    r.amax = am;
-    r.iterations_cum = st->iterations_total;
-    r.substeps = st->substeps;
-    r.phi_status = st->status;
-    r.pad = 0;
-    if (failed || !isfinite(am) || am > st->blow_up_scale) {
-      r.status = 1;
-      st->stopped = 1;
+    if (st->multi) {  // partitioned: max-allreduce of st->mx, then k_step_decide
+      st->mx[0] = mx;
+      st->mx[1] = bad;
     } else {
-      r.status = 0;
+      step_decide(st, rec, mx, bad);
     }
-    rec[step] = r;
-    st->step = step + 1;
-    if (st->step >= st->max_steps) st->stopped = 1;
   }
+}
+
+// The blow-up decision on the (rank-reduced) max|u| and non-finite flag.
+__global__ void k_step_decide(PhiState* st, StepRecord* rec) {
+  if (st->stopped) return;
+  step_decide(st, rec, st->mx[0], st->mx[1]);
 }
 
 // max|u| (and finiteness) of the initial state.
@@ -141,6 +156,7 @@ void launch_exprb_d2(cudaStream_t s, const PhiState* st, const double* dt_seq, d
                      const double* b, double c, long long n) {
   k_exprb_d2<<<1184, 256, 0, s>>>(st, dt_seq, d, a, b, c, n);
 }
+void launch_step_decide(cudaStream_t s, PhiState* st, StepRecord* rec) { k_step_decide<<<1, 1, 0, s>>>(st, rec); }
 void launch_absmax(cudaStream_t s, const double* u, long long n, double* out2, int grid) {
   k_absmax<<<grid, 256, 0, s>>>(u, n, out2);
 }

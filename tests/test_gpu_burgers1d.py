@@ -67,7 +67,7 @@ def test_errors_map_to_reference_exceptions(ctx):
     with pytest.raises(ValueError):
         pkg.Operator(ctx, pkg.OperatorSpec("burgers1d", 4, 8, sigma=-1.0))
     with pytest.raises(pkg.UnsupportedError):
-        pkg.Operator(ctx, pkg.OperatorSpec("burgers1d", 4, 8, over_integrate=True))
+        pkg.Operator(ctx, pkg.OperatorSpec("burgers2d", 4, 8, 8, over_integrate=True))
     op = pkg.Operator(ctx, pkg.OperatorSpec("burgers1d", 4, 8))
     bad = np.zeros(op.dim)
     bad[3] = np.nan

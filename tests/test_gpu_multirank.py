@@ -1,0 +1,141 @@
+"""GPU parity of the slab-partitioned device path.
+
+Several ranks of ONE process share the GPU through a host-staged communicator
+group (expdg_ctx_attach_local): each rank is a host thread with its own context,
+stream and element-row slab; the halo rows and the Gram-Schmidt / norm
+reductions go through host barriers, so no rank's kernel ever waits on another
+rank's kernel on the device.  The partitioned run must reproduce the
+single-rank device run (same algorithm, reductions summed in a different order)
+and the NCCL communicator is exercised at world size 1.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2011_01316_b200 as pkg
+from paper_2011_01316_b200 import configs
+from paper_2011_01316_b200.partition import slab_ranges
+from tests.gpu_util import rel, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(parts, fn):
+    """fn(rank, ctx) on `parts` threads, each with its own context of a local group."""
+    group = pkg.LocalGroup(parts)
+    out, errs = [None] * parts, []
+
+    def body(r):
+        try:
+            ctx = pkg.Context(0).attach_local(group, r)
+            out[r] = fn(r, ctx)
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(parts)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+    return out
+
+
+def slab(spec, rows):
+    blk = spec.nx * (spec.order + 1) ** 2 * 4
+    return slice(rows[0] * blk, rows[1] * blk)
+
+
+@pytest.mark.parametrize("flux", ["lf", "roe"])
+@pytest.mark.parametrize("parts", [2, 3])
+def test_partitioned_operator_matches_single_rank(flux, parts):
+    w = configs.scaled(configs.C4, 9, steps=1)
+    spec = w.spec()
+    spec.euler_flux = flux
+    rng = np.random.default_rng(7)
+    ref = w.initial_condition()
+    x = rng.standard_normal(ref.size)
+    ctx = pkg.Context(0)
+    op = pkg.Operator(ctx, spec)
+    op.linearize(to_dev(ref))
+    want = [to_host(op.apply_linear(to_dev(x))), to_host(op.apply_nonlinear(to_dev(ref))),
+            to_host(op.full_rhs(to_dev(ref)))]
+    ranges = slab_ranges(spec.ny, parts)
+
+    def fn(r, c):
+        s = pkg.OperatorSpec(**{**spec.__dict__, "part": ranges[r]})
+        o = pkg.Operator(c, s)
+        sl = slab(spec, ranges[r])
+        o.linearize(to_dev(ref[sl]))
+        return [to_host(o.apply_linear(to_dev(x[sl]))), to_host(o.apply_nonlinear(to_dev(ref[sl]))),
+                to_host(o.full_rhs(to_dev(ref[sl])))]
+
+    got = run_ranks(parts, fn)
+    for i in range(3):
+        assert rel(np.concatenate([g[i] for g in got]), want[i]) < 1e-14
+
+
+@pytest.mark.parametrize("integ", ["epi2", "exprb42"])
+@pytest.mark.parametrize("parts", [2, 4])
+def test_partitioned_integrate_matches_single_rank(integ, parts):
+    w = configs.scaled(configs.C4, 16, steps=3)
+    spec = w.spec()
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    ctx = pkg.Context(0)
+    single = pkg.integrate(ctx, pkg.Operator(ctx, spec), to_dev(u0), integ, dt, w.steps * dt, **kw)
+    ranges = slab_ranges(spec.ny, parts)
+
+    def fn(r, c):
+        o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": ranges[r]}))
+        res = pkg.integrate(c, o, to_dev(u0[slab(spec, ranges[r])]), integ, dt, w.steps * dt, **kw)
+        return res, to_host(res.u)
+
+    got = run_ranks(parts, fn)
+    assert all(g[0].status == single.status == "completed" for g in got)
+    assert rel(np.concatenate([g[1] for g in got]), to_host(single.u)) <= 1e-11
+    for g in got:  # every rank ran the same control: identical per-step Krylov dimensions
+        assert list(g[0].iters_per_step) == list(got[0][0].iters_per_step)
+    d_part = np.diff(np.concatenate([[0], got[0][0].iters_per_step]))
+    d_single = np.diff(np.concatenate([[0], single.iters_per_step]))
+    assert np.max(np.abs(d_part - d_single)) <= 1
+
+
+def test_nccl_world_size_one_matches_single_rank():
+    w = configs.scaled(configs.C4, 12, steps=2)
+    spec = w.spec()
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    ctx = pkg.Context(0)
+    single = pkg.integrate(ctx, pkg.Operator(ctx, spec), to_dev(u0), "epi2", dt, w.steps * dt, **kw)
+    c = pkg.Context(0).attach_nccl(pkg.nccl_unique_id(), 0, 1)
+    assert c.comm == (0, 1)
+    o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": (0, spec.ny)}))
+    r = pkg.integrate(c, o, to_dev(u0), "epi2", dt, w.steps * dt, **kw)
+    assert r.status == "completed"
+    assert rel(to_host(r.u), to_host(single.u)) <= 1e-12
+    assert list(r.iters_per_step) == list(single.iters_per_step)
+
+
+def test_partitioned_blow_up_is_collective():
+    # an inadmissible state on ONE rank fails the step on every rank (domain flag max-reduced)
+    w = configs.scaled(configs.C4, 8, steps=2)
+    spec = w.spec()
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    ranges = slab_ranges(spec.ny, 2)
+    bad = u0.copy()
+    bad[slab(spec, ranges[1])][0] = -1.0  # negative density on rank 1
+
+    def fn(r, c):
+        o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": ranges[r]}))
+        return pkg.integrate(c, o, to_dev(bad[slab(spec, ranges[r])]), "epi2", dt, 2 * dt, tol=w.tol,
+                             max_basis=40, orth_length=40)
+
+    got = run_ranks(2, fn)
+    assert [g.status for g in got] == ["blew_up", "blew_up"]
+    assert [g.blow_up_step for g in got] == [1, 1]
