@@ -155,6 +155,9 @@ def main():
     ap.add_argument("--cpu-nx", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partition", action="store_true",
+                    help="slab-partitioned NCCL path even at N = 1 (always used for N > 1)")
+    ap.add_argument("--replicas", action="store_true", help="N > 1: independent full-size replicas instead")
     ap.add_argument("--host-control", action="store_true",
                     help="host-stepped controller (same kernels, no graph WHILE nodes): for ncu, which "
                          "cannot profile kernel nodes of graphs with conditional nodes")
@@ -177,7 +180,29 @@ def main():
     w = workload
     u0 = w.initial_condition()
     dt = w.time_step(u0) if w.dt is None else w.dt
-    op = pkg.Operator(ctx, w.spec())
+    spec = w.spec()
+    n_global = u0.size
+    # N > 1: element-row slabs of the one C4 mesh (strong scaling), halo rows and the
+    # Gram-Schmidt / norm sums over NCCL; --partition forces the
+    # partitioned path at N = 1 (NCCL world of one) to exercise it on a single GPU.
+    partitioned = (world > 1 or args.partition) and not args.replicas
+    if partitioned:
+        from paper_2011_01316_b200.partition import slab_ranges
+        if spec.kind != "euler2d":
+            raise SystemExit("the slab-partitioned path is 2D Euler (C4) only")
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            uid = torch.tensor(list(pkg.nccl_unique_id()), dtype=torch.uint8)
+        if world > 1:
+            t_uid = uid.to(f"cuda:{local}")
+            torch.distributed.broadcast(t_uid, 0)
+            uid = t_uid.cpu()
+        ctx.attach_nccl(bytes(uid.tolist()), rank, world)
+        rows = slab_ranges(spec.ny, world)[rank]
+        spec.part = rows
+        blk = spec.nx * (spec.order + 1) ** 2 * 4
+        u0 = u0[rows[0] * blk:rows[1] * blk].copy()
+    op = pkg.Operator(ctx, spec)
     n = op.dim
     kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis, use_graph=not args.host_control)
     u = torch.tensor(u0, device=f"cuda:{local}")
@@ -208,7 +233,8 @@ def main():
         t = torch.tensor([loop_s], device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         loop_s = float(t.item())
-    value = world * n * args.steps / loop_s
+    total_dofs = n_global if partitioned else world * n
+    value = total_dofs * args.steps / loop_s
     peak, peak_kind = hbm_peak()
     achieved = traffic["alg_bytes"] / (r.loop_ms / 1e3) / 1e9
     iters_per_step = np.diff(np.concatenate([[0], r.iters_per_step])) if len(r.iters_per_step) else []
@@ -232,7 +258,7 @@ def main():
             tt = torch.tensor([e_s], device=f"cuda:{local}")
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             e_s = float(tt.item())
-        e2e = {"value": world * n * args.steps / e_s, "unit": "DOF-steps/s", "h2d_bytes_per_step": 8 * n,
+        e2e = {"value": total_dofs * args.steps / e_s, "unit": "DOF-steps/s", "h2d_bytes_per_step": 8 * n,
                "d2h_bytes_per_step": 8 * n, "seconds": e_s}
 
     cpu = None
@@ -247,15 +273,18 @@ def main():
         line = {
             "metric": "DOF-steps/s per exponential-DG step", "value": value, "unit": "DOF-steps/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * loop_s / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1e3 * loop_s / args.steps, "higher_is_better": True,
+            "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded strength-5 isentropic vortex + 1e-6 N(0,1) density noise)",
-            "config": {"workload": w.name, "dofs": n, "elements": f"{w.nx}x{w.ny}", "order": w.order,
+            "config": {"workload": w.name, "dofs": n_global, "dofs_per_rank": n, "elements": f"{w.nx}x{w.ny}",
+                       "order": w.order,
                        "dt": dt, "cr_a": w.cfl, "krylov": {"tol": w.tol, "max_basis": w.max_basis,
                                                            "orth_length": w.max_basis},
                        "integrator": "epi2", "l2": "inputs larger than L2 (Krylov workspace "
                        f"{(w.max_basis + 2) * 8 * n / 1e9:.1f} GB vs 126 MB L2)",
-                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                       "parallelism": (f"{world}-way element-row slabs (NCCL halo + allreduce)" if partitioned
+                                       else "single GPU" if world == 1 else f"{world} independent replicas"),
                        "krylov_iters_per_step": [int(v) for v in iters_per_step]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,

@@ -530,7 +530,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   };
   (void)vgrid;
   const int per_step = (exprb ? 13 : 5) + (e.comm ? 1 : 0);
-  const int body_k = dev.fused_dots() ? 5 : 6;
+  const int body_k = (dev.fused_dots() ? 5 : 6) + (dev.partitioned() ? 1 : 0);  // + halo pack kernel
   cudaGraphExec_t ex = nullptr;
   const bool graph = cfg->use_graph != 0 && !e.comm;  // partitioned: host-stepped control
   int launched = 0;

@@ -168,14 +168,20 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
           if (g0 + d < n) nacc = fma(wv, wv, nacc);
         }
       }
+      if ((MODE == TS_DOTS || MODE == TS_UPD_DOTS) && g0 + T > ndot) {
+        // a non-zero rank's tile holding the replicated phi tail: keep it out of the dots
+        consumer_sync();
+        for (int d = tid; d < T; d += kTsConsumers)
+          if (g0 + d >= ndot) Y[d] = 0.0;
+        consumer_sync();
+      }
       if (MODE == TS_DOTS || MODE == TS_UPD_DOTS) {
         // y chunk of 512 cached in registers (lane owns d = c0 + lane + 32 m)
         for (int c0 = 0; c0 < T; c0 += kTsChunk) {
           const int per = min(T - c0, kTsChunk) >> 5;  // T >= 32
-          const long long lim = ndot - g0 - c0 - lane;
           double yr[kTsChunk / 32];
 #pragma unroll
-          for (int m = 0; m < kTsChunk / 32; ++m) yr[m] = (m < per && 32 * m < lim) ? Y[c0 + lane + 32 * m] : 0.0;
+          for (int m = 0; m < kTsChunk / 32; ++m) yr[m] = m < per ? Y[c0 + lane + 32 * m] : 0.0;
 #pragma unroll
           for (int v = 0; v < kAccPerLane; ++v) {
             const int i = wid + 8 * v;
