@@ -20,7 +20,9 @@
 #include <cstddef>
 #include <stdexcept>
 #include <string>
+#include <array>
 #include <functional>
+#include <utility>
 #include <vector>
 
 #include "expdg_b200.h"
@@ -98,10 +100,27 @@ class Context {
   Context& operator=(const Context&) = delete;
   expdg_ctx* get() const { return h_; }
   void synchronize() { check(expdg_ctx_synchronize(h_)); }
+  // multi-GPU slab partition (one process per GPU): collective over `size` ranks
+  Context& attach_nccl(const std::array<unsigned char, 128>& id, int rank, int size) {
+    check(expdg_ctx_attach_nccl(h_, id.data(), rank, size));
+    return *this;
+  }
+  std::pair<int, int> comm() const {
+    int r = 0, n = 1;
+    check(expdg_ctx_comm(h_, &r, &n));
+    return {r, n};
+  }
 
  private:
   expdg_ctx* h_ = nullptr;
 };
+
+// rank 0 creates the id and broadcasts it (MPI, sockets, torch.distributed ...)
+inline std::array<unsigned char, 128> nccl_unique_id() {
+  std::array<unsigned char, 128> id{};
+  check(expdg_nccl_unique_id(id.data()));
+  return id;
+}
 
 // The split operator (proj/include/expdg/split_operator.hpp:12-20), frozen at
 // the state passed to linearize (device pointer).  linear/nonlinear act on
