@@ -42,8 +42,123 @@ constexpr int kAccPerLane = (kMaxSlots + 7) / 8;
 constexpr int kTsConsumers = 256;
 constexpr int kTsBlock = kTsConsumers + 32;
 constexpr int kTsMaxT = 2048;
-constexpr int kTsChunk = 512;
+constexpr int kTsChunk = 256;  // doubles of y held in registers per dot chunk (128 pairs)
 
+
+// Consumer side of one tall-skinny pass (warps 0-7).  NV = most basis vectors
+// any warp owns in the dots (ceil(k/8)), a compile-time bound so the per-vector
+// accumulators stay in registers without per-chunk checks of all 17 slots.
+template <int MODE, int NV>
+__device__ __forceinline__ void ts_consume(const PhiState* st, double* base, double* smem, uint64_t* full,
+                                           uint64_t* empty, const double* s_coef, int k, int T, int S,
+                                           long long ntiles, long long n, long long ndot, int nst,
+                                           double* ybase, double (&acc)[kAccPerLane], double& nacc) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  int s = 0, use = 0;
+  for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    mbar_wait(&full[s], use & 1);
+    double* V = smem + (size_t)s * nst * T;
+    double* Y = V + (size_t)k * T;
+    const long long g0 = tl * T;
+    // element pairs: one LDS.128 per stream and coefficient pair feeds 4 FMAs
+    const double2* V2 = reinterpret_cast<const double2*>(V);
+    const double2* C2 = reinterpret_cast<const double2*>(s_coef);
+    const int T2 = T >> 1;
+    if (MODE == TS_UPD_DOTS || MODE == TS_UPD_NORM) {
+      for (int p = tid; p < T2; p += kTsConsumers) {
+        const double2 y = reinterpret_cast<const double2*>(Y)[p];
+        double a0 = y.x, a1 = y.y, b0 = 0.0, b1 = 0.0;
+        int i = 0;
+        for (; i + 1 < k; i += 2) {
+          const double2 c = C2[i >> 1];
+          const double2 v0 = V2[(size_t)i * T2 + p];
+          const double2 v1 = V2[(size_t)(i + 1) * T2 + p];
+          a0 = fma(-c.x, v0.x, a0);
+          a1 = fma(-c.x, v0.y, a1);
+          b0 = fma(-c.y, v1.x, b0);
+          b1 = fma(-c.y, v1.y, b1);
+        }
+        if (i < k) {
+          const double c = s_coef[i];
+          const double2 v0 = V2[(size_t)i * T2 + p];
+          a0 = fma(-c, v0.x, a0);
+          a1 = fma(-c, v0.y, a1);
+        }
+        const double2 yv = make_double2(a0 + b0, a1 + b1);
+        reinterpret_cast<double2*>(Y)[p] = yv;
+        reinterpret_cast<double2*>(ybase + g0)[p] = yv;
+        if (MODE == TS_UPD_NORM) {
+          if (g0 + 2 * p < ndot) nacc = fma(yv.x, yv.x, nacc);
+          if (g0 + 2 * p + 1 < ndot) nacc = fma(yv.y, yv.y, nacc);
+        }
+      }
+      if (MODE == TS_UPD_DOTS) consumer_sync();
+    } else if (MODE == TS_COMBINE) {
+      for (int p = tid; p < T2; p += kTsConsumers) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        int i = 0;
+        for (; i + 1 < k; i += 2) {
+          const double2 c = C2[i >> 1];
+          const double2 v0 = V2[(size_t)i * T2 + p];
+          const double2 v1 = V2[(size_t)(i + 1) * T2 + p];
+          a0 = fma(c.x, v0.x, a0);
+          a1 = fma(c.x, v0.y, a1);
+          b0 = fma(c.y, v1.x, b0);
+          b1 = fma(c.y, v1.y, b1);
+        }
+        if (i < k) {
+          const double c = s_coef[i];
+          const double2 v0 = V2[(size_t)i * T2 + p];
+          a0 = fma(c, v0.x, a0);
+          a1 = fma(c, v0.y, a1);
+        }
+        const double2 wv = make_double2(a0 + b0, a1 + b1);
+        reinterpret_cast<double2*>(base + g0)[p] = wv;  // slot 0, in place (this tile already staged)
+        if (g0 + 2 * p < n) nacc = fma(wv.x, wv.x, nacc);
+        if (g0 + 2 * p + 1 < n) nacc = fma(wv.y, wv.y, nacc);
+      }
+    }
+    if ((MODE == TS_DOTS || MODE == TS_UPD_DOTS) && g0 + T > ndot) {
+      // a non-zero rank's tile holding the replicated phi tail: keep it out of the dots
+      consumer_sync();
+      for (int d = tid; d < T; d += kTsConsumers)
+        if (g0 + d >= ndot) Y[d] = 0.0;
+      consumer_sync();
+    }
+    if (MODE == TS_DOTS || MODE == TS_UPD_DOTS) {
+      // y chunk of 256 doubles in registers (lane owns pairs c0/2 + lane + 32 m)
+      const double2* Y2 = reinterpret_cast<const double2*>(Y);
+      for (int c0 = 0; c0 < T; c0 += kTsChunk) {
+        const int per = min(T - c0, kTsChunk) >> 6;  // pairs per lane (T >= 64)
+        double2 yr[kTsChunk / 64];
+#pragma unroll
+        for (int m = 0; m < kTsChunk / 64; ++m)
+          yr[m] = m < per ? Y2[(c0 >> 1) + lane + 32 * m] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const int i = wid + 8 * v;
+          if (i < k) {
+            const double2* Vi = V2 + (size_t)i * T2 + (c0 >> 1) + lane;
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int m = 0; m < kTsChunk / 64; ++m) {
+              if (m < per) {
+                const double2 x = Vi[32 * m];
+                a0 = fma(x.x, yr[m].x, a0);
+                a1 = fma(x.y, yr[m].y, a1);
+              }
+            }
+            acc[v] += a0 + a1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == S) { s = 0; ++use; }
+  }
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, double* partials, int budget,
@@ -52,7 +167,7 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
   __shared__ uint64_t full[kTsMaxStages], empty[kTsMaxStages];
   __shared__ int s_active, s_i0, s_k, s_y, s_T, s_S;
   __shared__ long long s_ld, s_n, s_ndot;
-  __shared__ double s_coef[kMaxSlots];
+  __shared__ __align__(16) double s_coef[kMaxSlots + 2];
   __shared__ double s_red[kMaxSlots + 1];
   __shared__ double s_buf[kTsBlock / 32];
 
@@ -75,7 +190,7 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
     int T = kTsMaxT;
     while (T > min_T && max_stages * nst * T * 8 > budget) T >>= 1;
     int S = budget / (nst * T * 8);
-    while (S < 2 && T > 32) {
+    while (S < 2 && T > 64) {  // T >= 64: whole 32-lane pair rows
       T >>= 1;
       S = budget / (nst * T * 8);
     }
@@ -133,75 +248,13 @@ __global__ void __launch_bounds__(kTsBlock, 1) k_ts(PhiState* st, double* base, 
     }
   } else {
     // ---------------- consumer warps
-    int s = 0, use = 0;
-    for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
-      mbar_wait(&full[s], use & 1);
-      double* V = smem + (size_t)s * nst * T;
-      double* Y = V + (size_t)k * T;
-      const long long g0 = tl * T;
-      if (MODE == TS_UPD_DOTS || MODE == TS_UPD_NORM) {
-        for (int d = tid; d < T; d += kTsConsumers) {
-          double y0 = Y[d], y1 = 0.0;
-          int i = 0;
-          for (; i + 1 < k; i += 2) {
-            y0 = fma(-s_coef[i], V[(size_t)i * T + d], y0);
-            y1 = fma(-s_coef[i + 1], V[(size_t)(i + 1) * T + d], y1);
-          }
-          if (i < k) y0 = fma(-s_coef[i], V[(size_t)i * T + d], y0);
-          const double yv = y0 + y1;
-          Y[d] = yv;
-          ybase[g0 + d] = yv;
-          if (MODE == TS_UPD_NORM && g0 + d < ndot) nacc = fma(yv, yv, nacc);
-        }
-        if (MODE == TS_UPD_DOTS) consumer_sync();
-      } else if (MODE == TS_COMBINE) {
-        for (int d = tid; d < T; d += kTsConsumers) {
-          double w0 = 0.0, w1 = 0.0;
-          int i = 0;
-          for (; i + 1 < k; i += 2) {
-            w0 = fma(s_coef[i], V[(size_t)i * T + d], w0);
-            w1 = fma(s_coef[i + 1], V[(size_t)(i + 1) * T + d], w1);
-          }
-          if (i < k) w0 = fma(s_coef[i], V[(size_t)i * T + d], w0);
-          const double wv = w0 + w1;
-          base[g0 + d] = wv;  // slot 0, in place (this tile already staged)
-          if (g0 + d < n) nacc = fma(wv, wv, nacc);
-        }
-      }
-      if ((MODE == TS_DOTS || MODE == TS_UPD_DOTS) && g0 + T > ndot) {
-        // a non-zero rank's tile holding the replicated phi tail: keep it out of the dots
-        consumer_sync();
-        for (int d = tid; d < T; d += kTsConsumers)
-          if (g0 + d >= ndot) Y[d] = 0.0;
-        consumer_sync();
-      }
-      if (MODE == TS_DOTS || MODE == TS_UPD_DOTS) {
-        // y chunk of 512 cached in registers (lane owns d = c0 + lane + 32 m)
-        for (int c0 = 0; c0 < T; c0 += kTsChunk) {
-          const int per = min(T - c0, kTsChunk) >> 5;  // T >= 32
-          double yr[kTsChunk / 32];
-#pragma unroll
-          for (int m = 0; m < kTsChunk / 32; ++m) yr[m] = m < per ? Y[c0 + lane + 32 * m] : 0.0;
-#pragma unroll
-          for (int v = 0; v < kAccPerLane; ++v) {
-            const int i = wid + 8 * v;
-            if (i < k) {
-              const double* Vi = V + (size_t)i * T + c0 + lane;
-              double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-              for (int m = 0; m < kTsChunk / 32; m += 2) {
-                if (m < per) a0 = fma(Vi[32 * m], yr[m], a0);
-                if (m + 1 < per) a1 = fma(Vi[32 * (m + 1)], yr[m + 1], a1);
-              }
-              acc[v] += a0 + a1;
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (++s == S) { s = 0; ++use; }
-    }
+    const int nvw = (k + 7) / 8;
+    if (MODE == TS_UPD_NORM || MODE == TS_COMBINE || nvw <= 1) ts_consume<MODE, 1>(st, base, smem, full, empty, s_coef, k, T, S, ntiles, n, ndot, nst, ybase, acc, nacc);
+    else if (nvw <= 2) ts_consume<MODE, 2>(st, base, smem, full, empty, s_coef, k, T, S, ntiles, n, ndot, nst, ybase, acc, nacc);
+    else if (nvw <= 3) ts_consume<MODE, 3>(st, base, smem, full, empty, s_coef, k, T, S, ntiles, n, ndot, nst, ybase, acc, nacc);
+    else if (nvw <= 5) ts_consume<MODE, 5>(st, base, smem, full, empty, s_coef, k, T, S, ntiles, n, ndot, nst, ybase, acc, nacc);
+    else if (nvw <= 8) ts_consume<MODE, 8>(st, base, smem, full, empty, s_coef, k, T, S, ntiles, n, ndot, nst, ybase, acc, nacc);
+    else ts_consume<MODE, kAccPerLane>(st, base, smem, full, empty, s_coef, k, T, S, ntiles, n, ndot, nst, ybase, acc, nacc);
   }
   __syncthreads();
 
