@@ -16,6 +16,17 @@ struct BArgs {
   int p;
 };
 
+#ifdef __CUDACC__
+// v + sum_{k<p} xt[k] b_{p-k}[g] (the augmented columns of proj/src/phi.cpp:151-158), in the
+// reference's order; compile-time indices into b so the kernel parameter stays out of local memory
+__device__ __forceinline__ double aug_tail(const BArgs& b, const double* xt, size_t g, double v) {
+#pragma unroll
+  for (int m = kMaxP; m >= 1; --m)
+    if (m <= b.p && b.b[m]) v = fma(xt[b.p - m], b.b[m][g], v);
+  return v;
+}
+#endif
+
 // Device operator: one DG operator frozen at a reference state (ũ pointer).
 class OpDevice {
  public:

@@ -116,8 +116,7 @@ __global__ void __launch_bounds__(kB1Threads) k_b1_phi(B1P<NP> P, PhiState* st, 
     for (int idx = threadIdx.x; idx < E * NP; idx += blockDim.x) {
       const long long g = e0 * NP + idx;
       double v = sy[idx];
-      for (int i = 0; i < b.p; ++i)
-        if (b.b[b.p - i]) v = fma(s_xt[i], b.b[b.p - i][g], v);
+      v = aug_tail(b, s_xt, g, v);
       v = dt * v;
       y[g] = v;
       nacc = fma(v, v, nacc);
@@ -290,8 +289,7 @@ __global__ void __launch_bounds__(kB1Threads) k_b1oi_phi(B1OP<NP, NQ> P, PhiStat
     for (int idx = threadIdx.x; idx < E * NP; idx += blockDim.x) {
       const long long g = e0 * NP + idx;
       double v = sy[idx];
-      for (int i = 0; i < b.p; ++i)
-        if (b.b[b.p - i]) v = fma(s_xt[i], b.b[b.p - i][g], v);
+      v = aug_tail(b, s_xt, g, v);
       v = dt * v;
       y[g] = v;
       nacc = fma(v, v, nacc);

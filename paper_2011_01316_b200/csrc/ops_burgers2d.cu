@@ -134,8 +134,7 @@ __global__ void __launch_bounds__(256) k_b2_phi(B1P<NP> Px, B1P<NP> Py, int nx, 
     for (int idx = threadIdx.x; idx < te * NN; idx += blockDim.x) {
       const long long g = e0 * NN + idx;
       double v = sout[idx];
-      for (int k = 0; k < b.p; ++k)
-        if (b.b[b.p - k]) v = fma(s_xt[k], b.b[b.p - k][g], v);
+      v = aug_tail(b, s_xt, g, v);
       v = dt * v;
       y[g] = v;
       nacc = fma(v, v, nacc);

@@ -29,6 +29,8 @@ struct E2P {
   const double* ut;    // frozen primitives (u, v, H, a) of q~ per node, state layout
   const double* hx;    // element widths per column (uniform breakpoints, proj/src/mesh.cpp:11-16)
   const double* hy;    // element heights per row
+  const double* ihx;   // 1 / hx, 1 / hy
+  const double* ihy;
   long long n;
   // slab partition: rows -1 and ny are the neighbours' halo rows (raw values of the
   // applied vector / the frozen primitives), exchanged before the kernel runs
@@ -453,8 +455,7 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
     for (int idx = t; idx < te * 4 * NN; idx += blockDim.x) {
       const size_t g = (size_t)e0 * 4 * NN + idx;
       double v = sx[idx];
-      for (int k = 0; k < b.p; ++k)
-        if (b.b[b.p - k]) v = fma(s_xt[k], b.b[b.p - k][g], v);
+      v = aug_tail(b, s_xt, g, v);
       v = dt * v;
       y[g] = v;
       nacc = fma(v, v, nacc);
@@ -488,18 +489,23 @@ struct E2Strip {
   static constexpr int BUFD = 2 * ROWD + W * BLK;  // x + frozen (with halo) + b_1
   static constexpr int NBUF = 4;
   static constexpr int ROWS_PER_UNIT = 64;
-  static constexpr int SMEM = (NBUF * BUFD + 2 * W * BLK) * 8;  // ring + sf
+  static constexpr int FX = (W + 1) * NP * 4;   // x-face fluxes of a row
+  static constexpr int FY = W * NP * 4;         // y-face fluxes of one face row
+  static constexpr int SMEM = (NBUF * BUFD + 2 * W * BLK + FX + 2 * FY) * 8;  // ring + sf + face fluxes
 };
 
 template <int NP, bool ROE>
-__global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st, double* base, double* partials,
+__global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st, double* base, double* partials,
                                                          BArgs b) {
   using S = E2Strip<NP>;
   constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;
   double* sf = smem + NBUF * S::BUFD;
+  double* sfx = sf + 2 * W * BLK;
+  double* sfy = sfx + S::FX;
   __shared__ uint64_t full[NBUF], empty[NBUF];
+  __shared__ double s_wd[NP * NP], s_wq[NP];
   __shared__ int s_go, s_j;
   __shared__ double s_xs, s_dt, s_xt[kMaxP];
   __shared__ long long s_ld;
@@ -523,6 +529,8 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
       fence_mbar_init();
     }
   }
+  for (int q = tid; q < NP * NP; q += blockDim.x) s_wd[q] = P.WD[q];
+  for (int q = tid; q < NP; q += blockDim.x) s_wq[q] = P.w[q];
   __syncthreads();
   if (!s_go) return;
   const double* x = base + (size_t)s_j * s_ld;
@@ -586,6 +594,16 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
     // ---------------- consumers: one thread per node of the strip row
     const int le = tid / NN, node = tid % NN;
     const int i = node % NP, j = node / NP;
+    // per-thread basis constants in registers (a runtime index into the kernel
+    // parameter arrays would spill them to local memory)
+    double wdi[NP], wdj[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      wdi[q] = s_wd[q * NP + i];
+      wdj[q] = s_wd[q * NP + j];
+    }
+    const double wi = s_wq[i], wj = s_wq[j];
+    const double iwij = 1.0 / (wi * wj);
     long long seq = 0;
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
       const int strip = u % nstrips, chunk = u / nstrips;
@@ -594,6 +612,8 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
       const bool active = le < w;
       const int ie = ie0 + le;
       const double hx = active ? __ldg(P.hx + ie) : 1.0;
+      const double ihx = active ? __ldg(P.ihx + ie) : 1.0;
+      const double sxs = 0.5 * hx * wi;
       auto slot = [&](long long q) { return ring + (size_t)((seq + q) % NBUF) * S::BUFD; };
       auto wait_row = [&](long long q) { mbar_wait(&full[(seq + q) % NBUF], (int)(((seq + q) / NBUF) & 1)); };
       wait_row(0);
@@ -605,6 +625,7 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
         const double* lo = slot(q - 1);
         const double* hi = slot(q + 1);
         const double hy = __ldg(P.hy + r);
+        const double ihy = __ldg(P.ihy + r);
         double qv[4], tv[4];
         if (active) {
 #pragma unroll
@@ -622,10 +643,50 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
             sf[((le * 2 + 1) * 4 + c) * NN + node] = fy[c];
           }
         }
+        // ---- numerical fluxes, once per face node (the reference's rhs_faces loop,
+        // proj/src/euler.cpp:260-297): x-faces of row r, the y-faces above it and, on the
+        // first row of a unit, the y-faces below it; the y-face row above is the next
+        // row's lower face row (2-deep ring)
+        {
+          double* ytop = sfy + ((r - r0 + 1) & 1) * S::FY;
+          double* ybot = sfy + ((r - r0) & 1) * S::FY;
+          const int nxf = (w + 1) * NP, nyf = w * NP;
+          const int total = nxf + nyf + (r == r0 ? nyf : 0);
+          for (int t = tid; t < total; t += 256) {  // the 8 consumer warps
+            double qa[4], ta[4], qb[4], tb[4], f[4];
+            const double* ra;
+            const double* rb;
+            int pa, pb, na, nb, dir;
+            double* dst;
+            if (t < nxf) {  // between ring elements fi (W side) and fi + 1 (E side)
+              const int fi = t / NP, jn = t - fi * NP;
+              ra = cur; rb = cur; pa = fi; pb = fi + 1; na = jn * NP + N; nb = jn * NP; dir = 0;
+              dst = sfx + (fi * NP + jn) * 4;
+            } else if (t < nxf + nyf) {  // top face of element le: (le, j = N) | row above (le, j = 0)
+              const int tt = t - nxf, le2 = tt / NP, in = tt - le2 * NP;
+              ra = cur; rb = hi; pa = pb = le2 + 1; na = N * NP + in; nb = in; dir = 1;
+              dst = ytop + (le2 * NP + in) * 4;
+            } else {  // bottom face of element le (first row of the unit)
+              const int tt = t - nxf - nyf, le2 = tt / NP, in = tt - le2 * NP;
+              ra = lo; rb = cur; pa = pb = le2 + 1; na = N * NP + in; nb = in; dir = 1;
+              dst = ybot + (le2 * NP + in) * 4;
+            }
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              qa[c] = ra[pa * BLK + c * NN + na] * xs;
+              ta[c] = ra[S::ROWD + pa * BLK + c * NN + na];
+              qb[c] = rb[pb * BLK + c * NN + nb] * xs;
+              tb[c] = rb[S::ROWD + pb * BLK + c * NN + nb];
+            }
+            bool bad = false;
+            face_flux<ROE>(0, dir, P.gamma, qa, qb, ta, tb, f, bad);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dst[c] = f[c];
+          }
+        }
         consumer_sync();
         if (active) {
-          const double sy = 0.5 * hy * P.w[j];
-          const double sxs = 0.5 * hx * P.w[i];
+          const double sy = 0.5 * hy * wj;
           double rr[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -634,47 +695,26 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
             double ax = 0.0, ay = 0.0;
 #pragma unroll
             for (int k = 0; k < NP; ++k) {
-              ax = fma(P.WD[k * NP + i], fxr[k], ax);
-              ay = fma(P.WD[k * NP + j], fyc[k * NP], ay);
+              ax = fma(wdi[k], fxr[k], ax);
+              ay = fma(wdj[k], fyc[k * NP], ay);
             }
             rr[c] = sy * ax;
             rr[c] += sxs * ay;
           }
-          bool bad = false;
+          // scatter of the face fluxes: owner side (normal +e) subtracts, neighbour adds
           if (i == N || i == 0) {
-            const bool owner = i == N;
-            const int pos = owner ? le + 2 : le;  // E / W neighbour in the row buffer
-            const int node2 = j * NP + (owner ? 0 : N);
-            double q2[4], u2[4], f[4];
+            const double* f = sfx + (((i == N ? le + 1 : le) * NP) + j) * 4;
+            const double fw = (i == N ? -0.5 : 0.5) * hy * wj;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              q2[c] = cur[pos * BLK + c * NN + node2] * xs;
-              u2[c] = cur[S::ROWD + pos * BLK + c * NN + node2];
-            }
-            if (owner) face_flux<ROE>(0, 0, P.gamma, qv, q2, tv, u2, f, bad);
-            else face_flux<ROE>(0, 0, P.gamma, q2, qv, u2, tv, f, bad);
-            const double fw = 0.5 * hy * P.w[j];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) rr[c] = owner ? rr[c] - fw * f[c] : rr[c] + fw * f[c];
+            for (int c = 0; c < 4; ++c) rr[c] = fma(fw, f[c], rr[c]);
           }
           if (j == N || j == 0) {
-            const bool owner = j == N;
-            const double* nb = owner ? hi : lo;
-            const int node2 = (owner ? 0 : N) * NP + i;
-            double q2[4], u2[4], f[4];
+            const double* f = sfy + (((r - r0 + (j == N ? 1 : 0)) & 1) * S::FY) + (le * NP + i) * 4;
+            const double fw = (j == N ? -0.5 : 0.5) * hx * wi;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              q2[c] = nb[(le + 1) * BLK + c * NN + node2] * xs;
-              u2[c] = nb[S::ROWD + (le + 1) * BLK + c * NN + node2];
-            }
-            if (owner) face_flux<ROE>(0, 1, P.gamma, qv, q2, tv, u2, f, bad);
-            else face_flux<ROE>(0, 1, P.gamma, q2, qv, u2, tv, f, bad);
-            const double fw = 0.5 * hx * P.w[i];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) rr[c] = owner ? rr[c] - fw * f[c] : rr[c] + fw * f[c];
+            for (int c = 0; c < 4; ++c) rr[c] = fma(fw, f[c], rr[c]);
           }
-          const double scale = 4.0 / (hx * hy);
-          const double im = scale / (P.w[i] * P.w[j]);
+          const double im = (4.0 * ihx * ihy) * iwij;  // 4 / (hx hy w_i w_j)
           const size_t e = (size_t)r * nx + ie;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -683,8 +723,7 @@ __global__ void __launch_bounds__(288, 2) k_e2_phi_strip(E2P<NP> P, PhiState* st
             if (b1) {
               v = fma(s_xt[0], cur[2 * S::ROWD + le * BLK + c * NN + node], v);
             } else {
-              for (int k = 0; k < b.p; ++k)
-                if (b.b[b.p - k]) v = fma(s_xt[k], b.b[b.p - k][g], v);
+              v = aug_tail(b, s_xt, g, v);
             }
             v = dt * v;
             y[g] = v;
@@ -801,14 +840,17 @@ class Euler2D : public OpDevice {
     P.ny = nyl;
     P.part = part ? 1 : 0;
     P.gamma = d.gamma;
-    std::vector<double> hs(d.nx + nyl);
+    std::vector<double> hs(2 * (d.nx + nyl));
     for (int i = 0; i < d.nx; ++i) hs[i] = ubreak(d.x0, d.x1, i + 1, d.nx) - ubreak(d.x0, d.x1, i, d.nx);
     for (int j = 0; j < nyl; ++j)
       hs[d.nx + j] = ubreak(d.y0, d.y1, row0 + j + 1, d.ny) - ubreak(d.y0, d.y1, row0 + j, d.ny);
+    for (int q = 0; q < d.nx + nyl; ++q) hs[d.nx + nyl + q] = 1.0 / hs[q];
     EXPDG_CUDA(cudaMalloc(&hbuf, sizeof(double) * hs.size()));
     EXPDG_CUDA(cudaMemcpy(hbuf, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice));
     P.hx = hbuf;
     P.hy = hbuf + d.nx;
+    P.ihx = hbuf + d.nx + nyl;
+    P.ihy = hbuf + 2 * d.nx + nyl;
     for (int a = 0; a < NP; ++a) {
       P.w[a] = hb.weights[a];
       for (int b2 = 0; b2 < NP; ++b2) P.WD[a * NP + b2] = hb.weights[a] * hb.D[a * NP + b2];
@@ -840,7 +882,7 @@ class Euler2D : public OpDevice {
     if (use_strip) {
       using SS = E2Strip<NP>;
       const int units = ((P.nx + SS::W - 1) / SS::W) * ((P.ny + SS::ROWS_PER_UNIT - 1) / SS::ROWS_PER_UNIT);
-      const int g = std::max(1, std::min(units, 2 * 148));
+      const int g = std::max(1, std::min(units, 148));  // one CTA per SM (smem-bound)
       if (roe) k_e2_phi_strip<NP, true><<<g, 288, SS::SMEM, s>>>(p, st, base, partials, b);
       else k_e2_phi_strip<NP, false><<<g, 288, SS::SMEM, s>>>(p, st, base, partials, b);
     } else {

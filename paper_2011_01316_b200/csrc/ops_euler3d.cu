@@ -345,8 +345,7 @@ __global__ void __launch_bounds__(256) k_e3_phi(E3P<NP> P, PhiState* st, double*
     for (int idx = t; idx < te * 5 * NN; idx += blockDim.x) {
       const size_t g = (size_t)e0 * 5 * NN + idx;
       double v = sx[idx];
-      for (int q = 0; q < b.p; ++q)
-        if (b.b[b.p - q]) v = fma(s_xt[q], b.b[b.p - q][g], v);
+      v = aug_tail(b, s_xt, g, v);
       v = dt * v;
       y[g] = v;
       nacc = fma(v, v, nacc);
