@@ -17,7 +17,7 @@ void launch_step_finish(cudaStream_t s, PhiState* st, double* u, const double* w
 void launch_absmax(cudaStream_t s, const double* u, long long n, double* out2, int grid);
 void launch_step_decide(cudaStream_t s, PhiState* st, StepRecord* rec);
 void launch_phi_config(cudaStream_t s, PhiState* st, const double* dt_seq, int p, double mult, int mmax,
-                       int full_orth, int window, int grow_cap);
+                       int full_orth, int window, int grow_cap, int dcgs);
 void launch_vec_add(cudaStream_t s, const PhiState* st, double* out, const double* u, const double* w, long long n);
 void launch_exprb_d2(cudaStream_t s, const PhiState* st, const double* dt_seq, double* d, const double* a,
                      const double* b, double c, long long n);
@@ -508,7 +508,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
       if (e.comm) e.comm->allreduce(&e.st->domain_flag, &e.st->domain_flag, 1, COMM_I32, COMM_MAX, s);
       if (exprb) {
         dev.launch_apply(s, 1, u, nu);
-        launch_phi_config(s, e.st, dts_dev, 1, mult1, c1.mmax, c1.full_orth, c1.window, c1.grow_cap);
+        launch_phi_config(s, e.st, dts_dev, 1, mult1, c1.mmax, c1.full_orth, c1.window, c1.grow_cap, c1.dcgs);
       }
     }
     e.launch_phi_init(s, b1);
@@ -517,7 +517,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     launch_vec_add(s, e.st, stage, u, e.slot(0), n);
     dev.launch_apply(s, 1, stage, ns);
     launch_exprb_d2(s, e.st, dts_dev, d2, ns, nu, dcoef, n);
-    launch_phi_config(s, e.st, dts_dev, 3, 1.0, c3.mmax, c3.full_orth, c3.window, c3.grow_cap);
+    launch_phi_config(s, e.st, dts_dev, 3, 1.0, c3.mmax, c3.full_orth, c3.window, c3.grow_cap, c3.dcgs);
     e.launch_phi_init(s, b2);
   };
   const int fgrid = std::min(2048, std::max(1, (int)std::min<long long>(e.num_sms * 4, (n + 255) / 256)));
@@ -553,9 +553,9 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     EXPDG_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
     return cp.conditional.phGraph_out[0];
   };
-  auto host_loop = [&](const BArgs& b) {
+  auto host_loop = [&](const BArgs& b, bool dcgs) {
     for (long long cyc = 0;; ++cyc) {
-      e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0);
+      e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0, dcgs);
       EXPDG_CUDA(cudaMemcpyAsync(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost, e.stream));
       EXPDG_CUDA(cudaStreamSynchronize(e.stream));
       if (e.st_host->action == ACT_DONE || e.st_host->action == ACT_NONE || e.st_host->stopped) break;
@@ -579,11 +579,11 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
       post(cs);
       EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
       EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body1, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-      e.launch_body(cs, dev, b1, h1, 1);
+      e.launch_body(cs, dev, b1, h1, 1, c1.dcgs != 0);
       EXPDG_CUDA(cudaStreamEndCapture(cs, &body1));
       if (exprb) {
         EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body2, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        e.launch_body(cs, dev, b2, h2, 1);
+        e.launch_body(cs, dev, b2, h2, 1, c3.dcgs != 0);
         EXPDG_CUDA(cudaStreamEndCapture(cs, &body2));
       }
       EXPDG_CUDA(cudaGraphInstantiate(&ex, g, 0));
@@ -606,10 +606,10 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
           EXPDG_CUDA(cudaGraphLaunch(ex, e.stream));
         } else {
           pre(e.stream);
-          host_loop(b1);
+          host_loop(b1, c1.dcgs != 0);
           if (exprb) {
             mid(e.stream);
-            host_loop(b2);
+            host_loop(b2, c3.dcgs != 0);
           }
           post(e.stream);
         }

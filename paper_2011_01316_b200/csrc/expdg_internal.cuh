@@ -82,6 +82,8 @@ struct PhiState {
     double dotA[kMaxSlots];
     double dotB[kMaxSlots];
     double bnorm2[kMaxP + 1];
+    double nrmU;  // DCGS2: ||reorthogonalised candidate||^2 after the update pass
+    double nrmW;  // DCGS2: ||next candidate||^2 after the update pass
   };
   Red red;
   Red loc;
@@ -95,6 +97,23 @@ struct PhiState {
   double scale[kMaxSlots];
   double comb[kMaxSlots];
   double tailw[kMaxP];
+  // ---- DCGS2: classical Gram-Schmidt with the reorthogonalisation of column j-1
+  // lagged into the pass that first projects column j (one dots pass + one update
+  // pass per column instead of CGS2's three).  Slot j holds the candidate u_j
+  // (projected once, scale[j] provisional); the JVP runs on it and the second
+  // projection of u_j rides in the same two passes as the first projection of A u_j.
+  int dcgs;        // 1: DCGS2 (full orthogonalisation only), 0: CGS2 / IOP passes
+  int dc_pending;  // the AVNORM cycle already extended column mc provisionally
+  double dc_gam;   // slot-space coefficient of the old candidate in the w update
+  double dc_c, dc_d, dc_ab;  // <u,u>, <u,w>, a.b (true, scaled)
+  double dc_gp;              // gamma used by the update pass (Pythagorean beta)
+  double pre_prev;           // ||dt A V_{j-1}|| (the lagged breakdown test, proj/src/phi.cpp:104-108)
+  long long dc_fixups;       // Pythagorean vs exact reorthogonalised norm disagreed (diagnostic)
+  double dc_a[kMaxSlots];      // a_i = <V_i, u>
+  double dc_b[kMaxSlots];      // b_i = <V_i, w>
+  double dc_g[kMaxSlots];      // (H a)_l with column j-1 corrected, l < j
+  double dc_alpha[kMaxSlots];  // slot-space update coefficients of u
+  double dc_mu[kMaxSlots];     // slot-space update coefficients of w
   // ---- Hessenberg (mmax+1) x mmax, row stride kMaxBasis
   double H[(kMaxBasis + 1) * kMaxBasis];
   // ---- last-block reduction tickets, one per reducing kernel kind

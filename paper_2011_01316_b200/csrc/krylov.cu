@@ -25,6 +25,9 @@
 
 namespace expdg {
 
+void launch_dcgs(cudaStream_t s, Engine& e, int which);
+void dcgs_init_attrs(int maxsm);
+
 enum TsMode { TS_DOTS = 0, TS_UPD_DOTS = 1, TS_UPD_NORM = 2, TS_COMBINE = 3 };
 enum Ticket { TK_DOTS = 0, TK_UPD_DOTS = 1, TK_UPD_NORM = 2, TK_COMBINE = 3, TK_APPLY = 4, TK_INIT = 5,
               TK_RES = 6, TK_FINISH = 7, TK_MAX = 8 };
@@ -508,6 +511,49 @@ __device__ __forceinline__ void set_window(PhiState* st, int j) {
   st->k = j - st->j0 + 1;
 }
 
+// DCGS2 (dcgs.cu): after the update pass of the cycle for column j, finish
+// column j-1 (reorthogonalisation correction H(:, j-1) += a, exact H(j, j-1) =
+// ||u - V a||, breakdown test of proj/src/phi.cpp:104-108 one cycle late) and write
+// column j provisionally from a, b, <u,w> and H.  Thread 0 of k_ctl.
+// Returns 1 on breakdown (mc = j), else 0.
+__device__ int dcgs_finish(PhiState* st) {
+  const int j = st->j;
+  const double nd = (double)st->n;
+  st->alg_bytes += 32.0 * nd + 8.0 * nd * (2.0 * j + 6.0);
+  double beta = 1.0;
+  if (j >= 1) {
+    beta = st->scale[j] * sqrt(st->red.nrmU);
+    for (int l = 0; l < j; ++l) st->H[l * kMaxBasis + (j - 1)] += st->dc_a[l];
+    if (beta <= 1e-14 * fmax(st->pre_prev, 1e-300)) {
+      st->H[j * kMaxBasis + (j - 1)] = 0.0;
+      st->mc = j;
+      st->breakdown = 1;
+      return 1;
+    }
+    st->H[j * kMaxBasis + (j - 1)] = beta;
+    st->scale[j] = 1.0 / sqrt(st->red.nrmU);  // V_j = slot_j / ||slot_j||
+  }
+  const double ib = 1.0 / beta;
+  // column j = kMaxBasis (the avnorm cycle at mc = mmax = 128) has no storage and no
+  // use: the space cannot grow past mmax
+  const bool store = j < kMaxBasis;
+  double hh = 0.0;
+  for (int l = 0; l < j; ++l) {
+    const double h = (st->dc_b[l] - st->dc_g[l]) * ib;
+    if (store) st->H[l * kMaxBasis + j] = h;
+    hh = fma(h, h, hh);
+  }
+  // the V_j coefficient the update pass actually removed (gamma from the Pythagorean
+  // beta); the next cycle's reorthogonalisation adds the remainder
+  const double gj = j >= 1 ? beta * st->dc_a[j - 1] : 0.0;
+  const double hj = st->dc_gp - gj * ib;
+  if (store) st->H[j * kMaxBasis + j] = hj;
+  hh = fma(hj, hj, hh);
+  st->scale[j + 1] = ib;                                   // u_{j+1} = slot_{j+1} / beta
+  st->pre_prev = sqrt(st->red.nrmW * ib * ib + hh);        // ||dt A V_j|| (incl. the augmentation)
+  return 0;
+}
+
 __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double* W,
                                              cudaGraphConditionalHandle cond, int use_graph) {
   __shared__ int s_phase, s_exit, s_zeroH, s_done;
@@ -525,6 +571,24 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
           phase = PH_SUBSTEP;
           break;
         case ACT_EXTEND: {
+          if (st->dcgs) {
+            if (dcgs_finish(st)) {
+              phase = PH_POST;  // breakdown in column j-1: no avnorm
+            } else {
+              st->iterations++;
+              st->extend_cols++;
+              const int mc = st->j + 1;
+              st->mc = mc;
+              if (mc < st->target) {
+                set_window(st, mc);
+                st->action = ACT_EXTEND;
+                s_exit = 1;
+              } else {
+                phase = PH_POST;
+              }
+            }
+            break;
+          }
           const int j = st->j;
           const double* sc = st->scale;
           for (int i = st->j0; i <= j; ++i) {
@@ -561,6 +625,18 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
           break;
         }
         case ACT_AVNORM:
+          if (st->dcgs) {  // the avnorm cycle extends column mc provisionally as well
+            if (dcgs_finish(st)) {
+              st->avnorm = 0.0;  // breakdown in column mc-1 (the reference computes no avnorm)
+            } else {
+              st->iterations++;
+              st->avnorms++;
+              st->avnorm = st->pre_prev;  // ||dt A V_mc|| (proj/src/phi.cpp:195-199)
+              st->dc_pending = 1;
+            }
+            phase = PH_DECIDE;
+            break;
+          }
           st->alg_bytes += 32.0 * (double)st->n;
           st->avnorms++;
           st->avnorm = sqrt(st->red.nrmA);
@@ -638,8 +714,24 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
           const int m = min(st->grow_cap, max(mc + 1, (3 * mc) / 2));
           st->m = m;
           st->target = m;
-          set_window(st, mc);
-          st->action = ACT_EXTEND;
+          if (st->dcgs && st->dc_pending) {
+            // column mc was extended by the avnorm cycle; the reference re-applies A to
+            // V_mc here, which counts as an iteration (proj/src/phi.cpp:84-112)
+            st->dc_pending = 0;
+            st->iterations++;
+            st->extend_cols++;
+            st->mc = mc + 1;
+            if (mc + 1 < m) {
+              set_window(st, mc + 1);
+              st->action = ACT_EXTEND;
+            } else {
+              st->j = mc + 1;
+              st->action = ACT_AVNORM;
+            }
+          } else {
+            set_window(st, mc);
+            st->action = ACT_EXTEND;
+          }
           s_exit = 1;
         } else {
           st->h = h * 0.5;
@@ -670,6 +762,7 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
             st->mc = 0;
             st->breakdown = 0;
             st->scale[0] = 1.0 / beta;
+            st->dc_pending = 0;
             st->target = st->m;
             set_window(st, 0);
             st->action = ACT_EXTEND;
@@ -681,7 +774,7 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
         if (!st->breakdown) {
           st->j = st->mc;
           st->action = ACT_AVNORM;
-          st->iterations++;
+          if (!st->dcgs) st->iterations++;  // DCGS2 counts it when the cycle finds no breakdown
           s_exit = 1;
         } else {
           st->avnorm = 0.0;
@@ -766,6 +859,8 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_TS_STAGES")) ts_tuning.stages = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_TS_MIN_T")) ts_tuning.min_T = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_LD_ODD")) ld_odd = std::atoi(v);
+  if (const char* v = std::getenv("EXPDG_ORTH")) use_dcgs = std::strcmp(v, "cgs2") != 0;
+  dcgs_init_attrs(maxsm);
 }
 
 Engine::~Engine() {
@@ -838,6 +933,7 @@ PhiState Engine::config(long long n, int p, double dt, const expdg_krylov_cfg& k
   const int orth = kc.orth_length;
   c.full_orth = (orth >= c.mmax || dim <= std::max(c.initial_basis, 16)) ? 1 : 0;  // :171-173
   c.window = c.full_orth ? c.mmax : orth;
+  c.dcgs = (c.full_orth && use_dcgs) ? 1 : 0;
   c.grow_cap = c.full_orth ? c.mmax : std::min(c.mmax, 32);  // :177
   c.max_cycles = 200000;
   c.action = ACT_NONE;
@@ -883,9 +979,20 @@ void Engine::launch_ts(cudaStream_t s, int mode) {
 }
 
 void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
-                         int use_graph) {
+                         int use_graph, bool dcgs) {
   op.launch_phi_apply(s, st, base, partials, b);
   reduce(s);
+  if (dcgs) {  // one dots pass + coefficients + one update pass (dcgs.cu)
+    launch_dcgs(s, *this, 0);
+    reduce(s);
+    launch_dcgs(s, *this, 1);
+    launch_dcgs(s, *this, 2);
+    reduce(s);
+    launch_ts(s, TS_COMBINE);
+    reduce(s);
+    k_ctl<<<1, 256, 0, s>>>(st, slot(0), ework, h, use_graph);
+    return;
+  }
   if (!op.fused_dots()) {
     launch_ts(s, TS_DOTS);
     reduce(s);
@@ -948,7 +1055,7 @@ void Engine::run_phi(OpDevice& op, const BArgs& b, int use_graph) {
   }
   launch_phi_init(stream, b);
   for (int cyc = 0; cyc < 1000000; ++cyc) {
-    launch_body(stream, op, b, cudaGraphConditionalHandle{}, 0);
+    launch_body(stream, op, b, cudaGraphConditionalHandle{}, 0, st_host->dcgs != 0);
     EXPDG_CUDA(cudaMemcpyAsync(st_host, st, sizeof(PhiState), cudaMemcpyDeviceToHost, stream));
     EXPDG_CUDA(cudaStreamSynchronize(stream));
     if (st_host->action == ACT_DONE || st_host->action == ACT_NONE || st_host->stopped) return;
@@ -982,7 +1089,7 @@ cudaGraphExec_t Engine::build_phi_graph(OpDevice& op, const BArgs& b) {
   EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  launch_body(cs, op, b, h, 1);
+  launch_body(cs, op, b, h, 1, st_host->dcgs != 0);
   EXPDG_CUDA(cudaStreamEndCapture(cs, &body));
   cudaGraphExec_t ex;
   EXPDG_CUDA(cudaGraphInstantiate(&ex, g, 0));

@@ -91,6 +91,7 @@ class Engine {
  public:
   TsTuning ts_tuning;
   int ld_odd = 1;
+  int use_dcgs = 1;  // DCGS2 for fully orthogonalised calls (EXPDG_ORTH=cgs2 selects CGS2)
   // Set when the context belongs to a slab-partitioned group: every reducing
   // kernel is followed by a sum-allreduce of PhiState::loc -> PhiState::red,
   // and the control runs host-stepped (no CUDA graphs).
@@ -129,7 +130,7 @@ class Engine {
   void launch_ts(cudaStream_t s, int mode);
   double bench_ts(long long n, int k, int mode, int reps);
   void launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
-                   int use_graph);
+                   int use_graph, bool dcgs);
   // Runs one phi call to completion; host-stepped or graph-driven control.
   void run_phi(OpDevice& op, const BArgs& b, int use_graph);
   // Builds a while-node graph around launch_body; caller owns the exec.

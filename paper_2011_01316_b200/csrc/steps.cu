@@ -15,7 +15,7 @@ __global__ void k_step_begin(PhiState* st, const double* dt_seq) {
 // Per-call configuration of the phi calls of an EXPRB step (p and the dt factor
 // differ between the two calls, proj/src/integrators.cpp:85-113).
 __global__ void k_phi_config(PhiState* st, const double* dt_seq, int p, double mult, int mmax, int full_orth,
-                             int window, int grow_cap) {
+                             int window, int grow_cap, int dcgs) {
   if (st->stopped) return;
   st->p = p;
   st->len = st->n + p;
@@ -24,6 +24,7 @@ __global__ void k_phi_config(PhiState* st, const double* dt_seq, int p, double m
   st->full_orth = full_orth;
   st->window = window;
   st->grow_cap = grow_cap;
+  st->dcgs = dcgs;
 }
 
 // S = u + w (the EXPRB internal stage, proj/src/integrators.cpp:93 / :108)
@@ -146,8 +147,8 @@ void launch_step_finish(cudaStream_t s, PhiState* st, double* u, const double* w
   k_step_finish<<<grid, 256, 0, s>>>(st, u, w, mode, rec, partials);
 }
 void launch_phi_config(cudaStream_t s, PhiState* st, const double* dt_seq, int p, double mult, int mmax,
-                       int full_orth, int window, int grow_cap) {
-  k_phi_config<<<1, 1, 0, s>>>(st, dt_seq, p, mult, mmax, full_orth, window, grow_cap);
+                       int full_orth, int window, int grow_cap, int dcgs) {
+  k_phi_config<<<1, 1, 0, s>>>(st, dt_seq, p, mult, mmax, full_orth, window, grow_cap, dcgs);
 }
 void launch_vec_add(cudaStream_t s, const PhiState* st, double* out, const double* u, const double* w, long long n) {
   k_vec_add<<<1184, 256, 0, s>>>(st, out, u, w, n);
