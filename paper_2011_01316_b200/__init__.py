@@ -83,7 +83,7 @@ EXPORTS = [
     "expdg_initial_condition", "expdg_ctx_kernel_launches", "expdg_ctx_last_loop_ms", "expdg_expm",
     "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts", "expdg_op_set_source",
     "expdg_op_set_source_fn", "expdg_nccl_unique_id", "expdg_ctx_attach_nccl", "expdg_local_group_create",
-    "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm",
+    "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
 ]
 
 _lib = None
@@ -144,6 +144,7 @@ def lib():
     L.expdg_local_group_destroy.argtypes = [vp]
     L.expdg_ctx_attach_local.argtypes = [vp, vp, C.c_int]
     L.expdg_ctx_comm.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.expdg_ctx_set_orthogonalization.argtypes = [vp, C.c_int]
     _lib = L
     return L
 
@@ -197,13 +198,18 @@ def initial_condition(config: int, nx: int, order: int, seed: int, noise: float 
 
 # ---------------------------------------------------------------- context / operators
 class Context:
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, orth: Optional[str] = None):
+        """orth: "dcgs2" (default) or "cgs2" for fully orthogonalised phi calls."""
         import torch
         torch.cuda.init()
         self.device = device
         h = C.c_void_p()
         _check(lib().expdg_ctx_create(device, C.byref(h)))
         self.h = h
+        if orth is not None:
+            if orth not in ("cgs2", "dcgs2"):
+                raise ValueError("orth must be 'cgs2' or 'dcgs2'")
+            _check(lib().expdg_ctx_set_orthogonalization(self.h, 1 if orth == "dcgs2" else 0))
 
     def close(self):
         if getattr(self, "h", None):

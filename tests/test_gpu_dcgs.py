@@ -1,0 +1,71 @@
+"""GPU: the two orthogonalisations of fully orthogonalised phi calls (CGS2, DCGS2)
+against the reference's two-pass modified Gram-Schmidt Arnoldi (proj/src/phi.cpp:84-112,
+restated in the oracle) on the dense augmented operator [[dt L, dt r], [0, 0]] of a
+stiff over-integrated Burgers problem (acceptance criterion 5's, Cr_d = 161), and
+against each other on the full time loop."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2011_01316_b200 as pkg
+from paper_2011_01316_b200 import configs
+from tests.gpu_util import rel, to_dev, to_host
+
+pytestmark = pytest.mark.gpu
+
+
+def stiff_problem():
+    u0, _, cfg = oracle.harness_burgers("burgers-smooth", 40, 4, "ef", 3e-4)
+    kw = dict(box=(0.0, 1.0, 0, 1, 0, 1), periodic=False, kappa=cfg["kappa"], flux=cfg["flux"], sigma=cfg["sigma"],
+              over_integrate=cfg["over_integrate"])
+    return u0, pkg.OperatorSpec("burgers1d", 4, 40, **kw), oracle.Problem("burgers1d", 4, 40, **kw)
+
+
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+@pytest.mark.parametrize("dt,m", [(1e-4, 16), (0.1, 40), (0.1, 128)])
+def test_hessenberg_matches_mgs2(orth, dt, m):
+    u0, spec, orc = stiff_problem()
+    n = u0.size
+    L = np.stack([orc.apply_linear(u0, np.eye(n)[i]) for i in range(n)], axis=1)
+    r = orc.apply_linear(u0, u0) + orc.apply_nonlinear(u0, u0)
+    aug = np.zeros((n + 1, n + 1))
+    aug[:n, :n] = dt * L
+    aug[:n, n] = dt * r
+    seed = np.zeros(n + 1)
+    seed[n] = 1.0
+    _, href, _, _, _ = oracle.krylov_build(aug, seed, m, m)
+    ctx = pkg.Context(0, orth=orth)
+    op = pkg.Operator(ctx, spec)
+    op.linearize(to_dev(u0))
+    try:  # one substep: H is the first Arnoldi's (rejections halve h and reuse it)
+        pkg.phi_combination(ctx, op, [None, to_dev(r)], dt, tol=1e-12, max_basis=m, orth_length=m, max_substeps=1)
+    except pkg.KrylovError:
+        pass
+    h = ctx.debug_hessenberg()[:m + 1, :m]
+    assert np.abs(h - href).max() <= 1e-11 * np.abs(href).max()
+
+
+def test_dcgs2_and_cgs2_time_loops_agree():
+    u0, spec, _ = stiff_problem()
+    out = {}
+    for orth in ("cgs2", "dcgs2"):
+        ctx = pkg.Context(0, orth=orth)
+        op = pkg.Operator(ctx, spec)
+        out[orth] = pkg.integrate(ctx, op, to_dev(u0), "epi2", 0.1, 1.0, tol=1e-12, max_basis=128, orth_length=128)
+    a, b = out["cgs2"], out["dcgs2"]
+    assert a.status == b.status == "completed"
+    assert rel(to_host(b.u), to_host(a.u)) <= 1e-10
+    assert list(a.iters_per_step) == list(b.iters_per_step)
+
+
+def test_dcgs2_euler_matches_cgs2():
+    w = configs.scaled(configs.C4, 24, steps=3)
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    res = {}
+    for orth in ("cgs2", "dcgs2"):
+        ctx = pkg.Context(0, orth=orth)
+        res[orth] = pkg.integrate(ctx, pkg.Operator(ctx, w.spec()), to_dev(u0), "epi2", dt, w.steps * dt, tol=w.tol,
+                                  max_basis=w.max_basis, orth_length=w.max_basis)
+    assert rel(to_host(res["dcgs2"].u), to_host(res["cgs2"].u)) <= 1e-11
+    assert list(res["dcgs2"].iters_per_step) == list(res["cgs2"].iters_per_step)
