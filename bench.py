@@ -288,8 +288,9 @@ def main():
                        "krylov_iters_per_step": [int(v) for v in iters_per_step]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": "phi engine cycle (operator apply + CGS2 passes + combine + controller), "
-                                   "canonical algorithmic bytes of the realised trajectory / step-loop time",
+                         "kernel": "phi engine cycle (operator apply + DCGS2 dots/update passes + combine + "
+                                   "controller): algorithmic bytes of the realised trajectory (DCGS2: JVP 32n + "
+                                   "8n(2k+6) per column; SURVEY's CGS2 count is 8n(3k+6)) / step-loop time",
                          "peak_kind": peak_kind, "alg_bytes_per_step": traffic["alg_bytes"] / args.steps,
                          "columns": traffic["columns"], "avnorms": traffic["avnorms"],
                          "combines": traffic["combines"]},
