@@ -138,13 +138,14 @@ int expdg_ctx_attach_local(expdg_ctx* ctx, expdg_local_group* g, int rank);
 int expdg_ctx_comm(const expdg_ctx* ctx, int* rank, int* size); /* 0, 1 without a communicator */
 
 /* Orthogonalisation of fully orthogonalised phi calls (orth_length >= max_basis):
- * EXPDG_ORTH_DCGS2 (default) classical Gram-Schmidt with the reorthogonalisation of
+ * EXPDG_ORTH_DCGS2 classical Gram-Schmidt with the reorthogonalisation of
  * column j-1 lagged into the two streaming passes of column j; EXPDG_ORTH_CGS2
  * classical Gram-Schmidt twice (three passes).  Both are the reference's two-pass
  * projector (proj/src/phi.cpp:94-100) up to rounding.  IOP windows always use one
  * classical pass over the window. */
 #define EXPDG_ORTH_CGS2 0
 #define EXPDG_ORTH_DCGS2 1
+#define EXPDG_ORTH_AUTO 2 /* default: DCGS2 from 2^18 DOF up, CGS2 below (launch-latency bound) */
 int expdg_ctx_set_orthogonalization(expdg_ctx* ctx, int mode);
 
 /* Operator factory: replaces BurgersOperator / EulerOperator construction

@@ -199,7 +199,7 @@ def initial_condition(config: int, nx: int, order: int, seed: int, noise: float 
 # ---------------------------------------------------------------- context / operators
 class Context:
     def __init__(self, device: int = 0, orth: Optional[str] = None):
-        """orth: "dcgs2" (default) or "cgs2" for fully orthogonalised phi calls."""
+        """orth: None (auto: DCGS2 from 2^18 DOF up), "dcgs2" or "cgs2" for fully orthogonalised phi calls."""
         import torch
         torch.cuda.init()
         self.device = device

@@ -212,8 +212,9 @@ int expdg_ctx_attach_local(expdg_ctx* ctx, expdg_local_group* g, int rank) {
 int expdg_ctx_set_orthogonalization(expdg_ctx* ctx, int mode) {
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null argument");
-    if (mode != EXPDG_ORTH_CGS2 && mode != EXPDG_ORTH_DCGS2) throw std::invalid_argument("unknown orthogonalization");
-    ctx->eng->use_dcgs = mode;
+    if (mode != EXPDG_ORTH_CGS2 && mode != EXPDG_ORTH_DCGS2 && mode != EXPDG_ORTH_AUTO)
+      throw std::invalid_argument("unknown orthogonalization");
+    ctx->eng->use_dcgs = mode == EXPDG_ORTH_AUTO ? 1 : (mode == EXPDG_ORTH_DCGS2 ? 2 : 0);
   });
 }
 

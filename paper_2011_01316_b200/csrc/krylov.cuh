@@ -91,7 +91,7 @@ class Engine {
  public:
   TsTuning ts_tuning;
   int ld_odd = 1;
-  int use_dcgs = 1;  // DCGS2 for fully orthogonalised calls (EXPDG_ORTH=cgs2 selects CGS2)
+  int use_dcgs = 1;  // 0 CGS2, 1 auto (DCGS2 from 2^18 DOF), 2 DCGS2 (EXPDG_ORTH=cgs2|dcgs2)
   // Set when the context belongs to a slab-partitioned group: every reducing
   // kernel is followed by a sum-allreduce of PhiState::loc -> PhiState::red,
   // and the control runs host-stepped (no CUDA graphs).
