@@ -491,7 +491,9 @@ struct E2Strip {
   static constexpr int ROWS_PER_UNIT = 64;
   static constexpr int FX = (W + 1) * NP * 4;   // x-face fluxes of a row
   static constexpr int FY = W * NP * 4;         // y-face fluxes of one face row
-  static constexpr int SMEM = (NBUF * BUFD + 2 * W * BLK + FX + 2 * FY) * 8;  // ring + sf + face fluxes
+  // ring + double-buffered volume fluxes and x-face fluxes + a 3-deep ring of y-face rows,
+  // so consecutive rows need one CTA barrier between them instead of two
+  static constexpr int SMEM = (NBUF * BUFD + 2 * (2 * W * BLK) + 2 * FX + 3 * FY) * 8;
 };
 
 template <int NP, bool ROE>
@@ -501,9 +503,9 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
   constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;
-  double* sf = smem + NBUF * S::BUFD;
-  double* sfx = sf + 2 * W * BLK;
-  double* sfy = sfx + S::FX;
+  double* sf0 = smem + NBUF * S::BUFD;
+  double* sfx0 = sf0 + 2 * (2 * W * BLK);
+  double* sfy = sfx0 + 2 * S::FX;
   __shared__ uint64_t full[NBUF], empty[NBUF];
   __shared__ double s_wd[NP * NP], s_wq[NP];
   __shared__ int s_go, s_j;
@@ -624,6 +626,8 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
         const double* cur = slot(q);
         const double* lo = slot(q - 1);
         const double* hi = slot(q + 1);
+        double* sf = sf0 + (q & 1) * (2 * W * BLK);
+        double* sfx = sfx0 + (q & 1) * S::FX;
         const double hy = __ldg(P.hy + r);
         const double ihy = __ldg(P.ihy + r);
         double qv[4], tv[4];
@@ -648,8 +652,8 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
         // first row of a unit, the y-faces below it; the y-face row above is the next
         // row's lower face row (2-deep ring)
         {
-          double* ytop = sfy + ((r - r0 + 1) & 1) * S::FY;
-          double* ybot = sfy + ((r - r0) & 1) * S::FY;
+          double* ytop = sfy + ((r - r0 + 1) % 3) * S::FY;
+          double* ybot = sfy + ((r - r0) % 3) * S::FY;
           const int nxf = (w + 1) * NP, nyf = w * NP;
           const int total = nxf + nyf + (r == r0 ? nyf : 0);
           for (int t = tid; t < total; t += 256) {  // the 8 consumer warps
@@ -684,7 +688,8 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
             for (int c = 0; c < 4; ++c) dst[c] = f[c];
           }
         }
-        consumer_sync();
+        consumer_sync();  // A/B of row r done; every thread has also finished C of row r-1
+        if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);  // ring row r-1 is free
         if (active) {
           const double sy = 0.5 * hy * wj;
           double rr[4];
@@ -709,7 +714,7 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
             for (int c = 0; c < 4; ++c) rr[c] = fma(fw, f[c], rr[c]);
           }
           if (j == N || j == 0) {
-            const double* f = sfy + (((r - r0 + (j == N ? 1 : 0)) & 1) * S::FY) + (le * NP + i) * 4;
+            const double* f = sfy + (((r - r0 + (j == N ? 1 : 0)) % 3) * S::FY) + (le * NP + i) * 4;
             const double fw = (j == N ? -0.5 : 0.5) * hx * wi;
 #pragma unroll
             for (int c = 0; c < 4; ++c) rr[c] = fma(fw, f[c], rr[c]);
@@ -730,9 +735,8 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
             nacc = fma(v, v, nacc);
           }
         }
-        consumer_sync();  // rows r-1 .. r fully consumed, sf free
-        if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);
       }
+      consumer_sync();  // C of the unit's last row done
       if (tid == 0) {
         mbar_arrive(&empty[(seq + (r1 - r0)) % NBUF]);      // row r1 - 1
         mbar_arrive(&empty[(seq + (r1 - r0) + 1) % NBUF]);  // row r1 (upper halo)
