@@ -111,8 +111,10 @@ void validate_desc(const expdg_op_desc& d) {
   } else {
     if (!d.periodic) throw std::invalid_argument("EulerOperator: periodic boundaries only");
     if (d.part_end > d.part_begin) {
-      if (d.kind != EXPDG_EULER2D) throw Unsupported("slab partition: 2D Euler only");
-      if (d.part_begin < 0 || d.part_end > d.ny) throw std::invalid_argument("slab partition: rows out of range");
+      if (d.kind != EXPDG_EULER2D && d.kind != EXPDG_EULER3D)
+        throw Unsupported("slab partition: 2D Euler (element rows) and 3D Euler (element planes)");
+      const int layers = d.kind == EXPDG_EULER2D ? d.ny : d.nz;
+      if (d.part_begin < 0 || d.part_end > layers) throw std::invalid_argument("slab partition: layers out of range");
     } else if (d.part_begin != 0 || d.part_end != 0) {
       throw std::invalid_argument("slab partition: empty row range");
     }

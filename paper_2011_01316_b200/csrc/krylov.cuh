@@ -137,6 +137,11 @@ class Engine {
   cudaGraphExec_t build_phi_graph(OpDevice& op, const BArgs& b);
 };
 
+// Halo send buffers <- first / last element layer of the slot the next phi-cycle apply
+// reads (slab-partitioned operators).
+void launch_pack_slot(cudaStream_t s, const PhiState* st, const double* base, long long layer, long long last,
+                      double* lo, double* hi);
+
 // Small utility kernels.
 void launch_axpy_into(cudaStream_t s, double* u, const double* w, long long n);  // u += w
 void launch_copy(cudaStream_t s, double* dst, const double* src, long long n);

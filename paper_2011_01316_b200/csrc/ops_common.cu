@@ -1,6 +1,8 @@
 // Reference-state checks shared by the operators: finiteness (Burgers,
 // proj/src/burgers.cpp:34-35) and Euler admissibility (proj/src/euler.cpp:8-13,
 // :210-211).
+#include <algorithm>
+
 #include "krylov.cuh"
 
 namespace expdg {
@@ -28,6 +30,26 @@ __global__ void k_check_ref(const double* __restrict__ q, long long nelem, int c
     }
     if (!ok) atomicOr(flag, 2);
   }
+}
+
+// First / last owned element layer of Krylov slot j (the vector the next phi-cycle
+// apply reads) into the halo send buffers; no-op unless this cycle applies the operator.
+__global__ void k_pack_slot(const PhiState* st, const double* base, long long layer, long long last,
+                            double* __restrict__ lo, double* __restrict__ hi) {
+  const int a = st->action;
+  if (st->stopped || !(a == ACT_EXTEND || a == ACT_AVNORM)) return;
+  const double* x = base + (size_t)st->j * st->ld;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < layer; i += stride) {
+    lo[i] = x[i];
+    hi[i] = x[last + i];
+  }
+}
+
+void launch_pack_slot(cudaStream_t s, const PhiState* st, const double* base, long long layer, long long last,
+                      double* lo, double* hi) {
+  const long long blocks = std::min<long long>(592, (layer + 255) / 256);
+  k_pack_slot<<<(unsigned)std::max<long long>(1, blocks), 256, 0, s>>>(st, base, layer, last, lo, hi);
 }
 
 int op_check_ref(OpDevice& op, cudaStream_t s, const double* ref) {

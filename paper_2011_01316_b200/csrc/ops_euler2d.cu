@@ -774,20 +774,6 @@ __global__ void k_e2_freeze(const double* __restrict__ q, long long nelem, int n
   }
 }
 
-// First / last owned element row of Krylov slot j (the vector the next phi-cycle
-// apply reads) into the halo send buffers; no-op unless this cycle applies the operator.
-__global__ void k_e2_pack_rows(const PhiState* st, const double* base, long long rowd, long long last,
-                               double* __restrict__ lo, double* __restrict__ hi) {
-  const int a = st->action;
-  if (st->stopped || !(a == ACT_EXTEND || a == ACT_AVNORM)) return;
-  const double* x = base + (size_t)st->j * st->ld;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rowd; i += stride) {
-    lo[i] = x[i];
-    hi[i] = x[last + i];
-  }
-}
-
 double ubreak(double a, double b, int i, int n) { return i == n ? b : a + (b - a) * i / n; }
 
 template <int NP>
@@ -879,7 +865,7 @@ class Euler2D : public OpDevice {
   }
   void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
     if (P.part) {  // halo rows of the slot this cycle applies the operator to
-      k_e2_pack_rows<<<296, 256, 0, s>>>(st, base, rowd, (long long)(P.ny - 1) * rowd, sb_lo(), sb_hi());
+      launch_pack_slot(s, st, base, rowd, (long long)(P.ny - 1) * rowd, sb_lo(), sb_hi());
       comm->halo(sb_lo(), sb_hi(), hx_lo(), hx_hi(), rowd, s);
     }
     const E2P<NP> p = params(frozen);

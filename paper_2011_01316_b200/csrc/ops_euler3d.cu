@@ -26,6 +26,13 @@ struct E3P {
   const double* hy;
   const double* hz;
   long long n;
+  // z-slab partition: planes -1 and nz are the neighbours' halo planes (raw values of the
+  // applied vector / the frozen primitives), exchanged before the kernel runs
+  int part;
+  const double* gx_lo;
+  const double* gx_hi;
+  const double* gt_lo;
+  const double* gt_hi;
 };
 
 struct Prim3 {
@@ -241,13 +248,25 @@ __device__ __forceinline__ void e3_tile(const E3P<NP>& P, int mode, long long e0
     if (a != 0 && a != N) continue;
     const bool owner = a == N;
     int p2[3] = {pos[0], pos[1], pos[2]};
-    p2[d] = owner ? (pos[d] + 1 == nel[d] ? 0 : pos[d] + 1) : (pos[d] == 0 ? nel[d] - 1 : pos[d] - 1);
-    const long long e2 = ((long long)p2[2] * P.ny + p2[1]) * P.nx + p2[0];
+    const int nb = owner ? pos[d] + 1 : pos[d] - 1;
+    p2[d] = nb < 0 ? nel[d] - 1 : (nb >= nel[d] ? 0 : nb);
     int n2[3] = {i, j, k};
     n2[d] = owner ? 0 : N;
     const int node2 = (n2[2] * NP + n2[1]) * NP + n2[0];
     double q2[5], u2[5], f[5];
-    load5<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
+    if (P.part && d == 2 && (nb < 0 || nb >= nel[2])) {  // halo plane of the neighbouring rank
+      const double* gx = nb < 0 ? P.gx_lo : P.gx_hi;
+      const double* gt = nb < 0 ? P.gt_lo : P.gt_hi;
+      const size_t ge = (size_t)p2[1] * P.nx + p2[0];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        q2[c] = gx[(ge * 5 + c) * NN + node2] * xs;
+        u2[c] = need_ut ? gt[(ge * 5 + c) * NN + node2] : 0.0;
+      }
+    } else {
+      const long long e2 = ((long long)p2[2] * P.ny + p2[1]) * P.nx + p2[0];
+      load5<NP>(sx, su, e0, te, e2, node2, x, xs, P.ut, q2, u2, need_ut);
+    }
     if (owner) face3(mode, d, P.gamma, q, q2, ut, u2, f, bad);
     else face3(mode, d, P.gamma, q2, q, u2, ut, f, bad);
     // face quadrature weight (1/4 area) w_t1 w_t2 with (t1, t2) the two tangential node indices
@@ -388,21 +407,44 @@ class Euler3D : public OpDevice {
   int grid = 1;
   double* frozen = nullptr;
   double* hbuf = nullptr;
+  double* halo = nullptr;  // slab partition: x lo/hi, frozen lo/hi, send lo/hi planes
+  long long plane = 0;     // doubles per element plane
   ~Euler3D() override {
     cudaFree(frozen);
     cudaFree(hbuf);
+    cudaFree(halo);
+  }
+  double* hb_(int q) const { return halo + (size_t)q * plane; }
+  void exchange(cudaStream_t s, const double* v, double* lo, double* hi) {
+    comm->halo(v, v + (size_t)(P.nz - 1) * plane, lo, hi, plane, s);
+  }
+  E3P<NP> params(const double* ut) const {
+    E3P<NP> p = P;
+    p.ut = ut;
+    if (p.part) {
+      p.gx_lo = hb_(0);
+      p.gx_hi = hb_(1);
+      p.gt_lo = hb_(2);
+      p.gt_hi = hb_(3);
+    }
+    return p;
   }
   explicit Euler3D(const expdg_op_desc& d) {
     desc = d;
     const HostBasis hb = host_lgl_basis(d.order);
+    const bool part = d.part_end > d.part_begin;
+    const int z0 = part ? d.part_begin : 0;
+    const int nzl = part ? d.part_end - d.part_begin : d.nz;
     P.nx = d.nx;
     P.ny = d.ny;
-    P.nz = d.nz;
+    P.nz = nzl;
+    P.part = part ? 1 : 0;
     P.gamma = d.gamma;
-    std::vector<double> hs(d.nx + d.ny + d.nz);
+    std::vector<double> hs(d.nx + d.ny + nzl);
     for (int i = 0; i < d.nx; ++i) hs[i] = ub3(d.x0, d.x1, i + 1, d.nx) - ub3(d.x0, d.x1, i, d.nx);
     for (int j = 0; j < d.ny; ++j) hs[d.nx + j] = ub3(d.y0, d.y1, j + 1, d.ny) - ub3(d.y0, d.y1, j, d.ny);
-    for (int k = 0; k < d.nz; ++k) hs[d.nx + d.ny + k] = ub3(d.z0, d.z1, k + 1, d.nz) - ub3(d.z0, d.z1, k, d.nz);
+    for (int k = 0; k < nzl; ++k)
+      hs[d.nx + d.ny + k] = ub3(d.z0, d.z1, z0 + k + 1, d.nz) - ub3(d.z0, d.z1, z0 + k, d.nz);
     EXPDG_CUDA(cudaMalloc(&hbuf, sizeof(double) * hs.size()));
     EXPDG_CUDA(cudaMemcpy(hbuf, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice));
     P.hx = hbuf;
@@ -412,31 +454,38 @@ class Euler3D : public OpDevice {
       P.w[a] = hb.weights[a];
       for (int b2 = 0; b2 < NP; ++b2) P.WD[a * NP + b2] = hb.weights[a] * hb.D[a * NP + b2];
     }
-    n = (long long)d.nx * d.ny * d.nz * NP * NP * NP * 5;
+    n = (long long)d.nx * d.ny * nzl * NP * NP * NP * 5;
     P.n = n;
     comps = 5;
+    plane = (long long)d.nx * d.ny * NP * NP * NP * 5;
     EXPDG_CUDA(cudaMalloc(&frozen, sizeof(double) * n));
-    const long long ntiles = ((long long)d.nx * d.ny * d.nz + E3Tile<NP>::TE - 1) / E3Tile<NP>::TE;
+    if (part) {
+      EXPDG_CUDA(cudaMalloc(&halo, sizeof(double) * 6 * plane));
+      EXPDG_CUDA(cudaMemset(halo, 0, sizeof(double) * 6 * plane));
+    }
+    const long long ntiles = ((long long)d.nx * d.ny * nzl + E3Tile<NP>::TE - 1) / E3Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
   }
   void freeze(cudaStream_t s, const double* r) override {
     ref = r;
     k_e3_freeze<<<1184, 256, 0, s>>>(r, (long long)P.nx * P.ny * P.nz, NP * NP * NP, P.gamma, frozen);
+    if (P.part) exchange(s, frozen, hb_(2), hb_(3));
   }
   void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
-    E3P<NP> p = P;
-    p.ut = frozen;
-    k_e3_phi<NP><<<grid, 256, 0, s>>>(p, st, base, partials, b);
+    if (P.part) {  // halo planes of the slot this cycle applies the operator to
+      launch_pack_slot(s, st, base, plane, (long long)(P.nz - 1) * plane, hb_(4), hb_(5));
+      comm->halo(hb_(4), hb_(5), hb_(0), hb_(1), plane, s);
+    }
+    k_e3_phi<NP><<<grid, 256, 0, s>>>(params(frozen), st, base, partials, b);
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
-    E3P<NP> p = P;
-    p.ut = frozen;
-    k_e3_apply<NP><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
+    if (P.part) exchange(s, x, hb_(0), hb_(1));
+    k_e3_apply<NP><<<grid, 256, 0, s>>>(params(frozen), which, x, y, nullptr, nullptr);
   }
   void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
-    E3P<NP> p = P;
-    p.ut = nullptr;
-    k_e3_apply<NP><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
+    if (P.part) exchange(s, u, hb_(0), hb_(1));
+    k_e3_apply<NP><<<grid, 256, 0, s>>>(params(nullptr), 2, u, r, st, frozen);
+    if (P.part) exchange(s, frozen, hb_(2), hb_(3));  // frozen halo for this step's JVPs
   }
 };
 

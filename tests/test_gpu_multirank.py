@@ -139,3 +139,38 @@ def test_partitioned_blow_up_is_collective():
     got = run_ranks(2, fn)
     assert [g.status for g in got] == ["blew_up", "blew_up"]
     assert [g.blow_up_step for g in got] == [1, 1]
+
+
+@pytest.mark.parametrize("parts", [2, 3])
+def test_partitioned_euler3d_matches_single_rank(parts):
+    # C5 physics (3D LF Euler, Taylor-Green) on 6^3 elements, z-plane slabs
+    w = configs.scaled(configs.C5, 6, steps=2)
+    spec = w.spec()
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    ctx = pkg.Context(0)
+    op = pkg.Operator(ctx, spec)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(u0.size)
+    op.linearize(to_dev(u0))
+    lin = to_host(op.apply_linear(to_dev(x)))
+    single = pkg.integrate(ctx, op, to_dev(u0), "epi2", dt, w.steps * dt, **kw)
+    ranges = slab_ranges(spec.nz, parts)
+    plane = spec.nx * spec.ny * (spec.order + 1) ** 3 * 5
+
+    def fn(r, c):
+        o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": ranges[r]}))
+        sl = slice(ranges[r][0] * plane, ranges[r][1] * plane)
+        o.linearize(to_dev(u0[sl]))
+        y = to_host(o.apply_linear(to_dev(x[sl])))
+        res = pkg.integrate(c, o, to_dev(u0[sl]), "epi2", dt, w.steps * dt, **kw)
+        return y, res, to_host(res.u)
+
+    got = run_ranks(parts, fn)
+    assert rel(np.concatenate([g[0] for g in got]), lin) < 1e-14
+    assert all(g[1].status == "completed" for g in got)
+    assert rel(np.concatenate([g[2] for g in got]), to_host(single.u)) <= 1e-11
+    d_part = np.diff(np.concatenate([[0], got[0][1].iters_per_step]))
+    d_single = np.diff(np.concatenate([[0], single.iters_per_step]))
+    assert np.max(np.abs(d_part - d_single)) <= 1
