@@ -21,8 +21,49 @@ struct B1P {
   double Lv[NP * NP];  // lift_vol(i,j) = D(j,i) w_j      (proj/src/burgers.cpp:50)
   const double* ut;
   const double* src;   // weak source (proj/src/burgers.cpp:80-92), may be null
-  long long n;
+  long long n;  // slab partition: this rank owns elements [eoff, eoff + nel) of the
+  // ne-element mesh; the H elements either side come from the halo buffers
+  int nel;
+  long long eoff;
+  int part;
+  const double* gx_lo;
+  const double* gx_hi;
+  const double* gt_lo;
+  const double* gt_hi;
 };
+
+// Stages local elements [e0 - H, e0 + E + H) of x (scaled by xs) and u~ into shared
+// memory: zero-Dirichlet ghosts outside the global mesh, periodic wrap when the mesh is
+// whole, the neighbouring rank's halo elements when it is slab-partitioned.
+template <int NP, int H, class PP>
+__device__ __forceinline__ void stage_elements(const PP& P, long long e0, int E, const double* x, double xs,
+                                               bool want_ut, double* sx, double* su) {
+  const int cnt = (E + 2 * H) * NP;
+  for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
+    const long long le = e0 - H + idx / NP;
+    const int node = idx % NP;
+    const long long gg = P.eoff + le;
+    double xv = 0.0, uv = 0.0;
+    if ((gg < 0 || gg >= P.ne) && !P.periodic) {
+      // outside the interval: zero Dirichlet data
+    } else if (le < 0 || le >= P.nel) {
+      if (P.part) {
+        const size_t hi = le < 0 ? (size_t)((le + H) * NP + node) : (size_t)((le - P.nel) * NP + node);
+        xv = (le < 0 ? P.gx_lo : P.gx_hi)[hi] * xs;
+        if (want_ut) uv = (le < 0 ? P.gt_lo : P.gt_hi)[hi];
+      } else {
+        const long long w = ((le % P.nel) + P.nel) % P.nel;
+        xv = x[w * NP + node] * xs;
+        if (want_ut) uv = P.ut[w * NP + node];
+      }
+    } else {
+      xv = x[le * NP + node] * xs;
+      if (want_ut) uv = P.ut[le * NP + node];
+    }
+    sx[idx] = xv;
+    su[idx] = uv;
+  }
+}
 
 // x_e of the uniform breakpoints (proj/src/mesh.cpp:11-16)
 __device__ __forceinline__ double b1_break(double a, double b, int i, int ne) {
@@ -129,7 +170,7 @@ __device__ __forceinline__ void b1_element(const B1P<NP>& P, int mode, int e, co
   }
   if (mode != 0 && P.src) {
 #pragma unroll
-    for (int i = 0; i < NP; ++i) r[i] += P.src[(long long)e * NP + i];
+    for (int i = 0; i < NP; ++i) r[i] += P.src[(long long)(e - P.eoff) * NP + i];
   }
   // faces (proj/src/burgers.cpp:159-173)
   if (hasL) {
@@ -215,6 +256,15 @@ struct B1OP {
   const double* ut;
   const double* src;    // weak source (proj/src/burgers.cpp:80-92), may be null
   long long n;
+  // slab partition: this rank owns elements [eoff, eoff + nel) of the
+  // ne-element mesh; the H elements either side come from the halo buffers
+  int nel;
+  long long eoff;
+  int part;
+  const double* gx_lo;
+  const double* gx_hi;
+  const double* gt_lo;
+  const double* gt_hi;
 };
 
 // r of one element's LDG gradient system before the mass solve (proj/src/burgers.cpp:105-123):
@@ -306,7 +356,7 @@ __device__ __forceinline__ void b1oi_element(const B1OP<NP, NQ>& P, int mode, in
   for (int i = 0; i < NP; ++i) r[i] = -r[i];
   if (mode != 0 && P.src) {
 #pragma unroll
-    for (int i = 0; i < NP; ++i) r[i] += P.src[(long long)e * NP + i];
+    for (int i = 0; i < NP; ++i) r[i] += P.src[(long long)(e - P.eoff) * NP + i];
   }
   // faces: identical to the collocated operator (traces are nodal end values)
   B1P<NP> F{};

@@ -110,16 +110,18 @@ void validate_desc(const expdg_op_desc& d) {
       throw Unsupported("over-integrated 2D Burgers is not on the device path");
   } else {
     if (!d.periodic) throw std::invalid_argument("EulerOperator: periodic boundaries only");
-    if (d.part_end > d.part_begin) {
-      if (d.kind != EXPDG_EULER2D && d.kind != EXPDG_EULER3D)
-        throw Unsupported("slab partition: 2D Euler (element rows) and 3D Euler (element planes)");
-      const int layers = d.kind == EXPDG_EULER2D ? d.ny : d.nz;
-      if (d.part_begin < 0 || d.part_end > layers) throw std::invalid_argument("slab partition: layers out of range");
-    } else if (d.part_begin != 0 || d.part_end != 0) {
-      throw std::invalid_argument("slab partition: empty row range");
-    }
     if (d.euler_flux != 1 && d.kind == EXPDG_EULER3D)
       throw Unsupported("3D Euler: Lax-Friedrichs flux only (the Roe flux is 2D, proj/src/euler.cpp:114-145)");
+  }
+  if (d.part_end > d.part_begin) {
+    if (d.kind != EXPDG_EULER2D && d.kind != EXPDG_EULER3D && d.kind != EXPDG_BURGERS1D)
+      throw Unsupported("slab partition: 1D Burgers (elements), 2D Euler (element rows), 3D Euler (planes)");
+    const int layers = d.kind == EXPDG_EULER2D ? d.ny : (d.kind == EXPDG_EULER3D ? d.nz : d.nx);
+    if (d.part_begin < 0 || d.part_end > layers) throw std::invalid_argument("slab partition: layers out of range");
+    if (d.kind == EXPDG_BURGERS1D && d.part_end - d.part_begin < (d.over_integrate ? 2 : 1))
+      throw std::invalid_argument("slab partition: over-integrated Burgers needs two elements per rank");
+  } else if (d.part_begin != 0 || d.part_end != 0) {
+    throw std::invalid_argument("slab partition: empty row range");
   }
 }
 
@@ -310,8 +312,10 @@ int expdg_op_set_source_fn(expdg_op* op, double (*source)(double x, void* user),
     if (!op || !source) throw std::invalid_argument("null argument");
     const expdg_op_desc& d = op->dev->desc;
     if (d.kind != EXPDG_BURGERS1D) throw std::invalid_argument("source terms are 1D Burgers only");
-    std::vector<double> w((size_t)op->dev->n);
-    host_burgers_source(d.order, d.nx, d.x0, d.x1, d.over_integrate != 0, source, user, w.data());
+    std::vector<double> wg((size_t)d.nx * (d.order + 1));
+    host_burgers_source(d.order, d.nx, d.x0, d.x1, d.over_integrate != 0, source, user, wg.data());
+    const size_t off = (size_t)(d.part_end > d.part_begin ? d.part_begin : 0) * (d.order + 1);
+    std::vector<double> w(wg.begin() + off, wg.begin() + off + (size_t)op->dev->n);  // owned elements
     cudaStream_t s = op->ctx->eng->stream;
     double* tmp = nullptr;
     EXPDG_CUDA(cudaMallocAsync(&tmp, sizeof(double) * w.size(), s));

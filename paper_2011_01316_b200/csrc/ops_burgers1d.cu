@@ -18,47 +18,23 @@ namespace {
 using namespace burgers;
 constexpr int kB1Threads = 128;
 
-// Stage [e0-1, e0+E] of x (scaled by xs) and u~ into shared memory.
-template <int NP>
-__device__ __forceinline__ void b1_stage(const B1P<NP>& P, long long e0, int E, const double* x, double xs,
-                                         bool want_ut, double* sx, double* su) {
-  const int cnt = (E + 2) * NP;
-  for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
-    long long ge = e0 - 1 + idx / NP;
-    const int node = idx % NP;
-    double xv = 0.0, uv = 0.0;
-    if (ge < 0 || ge >= P.ne) {
-      if (P.periodic) {
-        ge = (ge + P.ne) % P.ne;
-        xv = x[ge * NP + node] * xs;
-        if (want_ut) uv = P.ut[ge * NP + node];
-      }
-    } else {
-      xv = x[ge * NP + node] * xs;
-      if (want_ut) uv = P.ut[ge * NP + node];
-    }
-    sx[idx] = xv;
-    su[idx] = uv;
-  }
-}
-
 // Standalone apply: y = L x | N x | rhs(x).
 template <int NP>
 __global__ void __launch_bounds__(kB1Threads) k_b1_apply(B1P<NP> P, int mode, const double* __restrict__ x,
                                                          double* __restrict__ y, const PhiState* st) {
   __shared__ double sx[(kB1Threads + 2) * NP], su[(kB1Threads + 2) * NP], sy[kB1Threads * NP];
   if (st && st->stopped) return;
-  const int ntiles = (P.ne + kB1Threads - 1) / kB1Threads;
+  const int ntiles = (P.nel + kB1Threads - 1) / kB1Threads;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long e0 = (long long)tile * kB1Threads;
-    const int E = (int)(P.ne - e0 < kB1Threads ? P.ne - e0 : kB1Threads);
+    const int E = (int)(P.nel - e0 < kB1Threads ? P.nel - e0 : kB1Threads);
     __syncthreads();
-    b1_stage(P, e0, E, x, 1.0, mode != 2, sx, su);
+    stage_elements<NP, 1>(P, e0, E, x, 1.0, mode != 2, sx, su);
     __syncthreads();
     const int t = threadIdx.x;
     if (t < E) {
       double out[NP];
-      b1_element<NP>(P, mode, (int)(e0 + t), sx + t * NP, sx + (t + 1) * NP, sx + (t + 2) * NP, su + t * NP,
+      b1_element<NP>(P, mode, (int)(P.eoff + e0 + t), sx + t * NP, sx + (t + 1) * NP, sx + (t + 2) * NP, su + t * NP,
                      su + (t + 1) * NP, su + (t + 2) * NP, out);
 #pragma unroll
       for (int i = 0; i < NP; ++i) sy[t * NP + i] = out[i];
@@ -97,17 +73,17 @@ __global__ void __launch_bounds__(kB1Threads) k_b1_phi(B1P<NP> P, PhiState* st, 
   double* y = base + (size_t)(s_j + 1) * s_ld;
   const double xs = s_xs, dt = s_dt;
   double nacc = 0.0;
-  const int ntiles = (P.ne + kB1Threads - 1) / kB1Threads;
+  const int ntiles = (P.nel + kB1Threads - 1) / kB1Threads;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long e0 = (long long)tile * kB1Threads;
-    const int E = (int)(P.ne - e0 < kB1Threads ? P.ne - e0 : kB1Threads);
+    const int E = (int)(P.nel - e0 < kB1Threads ? P.nel - e0 : kB1Threads);
     __syncthreads();
-    b1_stage(P, e0, E, x, xs, true, sx, su);
+    stage_elements<NP, 1>(P, e0, E, x, xs, true, sx, su);
     __syncthreads();
     const int t = threadIdx.x;
     if (t < E) {
       double out[NP];
-      b1_element<NP>(P, 0, (int)(e0 + t), sx + t * NP, sx + (t + 1) * NP, sx + (t + 2) * NP, su + t * NP,
+      b1_element<NP>(P, 0, (int)(P.eoff + e0 + t), sx + t * NP, sx + (t + 1) * NP, sx + (t + 2) * NP, su + t * NP,
                      su + (t + 1) * NP, su + (t + 2) * NP, out);
 #pragma unroll
       for (int i = 0; i < NP; ++i) sy[t * NP + i] = out[i];
@@ -135,21 +111,26 @@ __global__ void __launch_bounds__(kB1Threads) k_b1_phi(B1P<NP> P, PhiState* st, 
   grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
-template <int NP>
-class Burgers1D : public OpDevice {
+// Mesh / slab-partition plumbing shared by the 1D Burgers operators (halo depth H
+// elements: 1 collocated, 2 over-integrated).  Partitioned operators own elements
+// [part_begin, part_end) and exchange H elements with each periodic neighbour
+// before every application (the reference mesh is one interval).
+template <class PP, int NP, int H>
+class B1Base : public OpDevice {
  public:
-  B1P<NP> P{};
+  PP P{};
   int grid = 1;
   double* src = nullptr;
-  ~Burgers1D() override { cudaFree(src); }
-  void set_source(cudaStream_t s, const double* weak) override {
-    if (!src) EXPDG_CUDA(cudaMalloc(&src, sizeof(double) * n));
-    EXPDG_CUDA(cudaMemcpyAsync(src, weak, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    P.src = src;
+  double* halo = nullptr;  // x lo/hi, u~ lo/hi, send lo/hi: H NP doubles each
+  long long layer = 0;
+  ~B1Base() override {
+    cudaFree(src);
+    cudaFree(halo);
   }
-  explicit Burgers1D(const expdg_op_desc& d) {
+  double* hq(int i) const { return halo + (size_t)i * layer; }
+  void init_mesh(const expdg_op_desc& d) {
     desc = d;
-    const HostBasis hb = host_lgl_basis(d.order);
+    const bool part = d.part_end > d.part_begin;
     P.ne = d.nx;
     P.periodic = d.periodic;
     P.a = d.x0;
@@ -158,80 +139,116 @@ class Burgers1D : public OpDevice {
     P.sigma = d.sigma;
     P.entropy = d.flux == 1;
     P.sigma_adaptive = d.sigma_adaptive;
-    for (int i = 0; i < NP; ++i) {
-      P.w[i] = hb.weights[i];
-      for (int j = 0; j < NP; ++j) {
-        P.G[i * NP + j] = hb.weights[i] * hb.D[i * NP + j];
-        P.Lv[i * NP + j] = hb.D[j * NP + i] * hb.weights[j];
-      }
-    }
-    n = (long long)d.nx * NP;
+    P.eoff = part ? d.part_begin : 0;
+    P.nel = part ? d.part_end - d.part_begin : d.nx;
+    P.part = part ? 1 : 0;
+    n = (long long)P.nel * NP;
     P.n = n;
     comps = 1;
-    const int ntiles = (d.nx + kB1Threads - 1) / kB1Threads;
+    layer = (long long)H * NP;
+    if (part) {
+      EXPDG_CUDA(cudaMalloc(&halo, sizeof(double) * 6 * layer));
+      EXPDG_CUDA(cudaMemset(halo, 0, sizeof(double) * 6 * layer));
+    }
+    const int ntiles = (P.nel + kB1Threads - 1) / kB1Threads;
     grid = std::max(1, std::min(ntiles, 148 * 8));
   }
+  void exchange(cudaStream_t s, const double* v, double* lo, double* hi) {
+    comm->halo(v, v + (size_t)(P.nel - H) * NP, lo, hi, layer, s);
+  }
+  PP params(const double* ut) const {
+    PP p = P;
+    p.ut = ut;
+    if (p.part) {
+      p.gx_lo = hq(0);
+      p.gx_hi = hq(1);
+      p.gt_lo = hq(2);
+      p.gt_hi = hq(3);
+    }
+    return p;
+  }
+  virtual void run_phi(cudaStream_t s, const PP& p, PhiState* st, double* base, double* partials,
+                       const BArgs& b) = 0;
+  virtual void run_apply(cudaStream_t s, const PP& p, int mode, const double* x, double* y, const PhiState* st) = 0;
+
+  void set_source(cudaStream_t s, const double* weak) override {
+    if (!src) EXPDG_CUDA(cudaMalloc(&src, sizeof(double) * n));
+    EXPDG_CUDA(cudaMemcpyAsync(src, weak, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    P.src = src;
+  }
+  void freeze(cudaStream_t s, const double* r) override {
+    ref = r;
+    if (P.part) exchange(s, r, hq(2), hq(3));
+  }
   void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
-    B1P<NP> p = P;
-    p.ut = ref;
-    k_b1_phi<NP><<<grid, kB1Threads, 0, s>>>(p, st, base, partials, b);
+    if (P.part) {  // halo elements of the slot this cycle applies the operator to
+      launch_pack_slot(s, st, base, layer, (long long)(P.nel - H) * NP, hq(4), hq(5));
+      comm->halo(hq(4), hq(5), hq(0), hq(1), layer, s);
+    }
+    run_phi(s, params(ref), st, base, partials, b);
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
-    B1P<NP> p = P;
-    p.ut = ref;
-    k_b1_apply<NP><<<grid, kB1Threads, 0, s>>>(p, which, x, y, nullptr);
+    if (P.part) exchange(s, x, hq(0), hq(1));
+    run_apply(s, params(ref), which, x, y, nullptr);
   }
+  // R at u~ = u; u's halo serves both the applied vector and u~ (and this step's JVPs)
   void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
-    B1P<NP> p = P;
-    p.ut = u;
-    k_b1_apply<NP><<<grid, kB1Threads, 0, s>>>(p, 2, u, r, st);
+    PP p = params(u);
+    if (P.part) {
+      exchange(s, u, hq(2), hq(3));
+      p.gx_lo = hq(2);
+      p.gx_hi = hq(3);
+    }
+    run_apply(s, p, 2, u, r, st);
+  }
+};
+
+template <int NP>
+class Burgers1D : public B1Base<B1P<NP>, NP, 1> {
+ public:
+  using B = B1Base<B1P<NP>, NP, 1>;
+  explicit Burgers1D(const expdg_op_desc& d) {
+    const HostBasis hb = host_lgl_basis(d.order);
+    this->init_mesh(d);
+    for (int i = 0; i < NP; ++i) {
+      this->P.w[i] = hb.weights[i];
+      for (int j = 0; j < NP; ++j) {
+        this->P.G[i * NP + j] = hb.weights[i] * hb.D[i * NP + j];
+        this->P.Lv[i * NP + j] = hb.D[j * NP + i] * hb.weights[j];
+      }
+    }
+  }
+  void run_phi(cudaStream_t s, const B1P<NP>& p, PhiState* st, double* base, double* partials,
+               const BArgs& b) override {
+    k_b1_phi<NP><<<this->grid, kB1Threads, 0, s>>>(p, st, base, partials, b);
+  }
+  void run_apply(cudaStream_t s, const B1P<NP>& p, int mode, const double* x, double* y,
+                 const PhiState* st) override {
+    k_b1_apply<NP><<<this->grid, kB1Threads, 0, s>>>(p, mode, x, y, st);
   }
 };
 
 // ---------------------------------------------------------------- over-integrated 1D Burgers
-// Stage [e0-2, e0+E+1] (two-element halo: the dense consistent-mass solve makes
-// a neighbour's face q depend on its other face).
-template <int NP, int NQ>
-__device__ __forceinline__ void b1oi_stage(const B1OP<NP, NQ>& P, long long e0, int E, const double* x, double xs,
-                                           bool want_ut, double* sx, double* su) {
-  const int cnt = (E + 4) * NP;
-  for (int idx = threadIdx.x; idx < cnt; idx += blockDim.x) {
-    long long ge = e0 - 2 + idx / NP;
-    const int node = idx % NP;
-    double xv = 0.0, uv = 0.0;
-    if (ge < 0 || ge >= P.ne) {
-      if (P.periodic) {
-        ge = ((ge % P.ne) + P.ne) % P.ne;
-        xv = x[ge * NP + node] * xs;
-        if (want_ut) uv = P.ut[ge * NP + node];
-      }
-    } else {
-      xv = x[ge * NP + node] * xs;
-      if (want_ut) uv = P.ut[ge * NP + node];
-    }
-    sx[idx] = xv;
-    su[idx] = uv;
-  }
-}
-
+// Over-integrated kernels stage a two-element halo: the dense consistent-mass solve
+// makes a neighbour's face q depend on its other face.
 template <int NP, int NQ>
 __global__ void __launch_bounds__(kB1Threads) k_b1oi_apply(B1OP<NP, NQ> P, int mode, const double* __restrict__ x,
                                                            double* __restrict__ y, const PhiState* st) {
   __shared__ double sx[(kB1Threads + 4) * NP], su[(kB1Threads + 4) * NP], sy[kB1Threads * NP];
   if (st && st->stopped) return;
-  const int ntiles = (P.ne + kB1Threads - 1) / kB1Threads;
+  const int ntiles = (P.nel + kB1Threads - 1) / kB1Threads;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long e0 = (long long)tile * kB1Threads;
-    const int E = (int)(P.ne - e0 < kB1Threads ? P.ne - e0 : kB1Threads);
+    const int E = (int)(P.nel - e0 < kB1Threads ? P.nel - e0 : kB1Threads);
     __syncthreads();
-    b1oi_stage(P, e0, E, x, 1.0, mode != 2, sx, su);
+    stage_elements<NP, 2>(P, e0, E, x, 1.0, mode != 2, sx, su);
     __syncthreads();
     const int t = threadIdx.x;
     if (t < E) {
       double out[NP];
       const double* b = sx + (t + 2) * NP;
       const double* ub = su + (t + 2) * NP;
-      b1oi_element<NP, NQ>(P, mode, (int)(e0 + t), b - 2 * NP, b - NP, b, b + NP, b + 2 * NP, ub - NP, ub, ub + NP,
+      b1oi_element<NP, NQ>(P, mode, (int)(P.eoff + e0 + t), b - 2 * NP, b - NP, b, b + NP, b + 2 * NP, ub - NP, ub, ub + NP,
                            out);
 #pragma unroll
       for (int i = 0; i < NP; ++i) sy[t * NP + i] = out[i];
@@ -268,19 +285,19 @@ __global__ void __launch_bounds__(kB1Threads) k_b1oi_phi(B1OP<NP, NQ> P, PhiStat
   double* y = base + (size_t)(s_j + 1) * s_ld;
   const double xs = s_xs, dt = s_dt;
   double nacc = 0.0;
-  const int ntiles = (P.ne + kB1Threads - 1) / kB1Threads;
+  const int ntiles = (P.nel + kB1Threads - 1) / kB1Threads;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long long e0 = (long long)tile * kB1Threads;
-    const int E = (int)(P.ne - e0 < kB1Threads ? P.ne - e0 : kB1Threads);
+    const int E = (int)(P.nel - e0 < kB1Threads ? P.nel - e0 : kB1Threads);
     __syncthreads();
-    b1oi_stage(P, e0, E, x, xs, true, sx, su);
+    stage_elements<NP, 2>(P, e0, E, x, xs, true, sx, su);
     __syncthreads();
     const int t = threadIdx.x;
     if (t < E) {
       double out[NP];
       const double* bb = sx + (t + 2) * NP;
       const double* ub = su + (t + 2) * NP;
-      b1oi_element<NP, NQ>(P, 0, (int)(e0 + t), bb - 2 * NP, bb - NP, bb, bb + NP, bb + 2 * NP, ub - NP, ub,
+      b1oi_element<NP, NQ>(P, 0, (int)(P.eoff + e0 + t), bb - 2 * NP, bb - NP, bb, bb + NP, bb + 2 * NP, ub - NP, ub,
                            ub + NP, out);
 #pragma unroll
       for (int i = 0; i < NP; ++i) sy[t * NP + i] = out[i];
@@ -309,57 +326,28 @@ __global__ void __launch_bounds__(kB1Threads) k_b1oi_phi(B1OP<NP, NQ> P, PhiStat
 }
 
 template <int NP, int NQ>
-class Burgers1DOI : public OpDevice {
+class Burgers1DOI : public B1Base<B1OP<NP, NQ>, NP, 2> {
  public:
-  B1OP<NP, NQ> P{};
-  int grid = 1;
-  double* src = nullptr;
-  ~Burgers1DOI() override { cudaFree(src); }
   explicit Burgers1DOI(const expdg_op_desc& d) {
-    desc = d;
     const HostOI o = host_burgers_oi(d.order);
     if (o.nq != NQ) throw std::invalid_argument("burgers1d: over-integration rule mismatch");
-    P.ne = d.nx;
-    P.periodic = d.periodic;
-    P.a = d.x0;
-    P.b = d.x1;
-    P.kappa = d.kappa;
-    P.sigma = d.sigma;
-    P.entropy = d.flux == 1;
-    P.sigma_adaptive = d.sigma_adaptive;
+    this->init_mesh(d);
     for (int i = 0; i < NP * NP; ++i) {
-      P.G[i] = o.G[i];
-      P.Mi[i] = o.Mi[i];
+      this->P.G[i] = o.G[i];
+      this->P.Mi[i] = o.Mi[i];
     }
     for (int i = 0; i < NP * NQ; ++i) {
-      P.Lv[i] = o.Lv[i];
-      P.I[i] = o.I[i];
+      this->P.Lv[i] = o.Lv[i];
+      this->P.I[i] = o.I[i];
     }
-    n = (long long)d.nx * NP;
-    P.n = n;
-    comps = 1;
-    const int ntiles = (d.nx + kB1Threads - 1) / kB1Threads;
-    grid = std::max(1, std::min(ntiles, 148 * 8));
   }
-  void set_source(cudaStream_t s, const double* weak) override {
-    if (!src) EXPDG_CUDA(cudaMalloc(&src, sizeof(double) * n));
-    EXPDG_CUDA(cudaMemcpyAsync(src, weak, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    P.src = src;
+  void run_phi(cudaStream_t s, const B1OP<NP, NQ>& p, PhiState* st, double* base, double* partials,
+               const BArgs& b) override {
+    k_b1oi_phi<NP, NQ><<<this->grid, kB1Threads, 0, s>>>(p, st, base, partials, b);
   }
-  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
-    B1OP<NP, NQ> p = P;
-    p.ut = ref;
-    k_b1oi_phi<NP, NQ><<<grid, kB1Threads, 0, s>>>(p, st, base, partials, b);
-  }
-  void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
-    B1OP<NP, NQ> p = P;
-    p.ut = ref;
-    k_b1oi_apply<NP, NQ><<<grid, kB1Threads, 0, s>>>(p, which, x, y, nullptr);
-  }
-  void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
-    B1OP<NP, NQ> p = P;
-    p.ut = u;
-    k_b1oi_apply<NP, NQ><<<grid, kB1Threads, 0, s>>>(p, 2, u, r, st);
+  void run_apply(cudaStream_t s, const B1OP<NP, NQ>& p, int mode, const double* x, double* y,
+                 const PhiState* st) override {
+    k_b1oi_apply<NP, NQ><<<this->grid, kB1Threads, 0, s>>>(p, mode, x, y, st);
   }
 };
 

@@ -174,3 +174,49 @@ def test_partitioned_euler3d_matches_single_rank(parts):
     d_part = np.diff(np.concatenate([[0], got[0][1].iters_per_step]))
     d_single = np.diff(np.concatenate([[0], single.iters_per_step]))
     assert np.max(np.abs(d_part - d_single)) <= 1
+
+
+@pytest.mark.parametrize("oi", [False, True])
+@pytest.mark.parametrize("periodic", [True, False])
+@pytest.mark.parametrize("parts", [2, 3])
+def test_partitioned_burgers1d_matches_single_rank(parts, periodic, oi):
+    # element ranges of one interval (C2's partition), collocated and over-integrated,
+    # periodic and zero-Dirichlet, with the MMS-style weak source on the over-integrated case
+    import math
+    k, ne = 3, 24
+    spec = pkg.OperatorSpec("burgers1d", k, ne, box=(0.0, 2 * math.pi, 0, 1, 0, 1), periodic=periodic, kappa=0.02,
+                            flux="ef", sigma=1e-3, over_integrate=oi)
+    rng = np.random.default_rng(11)
+    u0 = 0.5 + 0.3 * np.sin(np.linspace(0, 2 * math.pi, ne * (k + 1)))
+    x = rng.standard_normal(u0.size)
+    src = lambda s: 0.1 * math.cos(s)  # noqa: E731
+    ctx = pkg.Context(0)
+    op = pkg.Operator(ctx, spec)
+    if oi:
+        op.set_source_function(src)
+    op.linearize(to_dev(u0))
+    want = [to_host(op.apply_linear(to_dev(x))), to_host(op.apply_nonlinear(to_dev(x))),
+            to_host(op.full_rhs(to_dev(x)))]
+    kw = dict(tol=1e-10, max_basis=30, orth_length=30)
+    single = pkg.integrate(ctx, op, to_dev(u0), "epi2", 0.05, 0.2, **kw)
+    ranges = slab_ranges(ne, parts)
+
+    def fn(r, c):
+        o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": ranges[r]}))
+        if oi:
+            o.set_source_function(src)
+        sl = slice(ranges[r][0] * (k + 1), ranges[r][1] * (k + 1))
+        o.linearize(to_dev(u0[sl]))
+        ys = [to_host(o.apply_linear(to_dev(x[sl]))), to_host(o.apply_nonlinear(to_dev(x[sl]))),
+              to_host(o.full_rhs(to_dev(x[sl])))]
+        res = pkg.integrate(c, o, to_dev(u0[sl]), "epi2", 0.05, 0.2, **kw)
+        return ys, res, to_host(res.u)
+
+    got = run_ranks(parts, fn)
+    for i in range(3):
+        assert rel(np.concatenate([g[0][i] for g in got]), want[i]) < 1e-14
+    assert all(g[1].status == single.status == "completed" for g in got)
+    assert rel(np.concatenate([g[2] for g in got]), to_host(single.u)) <= 1e-11
+    d_part = np.diff(np.concatenate([[0], got[0][1].iters_per_step]))
+    d_single = np.diff(np.concatenate([[0], single.iters_per_step]))
+    assert np.max(np.abs(d_part - d_single)) <= 1
