@@ -69,8 +69,8 @@ typedef struct {
   double gamma;        /* Euler */
   int euler_flux;      /* 0 roe (2D only, proj/src/euler.cpp:114-145), 1 lax_friedrichs */
   /* Slab partition (0, 0 = the whole mesh): this rank owns the element
-   * layers [part_begin, part_end) along the slowest axis — rows of a 2D Euler mesh, z-planes
-   * of a 3D Euler mesh.  The global mesh stays nx x ny (x nz); the operator's state holds
+   * layers [part_begin, part_end) along the slowest axis — elements of a 1D Burgers mesh,
+   * element rows of a 2D mesh (Burgers, Euler), z-planes of a 3D Euler mesh.  The global mesh stays nx x ny (x nz); the operator's state holds
    * only the owned layers and exchanges one halo layer with its periodic neighbours
    * (rank -+ 1) through the context's communicator. */
   int part_begin, part_end;

@@ -114,9 +114,7 @@ void validate_desc(const expdg_op_desc& d) {
       throw Unsupported("3D Euler: Lax-Friedrichs flux only (the Roe flux is 2D, proj/src/euler.cpp:114-145)");
   }
   if (d.part_end > d.part_begin) {
-    if (d.kind != EXPDG_EULER2D && d.kind != EXPDG_EULER3D && d.kind != EXPDG_BURGERS1D)
-      throw Unsupported("slab partition: 1D Burgers (elements), 2D Euler (element rows), 3D Euler (planes)");
-    const int layers = d.kind == EXPDG_EULER2D ? d.ny : (d.kind == EXPDG_EULER3D ? d.nz : d.nx);
+    const int layers = d.kind == EXPDG_BURGERS1D ? d.nx : (d.kind == EXPDG_EULER3D ? d.nz : d.ny);
     if (d.part_begin < 0 || d.part_end > layers) throw std::invalid_argument("slab partition: layers out of range");
     if (d.kind == EXPDG_BURGERS1D && d.part_end - d.part_begin < (d.over_integrate ? 2 : 1))
       throw std::invalid_argument("slab partition: over-integrated Burgers needs two elements per rank");

@@ -61,18 +61,19 @@ __device__ __forceinline__ void b2_tile(const B1P<NP>& Px, const B1P<NP>& Py, in
   }
   __syncthreads();
   if (active) {
-    // y-line (column `line`)
+    // y-line (column `line`); a row slab takes rows -1 / ny from the halo rows
+    const bool gS = Py.part && je == 0, gN = Py.part && je == ny - 1;
     const long long eS = (long long)(je == 0 ? ny - 1 : je - 1) * nx + ie;
     const long long eN = (long long)(je == ny - 1 ? 0 : je + 1) * nx + ie;
-    gather(x, xs, eS, NP, line, false, xL);
+    gather(gS ? Py.gx_lo : x, xs, gS ? ie : eS, NP, line, false, xL);
     gather(x, xs, e, NP, line, false, xC);
-    gather(x, xs, eN, NP, line, false, xR);
+    gather(gN ? Py.gx_hi : x, xs, gN ? ie : eN, NP, line, false, xR);
     if (need_ut) {
-      gather(Py.ut, 1.0, eS, NP, line, false, uL);
+      gather(gS ? Py.gt_lo : Py.ut, 1.0, gS ? ie : eS, NP, line, false, uL);
       gather(Py.ut, 1.0, e, NP, line, false, uC);
-      gather(Py.ut, 1.0, eN, NP, line, false, uR);
+      gather(gN ? Py.gt_hi : Py.ut, 1.0, gN ? ie : eN, NP, line, false, uR);
     }
-    b1_element<NP>(Py, mode, je, xL, xC, xR, uL, uC, uR, out);
+    b1_element<NP>(Py, mode, (int)Py.eoff + je, xL, xC, xR, uL, uC, uR, out);
 #pragma unroll
     for (int j = 0; j < NP; ++j) sout[le * NN + j * NP + line] += out[j];
   }
@@ -158,12 +159,17 @@ template <int NP>
 class Burgers2D : public OpDevice {
  public:
   B1P<NP> Px{}, Py{};
-  int nx = 0, ny = 0, grid = 1;
+  int nx = 0, ny = 0, grid = 1;  // ny: owned element rows
+  double* halo = nullptr;        // row slab: x lo/hi, u~ lo/hi, send lo/hi (one element row each)
+  long long rowd = 0;
+  ~Burgers2D() override { cudaFree(halo); }
+  double* hq(int i) const { return halo + (size_t)i * rowd; }
   explicit Burgers2D(const expdg_op_desc& d) {
     desc = d;
     const HostBasis hb = host_lgl_basis(d.order);
+    const bool part = d.part_end > d.part_begin;
     nx = d.nx;
-    ny = d.ny;
+    ny = part ? d.part_end - d.part_begin : d.ny;
     for (B1P<NP>* P : {&Px, &Py}) {
       P->periodic = d.periodic;
       P->kappa = d.kappa;
@@ -179,30 +185,62 @@ class Burgers2D : public OpDevice {
       }
     }
     Px.ne = d.nx;
+    Px.nel = d.nx;
     Px.a = d.x0;
     Px.b = d.x1;
-    Py.ne = d.ny;
+    Py.ne = d.ny;  // global rows: boundary faces and h come from the global index
+    Py.nel = ny;
+    Py.eoff = part ? d.part_begin : 0;
+    Py.part = part ? 1 : 0;
     Py.a = d.y0;
     Py.b = d.y1;
-    n = (long long)d.nx * d.ny * NP * NP;
+    n = (long long)d.nx * ny * NP * NP;
     Px.n = Py.n = n;
     comps = 1;
-    const long long ntiles = ((long long)d.nx * d.ny + B2Tile<NP>::TE - 1) / B2Tile<NP>::TE;
+    rowd = (long long)d.nx * NP * NP;
+    if (part) {
+      EXPDG_CUDA(cudaMalloc(&halo, sizeof(double) * 6 * rowd));
+      EXPDG_CUDA(cudaMemset(halo, 0, sizeof(double) * 6 * rowd));
+    }
+    const long long ntiles = ((long long)d.nx * ny + B2Tile<NP>::TE - 1) / B2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
   }
+  void exchange(cudaStream_t s, const double* v, double* lo, double* hi) {
+    comm->halo(v, v + (size_t)(ny - 1) * rowd, lo, hi, rowd, s);
+  }
+  void with_halo(B1P<NP>& py, bool x_is_ut) const {
+    if (!Py.part) return;
+    py.gt_lo = hq(2);
+    py.gt_hi = hq(3);
+    py.gx_lo = x_is_ut ? hq(2) : hq(0);
+    py.gx_hi = x_is_ut ? hq(3) : hq(1);
+  }
+  void freeze(cudaStream_t s, const double* r) override {
+    ref = r;
+    if (Py.part) exchange(s, r, hq(2), hq(3));
+  }
   void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+    if (Py.part) {
+      launch_pack_slot(s, st, base, rowd, (long long)(ny - 1) * rowd, hq(4), hq(5));
+      comm->halo(hq(4), hq(5), hq(0), hq(1), rowd, s);
+    }
     B1P<NP> px = Px, py = Py;
     px.ut = py.ut = ref;
+    with_halo(py, false);
     k_b2_phi<NP><<<grid, 256, 0, s>>>(px, py, nx, ny, st, base, partials, b);
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
+    if (Py.part) exchange(s, x, hq(0), hq(1));
     B1P<NP> px = Px, py = Py;
     px.ut = py.ut = ref;
+    with_halo(py, false);
     k_b2_apply<NP><<<grid, 256, 0, s>>>(px, py, nx, ny, which, x, y, nullptr);
   }
   void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
+    if (Py.part) exchange(s, u, hq(2), hq(3));  // u~ = u for this step's residual and JVPs
     B1P<NP> px = Px, py = Py;
     px.ut = py.ut = u;
+    with_halo(py, true);
     k_b2_apply<NP><<<grid, 256, 0, s>>>(px, py, nx, ny, 2, u, r, st);
   }
 };

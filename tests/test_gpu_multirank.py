@@ -220,3 +220,36 @@ def test_partitioned_burgers1d_matches_single_rank(parts, periodic, oi):
     d_part = np.diff(np.concatenate([[0], got[0][1].iters_per_step]))
     d_single = np.diff(np.concatenate([[0], single.iters_per_step]))
     assert np.max(np.abs(d_part - d_single)) <= 1
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_partitioned_burgers2d_matches_single_rank(periodic):
+    # C3 physics (2D tensor-product LDG Burgers) on 10 x 9 elements, 3 row slabs
+    w = configs.scaled(configs.C3, 9, steps=2)
+    spec = w.spec()
+    spec.nx, spec.periodic = 10, periodic
+    rng = np.random.default_rng(2)
+    u0 = 0.3 * rng.standard_normal(spec.nx * spec.ny * (spec.order + 1) ** 2)
+    x = rng.standard_normal(u0.size)
+    kw = dict(tol=1e-10, max_basis=30, orth_length=30)
+    ctx = pkg.Context(0)
+    op = pkg.Operator(ctx, spec)
+    op.linearize(to_dev(u0))
+    want = [to_host(op.apply_linear(to_dev(x))), to_host(op.full_rhs(to_dev(x)))]
+    single = pkg.integrate(ctx, op, to_dev(u0), "epi2", 1e-3, 3e-3, **kw)
+    ranges = slab_ranges(spec.ny, 3)
+    row = spec.nx * (spec.order + 1) ** 2
+
+    def fn(r, c):
+        o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": ranges[r]}))
+        sl = slice(ranges[r][0] * row, ranges[r][1] * row)
+        o.linearize(to_dev(u0[sl]))
+        ys = [to_host(o.apply_linear(to_dev(x[sl]))), to_host(o.full_rhs(to_dev(x[sl])))]
+        res = pkg.integrate(c, o, to_dev(u0[sl]), "epi2", 1e-3, 3e-3, **kw)
+        return ys, res, to_host(res.u)
+
+    got = run_ranks(3, fn)
+    for i in range(2):
+        assert rel(np.concatenate([g[0][i] for g in got]), want[i]) < 1e-14
+    assert all(g[1].status == single.status == "completed" for g in got)
+    assert rel(np.concatenate([g[2] for g in got]), to_host(single.u)) <= 1e-11
