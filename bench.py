@@ -188,8 +188,7 @@ def main():
     partitioned = (world > 1 or args.partition) and not args.replicas
     if partitioned:
         from paper_2011_01316_b200.partition import slab_ranges
-        if spec.kind not in ("euler2d", "euler3d"):
-            raise SystemExit("the slab-partitioned path is 2D Euler (C4) / 3D Euler (C5)")
+
         uid = torch.zeros(128, dtype=torch.uint8)
         if rank == 0:
             uid = torch.tensor(list(pkg.nccl_unique_id()), dtype=torch.uint8)
@@ -198,10 +197,12 @@ def main():
             torch.distributed.broadcast(t_uid, 0)
             uid = t_uid.cpu()
         ctx.attach_nccl(bytes(uid.tolist()), rank, world)
-        d3 = spec.kind == "euler3d"
-        rows = slab_ranges(spec.nz if d3 else spec.ny, world)[rank]
+        npe = spec.order + 1
+        layers, blk = {"burgers1d": (spec.nx, npe), "burgers2d": (spec.ny, spec.nx * npe ** 2),
+                       "euler2d": (spec.ny, spec.nx * npe ** 2 * 4),
+                       "euler3d": (spec.nz, spec.nx * spec.ny * npe ** 3 * 5)}[spec.kind]
+        rows = slab_ranges(layers, world)[rank]
         spec.part = rows
-        blk = spec.nx * (spec.ny * (spec.order + 1) ** 3 * 5 if d3 else (spec.order + 1) ** 2 * 4)
         u0 = u0[rows[0] * blk:rows[1] * blk].copy()
     op = pkg.Operator(ctx, spec)
     n = op.dim
