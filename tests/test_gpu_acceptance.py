@@ -144,3 +144,18 @@ def test_criterion_8_vortex_orders_roe(ctx):
         assert f"{math.log2(errs[0] / errs[1]):.3f}" == want[k]
         if k == 2:
             assert f"{errs[1]:.3e}" == "1.486e-05"
+
+
+def test_device_run_against_a_stored_reference_file(ctx, tmp_path):
+    # the harness's reference-file cache (proj/src/harness.cpp:355-386): an RK4 fine-step
+    # reference written in the expdg-reference-v1 format, loaded back, device EPI2 error vs it
+    from paper_2011_01316_b200 import refio
+    spec = refio.ReferenceSpec("burgers-smooth", "lf", over_integrate=True, kappa=0.03, integrator="rk4", k=3, ne=20,
+                               dt=1e-5, t_final=1.0)
+    path = str(tmp_path / refio.reference_filename(spec))
+    refio.save_reference(path, spec, oracle.rk4_reference("burgers-smooth", 20, 3, "lf", 1, 1e-5, 1.0))
+    uref = refio.load_reference(path, spec)
+    op, u0 = device_problem(ctx, "burgers-smooth", 20, 3, "lf")
+    r = pkg.integrate(ctx, op, to_dev(u0), "epi2", 0.05, 1.0, **KRYLOV)
+    err = oracle.l2_error_discrete("burgers-smooth", 20, 3, to_host(r.u), 20, 3, uref)
+    assert 0 < err < 1e-4
