@@ -480,10 +480,11 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
 // primitives, each with its E/W halo element) by 1D TMA bulk copies into a
 // 4-row smem ring (full/empty mbarriers); warps 0-7 compute row r from the
 // ring rows r-1, r, r+1, so every byte of x and q~ comes from HBM once per JVP.
-template <int NP>
+template <int NP, int CW>
 struct E2Strip {
   static constexpr int NN = NP * NP;
-  static constexpr int W = 256 / NN;          // elements per strip
+  static constexpr int CONS = 32 * CW;        // consumer threads (CW warps) + one producer warp
+  static constexpr int W = CONS / NN > 0 ? CONS / NN : 1;  // elements per strip
   static constexpr int BLK = 4 * NN;          // doubles per element
   static constexpr int ROWD = (W + 2) * BLK;  // doubles per array per row (with halo)
   static constexpr int BUFD = 2 * ROWD + W * BLK;  // x + frozen (with halo) + b_1
@@ -496,10 +497,13 @@ struct E2Strip {
   static constexpr int SMEM = (NBUF * BUFD + 2 * (2 * W * BLK) + 2 * FX + 3 * FY) * 8;
 };
 
-template <int NP, bool ROE>
-__global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st, double* base, double* partials,
-                                                         BArgs b) {
-  using S = E2Strip<NP>;
+template <int CONS>
+__device__ __forceinline__ void strip_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONS) : "memory"); }
+
+template <int NP, bool ROE, int CW>
+__global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
+    k_e2_phi_strip(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
+  using S = E2Strip<NP, CW>;
   constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
   __shared__ int s_go, s_j;
   __shared__ double s_xs, s_dt, s_xt[kMaxP];
   __shared__ long long s_ld;
-  __shared__ double s_buf[9];
+  __shared__ double s_buf[CW + 1];
   __shared__ double s_red[1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
   const double* b1 = (b.p == 1) ? b.b[1] : nullptr;
   double nacc = 0.0;
 
-  if (wid == 8) {
+  if (wid == CW) {
     // ---------------- producer
     if (lane == 0) {
       long long seq = 0;
@@ -656,7 +660,7 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
           double* ybot = sfy + ((r - r0) % 3) * S::FY;
           const int nxf = (w + 1) * NP, nyf = w * NP;
           const int total = nxf + nyf + (r == r0 ? nyf : 0);
-          for (int t = tid; t < total; t += 256) {  // the 8 consumer warps
+          for (int t = tid; t < total; t += S::CONS) {  // the consumer warps
             double qa[4], ta[4], qb[4], tb[4], f[4];
             const double* ra;
             const double* rb;
@@ -688,7 +692,7 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
             for (int c = 0; c < 4; ++c) dst[c] = f[c];
           }
         }
-        consumer_sync();  // A/B of row r done; every thread has also finished C of row r-1
+        strip_sync<S::CONS>();  // A/B of row r done; every thread has also finished C of row r-1
         if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);  // ring row r-1 is free
         if (active) {
           const double sy = 0.5 * hy * wj;
@@ -736,7 +740,7 @@ __global__ void __launch_bounds__(288, 1) k_e2_phi_strip(E2P<NP> P, PhiState* st
           }
         }
       }
-      consumer_sync();  // C of the unit's last row done
+      strip_sync<S::CONS>();  // C of the unit's last row done
       if (tid == 0) {
         mbar_arrive(&empty[(seq + (r1 - r0)) % NBUF]);      // row r1 - 1
         mbar_arrive(&empty[(seq + (r1 - r0) + 1) % NBUF]);  // row r1 (upper halo)
@@ -785,6 +789,19 @@ class Euler2D : public OpDevice {
   double* hbuf = nullptr;
   bool use_strip = true;
   bool roe = false;
+  int strip_cw = 8;  // consumer warps per strip CTA (EXPDG_E2_CW=4: half-width strips, 2 CTAs / SM)
+  template <int CW>
+  void launch_strip(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
+                    const BArgs& b) {
+    using SS = E2Strip<NP, CW>;
+    int per_sm = 1;
+    EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_e2_phi_strip<NP, false, CW>, 32 * CW + 32,
+                                                             SS::SMEM));
+    const int units = ((P.nx + SS::W - 1) / SS::W) * ((P.ny + SS::ROWS_PER_UNIT - 1) / SS::ROWS_PER_UNIT);
+    const int g = std::max(1, std::min(units, 148 * std::max(1, per_sm)));
+    if (roe) k_e2_phi_strip<NP, true, CW><<<g, 32 * CW + 32, SS::SMEM, s>>>(p, st, base, partials, b);
+    else k_e2_phi_strip<NP, false, CW><<<g, 32 * CW + 32, SS::SMEM, s>>>(p, st, base, partials, b);
+  }
   // slab partition: halo rows (x lo/hi, frozen lo/hi) and send staging (lo/hi)
   double* halo = nullptr;
   long long rowd = 0;  // doubles per element row
@@ -856,10 +873,15 @@ class Euler2D : public OpDevice {
     }
     use_strip = !(std::getenv("EXPDG_E2_TILE") && std::getenv("EXPDG_E2_TILE")[0] == '1');
     roe = d.euler_flux == 0;
-    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    E2Strip<NP>::SMEM));
-    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    E2Strip<NP>::SMEM));
+    if (const char* v = std::getenv("EXPDG_E2_CW")) strip_cw = std::atoi(v) == 4 ? 4 : 8;
+    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    E2Strip<NP, 8>::SMEM));
+    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    E2Strip<NP, 8>::SMEM));
+    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    E2Strip<NP, 4>::SMEM));
+    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    E2Strip<NP, 4>::SMEM));
     const long long ntiles = ((long long)d.nx * nyl + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
   }
@@ -870,11 +892,8 @@ class Euler2D : public OpDevice {
     }
     const E2P<NP> p = params(frozen);
     if (use_strip) {
-      using SS = E2Strip<NP>;
-      const int units = ((P.nx + SS::W - 1) / SS::W) * ((P.ny + SS::ROWS_PER_UNIT - 1) / SS::ROWS_PER_UNIT);
-      const int g = std::max(1, std::min(units, 148));  // one CTA per SM (smem-bound)
-      if (roe) k_e2_phi_strip<NP, true><<<g, 288, SS::SMEM, s>>>(p, st, base, partials, b);
-      else k_e2_phi_strip<NP, false><<<g, 288, SS::SMEM, s>>>(p, st, base, partials, b);
+      if (strip_cw == 4) launch_strip<4>(s, p, st, base, partials, b);
+      else launch_strip<8>(s, p, st, base, partials, b);
     } else {
       if (roe) k_e2_phi<NP, true><<<grid, 256, 0, s>>>(p, st, base, partials, b);
       else k_e2_phi<NP, false><<<grid, 256, 0, s>>>(p, st, base, partials, b);
