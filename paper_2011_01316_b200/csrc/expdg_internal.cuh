@@ -114,8 +114,6 @@ struct PhiState {
   double dc_g[kMaxSlots];      // (H a)_l with column j-1 corrected, l < j
   double dc_alpha[kMaxSlots];  // slot-space update coefficients of u
   double dc_mu[kMaxSlots];     // slot-space update coefficients of w
-  // ---- Hessenberg (mmax+1) x mmax, row stride kMaxBasis
-  double H[(kMaxBasis + 1) * kMaxBasis];
   // ---- last-block reduction tickets, one per reducing kernel kind
   unsigned int ticket[16];
   // ---- step-level bookkeeping (integrate)
@@ -134,6 +132,9 @@ struct PhiState {
   long long extend_cols, avnorms, combines;
   double blow_up_scale;
   double amax_step;
+  // ---- Hessenberg (mmax+1) x mmax, row stride kMaxBasis; last, so the controller
+  // copies the scalar state plus only the rows in use
+  alignas(16) double H[(kMaxBasis + 1) * kMaxBasis];
 };
 
 // One record per integrate step, read back by the host at the end.

@@ -554,8 +554,8 @@ __device__ int dcgs_finish(PhiState* st) {
   return 0;
 }
 
-__global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double* W,
-                                             cudaGraphConditionalHandle cond, int use_graph) {
+__device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W, double* Wsm, int ws_cap,
+                                         cudaGraphConditionalHandle cond, int use_graph) {
   __shared__ int s_phase, s_exit, s_zeroH, s_done;
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -674,15 +674,16 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
       // hbar (mc+2)^2 = [H(0:mc, 0:mc-1) 0; 0 .. 1 0], scaled by h (proj/src/phi.cpp:208-211)
       const int mc = st->mc, N = mc + 2;
       const double h = st->h;
+      double* Wx = 9 * N * N <= ws_cap ? Wsm : W;
       for (int idx = tid; idx < N * N; idx += blockDim.x) {
         const int i = idx / N, j = idx % N;
         double v = 0.0;
         if (i <= mc && j < mc) v = st->H[i * kMaxBasis + j];
         if (i == mc + 1 && j == mc) v = 1.0;
-        W[idx] = h * v;
+        Wx[idx] = h * v;
       }
       __syncthreads();
-      const double* F = blk_expm(W, N);
+      const double* F = blk_expm(9 * N * N <= ws_cap ? Wsm : W, N);
       if (tid == 0) {
         const double beta = st->beta;
         double err = 0.0;
@@ -799,6 +800,11 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
   }
   if (tid == 0) st->phase = s_phase;
   if (tid == 0 && s_done && use_graph) cudaGraphSetConditional(cond, 0u);
+}
+
+__global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double* W,
+                                             cudaGraphConditionalHandle cond, int use_graph) {
+  ctl_body(st, slot0, W, nullptr, 0, cond, use_graph);
 }
 
 // Sets action = START / DONE after the init reduction (separate tiny kernel so the
