@@ -55,6 +55,7 @@ def lib():
         L.oracle_problem_dim.argtypes = [C.c_void_p]
         L.oracle_apply.argtypes = [C.c_void_p, C.c_int, dp, dp, dp]
         L.oracle_burgers_diag.argtypes = [C.c_void_p, dp, dp, dp, dp, dp, dp, dp]
+        L.oracle_burgers_inner.argtypes = [C.c_void_p, dp, dp, dp]
         L.oracle_integrate.argtypes = [C.c_void_p, C.c_int, dp, C.c_double, C.c_double, C.c_double,
                                        C.c_int, C.c_int, C.c_int, C.POINTER(C.c_long), dp,
                                        C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -314,6 +315,15 @@ def burgers_diag(problem: Problem, ref, u):
     _check(lib().oracle_burgers_diag(problem.h, _p(ref), _p(u), _p(q),
                                      *[C.byref(v) for v in vals]))
     return q, tuple(v.value for v in vals)
+
+
+def burgers_inner(problem: Problem, a, b):
+    """<a, b> in the Burgers operator's mass inner product (checker for device residuals)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().oracle_burgers_inner(problem.h, _p(a), _p(b), C.byref(out)))
+    return out.value
 
 
 # ---------------------------------------------------------------- harness helpers (checker side)

@@ -171,6 +171,17 @@ int oracle_burgers_diag(void* h, const double* ref, const double* u, double* q_o
   } catch (const std::exception& e) { set_err(e.what()); return 3; }
 }
 
+// Mass inner product <a, b> of the Burgers operator's quadrature (BurgersOperator::inner_product):
+// the checker for device right-hand sides in the energy / conservation identities.
+int oracle_burgers_inner(void* h, const double* a, const double* b, double* out) {
+  try {
+    const Problem& P = *static_cast<Problem*>(h);
+    BurgersOperator op(P.mesh, P.basis, P.bcfg, Vec(a, a + P.dim));
+    *out = op.inner_product(Vec(a, a + P.dim), Vec(b, b + P.dim));
+    return 0;
+  } catch (const std::exception& e) { set_err(e.what()); return 3; }
+}
+
 // integrator: 0 exp_euler 1 epi2 2 exprb32 3 exprb42 4 rk2 5 rk3 6 rk4
 // Per-step outputs (nullable, capacity max_steps): cumulative Krylov iterations, max|u|.
 int oracle_integrate(void* h, int integrator, double* u, double dt, double t_final, double tol,

@@ -161,3 +161,80 @@ def test_device_run_against_a_stored_reference_file(ctx, tmp_path):
     direct = oracle.l2_error_discrete("burgers-smooth", 20, 3, to_host(r.u), 20, 3,
                                       oracle.rk4_reference("burgers-smooth", 20, 3, "lf", 1, 1e-5, 1.0))
     assert err == direct and 0 < err < 1e-3  # %.17g files round-trip the reference exactly
+
+
+def test_criterion_6_energy_identity_on_device_residuals(ctx):
+    # proj/tests/acceptance.cpp:241-271 (recorded worst 2.12e-13, tolerance 1e-10): the DEVICE
+    # residual L u + N u of the over-integrated EF Burgers operator satisfies the discrete energy
+    # identity <u, r> + kappa <q, q> + penalty(u) = 0 (q, the penalty and <.,.> from the checker)
+    rng = np.random.default_rng(616)
+    worst = 0.0
+    for k in range(1, 7):
+        kw = dict(box=(0.0, 1.0, 0, 1, 0, 1), periodic=True, kappa=0.04, flux="ef", sigma=2e-3, over_integrate=True)
+        op = pkg.Operator(ctx, pkg.OperatorSpec("burgers1d", k, 8, **kw))
+        orc = oracle.Problem("burgers1d", k, 8, **kw)
+        for _ in range(17):
+            u = rng.standard_normal(op.dim)
+            ud = to_dev(u)
+            op.linearize(ud)
+            r = to_host(op.apply_linear(ud) + op.apply_nonlinear(ud))
+            _, (_, ip_qq, pen, ip_uu) = oracle.burgers_diag(orc, u, u)
+            lhs = oracle.burgers_inner(orc, u, r) + 0.04 * ip_qq + pen
+            worst = max(worst, abs(lhs) / (1.0 + ip_uu))
+    assert worst <= 1e-10
+
+
+def test_criteria_7_11_splitting_invariance_and_conservation(ctx):
+    # proj/tests/acceptance.cpp:275-331, :467-527: L(a) u + N(a) u independent of a (recorded
+    # 6.61e-16) and the mass-weighted mean of the periodic RHS vanishing (recorded 1.70e-16)
+    rng = np.random.default_rng(707)
+    worst_split, worst_cons = 0.0, 0.0
+    kw = dict(box=(0.0, 1.0, 0, 1, 0, 1), periodic=True, kappa=0.02, flux="ef", sigma=3e-4)
+    op1, op2 = pkg.Operator(ctx, pkg.OperatorSpec("burgers1d", 3, 9, **kw)), pkg.Operator(
+        ctx, pkg.OperatorSpec("burgers1d", 3, 9, **kw))
+    orc = oracle.Problem("burgers1d", 3, 9, **kw)
+    for _ in range(25):
+        u, a, b = (rng.standard_normal(op1.dim) for _ in range(3))
+        op1.linearize(to_dev(a))
+        op2.linearize(to_dev(b))
+        ud = to_dev(u)
+        r1 = to_host(op1.apply_linear(ud) + op1.apply_nonlinear(ud))
+        r2 = to_host(op2.apply_linear(ud) + op2.apply_nonlinear(ud))
+        worst_split = max(worst_split, np.linalg.norm(r1 - r2) / np.linalg.norm(r1))
+        worst_cons = max(worst_cons, abs(oracle.burgers_inner(orc, np.ones(op1.dim), r1)) /
+                         (1.0 + np.linalg.norm(r1)))
+    ek = dict(box=(0.0, 10.0, -5.0, 5.0, 0, 1), euler_flux="lf")
+    e1 = pkg.Operator(ctx, pkg.OperatorSpec("euler2d", 2, 3, 3, **ek))
+    e2 = pkg.Operator(ctx, pkg.OperatorSpec("euler2d", 2, 3, 3, **ek))
+    npe = 9
+    for _ in range(25):
+        def state():
+            q = np.empty(9 * 4 * npe)
+            for e in range(9):
+                blk = q[e * 4 * npe:(e + 1) * 4 * npe].reshape(4, npe)
+                rho, vx, vy, p = (rng.uniform(0.5, 2.0, npe), rng.uniform(-1, 1, npe), rng.uniform(-1, 1, npe),
+                                  rng.uniform(0.5, 2.0, npe))
+                blk[0], blk[1], blk[2], blk[3] = rho, rho * vx, rho * vy, p / 0.4 + 0.5 * rho * (vx * vx + vy * vy)
+            return q
+        q, a, b = state(), state(), state()
+        e1.linearize(to_dev(a))
+        e2.linearize(to_dev(b))
+        qd = to_dev(q)
+        r1 = to_host(e1.apply_linear(qd) + e1.apply_nonlinear(qd))
+        r2 = to_host(e2.apply_linear(qd) + e2.apply_nonlinear(qd))
+        worst_split = max(worst_split, np.linalg.norm(r1 - r2) / np.linalg.norm(r1))
+    assert worst_split <= 1e-12
+    assert worst_cons <= 1e-12
+
+
+def test_criterion_10_exp_euler_joint_estimate(ctx):
+    # proj/test_output.txt:27 — exp_euler, k = 2, (ne, dt) = (10, 0.2), (20, 0.1), (40, 0.05)
+    # against the RK4 k = 6, ne = 80, dt = 5e-6 reference: errors 8.303e-03 3.847e-03 1.866e-03
+    uref = oracle.rk4_reference("burgers-smooth", 80, 6, "lf", 1, 5e-6, 1.0)
+    errs = []
+    for ne, dt in ((10, 0.2), (20, 0.1), (40, 0.05)):
+        op, u0 = device_problem(ctx, "burgers-smooth", ne, 2, "lf")
+        r = pkg.integrate(ctx, op, to_dev(u0), "exp_euler", dt, 1.0, **KRYLOV)
+        assert r.status == "completed"
+        errs.append(oracle.l2_error_discrete("burgers-smooth", ne, 2, to_host(r.u), 80, 6, uref))
+    assert [f"{e:.3e}" for e in errs] == ["8.303e-03", "3.847e-03", "1.866e-03"]
