@@ -148,6 +148,10 @@ int expdg_ctx_comm(const expdg_ctx* ctx, int* rank, int* size); /* 0, 1 without 
 #define EXPDG_ORTH_DCGS2 1
 #define EXPDG_ORTH_AUTO 2 /* default: DCGS2 from 2^18 DOF up, CGS2 below (launch-latency bound) */
 int expdg_ctx_set_orthogonalization(expdg_ctx* ctx, int mode);
+/* Small problems (1D Burgers, <= 2^15 DOF, one rank, CGS2) run each phi call as one
+ * single-CTA kernel with the controller state in shared memory (default 1); 0 forces
+ * the multi-kernel engine.  Same algorithm either way. */
+int expdg_ctx_set_fused(expdg_ctx* ctx, int enable);
 
 /* Operator factory: replaces BurgersOperator / EulerOperator construction
  * (proj/src/burgers.cpp:20-93, proj/src/euler.cpp:186-244) minus the frozen
@@ -223,6 +227,9 @@ double expdg_ctx_last_loop_ms(expdg_ctx* ctx);
 /* Canonical algorithmic HBM bytes of the last integrate / phi call's
  * realised trajectory, and its counts of Arnoldi columns, avnorm applications and
  * accepted substeps: out4 = {bytes, columns, avnorms, combines}. */
+/* Fused small-problem engine: SM clock cycles spent per phase in the last run
+ * (apply, dots, updates, combine, controller; 0 for the multi-kernel engine). */
+int expdg_debug_profile(expdg_ctx* ctx, long long* out8);
 int expdg_ctx_traffic(expdg_ctx* ctx, double* out4);
 
 #ifdef __cplusplus

@@ -84,6 +84,7 @@ EXPORTS = [
     "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts", "expdg_op_set_source",
     "expdg_op_set_source_fn", "expdg_nccl_unique_id", "expdg_ctx_attach_nccl", "expdg_local_group_create",
     "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
+    "expdg_debug_profile", "expdg_ctx_set_fused",
 ]
 
 _lib = None
@@ -145,6 +146,8 @@ def lib():
     L.expdg_ctx_attach_local.argtypes = [vp, vp, C.c_int]
     L.expdg_ctx_comm.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     L.expdg_ctx_set_orthogonalization.argtypes = [vp, C.c_int]
+    L.expdg_debug_profile.argtypes = [vp, C.POINTER(C.c_longlong)]
+    L.expdg_ctx_set_fused.argtypes = [vp, C.c_int]
     _lib = L
     return L
 
@@ -198,8 +201,9 @@ def initial_condition(config: int, nx: int, order: int, seed: int, noise: float 
 
 # ---------------------------------------------------------------- context / operators
 class Context:
-    def __init__(self, device: int = 0, orth: Optional[str] = None):
-        """orth: None (auto: DCGS2 from 2^18 DOF up), "dcgs2" or "cgs2" for fully orthogonalised phi calls."""
+    def __init__(self, device: int = 0, orth: Optional[str] = None, fused: Optional[bool] = None):
+        """orth: None (auto: DCGS2 from 2^18 DOF up), "dcgs2" or "cgs2" for fully orthogonalised phi calls;
+        fused: None / True runs small 1D Burgers phi calls as one single-CTA kernel, False never."""
         import torch
         torch.cuda.init()
         self.device = device
@@ -210,6 +214,8 @@ class Context:
             if orth not in ("cgs2", "dcgs2"):
                 raise ValueError("orth must be 'cgs2' or 'dcgs2'")
             _check(lib().expdg_ctx_set_orthogonalization(self.h, 1 if orth == "dcgs2" else 0))
+        if fused is not None:
+            _check(lib().expdg_ctx_set_fused(self.h, 1 if fused else 0))
 
     def close(self):
         if getattr(self, "h", None):
@@ -255,6 +261,12 @@ class Context:
         ms = C.c_double()
         _check(lib().expdg_bench_ts(self.h, n, k, mode, reps, C.byref(ms)))
         return ms.value
+
+    def debug_profile(self) -> dict:
+        """Fused small-problem engine: SM cycles per phase of the last run."""
+        v = (C.c_longlong * 8)()
+        _check(lib().expdg_debug_profile(self.h, v))
+        return dict(zip(["apply", "dots", "update", "combine", "control"], list(v)[:5]))
 
     def debug_hessenberg(self) -> np.ndarray:
         h = np.zeros((129, 128))

@@ -220,6 +220,13 @@ int expdg_ctx_set_orthogonalization(expdg_ctx* ctx, int mode) {
   });
 }
 
+int expdg_ctx_set_fused(expdg_ctx* ctx, int enable) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null argument");
+    ctx->eng->use_fused = enable != 0;
+  });
+}
+
 int expdg_ctx_comm(const expdg_ctx* ctx, int* rank, int* size) {
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null argument");
@@ -542,7 +549,8 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     }
   };
   (void)vgrid;
-  const int per_step = (exprb ? 13 : 5) + (e.comm ? 1 : 0);
+  const bool fused = e.fused_ok(dev);
+  const int per_step = (exprb ? 13 : 5) + (e.comm ? 1 : 0) + (fused ? (exprb ? 2 : 1) : 0);
   const int body_k = (dev.fused_dots() ? 5 : 6) + (dev.partitioned() ? 1 : 0);  // + halo pack kernel
   cudaGraphExec_t ex = nullptr;
   const bool graph = cfg->use_graph != 0 && !e.comm;  // partitioned: host-stepped control
@@ -583,21 +591,31 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
       EXPDG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
       EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
       pre(cs);
-      cudaGraphConditionalHandle h1, h2;
-      cudaGraph_t body1 = add_while(cs, g, &h1), body2 = nullptr;
-      if (exprb) {
-        mid(cs);
-        body2 = add_while(cs, g, &h2);
-      }
-      post(cs);
-      EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
-      EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body1, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-      e.launch_body(cs, dev, b1, h1, 1, c1.dcgs != 0);
-      EXPDG_CUDA(cudaStreamEndCapture(cs, &body1));
-      if (exprb) {
-        EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body2, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        e.launch_body(cs, dev, b2, h2, 1, c3.dcgs != 0);
-        EXPDG_CUDA(cudaStreamEndCapture(cs, &body2));
+      if (fused) {  // small problem: each phi call is one fused kernel node
+        dev.launch_fused(cs, e, b1);
+        if (exprb) {
+          mid(cs);
+          dev.launch_fused(cs, e, b2);
+        }
+        post(cs);
+        EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
+      } else {
+        cudaGraphConditionalHandle h1, h2;
+        cudaGraph_t body1 = add_while(cs, g, &h1), body2 = nullptr;
+        if (exprb) {
+          mid(cs);
+          body2 = add_while(cs, g, &h2);
+        }
+        post(cs);
+        EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
+        EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body1, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        e.launch_body(cs, dev, b1, h1, 1, c1.dcgs != 0);
+        EXPDG_CUDA(cudaStreamEndCapture(cs, &body1));
+        if (exprb) {
+          EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body2, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+          e.launch_body(cs, dev, b2, h2, 1, c3.dcgs != 0);
+          EXPDG_CUDA(cudaStreamEndCapture(cs, &body2));
+        }
       }
       EXPDG_CUDA(cudaGraphInstantiate(&ex, g, 0));
       cudaGraphDestroy(g);
@@ -619,10 +637,12 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
           EXPDG_CUDA(cudaGraphLaunch(ex, e.stream));
         } else {
           pre(e.stream);
-          host_loop(b1, c1.dcgs != 0);
+          if (fused) dev.launch_fused(e.stream, e, b1);
+          else host_loop(b1, c1.dcgs != 0);
           if (exprb) {
             mid(e.stream);
-            host_loop(b2, c3.dcgs != 0);
+            if (fused) dev.launch_fused(e.stream, e, b2);
+            else host_loop(b2, c3.dcgs != 0);
           }
           post(e.stream);
         }
@@ -654,7 +674,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   restore_ref(dev, e.stream, saved_ref);
   EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
   const PhiState st = *e.st_host;
-  ctx->launches += (long long)launched * per_step + st.body_runs * body_k;
+  ctx->launches += (long long)launched * per_step + (fused ? 0 : st.body_runs * body_k);
   std::vector<StepRecord> rec(std::max(1, st.step));
   if (st.step > 0)
     EXPDG_CUDA(cudaMemcpy(rec.data(), rec_dev, sizeof(StepRecord) * st.step, cudaMemcpyDeviceToHost));
@@ -730,6 +750,14 @@ int expdg_debug_state(expdg_ctx* ctx, double* out16) {
                           (double)s.iterations, (double)s.breakdown, (double)s.status, (double)s.mmax,
                           (double)s.grow_cap, (double)s.full_orth, (double)s.cycles, s.pre_norm, (double)s.m};
     std::memcpy(out16, v, sizeof(v));
+  });
+}
+
+int expdg_debug_profile(expdg_ctx* ctx, long long* out8) {
+  return guard([&] {
+    if (!ctx || !out8) throw std::invalid_argument("null argument");
+    EXPDG_CUDA(cudaMemcpy(ctx->eng->st_host, ctx->eng->st, sizeof(PhiState), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 8; ++i) out8[i] = ctx->eng->st_host->prof[i];
   });
 }
 

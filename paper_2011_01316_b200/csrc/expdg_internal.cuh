@@ -132,6 +132,7 @@ struct PhiState {
   long long extend_cols, avnorms, combines;
   double blow_up_scale;
   double amax_step;
+  long long prof[8];  // fused engine: SM clock cycles per phase (apply, dots, update, combine, ctl)
   // ---- Hessenberg (mmax+1) x mmax, row stride kMaxBasis; last, so the controller
   // copies the scalar state plus only the rows in use
   alignas(16) double H[(kMaxBasis + 1) * kMaxBasis];

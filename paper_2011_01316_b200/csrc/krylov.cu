@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "fused.cuh"
 #include "krylov.cuh"
 
 namespace expdg {
@@ -807,6 +808,265 @@ __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double
   ctl_body(st, slot0, W, nullptr, 0, cond, use_graph);
 }
 
+// ------------------------------------------------------------------ fused small-problem engine
+// (fused.cuh).  PhiState is copied into shared memory up to the Hessenberg rows in use.
+constexpr size_t kPhiHOff = offsetof(PhiState, H);
+static_assert(kPhiHOff % 8 == 0 && offsetof(PhiState, H) + sizeof(double) * (kMaxBasis + 1) * kMaxBasis ==
+                  sizeof(PhiState), "H must be the last PhiState member");
+
+// [0, HOff + hbytes) in 8-byte words, 16 independent loads in flight per thread
+__device__ __forceinline__ void state_copy(unsigned char* dst, const unsigned char* src, size_t hbytes) {
+  const size_t nw = (kPhiHOff + hbytes) / 8;
+  const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src);
+  unsigned long long* d = reinterpret_cast<unsigned long long*>(dst);
+  const size_t t = threadIdx.x, nt = blockDim.x;
+  for (size_t b0 = 0; b0 < nw; b0 += 16 * nt) {
+    unsigned long long v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const size_t i = b0 + u * nt + t;
+      v[u] = i < nw ? s[i] : 0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const size_t i = b0 + u * nt + t;
+      if (i < nw) d[i] = v[u];
+    }
+  }
+}
+
+// The fused passes run over [0, Lp), Lp = L rounded up to the block size (<= ld): the
+// slot padding is zero and stays zero, so no per-element predicates; 32-bit indices.
+//
+// dst[i] = <slot_{i0+i}, y> for i < k: one warp per vector, four lane accumulators,
+// fixed-order warp reductions.
+__device__ __forceinline__ void fused_dots(const double* base, int ld, int i0, int k, const double* y, int Lp,
+                                           double* dst) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = wid; i < k; i += nw) {
+    const double* v = base + (i0 + i) * ld;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+    int d = lane;
+    for (; d + 96 < Lp; d += 128) {
+      p0 = fma(v[d], y[d], p0);
+      p1 = fma(v[d + 32], y[d + 32], p1);
+      p2 = fma(v[d + 64], y[d + 64], p2);
+      p3 = fma(v[d + 96], y[d + 96], p3);
+    }
+    for (; d < Lp; d += 32) p0 = fma(v[d], y[d], p0);
+    const double p = warp_sum((p0 + p1) + (p2 + p3));
+    if (lane == 0) dst[i] = p;
+  }
+  __syncthreads();
+}
+
+// y -= sum_i c_i slot_{i0+i}; a thread updates up to 8 of its elements together,
+// two basis vectors per step (16 independent loads in flight); returns its ||y||^2 share
+__device__ __forceinline__ double fused_update(double* base, int ld, int i0, int k, const double* c, double* y,
+                                               int Lp) {
+  const int T = blockDim.x, nq = Lp / T;
+  const double* v0 = base + i0 * ld + threadIdx.x;
+  double* yt = y + threadIdx.x;
+  double nacc = 0.0;
+  for (int q0 = 0; q0 < nq; q0 += 8) {
+    const int qn = min(8, nq - q0);
+    double a[8], b2[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      a[q] = q < qn ? yt[(q0 + q) * T] : 0.0;
+      b2[q] = 0.0;
+    }
+    int i = 0;
+    for (; i + 1 < k; i += 2) {
+      const double c0 = c[i], c1 = c[i + 1];
+      const double* p0 = v0 + i * ld + q0 * T;
+      const double* p1 = p0 + ld;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < qn) {
+          a[q] = fma(-c0, p0[q * T], a[q]);
+          b2[q] = fma(-c1, p1[q * T], b2[q]);
+        }
+    }
+    if (i < k) {
+      const double c0 = c[i];
+      const double* p0 = v0 + i * ld + q0 * T;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < qn) a[q] = fma(-c0, p0[q * T], a[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < qn) {
+        const double yv = a[q] + b2[q];
+        yt[(q0 + q) * T] = yv;
+        nacc = fma(yv, yv, nacc);
+      }
+  }
+  return nacc;
+}
+
+// dynamic shared memory of the fused kernel: PhiState up to the Hessenberg rows in use,
+// then the controller's expm workspace when the augmented Hessenberg is small
+__host__ __device__ constexpr size_t fused_state_bytes(int mmax) {
+  return ((kPhiHOff + sizeof(double) * (size_t)(mmax + 2 < kMaxBasis + 1 ? mmax + 2 : kMaxBasis + 1) * kMaxBasis +
+           15) / 16) * 16;
+}
+constexpr int kFusedWsN = 48;  // expm workspace in shared memory for N <= 48 (9 N^2 doubles)
+
+template <class EL>
+__global__ void __launch_bounds__(kFusedThreads, 1) k_phi_fused(PhiState* gst, double* base, double* W, BArgs b,
+                                                               EL el, int ws_cap) {
+  extern __shared__ __align__(16) unsigned char fsm[];
+  PhiState* st = reinterpret_cast<PhiState*>(fsm);
+  __shared__ size_t s_hb;
+  __shared__ int s_act;
+  __shared__ double s_buf[kFusedThreads / 32];
+  __shared__ double s_c[kMaxSlots];
+  __shared__ double s_xt[kMaxP];
+  const int tid = threadIdx.x;
+  if (tid == 0) s_hb = sizeof(double) * (size_t)min(gst->mmax + 2, kMaxBasis + 1) * kMaxBasis;
+  __syncthreads();
+  const size_t hb = s_hb;
+  double* Wsm = reinterpret_cast<double*>(fsm + ((kPhiHOff + hb + 15) / 16) * 16);
+  state_copy(fsm, reinterpret_cast<const unsigned char*>(gst), hb);
+  __syncthreads();
+  const long long n = st->n, L = n + kTailPad, ld = st->ld;
+  const int ld32 = (int)ld;
+  const long long Lr = ((L + kFusedThreads - 1) / kFusedThreads) * kFusedThreads;
+  const int Lp = (int)(Lr < ld ? Lr : ld);
+  constexpr int NP = EL::kNP;
+  long long t0 = clock64();
+  auto mark = [&](int slot) {  // thread 0 after a barrier: cycles of the phase just finished
+    if (tid == 0) {
+      const long long t1 = clock64();
+      st->prof[slot] += t1 - t0;
+      t0 = t1;
+    }
+  };
+  for (;;) {
+    if (tid == 0) s_act = st->stopped ? ACT_DONE : st->action;
+    __syncthreads();
+    const int act = s_act;
+    if (act == ACT_DONE || act == ACT_NONE) break;
+    if (act == ACT_EXTEND || act == ACT_AVNORM) {
+      // y = dt (L s_j V_j + sum x_tail b) into slot j+1 (proj/src/phi.cpp:151-158)
+      const int j = st->j;
+      const double xs = st->scale[j], dt = st->dt;
+      const double* x = base + (size_t)j * ld;
+      double* y = base + (size_t)(j + 1) * ld;
+      if (tid < kMaxP) s_xt[tid] = tid < b.p ? x[n + tid] * xs : 0.0;
+      __syncthreads();
+      double nacc = 0.0;
+      const int ne = el.elements();
+      for (int e = tid; e < ne; e += kFusedThreads) {
+        double out[NP];
+        el.apply(e, x, xs, out);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const size_t g = (size_t)e * NP + i;
+          const double v = dt * aug_tail(b, s_xt, g, out[i]);
+          y[g] = v;
+          nacc = fma(v, v, nacc);
+        }
+      }
+      if (tid < kTailPad) {
+        const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
+        y[n + tid] = v;
+        nacc = fma(v, v, nacc);
+      }
+      const double tot = block_sum(nacc, s_buf);
+      if (tid == 0) st->red.nrmA = tot;
+      __syncthreads();
+      mark(0);
+      if (act == ACT_EXTEND) {  // CGS2 passes of krylov.cu (same coefficients), or one IOP pass
+        const int i0 = st->j0, k = j - i0 + 1;
+        fused_dots(base, ld32, i0, k, y, Lp, st->red.dotA + i0);
+        mark(1);
+        if (st->full_orth) {
+          for (int i = tid; i < k; i += blockDim.x) {
+            const double sc = st->scale[i0 + i];
+            s_c[i] = sc * sc * st->red.dotA[i0 + i];
+          }
+          __syncthreads();
+          fused_update(base, ld32, i0, k, s_c, y, Lp);
+          __syncthreads();
+          mark(2);
+          fused_dots(base, ld32, i0, k, y, Lp, st->red.dotB + i0);
+          mark(1);
+        }
+        for (int i = tid; i < k; i += blockDim.x) {
+          const double sc = st->scale[i0 + i];
+          s_c[i] = sc * sc * (st->full_orth ? st->red.dotB[i0 + i] : st->red.dotA[i0 + i]);
+        }
+        __syncthreads();
+        const double nn = block_sum(fused_update(base, ld32, i0, k, s_c, y, Lp), s_buf);
+        if (tid == 0) st->red.nrmC = nn;
+        __syncthreads();
+        mark(2);
+      }
+    } else if (act == ACT_COMBINE) {
+      // w = V_{0:mc} (beta f(0:mc, 0)) in place in slot 0 (proj/src/phi.cpp:227)
+      const int k = st->mc;
+      for (int i = tid; i < k; i += blockDim.x) s_c[i] = st->scale[i] * st->comb[i];
+      __syncthreads();
+      double nacc = 0.0;
+      for (long long d = tid; d < L; d += blockDim.x) {
+        double a = 0.0;
+        for (int i = 0; i < k; ++i) a = fma(s_c[i], base[(size_t)i * ld + d], a);
+        base[d] = a;
+        if (d < n) nacc = fma(a, a, nacc);
+      }
+      const double tot = block_sum(nacc, s_buf);
+      if (tid == 0) st->red.w2 = tot;
+      __syncthreads();
+      mark(3);
+    }
+    ctl_body(st, base, W, Wsm, ws_cap, cudaGraphConditionalHandle{}, 0);
+    __syncthreads();
+    mark(4);
+  }
+  __syncthreads();
+  state_copy(reinterpret_cast<unsigned char*>(gst), fsm, hb);
+}
+
+template <class EL>
+void launch_phi_fused(cudaStream_t s, Engine& e, const EL& el, const BArgs& b) {
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    cudaFuncAttributes fa;
+    EXPDG_CUDA(cudaFuncGetAttributes(&fa, k_phi_fused<EL>));
+    max_dyn = 232448 - (int)fa.sharedSizeBytes;
+    EXPDG_CUDA(cudaFuncSetAttribute(k_phi_fused<EL>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+  }
+  const int mmax = e.st_host->mmax;
+  const size_t state = fused_state_bytes(mmax);
+  int nws = std::min(mmax + 2, kFusedWsN);
+  while (nws > 0 && state + sizeof(double) * 9 * nws * nws > (size_t)max_dyn) --nws;
+  const size_t smem = state + sizeof(double) * 9 * nws * nws;
+  k_phi_fused<EL><<<1, kFusedThreads, smem, s>>>(e.st, e.base, e.ework, b, el, 9 * nws * nws);
+}
+
+template void launch_phi_fused<B1FusedElem<2>>(cudaStream_t, Engine&, const B1FusedElem<2>&, const BArgs&);
+template void launch_phi_fused<B1FusedElem<3>>(cudaStream_t, Engine&, const B1FusedElem<3>&, const BArgs&);
+template void launch_phi_fused<B1FusedElem<4>>(cudaStream_t, Engine&, const B1FusedElem<4>&, const BArgs&);
+template void launch_phi_fused<B1FusedElem<5>>(cudaStream_t, Engine&, const B1FusedElem<5>&, const BArgs&);
+template void launch_phi_fused<B1FusedElem<6>>(cudaStream_t, Engine&, const B1FusedElem<6>&, const BArgs&);
+template void launch_phi_fused<B1FusedElem<7>>(cudaStream_t, Engine&, const B1FusedElem<7>&, const BArgs&);
+template void launch_phi_fused<B1FusedElem<8>>(cudaStream_t, Engine&, const B1FusedElem<8>&, const BArgs&);
+template void launch_phi_fused<B1FusedElem<9>>(cudaStream_t, Engine&, const B1FusedElem<9>&, const BArgs&);
+#define FUSED_OI(NP, NQ) \
+  template void launch_phi_fused<B1OIFusedElem<NP, NQ>>(cudaStream_t, Engine&, const B1OIFusedElem<NP, NQ>&, const BArgs&);
+FUSED_OI(2, 3)
+FUSED_OI(3, 4)
+FUSED_OI(4, 6)
+FUSED_OI(5, 7)
+FUSED_OI(6, 9)
+FUSED_OI(7, 10)
+FUSED_OI(8, 12)
+FUSED_OI(9, 13)
+#undef FUSED_OI
+
 // Sets action = START / DONE after the init reduction (separate tiny kernel so the
 // decision sees the fully reduced norms).
 __global__ void k_phi_start(PhiState* st) {
@@ -865,6 +1125,7 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_TS_STAGES")) ts_tuning.stages = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_TS_MIN_T")) ts_tuning.min_T = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_LD_ODD")) ld_odd = std::atoi(v);
+  if (const char* v = std::getenv("EXPDG_FUSED")) use_fused = std::atoi(v) != 0;
   if (const char* v = std::getenv("EXPDG_ORTH"))
     use_dcgs = std::strcmp(v, "cgs2") == 0 ? 0 : (std::strcmp(v, "dcgs2") == 0 ? 2 : 1);
   dcgs_init_attrs(maxsm);
@@ -1054,7 +1315,17 @@ double Engine::bench_ts(long long n, int k, int mode, int reps) {
   return ms / reps;
 }
 
+bool Engine::fused_ok(const OpDevice& op) const {
+  return use_fused && !comm && !st_host->dcgs && op.fused_capable();
+}
+
 void Engine::run_phi(OpDevice& op, const BArgs& b, int use_graph) {
+  if (fused_ok(op)) {  // small problem: the whole call in one single-CTA kernel
+    launch_phi_init(stream, b);
+    op.launch_fused(stream, *this, b);
+    EXPDG_CUDA(cudaStreamSynchronize(stream));
+    return;
+  }
   if (use_graph && !comm) {
     cudaGraphExec_t ex = build_phi_graph(op, b);
     EXPDG_CUDA(cudaGraphLaunch(ex, stream));

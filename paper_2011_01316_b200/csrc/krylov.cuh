@@ -27,6 +27,8 @@ __device__ __forceinline__ double aug_tail(const BArgs& b, const double* xt, siz
 }
 #endif
 
+class Engine;
+
 // Device operator: one DG operator frozen at a reference state (ũ pointer).
 class OpDevice {
  public:
@@ -50,6 +52,9 @@ class OpDevice {
                                double* partials) = 0;
   // Whether the apply kernel also writes pass-A dots (else the generic kernel runs).
   virtual bool fused_dots() const { return false; }
+  // Small problems: the whole phi call as one single-CTA kernel (fused.cuh)
+  virtual bool fused_capable() const { return false; }
+  virtual void launch_fused(cudaStream_t, Engine&, const BArgs&) {}
   // Freeze the reference state (proj/src/burgers.cpp:53-78, proj/src/euler.cpp:198-243):
   // operators that keep derived frozen data compute it here.
   virtual void freeze(cudaStream_t s, const double* r) { ref = r; }
@@ -92,6 +97,8 @@ class Engine {
   TsTuning ts_tuning;
   int ld_odd = 1;
   int use_dcgs = 1;  // 0 CGS2, 1 auto (DCGS2 from 2^18 DOF), 2 DCGS2 (EXPDG_ORTH=cgs2|dcgs2)
+  int use_fused = 1;  // small problems run each phi call as one fused kernel (EXPDG_FUSED=0: off)
+  bool fused_ok(const OpDevice& op) const;
   // Set when the context belongs to a slab-partitioned group: every reducing
   // kernel is followed by a sum-allreduce of PhiState::loc -> PhiState::red,
   // and the control runs host-stepped (no CUDA graphs).

@@ -9,7 +9,7 @@
 // and writes y once: 32 B/DOF (SURVEY.md §8d canonical JVP bytes).
 #include <algorithm>
 
-#include "burgers_common.cuh"
+#include "fused.cuh"
 
 namespace expdg {
 
@@ -222,6 +222,11 @@ class Burgers1D : public B1Base<B1P<NP>, NP, 1> {
                const BArgs& b) override {
     k_b1_phi<NP><<<this->grid, kB1Threads, 0, s>>>(p, st, base, partials, b);
   }
+  bool fused_capable() const override { return !this->P.part && this->n <= kFusedMaxN; }
+  void launch_fused(cudaStream_t s, Engine& e, const BArgs& b) override {
+    B1FusedElem<NP> el{this->params(this->ref)};
+    launch_phi_fused(s, e, el, b);
+  }
   void run_apply(cudaStream_t s, const B1P<NP>& p, int mode, const double* x, double* y,
                  const PhiState* st) override {
     k_b1_apply<NP><<<this->grid, kB1Threads, 0, s>>>(p, mode, x, y, st);
@@ -344,6 +349,11 @@ class Burgers1DOI : public B1Base<B1OP<NP, NQ>, NP, 2> {
   void run_phi(cudaStream_t s, const B1OP<NP, NQ>& p, PhiState* st, double* base, double* partials,
                const BArgs& b) override {
     k_b1oi_phi<NP, NQ><<<this->grid, kB1Threads, 0, s>>>(p, st, base, partials, b);
+  }
+  bool fused_capable() const override { return !this->P.part && this->n <= kFusedMaxN; }
+  void launch_fused(cudaStream_t s, Engine& e, const BArgs& b) override {
+    B1OIFusedElem<NP, NQ> el{this->params(this->ref)};
+    launch_phi_fused(s, e, el, b);
   }
   void run_apply(cudaStream_t s, const B1OP<NP, NQ>& p, int mode, const double* x, double* y,
                  const PhiState* st) override {

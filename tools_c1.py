@@ -17,6 +17,8 @@ pkg.integrate(ctx, op, to_dev(u0), "epi2", w.dt, 20 * w.dt, **kw)
 r = pkg.integrate(ctx, op, to_dev(u0), "epi2", w.dt, w.steps * w.dt, **kw)
 print(f"device: {r.loop_ms / r.steps * 1e3:.1f} us/step, {r.krylov_iterations / r.steps:.1f} iters/step, "
       f"launches {ctx.kernel_launches}")
+prof = ctx.debug_profile()
+print("fused phases (us/step at 1.9 GHz):", {k: round(v / 1.9e3 / r.steps, 1) for k, v in prof.items()})
 if len(sys.argv) > 2:
     import oracle
     from tests.gpu_util import oracle_problem
