@@ -3,7 +3,7 @@ import json
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2011_01316_b200 as pkg
 
 n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 104857601
