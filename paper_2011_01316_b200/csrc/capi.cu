@@ -489,6 +489,18 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     return v;
   };
   max0 = global_max(max0);
+  // the first linearisation of a non-finite Burgers state throws invalid_argument out of
+  // integrate (proj/src/burgers.cpp:34-35; integrate only converts KrylovError /
+  // domain_error, proj/src/integrators.cpp:179-183); Euler reports it as a domain error
+  // (blew_up at step 1) through the residual's admissibility test
+  {
+    double nonfinite = 0.0;
+    for (int i = 0; i < rgrid; ++i) nonfinite = std::max(nonfinite, h2[2 * i + 1]);
+    nonfinite = global_max(nonfinite);
+    const int k = dev.desc.kind;
+    if (nonfinite > 0.0 && (k == EXPDG_BURGERS1D || k == EXPDG_BURGERS2D))
+      throw std::invalid_argument("BurgersOperator: reference state not finite");
+  }
   if (kind == EXPDG_EXP_EULER) {
     const int chk = (int)global_max((double)op_check_ref(dev, e.stream, u));
     if (chk == 2) throw std::domain_error("EulerOperator: inadmissible reference state");
