@@ -47,6 +47,32 @@ struct B1FusedElem {
     load(P.ut, 1.0, e + 1, ur);
     burgers::b1_element<NP>(P, 0, e, xl, xc, xr, ul, uc, ur, out);
   }
+  // same with the applied vector and u~ gathered by fx / fu(element, out[NP]) (cluster
+  // engine: shared-memory slices, possibly another CTA's); boundary handling as load()
+  template <class FX, class FU>
+  __device__ __forceinline__ void apply_with(int e, FX&& fx, FU&& fu, double* out) const {
+    double xl[NP], xc[NP], xr[NP], ul[NP], uc[NP], ur[NP];
+    gather(fx, e - 1, xl);
+    gather(fx, e, xc);
+    gather(fx, e + 1, xr);
+    gather(fu, e - 1, ul);
+    gather(fu, e, uc);
+    gather(fu, e + 1, ur);
+    burgers::b1_element<NP>(P, 0, e, xl, xc, xr, ul, uc, ur, out);
+  }
+  template <class FX>
+  __device__ __forceinline__ void gather(FX&& fx, int le, double* out) const {
+    int w = le;
+    if (w < 0 || w >= P.nel) {
+      if (!P.periodic) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) out[i] = 0.0;
+        return;
+      }
+      w = w < 0 ? w + P.nel : w - P.nel;
+    }
+    fx(w, out);
+  }
   __device__ __forceinline__ int elements() const { return P.nel; }
 };
 
@@ -79,6 +105,32 @@ struct B1OIFusedElem {
     load(P.ut, 1.0, e, uc);
     load(P.ut, 1.0, e + 1, ur);
     burgers::b1oi_element<NP, NQ>(P, 0, e, xll, xl, xc, xr, xrr, ul, uc, ur, out);
+  }
+  template <class FX, class FU>
+  __device__ __forceinline__ void apply_with(int e, FX&& fx, FU&& fu, double* out) const {
+    double xll[NP], xl[NP], xc[NP], xr[NP], xrr[NP], ul[NP], uc[NP], ur[NP];
+    gather(fx, e - 2, xll);
+    gather(fx, e - 1, xl);
+    gather(fx, e, xc);
+    gather(fx, e + 1, xr);
+    gather(fx, e + 2, xrr);
+    gather(fu, e - 1, ul);
+    gather(fu, e, uc);
+    gather(fu, e + 1, ur);
+    burgers::b1oi_element<NP, NQ>(P, 0, e, xll, xl, xc, xr, xrr, ul, uc, ur, out);
+  }
+  template <class FX>
+  __device__ __forceinline__ void gather(FX&& fx, int le, double* out) const {
+    int w = le;
+    if (w < 0 || w >= P.nel) {
+      if (!P.periodic) {
+#pragma unroll
+        for (int i = 0; i < NP; ++i) out[i] = 0.0;
+        return;
+      }
+      w = w < 0 ? w + P.nel : w - P.nel;
+    }
+    fx(w, out);
   }
   __device__ __forceinline__ int elements() const { return P.nel; }
 };

@@ -21,6 +21,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "fused.cuh"
 #include "krylov.cuh"
 
@@ -1030,8 +1032,305 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_phi_fused(PhiState* gst, d
   state_copy(reinterpret_cast<unsigned char*>(gst), fsm, hb);
 }
 
+// ------------------------------------------------------------------ cluster engine (small problems)
+// The fused engine spread over a thread-block cluster: CTA r of an 8-CTA cluster owns
+// elements [r epc, (r+1) epc) and keeps its slice of EVERY Krylov vector in its own
+// shared memory; neighbour elements of the operator and the partial sums of every
+// reduction are read from the other CTAs' shared memory (DSMEM).  Each reduction is
+// one cluster barrier: every CTA writes its partials to its own (double-buffered)
+// buffer, then every CTA sums all of them in rank order (identical totals).  CTA 0
+// holds PhiState in shared memory and runs the controller (ctl_body); the others read
+// its decisions through DSMEM.  No basis traffic leaves the SMs.
+namespace cg = cooperative_groups;
+constexpr int kClusterCTAs = 8;
+constexpr int kClusterThreads = 256;
+
+template <class EL>
+__global__ void __launch_bounds__(kClusterThreads, 1)
+    k_phi_cluster(PhiState* gst, double* base, double* W, BArgs b, EL el, int epc, int lds, int nslots,
+                  int ws_cap, int state_off, int ws_off) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank(), CS = (int)cl.num_blocks();
+  extern __shared__ __align__(16) unsigned char csm[];
+  double* V = reinterpret_cast<double*>(csm);
+  double* part = V + (size_t)nslots * lds;  // 2 x (2 kMaxSlots + 2)
+  double* ul = part + 2 * (2 * kMaxSlots + 2);  // u~ of elements [e_lo - 1, e_hi + 1), frozen for the call
+  double* bl = ul + (size_t)(epc + 2) * EL::kNP;  // b_1..b_p slices: p x (epc NP)
+  PhiState* st0 = reinterpret_cast<PhiState*>(csm + state_off);
+  double* Wsm = reinterpret_cast<double*>(csm + ws_off);
+  __shared__ int s_act, s_j, s_j0, s_full, s_mc, s_p, s_tailhere;
+  __shared__ double s_dt;
+  __shared__ double s_scale[kMaxSlots], s_c[kMaxSlots], s_mine[2 * kMaxSlots + 2], s_tot[2 * kMaxSlots + 2];
+  __shared__ double s_xt[kMaxP], s_buf[kClusterThreads / 32];
+  __shared__ size_t s_hb;
+  constexpr int NP = EL::kNP;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, T = blockDim.x;
+  const int nel = el.elements();
+  const int e_lo = min(rank * epc, nel), e_hi = min(e_lo + epc, nel);
+  const int nloc = (e_hi - e_lo) * NP, tail_at = epc * NP;
+  const long long n = gst->n;
+  // ---- init: this CTA's slice of slot 0 (the phi vector of k_phi_init); CTA 0: PhiState
+  for (int i = tid; i < nloc; i += T) V[i] = base[(size_t)e_lo * NP + i];
+  for (int i = tid; i < kTailPad; i += T) V[tail_at + i] = base[n + i];
+  for (int i = tid; i < (e_hi - e_lo + 2) * NP; i += T) {  // u~ with one element either side
+    double o[NP];
+    el.gather([&](int w, double* oo) {
+#pragma unroll
+      for (int q = 0; q < NP; ++q) oo[q] = el.P.ut[(size_t)w * NP + q];
+    }, e_lo - 1 + i / NP, o);
+    ul[i] = o[i % NP];
+  }
+  for (int m = 1; m <= b.p && m <= kMaxP; ++m)
+    for (int i = tid; i < nloc; i += T) bl[(size_t)(m - 1) * epc * NP + i] = b.b[m] ? b.b[m][(size_t)e_lo * NP + i] : 0.0;
+  if (rank == 0) {
+    if (tid == 0) s_hb = sizeof(double) * (size_t)min(gst->mmax + 2, kMaxBasis + 1) * kMaxBasis;
+    __syncthreads();
+    state_copy(reinterpret_cast<unsigned char*>(st0), reinterpret_cast<const unsigned char*>(gst), s_hb);
+  }
+  const PhiState* S = cl.map_shared_rank(st0, 0);
+  const int nsc = nslots < kMaxSlots ? nslots : kMaxSlots;
+  // CTA 0 pushes the controller's decision (action, column, scales) into every CTA's
+  // shared memory, so the other CTAs never chase scalars through DSMEM
+  auto push = [&]() {
+    __syncthreads();
+    for (int r = tid; r < CS; r += T) {
+      *cl.map_shared_rank(&s_act, r) = st0->stopped ? ACT_DONE : st0->action;
+      *cl.map_shared_rank(&s_j, r) = st0->j;
+      *cl.map_shared_rank(&s_j0, r) = st0->j0;
+      *cl.map_shared_rank(&s_full, r) = st0->full_orth;
+      *cl.map_shared_rank(&s_mc, r) = st0->mc;
+      *cl.map_shared_rank(&s_dt, r) = st0->dt;
+    }
+    for (int idx = tid; idx < CS * nsc; idx += T) {
+      const int r = idx / nsc, i = idx - r * nsc;
+      cl.map_shared_rank(s_scale, r)[i] = st0->scale[i];
+    }
+  };
+  if (rank == 0) push();
+  cl.sync();
+  int round = 0;
+  // cluster totals of cnt partial sums in s_mine -> s_tot (every CTA, rank order)
+  auto reduce = [&](int cnt) {
+    double* buf = part + (round & 1) * (2 * kMaxSlots + 2);
+    for (int i = tid; i < cnt; i += T) buf[i] = s_mine[i];
+    cl.sync();
+    for (int i = tid; i < cnt; i += T) {
+      double sum = 0.0;
+      for (int r = 0; r < CS; ++r) sum += cl.map_shared_rank(buf, r)[i];
+      s_tot[i] = sum;
+    }
+    __syncthreads();
+    ++round;
+  };
+  // this CTA's <V_{i0+i}, y> for i < k, one warp per vector (the tail counts on rank 0)
+  auto local_dots = [&](int i0, int k, const double* y) {
+    for (int i = wid; i < k; i += T / 32) {
+      const double* v = V + (size_t)(i0 + i) * lds;
+      double p0 = 0.0, p1 = 0.0;
+      for (int d = lane; d < nloc; d += 64) {
+        p0 = fma(v[d], y[d], p0);
+        if (d + 32 < nloc) p1 = fma(v[d + 32], y[d + 32], p1);
+      }
+      if (s_tailhere && lane < kTailPad) p0 = fma(v[tail_at + lane], y[tail_at + lane], p0);
+      const double p = warp_sum(p0 + p1);
+      if (lane == 0) s_mine[i] = p;
+    }
+    __syncthreads();
+  };
+  // y -= sum_i c_i V_{i0+i} on the local head and the replicated tail; returns this thread's ||y||^2
+  auto local_update = [&](int i0, int k, double* y) {
+    double nacc = 0.0;
+    for (int d = tid; d < nloc + kTailPad; d += T) {
+      const int dd = d < nloc ? d : tail_at + (d - nloc);
+      double a = y[dd], a2 = 0.0;
+      int i = 0;
+      for (; i + 1 < k; i += 2) {
+        a = fma(-s_c[i], V[(size_t)(i0 + i) * lds + dd], a);
+        a2 = fma(-s_c[i + 1], V[(size_t)(i0 + i + 1) * lds + dd], a2);
+      }
+      if (i < k) a = fma(-s_c[i], V[(size_t)(i0 + i) * lds + dd], a);
+      const double yv = a + a2;
+      y[dd] = yv;
+      if (d < nloc || s_tailhere) nacc = fma(yv, yv, nacc);
+    }
+    return nacc;
+  };
+  long long t0 = clock64();
+  auto mark = [&](int slot) {  // CTA 0, thread 0: SM cycles of the phase just finished
+    if (rank == 0 && tid == 0) {
+      const long long t1 = clock64();
+      st0->prof[slot] += t1 - t0;
+      t0 = t1;
+    }
+  };
+  for (;;) {
+    if (tid == 0) {
+      s_p = b.p;
+      s_tailhere = rank == 0;
+    }
+    __syncthreads();
+    const int act = s_act;
+    if (act == ACT_DONE || act == ACT_NONE) break;
+    if (act == ACT_EXTEND || act == ACT_AVNORM) {
+      const int j = s_j;
+      const double xs = s_scale[j], dt = s_dt;
+      const double* x = V + (size_t)j * lds;
+      double* y = V + (size_t)(j + 1) * lds;
+      if (tid < kMaxP) s_xt[tid] = tid < s_p ? x[tail_at + tid] * xs : 0.0;
+      __syncthreads();
+      double nacc = 0.0;
+      for (int e = e_lo + tid; e < e_hi; e += T) {
+        double out[NP];
+        el.apply_with(
+            e,
+            [&](int w, double* o) {
+              const int r = w / epc, li = w - r * epc;
+              const double* src = (r == rank ? V : cl.map_shared_rank(V, r)) + (size_t)j * lds + (size_t)li * NP;
+#pragma unroll
+              for (int i = 0; i < NP; ++i) o[i] = src[i] * xs;
+            },
+            [&](int w, double* o) {  // u~ of a neighbour element (w is already wrapped)
+              int li = w - (e_lo - 1);
+              if (li < 0) li += nel;
+              if (li >= e_hi - e_lo + 2) li -= nel;
+#pragma unroll
+              for (int i = 0; i < NP; ++i) o[i] = ul[(size_t)li * NP + i];
+            },
+            out);
+        const int le = e - e_lo;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          double v = out[i];
+          for (int m = kMaxP; m >= 1; --m)  // aug_tail order (proj/src/phi.cpp:151-158)
+            if (m <= s_p && b.b[m]) v = fma(s_xt[s_p - m], bl[(size_t)(m - 1) * epc * NP + le * NP + i], v);
+          v = dt * v;
+          y[le * NP + i] = v;
+          nacc = fma(v, v, nacc);
+        }
+      }
+      if (tid < kTailPad) {
+        const double v = (tid + 1 < s_p) ? dt * s_xt[tid + 1] : 0.0;
+        y[tail_at + tid] = v;
+        if (s_tailhere) nacc = fma(v, v, nacc);
+      }
+      const double tot = block_sum(nacc, s_buf);
+      if (tid == 0) s_mine[0] = tot;
+      __syncthreads();
+      reduce(1);
+      if (rank == 0 && tid == 0) st0->red.nrmA = s_tot[0];
+      mark(0);
+      if (act == ACT_EXTEND) {  // CGS2 passes (krylov.cu coefficients) or one IOP pass
+        const int i0 = s_j0, k = j - i0 + 1;
+        local_dots(i0, k, y);
+        reduce(k);
+        if (rank == 0)
+          for (int i = tid; i < k; i += T) st0->red.dotA[i0 + i] = s_tot[i];
+        mark(1);
+        if (s_full) {
+          for (int i = tid; i < k; i += T) s_c[i] = s_scale[i0 + i] * s_scale[i0 + i] * s_tot[i];
+          __syncthreads();
+          local_update(i0, k, y);
+          __syncthreads();
+          mark(2);
+          local_dots(i0, k, y);
+          reduce(k);
+          mark(1);
+          if (rank == 0)
+            for (int i = tid; i < k; i += T) st0->red.dotB[i0 + i] = s_tot[i];
+        }
+        for (int i = tid; i < k; i += T) s_c[i] = s_scale[i0 + i] * s_scale[i0 + i] * s_tot[i];
+        __syncthreads();
+        const double nn = block_sum(local_update(i0, k, y), s_buf);
+        if (tid == 0) s_mine[0] = nn;
+        __syncthreads();
+        reduce(1);
+        if (rank == 0 && tid == 0) st0->red.nrmC = s_tot[0];
+        mark(2);
+      }
+    } else if (act == ACT_COMBINE) {
+      const int k = s_mc;
+      for (int i = tid; i < k; i += T) s_c[i] = s_scale[i] * S->comb[i];
+      __syncthreads();
+      double nacc = 0.0;
+      for (int d = tid; d < nloc + kTailPad; d += T) {
+        const int dd = d < nloc ? d : tail_at + (d - nloc);
+        double a = 0.0;
+        for (int i = 0; i < k; ++i) a = fma(s_c[i], V[(size_t)i * lds + dd], a);
+        V[dd] = a;
+        if (d < nloc) nacc = fma(a, a, nacc);
+      }
+      const double tot = block_sum(nacc, s_buf);
+      if (tid == 0) s_mine[0] = tot;
+      __syncthreads();
+      reduce(1);
+      if (rank == 0 && tid == 0) st0->red.w2 = s_tot[0];
+      mark(3);
+    }
+    if (rank == 0) {
+      __syncthreads();
+      // the controller writes the phi tail into CTA 0's slot-0 tail (slot0[n + j])
+      ctl_body(st0, V + tail_at - n, W, Wsm, ws_cap, cudaGraphConditionalHandle{}, 0);
+      push();
+    }
+    cl.sync();
+    if (act == ACT_COMBINE && rank != 0 && tid < kTailPad)  // replicate the reset tail
+      V[tail_at + tid] = cl.map_shared_rank(V, 0)[tail_at + tid];
+    __syncthreads();
+    mark(4);
+  }
+  // ---- the phi vector back to global slot 0; CTA 0: PhiState
+  for (int i = tid; i < nloc; i += T) base[(size_t)e_lo * NP + i] = V[i];
+  if (rank == 0) {
+    for (int i = tid; i < kTailPad; i += T) base[n + i] = V[tail_at + i];
+    __syncthreads();
+    state_copy(reinterpret_cast<unsigned char*>(gst), reinterpret_cast<const unsigned char*>(st0), s_hb);
+  }
+  cl.sync();  // no CTA leaves while others may still read its shared memory
+}
+
+template <class EL>
+bool launch_phi_cluster(cudaStream_t s, Engine& e, const EL& el, const BArgs& b) {
+  static int max_dyn = -1;
+  if (max_dyn < 0) {
+    cudaFuncAttributes fa;
+    EXPDG_CUDA(cudaFuncGetAttributes(&fa, k_phi_cluster<EL>));
+    max_dyn = 232448 - (int)fa.sharedSizeBytes;
+    EXPDG_CUDA(cudaFuncSetAttribute(k_phi_cluster<EL>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+  }
+  const PhiState& c = *e.st_host;
+  const int nel = (int)(c.n / EL::kNP);
+  if (nel < 2 * kClusterCTAs) return false;
+  const int epc = (nel + kClusterCTAs - 1) / kClusterCTAs;
+  const int lds = ((epc * EL::kNP + kTailPad + 1) / 2) * 2;
+  const int nslots = std::min(c.mmax + 2, kMaxSlots);
+  const size_t vbytes = sizeof(double) * ((size_t)nslots * lds + 2 * (2 * kMaxSlots + 2) +
+                                          (size_t)(epc + 2) * EL::kNP + (size_t)b.p * epc * EL::kNP);
+  const size_t state_off = ((vbytes + 15) / 16) * 16;
+  const size_t state = fused_state_bytes(c.mmax);
+  if (state_off + state > (size_t)max_dyn) return false;
+  int nws = std::min(c.mmax + 2, kFusedWsN);
+  while (nws > 0 && state_off + state + sizeof(double) * 9 * nws * nws > (size_t)max_dyn) --nws;
+  const size_t smem = state_off + state + sizeof(double) * 9 * nws * nws;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kClusterCTAs);
+  cfg.blockDim = dim3(kClusterThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kClusterCTAs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  EXPDG_CUDA(cudaLaunchKernelEx(&cfg, k_phi_cluster<EL>, e.st, e.base, e.ework, b, el, epc, lds, nslots,
+                                9 * nws * nws, (int)state_off, (int)(state_off + state)));
+  return true;
+}
+
 template <class EL>
 void launch_phi_fused(cudaStream_t s, Engine& e, const EL& el, const BArgs& b) {
+  if (e.use_fused != 2 && launch_phi_cluster(s, e, el, b)) return;  // EXPDG_FUSED=2: single CTA
   static int max_dyn = -1;
   if (max_dyn < 0) {
     cudaFuncAttributes fa;
@@ -1125,7 +1424,7 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_TS_STAGES")) ts_tuning.stages = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_TS_MIN_T")) ts_tuning.min_T = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_LD_ODD")) ld_odd = std::atoi(v);
-  if (const char* v = std::getenv("EXPDG_FUSED")) use_fused = std::atoi(v) != 0;
+  if (const char* v = std::getenv("EXPDG_FUSED")) use_fused = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_ORTH"))
     use_dcgs = std::strcmp(v, "cgs2") == 0 ? 0 : (std::strcmp(v, "dcgs2") == 0 ? 2 : 1);
   dcgs_init_attrs(maxsm);
