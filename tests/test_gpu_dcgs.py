@@ -3,6 +3,8 @@ against the reference's two-pass modified Gram-Schmidt Arnoldi (proj/src/phi.cpp
 restated in the oracle) on the dense augmented operator [[dt L, dt r], [0, 0]] of a
 stiff over-integrated Burgers problem (acceptance criterion 5's, Cr_d = 161), and
 against each other on the full time loop."""
+import math
+
 import numpy as np
 import pytest
 
@@ -69,3 +71,31 @@ def test_dcgs2_euler_matches_cgs2():
                                   max_basis=w.max_basis, orth_length=w.max_basis)
     assert rel(to_host(res["dcgs2"].u), to_host(res["cgs2"].u)) <= 1e-11
     assert list(res["dcgs2"].iters_per_step) == list(res["cgs2"].iters_per_step)
+
+
+@pytest.mark.parametrize("orth", ["cgs2", "dcgs2"])
+def test_dense_fakes_with_breakdown(orth):
+    # criterion-1 style dense fakes (proj/tests/acceptance.cpp:70-108) forced through each
+    # orthogonalisation; n + p <= max_basis, so every call ends in a (lagged, for DCGS2)
+    # happy breakdown at m = n + p
+    from tests.gpu_util import matrix_with_spectrum
+    rng = np.random.default_rng(77)
+    ctx = pkg.Context(0, orth=orth, fused=False)
+    worst = 0.0
+    for trial in range(12):
+        n = int(rng.integers(6, 60))
+        M = matrix_with_spectrum(rng, n, -30.0, 2.0, 1.0)
+        b = [rng.standard_normal(n) for _ in range(4)]
+        fam = oracle.phi_dense_family(3, M)
+        expect = sum(fam[i] @ b[i] for i in range(4))
+        op = pkg.Operator(ctx, dense=M)
+        got, st = pkg.phi_combination(ctx, op, [to_dev(v) for v in b], 1.0, tol=1e-10)
+        worst = max(worst, rel(to_host(got), expect))
+        _, iters, subs = oracle.phi_combination_dense(M, b, 1.0, tol=1e-10)
+        assert abs(st.iterations - iters) <= 1 and st.substeps == subs
+    assert worst <= 1e-8
+    # the identity: breakdown after one column
+    op = pkg.Operator(ctx, dense=np.eye(8))
+    b0 = rng.standard_normal(8)
+    got, st = pkg.phi_combination(ctx, op, [to_dev(b0)], 0.5, tol=1e-12)
+    assert rel(to_host(got), math.exp(0.5) * b0) < 1e-13
