@@ -253,3 +253,39 @@ def test_partitioned_burgers2d_matches_single_rank(periodic):
         assert rel(np.concatenate([g[0][i] for g in got]), want[i]) < 1e-14
     assert all(g[1].status == single.status == "completed" for g in got)
     assert rel(np.concatenate([g[2] for g in got]), to_host(single.u)) <= 1e-11
+
+
+@pytest.mark.parametrize("integ", ["epi2", "exprb32"])
+def test_partitioned_dcgs2_matches_single_rank(integ):
+    # the DCGS2 passes (k_ts2) with rank-reduced dots: replicated tail masked on ranks > 0
+    w = configs.scaled(configs.C4, 12, steps=2)
+    spec = w.spec()
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    ctx = pkg.Context(0, orth="dcgs2")
+    single = pkg.integrate(ctx, pkg.Operator(ctx, spec), to_dev(u0), integ, dt, w.steps * dt, **kw)
+    ranges = slab_ranges(spec.ny, 3)
+    group = pkg.LocalGroup(3)
+    out, errs = [None] * 3, []
+
+    def body(r):
+        try:
+            c = pkg.Context(0, orth="dcgs2").attach_local(group, r)
+            o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": ranges[r]}))
+            res = pkg.integrate(c, o, to_dev(u0[slab(spec, ranges[r])]), integ, dt, w.steps * dt, **kw)
+            out[r] = (res, to_host(res.u))
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+    assert all(o[0].status == "completed" for o in out)
+    assert rel(np.concatenate([o[1] for o in out]), to_host(single.u)) <= 1e-11
+    assert np.max(np.abs(np.diff(np.concatenate([[0], out[0][0].iters_per_step])) -
+                         np.diff(np.concatenate([[0], single.iters_per_step])))) <= 1
