@@ -127,6 +127,37 @@ def _ref_worker(a):
     return cpu_sample(w, steps=steps, nx=nx, warmup=warmup)
 
 
+def roofline(dominant, step_achieved, peak, peak_kind, traffic, steps):
+    """Roofline of the dominant kernel (live CUDA-event timing of its launches) plus the
+    whole step's algorithmic bandwidth."""
+    step = {"achieved": step_achieved, "frac": step_achieved / peak,
+            "what": "phi engine (JVP + DCGS2 passes + combine + controller): algorithmic bytes of the realised "
+                    "trajectory (DCGS2: JVP 32n + 8n(2k+6) per column; SURVEY's CGS2 count is 8n(3k+6)) / "
+                    "step-loop time",
+            "alg_bytes_per_step": traffic["alg_bytes"] / steps, "columns": traffic["columns"],
+            "avnorms": traffic["avnorms"], "combines": traffic["combines"]}
+    if not dominant or dominant["launches"] == 0 or dominant["ms"] <= 0:
+        return {"bound": "hbm", "achieved": step_achieved, "peak": peak, "unit": "GB/s",
+                "frac": step_achieved / peak, "traffic": None, "kernel": "phi engine step", "peak_kind": peak_kind,
+                "step": step}
+    per_launch_bytes = dominant["bytes"] / dominant["launches"]
+    ach = dominant["bytes"] / (dominant["ms"] * 1e-3) / 1e9
+    traffic_launch, ncu = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_dominant.json")) as f:
+            ncu = json.load(f)
+        traffic_launch = ncu["dram_over_alg"] * per_launch_bytes
+    except Exception:
+        pass
+    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+            "traffic": traffic_launch,
+            "kernel": "k_ts2<TS2_UPD> (DCGS2 update pass: reads V_0..V_{j-1}, u, w; writes u, w)",
+            "alg_bytes_per_launch": per_launch_bytes, "launch_ms": dominant["ms"] / dominant["launches"],
+            "launches": dominant["launches"], "peak_kind": peak_kind,
+            "traffic_source": (ncu or {}).get("source"),
+            "step": step}
+
+
 def run_reference(args, workload):
     """--impl reference: the reference's CPU path (the oracle port; the reference
     itself cannot be built here) on the host cores, bounded samples per step.  The
@@ -178,6 +209,7 @@ def main():
     ap.add_argument("--cpu-nx", type=int, default=128)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dominant", action="store_true", help="skip the dominant-kernel event timing")
     ap.add_argument("--partition", action="store_true",
                     help="slab-partitioned NCCL path even at N = 1 (always used for N > 1)")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent full-size replicas instead")
@@ -251,6 +283,16 @@ def main():
         torch.distributed.barrier()
     launches = ctx.kernel_launches - l0
     traffic = ctx.traffic()
+    dominant = None
+    if not args.no_dominant:
+        # the dominant kernel (DCGS2 update pass, ~42 % of the step): CUDA events around each of
+        # its launches on the context stream over one host-stepped step of the same trajectory
+        ud = u.clone()
+        ctx.time_dominant(True)
+        pkg.integrate(ctx, op, ud, "epi2", dt, dt, **{**kw, "use_graph": False})
+        dominant = ctx.dominant_stats()
+        ctx.time_dominant(False)
+        del ud
     if r.status != "completed" or r.steps != args.steps:
         raise RuntimeError(f"timed run: {r.status} after {r.steps} steps")
     loop_s = r.loop_ms / 1e3
@@ -311,14 +353,7 @@ def main():
                        "parallelism": (f"{world}-way element-row slabs (NCCL halo + allreduce)" if partitioned
                                        else "single GPU" if world == 1 else f"{world} independent replicas"),
                        "krylov_iters_per_step": [int(v) for v in iters_per_step]},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
-                         "kernel": "phi engine cycle (operator apply + DCGS2 dots/update passes + combine + "
-                                   "controller): algorithmic bytes of the realised trajectory (DCGS2: JVP 32n + "
-                                   "8n(2k+6) per column; SURVEY's CGS2 count is 8n(3k+6)) / step-loop time",
-                         "peak_kind": peak_kind, "alg_bytes_per_step": traffic["alg_bytes"] / args.steps,
-                         "columns": traffic["columns"], "avnorms": traffic["avnorms"],
-                         "combines": traffic["combines"]},
+            "roofline": roofline(dominant, achieved, peak, peak_kind, traffic, args.steps),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

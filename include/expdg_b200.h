@@ -227,6 +227,12 @@ double expdg_ctx_last_loop_ms(expdg_ctx* ctx);
 /* Canonical algorithmic HBM bytes of the last integrate / phi call's
  * realised trajectory, and its counts of Arnoldi columns, avnorm applications and
  * accepted substeps: out4 = {bytes, columns, avnorms, combines}. */
+/* Roofline of the dominant kernel (the DCGS2 update pass): with enable = 1 the next
+ * host-stepped runs (expdg_time_cfg.use_graph = 0) record CUDA events around every
+ * update-pass launch on the context stream.  out3 = {summed launch ms, summed
+ * algorithmic bytes 8 n (j + 4), launches that extended a column}. */
+int expdg_ctx_time_dominant(expdg_ctx* ctx, int enable);
+int expdg_ctx_dominant_stats(expdg_ctx* ctx, double* out3);
 /* Fused small-problem engine: SM clock cycles spent per phase in the last run
  * (apply, dots, updates, combine, controller; 0 for the multi-kernel engine). */
 int expdg_debug_profile(expdg_ctx* ctx, long long* out8);

@@ -84,7 +84,7 @@ EXPORTS = [
     "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts", "expdg_op_set_source",
     "expdg_op_set_source_fn", "expdg_nccl_unique_id", "expdg_ctx_attach_nccl", "expdg_local_group_create",
     "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
-    "expdg_debug_profile", "expdg_ctx_set_fused",
+    "expdg_debug_profile", "expdg_ctx_set_fused", "expdg_ctx_time_dominant", "expdg_ctx_dominant_stats",
 ]
 
 _lib = None
@@ -148,6 +148,8 @@ def lib():
     L.expdg_ctx_set_orthogonalization.argtypes = [vp, C.c_int]
     L.expdg_debug_profile.argtypes = [vp, C.POINTER(C.c_longlong)]
     L.expdg_ctx_set_fused.argtypes = [vp, C.c_int]
+    L.expdg_ctx_time_dominant.argtypes = [vp, C.c_int]
+    L.expdg_ctx_dominant_stats.argtypes = [vp, dp]
     _lib = L
     return L
 
@@ -261,6 +263,15 @@ class Context:
         ms = C.c_double()
         _check(lib().expdg_bench_ts(self.h, n, k, mode, reps, C.byref(ms)))
         return ms.value
+
+    def time_dominant(self, enable: bool = True):
+        """CUDA events around every DCGS2 update pass of the next host-stepped runs."""
+        _check(lib().expdg_ctx_time_dominant(self.h, 1 if enable else 0))
+
+    def dominant_stats(self) -> dict:
+        v = np.zeros(3)
+        _check(lib().expdg_ctx_dominant_stats(self.h, _np_ptr(v)))
+        return {"ms": v[0], "bytes": v[1], "launches": int(v[2])}
 
     def debug_profile(self) -> dict:
         """Fused small-problem engine: SM cycles per phase of the last run."""

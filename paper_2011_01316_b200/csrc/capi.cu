@@ -765,6 +765,28 @@ int expdg_debug_state(expdg_ctx* ctx, double* out16) {
   });
 }
 
+int expdg_ctx_time_dominant(expdg_ctx* ctx, int enable) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null argument");
+    ctx->eng->time_upd = enable != 0;
+    ctx->eng->upd_used = 0;
+    EXPDG_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ctx->eng->st) + offsetof(PhiState, upd_bytes), 0,
+                               sizeof(double) + sizeof(long long), ctx->eng->stream));
+    EXPDG_CUDA(cudaStreamSynchronize(ctx->eng->stream));
+  });
+}
+
+int expdg_ctx_dominant_stats(expdg_ctx* ctx, double* out3) {
+  return guard([&] {
+    if (!ctx || !out3) throw std::invalid_argument("null argument");
+    Engine& e = *ctx->eng;
+    EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
+    out3[0] = e.upd_ms();
+    out3[1] = e.st_host->upd_bytes;
+    out3[2] = (double)e.st_host->upd_launches;
+  });
+}
+
 int expdg_debug_profile(expdg_ctx* ctx, long long* out8) {
   return guard([&] {
     if (!ctx || !out8) throw std::invalid_argument("null argument");

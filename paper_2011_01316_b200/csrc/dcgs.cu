@@ -255,6 +255,10 @@ __global__ void __launch_bounds__(kT2Block, 1) k_ts2(PhiState* st, double* base,
       if (i == 0) st->rs().nrmU = v;
       else st->rs().nrmW = v;
     });
+    if (blockIdx.x == 0 && tid == 0) {  // per-launch algorithmic bytes (the dominant kernel's roofline)
+      st->upd_bytes += 8.0 * (double)st->n * (double)(j + 4);
+      st->upd_launches++;
+    }
   }
 }
 

@@ -133,6 +133,8 @@ struct PhiState {
   double blow_up_scale;
   double amax_step;
   long long prof[8];  // fused engine: SM clock cycles per phase (apply, dots, update, combine, ctl)
+  double upd_bytes;   // algorithmic bytes of the DCGS2 update passes that ran (8 n (j + 4) each)
+  long long upd_launches;
   // ---- Hessenberg (mmax+1) x mmax, row stride kMaxBasis; last, so the controller
   // copies the scalar state plus only the rows in use
   alignas(16) double H[(kMaxBasis + 1) * kMaxBasis];

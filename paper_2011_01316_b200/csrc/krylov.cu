@@ -398,6 +398,7 @@ Engine::Engine(int dev) : device(dev) {
 }
 
 Engine::~Engine() {
+  for (cudaEvent_t ev : upd_events) cudaEventDestroy(ev);
   cudaFree(base);
   cudaFree(st);
   cudaFreeHost(st_host);
@@ -522,7 +523,20 @@ void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraph
     launch_dcgs(s, *this, 0);
     reduce(s);
     launch_dcgs(s, *this, 1);
-    launch_dcgs(s, *this, 2);
+    if (time_upd && !use_graph) {
+      if (upd_used + 2 > upd_events.size())
+        for (int q = 0; q < 64; ++q) {
+          cudaEvent_t ev;
+          EXPDG_CUDA(cudaEventCreate(&ev));
+          upd_events.push_back(ev);
+        }
+      EXPDG_CUDA(cudaEventRecord(upd_events[upd_used], s));
+      launch_dcgs(s, *this, 2);
+      EXPDG_CUDA(cudaEventRecord(upd_events[upd_used + 1], s));
+      upd_used += 2;
+    } else {
+      launch_dcgs(s, *this, 2);
+    }
     reduce(s);
     launch_ts(s, TS_COMBINE);
     reduce(s);
@@ -579,6 +593,18 @@ double Engine::bench_ts(long long n, int k, int mode, int reps) {
   cudaEventDestroy(b);
   EXPDG_CUDA(cudaGetLastError());
   return ms / reps;
+}
+
+// Sum of the timed DCGS2 update-pass launches (events recorded by launch_body).  A
+// no-op launch (no extension this cycle) contributes its few microseconds too.
+double Engine::upd_ms() const {
+  double tot = 0.0;
+  for (size_t q = 0; q + 1 < upd_used; q += 2) {
+    float ms = 0.f;
+    EXPDG_CUDA(cudaEventElapsedTime(&ms, upd_events[q], upd_events[q + 1]));
+    tot += ms;
+  }
+  return tot;
 }
 
 bool Engine::fused_ok(const OpDevice& op) const {

@@ -98,6 +98,12 @@ class Engine {
   int ld_odd = 1;
   int use_dcgs = 1;  // 0 CGS2, 1 auto (DCGS2 from 2^18 DOF), 2 DCGS2 (EXPDG_ORTH=cgs2|dcgs2)
   int use_fused = 1;  // small problems run each phi call as one fused kernel (EXPDG_FUSED=0: off)
+  // host-stepped runs: CUDA events around every DCGS2 update pass (the dominant kernel),
+  // so bench.py can report its live per-launch bandwidth
+  bool time_upd = false;
+  std::vector<cudaEvent_t> upd_events;
+  size_t upd_used = 0;
+  double upd_ms() const;
   bool fused_ok(const OpDevice& op) const;
   // Set when the context belongs to a slab-partitioned group: every reducing
   // kernel is followed by a sum-allreduce of PhiState::loc -> PhiState::red,
