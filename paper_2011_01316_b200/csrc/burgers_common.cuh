@@ -21,6 +21,8 @@ struct B1P {
   double Lv[NP * NP];  // lift_vol(i,j) = D(j,i) w_j      (proj/src/burgers.cpp:50)
   const double* ut;
   const double* src;   // weak source (proj/src/burgers.cpp:80-92), may be null
+  const double* hh;    // per global element: h_e, 2 / h_e (host-computed from the breakpoints)
+  double iw[NP];       // 1 / w_i
   long long n;  // slab partition: this rank owns elements [eoff, eoff + nel) of the
   // ne-element mesh; the H elements either side come from the halo buffers
   int nel;
@@ -111,9 +113,9 @@ __device__ __forceinline__ void b1_element(const B1P<NP>& P, int mode, int e, co
   const bool hasR = P.periodic || e < P.ne - 1;
   const int eL = e == 0 ? P.ne - 1 : e - 1;
   const int eR = e == P.ne - 1 ? 0 : e + 1;
-  const double hC = b1_break(P.a, P.b, e + 1, P.ne) - b1_break(P.a, P.b, e, P.ne);
-  const double hL = b1_break(P.a, P.b, eL + 1, P.ne) - b1_break(P.a, P.b, eL, P.ne);
-  const double hR = b1_break(P.a, P.b, eR + 1, P.ne) - b1_break(P.a, P.b, eR, P.ne);
+  // element widths of the breakpoints (proj/src/mesh.cpp:11-16) and 2 / h from the host table
+  const double hC = P.hh[2 * e], hL = P.hh[2 * eL], hR = P.hh[2 * eR];
+  const double cC = P.hh[2 * e + 1];
   double q[NP], qLN = 0.0, qR0 = 0.0;
   if (mode != 1) {
     // LDG gradient (proj/src/burgers.cpp:105-130)
@@ -132,7 +134,7 @@ __device__ __forceinline__ void b1_element(const B1P<NP>& P, int mode, int e, co
 #pragma unroll
       for (int j = 0; j < NP; ++j) s = fma(P.G[N * NP + j], xL[j], s);
       s += (us - xL[N]);
-      qLN = (2.0 / hL) * (s / P.w[N]);
+      qLN = P.hh[2 * eL + 1] * (s * P.iw[N]);
     } else {
       r[0] += -1.0 * (0.0 - xC[0]);
     }
@@ -143,13 +145,12 @@ __device__ __forceinline__ void b1_element(const B1P<NP>& P, int mode, int e, co
 #pragma unroll
       for (int j = 0; j < NP; ++j) s = fma(P.G[j], xR[j], s);
       s -= (us - xR[0]);
-      qR0 = (2.0 / hR) * (s / P.w[0]);
+      qR0 = P.hh[2 * eR + 1] * (s * P.iw[0]);
     } else {
       r[N] += (0.0 - xC[N]);
     }
-    const double c = 2.0 / hC;
 #pragma unroll
-    for (int i = 0; i < NP; ++i) q[i] = c * (r[i] / P.w[i]);
+    for (int i = 0; i < NP; ++i) q[i] = cC * (r[i] * P.iw[i]);
   }
   // volume: gq = kappa q - u~ x | u~ x - x^2/2 | kappa q - x^2/2 ; r = -lift gq
   double gq[NP];
@@ -228,9 +229,8 @@ __device__ __forceinline__ void b1_element(const B1P<NP>& P, int mode, int e, co
     }
     r[N] += f;
   }
-  const double c = 2.0 / hC;
 #pragma unroll
-  for (int i = 0; i < NP; ++i) out[i] = c * (r[i] / P.w[i]);
+  for (int i = 0; i < NP; ++i) out[i] = cC * (r[i] * P.iw[i]);
 }
 
 }  // namespace burgers
@@ -255,6 +255,7 @@ struct B1OP {
   double Mi[NP * NP];   // M^-1
   const double* ut;
   const double* src;    // weak source (proj/src/burgers.cpp:80-92), may be null
+  const double* hh;     // per global element: h_e, 2 / h_e
   long long n;
   // slab partition: this rank owns elements [eoff, eoff + nel) of the
   // ne-element mesh; the H elements either side come from the halo buffers
@@ -311,24 +312,22 @@ __device__ __forceinline__ void b1oi_element(const B1OP<NP, NQ>& P, int mode, in
   const bool hasR = P.periodic || e < ne - 1;
   const int eL = e == 0 ? ne - 1 : e - 1;
   const int eR = e == ne - 1 ? 0 : e + 1;
-  const double hC = b1_break(P.a, P.b, e + 1, ne) - b1_break(P.a, P.b, e, ne);
-  const double hL = b1_break(P.a, P.b, eL + 1, ne) - b1_break(P.a, P.b, eL, ne);
-  const double hR = b1_break(P.a, P.b, eR + 1, ne) - b1_break(P.a, P.b, eR, ne);
+  const double hC = P.hh[2 * e], hL = P.hh[2 * eL], hR = P.hh[2 * eR];
   double q[NP], qLN = 0.0, qR0 = 0.0;
   if (mode != 1) {
     double r[NP], t[NP];
     b1oi_grad_r(P, xL, xC, xR, hasL, hasR, r);
-    b1oi_minv(P, 2.0 / hC, r, q);
+    b1oi_minv(P, P.hh[2 * e + 1], r, q);
     if (hasL) {
       const bool hLL = P.periodic || eL > 0;
       b1oi_grad_r(P, xLL, xL, xC, hLL, true, r);
-      b1oi_minv(P, 2.0 / hL, r, t);
+      b1oi_minv(P, P.hh[2 * eL + 1], r, t);
       qLN = t[N];
     }
     if (hasR) {
       const bool hRR = P.periodic || eR < ne - 1;
       b1oi_grad_r(P, xC, xR, xRR, true, hRR, r);
-      b1oi_minv(P, 2.0 / hR, r, t);
+      b1oi_minv(P, P.hh[2 * eR + 1], r, t);
       qR0 = t[0];
     }
   }
@@ -414,7 +413,7 @@ __device__ __forceinline__ void b1oi_element(const B1OP<NP, NQ>& P, int mode, in
     }
     r[N] += f;
   }
-  b1oi_minv(P, 2.0 / hC, r, out);
+  b1oi_minv(P, P.hh[2 * e + 1], r, out);
 }
 
 }  // namespace burgers

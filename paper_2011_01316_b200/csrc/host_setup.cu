@@ -306,6 +306,19 @@ void host_burgers_source(int order, int ne, double a, double b, bool over_integr
   }
 }
 
+// Per-element {h_e, 2 / h_e} of uniform breakpoints (proj/src/mesh.cpp:11-16), for the
+// Burgers element kernels (no divisions on the device).
+std::vector<double> host_h_table(double a, double b, int ne) {
+  std::vector<double> t(2 * (size_t)ne);
+  for (int e = 0; e < ne; ++e) {
+    const double x0 = e == ne ? b : a + (b - a) * e / ne;
+    const double x1 = e + 1 == ne ? b : a + (b - a) * (e + 1) / ne;
+    t[2 * e] = x1 - x0;
+    t[2 * e + 1] = 2.0 / (x1 - x0);
+  }
+  return t;
+}
+
 // Seeded inputs (identical generator and formulas to the oracle's inputs.cpp).
 void host_initial_condition(int cfg, int nx, int order, uint64_t seed, double noise, double* out) {
   const HostBasis b = host_lgl_basis(order);

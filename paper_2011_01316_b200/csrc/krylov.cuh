@@ -82,6 +82,7 @@ struct HostOI {
   std::vector<double> I, G, Lv, Mi;  // interp (nq x np), grad_vol, lift_vol (np x nq), M^-1
 };
 HostOI host_burgers_oi(int order);
+std::vector<double> host_h_table(double a, double b, int ne);
 void host_burgers_source(int order, int ne, double a, double b, bool over_integrate,
                          double (*fn)(double, void*), void* user, double* out);
 

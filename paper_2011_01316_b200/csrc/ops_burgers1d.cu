@@ -122,10 +122,12 @@ class B1Base : public OpDevice {
   int grid = 1;
   double* src = nullptr;
   double* halo = nullptr;  // x lo/hi, u~ lo/hi, send lo/hi: H NP doubles each
+  double* htab = nullptr;  // {h_e, 2 / h_e} per global element
   long long layer = 0;
   ~B1Base() override {
     cudaFree(src);
     cudaFree(halo);
+    cudaFree(htab);
   }
   double* hq(int i) const { return halo + (size_t)i * layer; }
   void init_mesh(const expdg_op_desc& d) {
@@ -152,6 +154,10 @@ class B1Base : public OpDevice {
     }
     const int ntiles = (P.nel + kB1Threads - 1) / kB1Threads;
     grid = std::max(1, std::min(ntiles, 148 * 8));
+    const std::vector<double> ht = host_h_table(d.x0, d.x1, d.nx);
+    EXPDG_CUDA(cudaMalloc(&htab, sizeof(double) * ht.size()));
+    EXPDG_CUDA(cudaMemcpy(htab, ht.data(), sizeof(double) * ht.size(), cudaMemcpyHostToDevice));
+    P.hh = htab;
   }
   void exchange(cudaStream_t s, const double* v, double* lo, double* hi) {
     comm->halo(v, v + (size_t)(P.nel - H) * NP, lo, hi, layer, s);
@@ -212,6 +218,7 @@ class Burgers1D : public B1Base<B1P<NP>, NP, 1> {
     this->init_mesh(d);
     for (int i = 0; i < NP; ++i) {
       this->P.w[i] = hb.weights[i];
+      this->P.iw[i] = 1.0 / hb.weights[i];
       for (int j = 0; j < NP; ++j) {
         this->P.G[i * NP + j] = hb.weights[i] * hb.D[i * NP + j];
         this->P.Lv[i * NP + j] = hb.D[j * NP + i] * hb.weights[j];

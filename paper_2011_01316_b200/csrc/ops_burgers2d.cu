@@ -161,8 +161,12 @@ class Burgers2D : public OpDevice {
   B1P<NP> Px{}, Py{};
   int nx = 0, ny = 0, grid = 1;  // ny: owned element rows
   double* halo = nullptr;        // row slab: x lo/hi, u~ lo/hi, send lo/hi (one element row each)
+  double* htab = nullptr;        // {h, 2 / h} per element column, then per element row
   long long rowd = 0;
-  ~Burgers2D() override { cudaFree(halo); }
+  ~Burgers2D() override {
+    cudaFree(halo);
+    cudaFree(htab);
+  }
   double* hq(int i) const { return halo + (size_t)i * rowd; }
   explicit Burgers2D(const expdg_op_desc& d) {
     desc = d;
@@ -178,6 +182,7 @@ class Burgers2D : public OpDevice {
       P->sigma_adaptive = d.sigma_adaptive;
       for (int i = 0; i < NP; ++i) {
         P->w[i] = hb.weights[i];
+        P->iw[i] = 1.0 / hb.weights[i];
         for (int j = 0; j < NP; ++j) {
           P->G[i * NP + j] = hb.weights[i] * hb.D[i * NP + j];
           P->Lv[i * NP + j] = hb.D[j * NP + i] * hb.weights[j];
@@ -198,6 +203,15 @@ class Burgers2D : public OpDevice {
     Px.n = Py.n = n;
     comps = 1;
     rowd = (long long)d.nx * NP * NP;
+    {
+      std::vector<double> ht = host_h_table(d.x0, d.x1, d.nx);
+      const std::vector<double> hy = host_h_table(d.y0, d.y1, d.ny);
+      ht.insert(ht.end(), hy.begin(), hy.end());
+      EXPDG_CUDA(cudaMalloc(&htab, sizeof(double) * ht.size()));
+      EXPDG_CUDA(cudaMemcpy(htab, ht.data(), sizeof(double) * ht.size(), cudaMemcpyHostToDevice));
+      Px.hh = htab;
+      Py.hh = htab + 2 * (size_t)d.nx;
+    }
     if (part) {
       EXPDG_CUDA(cudaMalloc(&halo, sizeof(double) * 6 * rowd));
       EXPDG_CUDA(cudaMemset(halo, 0, sizeof(double) * 6 * rowd));
