@@ -589,8 +589,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   auto host_loop = [&](const BArgs& b, bool dcgs) {
     for (long long cyc = 0;; ++cyc) {
       e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0, dcgs);
-      EXPDG_CUDA(cudaMemcpyAsync(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost, e.stream));
-      EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+      e.fetch_control(e.stream);  // action + stopped only (8 bytes, not the whole PhiState)
       if (e.st_host->action == ACT_DONE || e.st_host->action == ACT_NONE || e.st_host->stopped) break;
       if (cyc > 10000000) throw CudaError("host-stepped phi did not terminate");
     }

@@ -607,6 +607,12 @@ double Engine::upd_ms() const {
   return tot;
 }
 
+void Engine::fetch_control(cudaStream_t s) {
+  EXPDG_CUDA(cudaMemcpyAsync(&st_host->action, &st->action, sizeof(int), cudaMemcpyDeviceToHost, s));
+  EXPDG_CUDA(cudaMemcpyAsync(&st_host->stopped, &st->stopped, sizeof(int), cudaMemcpyDeviceToHost, s));
+  EXPDG_CUDA(cudaStreamSynchronize(s));
+}
+
 bool Engine::fused_ok(const OpDevice& op) const {
   return use_fused && !comm && !st_host->dcgs && op.fused_capable();
 }
@@ -628,8 +634,7 @@ void Engine::run_phi(OpDevice& op, const BArgs& b, int use_graph) {
   launch_phi_init(stream, b);
   for (int cyc = 0; cyc < 1000000; ++cyc) {
     launch_body(stream, op, b, cudaGraphConditionalHandle{}, 0, st_host->dcgs != 0);
-    EXPDG_CUDA(cudaMemcpyAsync(st_host, st, sizeof(PhiState), cudaMemcpyDeviceToHost, stream));
-    EXPDG_CUDA(cudaStreamSynchronize(stream));
+    fetch_control(stream);
     if (st_host->action == ACT_DONE || st_host->action == ACT_NONE || st_host->stopped) return;
   }
   throw std::runtime_error("phi host loop did not terminate");

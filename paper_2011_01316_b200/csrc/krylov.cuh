@@ -106,6 +106,7 @@ class Engine {
   size_t upd_used = 0;
   double upd_ms() const;
   bool fused_ok(const OpDevice& op) const;
+  void fetch_control(cudaStream_t s);  // host-stepped loops: action / stopped to st_host
   // Set when the context belongs to a slab-partitioned group: every reducing
   // kernel is followed by a sum-allreduce of PhiState::loc -> PhiState::red,
   // and the control runs host-stepped (no CUDA graphs).
