@@ -34,7 +34,8 @@ extern "C" {
 #define EXPDG_E_DOMAIN 2      /* std::domain_error      (proj/src/euler.cpp:27-28, :210-211)    */
 #define EXPDG_E_KRYLOV 3      /* KrylovError            (proj/include/expdg/phi.hpp:61-66)      */
 #define EXPDG_E_CUDA 4        /* device / runtime failure (no reference analogue)             */
-#define EXPDG_E_UNSUPPORTED 5 /* valid for the reference, not on the device path (e.g. over-integration) */
+#define EXPDG_E_UNSUPPORTED 5 /* valid for the reference, not on the device path (e.g. 3D Roe)       */
+#define EXPDG_E_COMM 6        /* communicator (NCCL / local group) failure of the multi-GPU path  */
 
 /* Operator kinds. */
 #define EXPDG_BURGERS1D 1 /* BurgersOperator (proj/src/burgers.cpp)                         */

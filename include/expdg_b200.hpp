@@ -50,6 +50,7 @@ inline void check(int rc, double estimate = 0.0) {
     case EXPDG_E_DOMAIN: throw std::domain_error(msg);
     case EXPDG_E_KRYLOV: throw KrylovError(msg, estimate);
     case EXPDG_E_UNSUPPORTED: throw std::invalid_argument("unsupported on the device path: " + msg);
+    case EXPDG_E_COMM: throw DeviceError("communicator: " + msg);
     default: throw DeviceError(msg);
   }
 }

@@ -23,7 +23,7 @@ import numpy as np
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "_build", "libexpdg_b200.so")
 
-EXPDG_OK, EXPDG_E_INVALID, EXPDG_E_DOMAIN, EXPDG_E_KRYLOV, EXPDG_E_CUDA, EXPDG_E_UNSUPPORTED = range(6)
+EXPDG_OK, EXPDG_E_INVALID, EXPDG_E_DOMAIN, EXPDG_E_KRYLOV, EXPDG_E_CUDA, EXPDG_E_UNSUPPORTED, EXPDG_E_COMM = range(7)
 BURGERS1D, BURGERS2D, EULER2D, EULER3D, DENSE = 1, 2, 3, 4, 5
 INTEGRATORS = {"exp_euler": 0, "epi2": 1, "exprb32": 2, "exprb42": 3}
 
@@ -42,6 +42,10 @@ class DeviceError(RuntimeError):
 
 class UnsupportedError(ValueError):
     pass
+
+
+class CommError(DeviceError):
+    """A communicator call (NCCL / local group) of the multi-GPU path failed."""
 
 
 class OpDesc(C.Structure):
@@ -166,6 +170,8 @@ def _check(rc, stats: Optional[KrylovStatsC] = None):
         raise KrylovError(msg, stats.last_estimate if stats is not None else 0.0)
     if rc == EXPDG_E_UNSUPPORTED:
         raise UnsupportedError(msg)
+    if rc == EXPDG_E_COMM:
+        raise CommError(msg)
     raise DeviceError(msg)
 
 

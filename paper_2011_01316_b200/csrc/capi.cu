@@ -77,6 +77,9 @@ int guard(F&& f) {
   } catch (const KrylovFailure& e) {
     g_err = e.what();
     return EXPDG_E_KRYLOV;
+  } catch (const CommError& e) {
+    g_err = e.what();
+    return EXPDG_E_COMM;
   } catch (const CudaError& e) {
     g_err = e.what();
     return EXPDG_E_CUDA;

@@ -51,13 +51,13 @@ const NcclApi& nccl() {
     api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
   });
   if (!api.CommInitRank || !api.AllReduce || !api.Send || !api.Recv)
-    throw std::runtime_error("NCCL: libnccl.so.2 not found (needed for the multi-GPU slab path)");
+    throw CommError("NCCL: libnccl.so.2 not found (needed for the multi-GPU slab path)");
   return api;
 }
 
 void ncheck(ncclResult_t r, const char* what) {
   if (r != ncclSuccess)
-    throw CudaError(std::string("NCCL ") + what + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "?"));
+    throw CommError(std::string("NCCL ") + what + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "?"));
 }
 
 class NcclComm : public Comm {

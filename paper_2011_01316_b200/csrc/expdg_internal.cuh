@@ -154,6 +154,10 @@ struct StepRecord {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// a communicator (NCCL / local group) call failed
+struct CommError : CudaError {
+  using CudaError::CudaError;
+};
 
 #define EXPDG_CUDA(call)                                                                  \
   do {                                                                                    \
