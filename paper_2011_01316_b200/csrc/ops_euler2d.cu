@@ -489,7 +489,6 @@ struct E2Strip {
   static constexpr int ROWD = (W + 2) * BLK;  // doubles per array per row (with halo)
   static constexpr int BUFD = 2 * ROWD + W * BLK;  // x + frozen (with halo) + b_1
   static constexpr int NBUF = 4;
-  static constexpr int ROWS_PER_UNIT = 64;
   static constexpr int FX = (W + 1) * NP * 4;   // x-face fluxes of a row
   static constexpr int FY = W * NP * 4;         // y-face fluxes of one face row
   // ring + double-buffered volume fluxes and x-face fluxes + a 3-deep ring of y-face rows,
@@ -544,8 +543,10 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
   const double xs = s_xs, dt = s_dt;
   const int nx = P.nx, ny = P.ny;
   const int nstrips = (nx + W - 1) / W;
-  const int nchunks = (ny + S::ROWS_PER_UNIT - 1) / S::ROWS_PER_UNIT;
-  const int nunits = nstrips * nchunks;
+  // each CTA owns one contiguous range of the (strip, row) row-steps: equal work per CTA,
+  // one or two segments (a new segment restarts the ring with its lower halo row)
+  const long long rsteps = (long long)nstrips * ny;
+  const long long k0 = rsteps * blockIdx.x / gridDim.x, k1 = rsteps * (blockIdx.x + 1) / gridDim.x;
   // p == 1 (EPI2, exp_euler): the single aug vector b_1 rides in the TMA ring too
   const double* b1 = (b.p == 1) ? b.b[1] : nullptr;
   double nacc = 0.0;
@@ -554,10 +555,11 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
     // ---------------- producer
     if (lane == 0) {
       long long seq = 0;
-      for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        const int strip = u % nstrips, chunk = u / nstrips;
+      for (long long k = k0; k < k1;) {
+        const int strip = (int)(k / ny), r0 = (int)(k - (long long)strip * ny);
+        const int r1 = (int)min((long long)ny, r0 + (k1 - k));
+        k += r1 - r0;
         const int ie0 = strip * W, w = min(W, nx - ie0);
-        const int r0 = chunk * S::ROWS_PER_UNIT, r1 = min(ny, r0 + S::ROWS_PER_UNIT);
         for (int q = 0; q < r1 - r0 + 2; ++q) {
           int row = r0 - 1 + q;
           const double* srcx = x;
@@ -611,10 +613,11 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
     const double wi = s_wq[i], wj = s_wq[j];
     const double iwij = 1.0 / (wi * wj);
     long long seq = 0;
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-      const int strip = u % nstrips, chunk = u / nstrips;
+    for (long long k = k0; k < k1;) {
+      const int strip = (int)(k / ny), r0 = (int)(k - (long long)strip * ny);
+      const int r1 = (int)min((long long)ny, r0 + (k1 - k));
+      k += r1 - r0;
       const int ie0 = strip * W, w = min(W, nx - ie0);
-      const int r0 = chunk * S::ROWS_PER_UNIT, r1 = min(ny, r0 + S::ROWS_PER_UNIT);
       const bool active = le < w;
       const int ie = ie0 + le;
       const double hx = active ? __ldg(P.hx + ie) : 1.0;
@@ -797,8 +800,8 @@ class Euler2D : public OpDevice {
     int per_sm = 1;
     EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_e2_phi_strip<NP, false, CW>, 32 * CW + 32,
                                                              SS::SMEM));
-    const int units = ((P.nx + SS::W - 1) / SS::W) * ((P.ny + SS::ROWS_PER_UNIT - 1) / SS::ROWS_PER_UNIT);
-    const int g = std::max(1, std::min(units, 148 * std::max(1, per_sm)));
+    const long long rows = (long long)((P.nx + SS::W - 1) / SS::W) * P.ny;
+    const int g = (int)std::max<long long>(1, std::min<long long>(rows, 148LL * std::max(1, per_sm)));
     if (roe) k_e2_phi_strip<NP, true, CW><<<g, 32 * CW + 32, SS::SMEM, s>>>(p, st, base, partials, b);
     else k_e2_phi_strip<NP, false, CW><<<g, 32 * CW + 32, SS::SMEM, s>>>(p, st, base, partials, b);
   }
