@@ -144,18 +144,24 @@ def roofline(dominant, step_achieved, peak, peak_kind, traffic, steps):
     ach = dominant["bytes"] / (dominant["ms"] * 1e-3) / 1e9
     traffic_launch, ncu = None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_dominant.json")) as f:
+        with open(os.path.join(ROOT, "profiles", dominant["ncu_file"])) as f:
             ncu = json.load(f)
         traffic_launch = ncu["dram_over_alg"] * per_launch_bytes
     except Exception:
         pass
-    return {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-            "traffic": traffic_launch,
-            "kernel": "k_ts2<TS2_UPD> (DCGS2 update pass: reads V_0..V_{j-1}, u, w; writes u, w)",
-            "alg_bytes_per_launch": per_launch_bytes, "launch_ms": dominant["ms"] / dominant["launches"],
-            "launches": dominant["launches"], "peak_kind": peak_kind,
-            "traffic_source": (ncu or {}).get("source"),
-            "step": step}
+    out = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+           "traffic": traffic_launch, "kernel": dominant["kernel"],
+           "alg_bytes_per_launch": per_launch_bytes, "launch_ms": dominant["ms"] / dominant["launches"],
+           "launches": dominant["launches"], "peak_kind": peak_kind,
+           "traffic_source": (ncu or {}).get("source"),
+           "step": step}
+    if dominant.get("other"):
+        o = dominant["other"]
+        out["next_kernel"] = {"kernel": o["kernel"], "achieved": o["bytes"] / (o["ms"] * 1e-3) / 1e9,
+                              "launch_ms": o["ms"] / o["launches"], "launches": o["launches"],
+                              "share_ms": o["ms"]}
+        out["share_ms"] = dominant["ms"]
+    return out
 
 
 def run_reference(args, workload):
@@ -285,14 +291,29 @@ def main():
     traffic = ctx.traffic()
     dominant = None
     if not args.no_dominant:
-        # the dominant kernel (DCGS2 update pass, ~42 % of the step): CUDA events around each of
-        # its launches on the context stream over one host-stepped step of the same trajectory
-        ud = u.clone()
-        ctx.time_dominant(True)
-        pkg.integrate(ctx, op, ud, "epi2", dt, dt, **{**kw, "use_graph": False})
-        dominant = ctx.dominant_stats()
-        ctx.time_dominant(False)
-        del ud
+        # the dominant kernel: CUDA events around each launch of the two largest kernels (the
+        # DCGS2 update pass; the operator sweep, which at C4 also takes the DCGS2 dots) on the
+        # context stream over one host-stepped step of the same trajectory; the one with the
+        # larger summed time is reported (its algorithmic bytes are accumulated on the device)
+        timed = []
+        for kind, name, ncu_file in (
+                (1, "k_ts2<TS2_UPD> (DCGS2 update pass: reads V_0..V_{j-1}, u, w; writes u, w)",
+                 "r01_ncu_dominant.json"),
+                (2, "k_e2_phi_strip<5,LF,8,DOT> (Euler strip JVP + DCGS2 pass-1 dots: reads x, q~, b_1, "
+                    "V_0..V_{j-1}; writes y)", "r01_ncu_dominant_fused.json")):
+            ud = u.clone()
+            ctx.time_dominant(kind)
+            pkg.integrate(ctx, op, ud, "epi2", dt, dt, **{**kw, "use_graph": False})
+            d = ctx.dominant_stats()
+            ctx.time_dominant(False)
+            del ud
+            if d["launches"] > 0 and d["bytes"] > 0:
+                timed.append({**d, "kernel": name, "ncu_file": ncu_file})
+        if timed:
+            timed.sort(key=lambda d: -d["ms"])
+            dominant = timed[0]
+            if len(timed) > 1:
+                dominant["other"] = timed[1]
     if r.status != "completed" or r.steps != args.steps:
         raise RuntimeError(f"timed run: {r.status} after {r.steps} steps")
     loop_s = r.loop_ms / 1e3

@@ -214,6 +214,11 @@ int expdg_debug_state(expdg_ctx* ctx, double* out16);
 /* Micro-benchmark of one CGS2 streaming pass (mode 0 dots, 1 update+dots,
  * 2 update+norm, 3 combine) against k basis vectors of length n; avg ms. */
 int expdg_bench_ts(expdg_ctx* ctx, long long n, int k, int mode, int reps, double* ms);
+/* Micro-benchmark of one phi-cycle operator application at column j (mode 0; the
+ * operator kernel also takes the DCGS2 pass-1 dots where it does so in the engine) or
+ * of the separate DCGS2 dots pass at column j (mode 1) on the current Krylov slots;
+ * the operator must be linearized; avg ms (diagnostics). */
+int expdg_bench_apply(expdg_ctx* ctx, expdg_op* op, int j, int mode, int reps, double* ms);
 /* Hessenberg matrix of the last phi call, (129 x 128) row-major (diagnostics). */
 int expdg_debug_hessenberg(expdg_ctx* ctx, double* out);
 
@@ -230,9 +235,11 @@ double expdg_ctx_last_loop_ms(expdg_ctx* ctx);
  * accepted substeps: out4 = {bytes, columns, avnorms, combines}. */
 /* Roofline of the dominant kernel (the DCGS2 update pass): with enable = 1 the next
  * host-stepped runs (expdg_time_cfg.use_graph = 0) record CUDA events around every
- * update-pass launch on the context stream.  out3 = {summed launch ms, summed
- * algorithmic bytes 8 n (j + 4), launches that extended a column}. */
-int expdg_ctx_time_dominant(expdg_ctx* ctx, int enable);
+ * DCGS2 update-pass launch (enable 1) or every phi-cycle operator application
+ * (enable 2) on the context stream.  out3 = {summed launch ms, summed algorithmic bytes
+ * (update pass 8 n (j + 4); Euler 2D strip sweep 32 n + 8 n j with fused dots),
+ * launches that extended a column}. */
+int expdg_ctx_time_dominant(expdg_ctx* ctx, int enable /* 0 off, 1 DCGS2 update pass, 2 operator sweep */);
 int expdg_ctx_dominant_stats(expdg_ctx* ctx, double* out3);
 /* Fused small-problem engine: SM clock cycles spent per phase in the last run
  * (apply, dots, updates, combine, controller; 0 for the multi-kernel engine). */

@@ -85,7 +85,7 @@ EXPORTS = [
     "expdg_op_apply_linear", "expdg_op_apply_nonlinear", "expdg_op_full_rhs", "expdg_phi_combination",
     "expdg_step_epi2", "expdg_integrate", "expdg_integrate_host", "expdg_lgl_basis",
     "expdg_initial_condition", "expdg_ctx_kernel_launches", "expdg_ctx_last_loop_ms", "expdg_expm",
-    "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts", "expdg_op_set_source",
+    "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts", "expdg_bench_apply", "expdg_op_set_source",
     "expdg_op_set_source_fn", "expdg_nccl_unique_id", "expdg_ctx_attach_nccl", "expdg_local_group_create",
     "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
     "expdg_debug_profile", "expdg_ctx_set_fused", "expdg_ctx_time_dominant", "expdg_ctx_dominant_stats",
@@ -142,6 +142,7 @@ def lib():
     L.expdg_debug_hessenberg.argtypes = [vp, dp]
     L.expdg_ctx_traffic.argtypes = [vp, dp]
     L.expdg_bench_ts.argtypes = [vp, C.c_longlong, C.c_int, C.c_int, C.c_int, dp]
+    L.expdg_bench_apply.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, dp]
     L.expdg_initial_condition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, dp]
     L.expdg_nccl_unique_id.argtypes = [C.c_char_p]
     L.expdg_ctx_attach_nccl.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
@@ -264,15 +265,23 @@ class Context:
         _check(lib().expdg_ctx_traffic(self.h, _np_ptr(v)))
         return {"alg_bytes": v[0], "columns": int(v[1]), "avnorms": int(v[2]), "combines": int(v[3])}
 
+    def bench_apply(self, op: "Operator", j: int, mode: int = 0, reps: int = 5) -> float:
+        """avg ms of one phi-cycle operator application at column j (mode 0, with the DCGS2
+        dots where the operator kernel takes them) or of the DCGS2 dots pass (mode 1)."""
+        ms = C.c_double()
+        _check(lib().expdg_bench_apply(self.h, op.h, j, mode, reps, C.byref(ms)))
+        return ms.value
+
     def bench_ts(self, n: int, k: int, mode: int, reps: int = 5) -> float:
         """avg ms of one CGS2 streaming pass (0 dots, 1 update+dots, 2 update+norm, 3 combine)."""
         ms = C.c_double()
         _check(lib().expdg_bench_ts(self.h, n, k, mode, reps, C.byref(ms)))
         return ms.value
 
-    def time_dominant(self, enable: bool = True):
-        """CUDA events around every DCGS2 update pass of the next host-stepped runs."""
-        _check(lib().expdg_ctx_time_dominant(self.h, 1 if enable else 0))
+    def time_dominant(self, enable=True):
+        """CUDA events around every DCGS2 update pass (enable True / 1) or every phi-cycle
+        operator application (2) of the next host-stepped runs; False / 0: off."""
+        _check(lib().expdg_ctx_time_dominant(self.h, int(enable)))
 
     def dominant_stats(self) -> dict:
         v = np.zeros(3)

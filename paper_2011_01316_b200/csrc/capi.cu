@@ -385,7 +385,7 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
     e.run_phi(*op->dev, b, use_graph_default() ? 1 : 0);
     EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
     const PhiState& s = *e.st_host;
-    ctx->launches += 2 + s.body_runs * (op->dev->fused_dots() ? 5 : 6);
+    ctx->launches += 2 + s.body_runs * Engine::body_kernels(*op->dev, s.dcgs != 0, s.mmax);
     if (stats) {
       stats->iterations = s.iterations;
       stats->substeps = s.substeps;
@@ -566,7 +566,8 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   (void)vgrid;
   const bool fused = e.fused_ok(dev);
   const int per_step = (exprb ? 13 : 5) + (e.comm ? 1 : 0) + (fused ? (exprb ? 2 : 1) : 0);
-  const int body_k = (dev.fused_dots() ? 5 : 6) + (dev.partitioned() ? 1 : 0);  // + halo pack kernel
+  const int body_k = Engine::body_kernels(dev, c1.dcgs != 0, exprb ? std::max(c1.mmax, c3.mmax) : c1.mmax) +
+                     (dev.partitioned() ? 1 : 0);  // + halo pack kernel
   cudaGraphExec_t ex = nullptr;
   const bool graph = cfg->use_graph != 0 && !e.comm;  // partitioned: host-stepped control
   int launched = 0;
@@ -589,9 +590,9 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     EXPDG_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
     return cp.conditional.phGraph_out[0];
   };
-  auto host_loop = [&](const BArgs& b, bool dcgs) {
+  auto host_loop = [&](const BArgs& b, bool dcgs, int mmax) {
     for (long long cyc = 0;; ++cyc) {
-      e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0, dcgs);
+      e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0, dcgs, mmax);
       e.fetch_control(e.stream);  // action + stopped only (8 bytes, not the whole PhiState)
       if (e.st_host->action == ACT_DONE || e.st_host->action == ACT_NONE || e.st_host->stopped) break;
       if (cyc > 10000000) throw CudaError("host-stepped phi did not terminate");
@@ -623,11 +624,11 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
         post(cs);
         EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
         EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body1, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        e.launch_body(cs, dev, b1, h1, 1, c1.dcgs != 0);
+        e.launch_body(cs, dev, b1, h1, 1, c1.dcgs != 0, c1.mmax);
         EXPDG_CUDA(cudaStreamEndCapture(cs, &body1));
         if (exprb) {
           EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body2, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-          e.launch_body(cs, dev, b2, h2, 1, c3.dcgs != 0);
+          e.launch_body(cs, dev, b2, h2, 1, c3.dcgs != 0, c3.mmax);
           EXPDG_CUDA(cudaStreamEndCapture(cs, &body2));
         }
       }
@@ -652,11 +653,11 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
         } else {
           pre(e.stream);
           if (fused) dev.launch_fused(e.stream, e, b1);
-          else host_loop(b1, c1.dcgs != 0);
+          else host_loop(b1, c1.dcgs != 0, c1.mmax);
           if (exprb) {
             mid(e.stream);
             if (fused) dev.launch_fused(e.stream, e, b2);
-            else host_loop(b2, c3.dcgs != 0);
+            else host_loop(b2, c3.dcgs != 0, c3.mmax);
           }
           post(e.stream);
         }
@@ -770,10 +771,11 @@ int expdg_debug_state(expdg_ctx* ctx, double* out16) {
 int expdg_ctx_time_dominant(expdg_ctx* ctx, int enable) {
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null argument");
-    ctx->eng->time_upd = enable != 0;
+    if (enable < 0 || enable > 2) throw std::invalid_argument("time_dominant: 0 off, 1 update pass, 2 apply");
+    ctx->eng->time_kind = enable;
     ctx->eng->upd_used = 0;
     EXPDG_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(ctx->eng->st) + offsetof(PhiState, upd_bytes), 0,
-                               sizeof(double) + sizeof(long long), ctx->eng->stream));
+                               2 * (sizeof(double) + sizeof(long long)), ctx->eng->stream));
     EXPDG_CUDA(cudaStreamSynchronize(ctx->eng->stream));
   });
 }
@@ -784,8 +786,9 @@ int expdg_ctx_dominant_stats(expdg_ctx* ctx, double* out3) {
     Engine& e = *ctx->eng;
     EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
     out3[0] = e.upd_ms();
-    out3[1] = e.st_host->upd_bytes;
-    out3[2] = (double)e.st_host->upd_launches;
+    const bool app = e.time_kind == 2;
+    out3[1] = app ? e.st_host->app_bytes : e.st_host->upd_bytes;
+    out3[2] = (double)(app ? e.st_host->app_launches : e.st_host->upd_launches);
   });
 }
 
@@ -813,6 +816,49 @@ int expdg_bench_ts(expdg_ctx* ctx, long long n, int k, int mode, int reps, doubl
   return guard([&] {
     if (k < 1 || k > kMaxBasis) throw std::invalid_argument("bench_ts: 1 <= k <= 128");
     *ms = ctx->eng->bench_ts(n, k, mode, reps);
+  });
+}
+
+// Times one phi-cycle operator application at column j (mode 0; with the DCGS2 dots
+// when the operator takes them) or the separate DCGS2 dots pass at column j (mode 1),
+// on the current slots; diagnostics for the fused sweep.  The operator must be linearized.
+int expdg_bench_apply(expdg_ctx* ctx, expdg_op* op, int j, int mode, int reps, double* ms) {
+  return guard([&] {
+    if (j < 0 || j >= kMaxBasis) throw std::invalid_argument("bench_apply: 0 <= j < 128");
+    if (!op->dev->ref) throw std::invalid_argument("operator not linearized (call expdg_op_linearize)");
+    Engine& e = *ctx->eng;
+    const long long n = op->dev->n;
+    e.ensure(n + 1, j + 2);
+    e.ensure_scratch(n + 1, 1);
+    EXPDG_CUDA(cudaMemsetAsync(e.scratch, 0, sizeof(double) * (n + 1), e.stream));
+    PhiState c = e.config(n, 1, 1e-3, expdg_krylov_cfg{1e-10, std::max(j + 1, 1), std::max(j + 1, 1), 0, 0});
+    c.dcgs = 1;
+    c.action = ACT_EXTEND;
+    c.j = j;
+    c.mc = j + 1;
+    for (int i = 0; i < kMaxSlots; ++i) c.scale[i] = 1.0;
+    e.upload_config(c, e.stream);
+    BArgs b{};
+    b.p = 1;
+    b.b[1] = e.scratch;
+    auto one = [&] {
+      if (mode == 0) op->dev->launch_phi_apply(e.stream, e.st, e.base, e.partials, b);
+      else launch_dcgs(e.stream, e, 0, -1);
+    };
+    one();  // warm-up
+    cudaEvent_t a, z;
+    EXPDG_CUDA(cudaEventCreate(&a));
+    EXPDG_CUDA(cudaEventCreate(&z));
+    EXPDG_CUDA(cudaEventRecord(a, e.stream));
+    for (int r = 0; r < reps; ++r) one();
+    EXPDG_CUDA(cudaEventRecord(z, e.stream));
+    EXPDG_CUDA(cudaEventSynchronize(z));
+    float t = 0.f;
+    EXPDG_CUDA(cudaEventElapsedTime(&t, a, z));
+    cudaEventDestroy(a);
+    cudaEventDestroy(z);
+    EXPDG_CUDA(cudaGetLastError());
+    *ms = t / reps;
   });
 }
 

@@ -206,7 +206,9 @@ __device__ __forceinline__ void set_window(PhiState* st, int j) {
 static __device__ int dcgs_finish(PhiState* st) {
   const int j = st->j;
   const double nd = (double)st->n;
-  st->alg_bytes += 32.0 * nd + 8.0 * nd * (2.0 * j + 6.0);
+  // JVP 32n + dots pass 8n(j + 2) + update pass 8n(j + 4); with the dots in the JVP sweep
+  // (dots_fused) u and w are not re-read: 32n + 8n j + 8n(j + 4)
+  st->alg_bytes += 32.0 * nd + 8.0 * nd * (2.0 * j + (st->dots_fused ? 4.0 : 6.0));
   double beta = 1.0;
   if (j >= 1) {
     beta = st->scale[j] * sqrt(st->red.nrmU);

@@ -143,7 +143,7 @@ __device__ __forceinline__ void ts2_consume(double* base, double* smem, uint64_t
 
 template <int MODE>
 __global__ void __launch_bounds__(kT2Block, 1) k_ts2(PhiState* st, double* base, double* partials, int budget,
-                                                     int max_stages, int min_T) {
+                                                     int max_stages, int min_T, int fused_jmax) {
   extern __shared__ __align__(128) double smem[];
   __shared__ uint64_t full[8], empty[8];
   __shared__ int s_active, s_j, s_T, s_S;
@@ -157,7 +157,9 @@ __global__ void __launch_bounds__(kT2Block, 1) k_ts2(PhiState* st, double* base,
   const int lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
     const int a = st->action;
-    const int active = !st->stopped && st->dcgs && (a == ACT_EXTEND || a == ACT_AVNORM);
+    int active = !st->stopped && st->dcgs && (a == ACT_EXTEND || a == ACT_AVNORM);
+    // the operator kernel already took the dots of this column (fused_dcgs_dots_jmax)
+    if (MODE == TS2_DOTS && active && st->j <= fused_jmax) active = 0;
     const int j = active ? st->j : 0;
     const int nst = j + 2;
     int T = kT2MaxT;
@@ -315,12 +317,13 @@ __global__ void __launch_bounds__(128) k_dcgs_coef(PhiState* st) {
   }
 }
 
-void launch_dcgs(cudaStream_t s, Engine& e, int which) {
+void launch_dcgs(cudaStream_t s, Engine& e, int which, int fused_jmax) {
   const int g = std::max(1, e.num_sms);
   const TsTuning& t = e.ts_tuning;
-  if (which == 0) k_ts2<TS2_DOTS><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T);
+  if (which == 0)
+    k_ts2<TS2_DOTS><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T, fused_jmax);
   else if (which == 1) k_dcgs_coef<<<1, 128, 0, s>>>(e.st);
-  else k_ts2<TS2_UPD><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T);
+  else k_ts2<TS2_UPD><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T, -1);
 }
 
 void dcgs_init_attrs(int maxsm) {

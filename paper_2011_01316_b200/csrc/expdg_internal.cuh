@@ -103,6 +103,7 @@ struct PhiState {
   // (projected once, scale[j] provisional); the JVP runs on it and the second
   // projection of u_j rides in the same two passes as the first projection of A u_j.
   int dcgs;        // 1: DCGS2 (full orthogonalisation only), 0: CGS2 / IOP passes
+  int dots_fused;  // the operator kernel of this cycle also took the DCGS2 pass-1 dots
   int dc_pending;  // the AVNORM cycle already extended column mc provisionally
   double dc_gam;   // slot-space coefficient of the old candidate in the w update
   double dc_c, dc_d, dc_ab;  // <u,u>, <u,w>, a.b (true, scaled)
@@ -135,6 +136,8 @@ struct PhiState {
   long long prof[8];  // fused engine: SM clock cycles per phase (apply, dots, update, combine, ctl)
   double upd_bytes;   // algorithmic bytes of the DCGS2 update passes that ran (8 n (j + 4) each)
   long long upd_launches;
+  double app_bytes;   // the same for the Euler 2D strip sweep: 32 n (JVP) + 8 n j (fused dots)
+  long long app_launches;
   // ---- Hessenberg (mmax+1) x mmax, row stride kMaxBasis; last, so the controller
   // copies the scalar state plus only the rows in use
   alignas(16) double H[(kMaxBasis + 1) * kMaxBasis];
@@ -274,6 +277,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t cnt) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(cnt) : "memory");
 }
 
 __host__ __device__ inline long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }

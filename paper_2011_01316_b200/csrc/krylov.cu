@@ -26,7 +26,6 @@
 
 namespace expdg {
 
-void launch_dcgs(cudaStream_t s, Engine& e, int which);
 void dcgs_init_attrs(int maxsm);
 
 enum TsMode { TS_DOTS = 0, TS_UPD_DOTS = 1, TS_UPD_NORM = 2, TS_COMBINE = 3 };
@@ -515,28 +514,39 @@ void Engine::launch_ts(cudaStream_t s, int mode) {
   }
 }
 
+int Engine::body_kernels(const OpDevice& op, bool dcgs, int mmax) {
+  if (dcgs) return (mmax >= 0 && op.fused_dcgs_dots_jmax() >= mmax) ? 5 : 6;
+  return op.fused_dots() ? 5 : 6;
+}
+
 void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
-                         int use_graph, bool dcgs) {
-  op.launch_phi_apply(s, st, base, partials, b);
+                         int use_graph, bool dcgs, int mmax) {
+  auto timed = [&](int kind, auto&& launch) {
+    if (time_kind != kind || use_graph) {
+      launch();
+      return;
+    }
+    if (upd_used + 2 > upd_events.size())
+      for (int q = 0; q < 64; ++q) {
+        cudaEvent_t ev;
+        EXPDG_CUDA(cudaEventCreate(&ev));
+        upd_events.push_back(ev);
+      }
+    EXPDG_CUDA(cudaEventRecord(upd_events[upd_used], s));
+    launch();
+    EXPDG_CUDA(cudaEventRecord(upd_events[upd_used + 1], s));
+    upd_used += 2;
+  };
+  timed(2, [&] { op.launch_phi_apply(s, st, base, partials, b); });
   reduce(s);
   if (dcgs) {  // one dots pass + coefficients + one update pass (dcgs.cu)
-    launch_dcgs(s, *this, 0);
-    reduce(s);
-    launch_dcgs(s, *this, 1);
-    if (time_upd && !use_graph) {
-      if (upd_used + 2 > upd_events.size())
-        for (int q = 0; q < 64; ++q) {
-          cudaEvent_t ev;
-          EXPDG_CUDA(cudaEventCreate(&ev));
-          upd_events.push_back(ev);
-        }
-      EXPDG_CUDA(cudaEventRecord(upd_events[upd_used], s));
-      launch_dcgs(s, *this, 2);
-      EXPDG_CUDA(cudaEventRecord(upd_events[upd_used + 1], s));
-      upd_used += 2;
-    } else {
-      launch_dcgs(s, *this, 2);
+    const int fj = op.fused_dcgs_dots_jmax();
+    if (!(mmax >= 0 && fj >= mmax)) {  // some column's dots are not taken by the operator kernel
+      launch_dcgs(s, *this, 0, fj);
+      reduce(s);
     }
+    launch_dcgs(s, *this, 1);
+    timed(1, [&] { launch_dcgs(s, *this, 2); });
     reduce(s);
     launch_ts(s, TS_COMBINE);
     reduce(s);
@@ -595,8 +605,8 @@ double Engine::bench_ts(long long n, int k, int mode, int reps) {
   return ms / reps;
 }
 
-// Sum of the timed DCGS2 update-pass launches (events recorded by launch_body).  A
-// no-op launch (no extension this cycle) contributes its few microseconds too.
+// Sum of the timed launches (events recorded by launch_body).  A no-op launch (no
+// extension this cycle) contributes its few microseconds too.
 double Engine::upd_ms() const {
   double tot = 0.0;
   for (size_t q = 0; q + 1 < upd_used; q += 2) {
@@ -633,7 +643,7 @@ void Engine::run_phi(OpDevice& op, const BArgs& b, int use_graph) {
   }
   launch_phi_init(stream, b);
   for (int cyc = 0; cyc < 1000000; ++cyc) {
-    launch_body(stream, op, b, cudaGraphConditionalHandle{}, 0, st_host->dcgs != 0);
+    launch_body(stream, op, b, cudaGraphConditionalHandle{}, 0, st_host->dcgs != 0, st_host->mmax);
     fetch_control(stream);
     if (st_host->action == ACT_DONE || st_host->action == ACT_NONE || st_host->stopped) return;
   }
@@ -666,7 +676,7 @@ cudaGraphExec_t Engine::build_phi_graph(OpDevice& op, const BArgs& b) {
   EXPDG_CUDA(cudaStreamEndCapture(cs, &g));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   EXPDG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  launch_body(cs, op, b, h, 1, st_host->dcgs != 0);
+  launch_body(cs, op, b, h, 1, st_host->dcgs != 0, st_host->mmax);
   EXPDG_CUDA(cudaStreamEndCapture(cs, &body));
   cudaGraphExec_t ex;
   EXPDG_CUDA(cudaGraphInstantiate(&ex, g, 0));

@@ -52,6 +52,9 @@ class OpDevice {
                                double* partials) = 0;
   // Whether the apply kernel also writes pass-A dots (else the generic kernel runs).
   virtual bool fused_dots() const { return false; }
+  // DCGS2: the apply kernel also takes the pass-1 dots (k_ts2<TS2_DOTS>) of columns
+  // j <= this bound (-1: never); k_ts2<TS2_DOTS> no-ops for those columns.
+  virtual int fused_dcgs_dots_jmax() const { return -1; }
   // Small problems: the whole phi call as one single-CTA kernel (fused.cuh)
   virtual bool fused_capable() const { return false; }
   virtual void launch_fused(cudaStream_t, Engine&, const BArgs&) {}
@@ -99,9 +102,10 @@ class Engine {
   int ld_odd = 1;
   int use_dcgs = 1;  // 0 CGS2, 1 auto (DCGS2 from 2^18 DOF), 2 DCGS2 (EXPDG_ORTH=cgs2|dcgs2)
   int use_fused = 1;  // small problems run each phi call as one fused kernel (EXPDG_FUSED=0: off)
-  // host-stepped runs: CUDA events around every DCGS2 update pass (the dominant kernel),
-  // so bench.py can report its live per-launch bandwidth
-  bool time_upd = false;
+  // host-stepped runs: CUDA events around every DCGS2 update pass (time_kind 1) or every
+  // phi-cycle operator application (2), so bench.py can report the live per-launch
+  // bandwidth of the dominant kernel
+  int time_kind = 0;
   std::vector<cudaEvent_t> upd_events;
   size_t upd_used = 0;
   double upd_ms() const;
@@ -144,13 +148,21 @@ class Engine {
   void launch_phi_init(cudaStream_t s, const BArgs& b);
   void launch_ts(cudaStream_t s, int mode);
   double bench_ts(long long n, int k, int mode, int reps);
+  // mmax: the phi call's basis bound (decides whether the DCGS2 dots pass can be left
+  // out entirely because the operator kernel takes the dots of every column)
   void launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
-                   int use_graph, bool dcgs);
+                   int use_graph, bool dcgs, int mmax);
+  // kernels one launch_body enqueues
+  static int body_kernels(const OpDevice& op, bool dcgs, int mmax);
   // Runs one phi call to completion; host-stepped or graph-driven control.
   void run_phi(OpDevice& op, const BArgs& b, int use_graph);
   // Builds a while-node graph around launch_body; caller owns the exec.
   cudaGraphExec_t build_phi_graph(OpDevice& op, const BArgs& b);
 };
+
+// DCGS2 kernels (dcgs.cu): which 0 dots pass (no-op for columns j <= fused_jmax), 1 coefficients,
+// 2 update pass.
+void launch_dcgs(cudaStream_t s, Engine& e, int which, int fused_jmax = -1);
 
 // Halo send buffers <- first / last element layer of the slot the next phi-cycle apply
 // reads (slab-partitioned operators).

@@ -39,6 +39,7 @@ struct E2P {
   const double* gx_hi;
   const double* gt_lo;
   const double* gt_hi;
+  int dbg;  // EXPDG_E2_DBG (diagnostics): bit 0 = the DOT sweep's dot warps skip their arithmetic
 };
 
 struct Prim {
@@ -476,11 +477,23 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
 
 // ---------------------------------------------------------------- 2.5D strip JVP (phi cycle)
 // A CTA owns a strip of W element columns and marches up a chunk of element
-// rows.  Warp 8 streams whole element rows (x = slot j and the frozen
+// rows.  Warp CW streams whole element rows (x = slot j and the frozen
 // primitives, each with its E/W halo element) by 1D TMA bulk copies into a
-// 4-row smem ring (full/empty mbarriers); warps 0-7 compute row r from the
+// 4-row smem ring (full/empty mbarriers); warps 0..CW-1 compute row r from the
 // ring rows r-1, r, r+1, so every byte of x and q~ comes from HBM once per JVP.
-template <int NP, int CW>
+//
+// DOT = true also takes the DCGS2 pass-1 dots of the cycle (dcgs.cu,
+// k_ts2<TS2_DOTS>: a_i = <V_i,u>, b_i = <V_i,w>, <u,u>, <u,w> with u = slot j,
+// w = the JVP result) in the same sweep: warp CW+1 streams the row tiles of
+// V_0..V_{j-1} into a VS-stage ring and two dot warps (one per tile half) consume
+// them against u (the centre of the x ring row) and w (the row just computed,
+// handed over through a double-buffered smem row).  u and w are never re-read
+// from HBM, and the JVP arithmetic runs under the V stream instead of before it.
+// The V ring takes what shared memory the JVP leaves (single-buffered volume
+// fluxes in this variant, one more CTA barrier per row).
+constexpr int kE2DotJ = 44;  // the sweep takes the dots of columns j < 44 (max_basis <= 43 skips k_ts2 dots)
+
+template <int NP, int CW, bool DOT>
 struct E2Strip {
   static constexpr int NN = NP * NP;
   static constexpr int CONS = 32 * CW;        // consumer threads (CW warps) + one producer warp
@@ -491,37 +504,258 @@ struct E2Strip {
   static constexpr int NBUF = 4;
   static constexpr int FX = (W + 1) * NP * 4;   // x-face fluxes of a row
   static constexpr int FY = W * NP * 4;         // y-face fluxes of one face row
-  // ring + double-buffered volume fluxes and x-face fluxes + a 3-deep ring of y-face rows,
-  // so consecutive rows need one CTA barrier between them instead of two
-  static constexpr int SMEM = (NBUF * BUFD + 2 * (2 * W * BLK) + 2 * FX + 3 * FY) * 8;
+  static constexpr int TILE = W * BLK;          // doubles of one row of one vector
+  static constexpr int ND = DOT ? 2 : 0;        // dot warps, one per tile half (12 warps: <= 168 registers)
+  static constexpr int JMAX = DOT ? kE2DotJ - 1 : -1;
+  static constexpr int SFB = DOT ? 1 : 2;       // volume-flux buffers (DOT: single, one more barrier per row)
+  static constexpr int THREADS = CONS + 32 + (DOT ? 32 + 32 * ND : 0);
+  // ring + volume fluxes (double-buffered without DOT) and double-buffered x-face fluxes +
+  // a 3-deep ring of y-face rows, so consecutive rows need one CTA barrier between them
+  static constexpr int BASE = NBUF * BUFD + SFB * (2 * W * BLK) + 2 * FX + 3 * FY;
+  // DOT: two w rows + a V ring of as many row tiles (<= 12) as the 227 KB opt-in
+  // shared memory leaves next to ~3 KB of static shared memory
+  static constexpr int SMAX = 232448 / 8 - 384;
+  static constexpr int VSF = (SMAX - BASE - 2 * TILE) / TILE;
+  static constexpr int VS = DOT ? (VSF > 12 ? 12 : (VSF < 1 ? 1 : VSF)) : 1;
+  static constexpr bool FITS = !DOT || VSF >= 4;
+  static constexpr int SMEM = (BASE + (DOT ? 2 * TILE + VS * TILE : 0)) * 8;
 };
 
 template <int CONS>
 __device__ __forceinline__ void strip_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONS) : "memory"); }
 
-template <int NP, bool ROE, int CW>
-__global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
+// The (strip, row) row-steps of a CTA: one contiguous range [k0, k1) of the
+// strip-major row-step order, walked as units of consecutive rows of one strip.
+struct StripUnit {
+  int ie0, w, r0, r1;
+};
+template <int W>
+__device__ __forceinline__ StripUnit strip_unit(long long& k, long long k1, int nx, int ny) {
+  StripUnit u;
+  const int strip = (int)(k / ny);
+  u.r0 = (int)(k - (long long)strip * ny);
+  u.r1 = (int)min((long long)ny, u.r0 + (k1 - k));
+  k += u.r1 - u.r0;
+  u.ie0 = strip * W;
+  u.w = min(W, nx - u.ie0);
+  return u;
+}
+
+// Dot warps of the DOT sweep.  The two dot warps split every row tile by 32-double2
+// blocks (warp h takes the double2 elements 64 m + 32 h + lane, conflict-free and
+// with immediate smem offsets).  The V_i tiles are consumed in quads (then a pair, a single), the
+// four per-lane sums of a pair reduced across the warp by one butterfly (6 64-bit
+// shuffles) and accumulated in shared memory, s_acc[h][2 i + {0: <V_i,u>, 1: <V_i,w>}]
+// (i = j: the candidate u itself).
+__device__ __forceinline__ void dots_bfly_add(double* acc, int lane, int ia, int ib, double xa, double ya,
+                                              double xb, double yb) {
+  // lanes [0,8) <V_ia,u>, [8,16) <V_ia,w>, [16,24) <V_ib,u>, [24,32) <V_ib,w>
+  const bool b4 = lane & 16, b3 = lane & 8;
+  const double a0 = (b4 ? xb : xa) + __shfl_xor_sync(0xffffffffu, b4 ? xa : xb, 16);
+  const double a1 = (b4 ? yb : ya) + __shfl_xor_sync(0xffffffffu, b4 ? ya : yb, 16);
+  double t = (b3 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, b3 ? a0 : a1, 8);
+  t += __shfl_xor_sync(0xffffffffu, t, 4);
+  t += __shfl_xor_sync(0xffffffffu, t, 2);
+  t += __shfl_xor_sync(0xffffffffu, t, 1);
+  if ((lane & 7) == 0) {
+    const int which = lane >> 3;
+    const int i = which < 2 ? ia : ib;
+    if (i >= 0) acc[2 * i + (which & 1)] += t;
+  }
+}
+
+// Position in an mbarrier ring: stage index and the parity of its current phase.
+struct RingPos {
+  int s = 0;
+  uint32_t ph = 0;
+  template <int N>
+  __device__ __forceinline__ void next() {
+    if (++s == N) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+// One row of dots.  FULL: a full-width strip (every element in range except the
+// tail of the last block, whose index is clamped); else every index is clamped.
+// u and w are read from shared memory next to each V tile (no register cache:
+// 16 accumulator chains per quad stay in flight); a clamped lane re-reads a valid
+// element against zero u, w.
+template <class S, bool FULL>
+__device__ __forceinline__ void dots_row(const double2* U2, const double2* W2, const double* vring, uint64_t* vfull,
+                                         uint64_t* vempty, RingPos& vp, int j, int cnt2, int lane, int h,
+                                         double* acc, bool skip) {
+  constexpr int T2 = S::TILE / 2;          // double2 per row tile
+  constexpr int PER = (T2 + 63) / 64;      // blocks of 64 double2 (32 per dot warp)
+  const int e0 = 32 * h + lane;
+  auto eidx = [&](int m) {
+    const bool in_range = FULL && 64 * m + 64 <= T2;  // compile-time per unrolled m
+    return in_range ? e0 + 64 * m : min(e0 + 64 * m, cnt2 - 1);
+  };
+  auto valid = [&](int m) { return (FULL && 64 * m + 64 <= T2) || e0 + 64 * m < cnt2; };
+  auto ld_uw = [&](int m, double2& u, double2& w) {
+    const bool v = valid(m);
+    const int e = eidx(m);
+    u = v ? U2[e] : make_double2(0.0, 0.0);
+    w = v ? W2[e] : make_double2(0.0, 0.0);
+  };
+  auto take = [&]() {
+    const int s = vp.s;
+    mbar_wait(&vfull[s], vp.ph);
+    vp.next<S::VS>();
+    return s;
+  };
+  auto tile = [&](int s) { return reinterpret_cast<const double2*>(vring + (size_t)s * S::TILE); };
+  if (skip) {  // diagnostics: the V stream without the arithmetic
+    for (int i = 0; i < j; ++i) {
+      const int s = take();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&vempty[s]);
+    }
+    return;
+  }
+  int i0 = 0;
+  for (; i0 + 3 < j; i0 += 4) {  // quads: 16 independent FMA chains, two butterflies
+    const int sa = take(), sb = take(), sc = take(), sd = take();
+    const double2 *A = tile(sa), *B = tile(sb), *C = tile(sc), *D = tile(sd);
+    double xa0 = 0.0, xa1 = 0.0, ya0 = 0.0, ya1 = 0.0, xb0 = 0.0, xb1 = 0.0, yb0 = 0.0, yb1 = 0.0;
+    double xc0 = 0.0, xc1 = 0.0, yc0 = 0.0, yc1 = 0.0, xd0 = 0.0, xd1 = 0.0, yd0 = 0.0, yd1 = 0.0;
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int e = eidx(m);
+      double2 u, w;
+      ld_uw(m, u, w);
+      const double2 ta = A[e], tb = B[e], tc = C[e], td = D[e];
+      xa0 = fma(ta.x, u.x, xa0);
+      xb0 = fma(tb.x, u.x, xb0);
+      xc0 = fma(tc.x, u.x, xc0);
+      xd0 = fma(td.x, u.x, xd0);
+      ya0 = fma(ta.x, w.x, ya0);
+      yb0 = fma(tb.x, w.x, yb0);
+      yc0 = fma(tc.x, w.x, yc0);
+      yd0 = fma(td.x, w.x, yd0);
+      xa1 = fma(ta.y, u.y, xa1);
+      xb1 = fma(tb.y, u.y, xb1);
+      xc1 = fma(tc.y, u.y, xc1);
+      xd1 = fma(td.y, u.y, xd1);
+      ya1 = fma(ta.y, w.y, ya1);
+      yb1 = fma(tb.y, w.y, yb1);
+      yc1 = fma(tc.y, w.y, yc1);
+      yd1 = fma(td.y, w.y, yd1);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&vempty[sa]);
+      mbar_arrive(&vempty[sb]);
+      mbar_arrive(&vempty[sc]);
+      mbar_arrive(&vempty[sd]);
+    }
+    dots_bfly_add(acc, lane, i0, i0 + 1, xa0 + xa1, ya0 + ya1, xb0 + xb1, yb0 + yb1);
+    dots_bfly_add(acc, lane, i0 + 2, i0 + 3, xc0 + xc1, yc0 + yc1, xd0 + xd1, yd0 + yd1);
+  }
+  // the remaining 0..3 V tiles, then the candidate u itself (i = j), two per butterfly
+  for (; i0 <= j; i0 += 2) {
+    const int sa = i0 < j ? take() : -1, sb = i0 + 1 < j ? take() : -1;
+    const double2* A = tile(max(sa, 0));
+    const double2* B = tile(max(sb, 0));
+    double xa0 = 0.0, xa1 = 0.0, ya0 = 0.0, ya1 = 0.0, xb0 = 0.0, xb1 = 0.0, yb0 = 0.0, yb1 = 0.0;
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int e = eidx(m);
+      double2 u, w;
+      ld_uw(m, u, w);
+      const double2 ta = sa >= 0 ? A[e] : u;  // i0 == j: the candidate
+      const double2 tb = sb >= 0 ? B[e] : (i0 + 1 == j ? u : make_double2(0.0, 0.0));
+      xa0 = fma(ta.x, u.x, xa0);
+      xb0 = fma(tb.x, u.x, xb0);
+      ya0 = fma(ta.x, w.x, ya0);
+      yb0 = fma(tb.x, w.x, yb0);
+      xa1 = fma(ta.y, u.y, xa1);
+      xb1 = fma(tb.y, u.y, xb1);
+      ya1 = fma(ta.y, w.y, ya1);
+      yb1 = fma(tb.y, w.y, yb1);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (sa >= 0) mbar_arrive(&vempty[sa]);
+      if (sb >= 0) mbar_arrive(&vempty[sb]);
+    }
+    dots_bfly_add(acc, lane, i0, i0 + 1 <= j ? i0 + 1 : -1, xa0 + xa1, ya0 + ya1, xb0 + xb1, yb0 + yb1);
+  }
+}
+
+template <class S>
+__device__ __forceinline__ void strip_dots(const double* ring, const double* swr, const double* vring,
+                                           uint64_t* full, uint64_t* empty, uint64_t* wfull, uint64_t* wempty,
+                                           uint64_t* vfull, uint64_t* vempty, long long k0, long long k1, int nx,
+                                           int ny, int j, double* s_acc, bool skip) {
+  const int lane = threadIdx.x & 31;
+  const int h = (threadIdx.x >> 5) - (S::CONS / 32 + 2);
+  double* acc = s_acc + h * 2 * (S::JMAX + 1);
+  RingPos vp, wp;  // V ring; the w-row double buffer
+  long long seq = 0;
+  for (long long k = k0; k < k1;) {
+    const StripUnit su = strip_unit<S::W>(k, k1, nx, ny);
+    const int cnt2 = su.w * S::BLK / 2;  // double2 per row tile
+    for (int r = su.r0; r < su.r1; ++r) {
+      const long long q = r - su.r0 + 1;  // ring index of row r
+      const int bsel = wp.s;
+      mbar_wait(&wfull[bsel], wp.ph);
+      wp.next<2>();
+      const int sl = (int)((seq + q) % S::NBUF);
+      mbar_wait(&full[sl], (int)(((seq + q) / S::NBUF) & 1));  // completed phase: returns at once
+      const double2* U2 = reinterpret_cast<const double2*>(ring + (size_t)sl * S::BUFD + S::BLK);
+      const double2* W2 = reinterpret_cast<const double2*>(swr + bsel * S::TILE);
+      if (su.w == S::W) dots_row<S, true>(U2, W2, vring, vfull, vempty, vp, j, cnt2, lane, h, acc, skip);
+      else dots_row<S, false>(U2, W2, vring, vfull, vempty, vp, j, cnt2, lane, h, acc, skip);
+      __syncwarp();
+      if (lane == 0) {  // u (the x ring row) and the w row are free
+        mbar_arrive(&wempty[bsel]);
+        mbar_arrive(&empty[sl]);
+      }
+    }
+    seq += su.r1 - su.r0 + 2;
+  }
+}
+
+template <int NP, bool ROE, int CW, bool DOT>
+__global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 2 : 1)
     k_e2_phi_strip(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
-  using S = E2Strip<NP, CW>;
+  using S = E2Strip<NP, CW, DOT>;
   constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
+  constexpr int NWARP = S::THREADS / 32;
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;
   double* sf0 = smem + NBUF * S::BUFD;
-  double* sfx0 = sf0 + 2 * (2 * W * BLK);
+  double* sfx0 = sf0 + S::SFB * (2 * W * BLK);
   double* sfy = sfx0 + 2 * S::FX;
+  double* swr = smem + S::BASE;       // DOT: w rows handed to the dot warps
+  double* vring = swr + 2 * S::TILE;  // DOT: V row tiles
   __shared__ uint64_t full[NBUF], empty[NBUF];
+  __shared__ uint64_t wfull[2], wempty[2], vfull[S::VS], vempty[S::VS];
   __shared__ double s_wd[NP * NP], s_wq[NP];
-  __shared__ int s_go, s_j;
+  __shared__ int s_go, s_j, s_dots;
   __shared__ double s_xs, s_dt, s_xt[kMaxP];
   __shared__ long long s_ld;
-  __shared__ double s_buf[CW + 1];
-  __shared__ double s_red[1];
+  __shared__ double s_buf[NWARP];
+  // DOT: per tile half, the dot sums 2 i + {0: <V_i,u>, 1: <V_i,w>}; then (reused in place)
+  // the grid-reduction inputs [dotA_0..j, dotB_0..j, ||y||^2]
+  __shared__ double s_red[DOT ? 4 * (S::JMAX + 1) : 1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     const int a = st->action;
     s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
     if (s_go) {
       s_j = st->j;
+      s_dots = DOT && st->dcgs && s_j <= S::JMAX;
+      if (blockIdx.x == 0) {
+        st->dots_fused = s_dots;
+        // algorithmic bytes of this sweep (bench.py's dominant-kernel roofline): x, q~, b_1, y
+        // plus, with the dots, V_0..V_{j-1}
+        st->app_bytes += 8.0 * (double)P.n * (4.0 + (s_dots ? (double)s_j : 0.0));
+        st->app_launches++;
+      }
       s_xs = st->scale[s_j];
       s_dt = st->dt;
       s_ld = st->ld;
@@ -529,19 +763,35 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
       for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
       for (int q = 0; q < NBUF; ++q) {
         mbar_init(&full[q], 1);
-        mbar_init(&empty[q], 1);
+        mbar_init(&empty[q], 1 + S::ND);  // the JVP warps + (DOT) every dot warp
+      }
+      if (DOT) {
+        for (int q = 0; q < 2; ++q) {
+          mbar_init(&wfull[q], CW);
+          mbar_init(&wempty[q], S::ND);
+        }
+        for (int q = 0; q < S::VS; ++q) {
+          mbar_init(&vfull[q], 1);
+          mbar_init(&vempty[q], S::ND);  // both tile-half dot warps
+        }
       }
       fence_mbar_init();
     }
   }
   for (int q = tid; q < NP * NP; q += blockDim.x) s_wd[q] = P.WD[q];
   for (int q = tid; q < NP; q += blockDim.x) s_wq[q] = P.w[q];
+  if (DOT)
+    for (int q = tid; q < 4 * (S::JMAX + 1); q += blockDim.x) s_red[q] = 0.0;
   __syncthreads();
   if (!s_go) return;
   const double* x = base + (size_t)s_j * s_ld;
   double* y = base + (size_t)(s_j + 1) * s_ld;
   const double xs = s_xs, dt = s_dt;
   const int nx = P.nx, ny = P.ny;
+  const bool dots = DOT && s_dots;
+  // ring rows the dot warps also read (u) are released by them too; halo rows and,
+  // without dots, every row are released by the JVP warps for all 1 + ND arrivals
+  const uint32_t rel_row = dots ? 1u : 1u + S::ND, rel_halo = 1u + S::ND;
   const int nstrips = (nx + W - 1) / W;
   // each CTA owns one contiguous range of the (strip, row) row-steps: equal work per CTA,
   // one or two segments (a new segment restarts the ring with its lower halo row)
@@ -552,14 +802,12 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
   double nacc = 0.0;
 
   if (wid == CW) {
-    // ---------------- producer
+    // ---------------- producer: x / frozen / b_1 rows
     if (lane == 0) {
       long long seq = 0;
       for (long long k = k0; k < k1;) {
-        const int strip = (int)(k / ny), r0 = (int)(k - (long long)strip * ny);
-        const int r1 = (int)min((long long)ny, r0 + (k1 - k));
-        k += r1 - r0;
-        const int ie0 = strip * W, w = min(W, nx - ie0);
+        const StripUnit su = strip_unit<W>(k, k1, nx, ny);
+        const int ie0 = su.ie0, w = su.w, r0 = su.r0, r1 = su.r1;
         for (int q = 0; q < r1 - r0 + 2; ++q) {
           int row = r0 - 1 + q;
           const double* srcx = x;
@@ -598,6 +846,33 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
         }
       }
     }
+  } else if (DOT && wid == CW + 1) {
+    // ---------------- producer: row tiles of V_0..V_{j-1} for the dot warps
+    if (dots && lane == 0) {
+      const int j = s_j;
+      const long long ld = s_ld;
+      RingPos vp;
+      for (long long k = k0; k < k1;) {
+        const StripUnit su = strip_unit<W>(k, k1, nx, ny);
+        const uint32_t bytes = (uint32_t)(su.w * BLK * 8);
+        for (int r = su.r0; r < su.r1; ++r) {
+          const double* src = base + ((size_t)r * nx + su.ie0) * BLK;
+          for (int i = 0; i < j; ++i) {
+            const int stg = vp.s;
+            mbar_wait(&vempty[stg], vp.ph ^ 1u);
+            mbar_arrive_expect_tx(&vfull[stg], bytes);
+            bulk_g2s(vring + (size_t)stg * S::TILE, src + (size_t)i * ld, bytes, &vfull[stg]);
+            vp.next<S::VS>();
+          }
+        }
+      }
+    }
+  } else if (DOT && wid > CW + 1) {
+    // ---------------- dot warps
+    if (dots) {
+      strip_dots<S>(ring, swr, vring, full, empty, wfull, wempty, vfull, vempty, k0, k1, nx, ny, s_j, s_red,
+                    (P.dbg & 1) != 0);
+    }
   } else {
     // ---------------- consumers: one thread per node of the strip row
     const int le = tid / NN, node = tid % NN;
@@ -613,11 +888,10 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
     const double wi = s_wq[i], wj = s_wq[j];
     const double iwij = 1.0 / (wi * wj);
     long long seq = 0;
+    int rowc = 0;
     for (long long k = k0; k < k1;) {
-      const int strip = (int)(k / ny), r0 = (int)(k - (long long)strip * ny);
-      const int r1 = (int)min((long long)ny, r0 + (k1 - k));
-      k += r1 - r0;
-      const int ie0 = strip * W, w = min(W, nx - ie0);
+      const StripUnit su = strip_unit<W>(k, k1, nx, ny);
+      const int ie0 = su.ie0, w = su.w, r0 = su.r0, r1 = su.r1;
       const bool active = le < w;
       const int ie = ie0 + le;
       const double hx = active ? __ldg(P.hx + ie) : 1.0;
@@ -633,7 +907,8 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
         const double* cur = slot(q);
         const double* lo = slot(q - 1);
         const double* hi = slot(q + 1);
-        double* sf = sf0 + (q & 1) * (2 * W * BLK);
+        double* sf = sf0 + (S::SFB == 2 ? (q & 1) : 0) * (2 * W * BLK);
+        if (S::SFB == 1 && r > r0) strip_sync<S::CONS>();  // C of row r-1 has read sf
         double* sfx = sfx0 + (q & 1) * S::FX;
         const double hy = __ldg(P.hy + r);
         const double ihy = __ldg(P.ihy + r);
@@ -696,7 +971,10 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
           }
         }
         strip_sync<S::CONS>();  // A/B of row r done; every thread has also finished C of row r-1
-        if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);  // ring row r-1 is free
+        if (tid == 0) mbar_arrive_cnt(&empty[(seq + q - 1) % NBUF], q == 1 ? rel_halo : rel_row);  // row r-1 free
+        const int bsel = rowc & 1;
+        double* wrow = swr + bsel * S::TILE;
+        if (dots) mbar_wait(&wempty[bsel], ((rowc >> 1) & 1) ^ 1);  // the dot warps took row r-2
         if (active) {
           const double sy = 0.5 * hy * wj;
           double rr[4];
@@ -739,28 +1017,61 @@ __global__ void __launch_bounds__(32 * CW + 32, CW <= 4 ? 2 : 1)
             }
             v = dt * v;
             y[g] = v;
+            if (dots) wrow[le * BLK + c * NN + node] = v;
             nacc = fma(v, v, nacc);
           }
         }
+        if (dots) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&wfull[bsel]);
+        }
+        ++rowc;
       }
       strip_sync<S::CONS>();  // C of the unit's last row done
       if (tid == 0) {
-        mbar_arrive(&empty[(seq + (r1 - r0)) % NBUF]);      // row r1 - 1
-        mbar_arrive(&empty[(seq + (r1 - r0) + 1) % NBUF]);  // row r1 (upper halo)
+        mbar_arrive_cnt(&empty[(seq + (r1 - r0)) % NBUF], r1 - r0 == 0 ? rel_halo : rel_row);  // row r1 - 1
+        mbar_arrive_cnt(&empty[(seq + (r1 - r0) + 1) % NBUF], rel_halo);                        // row r1 (upper halo)
       }
       seq += r1 - r0 + 2;
     }
   }
   __syncthreads();
+  const int cnt = dots ? s_j + 1 : 0;
   if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
     const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
     y[P.n + tid] = v;
     if (st->tail_here) nacc = fma(v, v, nacc);
   }
   const double tot = block_sum(nacc, s_buf);
-  if (tid == 0) s_red[0] = tot;
+  // dots: the two tile halves, plus (rank 0) the tail region [n, n + kTailPad) of every
+  // slot, which k_ts2 streams with the head; cnt <= JMAX + 1 <= blockDim.x
+  double ca = 0.0, cb = 0.0;
+  if (tid < cnt) {
+    constexpr int JS = 2 * (S::JMAX + 1);
+    ca = s_red[2 * tid] + s_red[JS + 2 * tid];
+    cb = s_red[2 * tid + 1] + s_red[JS + 2 * tid + 1];
+    if (blockIdx.x == 0 && st->tail_here) {
+      const double* ut = base + (size_t)s_j * s_ld + P.n;
+      const double* vt = base + (size_t)tid * s_ld + P.n;
+      for (int t = 0; t < kTailPad; ++t) {
+        const double yt = (t + 1 < b.p) ? dt * s_xt[t + 1] : 0.0;
+        ca = fma(vt[t], ut[t], ca);
+        cb = fma(vt[t], yt, cb);
+      }
+    }
+  }
   __syncthreads();
-  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
+  if (tid < cnt) {
+    s_red[tid] = ca;
+    s_red[cnt + tid] = cb;
+  }
+  if (tid == 0) s_red[2 * cnt] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 2 * cnt + 1, partials, 2 * kMaxSlots + 2, &st->ticket[4], [&](int i, double v) {
+    if (i < cnt) st->rs().dotA[i] = v;
+    else if (i < 2 * cnt) st->rs().dotB[i - cnt] = v;
+    else st->rs().nrmA = v;
+  });
 }
 
 // (u, v, H, a | sqrt(rho)) of q~ per node (proj/src/euler.cpp:15-24): the frozen
@@ -793,17 +1104,31 @@ class Euler2D : public OpDevice {
   bool use_strip = true;
   bool roe = false;
   int strip_cw = 8;  // consumer warps per strip CTA (EXPDG_E2_CW=4: half-width strips, 2 CTAs / SM)
-  template <int CW>
+  template <int CW, bool DOT>
   void launch_strip(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
                     const BArgs& b) {
-    using SS = E2Strip<NP, CW>;
+    using SS = E2Strip<NP, CW, DOT>;
     int per_sm = 1;
-    EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_e2_phi_strip<NP, false, CW>, 32 * CW + 32,
-                                                             SS::SMEM));
+    EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_e2_phi_strip<NP, false, CW, DOT>,
+                                                             SS::THREADS, SS::SMEM));
     const long long rows = (long long)((P.nx + SS::W - 1) / SS::W) * P.ny;
     const int g = (int)std::max<long long>(1, std::min<long long>(rows, 148LL * std::max(1, per_sm)));
-    if (roe) k_e2_phi_strip<NP, true, CW><<<g, 32 * CW + 32, SS::SMEM, s>>>(p, st, base, partials, b);
-    else k_e2_phi_strip<NP, false, CW><<<g, 32 * CW + 32, SS::SMEM, s>>>(p, st, base, partials, b);
+    if (roe) k_e2_phi_strip<NP, true, CW, DOT><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b);
+    else k_e2_phi_strip<NP, false, CW, DOT><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b);
+  }
+  // The strip JVP also takes the DCGS2 pass-1 dots of columns j <= JMAX (EXPDG_E2_DOTS=0:
+  // off).  Same-box A/B at C4 (bench.py, 5 steps): 257.7 vs 263.3 ms per step.
+  static constexpr bool kDotFits = E2Strip<NP, 8, true>::FITS;
+  bool use_dots = true;
+  bool dots_on() const { return kDotFits && use_dots && use_strip && strip_cw == 8; }
+  int fused_dcgs_dots_jmax() const override { return dots_on() ? E2Strip<NP, 8, true>::JMAX : -1; }
+  template <int CW, bool DOT>
+  static void set_strip_attrs() {
+    using SS = E2Strip<NP, CW, DOT>;
+    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, false, CW, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    SS::SMEM));
+    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, true, CW, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    SS::SMEM));
   }
   // slab partition: halo rows (x lo/hi, frozen lo/hi) and send staging (lo/hi)
   double* halo = nullptr;
@@ -877,14 +1202,11 @@ class Euler2D : public OpDevice {
     use_strip = !(std::getenv("EXPDG_E2_TILE") && std::getenv("EXPDG_E2_TILE")[0] == '1');
     roe = d.euler_flux == 0;
     if (const char* v = std::getenv("EXPDG_E2_CW")) strip_cw = std::atoi(v) == 4 ? 4 : 8;
-    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, false, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    E2Strip<NP, 8>::SMEM));
-    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, true, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    E2Strip<NP, 8>::SMEM));
-    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    E2Strip<NP, 4>::SMEM));
-    EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip<NP, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    E2Strip<NP, 4>::SMEM));
+    if (const char* v = std::getenv("EXPDG_E2_DOTS")) use_dots = v[0] != '0';
+    if (const char* v = std::getenv("EXPDG_E2_DBG")) P.dbg = std::atoi(v);
+    set_strip_attrs<8, false>();
+    set_strip_attrs<4, false>();
+    if constexpr (kDotFits) set_strip_attrs<8, true>();
     const long long ntiles = ((long long)d.nx * nyl + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
   }
@@ -895,8 +1217,13 @@ class Euler2D : public OpDevice {
     }
     const E2P<NP> p = params(frozen);
     if (use_strip) {
-      if (strip_cw == 4) launch_strip<4>(s, p, st, base, partials, b);
-      else launch_strip<8>(s, p, st, base, partials, b);
+      if (strip_cw == 4) {
+        launch_strip<4, false>(s, p, st, base, partials, b);
+      } else if (dots_on()) {
+        if constexpr (kDotFits) launch_strip<8, true>(s, p, st, base, partials, b);
+      } else {
+        launch_strip<8, false>(s, p, st, base, partials, b);
+      }
     } else {
       if (roe) k_e2_phi<NP, true><<<grid, 256, 0, s>>>(p, st, base, partials, b);
       else k_e2_phi<NP, false><<<grid, 256, 0, s>>>(p, st, base, partials, b);

@@ -99,3 +99,41 @@ def test_dense_fakes_with_breakdown(orth):
     b0 = rng.standard_normal(8)
     got, st = pkg.phi_combination(ctx, op, [to_dev(b0)], 0.5, tol=1e-12)
     assert rel(to_host(got), math.exp(0.5) * b0) < 1e-13
+
+
+def _euler_run(monkeypatch, fused, max_basis, flux="lf"):
+    # the strip JVP takes the DCGS2 pass-1 dots of columns j <= 43 in its own sweep
+    # (EXPDG_E2_DOTS=0: the separate k_ts2 dots pass for every column); nx = 24 leaves a
+    # partial last strip (10 + 10 + 4 elements)
+    monkeypatch.setenv("EXPDG_E2_DOTS", fused)
+    w = configs.scaled(configs.C4, 24, steps=3)
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    spec = w.spec()
+    if flux != "lf":
+        spec = pkg.OperatorSpec("euler2d", spec.order, spec.nx, spec.ny, box=spec.box, euler_flux=flux)
+    ctx = pkg.Context(0, orth="dcgs2", fused=False)
+    op = pkg.Operator(ctx, spec)
+    res = pkg.integrate(ctx, op, to_dev(u0), "epi2", dt, w.steps * dt, tol=w.tol, max_basis=max_basis,
+                        orth_length=max_basis)
+    res.alg_bytes = ctx.traffic()["alg_bytes"]
+    op.linearize(to_dev(u0))
+    r = to_dev(to_host(op.apply_linear(to_dev(u0))) + to_host(op.apply_nonlinear(to_dev(u0))))
+    try:  # one substep at 2x dt: H of one Arnoldi with columns past the fused bound
+        pkg.phi_combination(ctx, op, [None, r], 2 * dt, tol=1e-14, max_basis=max_basis, orth_length=max_basis,
+                            max_substeps=1)
+    except pkg.KrylovError:
+        pass
+    return res, ctx.debug_hessenberg()[:max_basis + 1, :max_basis]
+
+
+@pytest.mark.parametrize("max_basis,flux", [(40, "lf"), (64, "lf"), (40, "roe")])
+def test_euler_fused_dots_match_dots_pass(monkeypatch, max_basis, flux):
+    a, ha = _euler_run(monkeypatch, "1", max_basis, flux)
+    b, hb = _euler_run(monkeypatch, "0", max_basis, flux)
+    assert a.status == b.status == "completed"
+    assert rel(to_host(a.u), to_host(b.u)) <= 1e-12
+    assert list(a.iters_per_step) == list(b.iters_per_step)
+    assert np.abs(ha - hb).max() <= 1e-12 * np.abs(hb).max()
+    # the sweep really took the dots: u and w are not re-read (16 n bytes less per column)
+    assert a.alg_bytes < b.alg_bytes
