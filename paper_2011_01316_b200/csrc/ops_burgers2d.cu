@@ -8,6 +8,7 @@
 // runs the 1D element kernel along x; phase 2: one thread per (element, column)
 // along y and adds.  Line neighbours come from L2.
 #include <algorithm>
+#include <cstdlib>
 
 #include "burgers_common.cuh"
 
@@ -155,6 +156,207 @@ __global__ void __launch_bounds__(256) k_b2_phi(B1P<NP> Px, B1P<NP> Py, int nx, 
   grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
+// ---------------------------------------------------------------- strip JVP (phi cycle)
+// A CTA owns a strip of W = 32 (16 for orders 7, 8) element columns and marches up a contiguous range of
+// element rows (the Euler strip kernel's scheme, ops_euler2d.cu): warp CW streams whole
+// element rows of x (slot j) and u~ with their E/W halo elements, plus b_1, by
+// asynchronous copies into a 4-row shared-memory ring; the consumer threads take row r's
+// x-lines (thread per element row-line, neighbours from the ring row's halo elements)
+// and y-lines (thread per element column-line, neighbours from ring rows r -+ 1), so
+// every byte of x and u~ leaves HBM once per JVP instead of being gathered from L2 by
+// three elements in two directions.
+template <int NP>
+struct B2Strip {
+  static constexpr int NN = NP * NP;
+  static constexpr int W = NP <= 7 ? 32 : 16;        // elements per strip
+  static constexpr int CONS = (W * NP + 31) / 32 * 32;  // consumer threads: one per element line
+  static constexpr int CW = CONS / 32;       // consumer warps
+  static constexpr int ROWD = (W + 2) * NN;  // doubles per array per ring row (with halo)
+  static constexpr int BUFD = 2 * ROWD + W * NN;  // x + u~ (with halo) + b_1
+  static constexpr int NBUF = 4;
+  static constexpr int OUT = W * NN;         // one row of x-line or y-line results
+  static constexpr int SMEM = (NBUF * BUFD + 2 * 2 * OUT) * 8;  // ring + double-buffered sX, sY
+};
+
+template <int NP>
+__global__ void __launch_bounds__(B2Strip<NP>::CONS + 32)
+    k_b2_phi_strip(B1P<NP> Px, B1P<NP> Py, int nx, int ny, PhiState* st, double* base, double* partials, BArgs b) {
+  using S = B2Strip<NP>;
+  constexpr int NN = S::NN, W = S::W, NBUF = S::NBUF, CW = S::CW;
+  extern __shared__ __align__(128) double smem[];
+  double* ring = smem;
+  double* sout = smem + NBUF * S::BUFD;  // [parity][X | Y][W * NN]
+  __shared__ uint64_t full[NBUF], empty[NBUF];
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[CW + 1];
+  __shared__ double s_red[1];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    const int a = st->action;
+    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    if (s_go) {
+      s_j = st->j;
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[Px.n + i] * s_xs : 0.0;
+      for (int q = 0; q < NBUF; ++q) {
+        mbar_init(&full[q], 32);  // every producer lane's cp.async arrival
+        mbar_init(&empty[q], 1);
+      }
+      fence_mbar_init();
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  const int nstrips = (nx + W - 1) / W;
+  const long long rsteps = (long long)nstrips * ny;
+  const long long k0 = rsteps * blockIdx.x / gridDim.x, k1 = rsteps * (blockIdx.x + 1) / gridDim.x;
+  const double* b1 = (b.p == 1) ? b.b[1] : nullptr;
+  double nacc = 0.0;
+  auto unit = [&](long long& k, int& ie0, int& w, int& r0, int& r1) {
+    const int strip = (int)(k / ny);
+    r0 = (int)(k - (long long)strip * ny);
+    r1 = (int)min((long long)ny, r0 + (k1 - k));
+    k += r1 - r0;
+    ie0 = strip * W;
+    w = min(W, nx - ie0);
+  };
+
+  if (wid == CW) {
+    // ---------------- producer warp: x / u~ rows with their E/W halo elements, b_1 rows.
+    // Element rows of NP^2 doubles are 8- but not 16-byte aligned, so the rows move by
+    // coalesced 8-byte cp.async (one warp) rather than TMA bulk copies; every lane's
+    // copies complete an arrival on the row's full barrier.
+    long long seq = 0;
+    auto copy = [&](double* d, const double* src, int cnt) {
+      for (int t = lane; t < cnt; t += 32) cp_async8(d + t, src + t);
+    };
+    for (long long k = k0; k < k1;) {
+      int ie0, w, r0, r1;
+      unit(k, ie0, w, r0, r1);
+      for (int q = 0; q < r1 - r0 + 2; ++q, ++seq) {
+        int row = r0 - 1 + q;
+        const double* srcx = x;
+        const double* srct = Py.ut;
+        if (Py.part && (row < 0 || row >= ny)) {  // halo row of the neighbouring rank
+          srcx = row < 0 ? Py.gx_lo : Py.gx_hi;
+          srct = row < 0 ? Py.gt_lo : Py.gt_hi;
+          row = 0;
+        } else {
+          row = row < 0 ? row + ny : (row >= ny ? row - ny : row);
+        }
+        const int sl = (int)(seq % NBUF);
+        if (lane == 0) mbar_wait(&empty[sl], (int)(((seq / NBUF) & 1) ^ 1));
+        __syncwarp();
+        double* dst = ring + (size_t)sl * S::BUFD;
+        const bool with_b = b1 && q >= 1 && q <= r1 - r0;
+        const size_t rbase = (size_t)row * nx;
+        const int left = ie0 == 0 ? nx - 1 : ie0 - 1;
+        const int right = ie0 + w == nx ? 0 : ie0 + w;
+        for (int arr = 0; arr < 2; ++arr) {
+          const double* src = arr == 0 ? srcx : srct;
+          double* d = dst + arr * S::ROWD;
+          if (ie0 >= 1 && ie0 + w < nx) {
+            copy(d, src + (rbase + left) * NN, (w + 2) * NN);
+          } else {
+            copy(d, src + (rbase + left) * NN, NN);
+            copy(d + NN, src + (rbase + ie0) * NN, w * NN);
+            copy(d + (size_t)(w + 1) * NN, src + (rbase + right) * NN, NN);
+          }
+        }
+        if (with_b) copy(dst + 2 * S::ROWD, b1 + ((size_t)(r0 - 1 + q) * nx + ie0) * NN, w * NN);
+        cp_async_arrive(&full[sl]);
+      }
+    }
+  } else {
+    // ---------------- consumers: thread (element le, line l)
+    const int le = tid / NP, l = tid % NP;
+    long long seq = 0;
+    int rowc = 0;
+    for (long long k = k0; k < k1;) {
+      int ie0, w, r0, r1;
+      unit(k, ie0, w, r0, r1);
+      const bool active = le < w;
+      auto slot = [&](long long q) { return ring + (size_t)((seq + q) % NBUF) * S::BUFD; };
+      auto wait_row = [&](long long q) { mbar_wait(&full[(seq + q) % NBUF], (int)(((seq + q) / NBUF) & 1)); };
+      wait_row(0);
+      wait_row(1);
+      for (int r = r0; r < r1; ++r, ++rowc) {
+        const long long q = r - r0 + 1;
+        wait_row(q + 1);
+        const double* cur = slot(q);
+        const double* lo = slot(q - 1);
+        const double* hi = slot(q + 1);
+        double* sX = sout + (rowc & 1) * 2 * S::OUT;
+        double* sY = sX + S::OUT;
+        if (active) {
+          double xL[NP], xC[NP], xR[NP], uL[NP], uC[NP], uR[NP], out[NP];
+          // x-line l (element row l): ring elements le, le + 1, le + 2 of row r
+#pragma unroll
+          for (int t = 0; t < NP; ++t) {
+            xL[t] = cur[le * NN + l * NP + t] * xs;
+            xC[t] = cur[(le + 1) * NN + l * NP + t] * xs;
+            xR[t] = cur[(le + 2) * NN + l * NP + t] * xs;
+            uL[t] = cur[S::ROWD + le * NN + l * NP + t];
+            uC[t] = cur[S::ROWD + (le + 1) * NN + l * NP + t];
+            uR[t] = cur[S::ROWD + (le + 2) * NN + l * NP + t];
+          }
+          b1_element<NP>(Px, 0, ie0 + le, xL, xC, xR, uL, uC, uR, out);
+#pragma unroll
+          for (int t = 0; t < NP; ++t) sX[le * NN + l * NP + t] = out[t];
+          // y-line l (element column l): element le + 1 of ring rows r - 1, r, r + 1
+#pragma unroll
+          for (int t = 0; t < NP; ++t) {
+            xL[t] = lo[(le + 1) * NN + t * NP + l] * xs;
+            xC[t] = cur[(le + 1) * NN + t * NP + l] * xs;
+            xR[t] = hi[(le + 1) * NN + t * NP + l] * xs;
+            uL[t] = lo[S::ROWD + (le + 1) * NN + t * NP + l];
+            uC[t] = cur[S::ROWD + (le + 1) * NN + t * NP + l];
+            uR[t] = hi[S::ROWD + (le + 1) * NN + t * NP + l];
+          }
+          b1_element<NP>(Py, 0, (int)Py.eoff + r, xL, xC, xR, uL, uC, uR, out);
+#pragma unroll
+          for (int t = 0; t < NP; ++t) sY[le * NN + t * NP + l] = out[t];
+        }
+        strip_sync<S::CONS>();  // sX, sY of row r complete; row r-1 is no longer read
+        if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);  // ring row r - 1 is free
+        const size_t g0 = ((size_t)r * nx + ie0) * NN;
+        for (int idx = tid; idx < w * NN; idx += S::CONS) {
+          double v = sX[idx] + sY[idx];
+          if (b1) v = fma(s_xt[0], cur[2 * S::ROWD + idx], v);
+          else v = aug_tail(b, s_xt, g0 + idx, v);
+          v = dt * v;
+          y[g0 + idx] = v;
+          nacc = fma(v, v, nacc);
+        }
+      }
+      strip_sync<S::CONS>();  // the unit's last row is done
+      if (tid == 0) {
+        mbar_arrive(&empty[(seq + (r1 - r0)) % NBUF]);      // row r1 - 1
+        mbar_arrive(&empty[(seq + (r1 - r0) + 1) % NBUF]);  // row r1 (upper halo)
+      }
+      seq += r1 - r0 + 2;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
+    const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
+    y[Px.n + tid] = v;
+    if (st->tail_here) nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (tid == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
+}
+
 template <int NP>
 class Burgers2D : public OpDevice {
  public:
@@ -163,6 +365,8 @@ class Burgers2D : public OpDevice {
   double* halo = nullptr;        // row slab: x lo/hi, u~ lo/hi, send lo/hi (one element row each)
   double* htab = nullptr;        // {h, 2 / h} per element column, then per element row
   long long rowd = 0;
+  bool use_strip = true;         // EXPDG_B2_TILE=1: the element-tile kernel (neighbours from L2)
+  int strip_grid = 1;
   ~Burgers2D() override {
     cudaFree(halo);
     cudaFree(htab);
@@ -218,6 +422,13 @@ class Burgers2D : public OpDevice {
     }
     const long long ntiles = ((long long)d.nx * ny + B2Tile<NP>::TE - 1) / B2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
+    use_strip = !(std::getenv("EXPDG_B2_TILE") && std::getenv("EXPDG_B2_TILE")[0] == '1');
+    using SS = B2Strip<NP>;
+    EXPDG_CUDA(cudaFuncSetAttribute(k_b2_phi_strip<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::SMEM));
+    int per_sm = 1;
+    EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_b2_phi_strip<NP>, SS::CONS + 32, SS::SMEM));
+    const long long rsteps = (long long)((d.nx + SS::W - 1) / SS::W) * ny;
+    strip_grid = (int)std::max<long long>(1, std::min<long long>(rsteps, 148LL * std::max(1, per_sm)));
   }
   void exchange(cudaStream_t s, const double* v, double* lo, double* hi) {
     comm->halo(v, v + (size_t)(ny - 1) * rowd, lo, hi, rowd, s);
@@ -241,7 +452,11 @@ class Burgers2D : public OpDevice {
     B1P<NP> px = Px, py = Py;
     px.ut = py.ut = ref;
     with_halo(py, false);
-    k_b2_phi<NP><<<grid, 256, 0, s>>>(px, py, nx, ny, st, base, partials, b);
+    if (use_strip)
+      k_b2_phi_strip<NP><<<strip_grid, B2Strip<NP>::CONS + 32, B2Strip<NP>::SMEM, s>>>(px, py, nx, ny, st, base,
+                                                                                         partials, b);
+    else
+      k_b2_phi<NP><<<grid, 256, 0, s>>>(px, py, nx, ny, st, base, partials, b);
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
     if (Py.part) exchange(s, x, hq(0), hq(1));

@@ -521,8 +521,6 @@ struct E2Strip {
   static constexpr int SMEM = (BASE + (DOT ? 2 * TILE + VS * TILE : 0)) * 8;
 };
 
-template <int CONS>
-__device__ __forceinline__ void strip_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONS) : "memory"); }
 
 // The (strip, row) row-steps of a CTA: one contiguous range [k0, k1) of the
 // strip-major row-step order, walked as units of consecutive rows of one strip.
