@@ -3,10 +3,12 @@
 // five conserved variables; the CPU definition is oracle/src/euler.cpp,
 // Euler3DOperator).  A z-invariant state with w = 0 reproduces the 2D operator.
 //
-// One thread per LGL node; CTA tile of floor(256 / NP^3) elements; the frozen
-// data are the per-node primitives (u, v, w, H, a) of q~ (40 B/node, the size
-// of q~ itself) written once per step by the residual kernel.
+// Residual / standalone applies: one thread per LGL node, CTA tile of
+// floor(256 / NP^3) elements.  Phi-cycle JVP: the z-march kernel below.  The frozen
+// data are the per-node primitives (u, v, w, H, a) of q~ (40 B/node, the size of q~
+// itself) written once per step by the residual kernel.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "krylov.cuh"
@@ -383,6 +385,313 @@ __global__ void __launch_bounds__(256) k_e3_phi(E3P<NP> P, PhiState* st, double*
   grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
+// ---------------------------------------------------------------- z-march JVP (phi cycle)
+// A CTA owns a TX x TY tile of element columns and marches up a contiguous range of
+// z-planes.  Warp CW streams the tile's elements of every plane (x = slot j, the frozen
+// primitives, b_1) by 1D TMA bulk copies into a 4-plane shared-memory ring, so every
+// byte of x and q~ leaves HBM once per JVP; only the face nodes of the x/y neighbour
+// elements outside the tile are gathered from L2.  Per plane: phase A computes the
+// volume fluxes A(q~) x of every node and every face flux of the plane ONCE (the
+// reference's rhs_faces loop, proj/src/euler.cpp:260-297, extended to 3D as in
+// oracle/src/euler.cpp): the x- and y-faces of the tile and the z-faces above it (and,
+// on a unit's first plane, below it); phase C differentiates and scatters the face
+// fluxes into each node.  Orders whose element block (5 NP^3 doubles) is a multiple of
+// 16 bytes (NP = 2, 4) use it; NP = 3 keeps the element-tile kernel.
+template <int NP>
+struct E3March {
+  static constexpr int NN = NP * NP * NP, NF = NP * NP, BLK = 5 * NN;
+  static constexpr int TX = NP == 4 ? 2 : 4, TY = NP == 4 ? 2 : 8;  // TX * TY * NN = 256
+  static constexpr int TE = TX * TY;
+  static constexpr int CONS = TE * NN;
+  static constexpr int CW = CONS / 32;
+  static constexpr int PL = TE * BLK;           // doubles per array per ring plane
+  static constexpr int BUFD = 3 * PL;           // x, q~ primitives, b_1
+  static constexpr int NBUF = 4;
+  static constexpr int FXD = (TX + 1) * TY * NF * 5;  // x-face fluxes of a plane
+  static constexpr int FYD = TX * (TY + 1) * NF * 5;  // y-face fluxes
+  static constexpr int FZD = TE * NF * 5;              // one layer of z-face fluxes
+  static constexpr int SMEM = (NBUF * BUFD + 3 * 5 * CONS + FXD + FYD + 2 * FZD) * 8;
+  static constexpr bool OK = (BLK * 8) % 16 == 0;
+};
+
+template <int NP>
+__global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
+    k_e3_phi_march(E3P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
+  using S = E3March<NP>;
+  constexpr int NN = S::NN, NF = S::NF, BLK = S::BLK, TX = S::TX, TY = S::TY, NBUF = S::NBUF, N = NP - 1;
+  extern __shared__ __align__(128) double smem[];
+  double* ring = smem;
+  double* sf = ring + NBUF * S::BUFD;  // [dir][c][thread]
+  double* fxf = sf + 3 * 5 * S::CONS;
+  double* fyf = fxf + S::FXD;
+  double* fzf = fyf + S::FYD;          // two layers
+  __shared__ uint64_t full[NBUF], empty[NBUF];
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[S::CW + 1];
+  __shared__ double s_red[1];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    const int a = st->action;
+    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    if (s_go) {
+      s_j = st->j;
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
+      for (int q = 0; q < NBUF; ++q) {
+        mbar_init(&full[q], 1);
+        mbar_init(&empty[q], 1);
+      }
+      fence_mbar_init();
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  const int nx = P.nx, ny = P.ny, nz = P.nz;
+  const int ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
+  const long long steps = (long long)ntx * nty * nz;
+  const long long k0 = steps * blockIdx.x / gridDim.x, k1 = steps * (blockIdx.x + 1) / gridDim.x;
+  const double* b1 = (b.p == 1) ? b.b[1] : nullptr;
+  double nacc = 0.0;
+  // unit: consecutive planes [z0, z1) of one tile
+  auto unit = [&](long long& k, int& ix0, int& iy0, int& tx, int& ty, int& z0, int& z1) {
+    const long long tile = k / nz;
+    z0 = (int)(k - tile * nz);
+    z1 = (int)min((long long)nz, z0 + (k1 - k));
+    k += z1 - z0;
+    ix0 = (int)(tile % ntx) * TX;
+    iy0 = (int)(tile / ntx) * TY;
+    tx = min(TX, nx - ix0);
+    ty = min(TY, ny - iy0);
+  };
+
+  if (wid == S::CW) {
+    // ---------------- producer: the tile's elements of planes z0 - 1 .. z1
+    if (lane == 0) {
+      long long seq = 0;
+      for (long long k = k0; k < k1;) {
+        int ix0, iy0, tx, ty, z0, z1;
+        unit(k, ix0, iy0, tx, ty, z0, z1);
+        for (int q = 0; q < z1 - z0 + 2; ++q, ++seq) {
+          int z = z0 - 1 + q;
+          const double* srcx = x;
+          const double* srct = P.ut;
+          size_t pbase;
+          if (P.part && (z < 0 || z >= nz)) {  // halo plane of the neighbouring rank
+            srcx = z < 0 ? P.gx_lo : P.gx_hi;
+            srct = z < 0 ? P.gt_lo : P.gt_hi;
+            pbase = 0;
+          } else {
+            z = z < 0 ? z + nz : (z >= nz ? z - nz : z);
+            pbase = (size_t)z * ny * nx;
+          }
+          const int sl = (int)(seq % NBUF);
+          mbar_wait(&empty[sl], (int)(((seq / NBUF) & 1) ^ 1));
+          double* dst = ring + (size_t)sl * S::BUFD;
+          const bool with_b = b1 && q >= 1 && q <= z1 - z0;
+          const uint32_t rowb = (uint32_t)tx * BLK * 8;
+          mbar_arrive_expect_tx(&full[sl], (2u + (with_b ? 1u : 0u)) * (uint32_t)ty * rowb);
+          for (int ly = 0; ly < ty; ++ly) {
+            const size_t e = pbase + (size_t)(iy0 + ly) * nx + ix0;
+            bulk_g2s(dst + (size_t)ly * TX * BLK, srcx + e * BLK, rowb, &full[sl]);
+            bulk_g2s(dst + S::PL + (size_t)ly * TX * BLK, srct + e * BLK, rowb, &full[sl]);
+            if (with_b) {
+              const size_t eb = ((size_t)(z0 - 1 + q) * ny + iy0 + ly) * nx + ix0;
+              bulk_g2s(dst + 2 * S::PL + (size_t)ly * TX * BLK, b1 + eb * BLK, rowb, &full[sl]);
+            }
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers: one thread per node of the tile
+    const int le = tid / NN, node = tid % NN;
+    const int lx = le % TX, ly = le / TX;
+    const int i = node % NP, j = (node / NP) % NP, kk = node / NF;
+    long long seq = 0;
+    for (long long k = k0; k < k1;) {
+      int ix0, iy0, tx, ty, z0, z1;
+      unit(k, ix0, iy0, tx, ty, z0, z1);
+      const bool active = lx < tx && ly < ty;
+      const int ix = ix0 + lx, iy = iy0 + ly;
+      const double hx = active ? __ldg(P.hx + ix) : 1.0, hy = active ? __ldg(P.hy + iy) : 1.0;
+      auto slot = [&](long long q) { return ring + (size_t)((seq + q) % NBUF) * S::BUFD; };
+      auto wait_plane = [&](long long q) { mbar_wait(&full[(seq + q) % NBUF], (int)(((seq + q) / NBUF) & 1)); };
+      const int nfx = (tx + 1) * ty * NF, nfy = tx * (ty + 1) * NF, nfz = tx * ty * NF;
+      wait_plane(0);
+      wait_plane(1);
+      for (int z = z0; z < z1; ++z) {
+        const long long q = z - z0 + 1;
+        wait_plane(q + 1);
+        const double* cur = slot(q);
+        const double* lo = slot(q - 1);
+        const double* hi = slot(q + 1);
+        double* fz_bot = fzf + ((z - z0) & 1) * S::FZD;
+        double* fz_top = fzf + ((z - z0 + 1) & 1) * S::FZD;
+        // ---- phase A: volume fluxes of this node
+        if (active) {
+          double qv[5], tv[5];
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            qv[c] = cur[le * BLK + c * NN + node] * xs;
+            tv[c] = cur[S::PL + le * BLK + c * NN + node];
+          }
+          const Prim3 tp = prim3_frozen(tv);
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            double fl[5];
+            jac3_apply(tp, d, P.gamma, qv, fl);
+#pragma unroll
+            for (int c = 0; c < 5; ++c) sf[(d * 5 + c) * S::CONS + tid] = fl[c];
+          }
+        }
+        // ---- phase A: every face flux of the plane, once
+        const int total = nfx + nfy + nfz + (z == z0 ? nfz : 0);
+        for (int f = tid; f < total; f += S::CONS) {
+          double qa[5], ta[5], qb[5], tb[5], fl[5];
+          int dir;
+          double* dst;
+          auto from_ring = [&](const double* pl, int e, int nd, double(&qq)[5], double(&tt)[5]) {
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+              qq[c] = pl[e * BLK + c * NN + nd] * xs;
+              tt[c] = pl[S::PL + e * BLK + c * NN + nd];
+            }
+          };
+          auto from_gmem = [&](int gx, int gy, int nd, double(&qq)[5], double(&tt)[5]) {
+            const size_t e = ((size_t)z * ny + gy) * nx + gx;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+              qq[c] = x[(e * 5 + c) * NN + nd] * xs;
+              tt[c] = __ldg(P.ut + (e * 5 + c) * NN + nd);
+            }
+          };
+          if (f < nfx) {  // x-face column fc between tile columns fc - 1 (low) and fc (high)
+            const int fc = f / (ty * NF), rem = f - fc * ty * NF, fy = rem / NF, fn = rem - fy * NF;
+            const int fj = fn % NP, fk = fn / NP;
+            const int nlo = (fk * NP + fj) * NP + N, nhi = (fk * NP + fj) * NP;
+            if (fc == 0) from_gmem(ix0 == 0 ? nx - 1 : ix0 - 1, iy0 + fy, nlo, qa, ta);
+            else from_ring(cur, fy * TX + fc - 1, nlo, qa, ta);
+            if (fc == tx) from_gmem(ix0 + tx == nx ? 0 : ix0 + tx, iy0 + fy, nhi, qb, tb);
+            else from_ring(cur, fy * TX + fc, nhi, qb, tb);
+            dir = 0;
+            dst = fxf + ((fc * TY + fy) * NF + fn) * 5;
+          } else if (f < nfx + nfy) {  // y-face row fc between tile rows fc - 1 and fc
+            const int g = f - nfx, fc = g / (tx * NF), rem = g - fc * tx * NF, fxl = rem / NF, fn = rem - fxl * NF;
+            const int fi = fn % NP, fk = fn / NP;
+            const int nlo = (fk * NP + N) * NP + fi, nhi = (fk * NP) * NP + fi;
+            if (fc == 0) from_gmem(ix0 + fxl, iy0 == 0 ? ny - 1 : iy0 - 1, nlo, qa, ta);
+            else from_ring(cur, (fc - 1) * TX + fxl, nlo, qa, ta);
+            if (fc == ty) from_gmem(ix0 + fxl, iy0 + ty == ny ? 0 : iy0 + ty, nhi, qb, tb);
+            else from_ring(cur, fc * TX + fxl, nhi, qb, tb);
+            dir = 1;
+            dst = fyf + ((fc * TX + fxl) * NF + fn) * 5;
+          } else {  // z-faces: above this plane (ring planes z | z + 1), or below it on the unit's first plane
+            const int g = f - nfx - nfy;
+            const bool top = g < nfz;
+            const int gg = top ? g : g - nfz;
+            const int e = gg / NF, fn = gg - e * NF;
+            const int el = (e / tx) * TX + e % tx;  // ring element index
+            const int nlo = (N * NP) * NP + fn, nhi = fn;
+            from_ring(top ? cur : lo, el, nlo, qa, ta);
+            from_ring(top ? hi : cur, el, nhi, qb, tb);
+            dir = 2;
+            dst = (top ? fz_top : fz_bot) + (el * NF + fn) * 5;
+          }
+          bool bad = false;
+          // a compile-time direction keeps the state arrays in registers (jac3_apply indexes them by dir)
+          if (dir == 0) face3(0, 0, P.gamma, qa, qb, ta, tb, fl, bad);
+          else if (dir == 1) face3(0, 1, P.gamma, qa, qb, ta, tb, fl, bad);
+          else face3(0, 2, P.gamma, qa, qb, ta, tb, fl, bad);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) dst[c] = fl[c];
+        }
+        strip_sync<S::CONS>();  // phase A of plane z complete
+        if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);  // ring plane z - 1 is free
+        // ---- phase C: differentiate, scatter the face fluxes, scale
+        if (active) {
+          const double hz = __ldg(P.hz + z);
+          const double sxv = (0.25 * hy * hz) * P.w[j] * P.w[kk];
+          const double syv = (0.25 * hz * hx) * P.w[i] * P.w[kk];
+          const double szv = (0.25 * hx * hy) * P.w[i] * P.w[j];
+          const int t0 = tid - node;  // this element's first thread
+          double r[5];
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            const double* fx = sf + (0 * 5 + c) * S::CONS + t0 + (kk * NP + j) * NP;
+            const double* fy = sf + (1 * 5 + c) * S::CONS + t0 + kk * NF + i;
+            const double* fzz = sf + (2 * 5 + c) * S::CONS + t0 + j * NP + i;
+            double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+            for (int m = 0; m < NP; ++m) {
+              ax = fma(P.WD[m * NP + i], fx[m], ax);
+              ay = fma(P.WD[m * NP + j], fy[m * NP], ay);
+              az = fma(P.WD[m * NP + kk], fzz[m * NF], az);
+            }
+            r[c] = sxv * ax;
+            r[c] += syv * ay;
+            r[c] += szv * az;
+          }
+          // faces x, y, z (oracle order); owner (low side, node a = N) subtracts
+          if (i == 0 || i == N) {
+            const double* f = fxf + (((lx + (i == N ? 1 : 0)) * TY + ly) * NF + kk * NP + j) * 5;
+            const double fw = (0.25 * (hy * hz)) * P.w[j] * P.w[kk];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) r[c] = i == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
+          }
+          if (j == 0 || j == N) {
+            const double* f = fyf + (((ly + (j == N ? 1 : 0)) * TX + lx) * NF + kk * NP + i) * 5;
+            const double fw = (0.25 * (hx * hz)) * P.w[i] * P.w[kk];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) r[c] = j == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
+          }
+          if (kk == 0 || kk == N) {
+            const double* f = (kk == N ? fz_top : fz_bot) + (le * NF + j * NP + i) * 5;
+            const double fw = (0.25 * (hx * hy)) * P.w[i] * P.w[j];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) r[c] = kk == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
+          }
+          const double im = (8.0 / (hx * hy * hz)) / (P.w[i] * P.w[j] * P.w[kk]);
+          const size_t e = ((size_t)z * ny + iy) * nx + ix;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            const size_t g = (e * 5 + c) * NN + node;
+            double v = r[c] * im;
+            if (b1) v = fma(s_xt[0], cur[2 * S::PL + le * BLK + c * NN + node], v);
+            else v = aug_tail(b, s_xt, g, v);
+            v = dt * v;
+            y[g] = v;
+            nacc = fma(v, v, nacc);
+          }
+        }
+        strip_sync<S::CONS>();  // phase C of plane z complete (sf, face arrays reusable)
+      }
+      if (tid == 0) {
+        mbar_arrive(&empty[(seq + (z1 - z0)) % NBUF]);      // plane z1 - 1
+        mbar_arrive(&empty[(seq + (z1 - z0) + 1) % NBUF]);  // plane z1 (upper halo)
+      }
+      seq += z1 - z0 + 2;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
+    const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
+    y[P.n + tid] = v;
+    if (st->tail_here) nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (tid == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
+}
+
 __global__ void k_e3_freeze(const double* __restrict__ q, long long nelem, int nn, double gamma,
                             double* __restrict__ frozen) {
   const long long nodes = nelem * nn;
@@ -409,6 +718,8 @@ class Euler3D : public OpDevice {
   double* hbuf = nullptr;
   double* halo = nullptr;  // slab partition: x lo/hi, frozen lo/hi, send lo/hi planes
   long long plane = 0;     // doubles per element plane
+  bool use_march = E3March<NP>::OK;  // EXPDG_E3_TILE=1: the element-tile JVP
+  int march_grid = 1;
   ~Euler3D() override {
     cudaFree(frozen);
     cudaFree(hbuf);
@@ -465,6 +776,16 @@ class Euler3D : public OpDevice {
     }
     const long long ntiles = ((long long)d.nx * d.ny * nzl + E3Tile<NP>::TE - 1) / E3Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
+    if (const char* v = std::getenv("EXPDG_E3_TILE")) use_march = use_march && v[0] != '1';
+    if constexpr (E3March<NP>::OK) {
+      using SM = E3March<NP>;
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::SMEM));
+      int per_sm = 1;
+      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_e3_phi_march<NP>, SM::CONS + 32, SM::SMEM));
+      const long long steps =
+          (long long)((d.nx + SM::TX - 1) / SM::TX) * ((d.ny + SM::TY - 1) / SM::TY) * nzl;
+      march_grid = (int)std::max<long long>(1, std::min<long long>(steps, 148LL * std::max(1, per_sm)));
+    }
   }
   void freeze(cudaStream_t s, const double* r) override {
     ref = r;
@@ -475,6 +796,13 @@ class Euler3D : public OpDevice {
     if (P.part) {  // halo planes of the slot this cycle applies the operator to
       launch_pack_slot(s, st, base, plane, (long long)(P.nz - 1) * plane, hb_(4), hb_(5));
       comm->halo(hb_(4), hb_(5), hb_(0), hb_(1), plane, s);
+    }
+    if constexpr (E3March<NP>::OK) {
+      if (use_march) {
+        k_e3_phi_march<NP><<<march_grid, E3March<NP>::CONS + 32, E3March<NP>::SMEM, s>>>(params(frozen), st, base,
+                                                                                        partials, b);
+        return;
+      }
     }
     k_e3_phi<NP><<<grid, 256, 0, s>>>(params(frozen), st, base, partials, b);
   }

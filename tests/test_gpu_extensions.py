@@ -227,3 +227,47 @@ def test_c5_extruded_vortex_converges_at_design_order(ctx):
         hs.append(h)
     order_obs = math.log(errs[0] / errs[1]) / math.log(hs[0] / hs[1])
     assert order_obs >= order + 0.5, (errs, order_obs)
+
+
+# ------------------------------------------------------------------ strip / z-march phi kernels
+def _two_kernels(monkeypatch, env, spec, u0, dt, steps=2, max_basis=30):
+    """EPI2 through the phi-cycle JVP kernel selected by env=0 (strip / z-march) and env=1
+    (the element-tile kernel, whose operator matches the oracle above)."""
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv(env, v)
+        c = pkg.Context(0, fused=False)
+        op = pkg.Operator(c, spec)
+        out.append(pkg.integrate(c, op, to_dev(u0), "epi2", dt, steps * dt, tol=1e-10, max_basis=max_basis,
+                                 orth_length=max_basis))
+    return out
+
+
+@pytest.mark.parametrize("order,nx,ny,periodic,flux", [
+    (4, 40, 3, True, "ef"),    # one full 32-element strip + a partial one
+    (4, 33, 4, False, "lf"),   # Dirichlet ends, a 1-element strip
+    (7, 18, 3, True, "lf"),    # 16-element strips at order 7
+    (2, 5, 6, False, "ef"),
+])
+def test_burgers2d_strip_matches_tile_kernel(monkeypatch, order, nx, ny, periodic, flux):
+    rng = np.random.default_rng(7 * nx + order)
+    spec = pkg.OperatorSpec("burgers2d", order, nx, ny, box=(0, 1, 0, 2, 0, 1), periodic=periodic, kappa=1e-2,
+                            flux=flux, sigma=1e-3 if flux == "ef" else 0.0)
+    u0 = 0.5 + 0.1 * rng.standard_normal(nx * ny * (order + 1) ** 2)
+    a, b = _two_kernels(monkeypatch, "EXPDG_B2_TILE", spec, u0, 1e-3)
+    assert a.status == b.status == "completed"
+    assert rel(to_host(a.u), to_host(b.u)) <= 1e-12
+    assert list(a.iters_per_step) == list(b.iters_per_step)
+
+
+@pytest.mark.parametrize("order,dims", [(3, (3, 5, 4)), (3, (4, 4, 1)), (1, (5, 9, 3)), (1, (4, 8, 2))])
+def test_euler3d_march_matches_tile_kernel(monkeypatch, order, dims):
+    # odd meshes leave partial 2x2 (order 3) / 4x8 (order 1) tiles; nz = 1 wraps onto itself
+    rng = np.random.default_rng(order + sum(dims))
+    nx, ny, nz = dims
+    spec = pkg.OperatorSpec("euler3d", order, nx, ny, nz, box=(0, 1, 0, 2, 0, 1.5), euler_flux="lf")
+    u0 = random_state5(rng, nx * ny * nz, (order + 1) ** 3)
+    a, b = _two_kernels(monkeypatch, "EXPDG_E3_TILE", spec, u0, 2e-3)
+    assert a.status == b.status == "completed"
+    assert rel(to_host(a.u), to_host(b.u)) <= 1e-12
+    assert list(a.iters_per_step) == list(b.iters_per_step)
