@@ -27,6 +27,9 @@ struct E3P {
   const double* hx;
   const double* hy;
   const double* hz;
+  const double* ihx;  // 1 / h tables (the z-march kernel multiplies instead of dividing)
+  const double* ihy;
+  const double* ihz;
   long long n;
   // z-slab partition: planes -1 and nz are the neighbours' halo planes (raw values of the
   // applied vector / the frozen primitives), exchanged before the kernel runs
@@ -386,7 +389,7 @@ __global__ void __launch_bounds__(256) k_e3_phi(E3P<NP> P, PhiState* st, double*
 }
 
 // ---------------------------------------------------------------- z-march JVP (phi cycle)
-// A CTA owns a TX x TY tile of element columns and marches up a contiguous range of
+// A CTA owns a TX x TY tile of element columns at a time and marches up all its
 // z-planes.  Warp CW streams the tile's elements of every plane (x = slot j, the frozen
 // primitives, b_1) by 1D TMA bulk copies into a 4-plane shared-memory ring, so every
 // byte of x and q~ leaves HBM once per JVP; only the face nodes of the x/y neighbour
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(256) k_e3_phi(E3P<NP> P, PhiState* st, double*
 template <int NP>
 struct E3March {
   static constexpr int NN = NP * NP * NP, NF = NP * NP, BLK = 5 * NN;
-  static constexpr int TX = NP == 4 ? 2 : 4, TY = NP == 4 ? 2 : 8;  // TX * TY * NN = 256
+  static constexpr int TX = NP == 4 ? 2 : 4, TY = NP == 4 ? 2 : 8;  // TX * TY * NN = 256 (1x2 tiles at two CTAs per SM measured slower)
   static constexpr int TE = TX * TY;
   static constexpr int CONS = TE * NN;
   static constexpr int CW = CONS / 32;
@@ -456,16 +459,15 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
   const double xs = s_xs, dt = s_dt;
   const int nx = P.nx, ny = P.ny, nz = P.nz;
   const int ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
-  const long long steps = (long long)ntx * nty * nz;
-  const long long k0 = steps * blockIdx.x / gridDim.x, k1 = steps * (blockIdx.x + 1) / gridDim.x;
+  // CTA c marches tiles c, c + G, c + 2G, ... over the whole z range: at any time the G
+  // CTAs work on G consecutive tiles at similar z, so the x/y neighbour faces they gather
+  // were staged by a neighbouring CTA moments before and come from L2
+  const long long ntiles = (long long)ntx * nty;
   const double* b1 = (b.p == 1) ? b.b[1] : nullptr;
   double nacc = 0.0;
-  // unit: consecutive planes [z0, z1) of one tile
-  auto unit = [&](long long& k, int& ix0, int& iy0, int& tx, int& ty, int& z0, int& z1) {
-    const long long tile = k / nz;
-    z0 = (int)(k - tile * nz);
-    z1 = (int)min((long long)nz, z0 + (k1 - k));
-    k += z1 - z0;
+  auto unit = [&](long long tile, int& ix0, int& iy0, int& tx, int& ty, int& z0, int& z1) {
+    z0 = 0;
+    z1 = nz;
     ix0 = (int)(tile % ntx) * TX;
     iy0 = (int)(tile / ntx) * TY;
     tx = min(TX, nx - ix0);
@@ -476,9 +478,9 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
     // ---------------- producer: the tile's elements of planes z0 - 1 .. z1
     if (lane == 0) {
       long long seq = 0;
-      for (long long k = k0; k < k1;) {
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int ix0, iy0, tx, ty, z0, z1;
-        unit(k, ix0, iy0, tx, ty, z0, z1);
+        unit(tile, ix0, iy0, tx, ty, z0, z1);
         for (int q = 0; q < z1 - z0 + 2; ++q, ++seq) {
           int z = z0 - 1 + q;
           const double* srcx = x;
@@ -515,16 +517,30 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
     const int le = tid / NN, node = tid % NN;
     const int lx = le % TX, ly = le / TX;
     const int i = node % NP, j = (node / NP) % NP, kk = node / NF;
+    // per-thread basis constants in registers (runtime indices into the kernel parameter
+    // arrays would be indexed constant-bank loads in the inner loops)
+    double wdi[NP], wdj[NP], wdk[NP];
+#pragma unroll
+    for (int m = 0; m < NP; ++m) {
+      wdi[m] = P.WD[m * NP + i];
+      wdj[m] = P.WD[m * NP + j];
+      wdk[m] = P.WD[m * NP + kk];
+    }
+    const double wi = P.w[i], wj = P.w[j], wk = P.w[kk];
+    const double iw3 = 1.0 / (wi * wj * wk);
     long long seq = 0;
-    for (long long k = k0; k < k1;) {
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       int ix0, iy0, tx, ty, z0, z1;
-      unit(k, ix0, iy0, tx, ty, z0, z1);
+      unit(tile, ix0, iy0, tx, ty, z0, z1);
       const bool active = lx < tx && ly < ty;
       const int ix = ix0 + lx, iy = iy0 + ly;
       const double hx = active ? __ldg(P.hx + ix) : 1.0, hy = active ? __ldg(P.hy + iy) : 1.0;
+      const double ihxy = active ? __ldg(P.ihx + ix) * __ldg(P.ihy + iy) : 1.0;
       auto slot = [&](long long q) { return ring + (size_t)((seq + q) % NBUF) * S::BUFD; };
       auto wait_plane = [&](long long q) { mbar_wait(&full[(seq + q) % NBUF], (int)(((seq + q) / NBUF) & 1)); };
-      const int nfx = (tx + 1) * ty * NF, nfy = tx * (ty + 1) * NF, nfz = tx * ty * NF;
+      // faces are enumerated over the full TX x TY tile (compile-time divisors); the ones
+      // outside a partial tile are skipped
+      constexpr int NFX = (TX + 1) * TY * NF, NFY = TX * (TY + 1) * NF, NFZ = TX * TY * NF;
       wait_plane(0);
       wait_plane(1);
       for (int z = z0; z < z1; ++z) {
@@ -535,7 +551,78 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
         const double* hi = slot(q + 1);
         double* fz_bot = fzf + ((z - z0) & 1) * S::FZD;
         double* fz_top = fzf + ((z - z0 + 1) & 1) * S::FZD;
-        // ---- phase A: volume fluxes of this node
+        // ---- phase A.  The operands of this thread's first face flux are gathered first, so
+        // the L2 latency of the x/y neighbour faces overlaps the volume arithmetic.
+        const int total = NFX + NFY + NFZ + (z == z0 ? NFZ : 0);
+        auto from_ring = [&](const double* pl, int e, int nd, double(&qq)[5], double(&tt)[5]) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            qq[c] = pl[e * BLK + c * NN + nd] * xs;
+            tt[c] = pl[S::PL + e * BLK + c * NN + nd];
+          }
+        };
+        auto from_gmem = [&](int gx, int gy, int nd, double(&qq)[5], double(&tt)[5]) {
+          const size_t e = ((size_t)z * ny + gy) * nx + gx;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            qq[c] = x[(e * 5 + c) * NN + nd] * xs;
+            tt[c] = __ldg(P.ut + (e * 5 + c) * NN + nd);
+          }
+        };
+        // operands of face f (false: outside a partial tile)
+        auto load_face = [&](int f, double(&qa)[5], double(&ta)[5], double(&qb)[5], double(&tb)[5], int& dir,
+                             double*& dst) {
+          if (f < NFX) {  // x-face column fc between tile columns fc - 1 (low) and fc (high)
+            const int fc = f / (TY * NF), rem = f - fc * TY * NF, fy = rem / NF, fn = rem - fy * NF;
+            if (fc > tx || fy >= ty) return false;
+            const int nlo = fn * NP + N, nhi = fn * NP;  // fn = k NP + j
+            if (fc == 0) from_gmem(ix0 == 0 ? nx - 1 : ix0 - 1, iy0 + fy, nlo, qa, ta);
+            else from_ring(cur, fy * TX + fc - 1, nlo, qa, ta);
+            if (fc == tx) from_gmem(ix0 + tx == nx ? 0 : ix0 + tx, iy0 + fy, nhi, qb, tb);
+            else from_ring(cur, fy * TX + fc, nhi, qb, tb);
+            dir = 0;
+            dst = fxf + ((fc * TY + fy) * NF + fn) * 5;
+          } else if (f < NFX + NFY) {  // y-face row fc between tile rows fc - 1 and fc
+            const int g = f - NFX, fc = g / (TX * NF), rem = g - fc * TX * NF, fxl = rem / NF, fn = rem - fxl * NF;
+            if (fc > ty || fxl >= tx) return false;
+            const int fi = fn % NP, fk = fn / NP;
+            const int nlo = (fk * NP + N) * NP + fi, nhi = (fk * NP) * NP + fi;
+            if (fc == 0) from_gmem(ix0 + fxl, iy0 == 0 ? ny - 1 : iy0 - 1, nlo, qa, ta);
+            else from_ring(cur, (fc - 1) * TX + fxl, nlo, qa, ta);
+            if (fc == ty) from_gmem(ix0 + fxl, iy0 + ty == ny ? 0 : iy0 + ty, nhi, qb, tb);
+            else from_ring(cur, fc * TX + fxl, nhi, qb, tb);
+            dir = 1;
+            dst = fyf + ((fc * TX + fxl) * NF + fn) * 5;
+          } else {  // z-faces: above this plane (ring planes z | z + 1), or below it on the unit's first plane
+            const int g = f - NFX - NFY;
+            const bool top = g < NFZ;
+            const int gg = top ? g : g - NFZ;
+            const int el = gg / NF, fn = gg - el * NF;  // ring element index
+            if (el % TX >= tx || el / TX >= ty) return false;
+            const int nlo = (N * NP) * NP + fn, nhi = fn;
+            from_ring(top ? cur : lo, el, nlo, qa, ta);
+            from_ring(top ? hi : cur, el, nhi, qb, tb);
+            dir = 2;
+            dst = (top ? fz_top : fz_bot) + (el * NF + fn) * 5;
+          }
+          return true;
+        };
+        auto face_out = [&](int dir, const double(&qa)[5], const double(&ta)[5], const double(&qb)[5],
+                            const double(&tb)[5], double* dst) {
+          double fl[5];
+          bool bad = false;
+          // a compile-time direction keeps the state arrays in registers (jac3_apply indexes them by dir)
+          if (dir == 0) face3(0, 0, P.gamma, qa, qb, ta, tb, fl, bad);
+          else if (dir == 1) face3(0, 1, P.gamma, qa, qb, ta, tb, fl, bad);
+          else face3(0, 2, P.gamma, qa, qb, ta, tb, fl, bad);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) dst[c] = fl[c];
+        };
+        double qa[5], ta[5], qb[5], tb[5];
+        int dir0 = 0;
+        double* dst0 = nullptr;
+        const bool has0 = tid < total && load_face(tid, qa, ta, qb, tb, dir0, dst0);
+        // volume fluxes of this node
         if (active) {
           double qv[5], tv[5];
 #pragma unroll
@@ -552,75 +639,21 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
             for (int c = 0; c < 5; ++c) sf[(d * 5 + c) * S::CONS + tid] = fl[c];
           }
         }
-        // ---- phase A: every face flux of the plane, once
-        const int total = nfx + nfy + nfz + (z == z0 ? nfz : 0);
-        for (int f = tid; f < total; f += S::CONS) {
-          double qa[5], ta[5], qb[5], tb[5], fl[5];
+        // every face flux of the plane, once
+        if (has0) face_out(dir0, qa, ta, qb, tb, dst0);
+        for (int f = tid + S::CONS; f < total; f += S::CONS) {
           int dir;
           double* dst;
-          auto from_ring = [&](const double* pl, int e, int nd, double(&qq)[5], double(&tt)[5]) {
-#pragma unroll
-            for (int c = 0; c < 5; ++c) {
-              qq[c] = pl[e * BLK + c * NN + nd] * xs;
-              tt[c] = pl[S::PL + e * BLK + c * NN + nd];
-            }
-          };
-          auto from_gmem = [&](int gx, int gy, int nd, double(&qq)[5], double(&tt)[5]) {
-            const size_t e = ((size_t)z * ny + gy) * nx + gx;
-#pragma unroll
-            for (int c = 0; c < 5; ++c) {
-              qq[c] = x[(e * 5 + c) * NN + nd] * xs;
-              tt[c] = __ldg(P.ut + (e * 5 + c) * NN + nd);
-            }
-          };
-          if (f < nfx) {  // x-face column fc between tile columns fc - 1 (low) and fc (high)
-            const int fc = f / (ty * NF), rem = f - fc * ty * NF, fy = rem / NF, fn = rem - fy * NF;
-            const int fj = fn % NP, fk = fn / NP;
-            const int nlo = (fk * NP + fj) * NP + N, nhi = (fk * NP + fj) * NP;
-            if (fc == 0) from_gmem(ix0 == 0 ? nx - 1 : ix0 - 1, iy0 + fy, nlo, qa, ta);
-            else from_ring(cur, fy * TX + fc - 1, nlo, qa, ta);
-            if (fc == tx) from_gmem(ix0 + tx == nx ? 0 : ix0 + tx, iy0 + fy, nhi, qb, tb);
-            else from_ring(cur, fy * TX + fc, nhi, qb, tb);
-            dir = 0;
-            dst = fxf + ((fc * TY + fy) * NF + fn) * 5;
-          } else if (f < nfx + nfy) {  // y-face row fc between tile rows fc - 1 and fc
-            const int g = f - nfx, fc = g / (tx * NF), rem = g - fc * tx * NF, fxl = rem / NF, fn = rem - fxl * NF;
-            const int fi = fn % NP, fk = fn / NP;
-            const int nlo = (fk * NP + N) * NP + fi, nhi = (fk * NP) * NP + fi;
-            if (fc == 0) from_gmem(ix0 + fxl, iy0 == 0 ? ny - 1 : iy0 - 1, nlo, qa, ta);
-            else from_ring(cur, (fc - 1) * TX + fxl, nlo, qa, ta);
-            if (fc == ty) from_gmem(ix0 + fxl, iy0 + ty == ny ? 0 : iy0 + ty, nhi, qb, tb);
-            else from_ring(cur, fc * TX + fxl, nhi, qb, tb);
-            dir = 1;
-            dst = fyf + ((fc * TX + fxl) * NF + fn) * 5;
-          } else {  // z-faces: above this plane (ring planes z | z + 1), or below it on the unit's first plane
-            const int g = f - nfx - nfy;
-            const bool top = g < nfz;
-            const int gg = top ? g : g - nfz;
-            const int e = gg / NF, fn = gg - e * NF;
-            const int el = (e / tx) * TX + e % tx;  // ring element index
-            const int nlo = (N * NP) * NP + fn, nhi = fn;
-            from_ring(top ? cur : lo, el, nlo, qa, ta);
-            from_ring(top ? hi : cur, el, nhi, qb, tb);
-            dir = 2;
-            dst = (top ? fz_top : fz_bot) + (el * NF + fn) * 5;
-          }
-          bool bad = false;
-          // a compile-time direction keeps the state arrays in registers (jac3_apply indexes them by dir)
-          if (dir == 0) face3(0, 0, P.gamma, qa, qb, ta, tb, fl, bad);
-          else if (dir == 1) face3(0, 1, P.gamma, qa, qb, ta, tb, fl, bad);
-          else face3(0, 2, P.gamma, qa, qb, ta, tb, fl, bad);
-#pragma unroll
-          for (int c = 0; c < 5; ++c) dst[c] = fl[c];
+          if (load_face(f, qa, ta, qb, tb, dir, dst)) face_out(dir, qa, ta, qb, tb, dst);
         }
         strip_sync<S::CONS>();  // phase A of plane z complete
         if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);  // ring plane z - 1 is free
         // ---- phase C: differentiate, scatter the face fluxes, scale
         if (active) {
           const double hz = __ldg(P.hz + z);
-          const double sxv = (0.25 * hy * hz) * P.w[j] * P.w[kk];
-          const double syv = (0.25 * hz * hx) * P.w[i] * P.w[kk];
-          const double szv = (0.25 * hx * hy) * P.w[i] * P.w[j];
+          const double sxv = (0.25 * hy * hz) * wj * wk;
+          const double syv = (0.25 * hz * hx) * wi * wk;
+          const double szv = (0.25 * hx * hy) * wi * wj;
           const int t0 = tid - node;  // this element's first thread
           double r[5];
 #pragma unroll
@@ -631,9 +664,9 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
             double ax = 0.0, ay = 0.0, az = 0.0;
 #pragma unroll
             for (int m = 0; m < NP; ++m) {
-              ax = fma(P.WD[m * NP + i], fx[m], ax);
-              ay = fma(P.WD[m * NP + j], fy[m * NP], ay);
-              az = fma(P.WD[m * NP + kk], fzz[m * NF], az);
+              ax = fma(wdi[m], fx[m], ax);
+              ay = fma(wdj[m], fy[m * NP], ay);
+              az = fma(wdk[m], fzz[m * NF], az);
             }
             r[c] = sxv * ax;
             r[c] += syv * ay;
@@ -642,23 +675,23 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
           // faces x, y, z (oracle order); owner (low side, node a = N) subtracts
           if (i == 0 || i == N) {
             const double* f = fxf + (((lx + (i == N ? 1 : 0)) * TY + ly) * NF + kk * NP + j) * 5;
-            const double fw = (0.25 * (hy * hz)) * P.w[j] * P.w[kk];
+            const double fw = (0.25 * (hy * hz)) * wj * wk;
 #pragma unroll
             for (int c = 0; c < 5; ++c) r[c] = i == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
           }
           if (j == 0 || j == N) {
             const double* f = fyf + (((ly + (j == N ? 1 : 0)) * TX + lx) * NF + kk * NP + i) * 5;
-            const double fw = (0.25 * (hx * hz)) * P.w[i] * P.w[kk];
+            const double fw = (0.25 * (hx * hz)) * wi * wk;
 #pragma unroll
             for (int c = 0; c < 5; ++c) r[c] = j == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
           }
           if (kk == 0 || kk == N) {
             const double* f = (kk == N ? fz_top : fz_bot) + (le * NF + j * NP + i) * 5;
-            const double fw = (0.25 * (hx * hy)) * P.w[i] * P.w[j];
+            const double fw = (0.25 * (hx * hy)) * wi * wj;
 #pragma unroll
             for (int c = 0; c < 5; ++c) r[c] = kk == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
           }
-          const double im = (8.0 / (hx * hy * hz)) / (P.w[i] * P.w[j] * P.w[kk]);
+          const double im = (8.0 * ihxy * __ldg(P.ihz + z)) * iw3;  // 8 / (hx hy hz w_i w_j w_k)
           const size_t e = ((size_t)z * ny + iy) * nx + ix;
 #pragma unroll
           for (int c = 0; c < 5; ++c) {
@@ -751,16 +784,22 @@ class Euler3D : public OpDevice {
     P.nz = nzl;
     P.part = part ? 1 : 0;
     P.gamma = d.gamma;
-    std::vector<double> hs(d.nx + d.ny + nzl);
+    std::vector<double> hs(2 * (d.nx + d.ny + nzl));
     for (int i = 0; i < d.nx; ++i) hs[i] = ub3(d.x0, d.x1, i + 1, d.nx) - ub3(d.x0, d.x1, i, d.nx);
     for (int j = 0; j < d.ny; ++j) hs[d.nx + j] = ub3(d.y0, d.y1, j + 1, d.ny) - ub3(d.y0, d.y1, j, d.ny);
     for (int k = 0; k < nzl; ++k)
       hs[d.nx + d.ny + k] = ub3(d.z0, d.z1, z0 + k + 1, d.nz) - ub3(d.z0, d.z1, z0 + k, d.nz);
     EXPDG_CUDA(cudaMalloc(&hbuf, sizeof(double) * hs.size()));
     EXPDG_CUDA(cudaMemcpy(hbuf, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice));
+    const int nh = d.nx + d.ny + nzl;
+    for (int q = 0; q < nh; ++q) hs[nh + q] = 1.0 / hs[q];
+    EXPDG_CUDA(cudaMemcpy(hbuf, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice));
     P.hx = hbuf;
     P.hy = hbuf + d.nx;
     P.hz = hbuf + d.nx + d.ny;
+    P.ihx = hbuf + nh;
+    P.ihy = hbuf + nh + d.nx;
+    P.ihz = hbuf + nh + d.nx + d.ny;
     for (int a = 0; a < NP; ++a) {
       P.w[a] = hb.weights[a];
       for (int b2 = 0; b2 < NP; ++b2) P.WD[a * NP + b2] = hb.weights[a] * hb.D[a * NP + b2];
@@ -782,9 +821,8 @@ class Euler3D : public OpDevice {
       EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::SMEM));
       int per_sm = 1;
       EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_e3_phi_march<NP>, SM::CONS + 32, SM::SMEM));
-      const long long steps =
-          (long long)((d.nx + SM::TX - 1) / SM::TX) * ((d.ny + SM::TY - 1) / SM::TY) * nzl;
-      march_grid = (int)std::max<long long>(1, std::min<long long>(steps, 148LL * std::max(1, per_sm)));
+      const long long tiles = (long long)((d.nx + SM::TX - 1) / SM::TX) * ((d.ny + SM::TY - 1) / SM::TY);
+      march_grid = (int)std::max<long long>(1, std::min<long long>(tiles, 148LL * std::max(1, per_sm)));
     }
   }
   void freeze(cudaStream_t s, const double* r) override {
