@@ -491,7 +491,9 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
 // from HBM, and the JVP arithmetic runs under the V stream instead of before it.
 // The V ring takes what shared memory the JVP leaves (single-buffered volume
 // fluxes in this variant, one more CTA barrier per row).
-constexpr int kE2DotJ = 44;  // the sweep takes the dots of columns j < 44 (max_basis <= 43 skips k_ts2 dots)
+// the sweep takes the dots of columns j < 34; beyond, the separate dots pass is faster
+// (tools/fusedbench.py at C4 size: fused 5.11 vs 5.18 ms at j = 32, 5.69 vs 5.59 at j = 36)
+constexpr int kE2DotJ = 34;
 
 template <int NP, int CW, bool DOT>
 struct E2Strip {
