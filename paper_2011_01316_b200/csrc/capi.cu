@@ -382,10 +382,12 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
     BArgs b{};
     b.p = p;
     for (int i = 0; i <= p; ++i) b.b[i] = b_dev[i];
+    const long long bl0 = e.body_launches;
     e.run_phi(*op->dev, b, use_graph_default() ? 1 : 0);
     EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
     const PhiState& s = *e.st_host;
-    ctx->launches += 2 + s.body_runs * Engine::body_kernels(*op->dev, s.dcgs != 0, s.mmax);
+    const long long hosted = e.body_launches - bl0;  // host-stepped cycles count their launches
+    ctx->launches += 2 + (hosted > 0 ? hosted : s.body_runs * Engine::body_kernels(*op->dev, s.dcgs != 0, s.mmax));
     if (stats) {
       stats->iterations = s.iterations;
       stats->substeps = s.substeps;
@@ -590,11 +592,15 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     EXPDG_CUDA(cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies));
     return cp.conditional.phGraph_out[0];
   };
+  const long long bl0 = e.body_launches;
   auto host_loop = [&](const BArgs& b, bool dcgs, int mmax) {
+    int hact = -1, hj = -1;  // the first cycle after phi init: unknown, launch every kernel
     for (long long cyc = 0;; ++cyc) {
-      e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0, dcgs, mmax);
-      e.fetch_control(e.stream);  // action + stopped only (8 bytes, not the whole PhiState)
+      e.launch_body(e.stream, dev, b, cudaGraphConditionalHandle{}, 0, dcgs, mmax, hact, hj);
+      e.fetch_control(e.stream);  // action, phase, j + stopped only (not the whole PhiState)
       if (e.st_host->action == ACT_DONE || e.st_host->action == ACT_NONE || e.st_host->stopped) break;
+      hact = e.st_host->action;
+      hj = e.st_host->j;
       if (cyc > 10000000) throw CudaError("host-stepped phi did not terminate");
     }
   };
@@ -689,7 +695,8 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   restore_ref(dev, e.stream, saved_ref);
   EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
   const PhiState st = *e.st_host;
-  ctx->launches += (long long)launched * per_step + (fused ? 0 : st.body_runs * body_k);
+  ctx->launches += (long long)launched * per_step +
+                   (fused ? 0 : (graph ? st.body_runs * body_k : e.body_launches - bl0));
   std::vector<StepRecord> rec(std::max(1, st.step));
   if (st.step > 0)
     EXPDG_CUDA(cudaMemcpy(rec.data(), rec_dev, sizeof(StepRecord) * st.step, cudaMemcpyDeviceToHost));

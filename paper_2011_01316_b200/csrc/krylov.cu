@@ -520,7 +520,22 @@ int Engine::body_kernels(const OpDevice& op, bool dcgs, int mmax) {
 }
 
 void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
-                         int use_graph, bool dcgs, int mmax) {
+                         int use_graph, bool dcgs, int mmax, int hact, int hj) {
+  // which kernels can do work this cycle (each no-ops on the device otherwise)
+  const bool known = hact >= 0 && !use_graph;
+  const bool ext = !known || hact == ACT_EXTEND || hact == ACT_AVNORM;
+  const bool ext_cgs = !known || hact == ACT_EXTEND;  // CGS2 / IOP passes skip the avnorm cycle
+  const bool comb = !known || hact == ACT_COMBINE;
+  const long long pack = op.partitioned() ? 1 : 0;  // the halo pack kernel of a slab apply
+  // graph capture records the body once: its launches are counted per body run instead
+  struct Uncount {
+    long long& c;
+    long long v;
+    bool on;
+    ~Uncount() {
+      if (on) c = v;
+    }
+  } uncount{body_launches, body_launches, use_graph != 0};
   auto timed = [&](int kind, auto&& launch) {
     if (time_kind != kind || use_graph) {
       launch();
@@ -537,33 +552,53 @@ void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraph
     EXPDG_CUDA(cudaEventRecord(upd_events[upd_used + 1], s));
     upd_used += 2;
   };
-  timed(2, [&] { op.launch_phi_apply(s, st, base, partials, b); });
-  reduce(s);
+  if (ext) {
+    timed(2, [&] { op.launch_phi_apply(s, st, base, partials, b); });
+    reduce(s);
+    body_launches += 1 + pack;
+  }
   if (dcgs) {  // one dots pass + coefficients + one update pass (dcgs.cu)
     const int fj = op.fused_dcgs_dots_jmax();
-    if (!(mmax >= 0 && fj >= mmax)) {  // some column's dots are not taken by the operator kernel
-      launch_dcgs(s, *this, 0, fj);
+    if (ext) {
+      // the dots pass, unless the operator kernel takes the dots of every column (or of this one)
+      if (!(mmax >= 0 && fj >= mmax) && !(known && hj <= fj)) {
+        launch_dcgs(s, *this, 0, fj);
+        reduce(s);
+        ++body_launches;
+      }
+      launch_dcgs(s, *this, 1);
+      timed(1, [&] { launch_dcgs(s, *this, 2); });
       reduce(s);
+      body_launches += 2;
     }
-    launch_dcgs(s, *this, 1);
-    timed(1, [&] { launch_dcgs(s, *this, 2); });
-    reduce(s);
-    launch_ts(s, TS_COMBINE);
-    reduce(s);
+    if (comb) {
+      launch_ts(s, TS_COMBINE);
+      reduce(s);
+      ++body_launches;
+    }
     k_ctl<<<1, 256, 0, s>>>(st, slot(0), ework, h, use_graph);
+    ++body_launches;
     return;
   }
-  if (!op.fused_dots()) {
-    launch_ts(s, TS_DOTS);
+  if (ext_cgs) {
+    if (!op.fused_dots()) {
+      launch_ts(s, TS_DOTS);
+      reduce(s);
+      ++body_launches;
+    }
+    launch_ts(s, TS_UPD_DOTS);
     reduce(s);
+    launch_ts(s, TS_UPD_NORM);
+    reduce(s);
+    body_launches += 2;
   }
-  launch_ts(s, TS_UPD_DOTS);
-  reduce(s);
-  launch_ts(s, TS_UPD_NORM);
-  reduce(s);
-  launch_ts(s, TS_COMBINE);
-  reduce(s);
+  if (comb) {
+    launch_ts(s, TS_COMBINE);
+    reduce(s);
+    ++body_launches;
+  }
   k_ctl<<<1, 256, 0, s>>>(st, slot(0), ework, h, use_graph);
+  ++body_launches;
 }
 
 // Micro-benchmark of one tall-skinny pass at column k-1 (diagnostics / tuning).
@@ -618,7 +653,8 @@ double Engine::upd_ms() const {
 }
 
 void Engine::fetch_control(cudaStream_t s) {
-  EXPDG_CUDA(cudaMemcpyAsync(&st_host->action, &st->action, sizeof(int), cudaMemcpyDeviceToHost, s));
+  // action, phase, j are consecutive ints of PhiState
+  EXPDG_CUDA(cudaMemcpyAsync(&st_host->action, &st->action, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
   EXPDG_CUDA(cudaMemcpyAsync(&st_host->stopped, &st->stopped, sizeof(int), cudaMemcpyDeviceToHost, s));
   EXPDG_CUDA(cudaStreamSynchronize(s));
 }
@@ -642,10 +678,15 @@ void Engine::run_phi(OpDevice& op, const BArgs& b, int use_graph) {
     return;
   }
   launch_phi_init(stream, b);
+  const bool dcgs = st_host->dcgs != 0;
+  const int mmax = st_host->mmax;
+  int hact = -1, hj = -1;
   for (int cyc = 0; cyc < 1000000; ++cyc) {
-    launch_body(stream, op, b, cudaGraphConditionalHandle{}, 0, st_host->dcgs != 0, st_host->mmax);
+    launch_body(stream, op, b, cudaGraphConditionalHandle{}, 0, dcgs, mmax, hact, hj);
     fetch_control(stream);
     if (st_host->action == ACT_DONE || st_host->action == ACT_NONE || st_host->stopped) return;
+    hact = st_host->action;
+    hj = st_host->j;
   }
   throw std::runtime_error("phi host loop did not terminate");
 }

@@ -110,7 +110,7 @@ class Engine {
   size_t upd_used = 0;
   double upd_ms() const;
   bool fused_ok(const OpDevice& op) const;
-  void fetch_control(cudaStream_t s);  // host-stepped loops: action / stopped to st_host
+  void fetch_control(cudaStream_t s);  // host-stepped loops: action, phase, j and stopped to st_host
   // Set when the context belongs to a slab-partitioned group: every reducing
   // kernel is followed by a sum-allreduce of PhiState::loc -> PhiState::red,
   // and the control runs host-stepped (no CUDA graphs).
@@ -150,8 +150,12 @@ class Engine {
   double bench_ts(long long n, int k, int mode, int reps);
   // mmax: the phi call's basis bound (decides whether the DCGS2 dots pass can be left
   // out entirely because the operator kernel takes the dots of every column)
+  // hact / hj: the action and column of this cycle when the host knows them (host-stepped
+  // loops read them back after every cycle, fetch_control): kernels that would no-op are
+  // not launched, and neither are their allreduces (slab-partitioned runs); -1: unknown
   void launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraphConditionalHandle h,
-                   int use_graph, bool dcgs, int mmax);
+                   int use_graph, bool dcgs, int mmax, int hact = -1, int hj = -1);
+  long long body_launches = 0;  // kernels launch_body enqueued (host-stepped launch accounting)
   // kernels one launch_body enqueues
   static int body_kernels(const OpDevice& op, bool dcgs, int mmax);
   // Runs one phi call to completion; host-stepped or graph-driven control.
