@@ -137,3 +137,24 @@ def test_euler_fused_dots_match_dots_pass(monkeypatch, max_basis, flux):
     assert np.abs(ha - hb).max() <= 1e-12 * np.abs(hb).max()
     # the sweep really took the dots: u and w are not re-read (16 n bytes less per column)
     assert a.alg_bytes < b.alg_bytes
+
+
+@pytest.mark.parametrize("orth", ["dcgs2", "cgs2"])
+def test_host_stepped_cycles_match_graph(orth):
+    # host-stepped loops launch only the kernels that do work in a cycle (the host reads back
+    # the next action and column); the graph launches every kernel and lets them no-op.  Both
+    # must give the same bits; max_basis 64 crosses the fused-dots bound (columns j > 33)
+    w = configs.scaled(configs.C4, 24, steps=2)
+    u0 = w.initial_condition()
+    dt = 2 * w.time_step(u0)
+    out = []
+    for graph in (True, False):
+        ctx = pkg.Context(0, orth=orth, fused=False)
+        op = pkg.Operator(ctx, w.spec())
+        out.append(pkg.integrate(ctx, op, to_dev(u0), "epi2", dt, w.steps * dt, tol=1e-12, max_basis=64,
+                                 orth_length=64, use_graph=graph))
+    a, b = out
+    assert a.status == b.status == "completed"
+    assert np.array_equal(to_host(a.u), to_host(b.u))
+    assert list(a.iters_per_step) == list(b.iters_per_step)
+    assert max(np.diff(np.concatenate([[0], a.iters_per_step]))) > 34  # columns past the fused bound
