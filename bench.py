@@ -127,10 +127,13 @@ def _ref_worker(a):
     return cpu_sample(w, steps=steps, nx=nx, warmup=warmup)
 
 
+SPEC_HBM_GBPS = 8000.0  # B200 HBM3e spec (the north star's "~8 TB/s"); `peak` is the measured copy bandwidth
+
+
 def roofline(dominant, step_achieved, peak, peak_kind, traffic, steps):
     """Roofline of the dominant kernel (live CUDA-event timing of its launches) plus the
     whole step's algorithmic bandwidth."""
-    step = {"achieved": step_achieved, "frac": step_achieved / peak,
+    step = {"achieved": step_achieved, "frac": step_achieved / peak, "frac_spec": step_achieved / SPEC_HBM_GBPS,
             "what": "phi engine (JVP + DCGS2 passes + combine + controller): algorithmic bytes of the realised "
                     "trajectory (DCGS2: JVP 32n + 8n(2k+6) per column; SURVEY's CGS2 count is 8n(3k+6)) / "
                     "step-loop time",
@@ -150,6 +153,7 @@ def roofline(dominant, step_achieved, peak, peak_kind, traffic, steps):
     except Exception:
         pass
     out = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+           "frac_spec": ach / SPEC_HBM_GBPS,
            "traffic": traffic_launch, "kernel": dominant["kernel"],
            "alg_bytes_per_launch": per_launch_bytes, "launch_ms": dominant["ms"] / dominant["launches"],
            "launches": dominant["launches"], "peak_kind": peak_kind,
