@@ -210,9 +210,15 @@ static __device__ int dcgs_finish(PhiState* st) {
   // (dots_fused) u and w are not re-read: 32n + 8n j + 8n(j + 4)
   st->alg_bytes += 32.0 * nd + 8.0 * nd * (2.0 * j + (st->dots_fused ? 4.0 : 6.0));
   double beta = 1.0;
+  // distinct PhiState arrays: restrict lets the loads of the loops below be issued ahead
+  double* __restrict__ Hm = st->H;
+  const double* __restrict__ da = st->dc_a;
+  const double* __restrict__ db = st->dc_b;
+  const double* __restrict__ dg = st->dc_g;
   if (j >= 1) {
     beta = st->scale[j] * sqrt(st->red.nrmU);
-    for (int l = 0; l < j; ++l) st->H[l * kMaxBasis + (j - 1)] += st->dc_a[l];
+#pragma unroll 4
+    for (int l = 0; l < j; ++l) Hm[l * kMaxBasis + (j - 1)] += da[l];
     if (beta <= 1e-14 * fmax(st->pre_prev, 1e-300)) {
       st->H[j * kMaxBasis + (j - 1)] = 0.0;
       st->mc = j;
@@ -227,9 +233,10 @@ static __device__ int dcgs_finish(PhiState* st) {
   // use: the space cannot grow past mmax
   const bool store = j < kMaxBasis;
   double hh = 0.0;
+#pragma unroll 4
   for (int l = 0; l < j; ++l) {
-    const double h = (st->dc_b[l] - st->dc_g[l]) * ib;
-    if (store) st->H[l * kMaxBasis + j] = h;
+    const double h = (db[l] - dg[l]) * ib;
+    if (store) Hm[l * kMaxBasis + j] = h;
     hh = fma(h, h, hh);
   }
   // the V_j coefficient the update pass actually removed (gamma from the Pythagorean

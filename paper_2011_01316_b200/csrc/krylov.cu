@@ -327,9 +327,18 @@ __global__ void __launch_bounds__(256) k_expm(double* W, int N, double* out) {
 
 void device_expm(cudaStream_t s, double* work, int N, double* out) { k_expm<<<1, 256, 0, s>>>(work, N, out); }
 
+// The controller; the expm workspace (9 (mmax+2)^2 doubles) lives in dynamic shared memory
+// when it fits (ws_cap > 0), else in the global `W`: the LU solve and the matrix products
+// of an expm at N = 42 take ~0.35 ms out of L2 and a fraction of it out of shared memory.
+constexpr int kCtlWsMax = 26000;  // doubles of dynamic shared memory (203 KB)
 __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double* W,
-                                             cudaGraphConditionalHandle cond, int use_graph) {
-  ctl_body(st, slot0, W, nullptr, 0, cond, use_graph);
+                                             cudaGraphConditionalHandle cond, int use_graph, int ws_cap) {
+  extern __shared__ __align__(16) double ctl_ws[];
+  ctl_body(st, slot0, W, ctl_ws, ws_cap, cond, use_graph);
+}
+static int ctl_ws_doubles(int mmax) {
+  const long long need = 9LL * (mmax + 2) * (mmax + 2);
+  return (mmax >= 0 && need <= kCtlWsMax) ? (int)need : 0;
 }
 
 // Sets action = START / DONE after the init reduction (separate tiny kernel so the
@@ -394,6 +403,7 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_ORTH"))
     use_dcgs = std::strcmp(v, "cgs2") == 0 ? 0 : (std::strcmp(v, "dcgs2") == 0 ? 2 : 1);
   dcgs_init_attrs(maxsm);
+  EXPDG_CUDA(cudaFuncSetAttribute(k_ctl, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtlWsMax * 8));
 }
 
 Engine::~Engine() {
@@ -576,7 +586,7 @@ void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraph
       reduce(s);
       ++body_launches;
     }
-    k_ctl<<<1, 256, 0, s>>>(st, slot(0), ework, h, use_graph);
+    k_ctl<<<1, 256, (size_t)ctl_ws_doubles(mmax) * 8, s>>>(st, slot(0), ework, h, use_graph, ctl_ws_doubles(mmax));
     ++body_launches;
     return;
   }
@@ -597,7 +607,7 @@ void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraph
     reduce(s);
     ++body_launches;
   }
-  k_ctl<<<1, 256, 0, s>>>(st, slot(0), ework, h, use_graph);
+  k_ctl<<<1, 256, (size_t)ctl_ws_doubles(mmax) * 8, s>>>(st, slot(0), ework, h, use_graph, ctl_ws_doubles(mmax));
   ++body_launches;
 }
 
