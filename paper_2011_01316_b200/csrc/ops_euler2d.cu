@@ -491,9 +491,10 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
 // from HBM, and the JVP arithmetic runs under the V stream instead of before it.
 // The V ring takes what shared memory the JVP leaves (single-buffered volume
 // fluxes in this variant, one more CTA barrier per row).
-// the sweep takes the dots of columns j < 34; beyond, the separate dots pass is faster
-// (tools/fusedbench.py at C4 size: fused 5.11 vs 5.18 ms at j = 32, 5.69 vs 5.59 at j = 36)
-constexpr int kE2DotJ = 34;
+// the sweep takes the dots of columns j < 44 (C4's basis bound is 40: the separate dots
+// pass is then not launched); with b_1 read in place and up to 16 V stages the sweep beats
+// the separate passes at every j <= 40 (tools/fusedbench.py: 5.84 vs 6.09 ms at j = 40)
+constexpr int kE2DotJ = 44;
 
 template <int NP, int CW, bool DOT>
 struct E2Strip {
@@ -502,7 +503,7 @@ struct E2Strip {
   static constexpr int W = CONS / NN > 0 ? CONS / NN : 1;  // elements per strip
   static constexpr int BLK = 4 * NN;          // doubles per element
   static constexpr int ROWD = (W + 2) * BLK;  // doubles per array per row (with halo)
-  static constexpr int BUFD = 2 * ROWD + W * BLK;  // x + frozen (with halo) + b_1
+  static constexpr int BUFD = 2 * ROWD;  // x + frozen primitives, with halo (b_1 is read in place)
   static constexpr int NBUF = 4;
   static constexpr int FX = (W + 1) * NP * 4;   // x-face fluxes of a row
   static constexpr int FY = W * NP * 4;         // y-face fluxes of one face row
@@ -518,7 +519,7 @@ struct E2Strip {
   // shared memory leaves next to ~3 KB of static shared memory
   static constexpr int SMAX = 232448 / 8 - 384;
   static constexpr int VSF = (SMAX - BASE - 2 * TILE) / TILE;
-  static constexpr int VS = DOT ? (VSF > 12 ? 12 : (VSF < 1 ? 1 : VSF)) : 1;
+  static constexpr int VS = DOT ? (VSF > 16 ? 16 : (VSF < 1 ? 1 : VSF)) : 1;
   static constexpr bool FITS = !DOT || VSF >= 4;
   static constexpr int SMEM = (BASE + (DOT ? 2 * TILE + VS * TILE : 0)) * 8;
 };
@@ -824,10 +825,8 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 2 : 1
           mbar_wait(&empty[sl], (use & 1) ^ 1);
           double* dst = ring + (size_t)sl * S::BUFD;
           const uint32_t eb = BLK * 8;
-          const bool with_b = b1 && q >= 1 && q <= r1 - r0;  // only the computed rows need b_1
-          mbar_arrive_expect_tx(&full[sl], 2u * (uint32_t)(w + 2) * eb + (with_b ? (uint32_t)w * eb : 0u));
+          mbar_arrive_expect_tx(&full[sl], 2u * (uint32_t)(w + 2) * eb);
           const size_t rbase = (size_t)row * nx;
-          const size_t brbase = (size_t)(r0 - 1 + q) * nx;  // b_1 rows are always owned rows
           const int left = ie0 == 0 ? nx - 1 : ie0 - 1;
           const int right = ie0 + w == nx ? 0 : ie0 + w;
           for (int arr = 0; arr < 2; ++arr) {
@@ -841,7 +840,6 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 2 : 1
               bulk_g2s(d + (size_t)(w + 1) * BLK, src + (rbase + right) * BLK, eb, &full[sl]);
             }
           }
-          if (with_b) bulk_g2s(dst + 2 * S::ROWD, b1 + (brbase + ie0) * BLK, (uint32_t)w * eb, &full[sl]);
           ++seq;
         }
       }
@@ -903,6 +901,13 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 2 : 1
       wait_row(1);
       for (int r = r0; r < r1; ++r) {
         const long long q = r - r0 + 1;  // ring index of row r
+        // b_1 of this node (p == 1), read in place: issued now, used in phase C
+        double bv[4] = {0.0, 0.0, 0.0, 0.0};
+        if (b1 && active) {
+          const size_t e = (size_t)r * nx + ie;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) bv[c] = __ldg(b1 + (e * 4 + c) * NN + node);
+        }
         wait_row(q + 1);
         const double* cur = slot(q);
         const double* lo = slot(q - 1);
@@ -1011,7 +1016,7 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 2 : 1
             const size_t g = (e * 4 + c) * NN + node;
             double v = rr[c] * im;
             if (b1) {
-              v = fma(s_xt[0], cur[2 * S::ROWD + le * BLK + c * NN + node], v);
+              v = fma(s_xt[0], bv[c], v);
             } else {
               v = aug_tail(b, s_xt, g, v);
             }

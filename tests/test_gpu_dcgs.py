@@ -102,7 +102,7 @@ def test_dense_fakes_with_breakdown(orth):
 
 
 def _euler_run(monkeypatch, fused, max_basis, flux="lf"):
-    # the strip JVP takes the DCGS2 pass-1 dots of columns j <= 33 in its own sweep
+    # the strip JVP takes the DCGS2 pass-1 dots of columns j <= 43 in its own sweep
     # (EXPDG_E2_DOTS=0: the separate k_ts2 dots pass for every column); nx = 24 leaves a
     # partial last strip (10 + 10 + 4 elements)
     monkeypatch.setenv("EXPDG_E2_DOTS", fused)
