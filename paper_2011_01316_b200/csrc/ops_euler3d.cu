@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "dots.cuh"
 #include "krylov.cuh"
 
 namespace expdg {
@@ -400,7 +401,9 @@ __global__ void __launch_bounds__(256) k_e3_phi(E3P<NP> P, PhiState* st, double*
 // on a unit's first plane, below it); phase C differentiates and scatters the face
 // fluxes into each node.  Orders whose element block (5 NP^3 doubles) is a multiple of
 // 16 bytes (NP = 2, 4) use it; NP = 3 keeps the element-tile kernel.
-template <int NP>
+constexpr int kE3DotJ = 44;  // DOT: the sweep takes the DCGS2 dots of columns j < 44
+
+template <int NP, bool DOT = false>
 struct E3March {
   static constexpr int NN = NP * NP * NP, NF = NP * NP, BLK = 5 * NN;
   static constexpr int TX = NP == 4 ? 2 : 4, TY = NP == 4 ? 2 : 8;  // TX * TY * NN = 256 (1x2 tiles at two CTAs per SM measured slower)
@@ -408,38 +411,93 @@ struct E3March {
   static constexpr int CONS = TE * NN;
   static constexpr int CW = CONS / 32;
   static constexpr int PL = TE * BLK;           // doubles per array per ring plane
-  static constexpr int BUFD = 3 * PL;           // x, q~ primitives, b_1
+  // x, q~ primitives (+ b_1 without DOT; with DOT b_1 is read in place to leave room for V)
+  static constexpr int BUFD = (DOT ? 2 : 3) * PL;
   static constexpr int NBUF = 4;
   static constexpr int FXD = (TX + 1) * TY * NF * 5;  // x-face fluxes of a plane
   static constexpr int FYD = TX * (TY + 1) * NF * 5;  // y-face fluxes
   static constexpr int FZD = TE * NF * 5;              // one layer of z-face fluxes
-  static constexpr int SMEM = (NBUF * BUFD + 3 * 5 * CONS + FXD + FYD + 2 * FZD) * 8;
+  static constexpr int BASE = NBUF * BUFD + 3 * 5 * CONS + FXD + FYD + 2 * FZD;
+  // DOT (the fused DCGS2 dots, as in the 2D strip sweep, dots.cuh): a V producer warp, two
+  // dot warps, the double-buffered w tile handed over by the JVP warps, a V ring
+  static constexpr int TILE = TE * BLK;
+  static constexpr int ND = DOT ? 2 : 0;
+  static constexpr int JMAX = DOT ? kE3DotJ - 1 : -1;
+  static constexpr int THREADS = CONS + 32 + (DOT ? 32 + 32 * ND : 0);
+  static constexpr int SMAX = 232448 / 8 - 384;
+  static constexpr int VSF = (SMAX - BASE - 2 * TILE) / TILE;
+  static constexpr int VS = DOT ? (VSF > 16 ? 16 : (VSF < 1 ? 1 : VSF)) : 1;
+  static constexpr bool FITS = !DOT || VSF >= 4;
+  static constexpr int SMEM = (BASE + (DOT ? 2 * TILE + VS * TILE : 0)) * 8;
   static constexpr bool OK = (BLK * 8) % 16 == 0;
 };
 
-template <int NP>
-__global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
+// Dot warps of the fused z-march: the march's (tile, plane) sequence, u = the tile's x in the
+// plane's ring slot, w = the tile handed over by the JVP warps (full tiles only).
+template <class S>
+__device__ __forceinline__ void march_dots(const double* ring, const double* swr, const double* vring, uint64_t* full,
+                                           uint64_t* empty, uint64_t* wfull, uint64_t* wempty, uint64_t* vfull,
+                                           uint64_t* vempty, long long ntiles, int nz, int j, double* s_acc) {
+  const int lane = threadIdx.x & 31;
+  const int h = (threadIdx.x >> 5) - (S::CONS / 32 + 2);
+  double* acc = s_acc + h * 2 * (S::JMAX + 1);
+  RingPos vp, wp;
+  long long seq = 0;
+  constexpr int cnt2 = S::TILE / 2;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int z = 0; z < nz; ++z) {
+      const long long q = z + 1;  // ring index of plane z
+      const int bsel = wp.s;
+      mbar_wait(&wfull[bsel], wp.ph);
+      wp.next<2>();
+      const int sl = (int)((seq + q) % S::NBUF);
+      mbar_wait(&full[sl], (int)(((seq + q) / S::NBUF) & 1));  // completed phase: returns at once
+      const double2* U2 = reinterpret_cast<const double2*>(ring + (size_t)sl * S::BUFD);
+      const double2* W2 = reinterpret_cast<const double2*>(swr + bsel * S::TILE);
+      dots_row<S, true>(U2, W2, vring, vfull, vempty, vp, j, cnt2, lane, h, acc, false);
+      __syncwarp();
+      if (lane == 0) {  // u (the ring plane) and the w tile are free
+        mbar_arrive(&wempty[bsel]);
+        mbar_arrive(&empty[sl]);
+      }
+    }
+    seq += nz + 2;
+  }
+}
+
+template <int NP, bool DOT>
+__global__ void __launch_bounds__(E3March<NP, DOT>::THREADS, 1)
     k_e3_phi_march(E3P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
-  using S = E3March<NP>;
+  using S = E3March<NP, DOT>;
   constexpr int NN = S::NN, NF = S::NF, BLK = S::BLK, TX = S::TX, TY = S::TY, NBUF = S::NBUF, N = NP - 1;
+  constexpr int CWN = S::CW;  // JVP warps
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;
   double* sf = ring + NBUF * S::BUFD;  // [dir][c][thread]
   double* fxf = sf + 3 * 5 * S::CONS;
   double* fyf = fxf + S::FXD;
   double* fzf = fyf + S::FYD;          // two layers
+  double* swr = smem + S::BASE;        // DOT: w tiles handed to the dot warps
+  double* vring = swr + 2 * S::TILE;   // DOT: V tiles
   __shared__ uint64_t full[NBUF], empty[NBUF];
-  __shared__ int s_go, s_j;
+  __shared__ uint64_t wfull[2], wempty[2], vfull[S::VS], vempty[S::VS];
+  __shared__ int s_go, s_j, s_dots;
   __shared__ double s_xs, s_dt, s_xt[kMaxP];
   __shared__ long long s_ld;
-  __shared__ double s_buf[S::CW + 1];
-  __shared__ double s_red[1];
+  __shared__ double s_buf[S::THREADS / 32];
+  __shared__ double s_red[DOT ? 2 * S::ND * (S::JMAX + 1) : 1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     const int a = st->action;
     s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
     if (s_go) {
       s_j = st->j;
+      s_dots = DOT && st->dcgs && s_j <= S::JMAX;
+      if (blockIdx.x == 0) {
+        if (DOT) st->dots_fused = s_dots;
+        st->app_bytes += 8.0 * (double)P.n * (4.0 + (s_dots ? (double)s_j : 0.0));
+        st->app_launches++;
+      }
       s_xs = st->scale[s_j];
       s_dt = st->dt;
       s_ld = st->ld;
@@ -447,13 +505,27 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
       for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
       for (int q = 0; q < NBUF; ++q) {
         mbar_init(&full[q], 1);
-        mbar_init(&empty[q], 1);
+        mbar_init(&empty[q], 1 + S::ND);  // the JVP warps + (DOT) every dot warp
+      }
+      if (DOT) {
+        for (int q = 0; q < 2; ++q) {
+          mbar_init(&wfull[q], CWN);
+          mbar_init(&wempty[q], S::ND);
+        }
+        for (int q = 0; q < S::VS; ++q) {
+          mbar_init(&vfull[q], 1);
+          mbar_init(&vempty[q], S::ND);
+        }
       }
       fence_mbar_init();
     }
   }
+  if (DOT)
+    for (int q = tid; q < 2 * S::ND * (S::JMAX + 1); q += blockDim.x) s_red[q] = 0.0;
   __syncthreads();
   if (!s_go) return;
+  const bool dots = DOT && s_dots;
+  const uint32_t rel_row = dots ? 1u : 1u + S::ND, rel_halo = 1u + S::ND;
   const double* x = base + (size_t)s_j * s_ld;
   double* y = base + (size_t)(s_j + 1) * s_ld;
   const double xs = s_xs, dt = s_dt;
@@ -497,7 +569,7 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
           const int sl = (int)(seq % NBUF);
           mbar_wait(&empty[sl], (int)(((seq / NBUF) & 1) ^ 1));
           double* dst = ring + (size_t)sl * S::BUFD;
-          const bool with_b = b1 && q >= 1 && q <= z1 - z0;
+          const bool with_b = !DOT && b1 && q >= 1 && q <= z1 - z0;
           const uint32_t rowb = (uint32_t)tx * BLK * 8;
           mbar_arrive_expect_tx(&full[sl], (2u + (with_b ? 1u : 0u)) * (uint32_t)ty * rowb);
           for (int ly = 0; ly < ty; ++ly) {
@@ -511,6 +583,38 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
           }
         }
       }
+    }
+  } else if (wid == S::CW + 1) {
+    // ---------------- producer: the tile's elements of V_0..V_{j-1} for every plane (DOT)
+    if constexpr (DOT) {
+      if (dots && lane == 0) {
+        const int jj = s_j;
+        const long long ld = s_ld;
+        RingPos vp;
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+          int ix0, iy0, tx, ty, z0, z1;
+          unit(tile, ix0, iy0, tx, ty, z0, z1);
+          const uint32_t rowb = (uint32_t)tx * BLK * 8;
+          for (int z = z0; z < z1; ++z) {
+            for (int i = 0; i < jj; ++i) {
+              const int stg = vp.s;
+              mbar_wait(&vempty[stg], vp.ph ^ 1u);
+              mbar_arrive_expect_tx(&vfull[stg], (uint32_t)ty * rowb);
+              for (int ly = 0; ly < ty; ++ly) {
+                const size_t e = ((size_t)z * ny + iy0 + ly) * nx + ix0;
+                bulk_g2s(vring + (size_t)stg * S::TILE + (size_t)ly * TX * BLK, base + (size_t)i * ld + e * BLK, rowb,
+                         &vfull[stg]);
+              }
+              vp.next<S::VS>();
+            }
+          }
+        }
+      }
+    }
+  } else if (wid > S::CW + 1) {
+    // ---------------- dot warps (DOT)
+    if constexpr (DOT) {
+      if (dots) march_dots<S>(ring, swr, vring, full, empty, wfull, wempty, vfull, vempty, ntiles, nz, s_j, s_red);
     }
   } else {
     // ---------------- consumers: one thread per node of the tile
@@ -543,8 +647,16 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
       constexpr int NFX = (TX + 1) * TY * NF, NFY = TX * (TY + 1) * NF, NFZ = TX * TY * NF;
       wait_plane(0);
       wait_plane(1);
+      int wrc = 0;  // DOT: planes handed to the dot warps
       for (int z = z0; z < z1; ++z) {
         const long long q = z - z0 + 1;
+        // b_1 of this node (p == 1), read in place: issued now, used in phase C
+        double bv[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        if (DOT && b1 && active) {
+          const size_t e = ((size_t)z * ny + iy) * nx + ix;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) bv[c] = __ldg(b1 + (e * 5 + c) * NN + node);
+        }
         wait_plane(q + 1);
         const double* cur = slot(q);
         const double* lo = slot(q - 1);
@@ -647,7 +759,10 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
           if (load_face(f, qa, ta, qb, tb, dir, dst)) face_out(dir, qa, ta, qb, tb, dst);
         }
         strip_sync<S::CONS>();  // phase A of plane z complete
-        if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);  // ring plane z - 1 is free
+        if (tid == 0) mbar_arrive_cnt(&empty[(seq + q - 1) % NBUF], q == 1 ? rel_halo : rel_row);  // plane z - 1
+        const int bsel = wrc & 1;
+        double* wt = swr + bsel * S::TILE;
+        if (dots) mbar_wait(&wempty[bsel], ((wrc >> 1) & 1) ^ 1);  // the dot warps took plane z - 2
         // ---- phase C: differentiate, scatter the face fluxes, scale
         if (active) {
           const double hz = __ldg(P.hz + z);
@@ -697,18 +812,24 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
           for (int c = 0; c < 5; ++c) {
             const size_t g = (e * 5 + c) * NN + node;
             double v = r[c] * im;
-            if (b1) v = fma(s_xt[0], cur[2 * S::PL + le * BLK + c * NN + node], v);
+            if (b1) v = fma(s_xt[0], DOT ? bv[c] : cur[(DOT ? 0 : 2) * S::PL + le * BLK + c * NN + node], v);
             else v = aug_tail(b, s_xt, g, v);
             v = dt * v;
             y[g] = v;
+            if (dots) wt[le * BLK + c * NN + node] = v;
             nacc = fma(v, v, nacc);
           }
         }
+        if (dots) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&wfull[bsel]);
+        }
+        ++wrc;
         strip_sync<S::CONS>();  // phase C of plane z complete (sf, face arrays reusable)
       }
       if (tid == 0) {
-        mbar_arrive(&empty[(seq + (z1 - z0)) % NBUF]);      // plane z1 - 1
-        mbar_arrive(&empty[(seq + (z1 - z0) + 1) % NBUF]);  // plane z1 (upper halo)
+        mbar_arrive_cnt(&empty[(seq + (z1 - z0)) % NBUF], rel_row);       // plane z1 - 1
+        mbar_arrive_cnt(&empty[(seq + (z1 - z0) + 1) % NBUF], rel_halo);  // plane z1 (upper halo)
       }
       seq += z1 - z0 + 2;
     }
@@ -720,9 +841,39 @@ __global__ void __launch_bounds__(E3March<NP>::CONS + 32, 1)
     if (st->tail_here) nacc = fma(v, v, nacc);
   }
   const double tot = block_sum(nacc, s_buf);
-  if (tid == 0) s_red[0] = tot;
+  // dots (DOT): the dot warps' sums in warp order, plus (rank 0) the tail region
+  // [n, n + kTailPad) of every slot; cnt <= JMAX + 1 <= blockDim.x
+  const int cnt = dots ? s_j + 1 : 0;
+  double ca = 0.0, cb = 0.0;
+  if (DOT && tid < cnt) {
+    constexpr int JS = 2 * (S::JMAX + 1);
+#pragma unroll
+    for (int q = 0; q < (DOT ? S::ND : 1); ++q) {
+      ca += s_red[q * JS + 2 * tid];
+      cb += s_red[q * JS + 2 * tid + 1];
+    }
+    if (blockIdx.x == 0 && st->tail_here) {
+      const double* ut = base + (size_t)s_j * s_ld + P.n;
+      const double* vt = base + (size_t)tid * s_ld + P.n;
+      for (int t = 0; t < kTailPad; ++t) {
+        const double yt = (t + 1 < b.p) ? dt * s_xt[t + 1] : 0.0;
+        ca = fma(vt[t], ut[t], ca);
+        cb = fma(vt[t], yt, cb);
+      }
+    }
+  }
   __syncthreads();
-  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
+  if (DOT && tid < cnt) {
+    s_red[tid] = ca;
+    s_red[cnt + tid] = cb;
+  }
+  if (tid == 0) s_red[2 * cnt] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 2 * cnt + 1, partials, 2 * kMaxSlots + 2, &st->ticket[4], [&](int i, double v) {
+    if (i < cnt) st->rs().dotA[i] = v;
+    else if (i < 2 * cnt) st->rs().dotB[i - cnt] = v;
+    else st->rs().nrmA = v;
+  });
 }
 
 __global__ void k_e3_freeze(const double* __restrict__ q, long long nelem, int nn, double gamma,
@@ -753,6 +904,14 @@ class Euler3D : public OpDevice {
   long long plane = 0;     // doubles per element plane
   bool use_march = E3March<NP>::OK;  // EXPDG_E3_TILE=1: the element-tile JVP
   int march_grid = 1;
+  // the z-march also takes the DCGS2 pass-1 dots (EXPDG_E3_DOTS=0: off) on meshes of whole
+  // tiles (the dot warps read the tile's elements as one contiguous block)
+  static constexpr bool kDotFits = E3March<NP>::OK && E3March<NP, true>::FITS;
+  bool use_dots = true;
+  bool whole_tiles = false;
+  int dots_grid = 1;
+  bool dots_on() const { return kDotFits && use_march && use_dots && whole_tiles; }
+  int fused_dcgs_dots_jmax() const override { return dots_on() ? E3March<NP, true>::JMAX : -1; }
   ~Euler3D() override {
     cudaFree(frozen);
     cudaFree(hbuf);
@@ -816,13 +975,25 @@ class Euler3D : public OpDevice {
     const long long ntiles = ((long long)d.nx * d.ny * nzl + E3Tile<NP>::TE - 1) / E3Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
     if (const char* v = std::getenv("EXPDG_E3_TILE")) use_march = use_march && v[0] != '1';
+    if (const char* v = std::getenv("EXPDG_E3_DOTS")) use_dots = v[0] != '0';
     if constexpr (E3March<NP>::OK) {
       using SM = E3March<NP>;
-      EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::SMEM));
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march<NP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SM::SMEM));
       int per_sm = 1;
-      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_e3_phi_march<NP>, SM::CONS + 32, SM::SMEM));
+      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_e3_phi_march<NP, false>, SM::THREADS,
+                                                               SM::SMEM));
       const long long tiles = (long long)((d.nx + SM::TX - 1) / SM::TX) * ((d.ny + SM::TY - 1) / SM::TY);
       march_grid = (int)std::max<long long>(1, std::min<long long>(tiles, 148LL * std::max(1, per_sm)));
+      whole_tiles = d.nx % SM::TX == 0 && d.ny % SM::TY == 0;
+      if constexpr (kDotFits) {
+        using SD = E3March<NP, true>;
+        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SD::SMEM));
+        int pd = 1;
+        EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pd, k_e3_phi_march<NP, true>, SD::THREADS, SD::SMEM));
+        dots_grid = (int)std::max<long long>(1, std::min<long long>(tiles, 148LL * std::max(1, pd)));
+      }
     }
   }
   void freeze(cudaStream_t s, const double* r) override {
@@ -837,8 +1008,15 @@ class Euler3D : public OpDevice {
     }
     if constexpr (E3March<NP>::OK) {
       if (use_march) {
-        k_e3_phi_march<NP><<<march_grid, E3March<NP>::CONS + 32, E3March<NP>::SMEM, s>>>(params(frozen), st, base,
-                                                                                        partials, b);
+        if constexpr (kDotFits) {
+          if (dots_on()) {
+            using SD = E3March<NP, true>;
+            k_e3_phi_march<NP, true><<<dots_grid, SD::THREADS, SD::SMEM, s>>>(params(frozen), st, base, partials, b);
+            return;
+          }
+        }
+        k_e3_phi_march<NP, false><<<march_grid, E3March<NP>::THREADS, E3March<NP>::SMEM, s>>>(params(frozen), st,
+                                                                                             base, partials, b);
         return;
       }
     }

@@ -158,3 +158,26 @@ def test_host_stepped_cycles_match_graph(orth):
     assert np.array_equal(to_host(a.u), to_host(b.u))
     assert list(a.iters_per_step) == list(b.iters_per_step)
     assert max(np.diff(np.concatenate([[0], a.iters_per_step]))) > 34  # columns past the fused bound
+
+
+@pytest.mark.parametrize("n,max_basis", [(4, 40), (6, 64)])
+def test_euler3d_fused_dots_match_dots_pass(monkeypatch, n, max_basis):
+    # the 3D z-march takes the DCGS2 pass-1 dots of columns j <= 43 in its own sweep on meshes
+    # of whole 2x2 tiles (EXPDG_E3_DOTS=0: the separate k_ts2 dots pass)
+    w = configs.scaled(configs.C5, n, steps=2)
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    out = []
+    for v in ("1", "0"):
+        monkeypatch.setenv("EXPDG_E3_DOTS", v)
+        ctx = pkg.Context(0, orth="dcgs2", fused=False)
+        op = pkg.Operator(ctx, w.spec())
+        r = pkg.integrate(ctx, op, to_dev(u0), "epi2", dt, w.steps * dt, tol=w.tol, max_basis=max_basis,
+                          orth_length=max_basis)
+        r.alg_bytes = ctx.traffic()["alg_bytes"]
+        out.append(r)
+    a, b = out
+    assert a.status == b.status == "completed"
+    assert rel(to_host(a.u), to_host(b.u)) <= 1e-12
+    assert list(a.iters_per_step) == list(b.iters_per_step)
+    assert a.alg_bytes < b.alg_bytes  # the sweep took the dots
