@@ -1,7 +1,8 @@
-"""Euler 2D (C4 size) phi-cycle operator apply vs the separate DCGS2 dots pass, per column j.
+"""Fused JVP + DCGS2-dots sweep vs the separate passes, per Krylov column j.
 
-python tools/fusedbench.py [nx] : for each j, ms of the strip JVP alone (EXPDG_E2_DOTS=0), the DCGS2
-dots pass, the fused JVP+dots sweep, and the fused sweep with the dot arithmetic skipped (EXPDG_E2_DBG=1).
+python tools/fusedbench.py [nx] [j,j,...] [C4|C5] : for each j, ms of the JVP alone (EXPDG_E2_DOTS=0 /
+EXPDG_E3_DOTS=0), the DCGS2 dots pass, the fused sweep, and (C4) the fused sweep with the dot arithmetic
+skipped (EXPDG_E2_DBG=1).
 """
 import json
 import os
@@ -19,13 +20,14 @@ from paper_2011_01316_b200 import configs  # noqa: E402
 def main():
     nx = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
     js = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 4, 10, 20, 30, 40]
-    w = configs.scaled(configs.C4, nx, steps=1)
+    cfg = sys.argv[3] if len(sys.argv) > 3 else "C4"
+    w = configs.scaled(configs.ALL[cfg], nx, steps=1)
+    dv = "EXPDG_E2_DOTS" if cfg == "C4" else "EXPDG_E3_DOTS"
     u0 = torch.tensor(w.initial_condition(), device="cuda:0")
     ctx = pkg.Context(0, orth="dcgs2")
     ops = {}
-    for name, env in (("jvp", {"EXPDG_E2_DOTS": "0"}), ("fused", {"EXPDG_E2_DOTS": "1"}),
-                      ("fused_nofma", {"EXPDG_E2_DOTS": "1", "EXPDG_E2_DBG": "1"})):
-        for k in ("EXPDG_E2_DOTS", "EXPDG_E2_DBG"):
+    for name, env in (("jvp", {dv: "0"}), ("fused", {dv: "1"}), ("fused_nofma", {dv: "1", "EXPDG_E2_DBG": "1"})):
+        for k in ("EXPDG_E2_DOTS", "EXPDG_E3_DOTS", "EXPDG_E2_DBG"):
             os.environ.pop(k, None)
         os.environ.update(env)
         op = pkg.Operator(ctx, w.spec())
