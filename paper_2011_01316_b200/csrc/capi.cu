@@ -1,5 +1,6 @@
 // C ABI of the B200 exponential-DG hot path (include/expdg_b200.h).
 // Maps the reference's exception types onto status codes.
+#include <chrono>
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -48,6 +49,13 @@ struct expdg_ctx {
   long long udev_len = 0;
   double* work2 = nullptr;  // small reduction buffer
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // integrate's per-call buffers, kept across calls: a pinned allocation per call cost
+  // ~40 ms of host time (the e2e path calls integrate once per step)
+  int* stop_host = nullptr;   // pinned: the lagged early-exit flag
+  cudaEvent_t chunk_ev = nullptr;
+  double* dts_dev = nullptr;  // dt sequence
+  StepRecord* rec_dev = nullptr;
+  long long steps_cap = 0;
 };
 
 struct expdg_op {
@@ -162,6 +170,10 @@ int expdg_ctx_destroy(expdg_ctx* ctx) {
     cudaFree(ctx->work2);
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
+    if (ctx->stop_host) cudaFreeHost(ctx->stop_host);
+    if (ctx->chunk_ev) cudaEventDestroy(ctx->chunk_ev);
+    cudaFree(ctx->dts_dev);
+    cudaFree(ctx->rec_dev);
     delete ctx;
   });
 }
@@ -441,6 +453,16 @@ static void restore_ref(OpDevice& dev, cudaStream_t s, const double* saved) {
 
 static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_time_cfg* cfg,
                            expdg_integration_result* res, long long* iters, double* amaxs, int cap) {
+  // EXPDG_TIMING=1: host wall-clock phases of the call on stderr (diagnostics)
+  static const bool timing = std::getenv("EXPDG_TIMING") && std::getenv("EXPDG_TIMING")[0] == '1';
+  auto tclk = std::chrono::steady_clock::now();
+  auto tmark = [&](const char* what) {
+    if (!timing) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[integrate] %-24s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tclk).count());
+    tclk = now;
+  };
   if (!ctx || !op || !u || !cfg || !res) throw std::invalid_argument("null argument");
   if (!(cfg->dt > 0.0)) throw std::invalid_argument("integrate: dt must be positive");
   if (cfg->t_final < cfg->dt) throw std::invalid_argument("integrate: t_final must be at least dt");
@@ -511,14 +533,26 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     if (chk == 2) throw std::domain_error("EulerOperator: inadmissible reference state");
     EXPDG_CUDA(cudaMemcpyAsync(refbuf, u, sizeof(double) * n, cudaMemcpyDeviceToDevice, e.stream));
   }
+  tmark("setup + absmax check");
   PhiState c = c1;
   c.max_steps = S;
   c.blow_up_scale = 1e10 * (1.0 + max0);
   e.upload_config(c, e.stream);
-  double* dts_dev = nullptr;
-  StepRecord* rec_dev = nullptr;
-  EXPDG_CUDA(cudaMalloc(&dts_dev, sizeof(double) * S));
-  EXPDG_CUDA(cudaMalloc(&rec_dev, sizeof(StepRecord) * S));
+  if (ctx->steps_cap < S) {
+    cudaFree(ctx->dts_dev);
+    cudaFree(ctx->rec_dev);
+    ctx->dts_dev = nullptr;
+    ctx->rec_dev = nullptr;
+    ctx->steps_cap = 0;
+    const long long cap2 = std::max<long long>(S, 64);
+    EXPDG_CUDA(cudaMalloc(&ctx->dts_dev, sizeof(double) * cap2));
+    EXPDG_CUDA(cudaMalloc(&ctx->rec_dev, sizeof(StepRecord) * cap2));
+    ctx->steps_cap = cap2;
+  }
+  if (!ctx->stop_host) EXPDG_CUDA(cudaMallocHost(&ctx->stop_host, sizeof(int) * 2));
+  if (!ctx->chunk_ev) EXPDG_CUDA(cudaEventCreateWithFlags(&ctx->chunk_ev, cudaEventDisableTiming));
+  double* dts_dev = ctx->dts_dev;
+  StepRecord* rec_dev = ctx->rec_dev;
   EXPDG_CUDA(cudaMemcpyAsync(dts_dev, dts.data(), sizeof(double) * S, cudaMemcpyHostToDevice, e.stream));
   const double* saved_ref = dev.ref;
   if (kind == EXPDG_EXP_EULER) dev.freeze(e.stream, refbuf);
@@ -639,15 +673,14 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
         }
       }
       EXPDG_CUDA(cudaGraphInstantiate(&ex, g, 0));
+      tmark("graph capture + instantiate");
       cudaGraphDestroy(g);
       cudaStreamDestroy(cs);
     }
     // lagged early-exit check: launch in chunks, look at `stopped` of the chunk before
-    int* stop_host = nullptr;
-    EXPDG_CUDA(cudaMallocHost(&stop_host, sizeof(int) * 2));
+    int* stop_host = ctx->stop_host;
     stop_host[0] = stop_host[1] = 0;
-    cudaEvent_t chunk_ev;
-    EXPDG_CUDA(cudaEventCreateWithFlags(&chunk_ev, cudaEventDisableTiming));
+    cudaEvent_t chunk_ev = ctx->chunk_ev;
     EXPDG_CUDA(cudaEventRecord(ctx->ev0, e.stream));
     const int chunk = 32;
     bool pending = false;
@@ -682,13 +715,10 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     float ms = 0.f;
     EXPDG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     ctx->last_loop_ms = ms;
-    cudaEventDestroy(chunk_ev);
-    cudaFreeHost(stop_host);
+    tmark("step loop");
   } catch (...) {
     if (ex) cudaGraphExecDestroy(ex);
     restore_ref(dev, e.stream, saved_ref);
-    cudaFree(dts_dev);
-    cudaFree(rec_dev);
     throw;
   }
   if (ex) cudaGraphExecDestroy(ex);
@@ -700,8 +730,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   std::vector<StepRecord> rec(std::max(1, st.step));
   if (st.step > 0)
     EXPDG_CUDA(cudaMemcpy(rec.data(), rec_dev, sizeof(StepRecord) * st.step, cudaMemcpyDeviceToHost));
-  cudaFree(dts_dev);
-  cudaFree(rec_dev);
+  tmark("teardown + readback");
   res->steps = st.step;
   res->status = 0;
   res->blow_up_step = -1;
