@@ -52,7 +52,7 @@ struct RingPos {
 template <class S, bool FULL>
 __device__ __forceinline__ void dots_row(const double2* U2, const double2* W2, const double* vring, uint64_t* vfull,
                                          uint64_t* vempty, RingPos& vp, int j, int cnt2, int lane, int h,
-                                         double* acc, bool skip) {
+                                         double* acc, int mode) {
   constexpr int T2 = S::TILE / 2;          // double2 per row tile
   constexpr int PER = (T2 + 63) / 64;      // blocks of 64 double2 (32 per dot warp)
   const int e0 = 32 * h + lane;
@@ -74,7 +74,7 @@ __device__ __forceinline__ void dots_row(const double2* U2, const double2* W2, c
     return s;
   };
   auto tile = [&](int s) { return reinterpret_cast<const double2*>(vring + (size_t)s * S::TILE); };
-  if (skip) {  // diagnostics: the V stream without the arithmetic
+  if (mode & 1) {  // diagnostics: the V stream without the arithmetic
     for (int i = 0; i < j; ++i) {
       const int s = take();
       __syncwarp();
@@ -83,7 +83,7 @@ __device__ __forceinline__ void dots_row(const double2* U2, const double2* W2, c
     return;
   }
   int i0 = 0;
-  for (; i0 + 3 < j; i0 += 4) {  // quads: 16 independent FMA chains, two butterflies
+  for (; !(mode & 2) && i0 + 3 < j; i0 += 4) {  // quads: 16 independent FMA chains, two butterflies
     const int sa = take(), sb = take(), sc = take(), sd = take();
     const double2 *A = tile(sa), *B = tile(sb), *C = tile(sc), *D = tile(sd);
     double xa0 = 0.0, xa1 = 0.0, ya0 = 0.0, ya1 = 0.0, xb0 = 0.0, xb1 = 0.0, yb0 = 0.0, yb1 = 0.0;

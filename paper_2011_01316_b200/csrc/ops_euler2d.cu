@@ -40,7 +40,7 @@ struct E2P {
   const double* gx_hi;
   const double* gt_lo;
   const double* gt_hi;
-  int dbg;  // EXPDG_E2_DBG (diagnostics): bit 0 = the DOT sweep's dot warps skip their arithmetic
+  int dbg;  // EXPDG_E2_DBG (diagnostics): bit 0 = the DOT sweep's dot warps skip their arithmetic, bit 1 = pairs only
 };
 
 struct Prim {
@@ -547,7 +547,7 @@ template <class S>
 __device__ __forceinline__ void strip_dots(const double* ring, const double* swr, const double* vring,
                                            uint64_t* full, uint64_t* empty, uint64_t* wfull, uint64_t* wempty,
                                            uint64_t* vfull, uint64_t* vempty, long long k0, long long k1, int nx,
-                                           int ny, int j, double* s_acc, bool skip) {
+                                           int ny, int j, double* s_acc, int skip) {
   const int lane = threadIdx.x & 31;
   const int h = (threadIdx.x >> 5) - (S::CONS / 32 + 2);
   double* acc = s_acc + h * 2 * (S::JMAX + 1);
@@ -726,7 +726,7 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 2 : 1
     // ---------------- dot warps
     if (dots) {
       strip_dots<S>(ring, swr, vring, full, empty, wfull, wempty, vfull, vempty, k0, k1, nx, ny, s_j, s_red,
-                    (P.dbg & 1) != 0);
+                    P.dbg);
     }
   } else {
     // ---------------- consumers: one thread per node of the strip row

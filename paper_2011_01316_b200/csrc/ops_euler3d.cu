@@ -454,7 +454,7 @@ __device__ __forceinline__ void march_dots(const double* ring, const double* swr
       mbar_wait(&full[sl], (int)(((seq + q) / S::NBUF) & 1));  // completed phase: returns at once
       const double2* U2 = reinterpret_cast<const double2*>(ring + (size_t)sl * S::BUFD);
       const double2* W2 = reinterpret_cast<const double2*>(swr + bsel * S::TILE);
-      dots_row<S, true>(U2, W2, vring, vfull, vempty, vp, j, cnt2, lane, h, acc, false);
+      dots_row<S, true>(U2, W2, vring, vfull, vempty, vp, j, cnt2, lane, h, acc, 0);
       __syncwarp();
       if (lane == 0) {  // u (the ring plane) and the w tile are free
         mbar_arrive(&wempty[bsel]);

@@ -26,7 +26,8 @@ def main():
     u0 = torch.tensor(w.initial_condition(), device="cuda:0")
     ctx = pkg.Context(0, orth="dcgs2")
     ops = {}
-    for name, env in (("jvp", {dv: "0"}), ("fused", {dv: "1"}), ("fused_nofma", {dv: "1", "EXPDG_E2_DBG": "1"})):
+    for name, env in (("jvp", {dv: "0"}), ("fused", {dv: "1"}), ("fused_nofma", {dv: "1", "EXPDG_E2_DBG": "1"}),
+                      *((("fused_dbg", {dv: "1", "EXPDG_E2_DBG": os.environ["FB_DBG"]}),) if "FB_DBG" in os.environ else ())):
         for k in ("EXPDG_E2_DOTS", "EXPDG_E3_DOTS", "EXPDG_E2_DBG"):
             os.environ.pop(k, None)
         os.environ.update(env)
@@ -40,6 +41,8 @@ def main():
         r["dots_ms"] = ctx.bench_apply(ops["jvp"], j, 1)
         r["fused_ms"] = ctx.bench_apply(ops["fused"], j, 0)
         r["fused_nofma_ms"] = ctx.bench_apply(ops["fused_nofma"], j, 0)
+        if "fused_dbg" in ops:
+            r["fused_dbg_ms"] = ctx.bench_apply(ops["fused_dbg"], j, 0)
         gb_f = 8.0 * n * (j + 4) / 1e9
         r["fused_GBps"] = gb_f / r["fused_ms"] * 1e3
         r["separate_ms"] = r["jvp_ms"] + r["dots_ms"]
