@@ -11,6 +11,7 @@
 #include <cstdlib>
 
 #include "burgers_common.cuh"
+#include "dots.cuh"
 
 namespace expdg {
 
@@ -165,39 +166,69 @@ __global__ void __launch_bounds__(256) k_b2_phi(B1P<NP> Px, B1P<NP> Py, int nx, 
 // and y-lines (thread per element column-line, neighbours from ring rows r -+ 1), so
 // every byte of x and u~ leaves HBM once per JVP instead of being gathered from L2 by
 // three elements in two directions.
-template <int NP>
+// DOT (as the 2D Euler strip sweep, ops_euler2d.cu): the sweep also takes the DCGS2 pass-1
+// dots of column j (a = V^T u, b = V^T w with u = slot j, w = the JVP output) — a TMA producer
+// warp streams the row tiles of V_0..V_{j-1} into a ring and two dot warps consume them
+// (dots.cuh).  Needs full-width strips whose rows are 16-byte aligned (nx % W == 0).
+constexpr int kB2DotJ = 44;
+
+template <int NP, bool DOT = false>
 struct B2Strip {
   static constexpr int NN = NP * NP;
   static constexpr int W = NP <= 7 ? 32 : 16;        // elements per strip
   static constexpr int CONS = (W * NP + 31) / 32 * 32;  // consumer threads: one per element line
   static constexpr int CW = CONS / 32;       // consumer warps
   static constexpr int ROWD = (W + 2) * NN;  // doubles per array per ring row (with halo)
-  static constexpr int BUFD = 2 * ROWD + W * NN;  // x + u~ (with halo) + b_1
+  // DOT: the x row starts one double into its slot when NN is odd, so that its interior
+  // (the dots' u) is 16-byte aligned
+  static constexpr int XOFF = DOT && (NN & 1) ? 1 : 0;
+  static constexpr int BUFD = (XOFF + 2 * ROWD + W * NN + 1) / 2 * 2;  // x + u~ (with halo) + b_1
   static constexpr int NBUF = 4;
   static constexpr int OUT = W * NN;         // one row of x-line or y-line results
-  static constexpr int SMEM = (NBUF * BUFD + 2 * 2 * OUT) * 8;  // ring + double-buffered sX, sY
+  static constexpr int TILE = W * NN;        // doubles of one row of one vector
+  static constexpr int ND = DOT ? 2 : 0;     // dot warps (one per tile half)
+  static constexpr int JMAX = DOT ? kB2DotJ - 1 : -1;
+  static constexpr int THREADS = CONS + 32 + (DOT ? 32 + 32 * ND : 0);
+  static constexpr int BASE = NBUF * BUFD + 2 * 2 * OUT;  // ring + double-buffered sX, sY
+  static constexpr int SMAX = 232448 / 8 - 384;
+  static constexpr int VSF = (SMAX - BASE - 2 * TILE) / TILE;
+  static constexpr int VS = DOT ? (VSF > 16 ? 16 : (VSF < 1 ? 1 : VSF)) : 1;
+  static constexpr bool FITS = !DOT || (VSF >= 4 && TILE % 2 == 0);
+  static constexpr int SMEM = (BASE + (DOT ? 2 * TILE + VS * TILE : 0)) * 8;
 };
 
-template <int NP>
-__global__ void __launch_bounds__(B2Strip<NP>::CONS + 32)
+template <int NP, bool DOT>
+__global__ void __launch_bounds__(B2Strip<NP, DOT>::THREADS)
     k_b2_phi_strip(B1P<NP> Px, B1P<NP> Py, int nx, int ny, PhiState* st, double* base, double* partials, BArgs b) {
-  using S = B2Strip<NP>;
+  using S = B2Strip<NP, DOT>;
   constexpr int NN = S::NN, W = S::W, NBUF = S::NBUF, CW = S::CW;
   extern __shared__ __align__(128) double smem[];
   double* ring = smem;
   double* sout = smem + NBUF * S::BUFD;  // [parity][X | Y][W * NN]
+  double* swr = smem + S::BASE;          // DOT: w rows handed to the dot warps
+  double* vring = swr + 2 * S::TILE;     // DOT: V row tiles
   __shared__ uint64_t full[NBUF], empty[NBUF];
-  __shared__ int s_go, s_j;
+  __shared__ uint64_t wfull[2], wempty[2], vfull[S::VS], vempty[S::VS];
+  __shared__ int s_go, s_j, s_dots;
   __shared__ double s_xs, s_dt, s_xt[kMaxP];
   __shared__ long long s_ld;
-  __shared__ double s_buf[CW + 1];
-  __shared__ double s_red[1];
+  __shared__ double s_buf[S::THREADS / 32];
+  // DOT: per tile half, the dot sums 2 i + {0: <V_i,u>, 1: <V_i,w>}; then (reused in place)
+  // the grid-reduction inputs [dotA_0..j, dotB_0..j, ||y||^2]
+  __shared__ double s_red[DOT ? 4 * (S::JMAX + 1) : 1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     const int a = st->action;
     s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
     if (s_go) {
       s_j = st->j;
+      s_dots = DOT && st->dcgs && s_j <= S::JMAX;
+      if (blockIdx.x == 0) {
+        st->dots_fused = s_dots;
+        // algorithmic bytes of this sweep: x, u~, b_1, y plus, with the dots, V_0..V_{j-1}
+        st->app_bytes += 8.0 * (double)Px.n * (4.0 + (s_dots ? (double)s_j : 0.0));
+        st->app_launches++;
+      }
       s_xs = st->scale[s_j];
       s_dt = st->dt;
       s_ld = st->ld;
@@ -205,16 +236,32 @@ __global__ void __launch_bounds__(B2Strip<NP>::CONS + 32)
       for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[Px.n + i] * s_xs : 0.0;
       for (int q = 0; q < NBUF; ++q) {
         mbar_init(&full[q], 32);  // every producer lane's cp.async arrival
-        mbar_init(&empty[q], 1);
+        mbar_init(&empty[q], 1 + S::ND);  // the JVP warps + (DOT) every dot warp
+      }
+      if (DOT) {
+        for (int q = 0; q < 2; ++q) {
+          mbar_init(&wfull[q], CW);
+          mbar_init(&wempty[q], S::ND);
+        }
+        for (int q = 0; q < S::VS; ++q) {
+          mbar_init(&vfull[q], 1);
+          mbar_init(&vempty[q], S::ND);
+        }
       }
       fence_mbar_init();
     }
   }
+  if (DOT)
+    for (int q = tid; q < 4 * (S::JMAX + 1); q += blockDim.x) s_red[q] = 0.0;
   __syncthreads();
   if (!s_go) return;
   const double* x = base + (size_t)s_j * s_ld;
   double* y = base + (size_t)(s_j + 1) * s_ld;
   const double xs = s_xs, dt = s_dt;
+  const bool dots = DOT && s_dots;
+  // ring rows the dot warps also read (u) are released by them too; halo rows and,
+  // without dots, every row are released by the JVP warps for all 1 + ND arrivals
+  const uint32_t rel_row = dots ? 1u : 1u + S::ND, rel_halo = 1u + S::ND;
   const int nstrips = (nx + W - 1) / W;
   const long long rsteps = (long long)nstrips * ny;
   const long long k0 = rsteps * blockIdx.x / gridDim.x, k1 = rsteps * (blockIdx.x + 1) / gridDim.x;
@@ -255,7 +302,7 @@ __global__ void __launch_bounds__(B2Strip<NP>::CONS + 32)
         const int sl = (int)(seq % NBUF);
         if (lane == 0) mbar_wait(&empty[sl], (int)(((seq / NBUF) & 1) ^ 1));
         __syncwarp();
-        double* dst = ring + (size_t)sl * S::BUFD;
+        double* dst = ring + (size_t)sl * S::BUFD + S::XOFF;
         const bool with_b = b1 && q >= 1 && q <= r1 - r0;
         const size_t rbase = (size_t)row * nx;
         const int left = ie0 == 0 ? nx - 1 : ie0 - 1;
@@ -275,6 +322,58 @@ __global__ void __launch_bounds__(B2Strip<NP>::CONS + 32)
         cp_async_arrive(&full[sl]);
       }
     }
+  } else if (DOT && wid == CW + 1) {
+    // ---------------- producer: row tiles of V_0..V_{j-1} for the dot warps (TMA)
+    if (dots && lane == 0) {
+      const int j = s_j;
+      const long long ld = s_ld;
+      RingPos vp;
+      for (long long k = k0; k < k1;) {
+        int ie0, w, r0, r1;
+        unit(k, ie0, w, r0, r1);
+        const uint32_t bytes = (uint32_t)(w * NN * 8);
+        for (int r = r0; r < r1; ++r) {
+          const double* src = base + ((size_t)r * nx + ie0) * NN;
+          for (int i = 0; i < j; ++i) {
+            const int stg = vp.s;
+            mbar_wait(&vempty[stg], vp.ph ^ 1u);
+            mbar_arrive_expect_tx(&vfull[stg], bytes);
+            bulk_g2s(vring + (size_t)stg * S::TILE, src + (size_t)i * ld, bytes, &vfull[stg]);
+            vp.next<S::VS>();
+          }
+        }
+      }
+    }
+  } else if (DOT && wid > CW + 1) {
+    // ---------------- dot warps: u = the x row in the ring, w = the row handed over
+    if (dots) {
+      const int h = wid - (CW + 2);
+      double* acc = s_red + h * 2 * (S::JMAX + 1);
+      RingPos vp, wp;
+      long long seq = 0;
+      for (long long k = k0; k < k1;) {
+        int ie0, w, r0, r1;
+        unit(k, ie0, w, r0, r1);
+        const int cnt2 = w * NN / 2;
+        for (int r = r0; r < r1; ++r) {
+          const long long q = r - r0 + 1;
+          const int bsel = wp.s;
+          mbar_wait(&wfull[bsel], wp.ph);
+          wp.next<2>();
+          const int sl = (int)((seq + q) % NBUF);
+          mbar_wait(&full[sl], (int)(((seq + q) / NBUF) & 1));  // completed phase: returns at once
+          const double2* U2 = reinterpret_cast<const double2*>(ring + (size_t)sl * S::BUFD + S::XOFF + NN);
+          const double2* W2 = reinterpret_cast<const double2*>(swr + bsel * S::TILE);
+          dots_row<S, true>(U2, W2, vring, vfull, vempty, vp, s_j, cnt2, lane, h, acc, 0);
+          __syncwarp();
+          if (lane == 0) {  // u (the x ring row) and the w row are free
+            mbar_arrive(&wempty[bsel]);
+            mbar_arrive(&empty[sl]);
+          }
+        }
+        seq += r1 - r0 + 2;
+      }
+    }
   } else {
     // ---------------- consumers: thread (element le, line l)
     const int le = tid / NP, l = tid % NP;
@@ -284,7 +383,7 @@ __global__ void __launch_bounds__(B2Strip<NP>::CONS + 32)
       int ie0, w, r0, r1;
       unit(k, ie0, w, r0, r1);
       const bool active = le < w;
-      auto slot = [&](long long q) { return ring + (size_t)((seq + q) % NBUF) * S::BUFD; };
+      auto slot = [&](long long q) { return ring + (size_t)((seq + q) % NBUF) * S::BUFD + S::XOFF; };
       auto wait_row = [&](long long q) { mbar_wait(&full[(seq + q) % NBUF], (int)(((seq + q) / NBUF) & 1)); };
       wait_row(0);
       wait_row(1);
@@ -326,7 +425,10 @@ __global__ void __launch_bounds__(B2Strip<NP>::CONS + 32)
           for (int t = 0; t < NP; ++t) sY[le * NN + t * NP + l] = out[t];
         }
         strip_sync<S::CONS>();  // sX, sY of row r complete; row r-1 is no longer read
-        if (tid == 0) mbar_arrive(&empty[(seq + q - 1) % NBUF]);  // ring row r - 1 is free
+        if (tid == 0) mbar_arrive_cnt(&empty[(seq + q - 1) % NBUF], q == 1 ? rel_halo : rel_row);  // row r-1 free
+        const int bsel = rowc & 1;
+        double* wrow = swr + bsel * S::TILE;
+        if (dots) mbar_wait(&wempty[bsel], ((rowc >> 1) & 1) ^ 1);  // the dot warps took row r-2
         const size_t g0 = ((size_t)r * nx + ie0) * NN;
         for (int idx = tid; idx < w * NN; idx += S::CONS) {
           double v = sX[idx] + sY[idx];
@@ -334,13 +436,18 @@ __global__ void __launch_bounds__(B2Strip<NP>::CONS + 32)
           else v = aug_tail(b, s_xt, g0 + idx, v);
           v = dt * v;
           y[g0 + idx] = v;
+          if (dots) wrow[idx] = v;
           nacc = fma(v, v, nacc);
+        }
+        if (dots) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&wfull[bsel]);
         }
       }
       strip_sync<S::CONS>();  // the unit's last row is done
       if (tid == 0) {
-        mbar_arrive(&empty[(seq + (r1 - r0)) % NBUF]);      // row r1 - 1
-        mbar_arrive(&empty[(seq + (r1 - r0) + 1) % NBUF]);  // row r1 (upper halo)
+        mbar_arrive_cnt(&empty[(seq + (r1 - r0)) % NBUF], r1 - r0 == 0 ? rel_halo : rel_row);  // row r1 - 1
+        mbar_arrive_cnt(&empty[(seq + (r1 - r0) + 1) % NBUF], rel_halo);                        // row r1 (upper halo)
       }
       seq += r1 - r0 + 2;
     }
@@ -352,9 +459,42 @@ __global__ void __launch_bounds__(B2Strip<NP>::CONS + 32)
     if (st->tail_here) nacc = fma(v, v, nacc);
   }
   const double tot = block_sum(nacc, s_buf);
-  if (tid == 0) s_red[0] = tot;
-  __syncthreads();
-  grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
+  if constexpr (DOT) {
+    // dots: the two tile halves, plus (rank 0) the tail region [n, n + kTailPad) of every
+    // slot, which k_ts2 streams with the head; cnt <= JMAX + 1 <= blockDim.x
+    const int cnt = dots ? s_j + 1 : 0;
+    double ca = 0.0, cb = 0.0;
+    if (tid < cnt) {
+      constexpr int JS = 2 * (S::JMAX + 1);
+      ca = s_red[2 * tid] + s_red[JS + 2 * tid];
+      cb = s_red[2 * tid + 1] + s_red[JS + 2 * tid + 1];
+      if (blockIdx.x == 0 && st->tail_here) {
+        const double* ut = base + (size_t)s_j * s_ld + Px.n;
+        const double* vt = base + (size_t)tid * s_ld + Px.n;
+        for (int t = 0; t < kTailPad; ++t) {
+          const double yt = (t + 1 < b.p) ? dt * s_xt[t + 1] : 0.0;
+          ca = fma(vt[t], ut[t], ca);
+          cb = fma(vt[t], yt, cb);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < cnt) {
+      s_red[tid] = ca;
+      s_red[cnt + tid] = cb;
+    }
+    if (tid == 0) s_red[2 * cnt] = tot;
+    __syncthreads();
+    grid_reduce_last(s_red, 2 * cnt + 1, partials, 2 * kMaxSlots + 2, &st->ticket[4], [&](int i, double v) {
+      if (i < cnt) st->rs().dotA[i] = v;
+      else if (i < 2 * cnt) st->rs().dotB[i - cnt] = v;
+      else st->rs().nrmA = v;
+    });
+  } else {
+    if (tid == 0) s_red[0] = tot;
+    __syncthreads();
+    grid_reduce_last(s_red, 1, partials, kMaxSlots, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
+  }
 }
 
 template <int NP>
@@ -424,12 +564,30 @@ class Burgers2D : public OpDevice {
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
     use_strip = !(std::getenv("EXPDG_B2_TILE") && std::getenv("EXPDG_B2_TILE")[0] == '1');
     using SS = B2Strip<NP>;
-    EXPDG_CUDA(cudaFuncSetAttribute(k_b2_phi_strip<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::SMEM));
+    EXPDG_CUDA(cudaFuncSetAttribute(k_b2_phi_strip<NP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SS::SMEM));
     int per_sm = 1;
-    EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_b2_phi_strip<NP>, SS::CONS + 32, SS::SMEM));
+    EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_b2_phi_strip<NP, false>, SS::THREADS, SS::SMEM));
     const long long rsteps = (long long)((d.nx + SS::W - 1) / SS::W) * ny;
     strip_grid = (int)std::max<long long>(1, std::min<long long>(rsteps, 148LL * std::max(1, per_sm)));
+    if (const char* v = std::getenv("EXPDG_B2_DOTS")) use_dots = v[0] != '0';
+    // the fused dots stream whole strip rows of V by TMA: full-width strips (then every
+    // row tile starts on a 16-byte boundary)
+    dots_ok = d.nx % SS::W == 0;
+    if constexpr (kDotFits) {
+      using SD = B2Strip<NP, true>;
+      EXPDG_CUDA(cudaFuncSetAttribute(k_b2_phi_strip<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SD::SMEM));
+      int per_sm_d = 1;
+      EXPDG_CUDA(
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_d, k_b2_phi_strip<NP, true>, SD::THREADS, SD::SMEM));
+      dots_grid = (int)std::max<long long>(1, std::min<long long>(rsteps, 148LL * std::max(1, per_sm_d)));
+    }
   }
+  // The strip JVP also takes the DCGS2 pass-1 dots of columns j <= JMAX (EXPDG_B2_DOTS=0: off).
+  static constexpr bool kDotFits = B2Strip<NP, true>::FITS;
+  bool use_dots = true, dots_ok = false;
+  int dots_grid = 1;
+  bool dots_on() const { return kDotFits && use_dots && use_strip && dots_ok; }
+  int fused_dcgs_dots_jmax() const override { return dots_on() ? B2Strip<NP, true>::JMAX : -1; }
   void exchange(cudaStream_t s, const double* v, double* lo, double* hi) {
     comm->halo(v, v + (size_t)(ny - 1) * rowd, lo, hi, rowd, s);
   }
@@ -452,9 +610,13 @@ class Burgers2D : public OpDevice {
     B1P<NP> px = Px, py = Py;
     px.ut = py.ut = ref;
     with_halo(py, false);
-    if (use_strip)
-      k_b2_phi_strip<NP><<<strip_grid, B2Strip<NP>::CONS + 32, B2Strip<NP>::SMEM, s>>>(px, py, nx, ny, st, base,
-                                                                                         partials, b);
+    if (dots_on()) {
+      if constexpr (kDotFits)
+        k_b2_phi_strip<NP, true><<<dots_grid, B2Strip<NP, true>::THREADS, B2Strip<NP, true>::SMEM, s>>>(
+            px, py, nx, ny, st, base, partials, b);
+    } else if (use_strip)
+      k_b2_phi_strip<NP, false><<<strip_grid, B2Strip<NP>::THREADS, B2Strip<NP>::SMEM, s>>>(px, py, nx, ny, st, base,
+                                                                                            partials, b);
     else
       k_b2_phi<NP><<<grid, 256, 0, s>>>(px, py, nx, ny, st, base, partials, b);
   }

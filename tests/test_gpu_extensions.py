@@ -260,6 +260,56 @@ def test_burgers2d_strip_matches_tile_kernel(monkeypatch, order, nx, ny, periodi
     assert list(a.iters_per_step) == list(b.iters_per_step)
 
 
+@pytest.mark.parametrize("order,nx,ny,periodic,flux,fused", [
+    (4, 64, 5, True, "ef", True),    # two full 32-element strips: the sweep takes the dots
+    (4, 32, 4, False, "lf", True),   # Dirichlet ends
+    (5, 32, 3, True, "lf", True),    # order 5: 6 V stages
+    (7, 32, 3, True, "ef", True),    # 16-element strips at order 7
+    (2, 32, 6, False, "ef", True),
+    (4, 40, 3, True, "ef", False),   # a partial strip: the separate dots pass
+])
+def test_burgers2d_fused_dots_match_dots_pass(monkeypatch, order, nx, ny, periodic, flux, fused):
+    # the 2D Burgers strip JVP takes the DCGS2 pass-1 dots of columns j <= 43 in its own sweep
+    # on meshes of full strips (EXPDG_B2_DOTS=0: the separate k_ts2 dots pass)
+    rng = np.random.default_rng(11 * nx + order)
+    spec = pkg.OperatorSpec("burgers2d", order, nx, ny, box=(0, 1, 0, 2, 0, 1), periodic=periodic, kappa=1e-2,
+                            flux=flux, sigma=1e-3 if flux == "ef" else 0.0)
+    u0 = 0.5 + 0.1 * rng.standard_normal(nx * ny * (order + 1) ** 2)
+    out = []
+    for v in ("1", "0"):
+        monkeypatch.setenv("EXPDG_B2_DOTS", v)
+        c = pkg.Context(0, orth="dcgs2", fused=False)
+        op = pkg.Operator(c, spec)
+        r = pkg.integrate(c, op, to_dev(u0), "epi2", 1e-3, 2e-3, tol=1e-10, max_basis=48, orth_length=48)
+        r.alg_bytes = c.traffic()["alg_bytes"]
+        out.append(r)
+    a, b = out
+    assert a.status == b.status == "completed"
+    assert rel(to_host(a.u), to_host(b.u)) <= 1e-12
+    assert list(a.iters_per_step) == list(b.iters_per_step)
+    if fused:
+        assert a.alg_bytes < b.alg_bytes  # the sweep took the dots (u and w not re-read)
+    else:
+        assert a.alg_bytes == b.alg_bytes
+
+
+def test_c3_fused_dots_epi2_parity():
+    # C3 physics on 32^2 elements (full strips) through the fused JVP + DCGS2 dots sweep vs the oracle
+    w = configs.scaled(configs.C3, 32, steps=3)
+    u0 = w.initial_condition()
+    orc = oracle_problem(w.spec()).integrate("epi2", u0, w.dt, w.steps * w.dt, tol=w.tol, max_basis=w.max_basis,
+                                             orth_length=w.max_basis)
+    c = pkg.Context(0, orth="dcgs2")
+    op = pkg.Operator(c, w.spec())
+    r = pkg.integrate(c, op, to_dev(u0), "epi2", w.dt, w.steps * w.dt, tol=w.tol, max_basis=w.max_basis,
+                      orth_length=w.max_basis)
+    assert r.status == orc.status == "completed"
+    assert rel(to_host(r.u), orc.u) <= 1e-9
+    d_dev = np.diff(np.concatenate([[0], r.iters_per_step]))
+    d_orc = np.diff(np.concatenate([[0], orc.iters_per_step]))
+    assert np.max(np.abs(d_dev - d_orc)) <= 1
+
+
 @pytest.mark.parametrize("order,dims", [(3, (3, 5, 4)), (3, (4, 4, 1)), (1, (5, 9, 3)), (1, (4, 8, 2))])
 def test_euler3d_march_matches_tile_kernel(monkeypatch, order, dims):
     # odd meshes leave partial 2x2 (order 3) / 4x8 (order 1) tiles; nz = 1 wraps onto itself

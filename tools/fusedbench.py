@@ -1,6 +1,6 @@
 """Fused JVP + DCGS2-dots sweep vs the separate passes, per Krylov column j.
 
-python tools/fusedbench.py [nx] [j,j,...] [C4|C5] : for each j, ms of the JVP alone (EXPDG_E2_DOTS=0 /
+python tools/fusedbench.py [nx] [j,j,...] [C3|C4|C5] : for each j, ms of the JVP alone (EXPDG_E2_DOTS=0 /
 EXPDG_E3_DOTS=0), the DCGS2 dots pass, the fused sweep, and (C4) the fused sweep with the dot arithmetic
 skipped (EXPDG_E2_DBG=1).
 """
@@ -22,13 +22,13 @@ def main():
     js = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 4, 10, 20, 30, 40]
     cfg = sys.argv[3] if len(sys.argv) > 3 else "C4"
     w = configs.scaled(configs.ALL[cfg], nx, steps=1)
-    dv = "EXPDG_E2_DOTS" if cfg == "C4" else "EXPDG_E3_DOTS"
+    dv = {"C4": "EXPDG_E2_DOTS", "C5": "EXPDG_E3_DOTS", "C3": "EXPDG_B2_DOTS"}[cfg]
     u0 = torch.tensor(w.initial_condition(), device="cuda:0")
     ctx = pkg.Context(0, orth="dcgs2")
     ops = {}
     for name, env in (("jvp", {dv: "0"}), ("fused", {dv: "1"}), ("fused_nofma", {dv: "1", "EXPDG_E2_DBG": "1"}),
                       *((("fused_dbg", {dv: "1", "EXPDG_E2_DBG": os.environ["FB_DBG"]}),) if "FB_DBG" in os.environ else ())):
-        for k in ("EXPDG_E2_DOTS", "EXPDG_E3_DOTS", "EXPDG_E2_DBG"):
+        for k in ("EXPDG_E2_DOTS", "EXPDG_E3_DOTS", "EXPDG_B2_DOTS", "EXPDG_E2_DBG"):
             os.environ.pop(k, None)
         os.environ.update(env)
         op = pkg.Operator(ctx, w.spec())
