@@ -64,6 +64,12 @@ class ClockSampler:
                  "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
+            return
+        # nvidia-smi takes ~0.1-0.5 s to print its first row: wait for it, so that a short timed
+        # region (C3: ~0.1 s) still has samples
+        t0 = time.time()
+        while time.time() - t0 < 3.0 and os.path.getsize(self.path) == 0:
+            time.sleep(0.02)
 
     def stop(self):
         if self.proc is None:
@@ -147,6 +153,8 @@ def roofline(dominant, step_achieved, peak, peak_kind, traffic, steps):
     ach = dominant["bytes"] / (dominant["ms"] * 1e-3) / 1e9
     traffic_launch, ncu = None, None
     try:
+        if dominant["ncu_file"] is None:
+            raise FileNotFoundError
         with open(os.path.join(ROOT, "profiles", dominant["ncu_file"])) as f:
             ncu = json.load(f)
         traffic_launch = ncu["dram_over_alg"] * per_launch_bytes
@@ -178,7 +186,7 @@ def run_reference(args, workload):
     world, rank, _ = dist_setup()
     if rank != 0:
         return
-    nx = args.ref_nx
+    nx = args.ref_nx if args.ref_nx > 0 else (10 if workload.kind == "euler3d" else 96)
     procs = args.ref_procs if args.ref_procs > 0 else (os.cpu_count() or 1)
     if procs == 1:
         samples = [cpu_sample(workload, steps=args.steps, nx=nx, warmup=args.warmup)]
@@ -195,10 +203,10 @@ def run_reference(args, workload):
         "unit": "DOF-steps/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * slowest / max(1, s0["steps"]), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload.name, "sample": f"{nx}x{nx} elements (same physics/Courant/Krylov)",
+        "config": {"workload": workload.name, "sample": f"{'x'.join([str(nx)] * (3 if workload.kind == 'euler3d' else 2))} elements (same physics/Courant/Krylov)",
                    "dofs": s0["dofs"], "instances": procs},
         "cpu_baseline": {"value": value, "unit": "DOF-steps/s", "cores": procs, "kind": "port",
-                         "sample": f"oracle EPI2, {workload.name} physics on {nx}x{nx} elements, "
+                         "sample": f"oracle EPI2, {workload.name} physics on {'x'.join([str(nx)] * (3 if workload.kind == 'euler3d' else 2))} elements, "
                                    f"{args.steps} timed steps after {args.warmup} warm-up, {procs} concurrent "
                                    f"single-threaded instances (the reference is single-threaded, "
                                    f"proj/README.md:43-45)"},
@@ -214,9 +222,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C4")
-    ap.add_argument("--ref-nx", type=int, default=96)
+    ap.add_argument("--ref-nx", type=int, default=0,
+                    help="elements per direction of the reference-arm sample (0: 96 in 2D, 10 in 3D)")
     ap.add_argument("--ref-procs", type=int, default=0, help="--impl reference instances (0: all host cores)")
-    ap.add_argument("--cpu-nx", type=int, default=128)
+    ap.add_argument("--cpu-nx", type=int, default=0,
+                    help="elements per direction of the CPU baseline sample (0: 128 in 2D, 12 in 3D)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dominant", action="store_true", help="skip the dominant-kernel event timing")
@@ -300,11 +310,20 @@ def main():
         # context stream over one host-stepped step of the same trajectory; the one with the
         # larger summed time is reported (its algorithmic bytes are accumulated on the device)
         timed = []
+        # the operator sweep of this workload, and the ncu capture (DRAM / algorithmic bytes of
+        # one launch) made on the same config, if any
+        sweep = {
+            "euler2d": ("k_e2_phi_strip<5,LF,8,DOT> (Euler strip JVP + DCGS2 pass-1 dots: reads x, q~, b_1, "
+                        "V_0..V_{j-1}; writes y)", "r01_ncu_dominant_fused.json"),
+            "burgers2d": ("k_b2_phi_strip<5,DOT> (2D Burgers strip JVP + DCGS2 pass-1 dots: reads x, u~, b_1, "
+                          "V_0..V_{j-1}; writes y)", "r01_ncu_dominant_fused_c3.json"),
+            "euler3d": ("k_e3_phi_march<4,DOT> (3D Euler z-march JVP + DCGS2 pass-1 dots: reads x, q~, b_1, "
+                        "V_0..V_{j-1}; writes y)", None),
+        }.get(w.kind, ("operator sweep (JVP of slot j)", None))
         for kind, name, ncu_file in (
                 (1, "k_ts2<TS2_UPD> (DCGS2 update pass: reads V_0..V_{j-1}, u, w; writes u, w)",
-                 "r01_ncu_dominant.json"),
-                (2, "k_e2_phi_strip<5,LF,8,DOT> (Euler strip JVP + DCGS2 pass-1 dots: reads x, q~, b_1, "
-                    "V_0..V_{j-1}; writes y)", "r01_ncu_dominant_fused.json")):
+                 "r01_ncu_dominant.json" if w.kind == "euler2d" else None),
+                (2, sweep[0], sweep[1])):
             ud = u.clone()
             ctx.time_dominant(kind)
             pkg.integrate(ctx, op, ud, "epi2", dt, dt, **{**kw, "use_graph": False})
@@ -355,10 +374,12 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if args.cpu_nx <= 0:
+            args.cpu_nx = 12 if w.kind == "euler3d" else 128
         s = cpu_sample(w, steps=1, nx=args.cpu_nx)
         cpu = {"value": s["value"], "unit": "DOF-steps/s", "cores": 1, "kind": "port",
                "sample": f"oracle EPI2 (CPU restatement of the reference, single-threaded), {w.name} physics "
-                         f"on {args.cpu_nx}x{args.cpu_nx} elements ({s['dofs']} DOF), 1 step, "
+                         f"on {'x'.join([str(args.cpu_nx)] * (3 if w.kind == 'euler3d' else 2))} elements ({s['dofs']} DOF), 1 step, "
                          f"{s['seconds']:.1f} s"}
 
     if rank == 0:
