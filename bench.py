@@ -108,22 +108,27 @@ def dist_setup():
 
 def cpu_sample(workload, steps: int = 1, nx: int = 128, warmup: int = 0):
     """The oracle (CPU restatement of the reference) on a bounded sample of the
-    same physics: same config, Courant rule and Krylov settings on nx x nx."""
+    same physics: same config, Courant rule and Krylov settings on nx x nx.  Loads
+    only oracle/ (the dt rule takes the oracle's LGL nodes), never the CUDA library."""
+    import numpy as np
+
     import oracle
     from paper_2011_01316_b200 import configs
     w = configs.scaled(workload, nx, steps=steps)
     spec = w.spec()
     u0 = oracle.initial_condition(w.config, w.nx, w.order, configs.SEEDS[w.config], w.noise)
-    dt = w.time_step(u0)
+    dt = w.time_step(u0, nodes=oracle.lgl(w.order)[0])
     P = oracle.Problem(spec.kind, spec.order, spec.nx, spec.ny, spec.nz, box=spec.box, periodic=spec.periodic,
-                       kappa=spec.kappa, flux=spec.flux, sigma=spec.sigma, euler_flux=spec.euler_flux)
+                       kappa=spec.kappa, flux=spec.flux, sigma=spec.sigma, euler_flux=spec.euler_flux,
+                       gamma=spec.gamma)
     u = u0
     if warmup:
         u = P.integrate("epi2", u, dt, warmup * dt, tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis).u
     r = P.integrate("epi2", u, dt, steps * dt, tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
     dofs = P.dim
+    per_step = np.diff(np.concatenate([[0], np.asarray(r.iters_per_step)])).astype(int).tolist()
     return {"value": dofs * r.steps / r.seconds, "seconds": r.seconds, "steps": r.steps, "dofs": dofs,
-            "nx": nx, "iterations": r.krylov_iterations}
+            "nx": nx, "iterations": r.krylov_iterations, "iters_per_step": per_step}
 
 
 def _ref_worker(a):
@@ -198,18 +203,25 @@ def run_reference(args, workload):
     slowest = max(x["seconds"] for x in samples)
     s0 = samples[0]
     value = sum(x["dofs"] * x["steps"] for x in samples) / slowest
+    mesh = "x".join([str(nx)] * (3 if workload.kind == "euler3d" else 2))
     line = {
         "impl": "reference", "metric": "DOF-steps/s per exponential-DG step", "value": value,
         "unit": "DOF-steps/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * slowest / max(1, s0["steps"]), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload.name, "sample": f"{'x'.join([str(nx)] * (3 if workload.kind == 'euler3d' else 2))} elements (same physics/Courant/Krylov)",
-                   "dofs": s0["dofs"], "instances": procs},
+        "config": {"workload": workload.name,
+                   "sample": f"{mesh} elements per instance (same physics, Cr_a, Krylov tol / max dim as the "
+                             f"workload; DOF-steps/s is per DOF, so the per-DOF work is comparable when the "
+                             f"Krylov iterations per step match)",
+                   "dofs": s0["dofs"], "instances": procs, "cores": procs,
+                   "krylov_iters_per_step": s0["iters_per_step"]},
         "cpu_baseline": {"value": value, "unit": "DOF-steps/s", "cores": procs, "kind": "port",
-                         "sample": f"oracle EPI2, {workload.name} physics on {'x'.join([str(nx)] * (3 if workload.kind == 'euler3d' else 2))} elements, "
+                         "sample": f"oracle EPI2 (CPU restatement of the reference; the reference itself needs "
+                                   f"Eigen, absent here), {workload.name} physics on {mesh} elements, "
                                    f"{args.steps} timed steps after {args.warmup} warm-up, {procs} concurrent "
-                                   f"single-threaded instances (the reference is single-threaded, "
-                                   f"proj/README.md:43-45)"},
+                                   f"single-threaded instances on {procs} host cores (the reference is "
+                                   f"single-threaded, proj/README.md:43-45); Krylov iterations per step "
+                                   f"{s0['iters_per_step']}"},
         "e2e": {"value": value, "unit": "DOF-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -288,6 +300,11 @@ def main():
     rw = pkg.integrate(ctx, op, u, "epi2", dt, args.warmup * dt, **kw)
     if rw.status != "completed":
         raise RuntimeError(f"warm-up blew up at step {rw.blow_up_step}")
+    # the e2e leg replays the timed trajectory from this same state (same steps, same
+    # Krylov dimensions), from pinned host memory
+    u_start = None if args.no_e2e else torch.empty(n, dtype=torch.float64, pin_memory=True)
+    if u_start is not None:
+        u_start.copy_(u)
 
     # timed region: barrier + synchronize on both sides, device events inside the library
     clocks = ClockSampler(local)
@@ -350,19 +367,20 @@ def main():
     achieved = traffic["alg_bytes"] / (r.loop_ms / 1e3) / 1e9
     iters_per_step = np.diff(np.concatenate([[0], r.iters_per_step])) if len(r.iters_per_step) else []
 
-    # e2e: public API with host buffers, H2D + D2H of u inside every step
+    # e2e: public API with host buffers, H2D + D2H of u inside every step, from the
+    # timed region's start state over the same K steps (one integrate call per step)
     e2e = None
     if not args.no_e2e:
-        uh = torch.empty(n, dtype=torch.float64, pin_memory=True)
-        uh.copy_(u.cpu())
-        uh_np = uh.numpy()
+        uh_np = u_start.numpy()
         if world > 1:
             torch.distributed.barrier()
+        e_iters = []
         t0 = time.perf_counter()
         for _ in range(args.steps):
             re = pkg.integrate(ctx, op, uh_np, "epi2", dt, dt, **kw)
             if re.status != "completed":
                 raise RuntimeError("e2e step blew up")
+            e_iters.append(int(re.krylov_iterations))
         t1 = time.perf_counter()
         e_s = t1 - t0
         if world > 1:
@@ -370,7 +388,8 @@ def main():
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             e_s = float(tt.item())
         e2e = {"value": total_dofs * args.steps / e_s, "unit": "DOF-steps/s", "h2d_bytes_per_step": 8 * n,
-               "d2h_bytes_per_step": 8 * n, "seconds": e_s}
+               "d2h_bytes_per_step": 8 * n, "seconds": e_s, "krylov_iters_per_step": e_iters,
+               "same_trajectory": [int(v) for v in iters_per_step] == e_iters}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -209,6 +209,11 @@ int expdg_integrate_host(expdg_ctx* ctx, expdg_op* op, double* u_host, const exp
  * n <= 130, row-major host in/out: the Eigen MatrixFunctions exp() call site
  * proj/src/phi.cpp:40. */
 int expdg_expm(expdg_ctx* ctx, int n, const double* a_host, double* out_host);
+/* Engine path of the last phi_combination / integrate call (instrumentation, so tests can
+ * assert they ran the path bench.py times): out4 = {DCGS2 orthogonalisation (0: CGS2 / IOP),
+ * the operator sweep took the DCGS2 pass-1 dots of every column, device-resident control in
+ * CUDA-graph WHILE nodes, small-problem fused / cluster engine}. */
+int expdg_ctx_last_path(expdg_ctx* ctx, int* out4);
 /* Controller state of the last phi call (16 doubles, for diagnostics). */
 int expdg_debug_state(expdg_ctx* ctx, double* out16);
 /* Micro-benchmark of one CGS2 streaming pass (mode 0 dots, 1 update+dots,

@@ -89,6 +89,7 @@ EXPORTS = [
     "expdg_op_set_source_fn", "expdg_nccl_unique_id", "expdg_ctx_attach_nccl", "expdg_local_group_create",
     "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
     "expdg_debug_profile", "expdg_ctx_set_fused", "expdg_ctx_time_dominant", "expdg_ctx_dominant_stats",
+    "expdg_ctx_last_path",
 ]
 
 _lib = None
@@ -155,6 +156,7 @@ def lib():
     L.expdg_ctx_set_fused.argtypes = [vp, C.c_int]
     L.expdg_ctx_time_dominant.argtypes = [vp, C.c_int]
     L.expdg_ctx_dominant_stats.argtypes = [vp, dp]
+    L.expdg_ctx_last_path.argtypes = [vp, C.POINTER(C.c_int)]
     _lib = L
     return L
 
@@ -287,6 +289,12 @@ class Context:
         v = np.zeros(3)
         _check(lib().expdg_ctx_dominant_stats(self.h, _np_ptr(v)))
         return {"ms": v[0], "bytes": v[1], "launches": int(v[2])}
+
+    def last_path(self) -> dict:
+        """Engine path of the last phi / integrate call."""
+        v = (C.c_int * 4)()
+        _check(lib().expdg_ctx_last_path(self.h, v))
+        return {"dcgs2": bool(v[0]), "fused_dots": bool(v[1]), "graph": bool(v[2]), "fused_engine": bool(v[3])}
 
     def debug_profile(self) -> dict:
         """Fused small-problem engine: SM cycles per phase of the last run."""

@@ -33,12 +33,13 @@ class Workload:
     tol: float = 1e-10
     max_basis: int = 30
     noise: float = 0.0
+    gamma: float = 1.4
 
     def spec(self):
         from . import OperatorSpec
         return OperatorSpec(kind=self.kind, order=self.order, nx=self.nx, ny=self.ny, nz=self.nz, box=self.box,
                             periodic=self.periodic, kappa=self.kappa, flux=self.flux, sigma=self.sigma,
-                            euler_flux=self.euler_flux)
+                            euler_flux=self.euler_flux, gamma=self.gamma)
 
     def initial_condition(self):
         from . import initial_condition
@@ -50,13 +51,17 @@ class Workload:
         comps = {"burgers1d": 1, "burgers2d": 1, "euler2d": 4, "euler3d": 5}[self.kind]
         return self.nx * self.ny * self.nz * npe * comps
 
-    def time_step(self, u0=None) -> float:
-        """dt, or the C4/C5 rule dt = cfl * dx_min / c_max (proj/src/harness.cpp:216-238)."""
+    def time_step(self, u0=None, nodes=None) -> float:
+        """dt, or the C4/C5 rule dt = cfl * dx_min / c_max (proj/src/harness.cpp:216-238).
+        `nodes`: the LGL nodes of the order (default: the library's host setup; the CPU
+        reference arm passes the oracle's, so it never loads the CUDA library)."""
         if self.dt is not None:
             return self.dt
         import numpy as np
-        from . import lgl_basis
-        x, _, _ = lgl_basis(self.order)
+        if nodes is None:
+            from . import lgl_basis
+            nodes = lgl_basis(self.order)[0]
+        x = np.asarray(nodes)
         gap = min(2.0, float(np.min(np.diff(x))))
         h = min((self.box[1] - self.box[0]) / self.nx, (self.box[3] - self.box[2]) / self.ny)
         if self.kind == "euler3d":
@@ -68,8 +73,8 @@ class Workload:
         rho = q[:, 0]
         vel = [q[:, 1 + d] / rho for d in range(comps - 2)]
         E = q[:, comps - 1]
-        p = 0.4 * (E - 0.5 * rho * sum(v * v for v in vel))
-        a = np.sqrt(1.4 * p / rho)
+        p = (self.gamma - 1.0) * (E - 0.5 * rho * sum(v * v for v in vel))
+        a = np.sqrt(self.gamma * p / rho)
         c = float(np.max(np.max(np.abs(np.stack(vel)), axis=0) + a))
         return self.cfl * dx / c
 

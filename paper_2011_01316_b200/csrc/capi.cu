@@ -56,6 +56,8 @@ struct expdg_ctx {
   double* dts_dev = nullptr;  // dt sequence
   StepRecord* rec_dev = nullptr;
   long long steps_cap = 0;
+  // engine path of the last phi / integrate call (expdg_ctx_last_path)
+  int last_path[4] = {0, 0, 0, 0};
 };
 
 struct expdg_op {
@@ -114,6 +116,9 @@ void validate_desc(const expdg_op_desc& d) {
       (d.kind == EXPDG_EULER3D && (d.ny < 1 || d.nz < 1)))
     throw std::invalid_argument("need at least one element per axis");
   if (!(d.x0 < d.x1)) throw std::invalid_argument("degenerate interval");
+  // build_quad_mesh: "degenerate box" (proj/src/mesh.cpp:99)
+  if (d.kind != EXPDG_BURGERS1D && !(d.y0 < d.y1)) throw std::invalid_argument("degenerate box");
+  if (d.kind == EXPDG_EULER3D && !(d.z0 < d.z1)) throw std::invalid_argument("degenerate box");
   if (d.kind == EXPDG_BURGERS1D || d.kind == EXPDG_BURGERS2D) {
     if (!(d.kappa > 0.0)) throw std::invalid_argument("BurgersOperator: kappa must be positive");
     if (d.sigma < 0.0) throw std::invalid_argument("BurgersOperator: sigma must be nonnegative");
@@ -143,6 +148,20 @@ void map_phi_status(const PhiState& s) {
     case PHI_ERR_DOMAIN: throw std::domain_error("EulerOperator: inadmissible reference state");
     default: throw CudaError("phi engine: controller did not finish (status " + std::to_string(s.status) + ")");
   }
+}
+
+// The engine takes "distributed" from the context's communicator: a whole-mesh or dense
+// operator on a context whose communicator spans several ranks would have its
+// Gram-Schmidt sums allreduced over replicated data (and its phi tail dropped on ranks
+// > 0).  Refuse the combination instead of computing a wrong phi.
+void check_pair(const expdg_ctx* ctx, const expdg_op* op) {
+  if (op->ctx != ctx) throw std::invalid_argument("operator belongs to another context");
+  const bool multi = ctx->comm && ctx->comm->size > 1;
+  if (multi && !op->dev->partitioned())
+    throw std::invalid_argument("context communicator spans " + std::to_string(ctx->comm->size) +
+                                " ranks: the operator must be slab-partitioned (desc.part_begin / part_end)");
+  if (op->dev->partitioned() && !ctx->comm)
+    throw std::invalid_argument("partitioned operator: attach a communicator to the context first");
 }
 
 }  // namespace
@@ -256,6 +275,8 @@ int expdg_op_create(expdg_ctx* ctx, const expdg_op_desc* desc, expdg_op** out) {
     validate_desc(*desc);
     if (desc->part_end > desc->part_begin && !ctx->comm)
       throw std::invalid_argument("partitioned operator: attach a communicator to the context first");
+    if (desc->part_end <= desc->part_begin && ctx->comm && ctx->comm->size > 1)
+      throw std::invalid_argument("context communicator spans several ranks: the operator must be slab-partitioned");
     EXPDG_CUDA(cudaSetDevice(ctx->eng->device));
     auto op = std::make_unique<expdg_op>();
     op->ctx = ctx;
@@ -273,6 +294,8 @@ int expdg_op_create(expdg_ctx* ctx, const expdg_op_desc* desc, expdg_op** out) {
 int expdg_dense_op_create(expdg_ctx* ctx, int n, const double* a_host, expdg_op** out) {
   return guard([&] {
     if (!ctx || !a_host || n < 1) throw std::invalid_argument("dense op: bad arguments");
+    if (ctx->comm && ctx->comm->size > 1)
+      throw std::invalid_argument("dense op: not on a context whose communicator spans several ranks");
     auto op = std::make_unique<expdg_op>();
     op->ctx = ctx;
     op->dev = make_dense(n, a_host);
@@ -382,6 +405,7 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
     if (!(dt > 0.0)) throw std::invalid_argument("phi_combination: dt must be positive");
     if (cfg->max_basis > kMaxBasis) throw Unsupported("phi_combination: max_basis > 128");
     if (cfg->max_basis < 1) throw std::invalid_argument("phi_combination: max_basis must be positive");
+    check_pair(ctx, op);
     if (!op->dev->ref && op->dev->desc.kind != EXPDG_DENSE)
       throw std::invalid_argument("operator not linearized (call expdg_op_linearize)");
     Engine& e = *ctx->eng;
@@ -395,6 +419,10 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
     b.p = p;
     for (int i = 0; i <= p; ++i) b.b[i] = b_dev[i];
     const long long bl0 = e.body_launches;
+    ctx->last_path[0] = c.dcgs;
+    ctx->last_path[1] = c.dcgs && op->dev->fused_dcgs_dots_jmax() >= c.mmax;
+    ctx->last_path[2] = use_graph_default() && !e.comm && !e.fused_ok(*op->dev);
+    ctx->last_path[3] = e.fused_ok(*op->dev) ? 1 : 0;
     e.run_phi(*op->dev, b, use_graph_default() ? 1 : 0);
     EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
     const PhiState& s = *e.st_host;
@@ -415,6 +443,7 @@ int expdg_step_epi2(expdg_ctx* ctx, expdg_op* op, double* u_dev, double dt, cons
                     expdg_krylov_stats* stats) {
   return guard([&] {
     if (!ctx || !op || !u_dev || !cfg) throw std::invalid_argument("null argument");
+    check_pair(ctx, op);
     Engine& e = *ctx->eng;
     const long long n = op->dev->n;
     if (!op->dev->ref && op->dev->desc.kind != EXPDG_DENSE) {
@@ -470,6 +499,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   if (kind < EXPDG_EXP_EULER || kind > EXPDG_EXPRB42) throw Unsupported("integrate: device integrators are "
                                                                         "exp_euler, epi2, exprb32, exprb42");
   if (cfg->krylov.max_basis > kMaxBasis) throw Unsupported("max_basis > 128");
+  check_pair(ctx, op);
   Engine& e = *ctx->eng;
   OpDevice& dev = *op->dev;
   const long long n = dev.n;
@@ -606,6 +636,10 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
                      (dev.partitioned() ? 1 : 0);  // + halo pack kernel
   cudaGraphExec_t ex = nullptr;
   const bool graph = cfg->use_graph != 0 && !e.comm;  // partitioned: host-stepped control
+  ctx->last_path[0] = c1.dcgs;
+  ctx->last_path[1] = c1.dcgs && dev.fused_dcgs_dots_jmax() >= (exprb ? std::max(c1.mmax, c3.mmax) : c1.mmax);
+  ctx->last_path[2] = graph ? 1 : 0;
+  ctx->last_path[3] = fused ? 1 : 0;
   int launched = 0;
 
   // Adds a WHILE node after the current capture position; returns its body graph.
@@ -789,6 +823,13 @@ int expdg_expm(expdg_ctx* ctx, int n, const double* a_host, double* out_host) {
     EXPDG_CUDA(cudaMemcpyAsync(out_host, out, sizeof(double) * n * n, cudaMemcpyDeviceToHost, e.stream));
     EXPDG_CUDA(cudaStreamSynchronize(e.stream));
     cudaFree(out);
+  });
+}
+
+int expdg_ctx_last_path(expdg_ctx* ctx, int* out4) {
+  return guard([&] {
+    if (!ctx || !out4) throw std::invalid_argument("null argument");
+    std::memcpy(out4, ctx->last_path, sizeof(ctx->last_path));
   });
 }
 

@@ -8,7 +8,7 @@
 namespace expdg {
 
 __global__ void k_check_ref(const double* __restrict__ q, long long nelem, int comps, int np, int euler_dim,
-                            int* flag) {
+                            double gm1, int* flag) {
   const long long nodes = nelem * np;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x; g < nodes; g += stride) {
@@ -25,7 +25,7 @@ __global__ void k_check_ref(const double* __restrict__ q, long long nelem, int c
     const double E = b[(1 + euler_dim) * np];
     bool ok = rho > 0.0;
     if (ok) {
-      const double p = 0.4 * (E - 0.5 * m2 / rho);
+      const double p = gm1 * (E - 0.5 * m2 / rho);  // admissible(q, cfg.gamma), proj/src/euler.cpp:8-13
       ok = p > 0.0;
     }
     if (!ok) atomicOr(flag, 2);
@@ -65,7 +65,7 @@ int op_check_ref(OpDevice& op, cudaStream_t s, const double* ref) {
   if (d.kind == EXPDG_EULER2D) { np = np1 * np1; ne = (long long)d.nx * d.ny; comps = 4; edim = 2; }
   if (d.kind == EXPDG_EULER3D) { np = np1 * np1 * np1; ne = (long long)d.nx * d.ny * d.nz; comps = 5; edim = 3; }
   ne = op.n / ((long long)comps * np);  // the owned elements (slab-partitioned operators)
-  k_check_ref<<<592, 256, 0, s>>>(ref, ne, comps, np, edim, flag);
+  k_check_ref<<<592, 256, 0, s>>>(ref, ne, comps, np, edim, d.gamma - 1.0, flag);
   int h = 0;
   EXPDG_CUDA(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
   EXPDG_CUDA(cudaFreeAsync(flag, s));

@@ -52,7 +52,7 @@ def test_iop_window_on_dg_operator(ctx):
     r = pkg.integrate(ctx, op, to_dev(u0), "epi2", dt, w.steps * dt, **kw)
     assert r.status == orc.status
     if r.status == "completed":
-        assert rel(to_host(r.u), orc.u) <= 1e-8
+        assert rel(to_host(r.u), orc.u) <= 1e-9
         assert np.max(np.abs(_dims(r) - _dims(orc))) <= 1
 
 

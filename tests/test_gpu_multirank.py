@@ -289,3 +289,18 @@ def test_partitioned_dcgs2_matches_single_rank(integ):
     assert rel(np.concatenate([o[1] for o in out]), to_host(single.u)) <= 1e-11
     assert np.max(np.abs(np.diff(np.concatenate([[0], out[0][0].iters_per_step])) -
                          np.diff(np.concatenate([[0], single.iters_per_step])))) <= 1
+
+
+def test_whole_mesh_or_dense_op_refused_on_multi_rank_context():
+    # a communicator spanning several ranks makes the engine allreduce every Gram-Schmidt sum
+    # (and drop the phi tail on ranks > 0): only slab-partitioned operators may use it
+    w = configs.scaled(configs.C4, 4, steps=1)
+
+    def fn(r, ctx):
+        with pytest.raises(ValueError):
+            pkg.Operator(ctx, w.spec())
+        with pytest.raises(ValueError):
+            pkg.Operator(ctx, dense=np.eye(3))
+        return True
+
+    assert run_ranks(2, fn) == [True, True]

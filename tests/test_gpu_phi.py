@@ -99,3 +99,26 @@ def test_krylov_error_budget(ctx):
     with pytest.raises(pkg.KrylovError):
         pkg.phi_combination(ctx, op, [None, to_dev(rng.standard_normal(n))], 1.0, tol=1e-12, max_basis=8,
                             max_substeps=1)
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 17, 42, 105, 130])
+def test_device_expm_matches_oracle(ctx, n):
+    # the controller's expm (csrc/ctl.cuh blk_expm: Higham 2005 scaling and squaring, Pade
+    # 3/5/7/9/13) through the exported expdg_expm, against the oracle's restatement of the
+    # Eigen MatrixFunctions exp() the reference calls (proj/src/phi.cpp:40), over 1-norms
+    # 1e-3 .. 300 (every Pade degree and squaring counts 0 .. 9)
+    rng = np.random.default_rng(1000 + n)
+    worst = 0.0
+    for norm in (1e-3, 1e-1, 0.5, 2.0, 5.0, 20.0, 80.0, 300.0):
+        # Hessenberg-like (the controller's input) and dense non-normal, negative-heavy spectra
+        for shape in ("hess", "dense"):
+            A = rng.standard_normal((n, n))
+            if shape == "hess":
+                A = np.triu(A, -1)
+            A -= 0.5 * np.abs(np.diag(np.diag(A))) * (shape == "dense")
+            A *= norm / max(np.abs(A).sum(axis=0).max(), 1e-300)
+            got = ctx.expm(A)
+            ref = oracle.expm(A)
+            assert np.all(np.isfinite(got))
+            worst = max(worst, rel(got, ref))
+    assert worst <= 1e-12, worst
