@@ -35,12 +35,13 @@ int main(int argc, char** argv) {
   cfg.krylov.tol = 1e-10;
   cfg.krylov.max_basis = 40;
   cfg.krylov.orth_length = 40;
-  cfg.on_step = [](int s, double t, double amax, long it, void*) {
+  cfg.snapshot_every = 2;
+  cfg.on_step = [](int s, double t, double amax, long it) {
     std::printf("step %d t=%.3f max|u|=%.6f krylov=%ld\n", s, t, amax, it);
   };
   const IntegrationResult r = integrate(ctx, op, IntegratorKind::epi2, u0, cfg);
-  std::printf("status=%s steps=%d t=%.3f krylov=%ld max_abs=%.6f\n",
+  std::printf("status=%s steps=%d t=%.3f krylov=%ld max_abs=%.6f snapshots=%zu\n",
               r.status == RunStatus::completed ? "completed" : "blew_up", r.steps, r.t, r.krylov_iterations,
-              r.max_abs);
+              r.max_abs, r.snapshots.size());
   return r.status == RunStatus::completed ? 0 : 1;
 }

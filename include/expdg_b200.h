@@ -43,6 +43,7 @@ extern "C" {
 #define EXPDG_EULER2D 3   /* EulerOperator (proj/src/euler.cpp), Lax-Friedrichs split        */
 #define EXPDG_EULER3D 4   /* extension: 3D Lax-Friedrichs Euler (config C5)                  */
 #define EXPDG_DENSE 5     /* dense matrix LinearAction (the test fakes of proj/tests/test_phi.cpp) */
+#define EXPDG_USER 6      /* user-supplied LinearAction / SplitProblem (expdg_user_op_create)     */
 
 /* Integrator kinds: IntegratorKind (proj/include/expdg/integrators.hpp:15). */
 #define EXPDG_EXP_EULER 0
@@ -75,6 +76,14 @@ typedef struct {
    * only the owned layers and exchanges one halo layer with its periodic neighbours
    * (rank -+ 1) through the context's communicator. */
   int part_begin, part_end;
+  /* Optional grading lists of build_quad_mesh (proj/src/mesh.cpp:96-120; grade_z: the 3D extension):
+   * host arrays of nx+1 / ny+1 / nz+1 strictly increasing breakpoints spanning [x0, x1] / [y0, y1] /
+   * [z0, z1] exactly ("grading list must span the domain" / "... strictly increasing" otherwise);
+   * NULL: uniform breakpoints.  2D / 3D kinds only (the interval mesh has no grading).  Copied at
+   * operator creation. */
+  const double* grade_x;
+  const double* grade_y;
+  const double* grade_z;
 } expdg_op_desc;
 
 /* KrylovSettings (proj/include/expdg/integrators.hpp:20-24) + the two
@@ -102,6 +111,19 @@ typedef struct {
   double t_final;
   expdg_krylov_cfg krylov;
   int use_graph;  /* 1: device-resident control in CUDA-graph WHILE nodes; 0: host-stepped control */
+  /* TimeLoopConfig::snapshot_every / IntegrationResult::snapshots (proj/include/expdg/integrators.hpp:60,
+   * :73; proj/src/integrators.cpp:195-196): after every snapshot_every-th completed step (0: none), u is
+   * copied into the next of snapshot_cap rows of `snapshots` (snapshot_cap x n doubles: device memory for
+   * expdg_integrate, host memory for expdg_integrate_host) and its time into snapshot_times (host). */
+  int snapshot_every;
+  int snapshot_cap;
+  double* snapshots;
+  double* snapshot_times;
+  /* TimeLoopConfig::on_step (proj/include/expdg/integrators.hpp:62): (step, t, max-norm of u, Krylov
+   * iterations so far) for every completed step, in order, as soon as that step finishes on the device
+   * (a stream-ordered host function: it must not call CUDA).  Not called for the step that blows up. */
+  void (*on_step)(int step, double t, double max_abs, long long krylov_iterations, void* user);
+  void* on_step_user;
 } expdg_time_cfg;
 
 /* IntegrationResult (proj/include/expdg/integrators.hpp:66-74), minus u (in place). */
@@ -112,6 +134,7 @@ typedef struct {
   long long krylov_iterations;
   int blow_up_step;
   double max_abs;
+  int snapshots;  /* snapshots taken (IntegrationResult::snapshots.size(); rows past snapshot_cap not stored) */
 } expdg_integration_result;
 
 const char* expdg_last_error(void);
@@ -161,6 +184,32 @@ int expdg_op_create(expdg_ctx* ctx, const expdg_op_desc* desc, expdg_op** out);
 /* Dense LinearAction y = A x (row-major n x n, host memory): the dense fakes of
  * proj/tests/test_phi.cpp:16-29 and proj/tests/test_integrators.cpp:15-23. */
 int expdg_dense_op_create(expdg_ctx* ctx, int n, const double* a_host, expdg_op** out);
+/* User operator: any reference LinearAction (proj/include/expdg/phi.hpp:11) or SplitProblem
+ * (proj/include/expdg/integrators.hpp:48-52) drives the device phi engine and time loop.
+ * The callbacks receive DEVICE pointers of n doubles and the stream to enqueue on, and return
+ * EXPDG_OK or a status code (EXPDG_E_DOMAIN plays the reference's std::domain_error — inside
+ * integrate it fails the step, which then reports blew_up like proj/src/integrators.cpp:179-193;
+ * EXPDG_E_INVALID plays std::invalid_argument and propagates).
+ *   apply_linear     y = L x at the frozen state (SplitOperator::linear).  Required.
+ *   apply_nonlinear  y = N x (SplitOperator::nonlinear).  NULL: N = 0 (a plain LinearAction).
+ *   linearize        freeze the user's operator at ref (SplitProblem::linearize(ref)); called by
+ *                    expdg_op_linearize and by integrate at u^n every step (at u0 once for
+ *                    exp_euler).  NULL: L does not depend on the state.  ref stays valid until
+ *                    the next linearize call.
+ *   graph_safe       1: the callbacks only enqueue stream-ordered work on `stream` (no host sync,
+ *                    no allocation), so the library may record them once into its CUDA graphs and
+ *                    replay them (device-resident control, no host round-trip per Krylov cycle);
+ *                    their host-side code then runs only while recording.  0: host-stepped
+ *                    control, every callback invoked for real each time.
+ * The engine hands the callbacks fixed scratch vectors (the same x / y pointers every cycle).
+ * Not slab-partitioned: refused on a context whose communicator spans several ranks. */
+typedef struct {
+  int (*apply_linear)(const double* x_dev, double* y_dev, void* stream, void* user);
+  int (*apply_nonlinear)(const double* x_dev, double* y_dev, void* stream, void* user);
+  int (*linearize)(const double* ref_dev, void* stream, void* user);
+  int graph_safe;
+} expdg_user_op_fns;
+int expdg_user_op_create(expdg_ctx* ctx, long long n, const expdg_user_op_fns* fns, void* user, expdg_op** out);
 int expdg_op_destroy(expdg_op* op);
 long long expdg_op_dim(const expdg_op* op);
 
@@ -188,6 +237,18 @@ int expdg_op_full_rhs(expdg_op* op, const double* x_dev, double* y_dev, void* st
  * vectors.  Synchronous; EXPDG_E_KRYLOV maps KrylovError (stats->last_estimate set). */
 int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_dev, int p, double dt,
                           const expdg_krylov_cfg* cfg, double* out_dev, expdg_krylov_stats* stats);
+
+/* krylov_build (proj/include/expdg/phi.hpp:40-42, proj/src/phi.cpp:115-130): Arnoldi
+ * (orth_length >= m) or incomplete-orthogonalisation factorisation of span{seed, L seed, ...}
+ * on the device engine (classical Gram-Schmidt with one reorthogonalisation pass; the
+ * reference's two MGS passes up to rounding; its breakdown test).  seed_dev: n doubles.
+ * Outputs (any may be NULL): basis_dev n x (m+1) column-major device matrix (columns past the
+ * returned m + (invariant ? 0 : 1) are left untouched), hessenberg_host (m+1) x m row-major,
+ * seed_norm, m_out (columns built), invariant (happy breakdown before m).  EXPDG_E_INVALID on a
+ * zero seed ("krylov_build: zero seed"); m <= 128. */
+int expdg_krylov_build(expdg_ctx* ctx, expdg_op* op, const double* seed_dev, int m, int orth_length,
+                       double* basis_dev, double* hessenberg_host, double* seed_norm, int* m_out,
+                       int* invariant);
 
 /* step_epi2 (proj/src/integrators.cpp:76-83) with the op linearised at u:
  * u <- u + phi_combination({0, L u + N u}).  Synchronous. */

@@ -13,6 +13,8 @@
 //   phi_combination(PhiCombinationProblem)            phi_combination(ctx, op, b, dt, settings)
 //   step_epi2(op, u, dt, ks, stats)                   step_epi2(ctx, op, u, dt, ks, stats)
 //   integrate(problem, kind, u0, TimeLoopConfig)      integrate(ctx, op, kind, u0, TimeLoopConfig)
+//   user LinearAction / SplitProblem                  SplitOperator(ctx, n, DeviceSplitProblem{...})
+//   krylov_build(op, seed, m, orth_length)            krylov_build(ctx, op, seed_dev, m, orth_length)
 //   KrylovError{last_estimate}                        KrylovError{last_estimate}
 //   std::invalid_argument / std::domain_error         same types
 #pragma once
@@ -71,15 +73,15 @@ struct KrylovSettings {
 enum class IntegratorKind { exp_euler, epi2, exprb32, exprb42 };
 enum class RunStatus { completed, blew_up };
 
-// proj/include/expdg/integrators.hpp:58-63 (on_step is called after the run, in
-// step order, with the same payload: step, t, max|u|, cumulative iterations)
+// proj/include/expdg/integrators.hpp:58-63.  on_step runs per completed step, in step order,
+// as each step finishes on the device (a stream-ordered host function: no CUDA calls in it)
 struct TimeLoopConfig {
   double dt = 0.1;
   double t_final = 1.0;
   KrylovSettings krylov;
+  int snapshot_every = 0;  // 0: keep no intermediate states
+  std::function<void(int, double, double, long)> on_step;
   bool device_control = true;  // CUDA-graph WHILE-node controller (no host round-trip)
-  void (*on_step)(int, double, double, long, void*) = nullptr;
-  void* on_step_user = nullptr;
 };
 
 // proj/include/expdg/integrators.hpp:66-74
@@ -91,7 +93,53 @@ struct IntegrationResult {
   long krylov_iterations = 0;
   int blow_up_step = -1;
   double max_abs = 0.0;
+  std::vector<std::pair<double, std::vector<double>>> snapshots;
 };
+
+// proj/include/expdg/phi.hpp:30-36 (basis on the host, n x (m+1) column-major)
+struct KrylovFactorization {
+  std::vector<double> basis;
+  std::vector<double> hessenberg;  // (m+1) x m row-major
+  double seed_norm = 0;
+  int m = 0;
+  bool invariant_subspace = false;
+};
+
+// A user LinearAction / SplitProblem on device vectors (proj/include/expdg/phi.hpp:11,
+// proj/include/expdg/integrators.hpp:48-52): linear / nonlinear act on the operator frozen by
+// the last linearize(ref).  Callables may throw std::domain_error / std::invalid_argument like the
+// reference's operators.  graph_safe: they only enqueue work on `stream` (see expdg_user_op_fns).
+struct DeviceSplitProblem {
+  std::function<void(const double* x_dev, double* y_dev, void* stream)> linear;
+  std::function<void(const double* x_dev, double* y_dev, void* stream)> nonlinear;  // empty: N = 0
+  std::function<void(const double* ref_dev, void* stream)> linearize;                // empty: L fixed
+  bool graph_safe = false;
+};
+
+namespace detail {
+template <class F>
+inline int guarded(F&& f) {
+  try {
+    f();
+    return EXPDG_OK;
+  } catch (const std::domain_error&) {
+    return EXPDG_E_DOMAIN;
+  } catch (const std::invalid_argument&) {
+    return EXPDG_E_INVALID;
+  } catch (...) {
+    return EXPDG_E_CUDA;
+  }
+}
+inline int user_linear(const double* x, double* y, void* s, void* u) {
+  return guarded([&] { static_cast<DeviceSplitProblem*>(u)->linear(x, y, s); });
+}
+inline int user_nonlinear(const double* x, double* y, void* s, void* u) {
+  return guarded([&] { static_cast<DeviceSplitProblem*>(u)->nonlinear(x, y, s); });
+}
+inline int user_linearize(const double* r, void* s, void* u) {
+  return guarded([&] { static_cast<DeviceSplitProblem*>(u)->linearize(r, s); });
+}
+}  // namespace detail
 
 class Context {
  public:
@@ -132,7 +180,20 @@ class SplitOperator {
   SplitOperator(Context& ctx, int n, const double* dense_rowmajor) : ctx_(&ctx) {
     check(expdg_dense_op_create(ctx.get(), n, dense_rowmajor, &h_));
   }
-  ~SplitOperator() { expdg_op_destroy(h_); }
+  // a user LinearAction / SplitProblem (kept alive by this object)
+  SplitOperator(Context& ctx, long long n, DeviceSplitProblem problem)
+      : ctx_(&ctx), user_(new DeviceSplitProblem(std::move(problem))) {
+    expdg_user_op_fns f{};
+    f.apply_linear = detail::user_linear;
+    f.apply_nonlinear = user_->nonlinear ? detail::user_nonlinear : nullptr;
+    f.linearize = user_->linearize ? detail::user_linearize : nullptr;
+    f.graph_safe = user_->graph_safe ? 1 : 0;
+    check(expdg_user_op_create(ctx.get(), n, &f, user_, &h_));
+  }
+  ~SplitOperator() {
+    expdg_op_destroy(h_);
+    delete user_;
+  }
   SplitOperator(const SplitOperator&) = delete;
   SplitOperator& operator=(const SplitOperator&) = delete;
 
@@ -164,10 +225,27 @@ class SplitOperator {
     check(expdg_op_full_rhs(h_, x_dev, y_dev, stream));
   }
 
+
  private:
   Context* ctx_;
   expdg_op* h_ = nullptr;
+  DeviceSplitProblem* user_ = nullptr;
 };
+
+// proj/src/phi.cpp:115-130 on the device engine
+inline KrylovFactorization krylov_build(Context& ctx, SplitOperator& op, const double* seed_dev, int m,
+                                        int orth_length, double* basis_dev = nullptr) {
+  KrylovFactorization f;
+  std::vector<double> h((size_t)(m + 1) * m);
+  int mo = 0, inv = 0;
+  check(expdg_krylov_build(ctx.get(), op.get(), seed_dev, m, orth_length, basis_dev, h.data(), &f.seed_norm, &mo,
+                           &inv));
+  f.m = mo;
+  f.invariant_subspace = inv != 0;
+  h.resize((size_t)(mo + 1) * mo);
+  f.hessenberg = std::move(h);
+  return f;
+}
 
 // proj/src/phi.cpp:133-260: out = sum_i dt^i phi_i(dt L) b_i (device pointers, b[i] may be null)
 inline KrylovStats phi_combination(Context& ctx, SplitOperator& op, const std::vector<const double*>& b_dev,
@@ -209,6 +287,19 @@ inline IntegrationResult integrate(Context& ctx, SplitOperator& op, IntegratorKi
   const int cap = (int)(cfg.t_final / cfg.dt + 2.5);
   std::vector<long long> iters(cap > 0 ? cap : 1);
   std::vector<double> amax(cap > 0 ? cap : 1);
+  const size_t n = u0.size();
+  const int scap = cfg.snapshot_every > 0 ? cap / cfg.snapshot_every : 0;
+  std::vector<double> snaps((size_t)scap * n), snap_t(scap);
+  t.snapshot_every = cfg.snapshot_every;
+  t.snapshot_cap = scap;
+  t.snapshots = scap ? snaps.data() : nullptr;
+  t.snapshot_times = scap ? snap_t.data() : nullptr;
+  if (cfg.on_step) {
+    t.on_step = [](int s, double tt, double a, long long it, void* u) {
+      (*static_cast<const std::function<void(int, double, double, long)>*>(u))(s, tt, a, (long)it);
+    };
+    t.on_step_user = const_cast<std::function<void(int, double, double, long)>*>(&cfg.on_step);
+  }
   expdg_integration_result r{};
   check(expdg_integrate_host(ctx.get(), op.get(), u0.data(), &t, &r, iters.data(), amax.data(), cap));
   IntegrationResult out;
@@ -219,14 +310,9 @@ inline IntegrationResult integrate(Context& ctx, SplitOperator& op, IntegratorKi
   out.krylov_iterations = (long)r.krylov_iterations;
   out.blow_up_step = r.blow_up_step;
   out.max_abs = r.max_abs;
-  if (cfg.on_step) {
-    const int ok = out.status == RunStatus::completed ? out.steps : out.steps - 1;
-    double tt = 0.0;
-    for (int s = 0; s < ok && s < cap; ++s) {
-      tt += cfg.dt < cfg.t_final - tt ? cfg.dt : cfg.t_final - tt;  // proj/src/integrators.cpp:157
-      cfg.on_step(s + 1, tt, amax[s], (long)iters[s], cfg.on_step_user);
-    }
-  }
+  for (int k = 0; k < r.snapshots && k < scap; ++k)
+    out.snapshots.emplace_back(snap_t[k], std::vector<double>(snaps.begin() + (size_t)k * n,
+                                                              snaps.begin() + (size_t)(k + 1) * n));
   return out;
 }
 

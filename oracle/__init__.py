@@ -17,6 +17,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
 _lib = None
+# user LinearAction / SplitProblem callbacks on host vectors: (x, y, user) -> status, (ref, user) -> status
+USER_APPLY = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
+USER_LINEARIZE = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_void_p)
 
 
 def build(force: bool = False) -> str:
@@ -37,6 +40,7 @@ class ProblemDesc(C.Structure):
         ("bc", C.c_int), ("kappa", C.c_double), ("flux", C.c_int), ("sigma", C.c_double),
         ("sigma_adaptive", C.c_int), ("over_integrate", C.c_int),
         ("gamma", C.c_double), ("euler_flux", C.c_int),
+        ("grade_x", C.POINTER(C.c_double)), ("grade_y", C.POINTER(C.c_double)), ("grade_z", C.POINTER(C.c_double)),
     ]
 
 
@@ -59,7 +63,15 @@ def lib():
         L.oracle_integrate.argtypes = [C.c_void_p, C.c_int, dp, C.c_double, C.c_double, C.c_double,
                                        C.c_int, C.c_int, C.c_int, C.POINTER(C.c_long), dp,
                                        C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
-                                       dp, C.POINTER(C.c_long), dp]
+                                       dp, C.POINTER(C.c_long), dp, C.c_int, dp, dp, C.c_int,
+                                       C.POINTER(C.c_int)]
+        L.oracle_phi_user.argtypes = [C.c_int, USER_APPLY, C.c_void_p, C.c_int, dp, C.c_double, C.c_double,
+                                      C.c_int, C.c_int, dp, C.POINTER(C.c_long), C.POINTER(C.c_int), dp]
+        L.oracle_integrate_user.argtypes = [C.c_long, USER_APPLY, USER_APPLY, USER_LINEARIZE, C.c_void_p, C.c_int,
+                                            dp, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                                            C.POINTER(C.c_long), dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                            C.POINTER(C.c_int), dp, C.POINTER(C.c_long), C.c_int, dp, dp,
+                                            C.c_int, C.POINTER(C.c_int)]
         L.oracle_phi_dense_op.argtypes = [C.c_int, dp, C.c_int, dp, C.c_double, C.c_double, C.c_int,
                                           C.c_int, dp, C.POINTER(C.c_long), C.POINTER(C.c_int), dp]
         L.oracle_expm.argtypes = [C.c_int, dp, dp]
@@ -142,6 +154,7 @@ class IntegrationResult:
     iters_per_step: np.ndarray  # cumulative, per completed step
     amax_per_step: np.ndarray
     seconds: float
+    snapshots: list = None
 
 
 class Problem:
@@ -152,7 +165,8 @@ class Problem:
     def __init__(self, kind: str, order: int, nx: int, ny: int = 1, nz: int = 1,
                  box=(0.0, 1.0, 0.0, 1.0, 0.0, 1.0), periodic: bool = True, kappa: float = 0.03,
                  flux: str = "lf", sigma: float = 0.0, sigma_adaptive: bool = False,
-                 over_integrate: bool = False, gamma: float = 1.4, euler_flux: str = "lf"):
+                 over_integrate: bool = False, gamma: float = 1.4, euler_flux: str = "lf",
+                 grade_x=None, grade_y=None, grade_z=None):
         d = ProblemDesc()
         d.kind = self.KINDS[kind]
         d.order, d.nx, d.ny, d.nz = order, nx, ny, nz
@@ -161,6 +175,10 @@ class Problem:
         d.kappa, d.flux, d.sigma = kappa, (1 if flux in ("ef", "entropy") else 0), sigma
         d.sigma_adaptive, d.over_integrate = int(sigma_adaptive), int(over_integrate)
         d.gamma, d.euler_flux = gamma, (0 if euler_flux == "roe" else 1)
+        # grading lists (proj/src/mesh.cpp:96-120): kept alive with the problem
+        self._grades = [None if g is None else np.ascontiguousarray(g, dtype=np.float64)
+                        for g in (grade_x, grade_y, grade_z)]
+        d.grade_x, d.grade_y, d.grade_z = [None if g is None else _p(g) for g in self._grades]
         self.desc = d
         self.kind = kind
         self.h = lib().oracle_problem_create(C.byref(d))
@@ -196,22 +214,89 @@ class Problem:
         return a.value, d.value
 
     def integrate(self, integrator: str, u0, dt, t_final, tol=1e-12, max_basis=128,
-                  orth_length=128, max_steps=None) -> IntegrationResult:
+                  orth_length=128, max_steps=None, snapshot_every=0) -> IntegrationResult:
         u = np.array(u0, dtype=np.float64, copy=True)
         nsteps_cap = max_steps or int(np.ceil(t_final / dt + 1e-9)) + 2
         iters = np.zeros(nsteps_cap, dtype=np.int64)
         amax = np.zeros(nsteps_cap)
         steps, status, bus = C.c_int(), C.c_int(), C.c_int()
         mx, tot, secs = C.c_double(), C.c_long(), C.c_double()
+        scap = nsteps_cap // snapshot_every if snapshot_every > 0 else 0
+        snaps, snap_t, nsn = np.zeros((max(scap, 1), self.dim)), np.zeros(max(scap, 1)), C.c_int()
         _check(lib().oracle_integrate(self.h, INTEGRATORS[integrator], _p(u), dt, t_final, tol,
                                       max_basis, orth_length, nsteps_cap,
                                       iters.ctypes.data_as(C.POINTER(C.c_long)), _p(amax),
                                       C.byref(steps), C.byref(status), C.byref(bus), C.byref(mx),
-                                      C.byref(tot), C.byref(secs)))
+                                      C.byref(tot), C.byref(secs), snapshot_every, _p(snaps), _p(snap_t),
+                                      scap, C.byref(nsn)))
         n_ok = steps.value if status.value == 0 else steps.value - 1
-        return IntegrationResult(u, steps.value, "completed" if status.value == 0 else "blew_up",
-                                 bus.value, mx.value, tot.value, iters[:n_ok].copy(),
-                                 amax[:n_ok].copy(), secs.value)
+        res = IntegrationResult(u, steps.value, "completed" if status.value == 0 else "blew_up",
+                                bus.value, mx.value, tot.value, iters[:n_ok].copy(),
+                                amax[:n_ok].copy(), secs.value)
+        res.snapshots = [(float(snap_t[k]), snaps[k].copy()) for k in range(min(nsn.value, scap))]
+        return res
+
+
+def _user_apply(f, n):
+    def cb(x, y, _user):
+        try:
+            out = f(np.ctypeslib.as_array(x, (n,)).copy())
+            np.ctypeslib.as_array(y, (n,))[:] = out
+            return 0
+        except ArithmeticError:
+            return 2
+        except ValueError:
+            return 1
+    return USER_APPLY(cb)
+
+
+def phi_combination_user(apply, n, b_list, dt, tol=1e-12, max_basis=128, orth_length=128):
+    """phi_combination (proj/src/phi.cpp:133-260) with a user LinearAction `apply(x) -> y` (numpy)."""
+    cb = _user_apply(apply, n)
+    b = np.ascontiguousarray(np.stack(b_list), dtype=np.float64)
+    out = np.empty(n)
+    iters, subs, est = C.c_long(), C.c_int(), C.c_double()
+    _check(lib().oracle_phi_user(n, cb, None, len(b_list) - 1, _p(b), dt, tol, max_basis, orth_length,
+                                 _p(out), C.byref(iters), C.byref(subs), C.byref(est)))
+    return out, iters.value, subs.value
+
+
+def integrate_user(n, linearize, integrator, u0, dt, t_final, tol=1e-12, max_basis=128, orth_length=128,
+                   snapshot_every=0) -> IntegrationResult:
+    """integrate (proj/src/integrators.cpp:140-201) of a user SplitProblem: `linearize(ref)` returns
+    (linear, nonlinear) callables on numpy vectors (nonlinear may be None)."""
+    state = {}
+
+    def lin_cb(ref, _user):
+        try:
+            L, N = linearize(np.ctypeslib.as_array(ref, (n,)).copy())
+            state["L"], state["N"] = L, N
+            return 0
+        except ArithmeticError:
+            return 2
+        except ValueError:
+            return 1
+
+    a_l = _user_apply(lambda x: state["L"](x), n)
+    a_n = _user_apply(lambda x: state["N"](x) if state["N"] is not None else np.zeros(n), n)
+    c_lin = USER_LINEARIZE(lin_cb)
+    u = np.array(u0, dtype=np.float64, copy=True)
+    cap = int(np.ceil(t_final / dt + 1e-9)) + 2
+    iters = np.zeros(cap, dtype=np.int64)
+    amax = np.zeros(cap)
+    steps, status, bus, nsn = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    mx, tot = C.c_double(), C.c_long()
+    scap = cap // snapshot_every if snapshot_every > 0 else 0
+    snaps, snap_t = np.zeros((max(scap, 1), n)), np.zeros(max(scap, 1))
+    _check(lib().oracle_integrate_user(n, a_l, a_n, c_lin, None, INTEGRATORS[integrator], _p(u), dt, t_final,
+                                       tol, max_basis, orth_length, cap, iters.ctypes.data_as(C.POINTER(C.c_long)),
+                                       _p(amax), C.byref(steps), C.byref(status), C.byref(bus), C.byref(mx),
+                                       C.byref(tot), snapshot_every, _p(snaps), _p(snap_t), scap, C.byref(nsn)))
+    n_ok = steps.value if status.value == 0 else steps.value - 1
+    res = IntegrationResult(u, steps.value, "completed" if status.value == 0 else "blew_up", bus.value, mx.value,
+                            tot.value, iters[:n_ok].copy(), amax[:n_ok].copy(), 0.0)
+    res.snapshots = [(float(snap_t[k]), snaps[k].copy()) for k in range(min(nsn.value, scap))]
+    return res
 
 
 def phi_combination_dense(A, b_list, dt, tol=1e-12, max_basis=128, orth_length=128):

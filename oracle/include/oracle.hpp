@@ -102,10 +102,11 @@ struct Mesh {
 };
 Mesh build_interval_mesh(double a, double b, int ne, BoundaryKind bc);
 Mesh build_quad_mesh(double x0, double x1, double y0, double y1, int nx, int ny,
-                     BoundaryKind bc);
+                     BoundaryKind bc, const Vec& grade_x = {}, const Vec& grade_y = {});
 // Extension (C5): periodic hex mesh, x-faces then y-faces then z-faces.
 Mesh build_hex_mesh(double x0, double x1, double y0, double y1, double z0,
-                    double z1, int nx, int ny, int nz);
+                    double z1, int nx, int ny, int nz, const Vec& grade_x = {},
+                    const Vec& grade_y = {}, const Vec& grade_z = {});
 double min_node_spacing(const Mesh& mesh, const NodalBasis& b);
 std::vector<int> face_node_indices(const Mesh& mesh, const NodalBasis& b,
                                    const Face& f, bool owner_side);
@@ -354,6 +355,7 @@ enum class RunStatus { completed, blew_up };
 struct TimeLoopConfig {
   double dt = 0.1, t_final = 1.0;
   KrylovSettings krylov;
+  int snapshot_every = 0;  // 0: keep no intermediate states
   std::function<void(int, double, double, long)> on_step;
 };
 struct IntegrationResult {
@@ -364,6 +366,7 @@ struct IntegrationResult {
   long krylov_iterations = 0;
   int blow_up_step = -1;
   double max_abs = 0.0;
+  std::vector<std::pair<double, Vec>> snapshots;
 };
 IntegrationResult integrate(const SplitProblem& problem, IntegratorKind kind, Vec u0,
                             const TimeLoopConfig& cfg);

@@ -27,6 +27,11 @@ typedef struct {
   int over_integrate;
   double gamma;
   int euler_flux;  // 0 roe, 1 lax_friedrichs
+  // optional grading lists (build_quad_mesh grade_x / grade_y, proj/src/mesh.cpp:96-120; 3D: + grade_z),
+  // nx+1 / ny+1 / nz+1 breakpoints, NULL: uniform
+  const double* grade_x;
+  const double* grade_y;
+  const double* grade_z;
 } oracle_problem_desc;
 
 }
@@ -110,8 +115,19 @@ void* oracle_problem_create(const oracle_problem_desc* d) {
     switch (d->kind) {
       case 1: P->mesh = build_interval_mesh(d->x0, d->x1, d->nx, bc); break;
       case 2:
-      case 3: P->mesh = build_quad_mesh(d->x0, d->x1, d->y0, d->y1, d->nx, d->ny, bc); break;
-      case 4: P->mesh = build_hex_mesh(d->x0, d->x1, d->y0, d->y1, d->z0, d->z1, d->nx, d->ny, d->nz); break;
+      case 3: {
+        const Vec gx = d->grade_x ? Vec(d->grade_x, d->grade_x + d->nx + 1) : Vec();
+        const Vec gy = d->grade_y ? Vec(d->grade_y, d->grade_y + d->ny + 1) : Vec();
+        P->mesh = build_quad_mesh(d->x0, d->x1, d->y0, d->y1, d->nx, d->ny, bc, gx, gy);
+        break;
+      }
+      case 4: {
+        const Vec gx = d->grade_x ? Vec(d->grade_x, d->grade_x + d->nx + 1) : Vec();
+        const Vec gy = d->grade_y ? Vec(d->grade_y, d->grade_y + d->ny + 1) : Vec();
+        const Vec gz = d->grade_z ? Vec(d->grade_z, d->grade_z + d->nz + 1) : Vec();
+        P->mesh = build_hex_mesh(d->x0, d->x1, d->y0, d->y1, d->z0, d->z1, d->nx, d->ny, d->nz, gx, gy, gz);
+        break;
+      }
       default: throw std::invalid_argument("unknown problem kind");
     }
     P->bcfg.kappa = d->kappa;
@@ -187,7 +203,8 @@ int oracle_burgers_inner(void* h, const double* a, const double* b, double* out)
 int oracle_integrate(void* h, int integrator, double* u, double dt, double t_final, double tol,
                      int max_basis, int orth_length, int max_steps, long* iters_per_step,
                      double* amax_per_step, int* steps_out, int* status_out, int* blow_up_step_out,
-                     double* max_abs_out, long* total_iters_out, double* seconds_out) {
+                     double* max_abs_out, long* total_iters_out, double* seconds_out, int snapshot_every,
+                     double* snaps, double* snap_t, int snap_cap, int* n_snaps) {
   try {
     const Problem& P = *static_cast<Problem*>(h);
     SplitProblem sp;
@@ -208,6 +225,7 @@ int oracle_integrate(void* h, int integrator, double* u, double dt, double t_fin
     tl.krylov.tol = tol;
     tl.krylov.max_basis = max_basis;
     tl.krylov.orth_length = orth_length;
+    tl.snapshot_every = snapshot_every;
     tl.on_step = [&](int step, double, double amax, long iters) {
       if (step - 1 < max_steps) {
         if (iters_per_step) iters_per_step[step - 1] = iters;
@@ -227,6 +245,14 @@ int oracle_integrate(void* h, int integrator, double* u, double dt, double t_fin
     *blow_up_step_out = r.blow_up_step;
     *max_abs_out = r.max_abs;
     *total_iters_out = r.krylov_iterations;
+    int k = 0;
+    for (const auto& sn : r.snapshots) {
+      if (k >= snap_cap) break;
+      if (snap_t) snap_t[k] = sn.first;
+      if (snaps) std::memcpy(snaps + size_t(k) * P.dim, sn.second.data(), sizeof(double) * P.dim);
+      ++k;
+    }
+    if (n_snaps) *n_snaps = (int)r.snapshots.size();
     return 0;
   } catch (const std::invalid_argument& e) { set_err(e.what()); return 1; }
   catch (const std::exception& e) { set_err(e.what()); return 3; }
@@ -256,6 +282,106 @@ int oracle_phi_dense_op(int n, const double* A, int p, const double* b, double d
     if (last_estimate) *last_estimate = e.last_estimate;
     return 4;
   } catch (const std::invalid_argument& e) { set_err(e.what()); return 1; }
+  catch (const std::exception& e) { set_err(e.what()); return 3; }
+}
+
+// ------------------------------------------------------------ user LinearAction / SplitProblem
+// (host callbacks on host vectors: the reference's std::function plug-ins,
+// proj/include/expdg/phi.hpp:11 and proj/include/expdg/integrators.hpp:48-52)
+typedef int (*UserApply)(const double* x, double* y, void* user);
+typedef int (*UserLinearize)(const double* ref, void* user);
+
+static void user_status(int rc, const char* what) {
+  if (rc == 0) return;
+  if (rc == 2) throw std::domain_error(std::string("user operator: ") + what);
+  if (rc == 1) throw std::invalid_argument(std::string("user operator: ") + what);
+  throw std::runtime_error(std::string("user operator: ") + what);
+}
+
+static LinearAction user_action(long n, UserApply f, void* user, const char* what) {
+  return [n, f, user, what](const Vec& v) {
+    Vec y(n, 0.0);
+    if (f) user_status(f(v.data(), y.data(), user), what);
+    return y;
+  };
+}
+
+int oracle_phi_user(int n, UserApply apply, void* user, int p, const double* b, double dt, double tol,
+                    int max_basis, int orth_length, double* out, long* iters, int* substeps,
+                    double* last_estimate) {
+  try {
+    PhiCombinationProblem prob;
+    prob.op = user_action(n, apply, user, "apply_linear");
+    for (int i = 0; i <= p; ++i) prob.b.emplace_back(b + size_t(i) * n, b + size_t(i + 1) * n);
+    prob.dt = dt;
+    prob.tol = tol;
+    prob.max_basis = max_basis;
+    prob.orth_length = orth_length;
+    const PhiCombinationResult r = phi_combination(prob);
+    std::memcpy(out, r.value.data(), sizeof(double) * n);
+    *iters = r.stats.iterations;
+    *substeps = r.stats.substeps;
+    return 0;
+  } catch (const KrylovError& e) {
+    set_err(e.what());
+    if (last_estimate) *last_estimate = e.last_estimate;
+    return 4;
+  } catch (const std::invalid_argument& e) { set_err(e.what()); return 1; }
+  catch (const std::domain_error& e) { set_err(e.what()); return 2; }
+  catch (const std::exception& e) { set_err(e.what()); return 3; }
+}
+
+int oracle_integrate_user(long n, UserApply lin, UserApply nonlin, UserLinearize linearize, void* user,
+                          int integrator, double* u, double dt, double t_final, double tol, int max_basis,
+                          int orth_length, int max_steps, long* iters_per_step, double* amax_per_step,
+                          int* steps_out, int* status_out, int* blow_up_step_out, double* max_abs_out,
+                          long* total_iters_out, int snapshot_every, double* snaps, double* snap_t, int snap_cap,
+                          int* n_snaps) {
+  try {
+    SplitProblem sp;
+    sp.dim = n;
+    sp.linearize = [=](const Vec& ref) {
+      if (linearize) user_status(linearize(ref.data(), user), "linearize");
+      SplitOperator op;
+      op.dim = n;
+      op.linear = user_action(n, lin, user, "apply_linear");
+      op.nonlinear = user_action(n, nonlin, user, "apply_nonlinear");
+      return op;
+    };
+    TimeLoopConfig tl;
+    tl.dt = dt;
+    tl.t_final = t_final;
+    tl.krylov.tol = tol;
+    tl.krylov.max_basis = max_basis;
+    tl.krylov.orth_length = orth_length;
+    tl.snapshot_every = snapshot_every;
+    tl.on_step = [&](int step, double, double amax, long it) {
+      if (step - 1 < max_steps) {
+        if (iters_per_step) iters_per_step[step - 1] = it;
+        if (amax_per_step) amax_per_step[step - 1] = amax;
+      }
+    };
+    const IntegratorKind kinds[] = {IntegratorKind::exp_euler, IntegratorKind::epi2, IntegratorKind::exprb32,
+                                    IntegratorKind::exprb42};
+    if (integrator < 0 || integrator > 3) throw std::invalid_argument("integrate_user: exponential integrators only");
+    IntegrationResult r = integrate(sp, kinds[integrator], Vec(u, u + n), tl);
+    std::memcpy(u, r.u.data(), sizeof(double) * n);
+    *steps_out = r.steps;
+    *status_out = r.status == RunStatus::completed ? 0 : 1;
+    *blow_up_step_out = r.blow_up_step;
+    *max_abs_out = r.max_abs;
+    *total_iters_out = r.krylov_iterations;
+    int k = 0;
+    for (const auto& sn : r.snapshots) {
+      if (k >= snap_cap) break;
+      if (snap_t) snap_t[k] = sn.first;
+      if (snaps) std::memcpy(snaps + size_t(k) * n, sn.second.data(), sizeof(double) * n);
+      ++k;
+    }
+    if (n_snaps) *n_snaps = (int)r.snapshots.size();
+    return 0;
+  } catch (const std::invalid_argument& e) { set_err(e.what()); return 1; }
+  catch (const std::domain_error& e) { set_err(e.what()); return 2; }
   catch (const std::exception& e) { set_err(e.what()); return 3; }
 }
 

@@ -265,6 +265,19 @@ Vec uniform_breaks(double a, double b, int n) {
   xs[n] = b;
   return xs;
 }
+// proj/src/mesh.cpp:18-24
+void check_grading(const Vec& g, double lo, double hi) {
+  if (g.front() != lo || g.back() != hi) throw std::invalid_argument("grading list must span the domain");
+  for (size_t i = 1; i < g.size(); ++i)
+    if (g[i] <= g[i - 1]) throw std::invalid_argument("grading list must be strictly increasing");
+}
+// the grading list when given (its size fixes the element count, proj/src/mesh.cpp:105-118), else uniform
+Vec axis_breaks(const Vec& grade, double lo, double hi, int& n) {
+  if (grade.empty()) return uniform_breaks(lo, hi, n);
+  check_grading(grade, lo, hi);
+  n = int(grade.size()) - 1;
+  return grade;
+}
 int locate(const Vec& breaks, double x) {
   const int n = int(breaks.size()) - 1;
   int i = int(std::upper_bound(breaks.begin(), breaks.end(), x) - breaks.begin()) - 1;
@@ -313,16 +326,16 @@ Mesh build_interval_mesh(double a, double b, int ne, BoundaryKind bc) {
   return mesh;
 }
 
-// proj/src/mesh.cpp:96-227 (uniform breakpoints; grading lists unused on the path)
+// proj/src/mesh.cpp:96-227 (optional grading lists replace the uniform axis breakpoints)
 Mesh build_quad_mesh(double x0, double x1, double y0, double y1, int nx, int ny,
-                     BoundaryKind bc) {
+                     BoundaryKind bc, const Vec& grade_x, const Vec& grade_y) {
   if (!(x0 < x1) || !(y0 < y1)) throw std::invalid_argument("degenerate box");
   if (nx < 1 || ny < 1) throw std::invalid_argument("need at least one element per axis");
   Mesh mesh;
   mesh.dim = 2;
   mesh.bc = bc;
-  mesh.xs = uniform_breaks(x0, x1, nx);
-  mesh.ys = uniform_breaks(y0, y1, ny);
+  mesh.xs = axis_breaks(grade_x, x0, x1, nx);
+  mesh.ys = axis_breaks(grade_y, y0, y1, ny);
   mesh.nx = nx;
   mesh.ny = ny;
   mesh.elements.resize(size_t(nx) * ny);
@@ -365,13 +378,13 @@ Mesh build_quad_mesh(double x0, double x1, double y0, double y1, int nx, int ny,
 }
 
 Mesh build_hex_mesh(double x0, double x1, double y0, double y1, double z0, double z1,
-                    int nx, int ny, int nz) {
+                    int nx, int ny, int nz, const Vec& grade_x, const Vec& grade_y, const Vec& grade_z) {
   Mesh mesh;
   mesh.dim = 3;
   mesh.bc = BoundaryKind::periodic;
-  mesh.xs = uniform_breaks(x0, x1, nx);
-  mesh.ys = uniform_breaks(y0, y1, ny);
-  mesh.zs = uniform_breaks(z0, z1, nz);
+  mesh.xs = axis_breaks(grade_x, x0, x1, nx);
+  mesh.ys = axis_breaks(grade_y, y0, y1, ny);
+  mesh.zs = axis_breaks(grade_z, z0, z1, nz);
   mesh.nx = nx; mesh.ny = ny; mesh.nz = nz;
   mesh.elements.resize(size_t(nx) * ny * nz);
   for (int k = 0; k < nz; ++k)

@@ -168,6 +168,8 @@ IntegrationResult integrate(const SplitProblem& problem, IntegratorKind kind, Ve
       break;
     }
     res.max_abs = std::max(res.max_abs, amax);
+    // proj/src/integrators.cpp:195-196
+    if (cfg.snapshot_every > 0 && res.steps % cfg.snapshot_every == 0) res.snapshots.emplace_back(res.t, res.u);
     if (cfg.on_step) cfg.on_step(res.steps, res.t, amax, stats.iterations);
   }
   res.krylov_iterations = stats.iterations;

@@ -56,6 +56,7 @@ class OpDesc(C.Structure):
         ("flux", C.c_int), ("sigma", C.c_double), ("sigma_adaptive", C.c_int),
         ("over_integrate", C.c_int), ("gamma", C.c_double), ("euler_flux", C.c_int),
         ("part_begin", C.c_int), ("part_end", C.c_int),
+        ("grade_x", C.POINTER(C.c_double)), ("grade_y", C.POINTER(C.c_double)), ("grade_z", C.POINTER(C.c_double)),
     ]
 
 
@@ -68,14 +69,30 @@ class KrylovStatsC(C.Structure):
     _fields_ = [("iterations", C.c_longlong), ("substeps", C.c_int), ("last_estimate", C.c_double)]
 
 
+ON_STEP_FN = C.CFUNCTYPE(None, C.c_int, C.c_double, C.c_double, C.c_longlong, C.c_void_p)
+
+
 class TimeCfg(C.Structure):
     _fields_ = [("integrator", C.c_int), ("dt", C.c_double), ("t_final", C.c_double),
-                ("krylov", KrylovCfg), ("use_graph", C.c_int)]
+                ("krylov", KrylovCfg), ("use_graph", C.c_int), ("snapshot_every", C.c_int),
+                ("snapshot_cap", C.c_int), ("snapshots", C.c_void_p), ("snapshot_times", C.POINTER(C.c_double)),
+                ("on_step", ON_STEP_FN), ("on_step_user", C.c_void_p)]
 
 
 class IntegrationResultC(C.Structure):
     _fields_ = [("t", C.c_double), ("status", C.c_int), ("steps", C.c_int),
-                ("krylov_iterations", C.c_longlong), ("blow_up_step", C.c_int), ("max_abs", C.c_double)]
+                ("krylov_iterations", C.c_longlong), ("blow_up_step", C.c_int), ("max_abs", C.c_double),
+                ("snapshots", C.c_int)]
+
+
+# user LinearAction / SplitProblem callbacks on device vectors (include/expdg_b200.h expdg_user_op_fns)
+USER_APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+USER_LINEARIZE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class UserOpFns(C.Structure):
+    _fields_ = [("apply_linear", USER_APPLY_FN), ("apply_nonlinear", USER_APPLY_FN),
+                ("linearize", USER_LINEARIZE_FN), ("graph_safe", C.c_int)]
 
 
 # symbols declared in include/expdg_b200.h (checked by tests/test_abi.py)
@@ -89,7 +106,7 @@ EXPORTS = [
     "expdg_op_set_source_fn", "expdg_nccl_unique_id", "expdg_ctx_attach_nccl", "expdg_local_group_create",
     "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
     "expdg_debug_profile", "expdg_ctx_set_fused", "expdg_ctx_time_dominant", "expdg_ctx_dominant_stats",
-    "expdg_ctx_last_path",
+    "expdg_ctx_last_path", "expdg_user_op_create", "expdg_krylov_build",
 ]
 
 _lib = None
@@ -157,6 +174,9 @@ def lib():
     L.expdg_ctx_time_dominant.argtypes = [vp, C.c_int]
     L.expdg_ctx_dominant_stats.argtypes = [vp, dp]
     L.expdg_ctx_last_path.argtypes = [vp, C.POINTER(C.c_int)]
+    L.expdg_user_op_create.argtypes = [vp, C.c_longlong, C.POINTER(UserOpFns), vp, C.POINTER(vp)]
+    L.expdg_krylov_build.argtypes = [vp, vp, vp, C.c_int, C.c_int, vp, dp, dp, C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int)]
     _lib = L
     return L
 
@@ -370,6 +390,10 @@ class OperatorSpec:
     gamma: float = 1.4
     euler_flux: str = "lf"
     part: tuple = (0, 0)  # owned element rows [begin, end) of a slab-partitioned 2D Euler mesh
+    # grading lists of build_quad_mesh (proj/src/mesh.cpp:96-120): nx+1 / ny+1 (/ nz+1) breakpoints
+    grade_x: Optional[Sequence[float]] = None
+    grade_y: Optional[Sequence[float]] = None
+    grade_z: Optional[Sequence[float]] = None
 
     def desc(self) -> OpDesc:
         d = OpDesc()
@@ -381,6 +405,10 @@ class OperatorSpec:
         d.sigma_adaptive, d.over_integrate = int(self.sigma_adaptive), int(self.over_integrate)
         d.gamma, d.euler_flux = self.gamma, (0 if self.euler_flux == "roe" else 1)
         d.part_begin, d.part_end = self.part
+        # the library copies the lists at creation; keep them alive until then
+        d._grades = [None if g is None else np.ascontiguousarray(g, dtype=np.float64)
+                     for g in (self.grade_x, self.grade_y, self.grade_z)]
+        d.grade_x, d.grade_y, d.grade_z = [None if g is None else _np_ptr(g) for g in d._grades]
         return d
 
     @property
@@ -451,6 +479,104 @@ class Operator:
         return self._apply("expdg_op_full_rhs", x, out)
 
 
+class _DeviceVector:
+    """A device pointer of n doubles seen by torch (no copy): __cuda_array_interface__."""
+
+    def __init__(self, ptr, n, readonly=False):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, readonly), "version": 3,
+                                         "strides": None, "stream": None}
+
+
+def _status_of(exc) -> int:
+    if isinstance(exc, ArithmeticError):
+        return EXPDG_E_DOMAIN
+    if isinstance(exc, ValueError):
+        return EXPDG_E_INVALID
+    return EXPDG_E_CUDA
+
+
+class SplitProblem:
+    """A user SplitProblem (proj/include/expdg/integrators.hpp:48-52) on device vectors:
+    `linearize(ref) -> (linear, nonlinear)` like the reference's factory, where `ref` is a
+    read-only CUDA tensor and `linear(x) -> y` / `nonlinear(x) -> y` act on CUDA tensors
+    (`nonlinear` may be None: N = 0).  A plain LinearAction is `SplitProblem(n, linear=f)`.
+    Raise ArithmeticError for the reference's std::domain_error (integrate then reports
+    blew_up) and ValueError for std::invalid_argument.  The callables run on the engine's
+    stream (it is torch's current stream inside them).  graph_safe=True lets the library
+    record them once into its CUDA graphs: the actions then take `(x, out)` and write into
+    `out`, enqueueing only allocation-free stream work (e.g. torch ops with `out=` buffers)."""
+
+    def __init__(self, dim: int, linearize=None, linear=None, nonlinear=None, graph_safe: bool = False):
+        if linearize is None and linear is None:
+            raise ValueError("SplitProblem: need linearize(ref) -> (linear, nonlinear) or a fixed linear action")
+        self.dim, self.graph_safe = int(dim), graph_safe
+        self._linearize, self._linear, self._nonlinear = linearize, linear, nonlinear
+
+
+class UserOperator:
+    """Operator of a user SplitProblem on the device engine (expdg_user_op_create)."""
+
+    def __init__(self, ctx: Context, problem: SplitProblem):
+        import torch
+        self.ctx, self.problem, self.dim = ctx, problem, problem.dim
+        n = problem.dim
+        self._L, self._N = problem._linear, problem._nonlinear
+
+        def run(stream, fn):
+            try:
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream or 0, device=f"cuda:{ctx.device}")):
+                    fn()
+                return EXPDG_OK
+            except Exception as e:  # noqa: BLE001 — mapped to the reference's exception types
+                return _status_of(e)
+
+        def vec(p, ro=False):
+            return torch.as_tensor(_DeviceVector(p, n, ro), device=f"cuda:{ctx.device}")
+
+        def apply(which):
+            def cb(x, y, stream, _user):
+                def go():
+                    f = self._L if which == 0 else self._N
+                    out = vec(y)
+                    if f is None:
+                        out.zero_()
+                    elif problem.graph_safe:
+                        f(vec(x, True), out)  # graph-safe actions write into `out`
+                    else:
+                        out.copy_(f(vec(x, True)))
+                return run(stream, go)
+            return cb
+
+        def lin_cb(ref, stream, _user):
+            def go():
+                r = problem._linearize(vec(ref, True))
+                self._L, self._N = (r if isinstance(r, tuple) else (r, None))
+            return run(stream, go)
+
+        self._cbs = (USER_APPLY_FN(apply(0)), USER_APPLY_FN(apply(1)),
+                     USER_LINEARIZE_FN(lin_cb) if problem._linearize is not None else USER_LINEARIZE_FN())
+        f = UserOpFns()
+        f.apply_linear, f.apply_nonlinear, f.linearize = self._cbs
+        f.graph_safe = 1 if problem.graph_safe else 0
+        h = C.c_void_p()
+        _check(lib().expdg_user_op_create(ctx.h, n, C.byref(f), None, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().expdg_op_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    linearize = None  # set below (shared with Operator)
+
+
+for _m in ("linearize", "_apply", "apply_linear", "apply_nonlinear", "full_rhs"):
+    setattr(UserOperator, _m, getattr(Operator, _m))
+
+
 def _kcfg(tol, max_basis, orth_length, initial_basis=0, max_substeps=0) -> KrylovCfg:
     k = KrylovCfg()
     k.tol, k.max_basis, k.orth_length = tol, max_basis, orth_length
@@ -507,12 +633,16 @@ class IntegrationResult:
     iters_per_step: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.int64))
     amax_per_step: np.ndarray = field(default_factory=lambda: np.zeros(0))
     loop_ms: float = 0.0
+    snapshots: list = field(default_factory=list)  # [(t, u)] every snapshot_every steps
 
 
-def integrate(ctx: Context, op: Operator, u0, integrator: str, dt: float, t_final: float, tol=1e-12,
-              max_basis=128, orth_length=128, use_graph: bool = True) -> IntegrationResult:
+def integrate(ctx: Context, op, u0, integrator: str, dt: float, t_final: float, tol=1e-12,
+              max_basis=128, orth_length=128, use_graph: bool = True, snapshot_every: int = 0,
+              on_step=None) -> IntegrationResult:
     """proj/src/integrators.cpp:140-201 on the device.  `u0` may be a CUDA
-    tensor (updated in place) or a host numpy array (copied in/out inside the call)."""
+    tensor (updated in place) or a host numpy array (copied in/out inside the call).
+    snapshot_every / on_step(step, t, max_abs, krylov_iterations): TimeLoopConfig
+    (proj/include/expdg/integrators.hpp:58-63); on_step runs as each step completes."""
     import torch
     cfg = TimeCfg()
     cfg.integrator = INTEGRATORS[integrator]
@@ -522,8 +652,22 @@ def integrate(ctx: Context, op: Operator, u0, integrator: str, dt: float, t_fina
     cap = int(math.ceil(t_final / dt + 1e-9)) + 2
     iters = np.zeros(cap, dtype=np.int64)
     amax = np.zeros(cap)
+    host = isinstance(u0, np.ndarray)
+    n = op.dim
+    scap = cap // snapshot_every if snapshot_every > 0 else 0
+    snap_t = np.zeros(max(scap, 1))
+    snaps = None
+    if scap:
+        snaps = np.zeros((scap, n)) if host else torch.empty((scap, n), dtype=torch.float64, device=u0.device)
+        cfg.snapshot_every, cfg.snapshot_cap = snapshot_every, scap
+        cfg.snapshots = snaps.ctypes.data if host else snaps.data_ptr()
+        cfg.snapshot_times = _np_ptr(snap_t)
+    cb = None
+    if on_step is not None:
+        cb = ON_STEP_FN(lambda s_, t_, a_, it_, _u: on_step(s_, t_, a_, it_))
+        cfg.on_step = cb
     res = IntegrationResultC()
-    if isinstance(u0, np.ndarray):
+    if host:
         u = np.ascontiguousarray(u0, dtype=np.float64)
         _check(lib().expdg_integrate_host(ctx.h, op.h, _np_ptr(u), C.byref(cfg), C.byref(res),
                                           iters.ctypes.data_as(C.POINTER(C.c_longlong)), _np_ptr(amax), cap))
@@ -533,9 +677,39 @@ def integrate(ctx: Context, op: Operator, u0, integrator: str, dt: float, t_fina
         _check(lib().expdg_integrate(ctx.h, op.h, C.c_void_p(_dptr(u)), C.byref(cfg), C.byref(res),
                                      iters.ctypes.data_as(C.POINTER(C.c_longlong)), _np_ptr(amax), cap))
     n_ok = res.steps if res.status == 0 else res.steps - 1
-    return IntegrationResult(u, res.t, "completed" if res.status == 0 else "blew_up", res.steps,
-                             res.krylov_iterations, res.blow_up_step, res.max_abs, iters[:n_ok].copy(),
-                             amax[:n_ok].copy(), ctx.last_loop_ms)
+    out = IntegrationResult(u, res.t, "completed" if res.status == 0 else "blew_up", res.steps,
+                            res.krylov_iterations, res.blow_up_step, res.max_abs, iters[:n_ok].copy(),
+                            amax[:n_ok].copy(), ctx.last_loop_ms)
+    out.snapshots = [(float(snap_t[k]), snaps[k]) for k in range(min(res.snapshots, scap))]
+    return out
+
+
+@dataclass
+class KrylovFactorization:
+    """proj/include/expdg/phi.hpp:30-36."""
+    basis: object        # CUDA tensor n x (m + 1) (n x m on an invariant subspace)
+    hessenberg: np.ndarray  # (m + 1) x m
+    seed_norm: float
+    m: int
+    invariant_subspace: bool
+
+
+def krylov_build(ctx: Context, op, seed, m: int, orth_length: int) -> KrylovFactorization:
+    """proj/src/phi.cpp:115-130 on the device engine: Arnoldi (orth_length >= m) or incomplete
+    orthogonalisation of span{seed, L seed, ...}."""
+    import torch
+    torch.cuda.current_stream().synchronize()
+    n = op.dim
+    basis = torch.zeros((m + 1, n), dtype=torch.float64, device=f"cuda:{ctx.device}")  # column c = row c
+    h = np.zeros((m + 1) * m)
+    sn, mo, inv = C.c_double(), C.c_int(), C.c_int()
+    _check(lib().expdg_krylov_build(ctx.h, op.h, C.c_void_p(_dptr(seed)), m, orth_length,
+                                    C.c_void_p(basis.data_ptr()), _np_ptr(h), C.byref(sn), C.byref(mo),
+                                    C.byref(inv)))
+    k = mo.value
+    cols = k + (0 if inv.value else 1)
+    return KrylovFactorization(basis[:cols].T, h[:(k + 1) * k].reshape(k + 1, k).copy(), sn.value, k,
+                               bool(inv.value))
 
 
 from . import configs  # noqa: E402,F401

@@ -129,6 +129,13 @@ void validate_desc(const expdg_op_desc& d) {
     if (d.euler_flux != 1 && d.kind == EXPDG_EULER3D)
       throw Unsupported("3D Euler: Lax-Friedrichs flux only (the Roe flux is 2D, proj/src/euler.cpp:114-145)");
   }
+  if (d.kind == EXPDG_BURGERS1D && d.grade_x)
+    throw Unsupported("1D Burgers: the interval mesh has uniform breakpoints (proj/src/mesh.cpp:41-94)");
+  if ((d.kind == EXPDG_BURGERS1D || d.kind == EXPDG_BURGERS2D || d.kind == EXPDG_EULER2D) && d.grade_z)
+    throw std::invalid_argument("grade_z: 3D meshes only");
+  host_axis_breaks(d.x0, d.x1, d.nx, d.grade_x);  // throws on a bad grading list
+  if (d.kind != EXPDG_BURGERS1D) host_axis_breaks(d.y0, d.y1, d.ny, d.grade_y);
+  if (d.kind == EXPDG_EULER3D) host_axis_breaks(d.z0, d.z1, d.nz, d.grade_z);
   if (d.part_end > d.part_begin) {
     const int layers = d.kind == EXPDG_BURGERS1D ? d.nx : (d.kind == EXPDG_EULER3D ? d.nz : d.ny);
     if (d.part_begin < 0 || d.part_end > layers) throw std::invalid_argument("slab partition: layers out of range");
@@ -287,6 +294,8 @@ int expdg_op_create(expdg_ctx* ctx, const expdg_op_desc* desc, expdg_op** out) {
       case EXPDG_EULER3D: op->dev = make_euler3d(*desc); break;
     }
     op->dev->comm = ctx->comm.get();
+    // the grading lists were copied into the operator's width tables
+    op->dev->desc.grade_x = op->dev->desc.grade_y = op->dev->desc.grade_z = nullptr;
     *out = op.release();
   });
 }
@@ -299,6 +308,20 @@ int expdg_dense_op_create(expdg_ctx* ctx, int n, const double* a_host, expdg_op*
     auto op = std::make_unique<expdg_op>();
     op->ctx = ctx;
     op->dev = make_dense(n, a_host);
+    *out = op.release();
+  });
+}
+
+int expdg_user_op_create(expdg_ctx* ctx, long long n, const expdg_user_op_fns* fns, void* user, expdg_op** out) {
+  return guard([&] {
+    if (!ctx || !fns || !out || n < 1) throw std::invalid_argument("user op: bad arguments");
+    if (!fns->apply_linear) throw std::invalid_argument("user op: apply_linear is required");
+    if (ctx->comm && ctx->comm->size > 1)
+      throw std::invalid_argument("user op: not on a context whose communicator spans several ranks");
+    EXPDG_CUDA(cudaSetDevice(ctx->eng->device));
+    auto op = std::make_unique<expdg_op>();
+    op->ctx = ctx;
+    op->dev = make_user(n, *fns, user, ctx->eng->num_sms);
     *out = op.release();
   });
 }
@@ -439,6 +462,80 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
   });
 }
 
+__global__ void k_scale_columns(const PhiState* st, const double* base, long long ld, long long n, int cols,
+                                double* out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int c = 0; c < cols; ++c) {
+    const double sc = st->scale[c];
+    const double* src = base + (size_t)c * ld;
+    double* dst = out + (size_t)c * n;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = sc * src[i];
+  }
+}
+
+int expdg_krylov_build(expdg_ctx* ctx, expdg_op* op, const double* seed_dev, int m, int orth_length,
+                       double* basis_dev, double* hessenberg_host, double* seed_norm, int* m_out,
+                       int* invariant) {
+  return guard([&] {
+    if (!ctx || !op || !seed_dev) throw std::invalid_argument("null argument");
+    if (m < 1) throw std::invalid_argument("krylov_build: m must be positive");
+    if (m > kMaxBasis) throw Unsupported("krylov_build: m > 128");
+    check_pair(ctx, op);
+    if (!op->dev->ref && op->dev->desc.kind != EXPDG_DENSE)
+      throw std::invalid_argument("operator not linearized (call expdg_op_linearize)");
+    Engine& e = *ctx->eng;
+    const long long n = op->dev->n;
+    // the plain operator (p = 0: no augmentation, dt = 1), m columns from the seed, then stop
+    // (proj/src/phi.cpp:115-130); CGS2 so every column is final in its own cycle
+    const expdg_krylov_cfg kc{1e-12, m, orth_length, m, 1};
+    e.ensure(n, m);
+    PhiState c = e.config(n, 0, 1.0, kc);
+    c.mmax = m;
+    c.initial_basis = m;
+    c.full_orth = orth_length >= m ? 1 : 0;
+    c.window = c.full_orth ? m : std::max(1, orth_length);
+    c.grow_cap = m;
+    c.dcgs = 0;
+    c.build_only = 1;
+    c.max_steps = 1;
+    e.upload_config(c, e.stream);
+    BArgs b{};
+    b.p = 0;
+    b.b[0] = seed_dev;
+    const int fused_saved = e.use_fused;
+    e.use_fused = 0;
+    const long long bl0 = e.body_launches;
+    try {
+      e.run_phi(*op->dev, b, use_graph_default() ? 1 : 0);
+    } catch (...) {
+      e.use_fused = fused_saved;
+      throw;
+    }
+    e.use_fused = fused_saved;
+    EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
+    const PhiState& st = *e.st_host;
+    const long long hosted = e.body_launches - bl0;
+    ctx->launches += 2 + (hosted > 0 ? hosted : st.body_runs * Engine::body_kernels(*op->dev, false, st.mmax));
+    if (!(st.red.bnorm2[0] > 0.0)) throw std::invalid_argument("krylov_build: zero seed");
+    map_phi_status(st);
+    const int built = st.mc;
+    if (m_out) *m_out = built;
+    if (invariant) *invariant = st.breakdown;
+    if (seed_norm) *seed_norm = st.beta;
+    if (hessenberg_host)
+      for (int i = 0; i <= built; ++i)
+        for (int j = 0; j < built; ++j) hessenberg_host[(size_t)i * built + j] = st.H[(size_t)i * kMaxBasis + j];
+    if (basis_dev) {
+      const int cols = built + (st.breakdown ? 0 : 1);
+      k_scale_columns<<<std::min<long long>(1184, (n + 255) / 256), 256, 0, e.stream>>>(e.st, e.base, e.ld, n, cols,
+                                                                                      basis_dev);
+      ctx->launches++;
+      EXPDG_CUDA(cudaGetLastError());
+    }
+    EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+  });
+}
+
 int expdg_step_epi2(expdg_ctx* ctx, expdg_op* op, double* u_dev, double dt, const expdg_krylov_cfg* cfg,
                     expdg_krylov_stats* stats) {
   return guard([&] {
@@ -473,6 +570,31 @@ int expdg_step_epi2(expdg_ctx* ctx, expdg_op* op, double* u_dev, double dt, cons
     ctx->launches++;
     EXPDG_CUDA(cudaStreamSynchronize(e.stream));
   });
+}
+
+// TimeLoopConfig::on_step from the stream: the step's record is copied to pinned memory
+// behind the step's kernels, then a host function hands it to the callback in step order
+struct OnStepFeed {
+  void (*fn)(int, double, double, long long, void*) = nullptr;
+  void* user = nullptr;
+  StepRecord* rec = nullptr;  // pinned, one per step
+  const double* tcum = nullptr;
+  bool blown = false;
+};
+struct OnStepItem {
+  OnStepFeed* feed;
+  int idx;
+};
+static void CUDART_CB on_step_host(void* p) {
+  const OnStepItem& it = *static_cast<OnStepItem*>(p);
+  OnStepFeed& f = *it.feed;
+  if (f.blown) return;
+  const StepRecord& r = f.rec[it.idx];
+  if (r.status) {  // the failing step: no callback (proj/src/integrators.cpp:186-197)
+    f.blown = true;
+    return;
+  }
+  f.fn(it.idx + 1, f.tcum[it.idx], r.amax, r.iterations_cum, f.user);
 }
 
 static void restore_ref(OpDevice& dev, cudaStream_t s, const double* saved) {
@@ -635,7 +757,10 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   const int body_k = Engine::body_kernels(dev, c1.dcgs != 0, exprb ? std::max(c1.mmax, c3.mmax) : c1.mmax) +
                      (dev.partitioned() ? 1 : 0);  // + halo pack kernel
   cudaGraphExec_t ex = nullptr;
-  const bool graph = cfg->use_graph != 0 && !e.comm;  // partitioned: host-stepped control
+  // partitioned: host-stepped control; user operators: only when their callbacks are graph-safe
+  const bool graph = cfg->use_graph != 0 && !e.comm && dev.graph_capturable();
+  // host callbacks must not see the states after a blow-up: look at `stopped` after every step
+  const bool check_each_step = !dev.graph_capturable();
   ctx->last_path[0] = c1.dcgs;
   ctx->last_path[1] = c1.dcgs && dev.fused_dcgs_dots_jmax() >= (exprb ? std::max(c1.mmax, c3.mmax) : c1.mmax);
   ctx->last_path[2] = graph ? 1 : 0;
@@ -711,6 +836,48 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
       cudaGraphDestroy(g);
       cudaStreamDestroy(cs);
     }
+    // snapshots and on_step, enqueued behind each step
+    const int snap_every = cfg->snapshot_every > 0 ? cfg->snapshot_every : 0;
+    int snaps_taken = 0;
+    std::vector<double> tcum(S);
+    for (int i = 0; i < S; ++i) tcum[i] = (i ? tcum[i - 1] : 0.0) + dts[i];
+    OnStepFeed feed;
+    std::vector<OnStepItem> items;
+    StepRecord* rec_pinned = nullptr;
+    if (cfg->on_step) {
+      EXPDG_CUDA(cudaMallocHost(&rec_pinned, sizeof(StepRecord) * S));
+      feed.fn = cfg->on_step;
+      feed.user = cfg->on_step_user;
+      feed.rec = rec_pinned;
+      feed.tcum = tcum.data();
+      items.resize(S);
+      for (int i = 0; i < S; ++i) items[i] = OnStepItem{&feed, i};
+    }
+    // pending host functions read feed / items / rec_pinned: drain the stream before they go
+    // (also when an exception unwinds this scope)
+    struct PinnedFree {
+      StepRecord*& p;
+      cudaStream_t s;
+      ~PinnedFree() {
+        if (p) {
+          cudaStreamSynchronize(s);
+          cudaFreeHost(p);
+        }
+      }
+    } pinned_free{rec_pinned, e.stream};
+    auto after_step = [&](int idx) {
+      if (snap_every && (idx + 1) % snap_every == 0) {
+        if (snaps_taken < cfg->snapshot_cap && cfg->snapshots)
+          EXPDG_CUDA(cudaMemcpyAsync(cfg->snapshots + (size_t)snaps_taken * n, u, sizeof(double) * n,
+                                     cudaMemcpyDefault, e.stream));
+        ++snaps_taken;
+      }
+      if (cfg->on_step) {
+        EXPDG_CUDA(cudaMemcpyAsync(rec_pinned + idx, rec_dev + idx, sizeof(StepRecord), cudaMemcpyDeviceToHost,
+                                   e.stream));
+        EXPDG_CUDA(cudaLaunchHostFunc(e.stream, on_step_host, &items[idx]));
+      }
+    };
     // lagged early-exit check: launch in chunks, look at `stopped` of the chunk before
     int* stop_host = ctx->stop_host;
     stop_host[0] = stop_host[1] = 0;
@@ -723,6 +890,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
       for (int i = 0; i < cnt; ++i) {
         if (graph) {
           EXPDG_CUDA(cudaGraphLaunch(ex, e.stream));
+          after_step(launched + i);
         } else {
           pre(e.stream);
           if (fused) dev.launch_fused(e.stream, e, b1);
@@ -733,6 +901,15 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
             else host_loop(b2, c3.dcgs != 0, c3.mmax);
           }
           post(e.stream);
+          after_step(launched + i);
+          if (check_each_step) {
+            EXPDG_CUDA(cudaMemcpyAsync(stop_host, &e.st->stopped, sizeof(int), cudaMemcpyDeviceToHost, e.stream));
+            EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+            if (stop_host[0]) {
+              launched += i + 1;
+              goto steps_done;
+            }
+          }
         }
       }
       launched += cnt;
@@ -744,6 +921,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
       EXPDG_CUDA(cudaEventRecord(chunk_ev, e.stream));
       pending = true;
     }
+  steps_done:
     EXPDG_CUDA(cudaEventRecord(ctx->ev1, e.stream));
     EXPDG_CUDA(cudaStreamSynchronize(e.stream));
     float ms = 0.f;
@@ -784,6 +962,16 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
     }
   }
   res->krylov_iterations = st.iterations_total;
+  // snapshots of completed, non-failing steps only (the reference stops before pushing one)
+  const int ok_steps = res->status ? res->blow_up_step - 1 : res->steps;
+  res->snapshots = cfg->snapshot_every > 0 ? ok_steps / cfg->snapshot_every : 0;
+  if (cfg->snapshot_times)
+    for (int k = 0; k < std::min(res->snapshots, cfg->snapshot_cap); ++k)
+      cfg->snapshot_times[k] = k < S ? [&] {
+        double t = 0.0;
+        for (int i = 0; i < (k + 1) * cfg->snapshot_every; ++i) t += dts[i];
+        return t;
+      }() : 0.0;
 }
 
 int expdg_integrate(expdg_ctx* ctx, expdg_op* op, double* u_dev, const expdg_time_cfg* cfg,

@@ -468,7 +468,9 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
           }
         }
       } else if (phase == PH_POST) {
-        if (!st->breakdown) {
+        if (st->build_only) {  // krylov_build (proj/src/phi.cpp:115-130): the factorisation only
+          s_phase = PH_DONE;
+        } else if (!st->breakdown) {
           st->j = st->mc;
           st->action = ACT_AVNORM;
           if (!st->dcgs) st->iterations++;  // DCGS2 counts it when the cycle finds no breakdown

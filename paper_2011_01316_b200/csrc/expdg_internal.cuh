@@ -64,6 +64,8 @@ struct PhiState {
   double tol;
   int mmax, window, grow_cap, max_substeps, full_orth, initial_basis;
   int max_cycles;
+  int build_only;    // krylov_build: stop after the Arnoldi columns (no avnorm / expm / combine)
+  int pad_build;
   // ---- dynamic control
   int action, phase, j, j0, k;
   int target, m, mc, breakdown, status;

@@ -308,6 +308,32 @@ void host_burgers_source(int order, int ne, double a, double b, bool over_integr
 
 // Per-element {h_e, 2 / h_e} of uniform breakpoints (proj/src/mesh.cpp:11-16), for the
 // Burgers element kernels (no divisions on the device).
+// Axis breakpoints: the grading list when given (checked like proj/src/mesh.cpp:18-24), else the
+// uniform breakpoints of proj/src/mesh.cpp:11-16
+std::vector<double> host_axis_breaks(double a, double b, int n, const double* grade) {
+  std::vector<double> xs(n + 1);
+  if (!grade) {
+    for (int i = 0; i <= n; ++i) xs[i] = i == n ? b : a + (b - a) * i / n;
+    return xs;
+  }
+  for (int i = 0; i <= n; ++i) xs[i] = grade[i];
+  if (xs.front() != a || xs.back() != b) throw std::invalid_argument("grading list must span the domain");
+  for (int i = 1; i <= n; ++i)
+    if (xs[i] <= xs[i - 1]) throw std::invalid_argument("grading list must be strictly increasing");
+  return xs;
+}
+
+// {h_e, 2 / h_e} per element of an axis with the given breakpoints
+std::vector<double> host_h_table(const std::vector<double>& xs) {
+  const int ne = (int)xs.size() - 1;
+  std::vector<double> t(2 * (size_t)ne);
+  for (int e = 0; e < ne; ++e) {
+    t[2 * e] = xs[e + 1] - xs[e];
+    t[2 * e + 1] = 2.0 / (xs[e + 1] - xs[e]);
+  }
+  return t;
+}
+
 std::vector<double> host_h_table(double a, double b, int ne) {
   std::vector<double> t(2 * (size_t)ne);
   for (int e = 0; e < ne; ++e) {

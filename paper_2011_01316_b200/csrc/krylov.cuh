@@ -55,6 +55,9 @@ class OpDevice {
   // DCGS2: the apply kernel also takes the pass-1 dots (k_ts2<TS2_DOTS>) of columns
   // j <= this bound (-1: never); k_ts2<TS2_DOTS> no-ops for those columns.
   virtual int fused_dcgs_dots_jmax() const { return -1; }
+  // Whether launch_phi_apply / launch_apply / launch_residual only enqueue stream work that
+  // may be recorded once into a CUDA graph and replayed (user operators may not).
+  virtual bool graph_capturable() const { return true; }
   // Small problems: the whole phi call as one single-CTA kernel (fused.cuh)
   virtual bool fused_capable() const { return false; }
   virtual void launch_fused(cudaStream_t, Engine&, const BArgs&) {}
@@ -73,6 +76,7 @@ std::unique_ptr<OpDevice> make_burgers2d(const expdg_op_desc& d);
 std::unique_ptr<OpDevice> make_euler2d(const expdg_op_desc& d);
 std::unique_ptr<OpDevice> make_euler3d(const expdg_op_desc& d);
 std::unique_ptr<OpDevice> make_dense(int n, const double* a_host);
+std::unique_ptr<OpDevice> make_user(long long n, const expdg_user_op_fns& fns, void* user, int num_sms);
 
 // Host-side LGL basis (same arithmetic as proj/src/basis.cpp:35-85).
 struct HostBasis {
@@ -86,6 +90,8 @@ struct HostOI {
 };
 HostOI host_burgers_oi(int order);
 std::vector<double> host_h_table(double a, double b, int ne);
+std::vector<double> host_h_table(const std::vector<double>& breaks);
+std::vector<double> host_axis_breaks(double a, double b, int n, const double* grade);
 void host_burgers_source(int order, int ne, double a, double b, bool over_integrate,
                          double (*fn)(double, void*), void* user, double* out);
 

@@ -548,8 +548,8 @@ class Burgers2D : public OpDevice {
     comps = 1;
     rowd = (long long)d.nx * NP * NP;
     {
-      std::vector<double> ht = host_h_table(d.x0, d.x1, d.nx);
-      const std::vector<double> hy = host_h_table(d.y0, d.y1, d.ny);
+      std::vector<double> ht = host_h_table(host_axis_breaks(d.x0, d.x1, d.nx, d.grade_x));
+      const std::vector<double> hy = host_h_table(host_axis_breaks(d.y0, d.y1, d.ny, d.grade_y));
       ht.insert(ht.end(), hy.begin(), hy.end());
       EXPDG_CUDA(cudaMalloc(&htab, sizeof(double) * ht.size()));
       EXPDG_CUDA(cudaMemcpy(htab, ht.data(), sizeof(double) * ht.size(), cudaMemcpyHostToDevice));

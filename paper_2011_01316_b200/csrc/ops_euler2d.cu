@@ -954,7 +954,6 @@ __global__ void k_e2_freeze(const double* __restrict__ q, long long nelem, int n
   }
 }
 
-double ubreak(double a, double b, int i, int n) { return i == n ? b : a + (b - a) * i / n; }
 
 template <int NP>
 class Euler2D : public OpDevice {
@@ -1038,9 +1037,11 @@ class Euler2D : public OpDevice {
     P.part = part ? 1 : 0;
     P.gamma = d.gamma;
     std::vector<double> hs(2 * (d.nx + nyl));
-    for (int i = 0; i < d.nx; ++i) hs[i] = ubreak(d.x0, d.x1, i + 1, d.nx) - ubreak(d.x0, d.x1, i, d.nx);
-    for (int j = 0; j < nyl; ++j)
-      hs[d.nx + j] = ubreak(d.y0, d.y1, row0 + j + 1, d.ny) - ubreak(d.y0, d.y1, row0 + j, d.ny);
+    // element widths from the axis breakpoints: uniform or the grading lists (proj/src/mesh.cpp:96-120)
+    const std::vector<double> xs = host_axis_breaks(d.x0, d.x1, d.nx, d.grade_x);
+    const std::vector<double> ys = host_axis_breaks(d.y0, d.y1, d.ny, d.grade_y);
+    for (int i = 0; i < d.nx; ++i) hs[i] = xs[i + 1] - xs[i];
+    for (int j = 0; j < nyl; ++j) hs[d.nx + j] = ys[row0 + j + 1] - ys[row0 + j];
     for (int q = 0; q < d.nx + nyl; ++q) hs[d.nx + nyl + q] = 1.0 / hs[q];
     EXPDG_CUDA(cudaMalloc(&hbuf, sizeof(double) * hs.size()));
     EXPDG_CUDA(cudaMemcpy(hbuf, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice));

@@ -891,7 +891,6 @@ __global__ void k_e3_freeze(const double* __restrict__ q, long long nelem, int n
   }
 }
 
-double ub3(double a, double b, int i, int n) { return i == n ? b : a + (b - a) * i / n; }
 
 template <int NP>
 class Euler3D : public OpDevice {
@@ -944,10 +943,12 @@ class Euler3D : public OpDevice {
     P.part = part ? 1 : 0;
     P.gamma = d.gamma;
     std::vector<double> hs(2 * (d.nx + d.ny + nzl));
-    for (int i = 0; i < d.nx; ++i) hs[i] = ub3(d.x0, d.x1, i + 1, d.nx) - ub3(d.x0, d.x1, i, d.nx);
-    for (int j = 0; j < d.ny; ++j) hs[d.nx + j] = ub3(d.y0, d.y1, j + 1, d.ny) - ub3(d.y0, d.y1, j, d.ny);
-    for (int k = 0; k < nzl; ++k)
-      hs[d.nx + d.ny + k] = ub3(d.z0, d.z1, z0 + k + 1, d.nz) - ub3(d.z0, d.z1, z0 + k, d.nz);
+    const std::vector<double> xs = host_axis_breaks(d.x0, d.x1, d.nx, d.grade_x);
+    const std::vector<double> ys = host_axis_breaks(d.y0, d.y1, d.ny, d.grade_y);
+    const std::vector<double> zs = host_axis_breaks(d.z0, d.z1, d.nz, d.grade_z);
+    for (int i = 0; i < d.nx; ++i) hs[i] = xs[i + 1] - xs[i];
+    for (int j = 0; j < d.ny; ++j) hs[d.nx + j] = ys[j + 1] - ys[j];
+    for (int k = 0; k < nzl; ++k) hs[d.nx + d.ny + k] = zs[z0 + k + 1] - zs[z0 + k];
     EXPDG_CUDA(cudaMalloc(&hbuf, sizeof(double) * hs.size()));
     EXPDG_CUDA(cudaMemcpy(hbuf, hs.data(), sizeof(double) * hs.size(), cudaMemcpyHostToDevice));
     const int nh = d.nx + d.ny + nzl;

@@ -28,4 +28,5 @@ def oracle_problem(spec):
     return oracle.Problem(spec.kind, spec.order, spec.nx, spec.ny, spec.nz, box=spec.box, periodic=spec.periodic,
                           kappa=spec.kappa, flux=spec.flux, sigma=spec.sigma, sigma_adaptive=spec.sigma_adaptive,
                           gamma=spec.gamma, euler_flux=spec.euler_flux,
-                          over_integrate=spec.over_integrate)
+                          over_integrate=spec.over_integrate, grade_x=spec.grade_x, grade_y=spec.grade_y,
+                          grade_z=spec.grade_z)
