@@ -181,10 +181,19 @@ def lib():
     return L
 
 
+import threading as _threading
+
+_user_exc = _threading.local()  # the Python exception a user-operator callback raised last
+
+
 def _check(rc, stats: Optional[KrylovStatsC] = None):
     if rc == EXPDG_OK:
         return
     msg = lib().expdg_last_error().decode()
+    exc = getattr(_user_exc, "e", None)
+    if exc is not None:
+        _user_exc.e = None
+        msg = f"{msg} ({type(exc).__name__}: {exc})"
     if rc == EXPDG_E_INVALID:
         raise ValueError(msg)
     if rc == EXPDG_E_DOMAIN:
@@ -483,7 +492,8 @@ class _DeviceVector:
     """A device pointer of n doubles seen by torch (no copy): __cuda_array_interface__."""
 
     def __init__(self, ptr, n, readonly=False):
-        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, readonly), "version": 3,
+        # torch accepts only writable views; `readonly` documents intent (the library never reads them back)
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
                                          "strides": None, "stream": None}
 
 
@@ -528,6 +538,7 @@ class UserOperator:
                     fn()
                 return EXPDG_OK
             except Exception as e:  # noqa: BLE001 — mapped to the reference's exception types
+                _user_exc.e = e
                 return _status_of(e)
 
         def vec(p, ro=False):

@@ -444,7 +444,7 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
     const long long bl0 = e.body_launches;
     ctx->last_path[0] = c.dcgs;
     ctx->last_path[1] = c.dcgs && op->dev->fused_dcgs_dots_jmax() >= c.mmax;
-    ctx->last_path[2] = use_graph_default() && !e.comm && !e.fused_ok(*op->dev);
+    ctx->last_path[2] = use_graph_default() && !e.comm && !e.fused_ok(*op->dev) && op->dev->graph_capturable();
     ctx->last_path[3] = e.fused_ok(*op->dev) ? 1 : 0;
     e.run_phi(*op->dev, b, use_graph_default() ? 1 : 0);
     EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));

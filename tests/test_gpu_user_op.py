@@ -229,7 +229,8 @@ def test_krylov_build_on_user_operator_matches_oracle(ctx):
     ref = u0_profile()
     L_np, _ = fd_numpy()(ref)
     A = np.stack([L_np(e) for e in np.eye(N)], axis=1)
-    seed = np.cos(np.arange(N) * H)
+    # a generic seed: a smooth one leaves the late Krylov directions at rounding level (ill-determined H)
+    seed = np.random.default_rng(8).standard_normal(N)
     V, Hm, k, inv, sn = oracle.krylov_build(A, seed, 25, 25)
     op = pkg.UserOperator(ctx, pkg.SplitProblem(N, linearize=fd_torch()))
     op.linearize(to_dev(ref))
