@@ -234,6 +234,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C4")
+    ap.add_argument("--nz", type=int, default=0,
+                    help="3D configs: z element count override (C5L --nz 32: one rank's share of the 4-GPU "
+                         "128^3 job on a single GPU; same box, so the same dt)")
     ap.add_argument("--ref-nx", type=int, default=0,
                     help="elements per direction of the reference-arm sample (0: 96 in 2D, 10 in 3D)")
     ap.add_argument("--ref-procs", type=int, default=0, help="--impl reference instances (0: all host cores)")
@@ -250,8 +253,14 @@ def main():
                          "cannot profile kernel nodes of graphs with conditional nodes")
     args = ap.parse_args()
 
+    from dataclasses import replace
+
     from paper_2011_01316_b200 import configs
     workload = configs.ALL[args.config]
+    if args.nz > 0:
+        if workload.kind != "euler3d":
+            raise SystemExit("--nz: 3D configs only")
+        workload = replace(workload, nz=args.nz, name=f"{workload.name}@{workload.nx}x{workload.ny}x{args.nz}")
     if args.impl == "reference":
         run_reference(args, workload)
         return
@@ -265,10 +274,8 @@ def main():
     torch.cuda.set_device(local)
     ctx = pkg.Context(local)
     w = workload
-    u0 = w.initial_condition()
-    dt = w.time_step(u0) if w.dt is None else w.dt
     spec = w.spec()
-    n_global = u0.size
+    n_global = w.dofs
     # N > 1: element-row slabs of the one C4 mesh (strong scaling), halo rows and the
     # Gram-Schmidt / norm sums over NCCL; --partition forces the
     # partitioned path at N = 1 (NCCL world of one) to exercise it on a single GPU.
@@ -290,7 +297,18 @@ def main():
                        "euler3d": (spec.nz, spec.nx * spec.ny * npe ** 3 * 5)}[spec.kind]
         rows = slab_ranges(layers, world)[rank]
         spec.part = rows
-        u0 = u0[rows[0] * blk:rows[1] * blk].copy()
+        if w.config == 5:  # each rank builds only its z-slab (C5L: 5.4 GB global state)
+            u0 = w.initial_condition_slab(*rows)
+        else:
+            u0 = w.initial_condition()[rows[0] * blk:rows[1] * blk].copy()
+    else:
+        u0 = w.initial_condition()
+    # dt = cfl dx_min / c_max over the whole state: the min over ranks of the local rule
+    dt = w.time_step(u0) if w.dt is None else w.dt
+    if world > 1:
+        t_dt = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t_dt, op=torch.distributed.ReduceOp.MIN)
+        dt = float(t_dt.item())
     op = pkg.Operator(ctx, spec)
     n = op.dim
     kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis, use_graph=not args.host_control)
@@ -408,8 +426,13 @@ def main():
             "ms_per_step": 1e3 * loop_s / args.steps, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded strength-5 isentropic vortex + 1e-6 N(0,1) density noise)",
-            "config": {"workload": w.name, "dofs": n_global, "dofs_per_rank": n, "elements": f"{w.nx}x{w.ny}",
+            "data": {"euler2d": "synthetic (seeded strength-5 isentropic vortex + 1e-6 N(0,1) density noise)",
+                     "euler3d": "synthetic (Taylor-Green vortex, Mach 0.1, analytic; per-rank z-slabs)",
+                     "burgers2d": "synthetic (sin(2 pi x) sin(2 pi y) + 0.01 N(0,1) seeded noise)",
+                     "burgers1d": "synthetic (seeded Burgers initial state)"}[w.kind],
+            "config": {"workload": w.name, "dofs": n_global, "dofs_per_rank": n,
+                       "elements": "x".join(str(v) for v in ((w.nx, w.ny, w.nz) if w.kind == "euler3d"
+                                                              else (w.nx, w.ny))),
                        "order": w.order,
                        "dt": dt, "cr_a": w.cfl, "krylov": {"tol": w.tol, "max_basis": w.max_basis,
                                                            "orth_length": w.max_basis},

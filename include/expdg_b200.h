@@ -292,6 +292,11 @@ int expdg_debug_hessenberg(expdg_ctx* ctx, double* out);
 int expdg_lgl_basis(int order, double* nodes, double* weights, double* diff_rowmajor);
 /* Seeded synthetic inputs of BASELINE.json configs 1..5. */
 int expdg_initial_condition(int config, int nx, int order, uint64_t seed, double noise, double* out_host);
+/* Config 5's Taylor-Green state on an nx x ny x nz mesh of box6 = {x0,x1,y0,y1,z0,z1}, z-planes
+ * [layer_begin, layer_end) only: each rank of a z-partitioned run (C5 at 128^3 over N GPUs) builds
+ * just its slab.  The cubic [0, 2 pi]^3 case equals expdg_initial_condition(5, ...) bit for bit. */
+int expdg_initial_condition_slab(int config, int nx, int ny, int nz, int order, const double* box6,
+                                 int layer_begin, int layer_end, double* out_host);
 /* Number of device kernels launched by this context since creation (instrumentation). */
 long long expdg_ctx_kernel_launches(expdg_ctx* ctx);
 /* Device-event time (ms) of the last expdg_integrate call's step loop. */

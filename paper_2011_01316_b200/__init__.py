@@ -106,7 +106,7 @@ EXPORTS = [
     "expdg_op_set_source_fn", "expdg_nccl_unique_id", "expdg_ctx_attach_nccl", "expdg_local_group_create",
     "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
     "expdg_debug_profile", "expdg_ctx_set_fused", "expdg_ctx_time_dominant", "expdg_ctx_dominant_stats",
-    "expdg_ctx_last_path", "expdg_user_op_create", "expdg_krylov_build",
+    "expdg_ctx_last_path", "expdg_user_op_create", "expdg_krylov_build", "expdg_initial_condition_slab",
 ]
 
 _lib = None
@@ -162,6 +162,8 @@ def lib():
     L.expdg_bench_ts.argtypes = [vp, C.c_longlong, C.c_int, C.c_int, C.c_int, dp]
     L.expdg_bench_apply.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, dp]
     L.expdg_initial_condition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, dp]
+    L.expdg_initial_condition_slab.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, dp, C.c_int, C.c_int,
+                                               dp]
     L.expdg_nccl_unique_id.argtypes = [C.c_char_p]
     L.expdg_ctx_attach_nccl.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
     L.expdg_local_group_create.argtypes = [C.c_int, C.POINTER(vp)]
@@ -236,6 +238,18 @@ def initial_condition(config: int, nx: int, order: int, seed: int, noise: float 
     ne = {1: nx, 2: nx, 3: nx * nx, 4: nx * nx, 5: nx ** 3}[config]
     out = np.empty(ne * npe * comps)
     _check(lib().expdg_initial_condition(config, nx, order, seed, noise, _np_ptr(out)))
+    return out
+
+
+def initial_condition_slab(config: int, nx: int, ny: int, nz: int, order: int, layer_begin: int, layer_end: int,
+                           box=(0.0, 2 * math.pi, 0.0, 2 * math.pi, 0.0, 2 * math.pi)) -> np.ndarray:
+    """Config 5's Taylor-Green state, z-planes [layer_begin, layer_end) of an nx x ny x nz mesh
+    (the owned slab of a z-partitioned rank)."""
+    npe = (order + 1) ** 3
+    out = np.empty((layer_end - layer_begin) * nx * ny * npe * 5)
+    b6 = np.ascontiguousarray(box, dtype=np.float64)
+    _check(lib().expdg_initial_condition_slab(config, nx, ny, nz, order, _np_ptr(b6), layer_begin, layer_end,
+                                              _np_ptr(out)))
     return out
 
 

@@ -43,7 +43,16 @@ class Workload:
 
     def initial_condition(self):
         from . import initial_condition
+        if self.config == 5 and not (self.nx == self.ny == self.nz):
+            return self.initial_condition_slab(0, self.nz)
         return initial_condition(self.config, self.nx, self.order, SEEDS[self.config], self.noise)
+
+    def initial_condition_slab(self, layer_begin: int, layer_end: int):
+        """The owned z-slab of a z-partitioned C5 run (no rank builds the global state)."""
+        from . import initial_condition_slab
+        if self.config != 5:
+            raise ValueError("initial_condition_slab: config 5 only (slice the global state otherwise)")
+        return initial_condition_slab(5, self.nx, self.ny, self.nz, self.order, layer_begin, layer_end, self.box)
 
     @property
     def dofs(self) -> int:
@@ -104,7 +113,15 @@ C4 = Workload("C4-euler2d-vortex-1024^2-N4", 4, "euler2d", 4, 1024, 1024, box=(0
 C5 = Workload("C5-euler3d-tgv-64^3-N3", 5, "euler3d", 3, 64, 64, 64, box=(0.0, TWO_PI, 0.0, TWO_PI, 0.0, TWO_PI),
               dt=None, cfl=5.0, steps=50, tol=1e-10, max_basis=40)
 
-ALL = {"C1": C1, "C1s": C1_S3E4, "C2": C2, "C3": C3, "C4": C4, "C5": C5}
+# C5 at the north star's full size, 128^3 (671,088,640 DOF): z-slab partitioned over 2/4/8 GPUs.
+# Memory: ~50 vectors of 5.37 GB (42 Krylov slots at max dim 40, 6 step scratch vectors, the
+# frozen primitives, u, the e2e staging copy) = ~270 GB in all, 134 GB per rank at N = 2,
+# 67 GB at N = 4, 34 GB at N = 8 -- it does not fit one 180 GB B200.  `bench.py --config C5L
+# --nz 32` runs the 128 x 128 x 32 mesh of the same box (one rank's share of the N = 4 job,
+# same dt: dx_min is set by the x/y spacing) on one GPU.
+C5L = replace(C5, name="C5L-euler3d-tgv-128^3-N3", nx=128, ny=128, nz=128)
+
+ALL = {"C1": C1, "C1s": C1_S3E4, "C2": C2, "C3": C3, "C4": C4, "C5": C5, "C5L": C5L}
 
 
 def scaled(w: Workload, nx: int, ny: Optional[int] = None, nz: Optional[int] = None, steps: Optional[int] = None):

@@ -1145,6 +1145,16 @@ int expdg_lgl_basis(int order, double* nodes, double* weights, double* diff) {
   });
 }
 
+int expdg_initial_condition_slab(int config, int nx, int ny, int nz, int order, const double* box6,
+                                 int layer_begin, int layer_end, double* out_host) {
+  return guard([&] {
+    if (!out_host || !box6) throw std::invalid_argument("initial_condition_slab: null argument");
+    if (config != 5) throw Unsupported("initial_condition_slab: config 5 (the z-partitioned Taylor-Green) only");
+    if (order < 1 || order > 20) throw std::invalid_argument("lgl_basis: order must be in [1, 20]");
+    host_tgv_slab(nx, ny, nz, order, box6, layer_begin, layer_end, out_host);
+  });
+}
+
 int expdg_initial_condition(int config, int nx, int order, uint64_t seed, double noise, double* out_host) {
   return guard([&] {
     if (nx < 1 || !out_host) throw std::invalid_argument("initial_condition: bad arguments");

@@ -451,19 +451,35 @@ void host_initial_condition(int cfg, int nx, int order, uint64_t seed, double no
     return;
   }
   if (cfg == 5) {
+    const double box[6] = {0.0, 2.0 * M_PI, 0.0, 2.0 * M_PI, 0.0, 2.0 * M_PI};
+    host_tgv_slab(nx, nx, nx, order, box, 0, nx, out);
+    return;
+  }
+  throw std::invalid_argument("initial_condition: config must be 1..5");
+}
+
+// C5's Taylor-Green state (Mach 0.1, rho0 = 1) on an nx x ny x nz hex mesh of `box`, z-planes
+// [k0, k1) only (element-major, z slowest: the owned slab of a z-partitioned rank, so no rank
+// builds the global array); the cubic 2 pi-periodic case is bit-identical to the oracle's
+// inputs.cpp generator.
+void host_tgv_slab(int nx, int ny, int nz, int order, const double* box, int k0, int k1, double* out) {
+  if (nx < 1 || ny < 1 || nz < 1 || k0 < 0 || k1 > nz || k0 >= k1) throw std::invalid_argument("tgv slab: bad mesh");
+  const HostBasis b = host_lgl_basis(order);
+  const int np1 = order + 1;
+  {
     const double gamma = 1.4, rho0 = 1.0, p0 = 1.0 / (gamma * 0.01);
     const int np = np1 * np1 * np1;
-    const double h = 2.0 * M_PI / nx;
-    for (int k = 0; k < nx; ++k)
-      for (int j = 0; j < nx; ++j)
+    const double hx = (box[1] - box[0]) / nx, hy = (box[3] - box[2]) / ny, hz = (box[5] - box[4]) / nz;
+    for (int k = k0; k < k1; ++k)
+      for (int j = 0; j < ny; ++j)
         for (int i = 0; i < nx; ++i) {
-          const size_t e = ((size_t)k * nx + j) * nx + i;
+          const size_t e = ((size_t)(k - k0) * ny + j) * nx + i;
           for (int c2 = 0; c2 < np1; ++c2)
             for (int c1 = 0; c1 < np1; ++c1)
               for (int c0 = 0; c0 < np1; ++c0) {
-                const double x = i * h + 0.5 * (b.nodes[c0] + 1.0) * h;
-                const double y = j * h + 0.5 * (b.nodes[c1] + 1.0) * h;
-                const double z = k * h + 0.5 * (b.nodes[c2] + 1.0) * h;
+                const double x = box[0] + i * hx + 0.5 * (b.nodes[c0] + 1.0) * hx;
+                const double y = box[2] + j * hy + 0.5 * (b.nodes[c1] + 1.0) * hy;
+                const double z = box[4] + k * hz + 0.5 * (b.nodes[c2] + 1.0) * hz;
                 const double u = std::sin(x) * std::cos(y) * std::cos(z);
                 const double v = -std::cos(x) * std::sin(y) * std::cos(z);
                 const double w = 0.0;
@@ -478,9 +494,7 @@ void host_initial_condition(int cfg, int nx, int order, uint64_t seed, double no
                 out[(e * 5 + 4) * np + node] = E;
               }
         }
-    return;
   }
-  throw std::invalid_argument("initial_condition: config must be 1..5");
 }
 
 }  // namespace expdg

@@ -92,6 +92,7 @@ HostOI host_burgers_oi(int order);
 std::vector<double> host_h_table(double a, double b, int ne);
 std::vector<double> host_h_table(const std::vector<double>& breaks);
 std::vector<double> host_axis_breaks(double a, double b, int n, const double* grade);
+void host_tgv_slab(int nx, int ny, int nz, int order, const double* box, int k0, int k1, double* out);
 void host_burgers_source(int order, int ne, double a, double b, bool over_integrate,
                          double (*fn)(double, void*), void* user, double* out);
 

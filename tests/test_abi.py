@@ -55,3 +55,16 @@ def test_invalid_arguments_map_to_value_error_without_gpu():
         pkg.lgl_basis(0)
     with pytest.raises(ValueError):
         pkg.initial_condition(9, 4, 4, 1)
+
+
+def test_tgv_slab_generator_matches_global_state():
+    # the per-rank C5 slabs (bench.py --config C5L at N > 1) concatenate to the global state
+    import numpy as np
+    import paper_2011_01316_b200 as pkg
+    from paper_2011_01316_b200 import configs
+    full = pkg.initial_condition(5, 6, 3, 0, 0.0)
+    parts = [pkg.initial_condition_slab(5, 6, 6, 6, 3, a, b) for a, b in ((0, 1), (1, 4), (4, 6))]
+    assert np.array_equal(np.concatenate(parts), full)
+    w = configs.scaled(configs.C5L, 4, nz=8)
+    assert np.array_equal(np.concatenate([w.initial_condition_slab(0, 3), w.initial_condition_slab(3, 8)]),
+                          w.initial_condition())

@@ -21,14 +21,14 @@ from tests.gpu_util import rel, to_dev, to_host
 pytestmark = pytest.mark.gpu
 
 
-def run_ranks(parts, fn):
+def run_ranks(parts, fn, orth=None):
     """fn(rank, ctx) on `parts` threads, each with its own context of a local group."""
     group = pkg.LocalGroup(parts)
     out, errs = [None] * parts, []
 
     def body(r):
         try:
-            ctx = pkg.Context(0).attach_local(group, r)
+            ctx = pkg.Context(0, orth=orth).attach_local(group, r)
             out[r] = fn(r, ctx)
         except BaseException as e:  # noqa: BLE001
             errs.append(e)
@@ -304,3 +304,54 @@ def test_whole_mesh_or_dense_op_refused_on_multi_rank_context():
         return True
 
     assert run_ranks(2, fn) == [True, True]
+
+
+def _dcgs2_partition_case(w, spec, axis_layers, layer_size, parts, u0):
+    """single-rank DCGS2 run vs `parts` slab ranks, all with the fused sweep dots."""
+    dt = w.time_step(u0) if w.dt is None else w.dt
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    ctx = pkg.Context(0, orth="dcgs2")
+    single = pkg.integrate(ctx, pkg.Operator(ctx, spec), to_dev(u0), "epi2", dt, w.steps * dt, **kw)
+    assert ctx.last_path()["fused_dots"]
+    ranges = slab_ranges(axis_layers, parts)
+
+    def fn(r, c):
+        o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": ranges[r]}))
+        sl = slice(ranges[r][0] * layer_size, ranges[r][1] * layer_size)
+        res = pkg.integrate(c, o, to_dev(u0[sl]), "epi2", dt, w.steps * dt, **kw)
+        return res, to_host(res.u), c.last_path()
+
+    got = run_ranks(parts, fn, orth="dcgs2")
+    assert all(g[2]["dcgs2"] and g[2]["fused_dots"] for g in got), [g[2] for g in got]
+    assert all(g[0].status == single.status == "completed" for g in got)
+    assert rel(np.concatenate([g[1] for g in got]), to_host(single.u)) <= 1e-11
+    for g in got:
+        assert list(g[0].iters_per_step) == list(got[0][0].iters_per_step)
+    d_part = np.diff(np.concatenate([[0], got[0][0].iters_per_step]))
+    d_single = np.diff(np.concatenate([[0], single.iters_per_step]))
+    assert np.max(np.abs(d_part - d_single)) <= 1
+
+
+def test_partitioned_burgers2d_fused_dcgs2_dots_matches_single_rank():
+    # C3 physics with nx % 32 == 0 (the fused strip dots of k_b2_phi_strip<..,DOT>) over 3 row slabs:
+    # the halo-row branches of the DOT producers against the single-rank run
+    w = configs.scaled(configs.C3, 32, ny=12, steps=2)
+    spec = w.spec()
+    u0 = w.initial_condition() if False else None
+    rng = np.random.default_rng(4)
+    npe = (spec.order + 1) ** 2
+    xs = np.linspace(0, 1, spec.nx * (spec.order + 1))
+    u0 = np.concatenate([0.5 * np.sin(2 * np.pi * (xs[:npe] + 0.1 * jj)) for jj in range(spec.nx * spec.ny)])
+    u0 += 0.01 * rng.standard_normal(u0.size)
+    _dcgs2_partition_case(w, spec, spec.ny, spec.nx * npe, 3, u0)
+
+
+def test_partitioned_euler3d_fused_dcgs2_dots_eight_ranks():
+    # C5 physics (N = 3, whole 2x2 tiles: the fused z-march dots of k_e3_phi_march<..,DOT>) on an
+    # 8 x 8 x 16 mesh over 8 z-slabs of 2 planes: the 8-GPU partition shape of C5 (128^3 / 8 =
+    # 16 planes per rank) at test size
+    w = configs.scaled(configs.C5, 8, nz=16, steps=2)
+    spec = w.spec()
+    spec.box = (0.0, 2 * np.pi, 0.0, 2 * np.pi, 0.0, 2 * np.pi)
+    u0 = pkg.initial_condition_slab(5, 8, 8, 16, spec.order, 0, 16, box=spec.box)
+    _dcgs2_partition_case(w, spec, spec.nz, spec.nx * spec.ny * (spec.order + 1) ** 3 * 5, 8, u0)
