@@ -172,6 +172,12 @@ int expdg_ctx_comm(const expdg_ctx* ctx, int* rank, int* size); /* 0, 1 without 
 #define EXPDG_ORTH_DCGS2 1
 #define EXPDG_ORTH_AUTO 2 /* default: DCGS2 from 2^18 DOF up, CGS2 below (launch-latency bound) */
 int expdg_ctx_set_orthogonalization(expdg_ctx* ctx, int mode);
+/* Pipelined DCGS2 (default 1): each DCGS2 column applies the operator to the previous column's
+ * image (a lookahead) and forms the new candidate's image by the Arnoldi relation, so the update
+ * of column j, that image and the pass-1 dots of column j+1 share ONE stream of the basis
+ * (8 n (j + 6) bytes + one operator application per column instead of two basis streams).
+ * Same projector; 0 selects the two-pass DCGS2. */
+int expdg_ctx_set_pipelined(expdg_ctx* ctx, int enable);
 /* Small problems (1D Burgers, <= 2^15 DOF, one rank, CGS2) run each phi call as one
  * single-CTA kernel with the controller state in shared memory (default 1); 0 forces
  * the multi-kernel engine.  Same algorithm either way. */
@@ -271,7 +277,8 @@ int expdg_integrate_host(expdg_ctx* ctx, expdg_op* op, double* u_host, const exp
  * proj/src/phi.cpp:40. */
 int expdg_expm(expdg_ctx* ctx, int n, const double* a_host, double* out_host);
 /* Engine path of the last phi_combination / integrate call (instrumentation, so tests can
- * assert they ran the path bench.py times): out4 = {DCGS2 orthogonalisation (0: CGS2 / IOP),
+ * assert they ran the path bench.py times): out4 = {DCGS2 orthogonalisation (0: CGS2 / IOP,
+ * 1: DCGS2, 2: pipelined DCGS2 -- one V stream per column),
  * the operator sweep took the DCGS2 pass-1 dots of every column, device-resident control in
  * CUDA-graph WHILE nodes, small-problem fused / cluster engine}. */
 int expdg_ctx_last_path(expdg_ctx* ctx, int* out4);

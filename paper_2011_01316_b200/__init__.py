@@ -107,6 +107,7 @@ EXPORTS = [
     "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
     "expdg_debug_profile", "expdg_ctx_set_fused", "expdg_ctx_time_dominant", "expdg_ctx_dominant_stats",
     "expdg_ctx_last_path", "expdg_user_op_create", "expdg_krylov_build", "expdg_initial_condition_slab",
+    "expdg_ctx_set_pipelined",
 ]
 
 _lib = None
@@ -173,6 +174,7 @@ def lib():
     L.expdg_ctx_set_orthogonalization.argtypes = [vp, C.c_int]
     L.expdg_debug_profile.argtypes = [vp, C.POINTER(C.c_longlong)]
     L.expdg_ctx_set_fused.argtypes = [vp, C.c_int]
+    L.expdg_ctx_set_pipelined.argtypes = [vp, C.c_int]
     L.expdg_ctx_time_dominant.argtypes = [vp, C.c_int]
     L.expdg_ctx_dominant_stats.argtypes = [vp, dp]
     L.expdg_ctx_last_path.argtypes = [vp, C.POINTER(C.c_int)]
@@ -255,9 +257,12 @@ def initial_condition_slab(config: int, nx: int, ny: int, nz: int, order: int, l
 
 # ---------------------------------------------------------------- context / operators
 class Context:
-    def __init__(self, device: int = 0, orth: Optional[str] = None, fused: Optional[bool] = None):
+    def __init__(self, device: int = 0, orth: Optional[str] = None, fused: Optional[bool] = None,
+                 pipelined: Optional[bool] = None):
         """orth: None (auto: DCGS2 from 2^18 DOF up), "dcgs2" or "cgs2" for fully orthogonalised phi calls;
-        fused: None / True runs small 1D Burgers phi calls as one single-CTA kernel, False never."""
+        fused: None / True runs small 1D Burgers phi calls as one single-CTA kernel, False never;
+        pipelined: None / True streams the basis once per DCGS2 column (lookahead application), False
+        runs the two-pass DCGS2."""
         import torch
         torch.cuda.init()
         self.device = device
@@ -270,6 +275,8 @@ class Context:
             _check(lib().expdg_ctx_set_orthogonalization(self.h, 1 if orth == "dcgs2" else 0))
         if fused is not None:
             _check(lib().expdg_ctx_set_fused(self.h, 1 if fused else 0))
+        if pipelined is not None:
+            _check(lib().expdg_ctx_set_pipelined(self.h, 1 if pipelined else 0))
 
     def close(self):
         if getattr(self, "h", None):
@@ -337,7 +344,8 @@ class Context:
         """Engine path of the last phi / integrate call."""
         v = (C.c_int * 4)()
         _check(lib().expdg_ctx_last_path(self.h, v))
-        return {"dcgs2": bool(v[0]), "fused_dots": bool(v[1]), "graph": bool(v[2]), "fused_engine": bool(v[3])}
+        return {"dcgs2": bool(v[0]), "pipelined": v[0] == 2, "fused_dots": bool(v[1]), "graph": bool(v[2]),
+                "fused_engine": bool(v[3])}
 
     def debug_profile(self) -> dict:
         """Fused small-problem engine: SM cycles per phase of the last run."""

@@ -261,6 +261,13 @@ int expdg_ctx_set_orthogonalization(expdg_ctx* ctx, int mode) {
   });
 }
 
+int expdg_ctx_set_pipelined(expdg_ctx* ctx, int enable) {
+  return guard([&] {
+    if (!ctx) throw std::invalid_argument("null argument");
+    ctx->eng->use_pipe = enable != 0;
+  });
+}
+
 int expdg_ctx_set_fused(expdg_ctx* ctx, int enable) {
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null argument");
@@ -442,7 +449,7 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
     b.p = p;
     for (int i = 0; i <= p; ++i) b.b[i] = b_dev[i];
     const long long bl0 = e.body_launches;
-    ctx->last_path[0] = c.dcgs;
+    ctx->last_path[0] = c.dcgs ? (e.use_pipe ? 2 : 1) : 0;
     ctx->last_path[1] = c.dcgs && op->dev->fused_dcgs_dots_jmax() >= c.mmax;
     ctx->last_path[2] = use_graph_default() && !e.comm && !e.fused_ok(*op->dev) && op->dev->graph_capturable();
     ctx->last_path[3] = e.fused_ok(*op->dev) ? 1 : 0;
@@ -450,7 +457,9 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
     EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
     const PhiState& s = *e.st_host;
     const long long hosted = e.body_launches - bl0;  // host-stepped cycles count their launches
-    ctx->launches += 2 + (hosted > 0 ? hosted : s.body_runs * Engine::body_kernels(*op->dev, s.dcgs != 0, s.mmax));
+    ctx->launches += 2 + (hosted > 0 ? hosted
+                                     : s.body_runs * Engine::body_kernels(*op->dev, s.dcgs != 0, s.mmax,
+                                                                          s.dcgs && e.use_pipe));
     if (stats) {
       stats->iterations = s.iterations;
       stats->substeps = s.substeps;
@@ -754,14 +763,15 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   (void)vgrid;
   const bool fused = e.fused_ok(dev);
   const int per_step = (exprb ? 13 : 5) + (e.comm ? 1 : 0) + (fused ? (exprb ? 2 : 1) : 0);
-  const int body_k = Engine::body_kernels(dev, c1.dcgs != 0, exprb ? std::max(c1.mmax, c3.mmax) : c1.mmax) +
-                     (dev.partitioned() ? 1 : 0);  // + halo pack kernel
+  const bool pipe = c1.dcgs && e.use_pipe;
+  const int body_k = Engine::body_kernels(dev, c1.dcgs != 0, exprb ? std::max(c1.mmax, c3.mmax) : c1.mmax, pipe) +
+                     (dev.partitioned() ? (pipe ? 2 : 1) : 0);  // + halo pack kernel(s)
   cudaGraphExec_t ex = nullptr;
   // partitioned: host-stepped control; user operators: only when their callbacks are graph-safe
   const bool graph = cfg->use_graph != 0 && !e.comm && dev.graph_capturable();
   // host callbacks must not see the states after a blow-up: look at `stopped` after every step
   const bool check_each_step = !dev.graph_capturable();
-  ctx->last_path[0] = c1.dcgs;
+  ctx->last_path[0] = c1.dcgs ? (e.use_pipe ? 2 : 1) : 0;
   ctx->last_path[1] = c1.dcgs && dev.fused_dcgs_dots_jmax() >= (exprb ? std::max(c1.mmax, c3.mmax) : c1.mmax);
   ctx->last_path[2] = graph ? 1 : 0;
   ctx->last_path[3] = fused ? 1 : 0;

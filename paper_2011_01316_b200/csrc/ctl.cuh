@@ -206,9 +206,13 @@ __device__ __forceinline__ void set_window(PhiState* st, int j) {
 static __device__ int dcgs_finish(PhiState* st) {
   const int j = st->j;
   const double nd = (double)st->n;
-  // JVP 32n + dots pass 8n(j + 2) + update pass 8n(j + 4); with the dots in the JVP sweep
-  // (dots_fused) u and w are not re-read: 32n + 8n j + 8n(j + 4)
-  st->alg_bytes += 32.0 * nd + 8.0 * nd * (2.0 * j + (st->dots_fused ? 4.0 : 6.0));
+  // stage-1 JVP 32n + dots pass 8n(j + 2) (with the dots in the JVP sweep, dots_fused: u and w
+  // are not re-read, 8n j); then the update pass 8n(j + 4), or with the lookahead (pipelined
+  // DCGS2) the stage-2 JVP 32n + the merged pass 8n(j + 6)
+  if (st->pl_direct) st->alg_bytes += 32.0 * nd + 8.0 * nd * (st->dots_fused ? (double)j : j + 2.0);
+  st->alg_bytes += st->pl_look ? 32.0 * nd + 8.0 * nd * (j + 6.0) : 8.0 * nd * (j + 4.0);
+  // the merged pass left the next column's image (slot j+2) and pass-1 dots
+  st->pl_ready = st->pl_look ? j + 1 : -1;
   double beta = 1.0;
   // distinct PhiState arrays: restrict lets the loads of the loops below be issued ahead
   double* __restrict__ Hm = st->H;
@@ -223,6 +227,7 @@ static __device__ int dcgs_finish(PhiState* st) {
       st->H[j * kMaxBasis + (j - 1)] = 0.0;
       st->mc = j;
       st->breakdown = 1;
+      st->pl_ready = -1;
       return 1;
     }
     st->H[j * kMaxBasis + (j - 1)] = beta;
@@ -248,6 +253,22 @@ static __device__ int dcgs_finish(PhiState* st) {
   st->scale[j + 1] = ib;                                   // u_{j+1} = slot_{j+1} / beta
   st->pre_prev = sqrt(st->red.nrmW * ib * ib + hh);        // ||dt A V_j|| (incl. the augmentation)
   return 0;
+}
+
+// Pipelined DCGS2 flags of the next cycle (see PhiState::pl_direct / pl_look): look ahead on every
+// extension; apply the operator to the candidate directly unless the last merged pass already
+// left this column's image and dots
+__device__ __forceinline__ void set_pipe(PhiState* st) {
+  const int a = st->action;
+  const bool pipe = st->dcgs && st->pipe_cfg;
+  // the avnorm cycle looks ahead too when the space may still grow: a direct application in the
+  // middle of a pipelined basis injects the recurrence's accumulated rounding into H at once
+  // (on the stiff criterion-5 operator, ||dt A|| ~ 2e3, direct re-applications after grows or
+  // periodic restarts cost 4-6 digits of H at m = 128; one uninterrupted recurrence keeps it at
+  // the two-pass DCGS2 level, tools/pipe_hess.py); slot j+2 exists for j < mmax
+  st->pl_look = pipe && (a == ACT_EXTEND || (a == ACT_AVNORM && st->j < st->grow_cap));
+  const bool restart = st->j > 0 && st->pipe_restart > 0 && st->j % st->pipe_restart == 0;
+  st->pl_direct = !(pipe && (a == ACT_EXTEND || a == ACT_AVNORM) && st->pl_ready == st->j && !restart);
 }
 
 __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W, double* Wsm, int ws_cap,
@@ -458,6 +479,7 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
             st->beta = beta;
             st->mc = 0;
             st->breakdown = 0;
+            st->pl_ready = -1;  // slot 0 holds a new phi vector
             st->scale[0] = 1.0 / beta;
             st->dc_pending = 0;
             st->target = st->m;
@@ -496,7 +518,10 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
     const int rows = st->mmax + 1;
     for (int idx = tid; idx < rows * kMaxBasis; idx += blockDim.x) st->H[idx] = 0.0;
   }
-  if (tid == 0) st->phase = s_phase;
+  if (tid == 0) {
+    st->phase = s_phase;
+    set_pipe(st);
+  }
   if (tid == 0 && s_done && use_graph) cudaGraphSetConditional(cond, 0u);
 }
 

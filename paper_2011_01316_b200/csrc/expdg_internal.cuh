@@ -65,9 +65,24 @@ struct PhiState {
   int mmax, window, grow_cap, max_substeps, full_orth, initial_basis;
   int max_cycles;
   int build_only;    // krylov_build: stop after the Arnoldi columns (no avnorm / expm / combine)
-  int pad_build;
-  // ---- dynamic control
-  int action, phase, j, j0, k;
+  int pipe_cfg;      // pipelined DCGS2 allowed (see pl_direct / pl_look)
+  int pipe_restart;  // diagnostics: apply the operator directly to every pipe_restart-th candidate
+  double* base;      // slot 0 of the Krylov workspace (stage-1 operator applications)
+  // ---- dynamic control (action, phase, j, pl_direct, pl_look: read back together by
+  // host-stepped loops, Engine::fetch_control)
+  int action, phase, j;
+  // Pipelined DCGS2 (dcgs.cu k_ts3): the merged pass of column j also builds the next
+  // candidate's operator image by the Arnoldi relation from a lookahead application
+  // dt A (slot j+1) written to slot j+2, plus the next column's pass-1 dots, so V is
+  // streamed once per column.  Per cycle:
+  //   pl_direct  stage-1 application dt A (s_j slot_j) -> slot j+1 and the pass-1 dots run
+  //              (substep start, after a grow, CGS2 / IOP); 0: slot j+1 and the dots come
+  //              from the previous cycle's merged pass
+  //   pl_look    stage-2 (lookahead) application dt A (s_j slot_{j+1}) -> slot j+2 and the
+  //              merged pass instead of the plain update pass
+  int pl_direct, pl_look;
+  int pl_ready;      // column whose W (slot j+1) and pass-1 dots the last merged pass left (-1: none)
+  int j0, k;
   int target, m, mc, breakdown, status;
   long long iterations;  // this call
   int substeps;          // this call
@@ -112,6 +127,9 @@ struct PhiState {
   double dc_gp;              // gamma used by the update pass (Pythagorean beta)
   double pre_prev;           // ||dt A V_{j-1}|| (the lagged breakdown test, proj/src/phi.cpp:104-108)
   long long dc_fixups;       // Pythagorean vs exact reorthogonalised norm disagreed (diagnostic)
+  double dc_wsc;             // W_true = dc_wsc * slot_{j+1} (1 after a stage-1 application, s_j after a merged pass)
+  double pl_zy, pl_zw, pl_kj; // merged pass: znew = zy Y - zw W - sum_l kappa_l slot_l - kj unew
+  double pl_kappa[kMaxSlots];
   double dc_a[kMaxSlots];      // a_i = <V_i, u>
   double dc_b[kMaxSlots];      // b_i = <V_i, w>
   double dc_g[kMaxSlots];      // (H a)_l with column j-1 corrected, l < j
@@ -144,6 +162,21 @@ struct PhiState {
   // copies the scalar state plus only the rows in use
   alignas(16) double H[(kMaxBasis + 1) * kMaxBasis];
 };
+
+#ifdef __CUDACC__
+// Stage of a phi-cycle operator application: 1 = the candidate s_j slot_j -> slot j+1 (base is
+// the workspace), 2 = pipelined DCGS2 lookahead s_j slot_{j+1} -> slot j+2 (the engine passes
+// base + ld, so every operator kernel's "slot j" / "slot j+1" address the next slots).
+__device__ __forceinline__ int apply_stage(const PhiState* st, const double* base) {
+  return base == st->base ? 1 : 2;
+}
+__device__ __forceinline__ bool apply_go(const PhiState* st, const double* base) {
+  if (st->stopped) return false;
+  if (apply_stage(st, base) == 2) return st->pl_look != 0 && (st->action == ACT_EXTEND || st->action == ACT_AVNORM);
+  const int a = st->action;
+  return (a == ACT_EXTEND || a == ACT_AVNORM) && st->pl_direct;
+}
+#endif
 
 // One record per integrate step, read back by the host at the end.
 struct StepRecord {

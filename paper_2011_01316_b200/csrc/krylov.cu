@@ -377,6 +377,9 @@ __global__ void k_phi_start(PhiState* st) {
     st->action = ACT_START;
   }
   st->phase = PH_SUBSTEP;
+  st->pl_direct = 1;
+  st->pl_look = 0;
+  st->pl_ready = -1;
 }
 
 // ------------------------------------------------------------------ host side
@@ -400,6 +403,8 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_TS_MIN_T")) ts_tuning.min_T = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_LD_ODD")) ld_odd = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_FUSED")) use_fused = std::atoi(v);
+  if (const char* v = std::getenv("EXPDG_PIPE")) use_pipe = std::atoi(v);
+  if (const char* v = std::getenv("EXPDG_PIPE_RESTART")) pipe_restart = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_ORTH"))
     use_dcgs = std::strcmp(v, "cgs2") == 0 ? 0 : (std::strcmp(v, "dcgs2") == 0 ? 2 : 1);
   dcgs_init_attrs(maxsm);
@@ -480,6 +485,11 @@ PhiState Engine::config(long long n, int p, double dt, const expdg_krylov_cfg& k
   // DCGS2 saves a streaming pass per column; below ~2^18 DOF the passes are launch-
   // latency bound and CGS2's lighter kernels win (C1: 789 vs 904 us/step)
   c.dcgs = (c.full_orth && use_dcgs && (use_dcgs == 2 || n >= (1LL << 18))) ? 1 : 0;
+  c.pipe_cfg = use_pipe;
+  c.pipe_restart = pipe_restart;
+  c.pl_direct = 1;
+  c.pl_look = 0;
+  c.pl_ready = -1;
   c.grow_cap = c.full_orth ? c.mmax : std::min(c.mmax, 32);  // :177
   c.max_cycles = 200000;
   c.action = ACT_NONE;
@@ -489,6 +499,7 @@ PhiState Engine::config(long long n, int p, double dt, const expdg_krylov_cfg& k
 // Uploads only the configuration prefix of PhiState (dynamic fields are reset on device).
 void Engine::upload_config(const PhiState& c, cudaStream_t s) {
   std::memcpy(st_host, &c, sizeof(PhiState));
+  st_host->base = base;  // stage-1 applications address the workspace itself (apply_stage)
   EXPDG_CUDA(cudaMemcpyAsync(st, st_host, sizeof(PhiState), cudaMemcpyHostToDevice, s));
 }
 
@@ -524,8 +535,9 @@ void Engine::launch_ts(cudaStream_t s, int mode) {
   }
 }
 
-int Engine::body_kernels(const OpDevice& op, bool dcgs, int mmax) {
-  if (dcgs) return (mmax >= 0 && op.fused_dcgs_dots_jmax() >= mmax) ? 5 : 6;
+int Engine::body_kernels(const OpDevice& op, bool dcgs, int mmax, bool pipe) {
+  // pipelined DCGS2: + the stage-2 application and the merged pass
+  if (dcgs) return ((mmax >= 0 && op.fused_dcgs_dots_jmax() >= mmax) ? 5 : 6) + (pipe ? 2 : 0);
   return op.fused_dots() ? 5 : 6;
 }
 
@@ -562,24 +574,40 @@ void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraph
     EXPDG_CUDA(cudaEventRecord(upd_events[upd_used + 1], s));
     upd_used += 2;
   };
-  if (ext) {
+  if (ext && (!dcgs || !known || !use_pipe || st_host->pl_direct)) {
     timed(2, [&] { op.launch_phi_apply(s, st, base, partials, b); });
     reduce(s);
     body_launches += 1 + pack;
   }
   if (dcgs) {  // one dots pass + coefficients + one update pass (dcgs.cu)
     const int fj = op.fused_dcgs_dots_jmax();
+    // pipelined DCGS2 (PhiState::pl_direct / pl_look), when the host knows this cycle's flags
+    const bool pipe = use_pipe != 0;
+    const bool hdirect = !known || !pipe || st_host->pl_direct;
+    const bool hlook = pipe && (!known || st_host->pl_look);
     if (ext) {
       // the dots pass, unless the operator kernel takes the dots of every column (or of this one)
-      if (!(mmax >= 0 && fj >= mmax) && !(known && hj <= fj)) {
+      // or the last merged pass took them
+      if (!(mmax >= 0 && fj >= mmax) && !(known && hj <= fj) && hdirect) {
         launch_dcgs(s, *this, 0, fj);
         reduce(s);
         ++body_launches;
       }
       launch_dcgs(s, *this, 1);
-      timed(1, [&] { launch_dcgs(s, *this, 2); });
+      ++body_launches;
+      if (hlook) {  // the lookahead application dt A (s_j slot_{j+1}) -> slot j+2
+        timed(2, [&] { op.launch_phi_apply(s, st, base + ld, partials, b, 2); });
+        body_launches += 1 + pack;
+      }
+      if (!known || !hlook) {
+        timed(1, [&] { launch_dcgs(s, *this, 2); });
+        ++body_launches;
+      }
+      if (hlook) {
+        timed(1, [&] { launch_dcgs(s, *this, 3); });
+        ++body_launches;
+      }
       reduce(s);
-      body_launches += 2;
     }
     if (comb) {
       launch_ts(s, TS_COMBINE);
@@ -663,8 +691,8 @@ double Engine::upd_ms() const {
 }
 
 void Engine::fetch_control(cudaStream_t s) {
-  // action, phase, j are consecutive ints of PhiState
-  EXPDG_CUDA(cudaMemcpyAsync(&st_host->action, &st->action, 3 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  // action, phase, j, pl_direct, pl_look are consecutive ints of PhiState
+  EXPDG_CUDA(cudaMemcpyAsync(&st_host->action, &st->action, 5 * sizeof(int), cudaMemcpyDeviceToHost, s));
   EXPDG_CUDA(cudaMemcpyAsync(&st_host->stopped, &st->stopped, sizeof(int), cudaMemcpyDeviceToHost, s));
   EXPDG_CUDA(cudaStreamSynchronize(s));
 }

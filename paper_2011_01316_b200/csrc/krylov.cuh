@@ -42,8 +42,11 @@ class OpDevice {
   Comm* comm = nullptr;
   bool partitioned() const { return desc.part_end > desc.part_begin; }
   // Cycle apply: y = dt * aug(s_j V_j) into slot j+1 plus ||y||^2 (action EXTEND/AVNORM).
+  // stage 2 (pipelined DCGS2 lookahead): the engine passes base + ld, so the kernels apply the
+  // operator to s_j slot_{j+1} and write slot j+2; operators then pick their plain (no fused
+  // dots) kernel variant.  The kernels gate themselves on apply_go().
   virtual void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials,
-                                const BArgs& b) = 0;
+                                const BArgs& b, int stage = 1) = 0;
   // Standalone: which 0 = L x (at ref), 1 = N x (at ref), 2 = full rhs (no ref).
   virtual void launch_apply(cudaStream_t s, int which, const double* x, double* y) = 0;
   // Step residual R = L u + N u at ref = u, with ||R||^2 -> st->red.bnorm2[1] and the
@@ -109,6 +112,8 @@ class Engine {
   int ld_odd = 1;
   int use_dcgs = 1;  // 0 CGS2, 1 auto (DCGS2 from 2^18 DOF), 2 DCGS2 (EXPDG_ORTH=cgs2|dcgs2)
   int use_fused = 1;  // small problems run each phi call as one fused kernel (EXPDG_FUSED=0: off)
+  int use_pipe = 1;   // pipelined DCGS2: one V stream per Krylov column (EXPDG_PIPE=0: off)
+  int pipe_restart = 0;  // diagnostics: direct application every n-th column (EXPDG_PIPE_RESTART)
   // host-stepped runs: CUDA events around every DCGS2 update pass (time_kind 1) or every
   // phi-cycle operator application (2), so bench.py can report the live per-launch
   // bandwidth of the dominant kernel
@@ -164,7 +169,7 @@ class Engine {
                    int use_graph, bool dcgs, int mmax, int hact = -1, int hj = -1);
   long long body_launches = 0;  // kernels launch_body enqueued (host-stepped launch accounting)
   // kernels one launch_body enqueues
-  static int body_kernels(const OpDevice& op, bool dcgs, int mmax);
+  static int body_kernels(const OpDevice& op, bool dcgs, int mmax, bool pipe = false);
   // Runs one phi call to completion; host-stepped or graph-driven control.
   void run_phi(OpDevice& op, const BArgs& b, int use_graph);
   // Builds a while-node graph around launch_body; caller owns the exec.

@@ -56,8 +56,7 @@ __global__ void __launch_bounds__(kB1Threads) k_b1_phi(B1P<NP> P, PhiState* st, 
   __shared__ double s_buf[kB1Threads / 32];
   __shared__ double s_red[1];
   if (threadIdx.x == 0) {
-    const int a = st->action;
-    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    s_go = apply_go(st, base);
     if (s_go) {
       s_j = st->j;
       s_xs = st->scale[s_j];
@@ -186,7 +185,7 @@ class B1Base : public OpDevice {
     ref = r;
     if (P.part) exchange(s, r, hq(2), hq(3));
   }
-  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b, int stage = 1) override {
     if (P.part) {  // halo elements of the slot this cycle applies the operator to
       launch_pack_slot(s, st, base, layer, (long long)(P.nel - H) * NP, hq(4), hq(5));
       comm->halo(hq(4), hq(5), hq(0), hq(1), layer, s);
@@ -280,8 +279,7 @@ __global__ void __launch_bounds__(kB1Threads) k_b1oi_phi(B1OP<NP, NQ> P, PhiStat
   __shared__ double s_buf[kB1Threads / 32];
   __shared__ double s_red[1];
   if (threadIdx.x == 0) {
-    const int a = st->action;
-    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    s_go = apply_go(st, base);
     if (s_go) {
       s_j = st->j;
       s_xs = st->scale[s_j];
@@ -385,8 +383,7 @@ __global__ void k_dense_phi(int n, const double* __restrict__ A, PhiState* st, d
   __shared__ double s_buf[32];
   __shared__ double s_xt[kMaxP];
   if (st->stopped) return;
-  const int a = st->action;
-  if (!(a == ACT_EXTEND || a == ACT_AVNORM)) return;
+  if (!apply_go(st, base)) return;
   const int j = st->j;
   const double xs = st->scale[j], dt = st->dt;
   const long long ld = st->ld;
@@ -429,7 +426,7 @@ class DenseOp : public OpDevice {
     EXPDG_CUDA(cudaMemcpy(A, a_host, sizeof(double) * (size_t)nn * nn, cudaMemcpyHostToDevice));
   }
   ~DenseOp() override { cudaFree(A); }
-  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double*, const BArgs& b) override {
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double*, const BArgs& b, int = 1) override {
     k_dense_phi<<<1, 1024, 0, s>>>((int)n, A, st, base, b);
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {

@@ -111,8 +111,7 @@ __global__ void __launch_bounds__(256) k_b2_phi(B1P<NP> Px, B1P<NP> Py, int nx, 
   __shared__ double s_buf[8];
   __shared__ double s_red[1];
   if (threadIdx.x == 0) {
-    const int a = st->action;
-    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    s_go = apply_go(st, base);
     if (s_go) {
       s_j = st->j;
       s_xs = st->scale[s_j];
@@ -218,13 +217,12 @@ __global__ void __launch_bounds__(B2Strip<NP, DOT>::THREADS)
   __shared__ double s_red[DOT ? 4 * (S::JMAX + 1) : 1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    const int a = st->action;
-    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    s_go = apply_go(st, base);
     if (s_go) {
       s_j = st->j;
-      s_dots = DOT && st->dcgs && s_j <= S::JMAX;
+      s_dots = DOT && st->dcgs && s_j <= S::JMAX && apply_stage(st, base) == 1;
       if (blockIdx.x == 0) {
-        st->dots_fused = s_dots;
+        if (apply_stage(st, base) == 1) st->dots_fused = s_dots;  // stage 2 never takes the dots
         // algorithmic bytes of this sweep: x, u~, b_1, y plus, with the dots, V_0..V_{j-1}
         st->app_bytes += 8.0 * (double)Px.n * (4.0 + (s_dots ? (double)s_j : 0.0));
         st->app_launches++;
@@ -602,7 +600,7 @@ class Burgers2D : public OpDevice {
     ref = r;
     if (Py.part) exchange(s, r, hq(2), hq(3));
   }
-  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b, int stage = 1) override {
     if (Py.part) {
       launch_pack_slot(s, st, base, rowd, (long long)(ny - 1) * rowd, hq(4), hq(5));
       comm->halo(hq(4), hq(5), hq(0), hq(1), rowd, s);
@@ -610,7 +608,7 @@ class Burgers2D : public OpDevice {
     B1P<NP> px = Px, py = Py;
     px.ut = py.ut = ref;
     with_halo(py, false);
-    if (dots_on()) {
+    if (dots_on() && stage == 1) {
       if constexpr (kDotFits)
         k_b2_phi_strip<NP, true><<<dots_grid, B2Strip<NP, true>::THREADS, B2Strip<NP, true>::SMEM, s>>>(
             px, py, nx, ny, st, base, partials, b);

@@ -36,8 +36,7 @@ __global__ void k_check_ref(const double* __restrict__ q, long long nelem, int c
 // apply reads) into the halo send buffers; no-op unless this cycle applies the operator.
 __global__ void k_pack_slot(const PhiState* st, const double* base, long long layer, long long last,
                             double* __restrict__ lo, double* __restrict__ hi) {
-  const int a = st->action;
-  if (st->stopped || !(a == ACT_EXTEND || a == ACT_AVNORM)) return;
+  if (!apply_go(st, base)) return;
   const double* x = base + (size_t)st->j * st->ld;
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < layer; i += stride) {

@@ -421,8 +421,7 @@ __global__ void __launch_bounds__(256) k_e2_phi(E2P<NP> P, PhiState* st, double*
   __shared__ double s_buf[8];
   __shared__ double s_red[1];
   if (threadIdx.x == 0) {
-    const int a = st->action;
-    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    s_go = apply_go(st, base);
     if (s_go) {
       s_j = st->j;
       s_xs = st->scale[s_j];
@@ -602,13 +601,12 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 2 : 1
   __shared__ double s_red[DOT ? 4 * (S::JMAX + 1) : 1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    const int a = st->action;
-    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    s_go = apply_go(st, base);
     if (s_go) {
       s_j = st->j;
-      s_dots = DOT && st->dcgs && s_j <= S::JMAX;
+      s_dots = DOT && st->dcgs && s_j <= S::JMAX && apply_stage(st, base) == 1;
       if (blockIdx.x == 0) {
-        st->dots_fused = s_dots;
+        if (apply_stage(st, base) == 1) st->dots_fused = s_dots;  // stage 2 never takes the dots
         // algorithmic bytes of this sweep (bench.py's dominant-kernel roofline): x, q~, b_1, y
         // plus, with the dots, V_0..V_{j-1}
         st->app_bytes += 8.0 * (double)P.n * (4.0 + (s_dots ? (double)s_j : 0.0));
@@ -1073,7 +1071,7 @@ class Euler2D : public OpDevice {
     const long long ntiles = ((long long)d.nx * nyl + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));
   }
-  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b, int stage = 1) override {
     if (P.part) {  // halo rows of the slot this cycle applies the operator to
       launch_pack_slot(s, st, base, rowd, (long long)(P.ny - 1) * rowd, sb_lo(), sb_hi());
       comm->halo(sb_lo(), sb_hi(), hx_lo(), hx_hi(), rowd, s);
@@ -1082,7 +1080,7 @@ class Euler2D : public OpDevice {
     if (use_strip) {
       if (strip_cw == 4) {
         launch_strip<4, false>(s, p, st, base, partials, b);
-      } else if (dots_on()) {
+      } else if (dots_on() && stage == 1) {
         if constexpr (kDotFits) launch_strip<8, true>(s, p, st, base, partials, b);
       } else {
         launch_strip<8, false>(s, p, st, base, partials, b);

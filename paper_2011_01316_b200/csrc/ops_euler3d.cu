@@ -334,8 +334,7 @@ __global__ void __launch_bounds__(256) k_e3_phi(E3P<NP> P, PhiState* st, double*
   __shared__ double s_buf[8];
   __shared__ double s_red[1];
   if (threadIdx.x == 0) {
-    const int a = st->action;
-    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    s_go = apply_go(st, base);
     if (s_go) {
       s_j = st->j;
       s_xs = st->scale[s_j];
@@ -488,13 +487,12 @@ __global__ void __launch_bounds__(E3March<NP, DOT>::THREADS, 1)
   __shared__ double s_red[DOT ? 2 * S::ND * (S::JMAX + 1) : 1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    const int a = st->action;
-    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    s_go = apply_go(st, base);
     if (s_go) {
       s_j = st->j;
-      s_dots = DOT && st->dcgs && s_j <= S::JMAX;
+      s_dots = DOT && st->dcgs && s_j <= S::JMAX && apply_stage(st, base) == 1;
       if (blockIdx.x == 0) {
-        if (DOT) st->dots_fused = s_dots;
+        if (DOT && apply_stage(st, base) == 1) st->dots_fused = s_dots;
         st->app_bytes += 8.0 * (double)P.n * (4.0 + (s_dots ? (double)s_j : 0.0));
         st->app_launches++;
       }
@@ -1002,7 +1000,7 @@ class Euler3D : public OpDevice {
     k_e3_freeze<<<1184, 256, 0, s>>>(r, (long long)P.nx * P.ny * P.nz, NP * NP * NP, P.gamma, frozen);
     if (P.part) exchange(s, frozen, hb_(2), hb_(3));
   }
-  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b, int stage = 1) override {
     if (P.part) {  // halo planes of the slot this cycle applies the operator to
       launch_pack_slot(s, st, base, plane, (long long)(P.nz - 1) * plane, hb_(4), hb_(5));
       comm->halo(hb_(4), hb_(5), hb_(0), hb_(1), plane, s);
@@ -1010,7 +1008,7 @@ class Euler3D : public OpDevice {
     if constexpr (E3March<NP>::OK) {
       if (use_march) {
         if constexpr (kDotFits) {
-          if (dots_on()) {
+          if (dots_on() && stage == 1) {
             using SD = E3March<NP, true>;
             k_e3_phi_march<NP, true><<<dots_grid, SD::THREADS, SD::SMEM, s>>>(params(frozen), st, base, partials, b);
             return;

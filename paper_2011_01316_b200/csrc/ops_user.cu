@@ -22,8 +22,7 @@ constexpr int kUThreads = 256;
 __global__ void __launch_bounds__(kUThreads) k_user_gather(const PhiState* st, const double* base,
                                                            double* __restrict__ x, long long n) {
   if (st->stopped) return;
-  const int a = st->action;
-  if (!(a == ACT_EXTEND || a == ACT_AVNORM)) return;
+  if (!apply_go(st, base)) return;
   const double xs = st->scale[st->j];
   const double* src = base + (size_t)st->j * st->ld;
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -40,8 +39,7 @@ __global__ void __launch_bounds__(kUThreads) k_user_scatter(PhiState* st, double
   __shared__ double s_buf[kUThreads / 32];
   __shared__ double s_red[1];
   if (threadIdx.x == 0) {
-    const int a = st->action;
-    s_go = !st->stopped && (a == ACT_EXTEND || a == ACT_AVNORM);
+    s_go = apply_go(st, base);
     if (s_go) {
       s_j = st->j;
       s_dt = st->dt;
@@ -131,7 +129,7 @@ class UserOp : public OpDevice {
     ref = r;
     if (f.linearize) check(f.linearize(r, s, user), "linearize");
   }
-  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b) override {
+  void launch_phi_apply(cudaStream_t s, PhiState* st, double* base, double* partials, const BArgs& b, int stage = 1) override {
     k_user_gather<<<grid, kUThreads, 0, s>>>(st, base, xbuf, n);
     linear(s, xbuf, ybuf);
     k_user_scatter<<<grid, kUThreads, 0, s>>>(st, base, ybuf, b, partials, n);

@@ -23,8 +23,8 @@ def _dims(r):
     return np.diff(np.concatenate([[0], np.asarray(r.iters_per_step)]))
 
 
-def _run_both(w, steps, integrator="epi2"):
-    ctx = pkg.Context(0)  # AUTO orthogonalisation (the bench's context)
+def _run_both(w, steps, integrator="epi2", pipelined=None):
+    ctx = pkg.Context(0, pipelined=pipelined)  # AUTO orthogonalisation (the bench's context)
     u0 = w.initial_condition()
     dt = w.time_step(u0)
     kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
@@ -35,22 +35,26 @@ def _run_both(w, steps, integrator="epi2"):
     return r, orc, path, op.dim
 
 
+@pytest.mark.parametrize("pipelined", [True, False])
 @pytest.mark.parametrize("name,nx,steps", [
     ("C4", 64, 5),    # 2D Euler vortex, 409,600 DOF: DCGS2 + fused strip dots (the bench workload's path)
     ("C3", 128, 5),   # 2D Burgers, 409,600 DOF, nx % 32 == 0: DCGS2 + fused strip dots
     ("C5", 16, 3),    # 3D Euler TGV, 1,310,720 DOF, whole 2x2 tiles: DCGS2 + fused z-march dots
 ])
-def test_bench_path_matches_oracle(name, nx, steps):
+def test_bench_path_matches_oracle(name, nx, steps, pipelined):
+    # pipelined (the default): one basis stream per column (k_ts3) after a lookahead application;
+    # the fused sweep dots then serve the first column of every substep
     w = configs.scaled(configs.ALL[name], nx, steps=steps)
-    r, orc, path, n = _run_both(w, steps)
+    r, orc, path, n = _run_both(w, steps, pipelined=pipelined)
     assert n >= 1 << 18
-    assert path == {"dcgs2": True, "fused_dots": True, "graph": True, "fused_engine": False}, path
+    assert path == {"dcgs2": True, "pipelined": pipelined, "fused_dots": True, "graph": True,
+                    "fused_engine": False}, path
     assert r.status == orc.status == "completed"
     assert r.steps == orc.steps == steps
     err = rel(to_host(r.u), orc.u)
     assert err <= 1e-9, err
     d_dev, d_orc = _dims(r), _dims(orc)
-    print(f"{name}@{nx}: n={n} rel L2 {err:.3e}, Krylov dims device {d_dev.tolist()} oracle {d_orc.tolist()}")
+    print(f"{name}@{nx} pipelined={pipelined}: n={n} rel L2 {err:.3e}, Krylov dims device {d_dev.tolist()} oracle {d_orc.tolist()}")
     assert len(d_dev) == len(d_orc) == steps
     assert np.max(np.abs(d_dev - d_orc)) <= 1, (d_dev, d_orc)
 
