@@ -146,8 +146,8 @@ def roofline(dominant, step_achieved, peak, peak_kind, traffic, steps):
     whole step's algorithmic bandwidth."""
     step = {"achieved": step_achieved, "frac": step_achieved / peak, "frac_spec": step_achieved / SPEC_HBM_GBPS,
             "what": "phi engine (JVP + DCGS2 passes + combine + controller): algorithmic bytes of the realised "
-                    "trajectory (DCGS2: JVP 32n + 8n(2k+6) per column; SURVEY's CGS2 count is 8n(3k+6)) / "
-                    "step-loop time",
+                    "trajectory (pipelined DCGS2: JVP 32n + merged pass 8n(k+6) per column; two-pass DCGS2 "
+                    "32n + 8n(2k+6); SURVEY's CGS2 count 32n + 8n(3k+6)) / step-loop time",
             "alg_bytes_per_step": traffic["alg_bytes"] / steps, "columns": traffic["columns"],
             "avnorms": traffic["avnorms"], "combines": traffic["combines"]}
     if not dominant or dominant["launches"] == 0 or dominant["ms"] <= 0:
@@ -347,17 +347,23 @@ def main():
         timed = []
         # the operator sweep of this workload, and the ncu capture (DRAM / algorithmic bytes of
         # one launch) made on the same config, if any
+        # pipelined DCGS2: per column one operator application (the lookahead, stage 2: reads W,
+        # q~, b_1, writes Y = 32 n bytes; the first column of a substep also runs stage 1 with the
+        # fused pass-1 dots) and one merged basis pass k_ts3 (8 n (j + 6) bytes)
         sweep = {
-            "euler2d": ("k_e2_phi_strip<5,LF,8,DOT> (Euler strip JVP + DCGS2 pass-1 dots: reads x, q~, b_1, "
-                        "V_0..V_{j-1}; writes y)", "r01_ncu_dominant_fused.json"),
-            "burgers2d": ("k_b2_phi_strip<5,DOT> (2D Burgers strip JVP + DCGS2 pass-1 dots: reads x, u~, b_1, "
-                          "V_0..V_{j-1}; writes y)", "r01_ncu_dominant_fused_c3.json"),
-            "euler3d": ("k_e3_phi_march<4,DOT> (3D Euler z-march JVP + DCGS2 pass-1 dots: reads x, q~, b_1, "
-                        "V_0..V_{j-1}; writes y)", None),
+            "euler2d": ("k_e2_phi_strip<5,LF,8,*> (Euler strip JVP: the lookahead application dt A (s_j W) "
+                        "-> Y, reads W, q~, b_1, writes Y; + the pass-1 dots at substep starts)",
+                        "r02_ncu_dominant_strip.json"),
+            "burgers2d": ("k_b2_phi_strip<5,*> (2D Burgers strip JVP: reads x, u~, b_1, writes y; + the pass-1 "
+                          "dots at substep starts)", None),
+            "euler3d": ("k_e3_phi_march<4,*> (3D Euler z-march JVP: reads x, q~, b_1, writes y; + the pass-1 "
+                        "dots at substep starts)", None),
         }.get(w.kind, ("operator sweep (JVP of slot j)", None))
         for kind, name, ncu_file in (
-                (1, "k_ts2<TS2_UPD> (DCGS2 update pass: reads V_0..V_{j-1}, u, w; writes u, w)",
-                 "r01_ncu_dominant.json" if w.kind == "euler2d" else None),
+                (1, "k_ts3 (pipelined DCGS2 merged pass, column j: u <- u - V a, W <- W - g u - V mu, "
+                    "Y <- Arnoldi-relation image, + column j+1 pass-1 dots; reads V_0..V_{j-1}, u, W, Y, "
+                    "writes u, W, Y; k_ts2<TS2_UPD> on substep-final avnorm cycles)",
+                 "r02_ncu_dominant_ts3.json" if w.kind == "euler2d" else None),
                 (2, sweep[0], sweep[1])):
             ud = u.clone()
             ctx.time_dominant(kind)
