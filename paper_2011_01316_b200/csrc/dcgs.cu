@@ -28,9 +28,9 @@ constexpr int kT2Acc = (kMaxSlots + 7) / 8;
 
 // Pass-1 dots of one staged tile: acc1[v] += <V_i, U>, acc2[v] += <V_i, W> for the vectors
 // i = wid + 8 v <= j (i = j: U itself).  Streams of the tile: V_0..V_{j-1}, U, W consecutive.
-template <int NV>
+template <int NV, int NA>
 __device__ __forceinline__ void ts2_tile_dots(const double* V, int j, int T, int lane, int wid,
-                                              double (&acc1)[kT2Acc], double (&acc2)[kT2Acc]) {
+                                              double (&acc1)[NA], double (&acc2)[NA]) {
   const int T2 = T >> 1;
   const double2* V2 = reinterpret_cast<const double2*>(V);
   const double2* U2 = reinterpret_cast<const double2*>(V + (size_t)j * T);
@@ -376,12 +376,12 @@ __global__ void __launch_bounds__(128) k_dcgs_coef(PhiState* st) {
 //   phase 2  the dots of [V_0..V_{j-1}, unew, wnew] against wnew and znew from the same
 //            shared-memory tile (the DCGS2 pass-1 dots of column j+1)
 // Streams of a tile: slots 0..j+2 (V, u, W, Y), consecutive in HBM: 8 n (j + 6) bytes.
-template <int NV>
+template <int NV, int NA>
 __device__ __forceinline__ void ts3_consume(double* base, double* smem, uint64_t* full, uint64_t* empty,
                                             const double* s_al, const double* s_mu, const double* s_ka,
                                             double gam, double wsc, double zy, double zw, double kj, int j, int T,
                                             int S, long long ntiles, long long ld, long long ndot, int nst,
-                                            double (&acc1)[kT2Acc], double (&acc2)[kT2Acc], double& nu) {
+                                            double (&acc1)[NA], double (&acc2)[NA], double& nu) {
   const int tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
   const int T2 = T >> 1;
@@ -436,8 +436,11 @@ __device__ __forceinline__ void ts3_consume(double* base, double* smem, uint64_t
   }
 }
 
-__global__ void __launch_bounds__(kT2Block, 1) k_ts3(PhiState* st, double* base, double* partials, int budget,
-                                                     int max_stages, int min_T) {
+// MINB CTAs per SM; NVMAX bounds the dot vectors per warp (NVMAX < kT2Acc: columns j + 2 <= 8 NVMAX
+// only, so two CTAs per SM fit their accumulators in 112 registers; the other launch no-ops)
+template <int MINB, int NVMAX>
+__global__ void __launch_bounds__(kT2Block, MINB) k_ts3(PhiState* st, double* base, double* partials, int budget,
+                                                        int max_stages, int min_T) {
   extern __shared__ __align__(128) double smem[];
   __shared__ uint64_t full[8], empty[8];
   __shared__ int s_active, s_j, s_T, s_S;
@@ -451,8 +454,11 @@ __global__ void __launch_bounds__(kT2Block, 1) k_ts3(PhiState* st, double* base,
   const int tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
-    const int active =
+    int active =
         !st->stopped && st->dcgs && st->pl_look && (st->action == ACT_EXTEND || st->action == ACT_AVNORM);
+    // the split by column: the NVMAX < kT2Acc kernel takes j + 2 <= 8 NVMAX, the full one the rest
+    if (active && st->j_split > 0)
+      active = NVMAX < kT2Acc ? (st->j + 2 <= 8 * NVMAX) : (st->j + 2 > 8 * st->j_split);
     const int j = active ? st->j : 0;
     const int nst = j + 3;
     int T = kT2MaxT;
@@ -493,9 +499,9 @@ __global__ void __launch_bounds__(kT2Block, 1) k_ts3(PhiState* st, double* base,
   __syncthreads();
   const long long ntiles = ld / T;
   const uint32_t tile_bytes = (uint32_t)T * 8u;
-  double acc1[kT2Acc], acc2[kT2Acc];
+  double acc1[NVMAX], acc2[NVMAX];
 #pragma unroll
-  for (int v = 0; v < kT2Acc; ++v) acc1[v] = acc2[v] = 0.0;
+  for (int v = 0; v < NVMAX; ++v) acc1[v] = acc2[v] = 0.0;
   double nu = 0.0;
   if (wid == kT2Consumers / 32) {
     if (lane == 0) {  // producer: slots 0..j+2 are consecutive
@@ -513,21 +519,22 @@ __global__ void __launch_bounds__(kT2Block, 1) k_ts3(PhiState* st, double* base,
     }
   } else {
     const int nvw = (j + 2 + 7) / 8;  // dots over vectors 0..j+1
-#define T3C(NVV)                                                                                                 \
-  ts3_consume<NVV>(base, smem, full, empty, s_al, s_mu, s_ka, s_sc[0], s_sc[1], s_sc[2], s_sc[3], s_sc[4], j, T, \
-                   S, ntiles, ld, ndot, nst, acc1, acc2, nu)
+#define T3C(NVV)                                                                                             \
+  ts3_consume<(NVV < NVMAX ? NVV : NVMAX), NVMAX>(base, smem, full, empty, s_al, s_mu, s_ka, s_sc[0], s_sc[1], \
+                                                  s_sc[2], s_sc[3], s_sc[4], j, T, S, ntiles, ld, ndot, nst, acc1, \
+                                                  acc2, nu)
     if (nvw <= 1) T3C(1);
     else if (nvw <= 2) T3C(2);
     else if (nvw <= 3) T3C(3);
     else if (nvw <= 5) T3C(5);
-    else if (nvw <= 8) T3C(8);
+    else if (nvw <= 8 || NVMAX <= 8) T3C(8);
     else T3C(kT2Acc);
 #undef T3C
   }
   __syncthreads();
   const int cnt = j + 2;
 #pragma unroll
-  for (int v = 0; v < kT2Acc; ++v) {
+  for (int v = 0; v < NVMAX; ++v) {
     const int i = wid + 8 * v;
     const double r1 = warp_sum(acc1[v]);
     const double r2 = warp_sum(acc2[v]);
@@ -558,13 +565,20 @@ void launch_dcgs(cudaStream_t s, Engine& e, int which, int fused_jmax) {
     k_ts2<TS2_DOTS><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T, fused_jmax);
   else if (which == 1) k_dcgs_coef<<<1, 128, 0, s>>>(e.st);
   else if (which == 2) k_ts2<TS2_UPD><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T, -1);
-  else k_ts3<<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T);
+  else if (which == 3) {
+    // the merged pass: columns j + 2 <= 64 at two CTAs per SM (half the staging budget each), the rest
+    // at one (st->j_split set by the engine config; 0: one kernel for every column)
+    if (e.ts3_ctas == 2)
+      k_ts3<2, 8><<<2 * g, kT2Block, t.budget / 2, s>>>(e.st, e.base, e.partials, t.budget / 2, t.stages, t.min_T);
+    k_ts3<1, kT2Acc><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T);
+  }
 }
 
 void dcgs_init_attrs(int maxsm) {
   EXPDG_CUDA(cudaFuncSetAttribute(k_ts2<TS2_DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   EXPDG_CUDA(cudaFuncSetAttribute(k_ts2<TS2_UPD>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
-  EXPDG_CUDA(cudaFuncSetAttribute(k_ts3, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  EXPDG_CUDA(cudaFuncSetAttribute(k_ts3<1, kT2Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+  EXPDG_CUDA(cudaFuncSetAttribute(k_ts3<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm / 2));
 }
 
 }  // namespace expdg

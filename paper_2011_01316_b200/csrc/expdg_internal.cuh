@@ -67,6 +67,7 @@ struct PhiState {
   int build_only;    // krylov_build: stop after the Arnoldi columns (no avnorm / expm / combine)
   int pipe_cfg;      // pipelined DCGS2 allowed (see pl_direct / pl_look)
   int pipe_restart;  // diagnostics: apply the operator directly to every pipe_restart-th candidate
+  int j_split;       // merged pass: columns j + 2 <= 8 j_split run in the two-CTA kernel (0: one kernel)
   double* base;      // slot 0 of the Krylov workspace (stage-1 operator applications)
   // ---- dynamic control (action, phase, j, pl_direct, pl_look: read back together by
   // host-stepped loops, Engine::fetch_control)

@@ -577,7 +577,7 @@ __device__ __forceinline__ void strip_dots(const double* ring, const double* swr
 }
 
 template <int NP, bool ROE, int CW, bool DOT>
-__global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 2 : 1)
+__global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 3 : 1)
     k_e2_phi_strip(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
   using S = E2Strip<NP, CW, DOT>;
   constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
@@ -963,6 +963,9 @@ class Euler2D : public OpDevice {
   bool use_strip = true;
   bool roe = false;
   int strip_cw = 8;  // consumer warps per strip CTA (EXPDG_E2_CW=4: half-width strips, 2 CTAs / SM)
+  // the same for the pipelined lookahead application (EXPDG_E2_CW2): half-width strips at three
+  // CTAs per SM (128 registers) run it in 1.01 vs 1.12 ms at C4 (same box)
+  int strip_cw2 = 4;
   template <int CW, bool DOT>
   void launch_strip(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
                     const BArgs& b) {
@@ -1063,6 +1066,7 @@ class Euler2D : public OpDevice {
     use_strip = !(std::getenv("EXPDG_E2_TILE") && std::getenv("EXPDG_E2_TILE")[0] == '1');
     roe = d.euler_flux == 0;
     if (const char* v = std::getenv("EXPDG_E2_CW")) strip_cw = std::atoi(v) == 4 ? 4 : 8;
+    if (const char* v = std::getenv("EXPDG_E2_CW2")) strip_cw2 = std::atoi(v) == 8 ? 8 : 4;
     if (const char* v = std::getenv("EXPDG_E2_DOTS")) use_dots = v[0] != '0';
     if (const char* v = std::getenv("EXPDG_E2_DBG")) P.dbg = std::atoi(v);
     set_strip_attrs<8, false>();
@@ -1078,7 +1082,7 @@ class Euler2D : public OpDevice {
     }
     const E2P<NP> p = params(frozen);
     if (use_strip) {
-      if (strip_cw == 4) {
+      if (strip_cw == 4 || (stage == 2 && strip_cw2 == 4)) {
         launch_strip<4, false>(s, p, st, base, partials, b);
       } else if (dots_on() && stage == 1) {
         if constexpr (kDotFits) launch_strip<8, true>(s, p, st, base, partials, b);
