@@ -505,12 +505,19 @@ __global__ void __launch_bounds__(kT2Block, MINB) k_ts3(PhiState* st, double* ba
   double nu = 0.0;
   if (wid == kT2Consumers / 32) {
     if (lane == 0) {  // producer: slots 0..j+2 are consecutive
+      // the basis V_0..V_{j-1} is streamed once per column and never re-read while it could still
+      // be in L2: evict it first, so the lookahead image Y the JVP just wrote keeps its L2 lines
+      const uint64_t ef = l2_policy_evict_first();
+      const bool hint = st->l2_hint != 0;
       int s = 0, use = 0;
       for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
         mbar_wait(&empty[s], (use & 1) ^ 1);
         double* dst = smem + (size_t)s * nst * T;
         mbar_arrive_expect_tx(&full[s], tile_bytes * (uint32_t)nst);
-        for (int q = 0; q < nst; ++q) bulk_g2s(dst + (size_t)q * T, base + (size_t)q * ld + tl * T, tile_bytes, &full[s]);
+        for (int q = 0; q < nst; ++q) {
+          if (hint && q < j) bulk_g2s_hint(dst + (size_t)q * T, base + (size_t)q * ld + tl * T, tile_bytes, &full[s], ef);
+          else bulk_g2s(dst + (size_t)q * T, base + (size_t)q * ld + tl * T, tile_bytes, &full[s]);
+        }
         if (++s == S) {
           s = 0;
           ++use;

@@ -406,6 +406,7 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_PIPE")) use_pipe = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_PIPE_RESTART")) pipe_restart = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_TS3_CTAS")) ts3_ctas = std::atoi(v) == 2 ? 2 : 1;
+  if (const char* v = std::getenv("EXPDG_L2_HINT")) l2_hint = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_ORTH"))
     use_dcgs = std::strcmp(v, "cgs2") == 0 ? 0 : (std::strcmp(v, "dcgs2") == 0 ? 2 : 1);
   dcgs_init_attrs(maxsm);
@@ -489,6 +490,7 @@ PhiState Engine::config(long long n, int p, double dt, const expdg_krylov_cfg& k
   c.pipe_cfg = use_pipe;
   c.pipe_restart = pipe_restart;
   c.j_split = ts3_ctas == 2 ? 8 : 0;
+  c.l2_hint = l2_hint;
   c.pl_direct = 1;
   c.pl_look = 0;
   c.pl_ready = -1;

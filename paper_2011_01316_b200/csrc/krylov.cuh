@@ -115,6 +115,7 @@ class Engine {
   int use_pipe = 1;   // pipelined DCGS2: one V stream per Krylov column (EXPDG_PIPE=0: off)
   int pipe_restart = 0;  // diagnostics: direct application every n-th column (EXPDG_PIPE_RESTART)
   int ts3_ctas = 1;       // CTAs per SM of the merged pass k_ts3 (EXPDG_TS3_CTAS=2)
+  int l2_hint = 0;        // L2 evict_first on the merged pass's basis stream (EXPDG_L2_HINT=1)
   // host-stepped runs: CUDA events around every DCGS2 update pass (time_kind 1) or every
   // phi-cycle operator application (2), so bench.py can report the live per-launch
   // bandwidth of the dominant kernel
