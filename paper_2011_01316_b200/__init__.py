@@ -351,7 +351,7 @@ class Context:
         """Fused small-problem engine: SM cycles per phase of the last run."""
         v = (C.c_longlong * 8)()
         _check(lib().expdg_debug_profile(self.h, v))
-        return dict(zip(["apply", "dots", "update", "combine", "control"], list(v)[:5]))
+        return dict(zip(["apply", "dots", "update", "combine", "control", "expm", "expm_calls"], list(v)[:7]))
 
     def debug_hessenberg(self) -> np.ndarray:
         h = np.zeros((129, 128))

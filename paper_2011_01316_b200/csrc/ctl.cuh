@@ -400,7 +400,12 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
         Wx[idx] = h * v;
       }
       __syncthreads();
+      const long long te0 = clock64();
       const double* F = blk_expm(9 * N * N <= ws_cap ? Wsm : W, N);
+      if (tid == 0) {  // diagnostics (expdg_debug_profile slots 5, 6): SM cycles in the expm, calls
+        st->prof[5] += clock64() - te0;
+        st->prof[6] += 1;
+      }
       if (tid == 0) {
         const double beta = st->beta;
         double err = 0.0;
