@@ -88,3 +88,47 @@ def test_c4_full_size_one_step_matches_oracle():
           f"{orc.krylov_iterations}, oracle {orc.seconds:.0f} s")
     assert err <= 1e-9
     assert abs(int(r.krylov_iterations) - int(orc.krylov_iterations)) <= 1
+
+
+def test_exprb42_on_pipelined_path_matches_oracle():
+    # the p = 3 phi calls of EXPRB42 (proj/src/integrators.cpp:100-113) on the pipelined DCGS2 path
+    w = configs.scaled(configs.C4, 64, steps=2)
+    r, orc, path, n = _run_both(w, 2, integrator="exprb42")
+    assert path["pipelined"] and path["graph"]
+    assert r.status == orc.status == "completed"
+    assert rel(to_host(r.u), orc.u) <= 1e-9
+    assert np.max(np.abs(_dims(r) - _dims(orc))) <= 1
+
+
+def test_user_operator_on_pipelined_path_matches_oracle():
+    # a user LinearAction at n >= 2^18 DOF: AUTO selects the pipelined DCGS2, whose lookahead
+    # application calls the user's action on slot j+1 (tests/test_gpu_user_op.py's split, larger)
+    import math
+
+    import oracle
+    import torch
+    n = 1 << 18
+    h = 2 * math.pi / n
+    x = np.arange(n) * h
+    ref = 0.5 + np.sin(x)
+    nu = 1e-6
+
+    def L_np(v):
+        return -(np.roll(ref * v, -1) - np.roll(ref * v, 1)) / (2 * h) + nu * (np.roll(v, -1) - 2 * v + np.roll(v, 1)) / h ** 2
+
+    rt = torch.tensor(ref, device="cuda:0")
+
+    def L_t(v):
+        return -(torch.roll(rt * v, -1) - torch.roll(rt * v, 1)) / (2 * h) + nu * (torch.roll(v, -1) - 2 * v + torch.roll(v, 1)) / h ** 2
+
+    rng = np.random.default_rng(3)
+    b = [rng.standard_normal(n), np.sin(3 * x)]
+    dt = 2e-5
+    ctx = pkg.Context(0)
+    op = pkg.UserOperator(ctx, pkg.SplitProblem(n, linear=L_t))
+    got, st = pkg.phi_combination(ctx, op, [to_dev(v) for v in b], dt, tol=1e-10, max_basis=40, orth_length=40)
+    path = ctx.last_path()
+    assert path["pipelined"], path
+    exp_, iters, subs = oracle.phi_combination_user(L_np, n, b, dt, tol=1e-10, max_basis=40, orth_length=40)
+    assert rel(to_host(got), exp_) <= 1e-10
+    assert abs(st.iterations - iters) <= 1 and st.substeps == subs
