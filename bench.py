@@ -30,6 +30,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL logs (e.g. its version banner) go to stderr: stdout carries exactly one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0
@@ -248,6 +250,9 @@ def main():
     ap.add_argument("--partition", action="store_true",
                     help="slab-partitioned NCCL path even at N = 1 (always used for N > 1)")
     ap.add_argument("--replicas", action="store_true", help="N > 1: independent full-size replicas instead")
+    ap.add_argument("--comm", default="peer", choices=["peer", "nccl"],
+                    help="partitioned runs: device-resident peer-memory collectives (graph control) or NCCL "
+                         "(host-stepped control)")
     ap.add_argument("--host-control", action="store_true",
                     help="host-stepped controller (same kernels, no graph WHILE nodes): for ncu, which "
                          "cannot profile kernel nodes of graphs with conditional nodes")
@@ -277,24 +282,35 @@ def main():
     spec = w.spec()
     n_global = w.dofs
     # N > 1: element-row slabs of the one C4 mesh (strong scaling), halo rows and the
-    # Gram-Schmidt / norm sums over NCCL; --partition forces the
-    # partitioned path at N = 1 (NCCL world of one) to exercise it on a single GPU.
+    # Gram-Schmidt / norm sums between the ranks; --partition forces the
+    # partitioned path at N = 1 (a world of one) to exercise it on a single GPU.  --comm peer
+    # (default): the device-resident peer-memory communicator (kernel allreduce / halo over
+    # NVLink P2P through CUDA IPC mappings, graph control kept); --comm nccl: NCCL with
+    # host-stepped control.
     partitioned = (world > 1 or args.partition) and not args.replicas
     if partitioned:
         from paper_2011_01316_b200.partition import slab_ranges
 
-        uid = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            uid = torch.tensor(list(pkg.nccl_unique_id()), dtype=torch.uint8)
-        if world > 1:
-            t_uid = uid.to(f"cuda:{local}")
-            torch.distributed.broadcast(t_uid, 0)
-            uid = t_uid.cpu()
-        ctx.attach_nccl(bytes(uid.tolist()), rank, world)
         npe = spec.order + 1
         layers, blk = {"burgers1d": (spec.nx, npe), "burgers2d": (spec.ny, spec.nx * npe ** 2),
                        "euler2d": (spec.ny, spec.nx * npe ** 2 * 4),
                        "euler3d": (spec.nz, spec.nx * spec.ny * npe ** 3 * 5)}[spec.kind]
+        if args.comm == "peer":
+            handle = ctx.peer_export(world, blk)
+            handles = [handle]
+            if world > 1:
+                handles = [None] * world
+                torch.distributed.all_gather_object(handles, handle)
+            ctx.attach_peer(handles, rank, world)
+        else:
+            uid = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                uid = torch.tensor(list(pkg.nccl_unique_id()), dtype=torch.uint8)
+            if world > 1:
+                t_uid = uid.to(f"cuda:{local}")
+                torch.distributed.broadcast(t_uid, 0)
+                uid = t_uid.cpu()
+            ctx.attach_nccl(bytes(uid.tolist()), rank, world)
         rows = slab_ranges(layers, world)[rank]
         spec.part = rows
         if w.config == 5:  # each rank builds only its z-slab (C5L: 5.4 GB global state)
@@ -444,7 +460,7 @@ def main():
                                                            "orth_length": w.max_basis},
                        "integrator": "epi2", "l2": "inputs larger than L2 (Krylov workspace "
                        f"{(w.max_basis + 2) * 8 * n / 1e9:.1f} GB vs 126 MB L2)",
-                       "parallelism": (f"{world}-way element-row slabs (NCCL halo + allreduce)" if partitioned
+                       "parallelism": (f"{world}-way element slabs ({args.comm} halo + allreduce)" if partitioned
                                        else "single GPU" if world == 1 else f"{world} independent replicas"),
                        "krylov_iters_per_step": [int(v) for v in iters_per_step]},
             "roofline": roofline(dominant, achieved, peak, peak_kind, traffic, args.steps),

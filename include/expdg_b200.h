@@ -149,7 +149,8 @@ int expdg_ctx_synchronize(expdg_ctx* ctx);
  * and has no distributed layer; these add the two collectives the partitioned path
  * needs (sum/max allreduce of the reduced Gram-Schmidt dots and norms, neighbour
  * halo exchange).  Attach the communicator before creating partitioned operators;
- * a context with a communicator runs its control host-stepped.
+ * with NCCL or the host-staged local group the control runs host-stepped, with the
+ * peer-memory communicator (below) it stays in the CUDA graphs.
  *   NCCL: rank 0 calls expdg_nccl_unique_id, broadcasts the 128 bytes, every rank
  *         calls expdg_ctx_attach_nccl (collective, like ncclCommInitRank).
  *   Local group: several ranks driven by threads of one process (host-staged
@@ -161,6 +162,20 @@ int expdg_local_group_create(int size, expdg_local_group** out);
 int expdg_local_group_destroy(expdg_local_group* g);
 int expdg_ctx_attach_local(expdg_ctx* ctx, expdg_local_group* g, int rank);
 int expdg_ctx_comm(const expdg_ctx* ctx, int* rank, int* size); /* 0, 1 without a communicator */
+/* Device-resident peer-memory communicator: the allreduce and the halo exchange as plain kernels
+ * over peer memory (P2P stores over NVLink + release/acquire epoch flags, fixed rank-order sums),
+ * so a partitioned run keeps the CUDA-graph WHILE-node control (no host round-trip per Krylov
+ * cycle).  halo_doubles: the largest element layer any operator of the context exchanges.
+ *   One process per GPU: every rank calls expdg_ctx_peer_export (allocates its region, returns a
+ *         64-byte CUDA IPC handle), the handles are all-gathered (rank order), every rank calls
+ *         expdg_ctx_attach_peer.
+ *   Threads of one process, one device (tests): expdg_peer_group_create + expdg_ctx_attach_peer_local. */
+typedef struct expdg_peer_group expdg_peer_group;
+int expdg_peer_group_create(int size, long long halo_doubles, expdg_peer_group** out);
+int expdg_peer_group_destroy(expdg_peer_group* g);
+int expdg_ctx_attach_peer_local(expdg_ctx* ctx, expdg_peer_group* g, int rank);
+int expdg_ctx_peer_export(expdg_ctx* ctx, int size, long long halo_doubles, unsigned char handle_out[64]);
+int expdg_ctx_attach_peer(expdg_ctx* ctx, const unsigned char* handles, int rank, int size);
 
 /* Orthogonalisation of fully orthogonalised phi calls (orth_length >= max_basis):
  * EXPDG_ORTH_DCGS2 classical Gram-Schmidt with the reorthogonalisation of

@@ -107,7 +107,8 @@ EXPORTS = [
     "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
     "expdg_debug_profile", "expdg_ctx_set_fused", "expdg_ctx_time_dominant", "expdg_ctx_dominant_stats",
     "expdg_ctx_last_path", "expdg_user_op_create", "expdg_krylov_build", "expdg_initial_condition_slab",
-    "expdg_ctx_set_pipelined",
+    "expdg_ctx_set_pipelined", "expdg_peer_group_create", "expdg_peer_group_destroy", "expdg_ctx_attach_peer_local",
+    "expdg_ctx_peer_export", "expdg_ctx_attach_peer",
 ]
 
 _lib = None
@@ -175,6 +176,11 @@ def lib():
     L.expdg_debug_profile.argtypes = [vp, C.POINTER(C.c_longlong)]
     L.expdg_ctx_set_fused.argtypes = [vp, C.c_int]
     L.expdg_ctx_set_pipelined.argtypes = [vp, C.c_int]
+    L.expdg_peer_group_create.argtypes = [C.c_int, C.c_longlong, C.POINTER(vp)]
+    L.expdg_peer_group_destroy.argtypes = [vp]
+    L.expdg_ctx_attach_peer_local.argtypes = [vp, vp, C.c_int]
+    L.expdg_ctx_peer_export.argtypes = [vp, C.c_int, C.c_longlong, C.c_char_p]
+    L.expdg_ctx_attach_peer.argtypes = [vp, C.c_char_p, C.c_int, C.c_int]
     L.expdg_ctx_time_dominant.argtypes = [vp, C.c_int]
     L.expdg_ctx_dominant_stats.argtypes = [vp, dp]
     L.expdg_ctx_last_path.argtypes = [vp, C.POINTER(C.c_int)]
@@ -373,6 +379,24 @@ class Context:
         _check(lib().expdg_ctx_attach_local(self.h, group.h, rank))
         return self
 
+    def attach_peer_local(self, group: "PeerGroup", rank: int):
+        """Rank `rank` of a device-resident peer-memory group of threads of this process."""
+        self._group = group
+        _check(lib().expdg_ctx_attach_peer_local(self.h, group.h, rank))
+        return self
+
+    def peer_export(self, size: int, halo_doubles: int) -> bytes:
+        """One process per GPU: allocate this rank's peer region; returns its 64-byte CUDA IPC handle."""
+        buf = C.create_string_buffer(64)
+        _check(lib().expdg_ctx_peer_export(self.h, size, halo_doubles, buf))
+        return buf.raw
+
+    def attach_peer(self, handles: Sequence[bytes], rank: int, size: int):
+        """Map the peers' regions (all ranks' handles in rank order) and attach the communicator."""
+        blob = b"".join(bytes(h) for h in handles)
+        _check(lib().expdg_ctx_attach_peer(self.h, blob, rank, size))
+        return self
+
     @property
     def comm(self) -> tuple:
         r, n = C.c_int(), C.c_int()
@@ -384,6 +408,24 @@ def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().expdg_nccl_unique_id(buf))
     return buf.raw
+
+
+class PeerGroup:
+    """Device-resident peer-memory communicator group for several ranks in one process (one device)."""
+
+    def __init__(self, size: int, halo_doubles: int = 1 << 20):
+        h = C.c_void_p()
+        _check(lib().expdg_peer_group_create(size, halo_doubles, C.byref(h)))
+        self.h = h
+        self.size = size
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                lib().expdg_peer_group_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
 
 
 class LocalGroup:

@@ -40,6 +40,10 @@ struct expdg_local_group {
   std::shared_ptr<LocalGroup> g;
 };
 
+struct expdg_peer_group {
+  std::shared_ptr<PeerGroup> g;
+};
+
 struct expdg_ctx {
   std::unique_ptr<Comm> comm;  // declared before eng: destroyed after it
   std::unique_ptr<Engine> eng;
@@ -56,6 +60,7 @@ struct expdg_ctx {
   double* dts_dev = nullptr;  // dt sequence
   StepRecord* rec_dev = nullptr;
   long long steps_cap = 0;
+  std::shared_ptr<PeerExport> peer_export;  // this rank's exported peer region, until attach
   // engine path of the last phi / integrate call (expdg_ctx_last_path)
   int last_path[4] = {0, 0, 0, 0};
 };
@@ -252,6 +257,50 @@ int expdg_ctx_attach_local(expdg_ctx* ctx, expdg_local_group* g, int rank) {
   });
 }
 
+int expdg_peer_group_create(int size, long long halo_doubles, expdg_peer_group** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null argument");
+    auto g = std::make_unique<expdg_peer_group>();
+    g->g = make_peer_group(size, halo_doubles);
+    *out = g.release();
+  });
+}
+
+int expdg_peer_group_destroy(expdg_peer_group* g) {
+  return guard([&] { delete g; });
+}
+
+int expdg_ctx_attach_peer_local(expdg_ctx* ctx, expdg_peer_group* g, int rank) {
+  return guard([&] {
+    if (!ctx || !g) throw std::invalid_argument("null argument");
+    if (ctx->comm) throw std::invalid_argument("context already has a communicator");
+    EXPDG_CUDA(cudaSetDevice(ctx->eng->device));
+    ctx->comm = make_peer_comm_local(g->g, rank);
+    ctx->eng->comm = ctx->comm.get();
+  });
+}
+
+int expdg_ctx_peer_export(expdg_ctx* ctx, int size, long long halo_doubles, unsigned char handle_out[64]) {
+  return guard([&] {
+    if (!ctx || !handle_out) throw std::invalid_argument("null argument");
+    if (ctx->comm) throw std::invalid_argument("context already has a communicator");
+    EXPDG_CUDA(cudaSetDevice(ctx->eng->device));
+    ctx->peer_export = make_peer_export(size, halo_doubles, handle_out);
+  });
+}
+
+int expdg_ctx_attach_peer(expdg_ctx* ctx, const unsigned char* handles, int rank, int size) {
+  return guard([&] {
+    if (!ctx || !handles) throw std::invalid_argument("null argument");
+    if (ctx->comm) throw std::invalid_argument("context already has a communicator");
+    if (!ctx->peer_export) throw std::invalid_argument("call expdg_ctx_peer_export first");
+    EXPDG_CUDA(cudaSetDevice(ctx->eng->device));
+    ctx->comm = make_peer_comm_ipc(ctx->peer_export, handles, rank, size);
+    ctx->eng->comm = ctx->comm.get();
+    ctx->peer_export.reset();  // owned by the communicator now
+  });
+}
+
 int expdg_ctx_set_orthogonalization(expdg_ctx* ctx, int mode) {
   return guard([&] {
     if (!ctx) throw std::invalid_argument("null argument");
@@ -348,6 +397,7 @@ long long expdg_op_dim(const expdg_op* op) { return op ? op->dev->n : 0; }
 static int check_ref(expdg_op* op, cudaStream_t s, const double* ref) {
   int chk = op_check_ref(*op->dev, s, ref);
   if (op->dev->partitioned()) {
+    op->ctx->comm->host_barrier();
     int* d = reinterpret_cast<int*>(op->ctx->work2);
     EXPDG_CUDA(cudaMemcpyAsync(d, &chk, sizeof(int), cudaMemcpyHostToDevice, s));
     op->ctx->comm->allreduce(d, d, 1, COMM_I32, COMM_MAX, s);
@@ -365,6 +415,7 @@ int expdg_op_linearize(expdg_op* op, const double* ref_dev) {
     if (chk == 1) throw std::invalid_argument("reference state not finite");
     if (chk == 2) throw std::domain_error("EulerOperator: inadmissible reference state");
     if (!op->ref_owned) EXPDG_CUDA(cudaMalloc(&op->ref_owned, sizeof(double) * op->dev->n));
+    if (op->dev->partitioned()) op->ctx->comm->host_barrier();
     EXPDG_CUDA(cudaMemcpyAsync(op->ref_owned, ref_dev, sizeof(double) * op->dev->n, cudaMemcpyDeviceToDevice, s));
     op->dev->freeze(s, op->ref_owned);
     // the caller may release ref_dev on return: finish reading it
@@ -451,8 +502,10 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
     const long long bl0 = e.body_launches;
     ctx->last_path[0] = c.dcgs ? (e.use_pipe ? 2 : 1) : 0;
     ctx->last_path[1] = c.dcgs && op->dev->fused_dcgs_dots_jmax() >= c.mmax;
-    ctx->last_path[2] = use_graph_default() && !e.comm && !e.fused_ok(*op->dev) && op->dev->graph_capturable();
+    ctx->last_path[2] = use_graph_default() && (!e.comm || e.comm->graph_capturable()) && !e.fused_ok(*op->dev) &&
+                        op->dev->graph_capturable();
     ctx->last_path[3] = e.fused_ok(*op->dev) ? 1 : 0;
+    if (e.comm) e.comm->host_barrier();
     e.run_phi(*op->dev, b, use_graph_default() ? 1 : 0);
     EXPDG_CUDA(cudaMemcpy(e.st_host, e.st, sizeof(PhiState), cudaMemcpyDeviceToHost));
     const PhiState& s = *e.st_host;
@@ -667,6 +720,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   EXPDG_CUDA(cudaStreamSynchronize(e.stream));
   double max0 = 0.0;
   for (int i = 0; i < rgrid; ++i) max0 = std::max(max0, h2[2 * i]);
+  if (e.comm) e.comm->host_barrier();  // every rank past its allocations before the first collective
   // partitioned: max over ranks (host value staged through a device double)
   auto global_max = [&](double v) {
     if (!e.comm) return v;
@@ -768,7 +822,8 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
                      (dev.partitioned() ? (pipe ? 2 : 1) : 0);  // + halo pack kernel(s)
   cudaGraphExec_t ex = nullptr;
   // partitioned: host-stepped control; user operators: only when their callbacks are graph-safe
-  const bool graph = cfg->use_graph != 0 && !e.comm && dev.graph_capturable();
+  // partitioned runs keep the graphs with the peer-memory communicator (kernel collectives)
+  const bool graph = cfg->use_graph != 0 && (!e.comm || e.comm->graph_capturable()) && dev.graph_capturable();
   // host callbacks must not see the states after a blow-up: look at `stopped` after every step
   const bool check_each_step = !dev.graph_capturable();
   ctx->last_path[0] = c1.dcgs ? (e.use_pipe ? 2 : 1) : 0;
@@ -888,6 +943,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
         EXPDG_CUDA(cudaLaunchHostFunc(e.stream, on_step_host, &items[idx]));
       }
     };
+    if (e.comm) e.comm->host_barrier();  // every rank's graph and buffers ready before the loop
     // lagged early-exit check: launch in chunks, look at `stopped` of the chunk before
     int* stop_host = ctx->stop_host;
     stop_host[0] = stop_host[1] = 0;

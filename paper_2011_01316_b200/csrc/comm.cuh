@@ -32,12 +32,27 @@ class Comm {
   virtual void halo(const double* send_lo, const double* send_hi, double* recv_lo, double* recv_hi, long long count,
                     cudaStream_t s) = 0;
   virtual const char* kind() const = 0;
+  // the collectives are plain kernels on the stream (recordable into the engine's CUDA graphs)
+  virtual bool graph_capturable() const { return false; }
+  // Ranks that share ONE device (threads of one process): a host barrier the library passes
+  // before launching device-side collectives, so no rank can sit in a device-synchronising
+  // runtime call (cudaFree, pinned allocation) while another rank's collective kernel spins on
+  // it.  No-op for one process per GPU.
+  virtual void host_barrier() {}
 };
 
 struct LocalGroup;
 std::shared_ptr<LocalGroup> make_local_group(int size);
 std::unique_ptr<Comm> make_local_comm(const std::shared_ptr<LocalGroup>& g, int rank);
 std::unique_ptr<Comm> make_nccl_comm(const void* unique_id, int rank, int size);
+// device-resident peer-memory communicator (comm_peer.cu)
+struct PeerGroup;
+struct PeerExport;
+std::shared_ptr<PeerGroup> make_peer_group(int size, long long halo_cap);
+std::unique_ptr<Comm> make_peer_comm_local(const std::shared_ptr<PeerGroup>& g, int rank);
+std::shared_ptr<PeerExport> make_peer_export(int size, long long halo_cap, unsigned char handle_out[64]);
+std::unique_ptr<Comm> make_peer_comm_ipc(const std::shared_ptr<PeerExport>& x, const unsigned char* handles,
+                                         int rank, int size);
 void nccl_unique_id(void* out128);
 
 }  // namespace expdg

@@ -712,7 +712,7 @@ void Engine::run_phi(OpDevice& op, const BArgs& b, int use_graph) {
     EXPDG_CUDA(cudaStreamSynchronize(stream));
     return;
   }
-  if (use_graph && !comm && op.graph_capturable()) {
+  if (use_graph && (!comm || comm->graph_capturable()) && op.graph_capturable()) {
     cudaGraphExec_t ex = build_phi_graph(op, b);
     EXPDG_CUDA(cudaGraphLaunch(ex, stream));
     EXPDG_CUDA(cudaStreamSynchronize(stream));

@@ -21,14 +21,16 @@ from tests.gpu_util import rel, to_dev, to_host
 pytestmark = pytest.mark.gpu
 
 
-def run_ranks(parts, fn, orth=None):
-    """fn(rank, ctx) on `parts` threads, each with its own context of a local group."""
-    group = pkg.LocalGroup(parts)
+def run_ranks(parts, fn, orth=None, peer=False):
+    """fn(rank, ctx) on `parts` threads, each with its own context of a local group (host-staged) or,
+    with peer=True, of a device-resident peer-memory group (kernel collectives, graph control)."""
+    group = pkg.PeerGroup(parts) if peer else pkg.LocalGroup(parts)
     out, errs = [None] * parts, []
 
     def body(r):
         try:
-            ctx = pkg.Context(0, orth=orth).attach_local(group, r)
+            ctx = pkg.Context(0, orth=orth)
+            ctx = ctx.attach_peer_local(group, r) if peer else ctx.attach_local(group, r)
             out[r] = fn(r, ctx)
         except BaseException as e:  # noqa: BLE001
             errs.append(e)
@@ -355,3 +357,58 @@ def test_partitioned_euler3d_fused_dcgs2_dots_eight_ranks():
     spec.box = (0.0, 2 * np.pi, 0.0, 2 * np.pi, 0.0, 2 * np.pi)
     u0 = pkg.initial_condition_slab(5, 8, 8, 16, spec.order, 0, 16, box=spec.box)
     _dcgs2_partition_case(w, spec, spec.nz, spec.nx * spec.ny * (spec.order + 1) ** 3 * 5, 8, u0)
+
+
+@pytest.mark.parametrize("kind,nx,parts", [("C4", 9, 3), ("C4", 12, 4), ("C5", 4, 2)])
+def test_peer_comm_graph_control_matches_single_rank(kind, nx, parts):
+    # the device-resident peer-memory communicator: the partitioned run keeps the CUDA-graph WHILE
+    # control (ctx.last_path()["graph"]) with the allreduce / halo as kernels, and reproduces the
+    # single-rank run like the host-staged path does
+    w = configs.scaled(configs.ALL[kind], nx, steps=2)
+    spec = w.spec()
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    ctx = pkg.Context(0)
+    single = pkg.integrate(ctx, pkg.Operator(ctx, spec), to_dev(u0), "epi2", dt, w.steps * dt, **kw)
+    axis = spec.nz if kind == "C5" else spec.ny
+    layer = u0.size // axis
+    ranges = slab_ranges(axis, parts)
+
+    def fn(r, c):
+        o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": ranges[r]}))
+        sl = slice(ranges[r][0] * layer, ranges[r][1] * layer)
+        res = pkg.integrate(c, o, to_dev(u0[sl]), "epi2", dt, w.steps * dt, **kw)
+        return res, to_host(res.u), c.last_path()
+
+    got = run_ranks(parts, fn, peer=True)
+    assert all(g[2]["graph"] for g in got), [g[2] for g in got]
+    assert all(g[0].status == single.status == "completed" for g in got)
+    assert rel(np.concatenate([g[1] for g in got]), to_host(single.u)) <= 1e-11
+    for g in got:
+        assert list(g[0].iters_per_step) == list(got[0][0].iters_per_step)
+    d_part = np.diff(np.concatenate([[0], got[0][0].iters_per_step]))
+    d_single = np.diff(np.concatenate([[0], single.iters_per_step]))
+    assert np.max(np.abs(d_part - d_single)) <= 1
+
+
+def test_peer_comm_ipc_world_size_one():
+    # the one-process-per-GPU attach (CUDA IPC export / map) at world size 1: same result as the
+    # whole-mesh run, under graph control
+    w = configs.scaled(configs.C4, 12, steps=2)
+    spec = w.spec()
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    kw = dict(tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+    ctx = pkg.Context(0)
+    single = pkg.integrate(ctx, pkg.Operator(ctx, spec), to_dev(u0), "epi2", dt, w.steps * dt, **kw)
+    c = pkg.Context(0)
+    h = c.peer_export(1, spec.nx * 100)
+    c.attach_peer([h], 0, 1)
+    assert c.comm == (0, 1)
+    o = pkg.Operator(c, pkg.OperatorSpec(**{**spec.__dict__, "part": (0, spec.ny)}))
+    r = pkg.integrate(c, o, to_dev(u0), "epi2", dt, w.steps * dt, **kw)
+    assert c.last_path()["graph"]
+    assert r.status == "completed"
+    assert rel(to_host(r.u), to_host(single.u)) <= 1e-12
+    assert list(r.iters_per_step) == list(single.iters_per_step)

@@ -1,0 +1,80 @@
+"""Two PROCESSES sharing the one GPU through the peer-memory communicator's CUDA IPC path
+(expdg_ctx_peer_export / expdg_ctx_attach_peer: each rank maps the other's region, the
+allreduce and halo run as kernels over it, graph control kept): the partitioned C4 run must
+reproduce the single-rank run.  (On one GPU without MPS the two contexts time-slice, so the
+collectives' spin waits progress at the scheduler's pace: a correctness test, not a timing.)"""
+import multiprocessing as mp
+import os
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _rank(rank, size, q_out, q_in, res):
+    try:
+        sys.path.insert(0, ROOT)
+        import paper_2011_01316_b200 as pkg
+        from paper_2011_01316_b200 import configs
+        from paper_2011_01316_b200.partition import slab_ranges
+        from tests.gpu_util import to_dev, to_host
+        w = configs.scaled(configs.C4, 8, steps=2)
+        spec = w.spec()
+        u0 = w.initial_condition()
+        dt = w.time_step(u0)
+        layer = u0.size // spec.ny
+        ctx = pkg.Context(0)
+        h = ctx.peer_export(size, layer)
+        q_out.put((rank, h))
+        handles = dict([q_in.get(timeout=60) for _ in range(size)])
+        ctx.attach_peer([handles[r] for r in range(size)], rank, size)
+        rows = slab_ranges(spec.ny, size)[rank]
+        o = pkg.Operator(ctx, pkg.OperatorSpec(**{**spec.__dict__, "part": rows}))
+        r = pkg.integrate(ctx, o, to_dev(u0[rows[0] * layer:rows[1] * layer]), "epi2", dt, w.steps * dt,
+                          tol=w.tol, max_basis=w.max_basis, orth_length=w.max_basis)
+        res.put((rank, to_host(r.u), list(r.iters_per_step), ctx.last_path()["graph"], r.status))
+    except BaseException as e:  # noqa: BLE001
+        res.put((rank, repr(e), None, None, None))
+
+
+def test_two_process_ipc_partition_matches_single_rank():
+    import paper_2011_01316_b200 as pkg
+    from paper_2011_01316_b200 import configs
+    from tests.gpu_util import rel, to_dev, to_host
+    w = configs.scaled(configs.C4, 8, steps=2)
+    u0 = w.initial_condition()
+    dt = w.time_step(u0)
+    ctx = pkg.Context(0)
+    single = pkg.integrate(ctx, pkg.Operator(ctx, w.spec()), to_dev(u0), "epi2", dt, w.steps * dt, tol=w.tol,
+                           max_basis=w.max_basis, orth_length=w.max_basis)
+    size = 2
+    mpx = mp.get_context("spawn")
+    hq, res = mpx.Queue(), mpx.Queue()
+    ins = [mpx.Queue() for _ in range(size)]
+    procs = [mpx.Process(target=_rank, args=(r, size, hq, ins[r], res)) for r in range(size)]
+    for p in procs:
+        p.start()
+    try:
+        hs = [hq.get(timeout=120) for _ in range(size)]
+        for q in ins:
+            for h in hs:
+                q.put(h)
+        out = dict((t[0], t[1:]) for t in (res.get(timeout=240) for _ in range(size)))
+    finally:
+        for p in procs:
+            p.join(timeout=30)
+            if p.is_alive():
+                p.kill()
+    for r in range(size):
+        assert not isinstance(out[r][0], str), out[r][0]
+    assert all(out[r][2] for r in range(size))  # graph control
+    assert all(out[r][3] == "completed" for r in range(size))
+    assert out[0][1] == out[1][1]
+    got = np.concatenate([out[r][0] for r in range(size)])
+    assert rel(got, to_host(single.u)) <= 1e-11
+    d_part = np.diff(np.concatenate([[0], out[0][1]]))
+    d_single = np.diff(np.concatenate([[0], single.iters_per_step]))
+    assert np.max(np.abs(d_part - d_single)) <= 1
