@@ -468,7 +468,10 @@ __global__ void __launch_bounds__(kT2Block, MINB) k_ts3(PhiState* st, double* ba
       T >>= 1;
       S = budget / (nst * T * 8);
     }
-    S = S > max_stages ? max_stages : (S > 8 ? 8 : S);
+    // T is the largest tile two stages of which fit; the stages then fill the budget (up to
+    // st->ts3_stages), so small columns keep more bytes in flight
+    const int cap = st->ts3_stages > 0 ? st->ts3_stages : max_stages;
+    S = S > cap ? cap : (S > 8 ? 8 : S);
     s_active = active;
     s_j = j;
     s_T = T;

@@ -69,6 +69,7 @@ struct PhiState {
   int pipe_restart;  // diagnostics: apply the operator directly to every pipe_restart-th candidate
   int j_split;       // merged pass: columns j + 2 <= 8 j_split run in the two-CTA kernel (0: one kernel)
   int l2_hint;       // merged pass: stream the basis with an L2 evict_first hint
+  int ts3_stages;    // merged pass: stage cap after the tile choice (0: the tile rule's cap)
   double* base;      // slot 0 of the Krylov workspace (stage-1 operator applications)
   // ---- dynamic control (action, phase, j, pl_direct, pl_look: read back together by
   // host-stepped loops, Engine::fetch_control)

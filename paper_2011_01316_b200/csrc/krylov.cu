@@ -393,7 +393,7 @@ Engine::Engine(int dev) : device(dev) {
   EXPDG_CUDA(cudaMalloc(&partials, sizeof(double) * kMaxPartials * kMaxSlots));
   ework_doubles = size_t(9) * (kMaxBasis + 2) * (kMaxBasis + 2);
   EXPDG_CUDA(cudaMalloc(&ework, sizeof(double) * ework_doubles));
-  const int maxsm = 200 * 1024;
+  const int maxsm = 216 * 1024;  // dynamic staging budget cap (EXPDG_TS_BUDGET <= this)
   EXPDG_CUDA(cudaFuncSetAttribute(k_ts<TS_DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   EXPDG_CUDA(cudaFuncSetAttribute(k_ts<TS_UPD_DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   EXPDG_CUDA(cudaFuncSetAttribute(k_ts<TS_UPD_NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
@@ -407,6 +407,7 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_PIPE_RESTART")) pipe_restart = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_TS3_CTAS")) ts3_ctas = std::atoi(v) == 2 ? 2 : 1;
   if (const char* v = std::getenv("EXPDG_L2_HINT")) l2_hint = std::atoi(v);
+  if (const char* v = std::getenv("EXPDG_TS3_STAGES")) ts3_stages = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_ORTH"))
     use_dcgs = std::strcmp(v, "cgs2") == 0 ? 0 : (std::strcmp(v, "dcgs2") == 0 ? 2 : 1);
   dcgs_init_attrs(maxsm);
@@ -491,6 +492,7 @@ PhiState Engine::config(long long n, int p, double dt, const expdg_krylov_cfg& k
   c.pipe_restart = pipe_restart;
   c.j_split = ts3_ctas == 2 ? 8 : 0;
   c.l2_hint = l2_hint;
+  c.ts3_stages = ts3_stages;
   c.pl_direct = 1;
   c.pl_look = 0;
   c.pl_ready = -1;

@@ -101,7 +101,9 @@ void host_burgers_source(int order, int ne, double a, double b, bool over_integr
 
 // Device workspace + launch helpers of the phi engine.
 struct TsTuning {
-  int budget = 196608;  // dynamic smem per CTA of the tall-skinny passes
+  // dynamic smem per CTA of the tall-skinny passes (216 KB; 192 KB: C4 same box 198.7 vs 195.3 ms
+  // per step, k_ts3 3.79 vs 3.68 ms per launch)
+  int budget = 221184;
   int stages = 2;       // pipeline depth cap
   int min_T = 64;       // smallest tile (doubles) before giving up stages
 };
@@ -116,6 +118,9 @@ class Engine {
   int pipe_restart = 0;  // diagnostics: direct application every n-th column (EXPDG_PIPE_RESTART)
   int ts3_ctas = 1;       // CTAs per SM of the merged pass k_ts3 (EXPDG_TS3_CTAS=2)
   int l2_hint = 0;        // L2 evict_first on the merged pass's basis stream (EXPDG_L2_HINT=1)
+  // merged-pass stage cap after the tile choice (EXPDG_TS3_STAGES): 4 stages where they fit
+  // (C4 same box: 3.78 vs 3.89 ms per k_ts3 launch, 198.8 vs 201.1 ms per step)
+  int ts3_stages = 4;
   // host-stepped runs: CUDA events around every DCGS2 update pass (time_kind 1) or every
   // phi-cycle operator application (2), so bench.py can report the live per-launch
   // bandwidth of the dominant kernel
