@@ -436,11 +436,10 @@ __device__ __forceinline__ void ts3_consume(double* base, double* smem, uint64_t
   }
 }
 
-// MINB CTAs per SM; NVMAX bounds the dot vectors per warp (NVMAX < kT2Acc: columns j + 2 <= 8 NVMAX
-// only, so two CTAs per SM fit their accumulators in 112 registers; the other launch no-ops)
-template <int MINB, int NVMAX>
-__global__ void __launch_bounds__(kT2Block, MINB) k_ts3(PhiState* st, double* base, double* partials, int budget,
-                                                        int max_stages, int min_T) {
+// (tried: a second instantiation at two CTAs per SM for columns j + 2 <= 64 -- 96 registers,
+// spills, half the staging: 4.59 vs 3.55 ms per launch at C4)
+__global__ void __launch_bounds__(kT2Block, 1) k_ts3(PhiState* st, double* base, double* partials, int budget,
+                                                     int max_stages, int min_T) {
   extern __shared__ __align__(128) double smem[];
   __shared__ uint64_t full[8], empty[8];
   __shared__ int s_active, s_j, s_T, s_S;
@@ -454,11 +453,8 @@ __global__ void __launch_bounds__(kT2Block, MINB) k_ts3(PhiState* st, double* ba
   const int tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
-    int active =
+    const int active =
         !st->stopped && st->dcgs && st->pl_look && (st->action == ACT_EXTEND || st->action == ACT_AVNORM);
-    // the split by column: the NVMAX < kT2Acc kernel takes j + 2 <= 8 NVMAX, the full one the rest
-    if (active && st->j_split > 0)
-      active = NVMAX < kT2Acc ? (st->j + 2 <= 8 * NVMAX) : (st->j + 2 > 8 * st->j_split);
     const int j = active ? st->j : 0;
     const int nst = j + 3;
     int T = kT2MaxT;
@@ -502,25 +498,18 @@ __global__ void __launch_bounds__(kT2Block, MINB) k_ts3(PhiState* st, double* ba
   __syncthreads();
   const long long ntiles = ld / T;
   const uint32_t tile_bytes = (uint32_t)T * 8u;
-  double acc1[NVMAX], acc2[NVMAX];
+  double acc1[kT2Acc], acc2[kT2Acc];
 #pragma unroll
-  for (int v = 0; v < NVMAX; ++v) acc1[v] = acc2[v] = 0.0;
+  for (int v = 0; v < kT2Acc; ++v) acc1[v] = acc2[v] = 0.0;
   double nu = 0.0;
   if (wid == kT2Consumers / 32) {
     if (lane == 0) {  // producer: slots 0..j+2 are consecutive
-      // the basis V_0..V_{j-1} is streamed once per column and never re-read while it could still
-      // be in L2: evict it first, so the lookahead image Y the JVP just wrote keeps its L2 lines
-      const uint64_t ef = l2_policy_evict_first();
-      const bool hint = st->l2_hint != 0;
       int s = 0, use = 0;
       for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
         mbar_wait(&empty[s], (use & 1) ^ 1);
         double* dst = smem + (size_t)s * nst * T;
         mbar_arrive_expect_tx(&full[s], tile_bytes * (uint32_t)nst);
-        for (int q = 0; q < nst; ++q) {
-          if (hint && q < j) bulk_g2s_hint(dst + (size_t)q * T, base + (size_t)q * ld + tl * T, tile_bytes, &full[s], ef);
-          else bulk_g2s(dst + (size_t)q * T, base + (size_t)q * ld + tl * T, tile_bytes, &full[s]);
-        }
+        for (int q = 0; q < nst; ++q) bulk_g2s(dst + (size_t)q * T, base + (size_t)q * ld + tl * T, tile_bytes, &full[s]);
         if (++s == S) {
           s = 0;
           ++use;
@@ -530,21 +519,21 @@ __global__ void __launch_bounds__(kT2Block, MINB) k_ts3(PhiState* st, double* ba
   } else {
     const int nvw = (j + 2 + 7) / 8;  // dots over vectors 0..j+1
 #define T3C(NVV)                                                                                             \
-  ts3_consume<(NVV < NVMAX ? NVV : NVMAX), NVMAX>(base, smem, full, empty, s_al, s_mu, s_ka, s_sc[0], s_sc[1], \
+  ts3_consume<NVV, kT2Acc>(base, smem, full, empty, s_al, s_mu, s_ka, s_sc[0], s_sc[1], \
                                                   s_sc[2], s_sc[3], s_sc[4], j, T, S, ntiles, ld, ndot, nst, acc1, \
                                                   acc2, nu)
     if (nvw <= 1) T3C(1);
     else if (nvw <= 2) T3C(2);
     else if (nvw <= 3) T3C(3);
     else if (nvw <= 5) T3C(5);
-    else if (nvw <= 8 || NVMAX <= 8) T3C(8);
+    else if (nvw <= 8) T3C(8);
     else T3C(kT2Acc);
 #undef T3C
   }
   __syncthreads();
   const int cnt = j + 2;
 #pragma unroll
-  for (int v = 0; v < NVMAX; ++v) {
+  for (int v = 0; v < kT2Acc; ++v) {
     const int i = wid + 8 * v;
     const double r1 = warp_sum(acc1[v]);
     const double r2 = warp_sum(acc2[v]);
@@ -575,20 +564,13 @@ void launch_dcgs(cudaStream_t s, Engine& e, int which, int fused_jmax) {
     k_ts2<TS2_DOTS><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T, fused_jmax);
   else if (which == 1) k_dcgs_coef<<<1, 128, 0, s>>>(e.st);
   else if (which == 2) k_ts2<TS2_UPD><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T, -1);
-  else if (which == 3) {
-    // the merged pass: columns j + 2 <= 64 at two CTAs per SM (half the staging budget each), the rest
-    // at one (st->j_split set by the engine config; 0: one kernel for every column)
-    if (e.ts3_ctas == 2)
-      k_ts3<2, 8><<<2 * g, kT2Block, t.budget / 2, s>>>(e.st, e.base, e.partials, t.budget / 2, t.stages, t.min_T);
-    k_ts3<1, kT2Acc><<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T);
-  }
+  else k_ts3<<<g, kT2Block, t.budget, s>>>(e.st, e.base, e.partials, t.budget, t.stages, t.min_T);
 }
 
 void dcgs_init_attrs(int maxsm) {
   EXPDG_CUDA(cudaFuncSetAttribute(k_ts2<TS2_DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
   EXPDG_CUDA(cudaFuncSetAttribute(k_ts2<TS2_UPD>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
-  EXPDG_CUDA(cudaFuncSetAttribute(k_ts3<1, kT2Acc>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
-  EXPDG_CUDA(cudaFuncSetAttribute(k_ts3<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm / 2));
+  EXPDG_CUDA(cudaFuncSetAttribute(k_ts3, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
 }
 
 }  // namespace expdg

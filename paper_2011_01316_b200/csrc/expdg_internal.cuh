@@ -67,8 +67,6 @@ struct PhiState {
   int build_only;    // krylov_build: stop after the Arnoldi columns (no avnorm / expm / combine)
   int pipe_cfg;      // pipelined DCGS2 allowed (see pl_direct / pl_look)
   int pipe_restart;  // diagnostics: apply the operator directly to every pipe_restart-th candidate
-  int j_split;       // merged pass: columns j + 2 <= 8 j_split run in the two-CTA kernel (0: one kernel)
-  int l2_hint;       // merged pass: stream the basis with an L2 evict_first hint
   int ts3_stages;    // merged pass: stage cap after the tile choice (0: the tile rule's cap)
   double* base;      // slot 0 of the Krylov workspace (stage-1 operator applications)
   // ---- dynamic control (action, phase, j, pl_direct, pl_look: read back together by
@@ -308,21 +306,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-// The same with an L2 eviction-priority hint (createpolicy ...L2::evict_first / evict_last)
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar,
-                                              uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst_smem)),
-      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
 

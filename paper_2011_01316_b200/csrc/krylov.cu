@@ -405,8 +405,6 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_FUSED")) use_fused = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_PIPE")) use_pipe = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_PIPE_RESTART")) pipe_restart = std::atoi(v);
-  if (const char* v = std::getenv("EXPDG_TS3_CTAS")) ts3_ctas = std::atoi(v) == 2 ? 2 : 1;
-  if (const char* v = std::getenv("EXPDG_L2_HINT")) l2_hint = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_TS3_STAGES")) ts3_stages = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_ORTH"))
     use_dcgs = std::strcmp(v, "cgs2") == 0 ? 0 : (std::strcmp(v, "dcgs2") == 0 ? 2 : 1);
@@ -490,8 +488,6 @@ PhiState Engine::config(long long n, int p, double dt, const expdg_krylov_cfg& k
   c.dcgs = (c.full_orth && use_dcgs && (use_dcgs == 2 || n >= (1LL << 18))) ? 1 : 0;
   c.pipe_cfg = use_pipe;
   c.pipe_restart = pipe_restart;
-  c.j_split = ts3_ctas == 2 ? 8 : 0;
-  c.l2_hint = l2_hint;
   c.ts3_stages = ts3_stages;
   c.pl_direct = 1;
   c.pl_look = 0;

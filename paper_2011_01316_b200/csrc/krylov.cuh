@@ -116,8 +116,6 @@ class Engine {
   int use_fused = 1;  // small problems run each phi call as one fused kernel (EXPDG_FUSED=0: off)
   int use_pipe = 1;   // pipelined DCGS2: one V stream per Krylov column (EXPDG_PIPE=0: off)
   int pipe_restart = 0;  // diagnostics: direct application every n-th column (EXPDG_PIPE_RESTART)
-  int ts3_ctas = 1;       // CTAs per SM of the merged pass k_ts3 (EXPDG_TS3_CTAS=2)
-  int l2_hint = 0;        // L2 evict_first on the merged pass's basis stream (EXPDG_L2_HINT=1)
   // merged-pass stage cap after the tile choice (EXPDG_TS3_STAGES): 4 stages where they fit
   // (C4 same box: 3.78 vs 3.89 ms per k_ts3 launch, 198.8 vs 201.1 ms per step)
   int ts3_stages = 4;
