@@ -98,14 +98,28 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
+# EXPDG_BENCH_SHARED_GPU=1: a FUNCTIONAL check of the N > 1 code path with every rank on the one
+# visible GPU (gloo for the bench's own small collectives, the library's peer-memory communicator
+# between the processes) -- never a timing: ranks that share a device and spin on each other's
+# collectives say nothing about multi-GPU speed.
+SHARED_GPU = os.environ.get("EXPDG_BENCH_SHARED_GPU") == "1"
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SHARED_GPU:
+        local = 0
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("gloo" if SHARED_GPU else "nccl", init_method="env://")
     return world, rank, local
+
+
+def _coll_dev(local):
+    """Device of the bench's own small collective tensors (CPU under gloo)."""
+    return "cpu" if SHARED_GPU else f"cuda:{local}"
 
 
 def cpu_sample(workload, steps: int = 1, nx: int = 128, warmup: int = 0):
@@ -307,7 +321,7 @@ def main():
             if rank == 0:
                 uid = torch.tensor(list(pkg.nccl_unique_id()), dtype=torch.uint8)
             if world > 1:
-                t_uid = uid.to(f"cuda:{local}")
+                t_uid = uid.to(_coll_dev(local))
                 torch.distributed.broadcast(t_uid, 0)
                 uid = t_uid.cpu()
             ctx.attach_nccl(bytes(uid.tolist()), rank, world)
@@ -322,7 +336,7 @@ def main():
     # dt = cfl dx_min / c_max over the whole state: the min over ranks of the local rule
     dt = w.time_step(u0) if w.dt is None else w.dt
     if world > 1:
-        t_dt = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+        t_dt = torch.tensor([dt], dtype=torch.float64, device=_coll_dev(local))
         torch.distributed.all_reduce(t_dt, op=torch.distributed.ReduceOp.MIN)
         dt = float(t_dt.item())
     op = pkg.Operator(ctx, spec)
@@ -398,7 +412,7 @@ def main():
         raise RuntimeError(f"timed run: {r.status} after {r.steps} steps")
     loop_s = r.loop_ms / 1e3
     if world > 1:
-        t = torch.tensor([loop_s], device=f"cuda:{local}")
+        t = torch.tensor([loop_s], device=_coll_dev(local))
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         loop_s = float(t.item())
     total_dofs = n_global if partitioned else world * n
@@ -424,7 +438,7 @@ def main():
         t1 = time.perf_counter()
         e_s = t1 - t0
         if world > 1:
-            tt = torch.tensor([e_s], device=f"cuda:{local}")
+            tt = torch.tensor([e_s], device=_coll_dev(local))
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             e_s = float(tt.item())
         e2e = {"value": total_dofs * args.steps / e_s, "unit": "DOF-steps/s", "h2d_bytes_per_step": 8 * n,

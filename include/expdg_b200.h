@@ -303,8 +303,9 @@ int expdg_debug_state(expdg_ctx* ctx, double* out16);
  * 2 update+norm, 3 combine) against k basis vectors of length n; avg ms. */
 int expdg_bench_ts(expdg_ctx* ctx, long long n, int k, int mode, int reps, double* ms);
 /* Micro-benchmark of one phi-cycle operator application at column j (mode 0; the
- * operator kernel also takes the DCGS2 pass-1 dots where it does so in the engine) or
- * of the separate DCGS2 dots pass at column j (mode 1) on the current Krylov slots;
+ * operator kernel also takes the DCGS2 pass-1 dots where it does so in the engine), of the
+ * separate DCGS2 dots pass at column j (mode 1), or of the pipelined DCGS2 lookahead application
+ * (mode 2: slot j+1 -> slot j+2, the plain kernel) on the current Krylov slots;
  * the operator must be linearized; avg ms (diagnostics). */
 int expdg_bench_apply(expdg_ctx* ctx, expdg_op* op, int j, int mode, int reps, double* ms);
 /* Hessenberg matrix of the last phi call, (129 x 128) row-major (diagnostics). */

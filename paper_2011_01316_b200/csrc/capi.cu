@@ -1159,11 +1159,12 @@ int expdg_bench_apply(expdg_ctx* ctx, expdg_op* op, int j, int mode, int reps, d
     if (!op->dev->ref) throw std::invalid_argument("operator not linearized (call expdg_op_linearize)");
     Engine& e = *ctx->eng;
     const long long n = op->dev->n;
-    e.ensure(n + 1, j + 2);
+    e.ensure(n + 1, j + 3);
     e.ensure_scratch(n + 1, 1);
     EXPDG_CUDA(cudaMemsetAsync(e.scratch, 0, sizeof(double) * (n + 1), e.stream));
     PhiState c = e.config(n, 1, 1e-3, expdg_krylov_cfg{1e-10, std::max(j + 1, 1), std::max(j + 1, 1), 0, 0});
     c.dcgs = 1;
+    c.pl_look = mode == 2 ? 1 : 0;  // mode 2: the pipelined DCGS2 lookahead application (stage 2)
     c.action = ACT_EXTEND;
     c.j = j;
     c.mc = j + 1;
@@ -1174,6 +1175,7 @@ int expdg_bench_apply(expdg_ctx* ctx, expdg_op* op, int j, int mode, int reps, d
     b.b[1] = e.scratch;
     auto one = [&] {
       if (mode == 0) op->dev->launch_phi_apply(e.stream, e.st, e.base, e.partials, b);
+      else if (mode == 2) op->dev->launch_phi_apply(e.stream, e.st, e.base + e.ld, e.partials, b, 2);
       else launch_dcgs(e.stream, e, 0, -1);
     };
     one();  // warm-up

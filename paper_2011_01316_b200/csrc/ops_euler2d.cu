@@ -797,7 +797,8 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 3 : 1
           double* ytop = sfy + ((r - r0 + 1) % 3) * S::FY;
           double* ybot = sfy + ((r - r0) % 3) * S::FY;
           const int nxf = (w + 1) * NP, nyf = w * NP;
-          const int total = nxf + nyf + (r == r0 ? nyf : 0);
+          // diagnostics (EXPDG_E2_DBG bit 2): skip the face fluxes (wrong results; timing only)
+          const int total = (P.dbg & 4) ? 0 : nxf + nyf + (r == r0 ? nyf : 0);
           for (int t = tid; t < total; t += S::CONS) {  // the consumer warps
             double qa[4], ta[4], qb[4], tb[4], f[4];
             const double* ra;
