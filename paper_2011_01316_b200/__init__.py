@@ -21,7 +21,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_build", "libexpdg_b200.so")
+# EXPDG_LIB: another in-tree build of the same library (same-box A/B of kernel variants)
+LIB_PATH = os.environ.get("EXPDG_LIB") or os.path.join(_PKG, "_build", "libexpdg_b200.so")
 
 EXPDG_OK, EXPDG_E_INVALID, EXPDG_E_DOMAIN, EXPDG_E_KRYLOV, EXPDG_E_CUDA, EXPDG_E_UNSUPPORTED, EXPDG_E_COMM = range(7)
 BURGERS1D, BURGERS2D, EULER2D, EULER3D, DENSE = 1, 2, 3, 4, 5
