@@ -821,8 +821,8 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   const int body_k = Engine::body_kernels(dev, c1.dcgs != 0, exprb ? std::max(c1.mmax, c3.mmax) : c1.mmax, pipe) +
                      (dev.partitioned() ? (pipe ? 2 : 1) : 0);  // + halo pack kernel(s)
   cudaGraphExec_t ex = nullptr;
-  // partitioned: host-stepped control; user operators: only when their callbacks are graph-safe
-  // partitioned runs keep the graphs with the peer-memory communicator (kernel collectives)
+  // partitioned runs keep the graphs with the peer-memory communicator (kernel collectives), run
+  // host-stepped over NCCL / the host-staged group; user operators only when graph-safe
   const bool graph = cfg->use_graph != 0 && (!e.comm || e.comm->graph_capturable()) && dev.graph_capturable();
   // host callbacks must not see the states after a blow-up: look at `stopped` after every step
   const bool check_each_step = !dev.graph_capturable();

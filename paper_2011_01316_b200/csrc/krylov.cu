@@ -1,9 +1,9 @@
 // Device-resident adaptive Krylov phi engine (the B200 replacement of
 // proj/src/phi.cpp:133-260 and the Arnoldi loop of proj/src/phi.cpp:84-112).
 //
-// One "cycle" of the engine is a fixed sequence of six kernels:
-//   [operator apply] -> [pass A dots] -> [pass B update+dots] -> [pass C update+norm]
-//   -> [combine] -> [controller]
+// One "cycle" of the engine is a fixed sequence of kernels, e.g. for the default pipelined
+// DCGS2: [operator apply, stage 1] -> [dots pass] -> [coefficients] -> [lookahead apply,
+// stage 2] -> [update pass | merged pass] -> [combine] -> [controller].
 // Each kernel reads the action chosen by the previous controller from device
 // memory and no-ops when it is not its turn, so the sequence is captured once
 // into the body of a CUDA-graph WHILE node; the controller (one CTA) runs the
@@ -11,11 +11,11 @@
 // estimator and the accept / grow / halve rules, and clears the WHILE
 // condition when the call is done.  No host round-trip per step.
 //
-// Orthogonalisation is classical Gram-Schmidt with one reorthogonalisation
-// (CGS2) instead of the reference's two-pass MGS (proj/src/phi.cpp:94-100): the
-// same projector in exact arithmetic, three streaming passes over V per column
-// instead of 2(k+1) sequential ones.  IOP windows use one pass (reference: one
-// MGS pass over the window).
+// Orthogonalisation of fully orthogonalised calls: pipelined DCGS2 (dcgs.cu, one
+// streaming pass over V per column), two-pass DCGS2, or classical Gram-Schmidt with
+// one reorthogonalisation (CGS2, the three k_ts passes below) -- the reference's two-pass
+// MGS projector (proj/src/phi.cpp:94-100) in exact arithmetic.  IOP windows use one pass
+// (reference: one MGS pass over the window).
 #include <algorithm>
 #include <cstddef>
 #include <cstdlib>

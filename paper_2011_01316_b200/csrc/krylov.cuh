@@ -129,8 +129,9 @@ class Engine {
   bool fused_ok(const OpDevice& op) const;
   void fetch_control(cudaStream_t s);  // host-stepped loops: action, phase, j and stopped to st_host
   // Set when the context belongs to a slab-partitioned group: every reducing
-  // kernel is followed by a sum-allreduce of PhiState::loc -> PhiState::red,
-  // and the control runs host-stepped (no CUDA graphs).
+  // kernel is followed by a sum-allreduce of PhiState::loc -> PhiState::red; the
+  // control stays in the CUDA graphs when the communicator's collectives are kernels
+  // (peer memory), else runs host-stepped (NCCL, host-staged group).
   Comm* comm = nullptr;
   void reduce(cudaStream_t s);
   explicit Engine(int device);
