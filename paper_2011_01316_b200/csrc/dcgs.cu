@@ -458,7 +458,8 @@ __global__ void __launch_bounds__(kT2Block, 1) k_ts3(PhiState* st, double* base,
     const int j = active ? st->j : 0;
     const int nst = j + 3;
     int T = kT2MaxT;
-    while (T > min_T && max_stages * nst * T * 8 > budget) T >>= 1;
+    const int tile_stages = st->ts3_tstages > 0 ? st->ts3_tstages : max_stages;  // stages the tile choice assumes
+    while (T > min_T && tile_stages * nst * T * 8 > budget) T >>= 1;
     int S = budget / (nst * T * 8);
     while (S < 2 && T > 64) {
       T >>= 1;
