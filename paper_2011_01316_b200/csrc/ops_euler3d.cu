@@ -74,30 +74,41 @@ __device__ __forceinline__ bool admissible5(const double q[5], double gamma) {
   return p > 0.0;
 }
 
-// out = A(pr, e_dir) x  (rows of the 3D flux Jacobian, oracle jac3)
-__device__ __forceinline__ void jac3_apply(const Prim3& pr, int dir, double gamma, const double x[5],
-                                           double out[5]) {
+// out = A(pr, e_dir) x  (rows of the 3D flux Jacobian, oracle jac3), factored so the three
+// directions share the x-dependent scalars:  with u.m = sum_c u_c x_{1+c},
+//   P = phi x_0 - (g-1) u.m + (g-1) x_4,   Q = (phi - H) x_0 - (g-1) u.m + g x_4,
+//   s = x_{1+d} - u_d x_0:   out_0 = x_{1+d},  out_{1+r} = u_r s + u_d x_{1+r} + delta_rd P,
+//   out_4 = u_d Q + H x_{1+d}.
+// (The entry-by-entry form multiplied by the zero entries: IEEE x * 0 cannot be folded away,
+// and the JVP kernels are fp64-bound.)
+__device__ __forceinline__ void jac3_pre(const Prim3& pr, double gamma, const double x[5], double& P, double& Q) {
   const double gm1 = gamma - 1.0;
-  const double un = pr.u[dir];
-  const double phi = 0.5 * gm1 * (pr.u[0] * pr.u[0] + pr.u[1] * pr.u[1] + pr.u[2] * pr.u[2]);
-  out[0] = x[1 + dir];
+  const double phi = 0.5 * gm1 * fma(pr.u[0], pr.u[0], fma(pr.u[1], pr.u[1], pr.u[2] * pr.u[2]));
+  const double um = fma(pr.u[0], x[1], fma(pr.u[1], x[2], pr.u[2] * x[3]));
+  P = fma(gm1, x[4] - um, phi * x[0]);
+  Q = fma(gamma, x[4], fma(-gm1, um, (phi - pr.H) * x[0]));
+}
+
+template <int D>
+__device__ __forceinline__ void jac3_dir(const Prim3& pr, double P, double Q, const double x[5], double out[5]) {
+  const double un = pr.u[D];
+  const double sd = fma(-un, x[0], x[1 + D]);
+  out[0] = x[1 + D];
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
-    const double nr = r == dir ? 1.0 : 0.0;
-    double s = (phi * nr - pr.u[r] * un) * x[0];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      const double nc = c == dir ? 1.0 : 0.0;
-      double a = pr.u[r] * nc - gm1 * nr * pr.u[c];
-      if (c == r) a += un;
-      s = fma(a, x[1 + c], s);
-    }
-    out[1 + r] = fma(gm1 * nr, x[4], s);
+    const double v = fma(pr.u[r], sd, un * x[1 + r]);
+    out[1 + r] = r == D ? v + P : v;
   }
-  double s = ((phi - pr.H) * un) * x[0];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) s = fma((c == dir ? pr.H : 0.0) - gm1 * pr.u[c] * un, x[1 + c], s);
-  out[4] = fma(gamma * un, x[4], s);
+  out[4] = fma(un, Q, pr.H * x[1 + D]);
+}
+
+__device__ __forceinline__ void jac3_apply(const Prim3& pr, int dir, double gamma, const double x[5],
+                                           double out[5]) {
+  double P, Q;
+  jac3_pre(pr, gamma, x, P, Q);
+  if (dir == 0) jac3_dir<0>(pr, P, Q, x, out);
+  else if (dir == 1) jac3_dir<1>(pr, P, Q, x, out);
+  else jac3_dir<2>(pr, P, Q, x, out);
 }
 
 __device__ __forceinline__ void flux3_dir(const double q[5], const Prim3& pr, int dir, double f[5]) {
@@ -741,13 +752,17 @@ __global__ void __launch_bounds__(E3March<NP, DOT>::THREADS, 1)
             tv[c] = cur[S::PL + le * BLK + c * NN + node];
           }
           const Prim3 tp = prim3_frozen(tv);
+          double Pv, Qv, fl[5];
+          jac3_pre(tp, P.gamma, qv, Pv, Qv);
+          jac3_dir<0>(tp, Pv, Qv, qv, fl);
 #pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            double fl[5];
-            jac3_apply(tp, d, P.gamma, qv, fl);
+          for (int c = 0; c < 5; ++c) sf[(0 * 5 + c) * S::CONS + tid] = fl[c];
+          jac3_dir<1>(tp, Pv, Qv, qv, fl);
 #pragma unroll
-            for (int c = 0; c < 5; ++c) sf[(d * 5 + c) * S::CONS + tid] = fl[c];
-          }
+          for (int c = 0; c < 5; ++c) sf[(1 * 5 + c) * S::CONS + tid] = fl[c];
+          jac3_dir<2>(tp, Pv, Qv, qv, fl);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) sf[(2 * 5 + c) * S::CONS + tid] = fl[c];
         }
         // every face flux of the plane, once
         if (has0) face_out(dir0, qa, ta, qb, tb, dst0);
