@@ -77,25 +77,46 @@ __device__ __forceinline__ bool admissible4(const double q[4], double gamma) {
   return p > 0.0;
 }
 
-// out = A(pr, n) x for n = e_x (dir 0) or e_y (dir 1), entries of
-// jacobian_from_primitives (proj/src/euler.cpp:44-73) with n substituted.
-__device__ __forceinline__ void jac_apply(const Prim& pr, int dir, double gamma, const double x[4], double out[4]) {
+// out = A(pr, n) x for n = e_x (dir 0) or e_y (dir 1): jacobian_from_primitives
+// (proj/src/euler.cpp:44-73) with n substituted, factored so both directions share the
+// x-dependent scalars:  with u.m = u x_1 + v x_2,
+//   P = phi x_0 - (g-1) u.m + (g-1) x_3,   Q = (phi - H) x_0 - (g-1) u.m + g x_3,
+//   s = x_{1+d} - u_d x_0:   out_0 = x_{1+d},  out_{1+r} = u_r s + u_d x_{1+r} + delta_rd P,
+//   out_3 = u_d Q + H x_{1+d}.
+__device__ __forceinline__ void jac_pre(const Prim& pr, double gamma, const double x[4], double& P, double& Q) {
   const double gm1 = gamma - 1.0;
-  const double u = pr.u, v = pr.v, H = pr.H;
-  const double phi = 0.5 * gm1 * (u * u + v * v);
-  if (dir == 0) {
-    const double un = u;
-    out[0] = x[1];
-    out[1] = (phi - u * un) * x[0] + (u - gm1 * u + un) * x[1] + (-gm1 * v) * x[2] + gm1 * x[3];
-    out[2] = (-v * un) * x[0] + v * x[1] + un * x[2];
-    out[3] = ((phi - H) * un) * x[0] + (H - gm1 * u * un) * x[1] + (-gm1 * v * un) * x[2] + (gamma * un) * x[3];
-  } else {
-    const double un = v;
-    out[0] = x[2];
-    out[1] = (-u * un) * x[0] + un * x[1] + u * x[2];
-    out[2] = (phi - v * un) * x[0] + (-gm1 * u) * x[1] + (v - gm1 * v + un) * x[2] + gm1 * x[3];
-    out[3] = ((phi - H) * un) * x[0] + (-gm1 * u * un) * x[1] + (H - gm1 * v * un) * x[2] + (gamma * un) * x[3];
-  }
+  const double phi = 0.5 * gm1 * fma(pr.u, pr.u, pr.v * pr.v);
+  const double um = fma(pr.u, x[1], pr.v * x[2]);
+  P = fma(gm1, x[3] - um, phi * x[0]);
+  Q = fma(gamma, x[3], fma(-gm1, um, (phi - pr.H) * x[0]));
+}
+
+template <int D>
+__device__ __forceinline__ void jac_dir(const Prim& pr, double P, double Q, const double x[4], double out[4]) {
+  const double un = D == 0 ? pr.u : pr.v;
+  const double sd = fma(-un, x[0], x[1 + D]);
+  out[0] = x[1 + D];
+  const double v1 = fma(pr.u, sd, un * x[1]);
+  const double v2 = fma(pr.v, sd, un * x[2]);
+  out[1] = D == 0 ? v1 + P : v1;
+  out[2] = D == 1 ? v2 + P : v2;
+  out[3] = fma(un, Q, pr.H * x[1 + D]);
+}
+
+__device__ __forceinline__ void jac_apply(const Prim& pr, int dir, double gamma, const double x[4], double out[4]) {
+  double P, Q;
+  jac_pre(pr, gamma, x, P, Q);
+  if (dir == 0) jac_dir<0>(pr, P, Q, x, out);
+  else jac_dir<1>(pr, P, Q, x, out);
+}
+
+// both directions of one node (the volume fluxes)
+__device__ __forceinline__ void jac_apply_xy(const Prim& pr, double gamma, const double x[4], double fx[4],
+                                             double fy[4]) {
+  double P, Q;
+  jac_pre(pr, gamma, x, P, Q);
+  jac_dir<0>(pr, P, Q, x, fx);
+  jac_dir<1>(pr, P, Q, x, fy);
 }
 
 // physical flux F(q) . e_dir (proj/src/euler.cpp:26-40)
@@ -289,8 +310,7 @@ __device__ __forceinline__ void e2_tile(const E2P<NP>& P, int mode, int e0, int 
     double fx[4], fy[4];
     if (mode != 2) {
       const Prim tp = prim_frozen(ut);
-      jac_apply(tp, 0, P.gamma, q, fx);
-      jac_apply(tp, 1, P.gamma, q, fy);
+      jac_apply_xy(tp, P.gamma, q, fx, fy);
     }
     if (mode != 0) {
       if (!admissible4(q, P.gamma)) bad = true;
@@ -781,8 +801,7 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 3 : 1
           }
           const Prim tp = prim_frozen(tv);
           double fx[4], fy[4];
-          jac_apply(tp, 0, P.gamma, qv, fx);
-          jac_apply(tp, 1, P.gamma, qv, fy);
+          jac_apply_xy(tp, P.gamma, qv, fx, fy);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             sf[((le * 2 + 0) * 4 + c) * NN + node] = fx[c];
