@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstddef>
+#include <cstdlib>
 
 #include "fused.cuh"
 #include "krylov.cuh"
@@ -773,9 +774,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) k_phi_fused(PhiState* gst, d
 // shared memory; neighbour elements of the operator and the partial sums of every
 // reduction are read from the other CTAs' shared memory (DSMEM).  Each reduction is
 // one cluster barrier: every CTA writes its partials to its own (double-buffered)
-// buffer, then every CTA sums all of them in rank order (identical totals).  CTA 0
-// holds PhiState in shared memory and runs the controller (ctl_body); the others read
-// its decisions through DSMEM.  No basis traffic leaves the SMs.
+// buffer, then every CTA sums all of them in rank order (identical totals).  Every CTA
+// holds its own copy of PhiState in shared memory and runs the controller (ctl_body) on the
+// identical totals, so all CTAs take identical decisions with no broadcast and no cluster
+// barrier after the controller (a cluster barrier costs ~1.6k SM cycles, as much as a
+// column's arithmetic at C1); CTA 0's copy goes back to global memory at the end.  No basis
+// traffic leaves the SMs.
 namespace cg = cooperative_groups;
 constexpr int kClusterCTAs = 8;
 constexpr int kClusterThreads = 256;
@@ -783,7 +787,7 @@ constexpr int kClusterThreads = 256;
 template <class EL>
 __global__ void __launch_bounds__(kClusterThreads, 1)
     k_phi_cluster(PhiState* gst, double* base, double* W, BArgs b, EL el, int epc, int lds, int nslots,
-                  int ws_cap, int state_off, int ws_off) {
+                  int ws_cap, int state_off, int ws_off, int redund) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank(), CS = (int)cl.num_blocks();
   extern __shared__ __align__(16) unsigned char csm[];
@@ -817,17 +821,33 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
   }
   for (int m = 1; m <= b.p && m <= kMaxP; ++m)
     for (int i = tid; i < nloc; i += T) bl[(size_t)(m - 1) * epc * NP + i] = b.b[m] ? b.b[m][(size_t)e_lo * NP + i] : 0.0;
-  if (rank == 0) {
+  // redund (every CTA runs the controller): each CTA has its own state copy and expm
+  // workspace; else CTA 0 alone (EXPDG_CLUSTER_CTL=0, diagnostics)
+  const bool ctl_here = redund || rank == 0;
+  if (redund) W += (size_t)rank * 9 * (kMaxBasis + 2) * (kMaxBasis + 2);
+  if (ctl_here) {
     if (tid == 0) s_hb = sizeof(double) * (size_t)min(gst->mmax + 2, kMaxBasis + 1) * kMaxBasis;
     __syncthreads();
     state_copy(reinterpret_cast<unsigned char*>(st0), reinterpret_cast<const unsigned char*>(gst), s_hb);
   }
-  const PhiState* S = cl.map_shared_rank(st0, 0);
+  const PhiState* S = redund ? st0 : cl.map_shared_rank(st0, 0);
   const int nsc = nslots < kMaxSlots ? nslots : kMaxSlots;
-  // CTA 0 pushes the controller's decision (action, column, scales) into every CTA's
-  // shared memory, so the other CTAs never chase scalars through DSMEM
+  // the controller's decision (action, column, scales) into shared scalars: from this CTA's own
+  // state (redund), or pushed by CTA 0 into every CTA's shared memory
   auto push = [&]() {
     __syncthreads();
+    if (redund) {
+      if (tid == 0) {
+        s_act = st0->stopped ? ACT_DONE : st0->action;
+        s_j = st0->j;
+        s_j0 = st0->j0;
+        s_full = st0->full_orth;
+        s_mc = st0->mc;
+        s_dt = st0->dt;
+      }
+      for (int i = tid; i < nsc; i += T) s_scale[i] = st0->scale[i];
+      return;
+    }
     for (int r = tid; r < CS; r += T) {
       *cl.map_shared_rank(&s_act, r) = st0->stopped ? ACT_DONE : st0->action;
       *cl.map_shared_rank(&s_j, r) = st0->j;
@@ -841,7 +861,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       cl.map_shared_rank(s_scale, r)[i] = st0->scale[i];
     }
   };
-  if (rank == 0) push();
+  if (ctl_here) push();
   cl.sync();
   int round = 0;
   // cluster totals of cnt partial sums in s_mine -> s_tot (every CTA, rank order)
@@ -850,8 +870,14 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     for (int i = tid; i < cnt; i += T) buf[i] = s_mine[i];
     cl.sync();
     for (int i = tid; i < cnt; i += T) {
+      // all CS remote loads in flight at once (one DSMEM round trip, not CS), summed in rank order
+      double v[kClusterCTAs];
+#pragma unroll
+      for (int r = 0; r < kClusterCTAs; ++r) v[r] = r < CS ? cl.map_shared_rank(buf, r)[i] : 0.0;
       double sum = 0.0;
-      for (int r = 0; r < CS; ++r) sum += cl.map_shared_rank(buf, r)[i];
+#pragma unroll
+      for (int r = 0; r < kClusterCTAs; ++r)
+        if (r < CS) sum += v[r];
       s_tot[i] = sum;
     }
     __syncthreads();
@@ -949,17 +975,23 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
         if (s_tailhere) nacc = fma(v, v, nacc);
       }
       const double tot = block_sum(nacc, s_buf);
-      if (tid == 0) s_mine[0] = tot;
-      __syncthreads();
-      reduce(1);
-      if (rank == 0 && tid == 0) st0->red.nrmA = s_tot[0];
+      if (act != ACT_EXTEND) {
+        if (tid == 0) s_mine[0] = tot;
+        __syncthreads();
+        reduce(1);
+        if (ctl_here && tid == 0) st0->red.nrmA = s_tot[0];
+      }
       mark(0);
       if (act == ACT_EXTEND) {  // CGS2 passes (krylov.cu coefficients) or one IOP pass
         const int i0 = s_j0, k = j - i0 + 1;
+        // ||y||^2 rides in the first dots reduction (one cluster barrier fewer per column)
+        if (tid == 0) s_mine[k] = tot;
         local_dots(i0, k, y);
-        reduce(k);
-        if (rank == 0)
+        reduce(k + 1);
+        if (ctl_here) {
           for (int i = tid; i < k; i += T) st0->red.dotA[i0 + i] = s_tot[i];
+          if (tid == 0) st0->red.nrmA = s_tot[k];
+        }
         mark(1);
         if (s_full) {
           for (int i = tid; i < k; i += T) s_c[i] = s_scale[i0 + i] * s_scale[i0 + i] * s_tot[i];
@@ -970,7 +1002,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
           local_dots(i0, k, y);
           reduce(k);
           mark(1);
-          if (rank == 0)
+          if (ctl_here)
             for (int i = tid; i < k; i += T) st0->red.dotB[i0 + i] = s_tot[i];
         }
         for (int i = tid; i < k; i += T) s_c[i] = s_scale[i0 + i] * s_scale[i0 + i] * s_tot[i];
@@ -979,7 +1011,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
         if (tid == 0) s_mine[0] = nn;
         __syncthreads();
         reduce(1);
-        if (rank == 0 && tid == 0) st0->red.nrmC = s_tot[0];
+        if (ctl_here && tid == 0) st0->red.nrmC = s_tot[0];
         mark(2);
       }
     } else if (act == ACT_COMBINE) {
@@ -998,18 +1030,22 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
       if (tid == 0) s_mine[0] = tot;
       __syncthreads();
       reduce(1);
-      if (rank == 0 && tid == 0) st0->red.w2 = s_tot[0];
+      if (ctl_here && tid == 0) st0->red.w2 = s_tot[0];
       mark(3);
     }
-    if (rank == 0) {
+    if (ctl_here) {
       __syncthreads();
-      // the controller writes the phi tail into CTA 0's slot-0 tail (slot0[n + j])
+      // the controller writes the phi tail into this CTA's slot-0 tail (slot0[n + j])
       ctl_body(st0, V + tail_at - n, W, Wsm, ws_cap, cudaGraphConditionalHandle{}, 0);
       push();
     }
-    cl.sync();
-    if (act == ACT_COMBINE && rank != 0 && tid < kTailPad)  // replicate the reset tail
-      V[tail_at + tid] = cl.map_shared_rank(V, 0)[tail_at + tid];
+    // redund: the last reduction's cluster barrier already ordered every basis write this
+    // cycle before any CTA's next read of a neighbour's slice
+    if (!redund) {
+      cl.sync();
+      if (act == ACT_COMBINE && rank != 0 && tid < kTailPad)  // replicate the reset tail
+        V[tail_at + tid] = cl.map_shared_rank(V, 0)[tail_at + tid];
+    }
     __syncthreads();
     mark(4);
   }
@@ -1058,8 +1094,12 @@ bool launch_phi_cluster(cudaStream_t s, Engine& e, const EL& el, const BArgs& b)
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  static const int redund = [] {
+    const char* v = std::getenv("EXPDG_CLUSTER_CTL");
+    return v && v[0] == '0' ? 0 : 1;
+  }();
   EXPDG_CUDA(cudaLaunchKernelEx(&cfg, k_phi_cluster<EL>, e.st, e.base, e.ework, b, el, epc, lds, nslots,
-                                9 * nws * nws, (int)state_off, (int)(state_off + state)));
+                                9 * nws * nws, (int)state_off, (int)(state_off + state), redund));
   return true;
 }
 

@@ -391,7 +391,8 @@ Engine::Engine(int dev) : device(dev) {
   EXPDG_CUDA(cudaMemset(st, 0, sizeof(PhiState)));
   EXPDG_CUDA(cudaMallocHost(&st_host, sizeof(PhiState)));
   EXPDG_CUDA(cudaMalloc(&partials, sizeof(double) * kMaxPartials * kMaxSlots));
-  ework_doubles = size_t(9) * (kMaxBasis + 2) * (kMaxBasis + 2);
+  // one expm workspace per cluster CTA (the cluster engine runs the controller in every CTA)
+  ework_doubles = size_t(kClusterCTAs) * 9 * (kMaxBasis + 2) * (kMaxBasis + 2);
   EXPDG_CUDA(cudaMalloc(&ework, sizeof(double) * ework_doubles));
   const int maxsm = 216 * 1024;  // dynamic staging budget cap (EXPDG_TS_BUDGET <= this)
   EXPDG_CUDA(cudaFuncSetAttribute(k_ts<TS_DOTS>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
