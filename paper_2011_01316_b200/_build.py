@@ -20,6 +20,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", CSRC, "-I", os.path.join(ROOT, "include")]
+FLAGS += os.environ.get("EXPDG_NVCC_EXTRA", "").split()  # A/B builds (tools/mk_ab.sh)
 
 
 def _sources():

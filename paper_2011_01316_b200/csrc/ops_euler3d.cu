@@ -889,6 +889,365 @@ __global__ void __launch_bounds__(E3March<NP, DOT>::THREADS, 1)
   });
 }
 
+// ---------------------------------------------------------------- z-march with face warps
+// The plain (no dots) march of the phi cycle, role-split: eight node warps (one thread per node:
+// volume fluxes of plane z into a double-buffered flux array, one CTA-group barrier, then the
+// differentiation / face scatter / store of plane z), four face warps computing every face flux
+// of the plane ONE PLANE AHEAD of the node warps (double-buffered x/y face arrays, a 4-layer ring
+// of z-face layers, full/empty mbarriers), and the TMA producer warp.  The face warps' L2
+// gathers of the x/y neighbour faces and their flux arithmetic run under the node warps'
+// phases instead of between their barriers, and the node warps need one barrier per plane.
+template <int NP>
+struct E3MarchFW {
+  using B = E3March<NP, false>;
+  static constexpr int NN = B::NN, NF = B::NF, BLK = B::BLK, TX = B::TX, TY = B::TY, TE = B::TE;
+  static constexpr int CONS = B::CONS, CW = B::CW, PL = B::PL;
+  static constexpr int FWARPS = 4, FTH = 32 * FWARPS;
+  static constexpr int THREADS = CONS + 32 + FTH;
+  static constexpr int BUFD = 3 * PL;  // x, q~ primitives, b_1
+  static constexpr int NBUF = 4;
+  static constexpr int FXD = B::FXD, FYD = B::FYD, FZD = B::FZD;
+  static constexpr int SF = 3 * 5 * CONS;  // [dir][c][thread], two buffers
+  static constexpr int NZL = 4;            // z-face layers in flight
+  static constexpr int SMEM = (NBUF * BUFD + 2 * SF + 2 * (FXD + FYD) + NZL * FZD) * 8;
+  static constexpr bool OK = B::OK && SMEM <= 232448 - 3072;
+};
+
+template <int NP>
+__global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
+    k_e3_phi_march_fw(E3P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
+  using S = E3MarchFW<NP>;
+  constexpr int NN = S::NN, NF = S::NF, BLK = S::BLK, TX = S::TX, TY = S::TY, NBUF = S::NBUF, N = NP - 1;
+  extern __shared__ __align__(128) double smem[];
+  double* ring = smem;
+  double* sf0 = ring + NBUF * S::BUFD;
+  double* fxy0 = sf0 + 2 * S::SF;                  // two sets of [x faces | y faces]
+  double* fzl = fxy0 + 2 * (S::FXD + S::FYD);      // NZL layers
+  __shared__ uint64_t full[NBUF], empty[NBUF], ffull[2], fempty[2];
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[S::THREADS / 32];
+  __shared__ double s_red[1];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    s_go = apply_go(st, base);
+    if (s_go) {
+      s_j = st->j;
+      if (blockIdx.x == 0) {
+        if (apply_stage(st, base) == 1) st->dots_fused = 0;
+        st->app_bytes += 8.0 * (double)P.n * 4.0;
+        st->app_launches++;
+      }
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
+      for (int q = 0; q < NBUF; ++q) {
+        mbar_init(&full[q], 1);
+        mbar_init(&empty[q], 1 + S::FWARPS);  // the node warps + every face warp
+      }
+      for (int q = 0; q < 2; ++q) {
+        mbar_init(&ffull[q], S::FWARPS);
+        mbar_init(&fempty[q], 1);
+      }
+      fence_mbar_init();
+    }
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  const int nx = P.nx, ny = P.ny, nz = P.nz;
+  const int ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
+  const long long ntiles = (long long)ntx * nty;  // CTA c marches tiles c, c + G, ... (see k_e3_phi_march)
+  const double* b1 = (b.p == 1) ? b.b[1] : nullptr;
+  double nacc = 0.0;
+  auto unit = [&](long long tile, int& ix0, int& iy0, int& tx, int& ty) {
+    ix0 = (int)(tile % ntx) * TX;
+    iy0 = (int)(tile / ntx) * TY;
+    tx = min(TX, nx - ix0);
+    ty = min(TY, ny - iy0);
+  };
+
+  if (wid == S::CW) {
+    // ---------------- producer: the tile's elements of planes -1 .. nz
+    if (lane == 0) {
+      long long seq = 0;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int ix0, iy0, tx, ty;
+        unit(tile, ix0, iy0, tx, ty);
+        for (int q = 0; q < nz + 2; ++q, ++seq) {
+          int z = q - 1;
+          const double* srcx = x;
+          const double* srct = P.ut;
+          size_t pbase;
+          if (P.part && (z < 0 || z >= nz)) {  // halo plane of the neighbouring rank
+            srcx = z < 0 ? P.gx_lo : P.gx_hi;
+            srct = z < 0 ? P.gt_lo : P.gt_hi;
+            pbase = 0;
+          } else {
+            z = z < 0 ? z + nz : (z >= nz ? z - nz : z);
+            pbase = (size_t)z * ny * nx;
+          }
+          const int sl = (int)(seq % NBUF);
+          mbar_wait(&empty[sl], (int)(((seq / NBUF) & 1) ^ 1));
+          double* dst = ring + (size_t)sl * S::BUFD;
+          const bool with_b = b1 && q >= 1 && q <= nz;
+          const uint32_t rowb = (uint32_t)tx * BLK * 8;
+          mbar_arrive_expect_tx(&full[sl], (2u + (with_b ? 1u : 0u)) * (uint32_t)ty * rowb);
+          for (int ly = 0; ly < ty; ++ly) {
+            const size_t e = pbase + (size_t)(iy0 + ly) * nx + ix0;
+            bulk_g2s(dst + (size_t)ly * TX * BLK, srcx + e * BLK, rowb, &full[sl]);
+            bulk_g2s(dst + S::PL + (size_t)ly * TX * BLK, srct + e * BLK, rowb, &full[sl]);
+            if (with_b) {
+              const size_t eb = ((size_t)(q - 1) * ny + iy0 + ly) * nx + ix0;
+              bulk_g2s(dst + 2 * S::PL + (size_t)ly * TX * BLK, b1 + eb * BLK, rowb, &full[sl]);
+            }
+          }
+        }
+      }
+    }
+  } else if (wid > S::CW) {
+    // ---------------- face warps: every face flux of plane z, once (the reference's rhs_faces
+    // loop, proj/src/euler.cpp:260-297, extended to 3D as in oracle/src/euler.cpp)
+    const int ft = tid - (S::CONS + 32), fw = wid - (S::CW + 1);
+    constexpr int NFX = (TX + 1) * TY * NF, NFY = TX * (TY + 1) * NF, NFZ = TX * TY * NF;
+    long long seq = 0;
+    unsigned it = 0, lc = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      int ix0, iy0, tx, ty;
+      unit(tile, ix0, iy0, tx, ty);
+      auto wait_plane = [&](long long q) { mbar_wait(&full[(seq + q) % NBUF], (int)(((seq + q) / NBUF) & 1)); };
+      auto slot = [&](long long q) { return ring + (size_t)((seq + q) % NBUF) * S::BUFD; };
+      wait_plane(0);
+      wait_plane(1);
+      unsigned lb = lc++ % S::NZL;
+      for (int z = 0; z < nz; ++z, ++it) {
+        const long long q = z + 1;
+        const unsigned lt = lc++ % S::NZL;
+        wait_plane(q + 1);
+        const int set = it & 1;
+        mbar_wait(&fempty[set], ((it >> 1) & 1) ^ 1);  // the node warps consumed this set two planes ago
+        const double* cur = slot(q);
+        const double* lo = slot(q - 1);
+        const double* hi = slot(q + 1);
+        double* fxf = fxy0 + set * (S::FXD + S::FYD);
+        double* fyf = fxf + S::FXD;
+        double* fz_bot = fzl + lb * S::FZD;
+        double* fz_top = fzl + lt * S::FZD;
+        const int total = NFX + NFY + NFZ + (z == 0 ? NFZ : 0);
+        auto from_ring = [&](const double* pl, int e, int nd, double(&qq)[5], double(&tt)[5]) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            qq[c] = pl[e * BLK + c * NN + nd] * xs;
+            tt[c] = pl[S::PL + e * BLK + c * NN + nd];
+          }
+        };
+        auto from_gmem = [&](int gx, int gy, int nd, double(&qq)[5], double(&tt)[5]) {
+          const size_t e = ((size_t)z * ny + gy) * nx + gx;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            qq[c] = x[(e * 5 + c) * NN + nd] * xs;
+            tt[c] = __ldg(P.ut + (e * 5 + c) * NN + nd);
+          }
+        };
+        for (int f = ft; f < total; f += S::FTH) {
+          double qa[5], ta[5], qb[5], tb[5], fl[5];
+          double* dst;
+          bool bad = false;
+          if (f < NFX) {  // x-face column fc between tile columns fc - 1 (low) and fc (high)
+            const int fc = f / (TY * NF), rem = f - fc * TY * NF, fy = rem / NF, fn = rem - fy * NF;
+            if (fc > tx || fy >= ty) continue;
+            const int nlo = fn * NP + N, nhi = fn * NP;  // fn = k NP + j
+            if (fc == 0) from_gmem(ix0 == 0 ? nx - 1 : ix0 - 1, iy0 + fy, nlo, qa, ta);
+            else from_ring(cur, fy * TX + fc - 1, nlo, qa, ta);
+            if (fc == tx) from_gmem(ix0 + tx == nx ? 0 : ix0 + tx, iy0 + fy, nhi, qb, tb);
+            else from_ring(cur, fy * TX + fc, nhi, qb, tb);
+            face3(0, 0, P.gamma, qa, qb, ta, tb, fl, bad);
+            dst = fxf + ((fc * TY + fy) * NF + fn) * 5;
+          } else if (f < NFX + NFY) {  // y-face row fc between tile rows fc - 1 and fc
+            const int g = f - NFX, fc = g / (TX * NF), rem = g - fc * TX * NF, fxl = rem / NF, fn = rem - fxl * NF;
+            if (fc > ty || fxl >= tx) continue;
+            const int fi = fn % NP, fk = fn / NP;
+            const int nlo = (fk * NP + N) * NP + fi, nhi = (fk * NP) * NP + fi;
+            if (fc == 0) from_gmem(ix0 + fxl, iy0 == 0 ? ny - 1 : iy0 - 1, nlo, qa, ta);
+            else from_ring(cur, (fc - 1) * TX + fxl, nlo, qa, ta);
+            if (fc == ty) from_gmem(ix0 + fxl, iy0 + ty == ny ? 0 : iy0 + ty, nhi, qb, tb);
+            else from_ring(cur, fc * TX + fxl, nhi, qb, tb);
+            face3(0, 1, P.gamma, qa, qb, ta, tb, fl, bad);
+            dst = fyf + ((fc * TX + fxl) * NF + fn) * 5;
+          } else {  // z-faces: above this plane, or below it on the tile's first plane
+            const int g = f - NFX - NFY;
+            const bool top = g < NFZ;
+            const int gg = top ? g : g - NFZ;
+            const int el = gg / NF, fn = gg - el * NF;
+            if (el % TX >= tx || el / TX >= ty) continue;
+            from_ring(top ? cur : lo, el, (N * NP) * NP + fn, qa, ta);
+            from_ring(top ? hi : cur, el, fn, qb, tb);
+            face3(0, 2, P.gamma, qa, qb, ta, tb, fl, bad);
+            dst = (top ? fz_top : fz_bot) + (el * NF + fn) * 5;
+          }
+#pragma unroll
+          for (int c = 0; c < 5; ++c) dst[c] = fl[c];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&ffull[set]);
+          // plane z is no longer needed here (the next iteration reads z + 1, z + 2); the halo
+          // planes are read by the face warps only, so warp 0 also arrives for the node warps
+          mbar_arrive(&empty[(seq + q) % NBUF]);
+          if (z == 0) mbar_arrive_cnt(&empty[seq % NBUF], fw == 0 ? 2u : 1u);
+          if (z == nz - 1) mbar_arrive_cnt(&empty[(seq + q + 1) % NBUF], fw == 0 ? 2u : 1u);
+        }
+        lb = lt;
+      }
+      seq += nz + 2;
+    }
+  } else {
+    // ---------------- node warps: one thread per node of the tile
+    const int le = tid / NN, node = tid % NN;
+    const int lx = le % TX, ly = le / TX;
+    const int i = node % NP, j = (node / NP) % NP, kk = node / NF;
+    double wdi[NP], wdj[NP], wdk[NP];
+#pragma unroll
+    for (int m = 0; m < NP; ++m) {
+      wdi[m] = P.WD[m * NP + i];
+      wdj[m] = P.WD[m * NP + j];
+      wdk[m] = P.WD[m * NP + kk];
+    }
+    const double wi = P.w[i], wj = P.w[j], wk = P.w[kk];
+    const double iw3 = 1.0 / (wi * wj * wk);
+    long long seq = 0;
+    unsigned it = 0, lc = 0;
+    int prev_slot = -1;  // ring slot of the plane differentiated in the previous iteration
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      int ix0, iy0, tx, ty;
+      unit(tile, ix0, iy0, tx, ty);
+      const bool active = lx < tx && ly < ty;
+      const int ix = ix0 + lx, iy = iy0 + ly;
+      const double hx = active ? __ldg(P.hx + ix) : 1.0, hy = active ? __ldg(P.hy + iy) : 1.0;
+      const double ihxy = active ? __ldg(P.ihx + ix) * __ldg(P.ihy + iy) : 1.0;
+      unsigned lb = lc++ % S::NZL;
+      for (int z = 0; z < nz; ++z, ++it) {
+        const long long q = z + 1;
+        const unsigned lt = lc++ % S::NZL;
+        const int sl = (int)((seq + q) % NBUF);
+        mbar_wait(&full[sl], (int)(((seq + q) / NBUF) & 1));
+        const double* cur = ring + (size_t)sl * S::BUFD;
+        double* sf = sf0 + (it & 1) * S::SF;
+        // ---- volume fluxes of this node
+        if (active) {
+          double qv[5], tv[5];
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            qv[c] = cur[le * BLK + c * NN + node] * xs;
+            tv[c] = cur[S::PL + le * BLK + c * NN + node];
+          }
+          const Prim3 tp = prim3_frozen(tv);
+          double Pv, Qv, fl[5];
+          jac3_pre(tp, P.gamma, qv, Pv, Qv);
+          jac3_dir<0>(tp, Pv, Qv, qv, fl);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) sf[(0 * 5 + c) * S::CONS + tid] = fl[c];
+          jac3_dir<1>(tp, Pv, Qv, qv, fl);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) sf[(1 * 5 + c) * S::CONS + tid] = fl[c];
+          jac3_dir<2>(tp, Pv, Qv, qv, fl);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) sf[(2 * 5 + c) * S::CONS + tid] = fl[c];
+        }
+        strip_sync<S::CONS>();  // volume fluxes of plane z complete; every thread is past plane z - 1
+        if (tid == 0 && prev_slot >= 0) {
+          mbar_arrive(&empty[prev_slot]);
+          mbar_arrive(&fempty[(it - 1) & 1]);
+        }
+        prev_slot = sl;
+        mbar_wait(&ffull[it & 1], (it >> 1) & 1);  // the face fluxes of plane z
+        // ---- differentiate, scatter the face fluxes, scale
+        if (active) {
+          const double* fxf = fxy0 + (it & 1) * (S::FXD + S::FYD);
+          const double* fyf = fxf + S::FXD;
+          const double* fz_bot = fzl + lb * S::FZD;
+          const double* fz_top = fzl + lt * S::FZD;
+          const double hz = __ldg(P.hz + z);
+          const double sxv = (0.25 * hy * hz) * wj * wk;
+          const double syv = (0.25 * hz * hx) * wi * wk;
+          const double szv = (0.25 * hx * hy) * wi * wj;
+          const int t0 = tid - node;  // this element's first thread
+          double r[5];
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            const double* fx = sf + (0 * 5 + c) * S::CONS + t0 + (kk * NP + j) * NP;
+            const double* fy = sf + (1 * 5 + c) * S::CONS + t0 + kk * NF + i;
+            const double* fzz = sf + (2 * 5 + c) * S::CONS + t0 + j * NP + i;
+            double ax = 0.0, ay = 0.0, az = 0.0;
+#pragma unroll
+            for (int m = 0; m < NP; ++m) {
+              ax = fma(wdi[m], fx[m], ax);
+              ay = fma(wdj[m], fy[m * NP], ay);
+              az = fma(wdk[m], fzz[m * NF], az);
+            }
+            r[c] = sxv * ax;
+            r[c] += syv * ay;
+            r[c] += szv * az;
+          }
+          // faces x, y, z (oracle order); owner (low side, node a = N) subtracts
+          if (i == 0 || i == N) {
+            const double* f = fxf + (((lx + (i == N ? 1 : 0)) * TY + ly) * NF + kk * NP + j) * 5;
+            const double fw = (0.25 * (hy * hz)) * wj * wk;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) r[c] = i == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
+          }
+          if (j == 0 || j == N) {
+            const double* f = fyf + (((ly + (j == N ? 1 : 0)) * TX + lx) * NF + kk * NP + i) * 5;
+            const double fw = (0.25 * (hx * hz)) * wi * wk;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) r[c] = j == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
+          }
+          if (kk == 0 || kk == N) {
+            const double* f = (kk == N ? fz_top : fz_bot) + (le * NF + j * NP + i) * 5;
+            const double fw = (0.25 * (hx * hy)) * wi * wj;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) r[c] = kk == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
+          }
+          const double im = (8.0 * ihxy * __ldg(P.ihz + z)) * iw3;  // 8 / (hx hy hz w_i w_j w_k)
+          const size_t e = ((size_t)z * ny + iy) * nx + ix;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            const size_t g = (e * 5 + c) * NN + node;
+            double v = r[c] * im;
+            if (b1) v = fma(s_xt[0], cur[2 * S::PL + le * BLK + c * NN + node], v);
+            else v = aug_tail(b, s_xt, g, v);
+            v = dt * v;
+            y[g] = v;
+            nacc = fma(v, v, nacc);
+          }
+        }
+        lb = lt;
+      }
+      seq += nz + 2;
+    }
+    strip_sync<S::CONS>();
+    if (tid == 0 && prev_slot >= 0) {
+      mbar_arrive(&empty[prev_slot]);
+      mbar_arrive(&fempty[(it - 1) & 1]);
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
+    const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
+    y[P.n + tid] = v;
+    if (st->tail_here) nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (tid == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, 2 * kMaxSlots + 2, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
+}
+
 __global__ void k_e3_freeze(const double* __restrict__ q, long long nelem, int nn, double gamma,
                             double* __restrict__ frozen) {
   const long long nodes = nelem * nn;
@@ -916,6 +1275,9 @@ class Euler3D : public OpDevice {
   long long plane = 0;     // doubles per element plane
   bool use_march = E3March<NP>::OK;  // EXPDG_E3_TILE=1: the element-tile JVP
   int march_grid = 1;
+  // the plain march with face warps (EXPDG_E3_FW=0: the single-role march)
+  static constexpr bool kFwOk = E3March<NP>::OK && E3MarchFW<NP>::OK;
+  bool use_fw = kFwOk;
   // the z-march also takes the DCGS2 pass-1 dots (EXPDG_E3_DOTS=0: off) on meshes of whole
   // tiles (the dot warps read the tile's elements as one contiguous block)
   static constexpr bool kDotFits = E3March<NP>::OK && E3March<NP, true>::FITS;
@@ -1000,6 +1362,10 @@ class Euler3D : public OpDevice {
       const long long tiles = (long long)((d.nx + SM::TX - 1) / SM::TX) * ((d.ny + SM::TY - 1) / SM::TY);
       march_grid = (int)std::max<long long>(1, std::min<long long>(tiles, 148LL * std::max(1, per_sm)));
       whole_tiles = d.nx % SM::TX == 0 && d.ny % SM::TY == 0;
+      if (const char* v = std::getenv("EXPDG_E3_FW")) use_fw = use_fw && v[0] != '0';
+      if constexpr (kFwOk)
+        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        E3MarchFW<NP>::SMEM));
       if constexpr (kDotFits) {
         using SD = E3March<NP, true>;
         EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1026,6 +1392,13 @@ class Euler3D : public OpDevice {
           if (dots_on() && stage == 1) {
             using SD = E3March<NP, true>;
             k_e3_phi_march<NP, true><<<dots_grid, SD::THREADS, SD::SMEM, s>>>(params(frozen), st, base, partials, b);
+            return;
+          }
+        }
+        if constexpr (kFwOk) {
+          if (use_fw) {
+            k_e3_phi_march_fw<NP><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(params(frozen), st, base,
+                                                                                                 partials, b);
             return;
           }
         }
