@@ -889,6 +889,9 @@ __global__ void __launch_bounds__(E3March<NP, DOT>::THREADS, 1)
   });
 }
 
+#ifndef EXPDG_E3_FWARPS
+#define EXPDG_E3_FWARPS 6
+#endif
 // ---------------------------------------------------------------- z-march with face warps
 // The plain (no dots) march of the phi cycle, role-split: eight node warps (one thread per node:
 // volume fluxes of plane z into a double-buffered flux array, one CTA-group barrier, then the
@@ -902,11 +905,14 @@ struct E3MarchFW {
   using B = E3March<NP, false>;
   static constexpr int NN = B::NN, NF = B::NF, BLK = B::BLK, TX = B::TX, TY = B::TY, TE = B::TE;
   static constexpr int CONS = B::CONS, CW = B::CW, PL = B::PL;
-  static constexpr int FWARPS = 4, FTH = 32 * FWARPS;
+  static constexpr int FWARPS = EXPDG_E3_FWARPS, FTH = 32 * FWARPS;
   static constexpr int THREADS = CONS + 32 + FTH;
   static constexpr int BUFD = 3 * PL;  // x, q~ primitives, b_1
   static constexpr int NBUF = 4;
-  static constexpr int FXD = B::FXD, FYD = B::FYD, FZD = B::FZD;
+  // x-face columns / y-face rows padded by two doubles: the low- and high-side nodes of an
+  // element then read their faces from different banks in the scatter
+  static constexpr int FXC = TY * NF * 5 + 2, FYR = TX * NF * 5 + 2;
+  static constexpr int FXD = (TX + 1) * FXC, FYD = (TY + 1) * FYR, FZD = B::FZD;
   static constexpr int SF = 3 * 5 * CONS;  // [dir][c][thread], two buffers
   static constexpr int NZL = 4;            // z-face layers in flight
   static constexpr int SMEM = (NBUF * BUFD + 2 * SF + 2 * (FXD + FYD) + NZL * FZD) * 8;
@@ -1067,7 +1073,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
             if (fc == tx) from_gmem(ix0 + tx == nx ? 0 : ix0 + tx, iy0 + fy, nhi, qb, tb);
             else from_ring(cur, fy * TX + fc, nhi, qb, tb);
             face3(0, 0, P.gamma, qa, qb, ta, tb, fl, bad);
-            dst = fxf + ((fc * TY + fy) * NF + fn) * 5;
+            dst = fxf + fc * S::FXC + (fy * NF + fn) * 5;
           } else if (f < NFX + NFY) {  // y-face row fc between tile rows fc - 1 and fc
             const int g = f - NFX, fc = g / (TX * NF), rem = g - fc * TX * NF, fxl = rem / NF, fn = rem - fxl * NF;
             if (fc > ty || fxl >= tx) continue;
@@ -1078,7 +1084,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
             if (fc == ty) from_gmem(ix0 + fxl, iy0 + ty == ny ? 0 : iy0 + ty, nhi, qb, tb);
             else from_ring(cur, fc * TX + fxl, nhi, qb, tb);
             face3(0, 1, P.gamma, qa, qb, ta, tb, fl, bad);
-            dst = fyf + ((fc * TX + fxl) * NF + fn) * 5;
+            dst = fyf + fc * S::FYR + (fxl * NF + fn) * 5;
           } else {  // z-faces: above this plane, or below it on the tile's first plane
             const int g = f - NFX - NFY;
             const bool top = g < NFZ;
@@ -1135,6 +1141,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
         const long long q = z + 1;
         const unsigned lt = lc++ % S::NZL;
         const int sl = (int)((seq + q) % NBUF);
+        const double hz = __ldg(P.hz + z), ihz = __ldg(P.ihz + z);  // issued before the waits, used after them
         mbar_wait(&full[sl], (int)(((seq + q) / NBUF) & 1));
         const double* cur = ring + (size_t)sl * S::BUFD;
         double* sf = sf0 + (it & 1) * S::SF;
@@ -1172,7 +1179,6 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
           const double* fyf = fxf + S::FXD;
           const double* fz_bot = fzl + lb * S::FZD;
           const double* fz_top = fzl + lt * S::FZD;
-          const double hz = __ldg(P.hz + z);
           const double sxv = (0.25 * hy * hz) * wj * wk;
           const double syv = (0.25 * hz * hx) * wi * wk;
           const double szv = (0.25 * hx * hy) * wi * wj;
@@ -1196,13 +1202,13 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
           }
           // faces x, y, z (oracle order); owner (low side, node a = N) subtracts
           if (i == 0 || i == N) {
-            const double* f = fxf + (((lx + (i == N ? 1 : 0)) * TY + ly) * NF + kk * NP + j) * 5;
+            const double* f = fxf + (lx + (i == N ? 1 : 0)) * S::FXC + (ly * NF + kk * NP + j) * 5;
             const double fw = (0.25 * (hy * hz)) * wj * wk;
 #pragma unroll
             for (int c = 0; c < 5; ++c) r[c] = i == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
           }
           if (j == 0 || j == N) {
-            const double* f = fyf + (((ly + (j == N ? 1 : 0)) * TX + lx) * NF + kk * NP + i) * 5;
+            const double* f = fyf + (ly + (j == N ? 1 : 0)) * S::FYR + (lx * NF + kk * NP + i) * 5;
             const double fw = (0.25 * (hx * hz)) * wi * wk;
 #pragma unroll
             for (int c = 0; c < 5; ++c) r[c] = j == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
@@ -1213,7 +1219,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
 #pragma unroll
             for (int c = 0; c < 5; ++c) r[c] = kk == N ? r[c] - fw * f[c] : r[c] + fw * f[c];
           }
-          const double im = (8.0 * ihxy * __ldg(P.ihz + z)) * iw3;  // 8 / (hx hy hz w_i w_j w_k)
+          const double im = (8.0 * ihxy * ihz) * iw3;  // 8 / (hx hy hz w_i w_j w_k)
           const size_t e = ((size_t)z * ny + iy) * nx + ix;
 #pragma unroll
           for (int c = 0; c < 5; ++c) {
