@@ -954,6 +954,328 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 3 : 1
   });
 }
 
+// ---------------------------------------------------------------- strip JVP with face warps
+// The plain (no dots) strip JVP, role-split like the 3D z-march (ops_euler3d.cu,
+// k_e3_phi_march_fw): the node warps compute the volume fluxes of row r into a double-buffered
+// flux array, pass one barrier, then differentiate / scatter / store row r; FWARPS face warps
+// compute every numerical flux of the row (the reference's rhs_faces loop,
+// proj/src/euler.cpp:260-297) one row ahead into double-buffered x-face arrays and a 4-deep ring
+// of y-face rows, handed over by full/empty mbarriers.  The face arithmetic leaves the node
+// warps' critical path (volume -> barrier -> differentiate).
+#ifndef EXPDG_E2_FWARPS
+#define EXPDG_E2_FWARPS 1
+#endif
+template <int NP, int CW>
+struct E2StripFW {
+  using B = E2Strip<NP, CW, false>;
+  static constexpr int NN = B::NN, CONS = B::CONS, W = B::W, BLK = B::BLK, ROWD = B::ROWD, BUFD = B::BUFD;
+  static constexpr int NBUF = 4, FX = B::FX, FY = B::FY;
+  static constexpr int FWARPS = EXPDG_E2_FWARPS, FTH = 32 * FWARPS;
+  static constexpr int THREADS = CONS + 32 + FTH;
+  static constexpr int SF = 2 * W * BLK;  // volume fluxes of a row, two buffers
+  static constexpr int NYL = 4;           // y-face rows in flight
+  static constexpr int SMEM = (NBUF * BUFD + 2 * SF + 2 * FX + NYL * FY) * 8;
+  static constexpr int PER_SM = CW <= 4 ? 3 : 1;
+};
+
+template <int NP, bool ROE, int CW>
+__global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>::PER_SM)
+    k_e2_phi_strip_fw(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
+  using S = E2StripFW<NP, CW>;
+  constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
+  extern __shared__ __align__(128) double smem[];
+  double* ring = smem;
+  double* sf0 = smem + NBUF * S::BUFD;
+  double* sfx0 = sf0 + 2 * S::SF;
+  double* sfy0 = sfx0 + 2 * S::FX;
+  __shared__ uint64_t full[NBUF], empty[NBUF], ffull[2], fempty[2];
+  __shared__ double s_wd[NP * NP], s_wq[NP];
+  __shared__ int s_go, s_j;
+  __shared__ double s_xs, s_dt, s_xt[kMaxP];
+  __shared__ long long s_ld;
+  __shared__ double s_buf[S::THREADS / 32];
+  __shared__ double s_red[1];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    s_go = apply_go(st, base);
+    if (s_go) {
+      s_j = st->j;
+      if (blockIdx.x == 0) {
+        if (apply_stage(st, base) == 1) st->dots_fused = 0;
+        st->app_bytes += 8.0 * (double)P.n * 4.0;
+        st->app_launches++;
+      }
+      s_xs = st->scale[s_j];
+      s_dt = st->dt;
+      s_ld = st->ld;
+      const double* xslot = base + (size_t)s_j * st->ld;
+      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
+      for (int q = 0; q < NBUF; ++q) {
+        mbar_init(&full[q], 1);
+        mbar_init(&empty[q], 1 + S::FWARPS);  // the node warps + every face warp
+      }
+      for (int q = 0; q < 2; ++q) {
+        mbar_init(&ffull[q], S::FWARPS);
+        mbar_init(&fempty[q], 1);
+      }
+      fence_mbar_init();
+    }
+  }
+  for (int q = tid; q < NP * NP; q += blockDim.x) s_wd[q] = P.WD[q];
+  for (int q = tid; q < NP; q += blockDim.x) s_wq[q] = P.w[q];
+  __syncthreads();
+  if (!s_go) return;
+  const double* x = base + (size_t)s_j * s_ld;
+  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double xs = s_xs, dt = s_dt;
+  const int nx = P.nx, ny = P.ny;
+  const int nstrips = (nx + W - 1) / W;
+  const long long rsteps = (long long)nstrips * ny;
+  const long long k0 = rsteps * blockIdx.x / gridDim.x, k1 = rsteps * (blockIdx.x + 1) / gridDim.x;
+  const double* b1 = (b.p == 1) ? b.b[1] : nullptr;
+  double nacc = 0.0;
+
+  if (wid == CW) {
+    // ---------------- producer: x / frozen rows with their E/W halo elements
+    if (lane == 0) {
+      long long seq = 0;
+      for (long long k = k0; k < k1;) {
+        const StripUnit su = strip_unit<W>(k, k1, nx, ny);
+        const int ie0 = su.ie0, w = su.w, r0 = su.r0, r1 = su.r1;
+        for (int q = 0; q < r1 - r0 + 2; ++q) {
+          int row = r0 - 1 + q;
+          const double* srcx = x;
+          const double* srct = P.ut;
+          if (P.part && (row < 0 || row >= ny)) {  // halo row of the neighbouring rank
+            srcx = row < 0 ? P.gx_lo : P.gx_hi;
+            srct = row < 0 ? P.gt_lo : P.gt_hi;
+            row = 0;
+          } else {
+            row = row < 0 ? row + ny : (row >= ny ? row - ny : row);
+          }
+          const int sl = (int)(seq % NBUF);
+          mbar_wait(&empty[sl], (int)(((seq / NBUF) & 1) ^ 1));
+          double* dst = ring + (size_t)sl * S::BUFD;
+          const uint32_t eb = BLK * 8;
+          mbar_arrive_expect_tx(&full[sl], 2u * (uint32_t)(w + 2) * eb);
+          const size_t rbase = (size_t)row * nx;
+          const int left = ie0 == 0 ? nx - 1 : ie0 - 1;
+          const int right = ie0 + w == nx ? 0 : ie0 + w;
+          for (int arr = 0; arr < 2; ++arr) {
+            const double* src = arr == 0 ? srcx : srct;
+            double* d = dst + arr * S::ROWD;
+            if (ie0 >= 1 && ie0 + w < nx) {
+              bulk_g2s(d, src + (rbase + left) * BLK, (uint32_t)(w + 2) * eb, &full[sl]);
+            } else {
+              bulk_g2s(d, src + (rbase + left) * BLK, eb, &full[sl]);
+              bulk_g2s(d + BLK, src + (rbase + ie0) * BLK, (uint32_t)w * eb, &full[sl]);
+              bulk_g2s(d + (size_t)(w + 1) * BLK, src + (rbase + right) * BLK, eb, &full[sl]);
+            }
+          }
+          ++seq;
+        }
+      }
+    }
+  } else if (wid > CW) {
+    // ---------------- face warps: x-faces of row r, the y-faces above it and, on a unit's first
+    // row, the y-faces below it
+    const int ft = tid - (S::CONS + 32), fw = wid - (CW + 1);
+    long long seq = 0;
+    unsigned it = 0, lc = 0;
+    for (long long k = k0; k < k1;) {
+      const StripUnit su = strip_unit<W>(k, k1, nx, ny);
+      const int w = su.w, r0 = su.r0, r1 = su.r1;
+      auto slot = [&](long long q) { return ring + (size_t)((seq + q) % NBUF) * S::BUFD; };
+      auto wait_row = [&](long long q) { mbar_wait(&full[(seq + q) % NBUF], (int)(((seq + q) / NBUF) & 1)); };
+      wait_row(0);
+      wait_row(1);
+      unsigned lb = lc++ % S::NYL;
+      const int nxf = (w + 1) * NP, nyf = w * NP;
+      for (int r = r0; r < r1; ++r, ++it) {
+        const long long q = r - r0 + 1;
+        const unsigned lt = lc++ % S::NYL;
+        wait_row(q + 1);
+        const int set = it & 1;
+        mbar_wait(&fempty[set], ((it >> 1) & 1) ^ 1);  // the node warps consumed this set two rows ago
+        const double* cur = slot(q);
+        const double* lo = slot(q - 1);
+        const double* hi = slot(q + 1);
+        double* sfx = sfx0 + set * S::FX;
+        double* ytop = sfy0 + lt * S::FY;
+        double* ybot = sfy0 + lb * S::FY;
+        const int total = nxf + nyf + (r == r0 ? nyf : 0);
+        for (int t = ft; t < total; t += S::FTH) {
+          double qa[4], ta[4], qb[4], tb[4], f[4];
+          const double* ra;
+          const double* rb;
+          int pa, pb, na, nb, dir;
+          double* dst;
+          if (t < nxf) {  // between ring elements fi (W side) and fi + 1 (E side)
+            const int fi = t / NP, jn = t - fi * NP;
+            ra = cur; rb = cur; pa = fi; pb = fi + 1; na = jn * NP + N; nb = jn * NP; dir = 0;
+            dst = sfx + (fi * NP + jn) * 4;
+          } else if (t < nxf + nyf) {  // top face of element le: (le, j = N) | row above (le, j = 0)
+            const int tt = t - nxf, le2 = tt / NP, in = tt - le2 * NP;
+            ra = cur; rb = hi; pa = pb = le2 + 1; na = N * NP + in; nb = in; dir = 1;
+            dst = ytop + (le2 * NP + in) * 4;
+          } else {  // bottom face of element le (first row of the unit)
+            const int tt = t - nxf - nyf, le2 = tt / NP, in = tt - le2 * NP;
+            ra = lo; rb = cur; pa = pb = le2 + 1; na = N * NP + in; nb = in; dir = 1;
+            dst = ybot + (le2 * NP + in) * 4;
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            qa[c] = ra[pa * BLK + c * NN + na] * xs;
+            ta[c] = ra[S::ROWD + pa * BLK + c * NN + na];
+            qb[c] = rb[pb * BLK + c * NN + nb] * xs;
+            tb[c] = rb[S::ROWD + pb * BLK + c * NN + nb];
+          }
+          bool bad = false;
+          face_flux<ROE>(0, dir, P.gamma, qa, qb, ta, tb, f, bad);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) dst[c] = f[c];
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&ffull[set]);
+          // row r is no longer needed here; the halo rows are read by the face warps only, so
+          // warp 0 also arrives for the node warps
+          mbar_arrive(&empty[(seq + q) % NBUF]);
+          if (r == r0) mbar_arrive_cnt(&empty[seq % NBUF], fw == 0 ? 2u : 1u);
+          if (r == r1 - 1) mbar_arrive_cnt(&empty[(seq + q + 1) % NBUF], fw == 0 ? 2u : 1u);
+        }
+        lb = lt;
+      }
+      seq += r1 - r0 + 2;
+    }
+  } else {
+    // ---------------- node warps: one thread per node of the strip row
+    const int le = tid / NN, node = tid % NN;
+    const int i = node % NP, j = node / NP;
+    double wdi[NP], wdj[NP];
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      wdi[q] = s_wd[q * NP + i];
+      wdj[q] = s_wd[q * NP + j];
+    }
+    const double wi = s_wq[i], wj = s_wq[j];
+    const double iwij = 1.0 / (wi * wj);
+    long long seq = 0;
+    unsigned it = 0, lc = 0;
+    int prev_slot = -1;
+    for (long long k = k0; k < k1;) {
+      const StripUnit su = strip_unit<W>(k, k1, nx, ny);
+      const int ie0 = su.ie0, w = su.w, r0 = su.r0, r1 = su.r1;
+      const bool active = le < w;
+      const int ie = ie0 + le;
+      const double hx = active ? __ldg(P.hx + ie) : 1.0;
+      const double ihx = active ? __ldg(P.ihx + ie) : 1.0;
+      const double sxs = 0.5 * hx * wi;
+      unsigned lb = lc++ % S::NYL;
+      for (int r = r0; r < r1; ++r, ++it) {
+        const long long q = r - r0 + 1;  // ring index of row r
+        const unsigned lt = lc++ % S::NYL;
+        // b_1 of this node (p == 1), read in place: issued now, used after the barrier
+        double bv[4] = {0.0, 0.0, 0.0, 0.0};
+        if (b1 && active) {
+          const size_t e = (size_t)r * nx + ie;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) bv[c] = __ldg(b1 + (e * 4 + c) * NN + node);
+        }
+        const double hy = __ldg(P.hy + r);
+        const double ihy = __ldg(P.ihy + r);
+        const int sl = (int)((seq + q) % NBUF);
+        mbar_wait(&full[sl], (int)(((seq + q) / NBUF) & 1));
+        const double* cur = ring + (size_t)sl * S::BUFD;
+        double* sf = sf0 + (it & 1) * S::SF;
+        if (active) {
+          double qv[4], tv[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            qv[c] = cur[(le + 1) * BLK + c * NN + node] * xs;
+            tv[c] = cur[S::ROWD + (le + 1) * BLK + c * NN + node];
+          }
+          const Prim tp = prim_frozen(tv);
+          double fx[4], fy[4];
+          jac_apply_xy(tp, P.gamma, qv, fx, fy);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            sf[((le * 2 + 0) * 4 + c) * NN + node] = fx[c];
+            sf[((le * 2 + 1) * 4 + c) * NN + node] = fy[c];
+          }
+        }
+        strip_sync<S::CONS>();  // volume fluxes of row r complete; every thread is past row r - 1
+        if (tid == 0 && prev_slot >= 0) {
+          mbar_arrive(&empty[prev_slot]);
+          mbar_arrive(&fempty[(it - 1) & 1]);
+        }
+        prev_slot = sl;
+        mbar_wait(&ffull[it & 1], (it >> 1) & 1);  // the face fluxes of row r
+        if (active) {
+          const double* sfx = sfx0 + (it & 1) * S::FX;
+          const double sy = 0.5 * hy * wj;
+          double rr[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double* fxr = sf + ((le * 2 + 0) * 4 + c) * NN + j * NP;
+            const double* fyc = sf + ((le * 2 + 1) * 4 + c) * NN + i;
+            double ax = 0.0, ay = 0.0;
+#pragma unroll
+            for (int m = 0; m < NP; ++m) {
+              ax = fma(wdi[m], fxr[m], ax);
+              ay = fma(wdj[m], fyc[m * NP], ay);
+            }
+            rr[c] = sy * ax;
+            rr[c] += sxs * ay;
+          }
+          // scatter of the face fluxes: owner side (normal +e) subtracts, neighbour adds
+          if (i == N || i == 0) {
+            const double* f = sfx + (((i == N ? le + 1 : le) * NP) + j) * 4;
+            const double fw = (i == N ? -0.5 : 0.5) * hy * wj;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) rr[c] = fma(fw, f[c], rr[c]);
+          }
+          if (j == N || j == 0) {
+            const double* f = sfy0 + (j == N ? lt : lb) * S::FY + (le * NP + i) * 4;
+            const double fw = (j == N ? -0.5 : 0.5) * hx * wi;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) rr[c] = fma(fw, f[c], rr[c]);
+          }
+          const double im = (4.0 * ihx * ihy) * iwij;  // 4 / (hx hy w_i w_j)
+          const size_t e = (size_t)r * nx + ie;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const size_t g = (e * 4 + c) * NN + node;
+            double v = rr[c] * im;
+            if (b1) v = fma(s_xt[0], bv[c], v);
+            else v = aug_tail(b, s_xt, g, v);
+            v = dt * v;
+            y[g] = v;
+            nacc = fma(v, v, nacc);
+          }
+        }
+        lb = lt;
+      }
+      seq += r1 - r0 + 2;
+    }
+    strip_sync<S::CONS>();
+    if (tid == 0 && prev_slot >= 0) {
+      mbar_arrive(&empty[prev_slot]);
+      mbar_arrive(&fempty[(it - 1) & 1]);
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
+    const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
+    y[P.n + tid] = v;
+    if (st->tail_here) nacc = fma(v, v, nacc);
+  }
+  const double tot = block_sum(nacc, s_buf);
+  if (tid == 0) s_red[0] = tot;
+  __syncthreads();
+  grid_reduce_last(s_red, 1, partials, 2 * kMaxSlots + 2, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
+}
+
 // (u, v, H, a | sqrt(rho)) of q~ per node (proj/src/euler.cpp:15-24): the frozen
 // data of the linearised operator, 32 B/node like q~ itself.
 template <bool ROE>
@@ -986,6 +1308,26 @@ class Euler2D : public OpDevice {
   // the same for the pipelined lookahead application (EXPDG_E2_CW2): half-width strips at three
   // CTAs per SM (128 registers) run it in 1.01 vs 1.12 ms at C4 (same box)
   int strip_cw2 = 4;
+  // the plain half-width strip with face warps (EXPDG_E2_FW=0: the single-role strip)
+  bool use_fw = true;
+  int fw_per_sm = 0;
+  void launch_strip_fw(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
+                       const BArgs& b) {
+    using SS = E2StripFW<NP, 4>;
+    if (fw_per_sm == 0) {
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SS::SMEM));
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SS::SMEM));
+      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw_per_sm, k_e2_phi_strip_fw<NP, false, 4>,
+                                                               SS::THREADS, SS::SMEM));
+      fw_per_sm = std::max(1, fw_per_sm);
+    }
+    const long long rows = (long long)((P.nx + SS::W - 1) / SS::W) * P.ny;
+    const int g = (int)std::max<long long>(1, std::min<long long>(rows, 148LL * fw_per_sm));
+    if (roe) k_e2_phi_strip_fw<NP, true, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b);
+    else k_e2_phi_strip_fw<NP, false, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b);
+  }
   template <int CW, bool DOT>
   void launch_strip(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
                     const BArgs& b) {
@@ -1089,6 +1431,7 @@ class Euler2D : public OpDevice {
     if (const char* v = std::getenv("EXPDG_E2_CW2")) strip_cw2 = std::atoi(v) == 8 ? 8 : 4;
     if (const char* v = std::getenv("EXPDG_E2_DOTS")) use_dots = v[0] != '0';
     if (const char* v = std::getenv("EXPDG_E2_DBG")) P.dbg = std::atoi(v);
+    if (const char* v = std::getenv("EXPDG_E2_FW")) use_fw = v[0] != '0';
     set_strip_attrs<8, false>();
     set_strip_attrs<4, false>();
     if constexpr (kDotFits) set_strip_attrs<8, true>();
@@ -1103,7 +1446,8 @@ class Euler2D : public OpDevice {
     const E2P<NP> p = params(frozen);
     if (use_strip) {
       if (strip_cw == 4 || (stage == 2 && strip_cw2 == 4)) {
-        launch_strip<4, false>(s, p, st, base, partials, b);
+        if (use_fw) launch_strip_fw(s, p, st, base, partials, b);
+        else launch_strip<4, false>(s, p, st, base, partials, b);
       } else if (dots_on() && stage == 1) {
         if constexpr (kDotFits) launch_strip<8, true>(s, p, st, base, partials, b);
       } else {

@@ -1,6 +1,7 @@
 """The pipelined DCGS2 lookahead JVP (stage 2) per launch at C4 size: the plain strip kernel as
 run (half-width strips, EXPDG_E2_CW2=4), at full width (EXPDG_E2_CW2=8), and without its face
-fluxes (EXPDG_E2_DBG=4: wrong results, the time the face phase costs)."""
+fluxes (EXPDG_E2_DBG=4: wrong results, the time the face phase costs); cw4_fw is the default
+(face warps, EXPDG_E2_FW=0 turns them off)."""
 import json
 import os
 import sys
@@ -18,12 +19,13 @@ cfg = sys.argv[2] if len(sys.argv) > 2 else "C4"
 w = configs.scaled(configs.ALL[cfg], nx, steps=1)
 u0 = torch.tensor(w.initial_condition(), device="cuda:0")
 ctx = pkg.Context(0, orth="dcgs2")
-variants = {"cw4": {"EXPDG_E2_CW2": "4"}, "cw8": {"EXPDG_E2_CW2": "8"},
-            "cw4_nofaces": {"EXPDG_E2_CW2": "4", "EXPDG_E2_DBG": "4"},
+variants = {"cw4_fw": {"EXPDG_E2_CW2": "4", "EXPDG_E2_FW": "1"}, "cw4": {"EXPDG_E2_CW2": "4", "EXPDG_E2_FW": "0"},
+            "cw8": {"EXPDG_E2_CW2": "8"},
+            "cw4_nofaces": {"EXPDG_E2_CW2": "4", "EXPDG_E2_DBG": "4", "EXPDG_E2_FW": "0"},
             "cw8_nofaces": {"EXPDG_E2_CW2": "8", "EXPDG_E2_DBG": "4"}}
 res = {}
 for name, env in variants.items():
-    for k in ("EXPDG_E2_CW2", "EXPDG_E2_DBG"):
+    for k in ("EXPDG_E2_CW2", "EXPDG_E2_DBG", "EXPDG_E2_FW"):
         os.environ.pop(k, None)
     os.environ.update(env)
     op = pkg.Operator(ctx, w.spec())
@@ -31,4 +33,5 @@ for name, env in variants.items():
     res[name] = ctx.bench_apply(op, 10, 2, reps=10)
 n = w.dofs
 print(json.dumps({"n": n, **{k: round(v, 4) for k, v in res.items()},
-                  "GBps_cw4": round(32.0 * n / res["cw4"] / 1e6, 1)}))
+                  "GBps_cw4": round(32.0 * n / res["cw4"] / 1e6, 1),
+                  "GBps_cw4_fw": round(32.0 * n / res["cw4_fw"] / 1e6, 1)}))
