@@ -338,6 +338,9 @@ int expdg_ctx_dominant_stats(expdg_ctx* ctx, double* out3);
 /* Fused small-problem engine: SM clock cycles spent per phase in the last run
  * (apply, dots, updates, combine, controller; 0 for the multi-kernel engine). */
 int expdg_debug_profile(expdg_ctx* ctx, long long* out8);
+/* SM clock cycles of the controller's expm sub-phases summed over its calls: norm + scaling,
+ * Pade powers / U / V, LU elimination, back substitution, squarings; then calls, squarings taken. */
+int expdg_debug_expm_profile(expdg_ctx* ctx, long long* out8);
 int expdg_ctx_traffic(expdg_ctx* ctx, double* out4);
 
 #ifdef __cplusplus

@@ -106,7 +106,7 @@ EXPORTS = [
     "expdg_debug_state", "expdg_debug_hessenberg", "expdg_ctx_traffic", "expdg_bench_ts", "expdg_bench_apply", "expdg_op_set_source",
     "expdg_op_set_source_fn", "expdg_nccl_unique_id", "expdg_ctx_attach_nccl", "expdg_local_group_create",
     "expdg_local_group_destroy", "expdg_ctx_attach_local", "expdg_ctx_comm", "expdg_ctx_set_orthogonalization",
-    "expdg_debug_profile", "expdg_ctx_set_fused", "expdg_ctx_time_dominant", "expdg_ctx_dominant_stats",
+    "expdg_debug_profile", "expdg_debug_expm_profile", "expdg_ctx_set_fused", "expdg_ctx_time_dominant", "expdg_ctx_dominant_stats",
     "expdg_ctx_last_path", "expdg_user_op_create", "expdg_krylov_build", "expdg_initial_condition_slab",
     "expdg_ctx_set_pipelined", "expdg_peer_group_create", "expdg_peer_group_destroy", "expdg_ctx_attach_peer_local",
     "expdg_ctx_peer_export", "expdg_ctx_attach_peer",
@@ -175,6 +175,7 @@ def lib():
     L.expdg_ctx_comm.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     L.expdg_ctx_set_orthogonalization.argtypes = [vp, C.c_int]
     L.expdg_debug_profile.argtypes = [vp, C.POINTER(C.c_longlong)]
+    L.expdg_debug_expm_profile.argtypes = [vp, C.POINTER(C.c_longlong)]
     L.expdg_ctx_set_fused.argtypes = [vp, C.c_int]
     L.expdg_ctx_set_pipelined.argtypes = [vp, C.c_int]
     L.expdg_peer_group_create.argtypes = [C.c_int, C.c_longlong, C.POINTER(vp)]
@@ -359,6 +360,12 @@ class Context:
         v = (C.c_longlong * 8)()
         _check(lib().expdg_debug_profile(self.h, v))
         return dict(zip(["apply", "dots", "update", "combine", "control", "expm", "expm_calls"], list(v)[:7]))
+
+    def debug_expm_profile(self) -> dict:
+        """SM cycles of the controller's expm sub-phases, summed over its calls."""
+        v = (C.c_longlong * 8)()
+        _check(lib().expdg_debug_expm_profile(self.h, v))
+        return dict(zip(["norm_scale", "pade", "lu", "backsub", "squarings", "calls", "squarings_taken"], list(v)[:7]))
 
     def debug_hessenberg(self) -> np.ndarray:
         h = np.zeros((129, 128))

@@ -1131,6 +1131,14 @@ int expdg_debug_profile(expdg_ctx* ctx, long long* out8) {
   });
 }
 
+int expdg_debug_expm_profile(expdg_ctx* ctx, long long* out8) {
+  return guard([&] {
+    if (!ctx || !out8) throw std::invalid_argument("null argument");
+    EXPDG_CUDA(cudaMemcpy(ctx->eng->st_host, ctx->eng->st, sizeof(PhiState), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 8; ++i) out8[i] = ctx->eng->st_host->xprof[i];
+  });
+}
+
 int expdg_ctx_traffic(expdg_ctx* ctx, double* out4) {
   return guard([&] {
     Engine& e = *ctx->eng;

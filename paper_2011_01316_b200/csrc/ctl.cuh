@@ -16,95 +16,186 @@
 namespace expdg {
 
 // ------------------------------------------------------------------ block dense linear algebra
-static __device__ void blk_matmul(double* C, const double* A, const double* B, int N) {
-  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
-    const int i = idx / N, j = idx - i * N;
-    double s = 0.0;
-    for (int k = 0; k < N; ++k) s = fma(A[i * N + k], B[k * N + j], s);
-    C[idx] = s;
+// diagnostics (expdg_debug_expm_profile): SM cycles of the expm sub-phases, summed over calls:
+// 0 norm + scaling, 1 Pade powers / U / V, 2 LU elimination, 3 back substitution + un-permute,
+// 4 squarings, 5 calls, 6 squarings taken
+// (PhiState::xprof; xp may be null)
+#define EXPM_PROBE(slot, t)                                     \
+  if (threadIdx.x == 0 && xp) {                                 \
+    const long long now_ = clock64();                           \
+    xp[slot] += now_ - (t);                                     \
+    (t) = now_;                                                 \
+  }
+// C = A B out of shared memory: a 2 x 2 register tile per thread (4 loads per 4 FMAs; one
+// output per thread is 2 loads per FMA and was load-bound: 2.6k SM cycles at N = 18), four k
+// steps of loads in flight, every output summed in k order.
+// (an integer division by a run-time divisor is ~200 cycles of dependent latency here: the
+// callers pass this thread's first-round indices, formed once per expm)
+struct BlkIdx {
+  int ti, tj;   // 2 x 2 tile of idx = tid in a row of (N + 1) / 2 tiles
+  bool diag;    // idx = tid is a diagonal entry of the N x N matrix
+};
+static __device__ BlkIdx blk_idx(int N) {
+  const int H = (N + 1) / 2, t = threadIdx.x;
+  BlkIdx b;
+  b.ti = t / H;
+  b.tj = t - b.ti * H;
+  b.diag = t % (N + 1) == 0;
+  return b;
+}
+static __device__ void blk_matmul(double* C, const double* A, const double* B, int N, const BlkIdx& bx) {
+  const int T = blockDim.x, H = (N + 1) / 2, tiles = H * H;
+  for (int t = threadIdx.x; t < tiles; t += T) {
+    const int ti = t < T ? bx.ti : t / H, tj = t < T ? bx.tj : t - ti * H;
+    const int i0 = 2 * ti, j0 = 2 * tj;
+    const int i1 = i0 + 1 < N ? i0 + 1 : i0, j1 = j0 + 1 < N ? j0 + 1 : j0;
+    const double* a0 = A + i0 * N;
+    const double* a1 = A + i1 * N;
+    const double* b0 = B + j0;
+    const double* b1 = B + j1;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    int k = 0;
+    for (; k + 4 <= N; k += 4) {
+      double x0[4], x1[4], y0[4], y1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        x0[u] = a0[k + u];
+        x1[u] = a1[k + u];
+        y0[u] = b0[(k + u) * N];
+        y1[u] = b1[(k + u) * N];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c00 = fma(x0[u], y0[u], c00);
+        c01 = fma(x0[u], y1[u], c01);
+        c10 = fma(x1[u], y0[u], c10);
+        c11 = fma(x1[u], y1[u], c11);
+      }
+    }
+    for (; k < N; ++k) {
+      const double x0 = a0[k], x1 = a1[k], y0 = b0[k * N], y1 = b1[k * N];
+      c00 = fma(x0, y0, c00);
+      c01 = fma(x0, y1, c01);
+      c10 = fma(x1, y0, c10);
+      c11 = fma(x1, y1, c11);
+    }
+    C[i0 * N + j0] = c00;
+    if (j1 != j0) C[i0 * N + j1] = c01;
+    if (i1 != i0) {
+      C[i1 * N + j0] = c10;
+      if (j1 != j0) C[i1 * N + j1] = c11;
+    }
   }
   __syncthreads();
 }
 
 // out = sum c_m M_m + ident * I
-static __device__ void blk_lincomb(double* out, int N, int cnt, const double* c, const double* const* M, double ident) {
+static __device__ void blk_lincomb(double* out, int N, int cnt, const double* c, const double* const* M, double ident,
+                                   const BlkIdx& bx) {
   for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
     double s = 0.0;
     for (int m = 0; m < cnt; ++m) s += c[m] * M[m][idx];
-    if (idx / N == idx % N) s += ident;
+    if (idx < (int)blockDim.x ? bx.diag : idx % (N + 1) == 0) s += ident;
     out[idx] = s;
   }
   __syncthreads();
 }
 
-// Solves A X = B (partial pivoting, first maximal pivot) in place of B; A is destroyed.
-// Rows are pivoted through a permutation (no row swaps), the multipliers are applied to B as
-// they are formed (never stored), the pivot reciprocal is formed once per column by the
-// pivot-search warp: two CTA barriers per column, and the back substitution runs one column of
-// B per thread with reciprocal multiplies.  (The straightforward version -- swaps, a stored
-// column of multipliers, a division per element and per back-substitution row, four barriers
-// per column -- took 53k of the 74k SM cycles of a C1 expm at N = 18.)
-static __device__ void blk_lu_solve(double* A, double* B, int N) {
-  __shared__ int s_perm[kMaxBasis + 2];
-  __shared__ double s_inv[kMaxBasis + 2];
-  const int tid = threadIdx.x;
-  for (int i = tid; i < N; i += blockDim.x) s_perm[i] = i;
+// v = sum c_m M_m + ident * I;  num = U + v, den = v - U  (the Pade numerator and denominator)
+static __device__ void blk_numden(double* num, double* den, const double* U, int N, int cnt, const double* c,
+                                  const double* const* M, double ident, const BlkIdx& bx) {
+  for (int idx = threadIdx.x; idx < N * N; idx += blockDim.x) {
+    double s = 0.0;
+    for (int m = 0; m < cnt; ++m) s += c[m] * M[m][idx];
+    if (idx < (int)blockDim.x ? bx.diag : idx % (N + 1) == 0) s += ident;
+    const double u = U[idx];
+    num[idx] = u + s;
+    den[idx] = s - u;
+  }
   __syncthreads();
+}
+
+// Solves A X = B by LU with partial pivoting (first maximal pivot); A and B are destroyed, X is
+// a third N x N array.  One CTA barrier per column in each phase: every warp finds the pivot
+// of column k itself (three warp reductions on the bit pattern of |a|), rows are pivoted
+// through a double-buffered permutation (no row swaps), the multipliers are applied to B as
+// they are formed (never stored) with the pivot reciprocal; the back substitution is
+// column-oriented over all threads (x_i = b_i / u_ii, then b_r -= u_ri x_i for r < i) and
+// writes X in natural row order.  (History at N = 18, C1: swaps + stored multipliers + four
+// barriers per column 53k SM cycles; permutation + two barriers + one thread per column of B
+// in the back substitution 36k; this version: tools/c1_profile.py.)
+static __device__ void blk_lu_solve(double* __restrict__ A, double* __restrict__ B, double* __restrict__ X, int N,
+                                    long long& tp, long long* xp) {
+  __shared__ int s_perm[2][kMaxBasis + 2];
+  __shared__ double s_inv[kMaxBasis + 2];
+  const int tid = threadIdx.x, lane = tid & 31, T = blockDim.x;
+  for (int i = tid; i < N; i += T) s_perm[0][i] = i;
+  __syncthreads();
+  // (row offset, column) of idx = tid and the step to idx + T, without a division per element
+  const int q0 = tid / N, j0 = tid - q0 * N, dq = T / N, dj = T - dq * N;
   for (int k = 0; k < N; ++k) {
-    if (tid < 32) {
-      double best = -1.0;
-      int bi = k;
-      for (int i = k + tid; i < N; i += 32) {
-        const double v = fabs(A[s_perm[i] * N + k]);
-        if (v > best) { best = v; bi = i; }
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-      }
-      if (tid == 0) {
-        const int pr = s_perm[bi];
-        s_perm[bi] = s_perm[k];
-        s_perm[k] = pr;
-        s_inv[k] = 1.0 / A[pr * N + k];
-      }
+    const int* perm = s_perm[k & 1];
+    int* pnew = s_perm[(k + 1) & 1];
+    // pivot of column k among rows i >= k: max |a|, first index on ties
+    unsigned long long bits = 0ull;
+    int bi = 0x7fffffff;
+    for (int i = k + lane; i < N; i += 32) {
+      const unsigned long long v = (unsigned long long)__double_as_longlong(fabs(A[perm[i] * N + k]));
+      if (bi == 0x7fffffff || v > bits) { bits = v; bi = i; }
     }
-    __syncthreads();
-    const int rk = s_perm[k];
-    const double inv = s_inv[k];
-    const int rows = N - k - 1;
+    const bool valid = bi != 0x7fffffff;
+    const unsigned hi = valid ? (unsigned)(bits >> 32) : 0u;
+    const unsigned m1 = __reduce_max_sync(0xffffffffu, hi);
+    const bool c1 = valid && hi == m1;
+    const unsigned m2 = __reduce_max_sync(0xffffffffu, c1 ? (unsigned)bits : 0u);
+    const bool c2 = c1 && (unsigned)bits == m2;
+    bi = (int)__reduce_min_sync(0xffffffffu, c2 ? (unsigned)bi : 0x7fffffffu);
+    const int pk = perm[k], rk = perm[bi];
+    const double inv = 1.0 / A[rk * N + k];
+    if (tid == 0) s_inv[k] = inv;
+    for (int i = tid; i < N; i += T) pnew[i] = i == k ? rk : (i == bi ? pk : perm[i]);
     // rows below k: l = A[r][k] / A[rk][k]; A[r][j] -= l A[rk][j] (j > k), B[r][j] -= l B[rk][j]
-    for (int idx = tid; idx < rows * N; idx += blockDim.x) {
-      const int ii = k + 1 + idx / N, j = idx % N;
-      const int r = s_perm[ii];
+    const int cnt = (N - k - 1) * N;
+    int q = q0, j = j0;
+    for (int idx = tid; idx < cnt; idx += T) {
+      const int ii = k + 1 + q;
+      const int r = ii == bi ? pk : perm[ii];
       const double l = A[r * N + k] * inv;
       if (j > k) A[r * N + j] -= l * A[rk * N + j];
       B[r * N + j] -= l * B[rk * N + j];
+      q += dq;
+      j += dj;
+      if (j >= N) { j -= N; ++q; }
     }
     __syncthreads();
   }
-  // back substitution, column j of B per thread; X overwrites B in natural row order through the
-  // first N rows of A's storage (U is read from the permuted rows of A first)
-  for (int j = tid; j < N; j += blockDim.x) {
-    for (int i = N - 1; i >= 0; --i) {
-      const int r = s_perm[i];
-      double s = B[r * N + j];
-      for (int kk = i + 1; kk < N; ++kk) s -= A[r * N + kk] * B[s_perm[kk] * N + j];
-      B[r * N + j] = s * s_inv[i];
+  EXPM_PROBE(2, tp);
+  const int* perm = s_perm[N & 1];
+  for (int i = N - 1; i >= 0; --i) {
+    const int ri = perm[i];
+    const double inv = s_inv[i];
+    const int cnt = (i + 1) * N;
+    int q = q0, j = j0;
+    for (int idx = tid; idx < cnt; idx += T) {
+      const double x = B[ri * N + j] * inv;
+      if (q == i) {
+        X[i * N + j] = x;
+      } else {
+        const int r = perm[q];
+        B[r * N + j] -= A[r * N + i] * x;
+      }
+      q += dq;
+      j += dj;
+      if (j >= N) { j -= N; ++q; }
     }
+    __syncthreads();
   }
-  __syncthreads();
-  // un-permute X: B rows are in pivot order; move them to natural order through A
-  for (int idx = tid; idx < N * N; idx += blockDim.x) A[idx] = B[s_perm[idx / N] * N + idx % N];
-  __syncthreads();
-  for (int idx = tid; idx < N * N; idx += blockDim.x) B[idx] = A[idx];
-  __syncthreads();
+  EXPM_PROBE(3, tp);
 }
 
 // Higham (2005) scaling and squaring, the algorithm of Eigen's MatrixFunctions
 // exp() (proj/src/phi.cpp:40).  A (N x N) in W[0]; result in *out (one of W's).
-static __device__ double* blk_expm(double* W, int N) {
+static __device__ double* blk_expm(double* W, int N, long long* xp = nullptr) {
   __shared__ double s_l1;
   __shared__ int s_sq;
   __shared__ double s_buf[32];
@@ -118,6 +209,8 @@ static __device__ double* blk_expm(double* W, int N) {
   double* V = W + 6 * NN;
   double* T1 = W + 7 * NN;
   double* T2 = W + 8 * NN;
+  long long tp = clock64();
+  const BlkIdx bx = blk_idx(N);
   // 1-norm
   double colmax = 0.0;
   for (int j = threadIdx.x; j < N; j += blockDim.x) {
@@ -149,59 +242,64 @@ static __device__ double* blk_expm(double* W, int N) {
     s_sq = 0;
   }
   __syncthreads();
-  blk_matmul(A2, A, A, N);
+  EXPM_PROBE(0, tp);
+  blk_matmul(A2, A, A, N, bx);
   if (deg == 3) {
     const double b[] = {120.0, 60.0, 12.0, 1.0};
-    { const double c[] = {b[3]}; const double* M[] = {A2}; blk_lincomb(T1, N, 1, c, M, b[1]); }
-    blk_matmul(U, A, T1, N);
-    { const double c[] = {b[2]}; const double* M[] = {A2}; blk_lincomb(V, N, 1, c, M, b[0]); }
+    { const double c[] = {b[3]}; const double* M[] = {A2}; blk_lincomb(T1, N, 1, c, M, b[1], bx); }
+    blk_matmul(U, A, T1, N, bx);
+    { const double c[] = {b[2]}; const double* M[] = {A2}; blk_numden(T1, T2, U, N, 1, c, M, b[0], bx); }
   } else if (deg == 5) {
     const double b[] = {30240.0, 15120.0, 3360.0, 420.0, 30.0, 1.0};
-    blk_matmul(A4, A2, A2, N);
-    { const double c[] = {b[5], b[3]}; const double* M[] = {A4, A2}; blk_lincomb(T1, N, 2, c, M, b[1]); }
-    blk_matmul(U, A, T1, N);
-    { const double c[] = {b[4], b[2]}; const double* M[] = {A4, A2}; blk_lincomb(V, N, 2, c, M, b[0]); }
+    blk_matmul(A4, A2, A2, N, bx);
+    { const double c[] = {b[5], b[3]}; const double* M[] = {A4, A2}; blk_lincomb(T1, N, 2, c, M, b[1], bx); }
+    blk_matmul(U, A, T1, N, bx);
+    { const double c[] = {b[4], b[2]}; const double* M[] = {A4, A2}; blk_numden(T1, T2, U, N, 2, c, M, b[0], bx); }
   } else if (deg == 7) {
     const double b[] = {17297280.0, 8648640.0, 1995840.0, 277200.0, 25200.0, 1512.0, 56.0, 1.0};
-    blk_matmul(A4, A2, A2, N);
-    blk_matmul(A6, A4, A2, N);
-    { const double c[] = {b[7], b[5], b[3]}; const double* M[] = {A6, A4, A2}; blk_lincomb(T1, N, 3, c, M, b[1]); }
-    blk_matmul(U, A, T1, N);
-    { const double c[] = {b[6], b[4], b[2]}; const double* M[] = {A6, A4, A2}; blk_lincomb(V, N, 3, c, M, b[0]); }
+    blk_matmul(A4, A2, A2, N, bx);
+    blk_matmul(A6, A4, A2, N, bx);
+    { const double c[] = {b[7], b[5], b[3]}; const double* M[] = {A6, A4, A2}; blk_lincomb(T1, N, 3, c, M, b[1], bx); }
+    blk_matmul(U, A, T1, N, bx);
+    { const double c[] = {b[6], b[4], b[2]}; const double* M[] = {A6, A4, A2}; blk_numden(T1, T2, U, N, 3, c, M, b[0], bx); }
   } else if (deg == 9) {
     const double b[] = {17643225600.0, 8821612800.0, 2075673600.0, 302702400.0, 30270240.0,
                         2162160.0,     110880.0,     3960.0,       90.0,        1.0};
-    blk_matmul(A4, A2, A2, N);
-    blk_matmul(A6, A4, A2, N);
-    blk_matmul(A8, A6, A2, N);
-    { const double c[] = {b[9], b[7], b[5], b[3]}; const double* M[] = {A8, A6, A4, A2}; blk_lincomb(T1, N, 4, c, M, b[1]); }
-    blk_matmul(U, A, T1, N);
-    { const double c[] = {b[8], b[6], b[4], b[2]}; const double* M[] = {A8, A6, A4, A2}; blk_lincomb(V, N, 4, c, M, b[0]); }
+    blk_matmul(A4, A2, A2, N, bx);
+    blk_matmul(A6, A4, A2, N, bx);
+    blk_matmul(A8, A6, A2, N, bx);
+    { const double c[] = {b[9], b[7], b[5], b[3]}; const double* M[] = {A8, A6, A4, A2}; blk_lincomb(T1, N, 4, c, M, b[1], bx); }
+    blk_matmul(U, A, T1, N, bx);
+    { const double c[] = {b[8], b[6], b[4], b[2]}; const double* M[] = {A8, A6, A4, A2}; blk_numden(T1, T2, U, N, 4, c, M, b[0], bx); }
   } else {
     const double b[] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
                         1187353796428800.0,  129060195264000.0,   10559470521600.0,
                         670442572800.0,      33522128640.0,       1323241920.0,
                         40840800.0,          960960.0,            16380.0,
                         182.0,               1.0};
-    blk_matmul(A4, A2, A2, N);
-    blk_matmul(A6, A4, A2, N);
-    { const double c[] = {b[13], b[11], b[9]}; const double* M[] = {A6, A4, A2}; blk_lincomb(T1, N, 3, c, M, 0.0); }
-    blk_matmul(T2, A6, T1, N);
-    { const double c[] = {1.0, b[7], b[5], b[3]}; const double* M[] = {T2, A6, A4, A2}; blk_lincomb(T1, N, 4, c, M, b[1]); }
-    blk_matmul(U, A, T1, N);
-    { const double c[] = {b[12], b[10], b[8]}; const double* M[] = {A6, A4, A2}; blk_lincomb(T1, N, 3, c, M, 0.0); }
-    blk_matmul(T2, A6, T1, N);
-    { const double c[] = {1.0, b[6], b[4], b[2]}; const double* M[] = {T2, A6, A4, A2}; blk_lincomb(V, N, 4, c, M, b[0]); }
+    blk_matmul(A4, A2, A2, N, bx);
+    blk_matmul(A6, A4, A2, N, bx);
+    { const double c[] = {b[13], b[11], b[9]}; const double* M[] = {A6, A4, A2}; blk_lincomb(T1, N, 3, c, M, 0.0, bx); }
+    blk_matmul(T2, A6, T1, N, bx);
+    { const double c[] = {1.0, b[7], b[5], b[3]}; const double* M[] = {T2, A6, A4, A2}; blk_lincomb(T1, N, 4, c, M, b[1], bx); }
+    blk_matmul(U, A, T1, N, bx);
+    { const double c[] = {b[12], b[10], b[8]}; const double* M[] = {A6, A4, A2}; blk_lincomb(T1, N, 3, c, M, 0.0, bx); }
+    blk_matmul(V, A6, T1, N, bx);
+    { const double c[] = {1.0, b[6], b[4], b[2]}; const double* M[] = {V, A6, A4, A2}; blk_numden(T1, T2, U, N, 4, c, M, b[0], bx); }
   }
-  // numer = U + V -> T1 ; denom = V - U -> T2 ; solve denom X = numer
-  { const double c[] = {1.0, 1.0}; const double* M[] = {U, V}; blk_lincomb(T1, N, 2, c, M, 0.0); }
-  { const double c[] = {-1.0, 1.0}; const double* M[] = {U, V}; blk_lincomb(T2, N, 2, c, M, 0.0); }
-  blk_lu_solve(T2, T1, N);
-  double* cur = T1;
+  // numer = U + V -> T1, denom = V - U -> T2 (blk_numden above); solve denom X = numer into U
+  EXPM_PROBE(1, tp);
+  blk_lu_solve(T2, T1, U, N, tp, xp);
+  double* cur = U;
   double* oth = A2;
   for (int i = 0; i < s_sq; ++i) {
-    blk_matmul(oth, cur, cur, N);
+    blk_matmul(oth, cur, cur, N, bx);
     double* t = cur; cur = oth; oth = t;
+  }
+  EXPM_PROBE(4, tp);
+  if (threadIdx.x == 0 && xp) {
+    xp[5] += 1;
+    xp[6] += s_sq;
   }
   return cur;
 }
@@ -417,7 +515,7 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
       }
       __syncthreads();
       const long long te0 = clock64();
-      const double* F = blk_expm(9 * N * N <= ws_cap ? Wsm : W, N);
+      const double* F = blk_expm(9 * N * N <= ws_cap ? Wsm : W, N, st->xprof);
       if (tid == 0) {  // diagnostics (expdg_debug_profile slots 5, 6): SM cycles in the expm, calls
         st->prof[5] += clock64() - te0;
         st->prof[6] += 1;

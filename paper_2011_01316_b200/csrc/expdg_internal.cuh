@@ -156,6 +156,7 @@ struct PhiState {
   double blow_up_scale;
   double amax_step;
   long long prof[8];  // fused engine: SM clock cycles per phase (apply, dots, update, combine, ctl)
+  long long xprof[8]; // expm sub-phases (ctl.cuh, EXPM_PROBE)
   double upd_bytes;   // algorithmic bytes of the DCGS2 update passes that ran (8 n (j + 4) each)
   long long upd_launches;
   double app_bytes;   // the same for the Euler 2D strip sweep: 32 n (JVP) + 8 n j (fused dots)

@@ -27,3 +27,7 @@ print(f"C1s: {r.steps} steps, {us:.1f} us/step, {r.krylov_iterations / r.steps:.
 for k, v in prof.items():
     print(f"  {k:8s} {v / r.steps:10.0f} cycles/step  {100 * v / max(tot, 1):5.1f} %  ~{us * v / max(tot, 1):6.1f} us")
 print(f"  expm calls per step {calls / r.steps:.2f}, cycles per call {prof['expm'] / max(calls, 1):.0f}")
+xp = ctx.debug_expm_profile()
+nc = max(xp["calls"], 1)
+print("  expm sub-phases, cycles per call: " + ", ".join(f"{k} {xp[k] / nc:.0f}" for k in
+      ("norm_scale", "pade", "lu", "backsub", "squarings")) + f"; squarings per call {xp['squarings_taken'] / nc:.2f}")
