@@ -389,6 +389,17 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
                                          cudaGraphConditionalHandle cond, int use_graph) {
   __shared__ int s_phase, s_exit, s_zeroH, s_done;
   const int tid = threadIdx.x;
+  // CGS2 / IOP column j of H from the two passes' sums (proj/src/phi.cpp:96-104), one entry per
+  // thread: thread 0's serial loop over the column cost ~100 cycles per entry (every access
+  // goes through the state pointer, nothing can be hoisted)
+  if (st->action == ACT_EXTEND && !st->dcgs && !st->stopped) {
+    const int j = st->j, full = st->full_orth;
+    for (int i = st->j0 + tid; i <= j; i += blockDim.x) {
+      const double sci = st->scale[i];
+      const double h1 = sci * st->red.dotA[i];
+      st->H[i * kMaxBasis + j] = full ? h1 + sci * st->red.dotB[i] : h1;
+    }
+  }
   if (tid == 0) {
     st->body_runs++;
     s_exit = 0; s_zeroH = 0; s_done = 0;
@@ -420,13 +431,7 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
             }
             break;
           }
-          const int j = st->j;
-          const double* sc = st->scale;
-          for (int i = st->j0; i <= j; ++i) {
-            const double h1 = sc[i] * st->red.dotA[i];
-            const double h2 = st->full_orth ? sc[i] * st->red.dotB[i] : 0.0;
-            st->H[i * kMaxBasis + j] = st->full_orth ? (h1 + h2) : h1;
-          }
+          const int j = st->j;  // H(j0..j, j): filled by all threads above
           {
             const double nd = (double)st->n, kk = (double)(j - st->j0 + 1);
             st->alg_bytes += 32.0 * nd + 8.0 * nd * (st->full_orth ? 3.0 * kk + 6.0 : 2.0 * kk + 4.0);
@@ -1014,6 +1019,7 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     }
     return nacc;
   };
+  bool cl_pending = false;  // a cluster barrier arrived at, not yet waited for
   long long t0 = clock64();
   auto mark = [&](int slot) {  // CTA 0, thread 0: SM cycles of the phase just finished
     if (rank == 0 && tid == 0) {
@@ -1091,26 +1097,61 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
           if (tid == 0) st0->red.nrmA = s_tot[k];
         }
         mark(1);
-        if (s_full) {
+        if (s_full && redund) {
+          // Two cluster reductions per column instead of three: ||y'||^2 (y' = y after the first
+          // update) rides in the second dots reduction and the norm of the twice-orthogonalised
+          // vector follows from it, ||y''||^2 = ||y'||^2 - sum_i (s_i d_i)^2 with d_i = <V_i, y'>
+          // (the second-pass corrections are O(eps) ||y'||, so the identity holds to O(eps^2));
+          // the cluster barrier that orders the last update before the neighbours' next reads is
+          // split around the controller (arrive here, wait after ctl_body).
           for (int i = tid; i < k; i += T) s_c[i] = s_scale[i0 + i] * s_scale[i0 + i] * s_tot[i];
           __syncthreads();
-          local_update(i0, k, y);
+          const double n1 = block_sum(local_update(i0, k, y), s_buf);
+          if (tid == 0) s_mine[k] = n1;
           __syncthreads();
           mark(2);
           local_dots(i0, k, y);
-          reduce(k);
+          reduce(k + 1);
           mark(1);
-          if (ctl_here)
-            for (int i = tid; i < k; i += T) st0->red.dotB[i0 + i] = s_tot[i];
+          for (int i = tid; i < k; i += T) {
+            st0->red.dotB[i0 + i] = s_tot[i];
+            s_c[i] = s_scale[i0 + i] * s_scale[i0 + i] * s_tot[i];
+          }
+          if (tid == 0) {
+            double corr = 0.0;
+            for (int i = 0; i < k; ++i) {
+              const double sd = s_scale[i0 + i] * s_tot[i];
+              corr = fma(sd, sd, corr);
+            }
+            st0->red.nrmC = fmax(s_tot[k] - corr, 0.0);
+          }
+          __syncthreads();
+          local_update(i0, k, y);
+          asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+          cl_pending = true;
+          mark(2);
+        } else {
+          if (s_full) {
+            for (int i = tid; i < k; i += T) s_c[i] = s_scale[i0 + i] * s_scale[i0 + i] * s_tot[i];
+            __syncthreads();
+            local_update(i0, k, y);
+            __syncthreads();
+            mark(2);
+            local_dots(i0, k, y);
+            reduce(k);
+            mark(1);
+            if (ctl_here)
+              for (int i = tid; i < k; i += T) st0->red.dotB[i0 + i] = s_tot[i];
+          }
+          for (int i = tid; i < k; i += T) s_c[i] = s_scale[i0 + i] * s_scale[i0 + i] * s_tot[i];
+          __syncthreads();
+          const double nn = block_sum(local_update(i0, k, y), s_buf);
+          if (tid == 0) s_mine[0] = nn;
+          __syncthreads();
+          reduce(1);
+          if (ctl_here && tid == 0) st0->red.nrmC = s_tot[0];
+          mark(2);
         }
-        for (int i = tid; i < k; i += T) s_c[i] = s_scale[i0 + i] * s_scale[i0 + i] * s_tot[i];
-        __syncthreads();
-        const double nn = block_sum(local_update(i0, k, y), s_buf);
-        if (tid == 0) s_mine[0] = nn;
-        __syncthreads();
-        reduce(1);
-        if (ctl_here && tid == 0) st0->red.nrmC = s_tot[0];
-        mark(2);
       }
     } else if (act == ACT_COMBINE) {
       const int k = s_mc;
@@ -1139,6 +1180,10 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     }
     // redund: the last reduction's cluster barrier already ordered every basis write this
     // cycle before any CTA's next read of a neighbour's slice
+    if (cl_pending) {  // the column's last update is visible cluster-wide from here
+      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      cl_pending = false;
+    }
     if (!redund) {
       cl.sync();
       if (act == ACT_COMBINE && rank != 0 && tid < kTailPad)  // replicate the reset tail
