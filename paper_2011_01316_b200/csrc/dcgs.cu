@@ -30,13 +30,14 @@ constexpr int kT2Acc = (kMaxSlots + 7) / 8;
 // i = wid + 8 v <= j (i = j: U itself).  Streams of the tile: V_0..V_{j-1}, U, W consecutive.
 template <int NV, int NA>
 __device__ __forceinline__ void ts2_tile_dots(const double* V, int j, int T, int lane, int wid,
-                                              double (&acc1)[NA], double (&acc2)[NA]) {
-  const int T2 = T >> 1;
+                                              double (&acc1)[NA], double (&acc2)[NA], int len = -1) {
+  const int T2 = T >> 1;  // stream stride in the tile; len (a multiple of 64) <= T doubles are valid
+  if (len < 0) len = T;
   const double2* V2 = reinterpret_cast<const double2*>(V);
   const double2* U2 = reinterpret_cast<const double2*>(V + (size_t)j * T);
   const double2* W2 = U2 + T2;
-  for (int c0 = 0; c0 < T; c0 += kT2Chunk) {
-    const int per = min(T - c0, kT2Chunk) >> 6;
+  for (int c0 = 0; c0 < len; c0 += kT2Chunk) {
+    const int per = min(len - c0, kT2Chunk) >> 6;
     double2 yu[kT2Chunk / 64], yw[kT2Chunk / 64];
 #pragma unroll
     for (int m = 0; m < kT2Chunk / 64; ++m) {
@@ -68,12 +69,14 @@ __device__ __forceinline__ void ts2_tile_dots(const double* V, int j, int T, int
 
 // A non-zero rank's tile holding the replicated phi tail: U, W (streams j, j+1) beyond ndot
 // are kept out of the dots.  Consumer-wide.
-__device__ __forceinline__ void ts2_mask_tail(double* V, int j, int T, long long g0, long long ndot, int tid) {
-  if (g0 + T <= ndot) return;
+__device__ __forceinline__ void ts2_mask_tail(double* V, int j, int T, long long g0, long long ndot, int tid,
+                                              int len = -1) {
+  if (len < 0) len = T;
+  if (g0 + len <= ndot) return;
   double* U = V + (size_t)j * T;
   double* W = U + T;
   consumer_sync();
-  for (int d = tid; d < T; d += kT2Consumers)
+  for (int d = tid; d < len; d += kT2Consumers)
     if (g0 + d >= ndot) {
       U[d] = 0.0;
       W[d] = 0.0;
@@ -397,7 +400,9 @@ __device__ __forceinline__ void ts3_consume(double* base, double* smem, uint64_t
     double2* Y2 = W2 + T2;
     const double2* V2 = reinterpret_cast<const double2*>(V);
     const long long g0 = tl * T;
-    for (int p = tid; p < T2; p += kT2Consumers) {
+    const int len = (int)min((long long)T, ld - g0);  // the last tile may be short (T need not divide ld)
+    const int L2 = len >> 1;
+    for (int p = tid; p < L2; p += kT2Consumers) {
       const double2 u = U2[p], w = W2[p], y = Y2[p];
       double ux = u.x, uy = u.y;
       double wx = fma(-gam, u.x, wsc * w.x), wy = fma(-gam, u.y, wsc * w.y);
@@ -425,8 +430,8 @@ __device__ __forceinline__ void ts3_consume(double* base, double* smem, uint64_t
       if (g0 + 2 * p + 1 < ndot) nu = fma(un.y, un.y, nu);
     }
     consumer_sync();  // the tile now holds [V_0..V_{j-1}, unew, wnew, znew]
-    ts2_mask_tail(V, j + 1, T, g0, ndot, tid);
-    ts2_tile_dots<NV>(V, j + 1, T, lane, wid, acc1, acc2);
+    ts2_mask_tail(V, j + 1, T, g0, ndot, tid, len);
+    ts2_tile_dots<NV>(V, j + 1, T, lane, wid, acc1, acc2, len);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (++s == S) {
@@ -457,16 +462,22 @@ __global__ void __launch_bounds__(kT2Block, 1) k_ts3(PhiState* st, double* base,
         !st->stopped && st->dcgs && st->pl_look && (st->action == ACT_EXTEND || st->action == ACT_AVNORM);
     const int j = active ? st->j : 0;
     const int nst = j + 3;
-    int T = kT2MaxT;
     const int tile_stages = st->ts3_tstages > 0 ? st->ts3_tstages : max_stages;  // stages the tile choice assumes
-    while (T > min_T && tile_stages * nst * T * 8 > budget) T >>= 1;
+    // the largest tile (a multiple of 64 doubles, not only a power of two: halving at
+    // j = 25 cost C4's large columns ~13 % of their bandwidth) two stages of which fit
+    int T = min(kT2MaxT, budget / (tile_stages * nst * 8) / 64 * 64);
+    if (st->ts3_pow2) {  // diagnostics: the power-of-two choice
+      T = kT2MaxT;
+      while (T > min_T && tile_stages * nst * T * 8 > budget) T >>= 1;
+    }
+    T = max(T, min(min_T, 64));
     int S = budget / (nst * T * 8);
     while (S < 2 && T > 64) {
-      T >>= 1;
+      T = max(64, (T >> 1) / 64 * 64);
       S = budget / (nst * T * 8);
     }
-    // T is the largest tile two stages of which fit; the stages then fill the budget (up to
-    // st->ts3_stages), so small columns keep more bytes in flight
+    // the stages then fill the budget (up to st->ts3_stages), so small columns keep more
+    // bytes in flight
     const int cap = st->ts3_stages > 0 ? st->ts3_stages : max_stages;
     S = S > cap ? cap : (S > 8 ? 8 : S);
     s_active = active;
@@ -497,8 +508,7 @@ __global__ void __launch_bounds__(kT2Block, 1) k_ts3(PhiState* st, double* base,
     s_ka[i] = st->pl_kappa[i];
   }
   __syncthreads();
-  const long long ntiles = ld / T;
-  const uint32_t tile_bytes = (uint32_t)T * 8u;
+  const long long ntiles = (ld + T - 1) / T;
   double acc1[kT2Acc], acc2[kT2Acc];
 #pragma unroll
   for (int v = 0; v < kT2Acc; ++v) acc1[v] = acc2[v] = 0.0;
@@ -509,6 +519,7 @@ __global__ void __launch_bounds__(kT2Block, 1) k_ts3(PhiState* st, double* base,
       for (long long tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
         mbar_wait(&empty[s], (use & 1) ^ 1);
         double* dst = smem + (size_t)s * nst * T;
+        const uint32_t tile_bytes = (uint32_t)min((long long)T, ld - tl * T) * 8u;
         mbar_arrive_expect_tx(&full[s], tile_bytes * (uint32_t)nst);
         for (int q = 0; q < nst; ++q) bulk_g2s(dst + (size_t)q * T, base + (size_t)q * ld + tl * T, tile_bytes, &full[s]);
         if (++s == S) {

@@ -69,6 +69,7 @@ struct PhiState {
   int pipe_restart;  // diagnostics: apply the operator directly to every pipe_restart-th candidate
   int ts3_stages;    // merged pass: stage cap after the tile choice (0: the tile rule's cap)
   int ts3_tstages;   // merged pass: stages the tile choice assumes (0: the tall-skinny rule's)
+  int ts3_pow2;      // merged pass: power-of-two tiles only (EXPDG_TS3_POW2=1, diagnostics)
   double* base;      // slot 0 of the Krylov workspace (stage-1 operator applications)
   // ---- dynamic control (action, phase, j, pl_direct, pl_look: read back together by
   // host-stepped loops, Engine::fetch_control)

@@ -408,6 +408,7 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_PIPE_RESTART")) pipe_restart = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_TS3_STAGES")) ts3_stages = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_TS3_TSTAGES")) ts3_tstages = std::atoi(v);
+  if (const char* v = std::getenv("EXPDG_TS3_POW2")) ts3_pow2 = std::atoi(v);
   if (const char* v = std::getenv("EXPDG_ORTH"))
     use_dcgs = std::strcmp(v, "cgs2") == 0 ? 0 : (std::strcmp(v, "dcgs2") == 0 ? 2 : 1);
   dcgs_init_attrs(maxsm);
@@ -492,6 +493,7 @@ PhiState Engine::config(long long n, int p, double dt, const expdg_krylov_cfg& k
   c.pipe_restart = pipe_restart;
   c.ts3_stages = ts3_stages;
   c.ts3_tstages = ts3_tstages;
+  c.ts3_pow2 = ts3_pow2;
   c.pl_direct = 1;
   c.pl_look = 0;
   c.pl_ready = -1;

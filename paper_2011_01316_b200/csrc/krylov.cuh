@@ -120,6 +120,7 @@ class Engine {
   // (C4 same box: 3.78 vs 3.89 ms per k_ts3 launch, 198.8 vs 201.1 ms per step)
   int ts3_stages = 4;
   int ts3_tstages = 0;  // stages the merged pass's tile choice assumes (EXPDG_TS3_TSTAGES; 0: 2)
+  int ts3_pow2 = 0;     // power-of-two merged-pass tiles only (EXPDG_TS3_POW2=1: the round-2 rule, for A/B runs)
   // host-stepped runs: CUDA events around every DCGS2 update pass (time_kind 1) or every
   // phi-cycle operator application (2), so bench.py can report the live per-launch
   // bandwidth of the dominant kernel

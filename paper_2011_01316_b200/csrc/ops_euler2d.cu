@@ -1310,6 +1310,7 @@ class Euler2D : public OpDevice {
   int strip_cw2 = 4;
   // the plain half-width strip with face warps (EXPDG_E2_FW=0: the single-role strip)
   bool use_fw = true;
+  bool fw_align = false;  // EXPDG_E2_ALIGN=1: whole CTAs per strip (see launch_strip_fw)
   int fw_per_sm = 0;
   void launch_strip_fw(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
                        const BArgs& b) {
@@ -1323,8 +1324,16 @@ class Euler2D : public OpDevice {
                                                                SS::THREADS, SS::SMEM));
       fw_per_sm = std::max(1, fw_per_sm);
     }
-    const long long rows = (long long)((P.nx + SS::W - 1) / SS::W) * P.ny;
-    const int g = (int)std::max<long long>(1, std::min<long long>(rows, 148LL * fw_per_sm));
+    const long long nstrips = (P.nx + SS::W - 1) / SS::W;
+    const long long rows = nstrips * P.ny;
+    int g = (int)std::max<long long>(1, std::min<long long>(rows, 148LL * fw_per_sm));
+    // EXPDG_E2_ALIGN=1 (diagnostics): whole CTAs per strip, every strip cut at the same rows, so
+    // the CTAs of neighbouring strips march the same rows at the same time and the E/W halo
+    // elements (2 of every W + 2 staged: 40 % more x / q~ reads at W = 5 when they miss) come
+    // from L2.  Measured slower at C4 (410 instead of 444 CTAs: 0.918 vs 0.860 ms per launch):
+    // the kernel is latency-bound, not DRAM-bound, and the lost CTAs cost more than the misses.
+    const long long q = g / nstrips;
+    if (fw_align && q >= 1 && P.ny % q == 0 && nstrips * q * 10 >= (long long)g * 8) g = (int)(nstrips * q);
     if (roe) k_e2_phi_strip_fw<NP, true, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b);
     else k_e2_phi_strip_fw<NP, false, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b);
   }
@@ -1432,6 +1441,7 @@ class Euler2D : public OpDevice {
     if (const char* v = std::getenv("EXPDG_E2_DOTS")) use_dots = v[0] != '0';
     if (const char* v = std::getenv("EXPDG_E2_DBG")) P.dbg = std::atoi(v);
     if (const char* v = std::getenv("EXPDG_E2_FW")) use_fw = v[0] != '0';
+    if (const char* v = std::getenv("EXPDG_E2_ALIGN")) fw_align = v[0] == '1';
     set_strip_attrs<8, false>();
     set_strip_attrs<4, false>();
     if constexpr (kDotFits) set_strip_attrs<8, true>();

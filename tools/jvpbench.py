@@ -19,13 +19,14 @@ cfg = sys.argv[2] if len(sys.argv) > 2 else "C4"
 w = configs.scaled(configs.ALL[cfg], nx, steps=1)
 u0 = torch.tensor(w.initial_condition(), device="cuda:0")
 ctx = pkg.Context(0, orth="dcgs2")
-variants = {"cw4_fw": {"EXPDG_E2_CW2": "4", "EXPDG_E2_FW": "1"}, "cw4": {"EXPDG_E2_CW2": "4", "EXPDG_E2_FW": "0"},
+variants = {"cw4_fw": {"EXPDG_E2_CW2": "4", "EXPDG_E2_FW": "1"},
+            "cw4_fw_align": {"EXPDG_E2_CW2": "4", "EXPDG_E2_FW": "1", "EXPDG_E2_ALIGN": "1"}, "cw4": {"EXPDG_E2_CW2": "4", "EXPDG_E2_FW": "0"},
             "cw8": {"EXPDG_E2_CW2": "8"},
             "cw4_nofaces": {"EXPDG_E2_CW2": "4", "EXPDG_E2_DBG": "4", "EXPDG_E2_FW": "0"},
             "cw8_nofaces": {"EXPDG_E2_CW2": "8", "EXPDG_E2_DBG": "4"}}
 res = {}
 for name, env in variants.items():
-    for k in ("EXPDG_E2_CW2", "EXPDG_E2_DBG", "EXPDG_E2_FW"):
+    for k in ("EXPDG_E2_CW2", "EXPDG_E2_DBG", "EXPDG_E2_FW", "EXPDG_E2_ALIGN"):
         os.environ.pop(k, None)
     os.environ.update(env)
     op = pkg.Operator(ctx, w.spec())
