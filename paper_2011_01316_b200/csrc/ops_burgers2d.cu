@@ -170,12 +170,19 @@ __global__ void __launch_bounds__(256) k_b2_phi(B1P<NP> Px, B1P<NP> Py, int nx, 
 // warp streams the row tiles of V_0..V_{j-1} into a ring and two dot warps consume them
 // (dots.cuh).  Needs full-width strips whose rows are 16-byte aligned (nx % W == 0).
 constexpr int kB2DotJ = 44;
+#ifndef EXPDG_B2_SPLIT
+#define EXPDG_B2_SPLIT 1
+#endif
 
 template <int NP, bool DOT = false>
 struct B2Strip {
   static constexpr int NN = NP * NP;
   static constexpr int W = NP <= 7 ? 32 : 16;        // elements per strip
-  static constexpr int CONS = (W * NP + 31) / 32 * 32;  // consumer threads: one per element line
+  static constexpr int LN = (W * NP + 31) / 32 * 32;  // threads of one line set (one per element line)
+  // the plain strip runs the x-lines and the y-lines of a row on separate warps at the same time
+  // (two line sets); with the dots, one set does both in turn (the dot warps take the threads)
+  static constexpr bool SPLIT = !DOT && EXPDG_B2_SPLIT;
+  static constexpr int CONS = (SPLIT ? 2 : 1) * LN;  // consumer threads
   static constexpr int CW = CONS / 32;       // consumer warps
   static constexpr int ROWD = (W + 2) * NN;  // doubles per array per ring row (with halo)
   // DOT: the x row starts one double into its slot when NN is odd, so that its interior
@@ -374,7 +381,9 @@ __global__ void __launch_bounds__(B2Strip<NP, DOT>::THREADS)
     }
   } else {
     // ---------------- consumers: thread (element le, line l)
-    const int le = tid / NP, l = tid % NP;
+    const int half = S::SPLIT ? tid / S::LN : 0, lt = S::SPLIT ? tid - half * S::LN : tid;
+    const int le = lt / NP, l = lt % NP;
+    const bool do_x = !S::SPLIT || half == 0, do_y = !S::SPLIT || half == 1;
     long long seq = 0;
     int rowc = 0;
     for (long long k = k0; k < k1;) {
@@ -395,32 +404,36 @@ __global__ void __launch_bounds__(B2Strip<NP, DOT>::THREADS)
         double* sY = sX + S::OUT;
         if (active) {
           double xL[NP], xC[NP], xR[NP], uL[NP], uC[NP], uR[NP], out[NP];
-          // x-line l (element row l): ring elements le, le + 1, le + 2 of row r
+          if (do_x) {
+            // x-line l (element row l): ring elements le, le + 1, le + 2 of row r
 #pragma unroll
-          for (int t = 0; t < NP; ++t) {
-            xL[t] = cur[le * NN + l * NP + t] * xs;
-            xC[t] = cur[(le + 1) * NN + l * NP + t] * xs;
-            xR[t] = cur[(le + 2) * NN + l * NP + t] * xs;
-            uL[t] = cur[S::ROWD + le * NN + l * NP + t];
-            uC[t] = cur[S::ROWD + (le + 1) * NN + l * NP + t];
-            uR[t] = cur[S::ROWD + (le + 2) * NN + l * NP + t];
+            for (int t = 0; t < NP; ++t) {
+              xL[t] = cur[le * NN + l * NP + t] * xs;
+              xC[t] = cur[(le + 1) * NN + l * NP + t] * xs;
+              xR[t] = cur[(le + 2) * NN + l * NP + t] * xs;
+              uL[t] = cur[S::ROWD + le * NN + l * NP + t];
+              uC[t] = cur[S::ROWD + (le + 1) * NN + l * NP + t];
+              uR[t] = cur[S::ROWD + (le + 2) * NN + l * NP + t];
+            }
+            b1_element<NP>(Px, 0, ie0 + le, xL, xC, xR, uL, uC, uR, out);
+#pragma unroll
+            for (int t = 0; t < NP; ++t) sX[le * NN + l * NP + t] = out[t];
           }
-          b1_element<NP>(Px, 0, ie0 + le, xL, xC, xR, uL, uC, uR, out);
+          if (do_y) {
+            // y-line l (element column l): element le + 1 of ring rows r - 1, r, r + 1
 #pragma unroll
-          for (int t = 0; t < NP; ++t) sX[le * NN + l * NP + t] = out[t];
-          // y-line l (element column l): element le + 1 of ring rows r - 1, r, r + 1
+            for (int t = 0; t < NP; ++t) {
+              xL[t] = lo[(le + 1) * NN + t * NP + l] * xs;
+              xC[t] = cur[(le + 1) * NN + t * NP + l] * xs;
+              xR[t] = hi[(le + 1) * NN + t * NP + l] * xs;
+              uL[t] = lo[S::ROWD + (le + 1) * NN + t * NP + l];
+              uC[t] = cur[S::ROWD + (le + 1) * NN + t * NP + l];
+              uR[t] = hi[S::ROWD + (le + 1) * NN + t * NP + l];
+            }
+            b1_element<NP>(Py, 0, (int)Py.eoff + r, xL, xC, xR, uL, uC, uR, out);
 #pragma unroll
-          for (int t = 0; t < NP; ++t) {
-            xL[t] = lo[(le + 1) * NN + t * NP + l] * xs;
-            xC[t] = cur[(le + 1) * NN + t * NP + l] * xs;
-            xR[t] = hi[(le + 1) * NN + t * NP + l] * xs;
-            uL[t] = lo[S::ROWD + (le + 1) * NN + t * NP + l];
-            uC[t] = cur[S::ROWD + (le + 1) * NN + t * NP + l];
-            uR[t] = hi[S::ROWD + (le + 1) * NN + t * NP + l];
+            for (int t = 0; t < NP; ++t) sY[le * NN + t * NP + l] = out[t];
           }
-          b1_element<NP>(Py, 0, (int)Py.eoff + r, xL, xC, xR, uL, uC, uR, out);
-#pragma unroll
-          for (int t = 0; t < NP; ++t) sY[le * NN + t * NP + l] = out[t];
         }
         strip_sync<S::CONS>();  // sX, sY of row r complete; row r-1 is no longer read
         if (tid == 0) mbar_arrive_cnt(&empty[(seq + q - 1) % NBUF], q == 1 ? rel_halo : rel_row);  // row r-1 free

@@ -965,17 +965,28 @@ __global__ void __launch_bounds__(E2Strip<NP, CW, DOT>::THREADS, CW <= 4 ? 3 : 1
 #ifndef EXPDG_E2_FWARPS
 #define EXPDG_E2_FWARPS 1
 #endif
+#ifndef EXPDG_E2_FW_NBUF
+#define EXPDG_E2_FW_NBUF 4
+#endif
+#ifndef EXPDG_E2_FW_PER_SM
+#define EXPDG_E2_FW_PER_SM 3
+#endif
 template <int NP, int CW>
 struct E2StripFW {
   using B = E2Strip<NP, CW, false>;
   static constexpr int NN = B::NN, CONS = B::CONS, W = B::W, BLK = B::BLK, ROWD = B::ROWD, BUFD = B::BUFD;
-  static constexpr int NBUF = 4, FX = B::FX, FY = B::FY;
+  static constexpr int NBUF = EXPDG_E2_FW_NBUF, FX = B::FX, FY = B::FY;
   static constexpr int FWARPS = EXPDG_E2_FWARPS, FTH = 32 * FWARPS;
   static constexpr int THREADS = CONS + 32 + FTH;
   static constexpr int SF = 2 * W * BLK;  // volume fluxes of a row, two buffers
   static constexpr int NYL = 4;           // y-face rows in flight
   static constexpr int SMEM = (NBUF * BUFD + 2 * SF + 2 * FX + NYL * FY) * 8;
-  static constexpr int PER_SM = CW <= 4 ? 3 : 1;
+  static constexpr int PER_SM = CW <= 4 ? EXPDG_E2_FW_PER_SM : 1;
+  // rows r (node warps), r + 1, r + 2 (face warps, up to two rows ahead) and one row in flight;
+  // measured at C4 (-DEXPDG_E2_FW_NBUF / _PER_SM): 5, 6 or 8 rows at two CTAs per SM 0.904 /
+  // 0.904 / 0.895 ms per launch against 0.860 ms for 4 rows at three CTAs per SM -- the kernel
+  // follows the resident warps, not the bytes in flight; 3 rows deadlock
+  static_assert(NBUF >= 4, "the face warps run up to two rows ahead of the node warps");
 };
 
 template <int NP, bool ROE, int CW>
