@@ -521,6 +521,7 @@ int expdg_phi_combination(expdg_ctx* ctx, expdg_op* op, const double* const* b_d
     map_phi_status(s);
     EXPDG_CUDA(cudaMemcpyAsync(out_dev, e.slot(0), sizeof(double) * n, cudaMemcpyDeviceToDevice, e.stream));
     EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+    if (e.comm) e.comm->check();
   });
 }
 
@@ -990,6 +991,7 @@ static void integrate_impl(expdg_ctx* ctx, expdg_op* op, double* u, const expdg_
   steps_done:
     EXPDG_CUDA(cudaEventRecord(ctx->ev1, e.stream));
     EXPDG_CUDA(cudaStreamSynchronize(e.stream));
+    if (e.comm) e.comm->check();
     float ms = 0.f;
     EXPDG_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
     ctx->last_loop_ms = ms;

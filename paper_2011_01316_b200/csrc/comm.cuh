@@ -39,6 +39,9 @@ class Comm {
   // runtime call (cudaFree, pinned allocation) while another rank's collective kernel spins on
   // it.  No-op for one process per GPU.
   virtual void host_barrier() {}
+  // After the stream has been synchronised: throws CommError if a device-side collective gave
+  // up waiting for a peer (bounded waits, comm_peer.cu).  No-op for the other communicators.
+  virtual void check() {}
 };
 
 struct LocalGroup;

@@ -19,6 +19,7 @@
 // (expdg_ctx_peer_export / expdg_ctx_attach_peer); ranks driven by threads of one process share
 // a group allocated on the device (expdg_peer_group_create / expdg_ctx_attach_peer_local).
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -43,6 +44,7 @@ struct PeerLayout {
   static constexpr long long kHaloFlag = kPeerMax;           // [2]
   static constexpr long long kRedEpoch = kPeerMax + 2;
   static constexpr long long kHaloEpoch = kPeerMax + 3;
+  static constexpr long long kErr = kPeerMax + 4;            // sticky: a wait for a peer timed out
   static constexpr long long kRedIn = 32;                    // [2][kPeerMax][kPeerRed]
   static constexpr long long kHaloIn = kRedIn + 2LL * kPeerMax * kPeerRed;  // [2][2][halo_cap]
   long long words() const { return kHaloIn + 4 * halo_cap; }
@@ -53,6 +55,7 @@ struct PeerView {
   unsigned long long* peer[kPeerMax];
   int rank, size;
   long long halo_cap;
+  unsigned long long wait_ns;  // bound of every wait for a peer (EXPDG_PEER_TIMEOUT_MS, default 20 s)
 };
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
@@ -62,6 +65,27 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   unsigned long long v;
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Bounded wait for a peer's flag to reach epoch e.  A peer that never arrives (a rank that died,
+// or ranks sharing one device whose kernels the hardware does not run at the same time) must
+// not hang the GPU: after v.wait_ns the wait gives up, records the epoch in the sticky error
+// word (the host turns it into a CommError, PeerComm::check) and every later wait returns at once.
+__device__ __forceinline__ void peer_wait(const PeerView& v, const unsigned long long* flag, unsigned long long e) {
+  if (ld_acquire_sys(flag) >= e) return;
+  if (ld_acquire_sys(v.mine + PeerLayout::kErr) != 0) return;
+  const unsigned long long t0 = global_ns();
+  while (ld_acquire_sys(flag) < e) {
+    if (global_ns() - t0 > v.wait_ns) {
+      st_release_sys(v.mine + PeerLayout::kErr, e);
+      return;
+    }
+  }
 }
 
 // count <= kPeerRed elements of 8 (F64) or 4 (I32) bytes; send / recv may alias
@@ -85,9 +109,7 @@ __global__ void __launch_bounds__(256) k_peer_allreduce(PeerView v, const void* 
     __threadfence_system();
     for (int r = 0; r < v.size; ++r) st_release_sys(v.peer[r] + PeerLayout::kRedFlag + v.rank, e);
   }
-  if (tid < v.size)
-    while (ld_acquire_sys(v.mine + PeerLayout::kRedFlag + tid) < e) {
-    }
+  if (tid < v.size) peer_wait(v, v.mine + PeerLayout::kRedFlag + tid, e);
   __syncthreads();
   for (int i = tid; i < count; i += blockDim.x) {
     const unsigned long long* in = v.mine + PeerLayout::kRedIn + par * kPeerMax * kPeerRed + i;
@@ -130,10 +152,8 @@ __global__ void k_peer_halo_flag(PeerView v) {
   __threadfence_system();
   st_release_sys(v.peer[lo] + PeerLayout::kHaloFlag + 1, e);  // lands in its hi inbox
   st_release_sys(v.peer[hi] + PeerLayout::kHaloFlag + 0, e);  // lands in its lo inbox
-  while (ld_acquire_sys(v.mine + PeerLayout::kHaloFlag + 0) < e) {
-  }
-  while (ld_acquire_sys(v.mine + PeerLayout::kHaloFlag + 1) < e) {
-  }
+  peer_wait(v, v.mine + PeerLayout::kHaloFlag + 0, e);
+  peer_wait(v, v.mine + PeerLayout::kHaloFlag + 1, e);
 }
 // halo, 3/3: the inboxes of this epoch into the operator's receive buffers
 __global__ void k_peer_halo_recv(PeerView v, double* recv_lo, double* recv_hi, long long count) {
@@ -175,6 +195,9 @@ class PeerComm : public Comm {
   PeerComm(const PeerView& view, std::shared_ptr<void> k, HostBarrier* b) : v(view), keep(std::move(k)), hb(b) {
     rank = v.rank;
     size = v.size;
+    long long ms = 20000;
+    if (const char* e = std::getenv("EXPDG_PEER_TIMEOUT_MS")) ms = std::max(1LL, std::atoll(e));
+    v.wait_ns = (unsigned long long)ms * 1000000ull;
   }
   bool graph_capturable() const override { return true; }
   void host_barrier() override {
@@ -197,6 +220,16 @@ class PeerComm : public Comm {
     EXPDG_CUDA(cudaGetLastError());
   }
   const char* kind() const override { return "peer"; }
+  void check() override {
+    unsigned long long err = 0;
+    EXPDG_CUDA(cudaMemcpy(&err, v.mine + PeerLayout::kErr, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err == 0) return;
+    EXPDG_CUDA(cudaMemset(v.mine + PeerLayout::kErr, 0, sizeof(err)));
+    throw CommError("peer communicator: rank " + std::to_string(rank) + " waited " +
+                    std::to_string(v.wait_ns / 1000000ull) + " ms for a peer at epoch " +
+                    std::to_string(err) + " (a rank that stopped, or ranks sharing one device that did not run "
+                    "concurrently); the results of this call are invalid");
+  }
 };
 
 }  // namespace

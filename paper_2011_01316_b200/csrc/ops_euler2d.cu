@@ -1322,19 +1322,10 @@ class Euler2D : public OpDevice {
   // the plain half-width strip with face warps (EXPDG_E2_FW=0: the single-role strip)
   bool use_fw = true;
   bool fw_align = false;  // EXPDG_E2_ALIGN=1: whole CTAs per strip (see launch_strip_fw)
-  int fw_per_sm = 0;
+  int fw_per_sm = 1;
   void launch_strip_fw(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
                        const BArgs& b) {
     using SS = E2StripFW<NP, 4>;
-    if (fw_per_sm == 0) {
-      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      SS::SMEM));
-      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      SS::SMEM));
-      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw_per_sm, k_e2_phi_strip_fw<NP, false, 4>,
-                                                               SS::THREADS, SS::SMEM));
-      fw_per_sm = std::max(1, fw_per_sm);
-    }
     const long long nstrips = (P.nx + SS::W - 1) / SS::W;
     const long long rows = nstrips * P.ny;
     int g = (int)std::max<long long>(1, std::min<long long>(rows, 148LL * fw_per_sm));
@@ -1455,6 +1446,17 @@ class Euler2D : public OpDevice {
     if (const char* v = std::getenv("EXPDG_E2_ALIGN")) fw_align = v[0] == '1';
     set_strip_attrs<8, false>();
     set_strip_attrs<4, false>();
+    {  // the face-warp strip: attributes and occupancy here, never on the launch path (a runtime
+       // call that synchronises the device must not run while another rank's collective spins)
+      using SF = E2StripFW<NP, 4>;
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SF::SMEM));
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SF::SMEM));
+      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw_per_sm, k_e2_phi_strip_fw<NP, false, 4>,
+                                                               SF::THREADS, SF::SMEM));
+      fw_per_sm = std::max(1, fw_per_sm);
+    }
     if constexpr (kDotFits) set_strip_attrs<8, true>();
     const long long ntiles = ((long long)d.nx * nyl + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
     grid = (int)std::max<long long>(1, std::min<long long>(ntiles, 148LL * 8));

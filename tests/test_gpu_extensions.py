@@ -229,6 +229,67 @@ def test_c5_extruded_vortex_converges_at_design_order(ctx):
     assert order_obs >= order + 0.5, (errs, order_obs)
 
 
+def _plane_vortex_errors(ctx, plane, sizes, order=3, t_end=0.5, dt=0.05):
+    """Density L2 errors of the exact vortex laid in the given coordinate plane (the third axis one
+    element wide, the solution constant along it) after EPI2 to t_end, one per mesh size."""
+    np1 = order + 1
+    x_lgl, w_lgl, _ = pkg.lgl_basis(order)
+    ax = {"x": 2, "y": 1, "z": 0}  # element axis of [kz][jy][ix], node axis = 4 + the same
+    errs = []
+    for n in sizes:
+        h = 10.0 / n
+        a = (np.arange(n)[:, None] + 0.5 * (x_lgl[None, :] + 1)) * h        # first in-plane coordinate [e][node]
+        b = -5 + (np.arange(n)[:, None] + 0.5 * (x_lgl[None, :] + 1)) * h   # second
+        dims = {c: (n if c in plane else 1) for c in "xyz"}
+        box = []
+        for c in "xyz":
+            box += ([0, 10] if c == plane[0] else [-5, 5]) if c in plane else [0, 1]
+        spec = pkg.OperatorSpec("euler3d", order, dims["x"], dims["y"], dims["z"], box=tuple(box), euler_flux="lf")
+        shape = (dims["z"], dims["y"], dims["x"], 5, np1, np1, np1)  # [kz][jy][ix][c][k][j][i]
+        full = shape[:3] + shape[4:]
+
+        def coord(vals, c):
+            idx = [None] * 6
+            idx[ax[c]] = slice(None)
+            idx[3 + ax[c]] = slice(None)
+            return np.broadcast_to(vals[tuple(idx)], full)
+
+        A, B = coord(a, plane[0]), coord(b, plane[1])
+        op = pkg.Operator(ctx, spec)
+
+        def state(t):
+            rho, u1, u2, p = _vortex(A, B, t)
+            q = np.zeros(shape)
+            mom = {c: 0 * rho for c in "xyz"}
+            mom[plane[0]], mom[plane[1]] = rho * u1, rho * u2
+            comps = [rho, mom["x"], mom["y"], mom["z"], p / 0.4 + 0.5 * rho * (u1 * u1 + u2 * u2)]
+            for c in range(5):
+                q[:, :, :, c] = comps[c]
+            return q.reshape(-1)
+
+        r = pkg.integrate(ctx, op, to_dev(state(0.0)), "epi2", dt, t_end, tol=1e-12, max_basis=40, orth_length=40)
+        assert r.status == "completed"
+        d = (to_host(r.u) - state(t_end)).reshape(shape)[:, :, :, 0]
+        wq = (w_lgl[:, None, None] * w_lgl[None, :, None] * w_lgl[None, None, :]) * (h * h * 1.0) / 8.0
+        errs.append(math.sqrt(float(np.sum(d * d * wq[None, None, None]))))
+    return errs
+
+
+@pytest.mark.parametrize("plane", ["xz", "yz"])
+def test_c5_vortex_in_a_z_plane_converges_like_the_xy_plane(ctx, plane):
+    # The exact vortex laid in the x-z (y-z) plane, so the z-derivatives, the z-faces and the
+    # w-momentum carry the solution and the z direction is refined: the design-order check of the
+    # test above (k = 3, meshes 4 and 8 as the reference's criterion 8 takes h and h / 2; observed
+    # 4.8 here) must hold there too, and the errors must equal those of the x-y plane (the 3D
+    # operator treats the three directions alike; measured equal to every printed digit).
+    ref = _plane_vortex_errors(ctx, "xy", (4, 8))
+    errs = _plane_vortex_errors(ctx, plane, (4, 8))
+    order_obs = math.log(errs[0] / errs[1]) / math.log(2.0)
+    assert order_obs >= 3.5, (errs, order_obs)
+    for e, r in zip(errs, ref):
+        assert abs(e - r) <= 1e-9 * r, (errs, ref)
+
+
 # ------------------------------------------------------------------ strip / z-march phi kernels
 def _two_kernels(monkeypatch, env, spec, u0, dt, steps=2, max_basis=30):
     """EPI2 through the phi-cycle JVP kernel selected by env=0 (strip / z-march) and env=1

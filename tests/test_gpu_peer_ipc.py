@@ -10,7 +10,12 @@ import sys
 import numpy as np
 import pytest
 
-pytestmark = pytest.mark.gpu
+# opt-in: two contexts time-slicing one GPU while their kernels wait on each other is exactly
+# what B200_PROFILING.md warns about (Xid 109 context-switch timeouts); see test_gpu_multirank.py
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(os.environ.get("EXPDG_SHARED_GPU_TESTS") != "1",
+                                 reason="two processes sharing one GPU with device-side waits: "
+                                        "set EXPDG_SHARED_GPU_TESTS=1")]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
