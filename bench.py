@@ -381,19 +381,20 @@ def main():
         # q~, b_1, writes Y = 32 n bytes; the first column of a substep also runs stage 1 with the
         # fused pass-1 dots) and one merged basis pass k_ts3 (8 n (j + 6) bytes)
         sweep = {
-            "euler2d": ("k_e2_phi_strip<5,LF,8,*> (Euler strip JVP: the lookahead application dt A (s_j W) "
-                        "-> Y, reads W, q~, b_1, writes Y; + the pass-1 dots at substep starts)",
-                        "r02_ncu_dominant_strip.json"),
+            "euler2d": ("k_e2_phi_strip_fw<5,LF,4> (Euler strip JVP with a face warp: the lookahead application "
+                        "dt A (s_j W) -> Y, reads W, q~, b_1, writes Y; + k_e2_phi_strip<5,LF,8,DOT> with the "
+                        "pass-1 dots at substep starts)",
+                        "r02f_ncu_dominant_strip.json"),
             "burgers2d": ("k_b2_phi_strip<5,*> (2D Burgers strip JVP: reads x, u~, b_1, writes y; + the pass-1 "
                           "dots at substep starts)", None),
-            "euler3d": ("k_e3_phi_march<4,*> (3D Euler z-march JVP: reads x, q~, b_1, writes y; + the pass-1 "
-                        "dots at substep starts)", None),
+            "euler3d": ("k_e3_phi_march_fw<4> (3D Euler z-march JVP with face warps: reads x, q~, b_1, writes y; "
+                        "+ k_e3_phi_march<4,DOT> with the pass-1 dots at substep starts)", None),
         }.get(w.kind, ("operator sweep (JVP of slot j)", None))
         for kind, name, ncu_file in (
                 (1, "k_ts3 (pipelined DCGS2 merged pass, column j: u <- u - V a, W <- W - g u - V mu, "
                     "Y <- Arnoldi-relation image, + column j+1 pass-1 dots; reads V_0..V_{j-1}, u, W, Y, "
                     "writes u, W, Y; k_ts2<TS2_UPD> on substep-final avnorm cycles)",
-                 "r02_ncu_dominant_ts3.json" if w.kind == "euler2d" else None),
+                 "r02f_ncu_dominant_ts3.json" if w.kind == "euler2d" else None),
                 (2, sweep[0], sweep[1])):
             ud = u.clone()
             ctx.time_dominant(kind)
