@@ -59,7 +59,7 @@ typedef struct expdg_op expdg_op;
  * (proj/include/expdg/burgers.hpp:16-23) and EulerConfig (proj/include/expdg/euler.hpp:33-37). */
 typedef struct {
   int kind;            /* EXPDG_BURGERS1D .. EXPDG_EULER3D */
-  int order;           /* LGL degree k (device: 1..8) */
+  int order;           /* LGL degree k (device: 1..8; 3D Euler 1..5) */
   int nx, ny, nz;      /* elements per axis */
   double x0, x1, y0, y1, z0, z1;
   int periodic;        /* 1 periodic, 0 zero-Dirichlet (Burgers 1D/2D only) */

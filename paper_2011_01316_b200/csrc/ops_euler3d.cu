@@ -439,7 +439,7 @@ struct E3March {
   static constexpr int VS = DOT ? (VSF > 16 ? 16 : (VSF < 1 ? 1 : VSF)) : 1;
   static constexpr bool FITS = !DOT || VSF >= 4;
   static constexpr int SMEM = (BASE + (DOT ? 2 * TILE + VS * TILE : 0)) * 8;
-  static constexpr bool OK = (BLK * 8) % 16 == 0;
+  static constexpr bool OK = (BLK * 8) % 16 == 0 && CONS <= 256;  // NP = 2, 4; the other orders keep the tile kernel
 };
 
 // Dot warps of the fused z-march: the march's (tile, plane) sequence, u = the tile's x in the
@@ -1433,8 +1433,10 @@ std::unique_ptr<OpDevice> make_euler3d(const expdg_op_desc& d) {
     case 2: return std::make_unique<Euler3D<2>>(d);
     case 3: return std::make_unique<Euler3D<3>>(d);
     case 4: return std::make_unique<Euler3D<4>>(d);
+    case 5: return std::make_unique<Euler3D<5>>(d);  // element-tile kernels (2 / 1 elements per CTA)
+    case 6: return std::make_unique<Euler3D<6>>(d);
   }
-  throw std::invalid_argument("euler3d: device orders are 1..3");
+  throw std::invalid_argument("euler3d: device orders are 1..5");
 }
 
 }  // namespace expdg

@@ -96,7 +96,7 @@ def random_state5(rng, ne, npe):
     return q
 
 
-@pytest.mark.parametrize("order,n", [(1, 3), (2, 3), (3, 2)])
+@pytest.mark.parametrize("order,n", [(1, 3), (2, 3), (3, 2), (4, 2), (5, 2)])
 def test_euler3d_apply_matches_oracle(ctx, order, n):
     rng = np.random.default_rng(order)
     spec = pkg.OperatorSpec("euler3d", order, n, n + 1, n, box=(0, 1, 0, 2, 0, 1.5), euler_flux="lf")
@@ -167,6 +167,24 @@ def test_c5_reduced_mesh_epi2_parity(ctx):
     op = pkg.Operator(ctx, w.spec())
     r = pkg.integrate(ctx, op, to_dev(u0), "epi2", dt, w.steps * dt, tol=w.tol, max_basis=w.max_basis,
                       orth_length=w.max_basis)
+    assert r.status == orc.status == "completed"
+    assert rel(to_host(r.u), orc.u) <= 1e-9
+    d_dev = np.diff(np.concatenate([[0], r.iters_per_step]))
+    d_orc = np.diff(np.concatenate([[0], orc.iters_per_step]))
+    assert np.max(np.abs(d_dev - d_orc)) <= 1
+
+
+@pytest.mark.parametrize("order", [4, 5])
+def test_euler3d_orders_4_5_epi2_parity(ctx, order):
+    # orders above C5's run the element-tile kernels (125 / 216 nodes per element: 2 / 1 elements
+    # per CTA); EPI2 against the oracle on a 2 x 3 x 2 mesh
+    rng = np.random.default_rng(order)
+    spec = pkg.OperatorSpec("euler3d", order, 2, 3, 2, box=(0, 1, 0, 2, 0, 1.5), euler_flux="lf")
+    op = pkg.Operator(ctx, spec)
+    u0 = random_state5(rng, 12, (order + 1) ** 3)
+    kw = dict(tol=1e-10, max_basis=20, orth_length=20)
+    r = pkg.integrate(ctx, op, to_dev(u0), "epi2", 1e-4, 3e-4, **kw)
+    orc = oracle_problem(spec).integrate("epi2", u0, 1e-4, 3e-4, **kw)
     assert r.status == orc.status == "completed"
     assert rel(to_host(r.u), orc.u) <= 1e-9
     d_dev = np.diff(np.concatenate([[0], r.iters_per_step]))
