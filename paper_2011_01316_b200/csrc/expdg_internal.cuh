@@ -325,6 +325,10 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
 // named barrier over the 256 consumer threads of a warp-specialised CTA
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 // named barrier over the CONS consumer threads of a strip kernel (producer warp excluded)
+// L2 prefetch of a global range (bytes a multiple of 16, 16-byte aligned)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src_gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src_gmem), "r"(bytes) : "memory");
+}
 template <int CONS>
 __device__ __forceinline__ void strip_sync() { asm volatile("bar.sync 1, %0;" ::"n"(CONS) : "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {

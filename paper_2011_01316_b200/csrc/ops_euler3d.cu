@@ -35,6 +35,7 @@ struct E3P {
   // z-slab partition: planes -1 and nz are the neighbours' halo planes (raw values of the
   // applied vector / the frozen primitives), exchanged before the kernel runs
   int part;
+  int dbg;  // EXPDG_E3_DBG (diagnostics)
   const double* gx_lo;
   const double* gx_hi;
   const double* gt_lo;
@@ -970,6 +971,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
   const int ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
   const long long ntiles = (long long)ntx * nty;  // CTA c marches tiles c, c + G, ... (see k_e3_phi_march)
   const double* b1 = (b.p == 1) ? b.b[1] : nullptr;
+  const bool l2pf = (P.dbg & 8) == 0;  // EXPDG_E3_DBG bit 3: no neighbour prefetch
   double nacc = 0.0;
   auto unit = [&](long long tile, int& ix0, int& iy0, int& tx, int& ty) {
     ix0 = (int)(tile % ntx) * TX;
@@ -1012,6 +1014,28 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
               const size_t eb = ((size_t)(q - 1) * ny + iy0 + ly) * nx + ix0;
               bulk_g2s(dst + 2 * S::PL + (size_t)ly * TX * BLK, b1 + eb * BLK, rowb, &full[sl]);
             }
+          }
+          // The x/y neighbour elements of this plane into L2 ahead of the face warps' gathers of
+          // their face nodes (L2 hit rate of the launch 29 -> 45 %, 0.912 -> 0.906 ms at C5).  The
+          // DRAM bytes do not move (2.36 GB read for 2.01 algorithmic): the excess is the y-neighbour
+          // rows across round boundaries (CTA c marches tiles c, c + G, ...: a round is 4.6 tile
+          // rows, so ~22 % of the tiles meet their N or S neighbour a whole round, ~280 MB of
+          // traffic, later), which no prefetch distance covers.
+          if (l2pf && q >= 1 && q <= nz) {
+            const uint32_t eb = BLK * 8;
+            const int gw = ix0 == 0 ? nx - 1 : ix0 - 1, ge = ix0 + tx == nx ? 0 : ix0 + tx;
+            const int gs = iy0 == 0 ? ny - 1 : iy0 - 1, gn = iy0 + ty == ny ? 0 : iy0 + ty;
+            for (int ly = 0; ly < ty; ++ly) {
+              const size_t row = pbase + (size_t)(iy0 + ly) * nx;
+              bulk_prefetch_l2(x + (row + gw) * BLK, eb);
+              bulk_prefetch_l2(P.ut + (row + gw) * BLK, eb);
+              bulk_prefetch_l2(x + (row + ge) * BLK, eb);
+              bulk_prefetch_l2(P.ut + (row + ge) * BLK, eb);
+            }
+            bulk_prefetch_l2(x + (pbase + (size_t)gs * nx + ix0) * BLK, rowb);
+            bulk_prefetch_l2(P.ut + (pbase + (size_t)gs * nx + ix0) * BLK, rowb);
+            bulk_prefetch_l2(x + (pbase + (size_t)gn * nx + ix0) * BLK, rowb);
+            bulk_prefetch_l2(P.ut + (pbase + (size_t)gn * nx + ix0) * BLK, rowb);
           }
         }
       }
@@ -1369,6 +1393,7 @@ class Euler3D : public OpDevice {
       march_grid = (int)std::max<long long>(1, std::min<long long>(tiles, 148LL * std::max(1, per_sm)));
       whole_tiles = d.nx % SM::TX == 0 && d.ny % SM::TY == 0;
       if (const char* v = std::getenv("EXPDG_E3_FW")) use_fw = use_fw && v[0] != '0';
+    if (const char* v = std::getenv("EXPDG_E3_DBG")) P.dbg = std::atoi(v);
       if constexpr (kFwOk)
         EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         E3MarchFW<NP>::SMEM));
