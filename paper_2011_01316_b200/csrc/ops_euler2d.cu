@@ -991,7 +991,10 @@ struct E2StripFW {
 
 template <int NP, bool ROE, int CW>
 __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>::PER_SM)
-    k_e2_phi_strip_fw(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
+    k_e2_phi_strip_fw(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b, const double* xin,
+                      double* yout) {
+  // st == nullptr: the standalone operator application y = L x (expdg_op_apply_linear), x / y the
+  // caller's vectors, no augmentation tail, no reductions
   using S = E2StripFW<NP, CW>;
   constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
   extern __shared__ __align__(128) double smem[];
@@ -1008,19 +1011,27 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
   __shared__ double s_red[1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    s_go = apply_go(st, base);
+    s_go = st ? apply_go(st, base) : 1;
     if (s_go) {
-      s_j = st->j;
-      if (blockIdx.x == 0) {
-        if (apply_stage(st, base) == 1) st->dots_fused = 0;
-        st->app_bytes += 8.0 * (double)P.n * 4.0;
-        st->app_launches++;
+      if (st) {
+        s_j = st->j;
+        if (blockIdx.x == 0) {
+          if (apply_stage(st, base) == 1) st->dots_fused = 0;
+          st->app_bytes += 8.0 * (double)P.n * 4.0;
+          st->app_launches++;
+        }
+        s_xs = st->scale[s_j];
+        s_dt = st->dt;
+        s_ld = st->ld;
+        const double* xslot = base + (size_t)s_j * st->ld;
+        for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
+      } else {
+        s_j = 0;
+        s_xs = 1.0;
+        s_dt = 1.0;
+        s_ld = 0;
+        for (int i = 0; i < kMaxP; ++i) s_xt[i] = 0.0;
       }
-      s_xs = st->scale[s_j];
-      s_dt = st->dt;
-      s_ld = st->ld;
-      const double* xslot = base + (size_t)s_j * st->ld;
-      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
       for (int q = 0; q < NBUF; ++q) {
         mbar_init(&full[q], 1);
         mbar_init(&empty[q], 1 + S::FWARPS);  // the node warps + every face warp
@@ -1036,8 +1047,8 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
   for (int q = tid; q < NP; q += blockDim.x) s_wq[q] = P.w[q];
   __syncthreads();
   if (!s_go) return;
-  const double* x = base + (size_t)s_j * s_ld;
-  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double* x = st ? base + (size_t)s_j * s_ld : xin;
+  double* y = st ? base + (size_t)(s_j + 1) * s_ld : yout;
   const double xs = s_xs, dt = s_dt;
   const int nx = P.nx, ny = P.ny;
   const int nstrips = (nx + W - 1) / W;
@@ -1276,6 +1287,7 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
     }
   }
   __syncthreads();
+  if (!st) return;
   if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
     const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
     y[P.n + tid] = v;
@@ -1324,7 +1336,7 @@ class Euler2D : public OpDevice {
   bool fw_align = false;  // EXPDG_E2_ALIGN=1: whole CTAs per strip (see launch_strip_fw)
   int fw_per_sm = 1;
   void launch_strip_fw(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
-                       const BArgs& b) {
+                       const BArgs& b, const double* xin = nullptr, double* yout = nullptr) {
     using SS = E2StripFW<NP, 4>;
     const long long nstrips = (P.nx + SS::W - 1) / SS::W;
     const long long rows = nstrips * P.ny;
@@ -1336,8 +1348,8 @@ class Euler2D : public OpDevice {
     // the kernel is latency-bound, not DRAM-bound, and the lost CTAs cost more than the misses.
     const long long q = g / nstrips;
     if (fw_align && q >= 1 && P.ny % q == 0 && nstrips * q * 10 >= (long long)g * 8) g = (int)(nstrips * q);
-    if (roe) k_e2_phi_strip_fw<NP, true, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b);
-    else k_e2_phi_strip_fw<NP, false, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b);
+    if (roe) k_e2_phi_strip_fw<NP, true, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, xin, yout);
+    else k_e2_phi_strip_fw<NP, false, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, xin, yout);
   }
   template <int CW, bool DOT>
   void launch_strip(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
@@ -1484,6 +1496,10 @@ class Euler2D : public OpDevice {
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
     if (P.part) exchange(s, x, hx_lo(), hx_hi());
     const E2P<NP> p = params(frozen);
+    if (which == 0 && use_strip && use_fw && x != y) {  // y = L x through the strip JVP (the same kernel as the phi cycle)
+      launch_strip_fw(s, p, nullptr, nullptr, nullptr, BArgs{}, x, y);
+      return;
+    }
     if (roe) k_e2_apply<NP, true><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
     else k_e2_apply<NP, false><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
   }

@@ -922,7 +922,10 @@ struct E3MarchFW {
 
 template <int NP>
 __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
-    k_e3_phi_march_fw(E3P<NP> P, PhiState* st, double* base, double* partials, BArgs b) {
+    k_e3_phi_march_fw(E3P<NP> P, PhiState* st, double* base, double* partials, BArgs b, const double* xin,
+                      double* yout) {
+  // st == nullptr: the standalone operator application y = L x (expdg_op_apply_linear), x / y the
+  // caller's vectors, no augmentation tail, no reductions
   using S = E3MarchFW<NP>;
   constexpr int NN = S::NN, NF = S::NF, BLK = S::BLK, TX = S::TX, TY = S::TY, NBUF = S::NBUF, N = NP - 1;
   extern __shared__ __align__(128) double smem[];
@@ -938,19 +941,27 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
   __shared__ double s_red[1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    s_go = apply_go(st, base);
+    s_go = st ? apply_go(st, base) : 1;
     if (s_go) {
-      s_j = st->j;
-      if (blockIdx.x == 0) {
-        if (apply_stage(st, base) == 1) st->dots_fused = 0;
-        st->app_bytes += 8.0 * (double)P.n * 4.0;
-        st->app_launches++;
+      if (st) {
+        s_j = st->j;
+        if (blockIdx.x == 0) {
+          if (apply_stage(st, base) == 1) st->dots_fused = 0;
+          st->app_bytes += 8.0 * (double)P.n * 4.0;
+          st->app_launches++;
+        }
+        s_xs = st->scale[s_j];
+        s_dt = st->dt;
+        s_ld = st->ld;
+        const double* xslot = base + (size_t)s_j * st->ld;
+        for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
+      } else {
+        s_j = 0;
+        s_xs = 1.0;
+        s_dt = 1.0;
+        s_ld = 0;
+        for (int i = 0; i < kMaxP; ++i) s_xt[i] = 0.0;
       }
-      s_xs = st->scale[s_j];
-      s_dt = st->dt;
-      s_ld = st->ld;
-      const double* xslot = base + (size_t)s_j * st->ld;
-      for (int i = 0; i < kMaxP; ++i) s_xt[i] = (i < b.p) ? xslot[P.n + i] * s_xs : 0.0;
       for (int q = 0; q < NBUF; ++q) {
         mbar_init(&full[q], 1);
         mbar_init(&empty[q], 1 + S::FWARPS);  // the node warps + every face warp
@@ -964,8 +975,8 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
   }
   __syncthreads();
   if (!s_go) return;
-  const double* x = base + (size_t)s_j * s_ld;
-  double* y = base + (size_t)(s_j + 1) * s_ld;
+  const double* x = st ? base + (size_t)s_j * s_ld : xin;
+  double* y = st ? base + (size_t)(s_j + 1) * s_ld : yout;
   const double xs = s_xs, dt = s_dt;
   const int nx = P.nx, ny = P.ny, nz = P.nz;
   const int ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
@@ -1267,6 +1278,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
     }
   }
   __syncthreads();
+  if (!st) return;
   if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
     const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
     y[P.n + tid] = v;
@@ -1428,8 +1440,8 @@ class Euler3D : public OpDevice {
         }
         if constexpr (kFwOk) {
           if (use_fw) {
-            k_e3_phi_march_fw<NP><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(params(frozen), st, base,
-                                                                                                 partials, b);
+            k_e3_phi_march_fw<NP><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+                params(frozen), st, base, partials, b, nullptr, nullptr);
             return;
           }
         }
@@ -1442,6 +1454,13 @@ class Euler3D : public OpDevice {
   }
   void launch_apply(cudaStream_t s, int which, const double* x, double* y) override {
     if (P.part) exchange(s, x, hb_(0), hb_(1));
+    if constexpr (kFwOk) {
+      if (which == 0 && use_march && use_fw && x != y) {  // y = L x through the z-march JVP (the phi cycle's kernel)
+        k_e3_phi_march_fw<NP><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+            params(frozen), nullptr, nullptr, nullptr, BArgs{}, x, y);
+        return;
+      }
+    }
     k_e3_apply<NP><<<grid, 256, 0, s>>>(params(frozen), which, x, y, nullptr, nullptr);
   }
   void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
