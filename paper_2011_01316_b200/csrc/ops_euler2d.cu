@@ -989,12 +989,20 @@ struct E2StripFW {
   static_assert(NBUF >= 4, "the face warps run up to two rows ahead of the node warps");
 };
 
-template <int NP, bool ROE, int CW>
+// MODE 0: the linear operator (the phi cycle's JVP).  MODE 2, standalone only: the full right-hand
+// side R(x) (proj/src/euler.cpp:249-297: nonlinear volume fluxes, full LF / Roe face fluxes, no
+// frozen state), which also writes the frozen primitives of x for the step's JVPs (`frozen`) and
+// raises fst->domain_flag on an inadmissible state -- the residual of every step
+// (expdg_op_full_rhs, launch_residual).
+template <int NP, bool ROE, int CW, int MODE>
 __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>::PER_SM)
     k_e2_phi_strip_fw(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b, const double* xin,
-                      double* yout) {
-  // st == nullptr: the standalone operator application y = L x (expdg_op_apply_linear), x / y the
-  // caller's vectors, no augmentation tail, no reductions
+                      double* yout, PhiState* fst, double* frozen) {
+  // st == nullptr: the standalone operator application y = L x / y = R(x) (expdg_op_apply_linear,
+  // expdg_op_full_rhs), x / y the caller's vectors, no augmentation tail, no reductions
+  constexpr int NARR = MODE == 2 ? 1 : 2;  // ring arrays in use: x (+ the frozen primitives)
+  if (MODE == 2 && fst && fst->stopped) return;
+  bool bad = false;
   using S = E2StripFW<NP, CW>;
   constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
   extern __shared__ __align__(128) double smem[];
@@ -1079,11 +1087,11 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
           mbar_wait(&empty[sl], (int)(((seq / NBUF) & 1) ^ 1));
           double* dst = ring + (size_t)sl * S::BUFD;
           const uint32_t eb = BLK * 8;
-          mbar_arrive_expect_tx(&full[sl], 2u * (uint32_t)(w + 2) * eb);
+          mbar_arrive_expect_tx(&full[sl], (uint32_t)NARR * (uint32_t)(w + 2) * eb);
           const size_t rbase = (size_t)row * nx;
           const int left = ie0 == 0 ? nx - 1 : ie0 - 1;
           const int right = ie0 + w == nx ? 0 : ie0 + w;
-          for (int arr = 0; arr < 2; ++arr) {
+          for (int arr = 0; arr < NARR; ++arr) {
             const double* src = arr == 0 ? srcx : srct;
             double* d = dst + arr * S::ROWD;
             if (ie0 >= 1 && ie0 + w < nx) {
@@ -1148,12 +1156,11 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             qa[c] = ra[pa * BLK + c * NN + na] * xs;
-            ta[c] = ra[S::ROWD + pa * BLK + c * NN + na];
+            ta[c] = MODE == 2 ? 0.0 : ra[S::ROWD + pa * BLK + c * NN + na];
             qb[c] = rb[pb * BLK + c * NN + nb] * xs;
-            tb[c] = rb[S::ROWD + pb * BLK + c * NN + nb];
+            tb[c] = MODE == 2 ? 0.0 : rb[S::ROWD + pb * BLK + c * NN + nb];
           }
-          bool bad = false;
-          face_flux<ROE>(0, dir, P.gamma, qa, qb, ta, tb, f, bad);
+          face_flux<ROE>(MODE, dir, P.gamma, qa, qb, ta, tb, f, bad);
 #pragma unroll
           for (int c = 0; c < 4; ++c) dst[c] = f[c];
         }
@@ -1211,15 +1218,28 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
         const double* cur = ring + (size_t)sl * S::BUFD;
         double* sf = sf0 + (it & 1) * S::SF;
         if (active) {
-          double qv[4], tv[4];
+          double qv[4], fx[4], fy[4];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            qv[c] = cur[(le + 1) * BLK + c * NN + node] * xs;
-            tv[c] = cur[S::ROWD + (le + 1) * BLK + c * NN + node];
+          for (int c = 0; c < 4; ++c) qv[c] = cur[(le + 1) * BLK + c * NN + node] * xs;
+          if (MODE == 2) {
+            if (!admissible4(qv, P.gamma)) bad = true;
+            const Prim pq = prim_of(qv, P.gamma);
+            flux_dir(qv, pq, 0, fx);
+            flux_dir(qv, pq, 1, fy);
+            if (frozen) {  // (u, v, H, a | sqrt(rho)) of the state for this step's JVPs
+              double fv[4];
+              frozen_of<ROE>(qv, P.gamma, fv);
+              const size_t e = (size_t)r * nx + ie;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) frozen[(e * 4 + c) * NN + node] = fv[c];
+            }
+          } else {
+            double tv[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tv[c] = cur[S::ROWD + (le + 1) * BLK + c * NN + node];
+            const Prim tp = prim_frozen(tv);
+            jac_apply_xy(tp, P.gamma, qv, fx, fy);
           }
-          const Prim tp = prim_frozen(tv);
-          double fx[4], fy[4];
-          jac_apply_xy(tp, P.gamma, qv, fx, fy);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             sf[((le * 2 + 0) * 4 + c) * NN + node] = fx[c];
@@ -1286,6 +1306,7 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
       mbar_arrive(&fempty[(it - 1) & 1]);
     }
   }
+  if (MODE == 2 && bad && fst) fst->domain_flag = 1;
   __syncthreads();
   if (!st) return;
   if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
@@ -1334,7 +1355,8 @@ class Euler2D : public OpDevice {
   // the plain half-width strip with face warps (EXPDG_E2_FW=0: the single-role strip)
   bool use_fw = true;
   bool fw_align = false;  // EXPDG_E2_ALIGN=1: whole CTAs per strip (see launch_strip_fw)
-  int fw_per_sm = 1;
+  bool rhs_strip = true;  // EXPDG_E2_RHS_TILE=1: the element-tile kernel for R(x) (residual, full_rhs)
+  int fw_per_sm = 1, fw2_per_sm = 1;
   void launch_strip_fw(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
                        const BArgs& b, const double* xin = nullptr, double* yout = nullptr) {
     using SS = E2StripFW<NP, 4>;
@@ -1348,8 +1370,25 @@ class Euler2D : public OpDevice {
     // the kernel is latency-bound, not DRAM-bound, and the lost CTAs cost more than the misses.
     const long long q = g / nstrips;
     if (fw_align && q >= 1 && P.ny % q == 0 && nstrips * q * 10 >= (long long)g * 8) g = (int)(nstrips * q);
-    if (roe) k_e2_phi_strip_fw<NP, true, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, xin, yout);
-    else k_e2_phi_strip_fw<NP, false, 4><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, xin, yout);
+    if (roe)
+      k_e2_phi_strip_fw<NP, true, 4, 0><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, xin, yout, nullptr,
+                                                                         nullptr);
+    else
+      k_e2_phi_strip_fw<NP, false, 4, 0><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, xin, yout,
+                                                                          nullptr, nullptr);
+  }
+  // R(x) -> y through the strip kernel (MODE 2); frozen_out / fst may be null (expdg_op_full_rhs)
+  void launch_strip_rhs(cudaStream_t s, const E2P<NP>& p, const double* x, double* y, PhiState* fst,
+                        double* frozen_out) {
+    using SS = E2StripFW<NP, 4>;
+    const long long rows = (long long)((P.nx + SS::W - 1) / SS::W) * P.ny;
+    const int g = (int)std::max<long long>(1, std::min<long long>(rows, 148LL * fw2_per_sm));
+    if (roe)
+      k_e2_phi_strip_fw<NP, true, 4, 2><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, BArgs{}, x, y,
+                                                                         fst, frozen_out);
+    else
+      k_e2_phi_strip_fw<NP, false, 4, 2><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, BArgs{}, x, y,
+                                                                          fst, frozen_out);
   }
   template <int CW, bool DOT>
   void launch_strip(cudaStream_t s, const E2P<NP>& p, PhiState* st, double* base, double* partials,
@@ -1456,18 +1495,26 @@ class Euler2D : public OpDevice {
     if (const char* v = std::getenv("EXPDG_E2_DBG")) P.dbg = std::atoi(v);
     if (const char* v = std::getenv("EXPDG_E2_FW")) use_fw = v[0] != '0';
     if (const char* v = std::getenv("EXPDG_E2_ALIGN")) fw_align = v[0] == '1';
+    if (const char* v = std::getenv("EXPDG_E2_RHS_TILE")) rhs_strip = v[0] != '1';
     set_strip_attrs<8, false>();
     set_strip_attrs<4, false>();
     {  // the face-warp strip: attributes and occupancy here, never on the launch path (a runtime
        // call that synchronises the device must not run while another rank's collective spins)
       using SF = E2StripFW<NP, 4>;
-      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SF::SMEM));
-      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SF::SMEM));
-      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw_per_sm, k_e2_phi_strip_fw<NP, false, 4>,
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SF::SMEM));
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SF::SMEM));
+      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw_per_sm, k_e2_phi_strip_fw<NP, false, 4, 0>,
                                                                SF::THREADS, SF::SMEM));
       fw_per_sm = std::max(1, fw_per_sm);
+      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw2_per_sm, k_e2_phi_strip_fw<NP, false, 4, 2>,
+                                                               SF::THREADS, SF::SMEM));
+      fw2_per_sm = std::max(1, fw2_per_sm);
     }
     if constexpr (kDotFits) set_strip_attrs<8, true>();
     const long long ntiles = ((long long)d.nx * nyl + E2Tile<NP>::TE - 1) / E2Tile<NP>::TE;
@@ -1500,6 +1547,10 @@ class Euler2D : public OpDevice {
       launch_strip_fw(s, p, nullptr, nullptr, nullptr, BArgs{}, x, y);
       return;
     }
+    if (which == 2 && use_strip && use_fw && rhs_strip && x != y) {  // y = R(x)
+      launch_strip_rhs(s, p, x, y, nullptr, nullptr);
+      return;
+    }
     if (roe) k_e2_apply<NP, true><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
     else k_e2_apply<NP, false><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);
   }
@@ -1507,7 +1558,8 @@ class Euler2D : public OpDevice {
   void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
     if (P.part) exchange(s, u, hx_lo(), hx_hi());
     const E2P<NP> p = params(nullptr);
-    if (roe) k_e2_apply<NP, true><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
+    if (use_strip && use_fw && rhs_strip && u != r) launch_strip_rhs(s, p, u, r, st, frozen);
+    else if (roe) k_e2_apply<NP, true><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
     else k_e2_apply<NP, false><<<grid, 256, 0, s>>>(p, 2, u, r, st, frozen);
     if (P.part) exchange(s, frozen, ht_lo(), ht_hi());  // frozen halo for this step's JVPs
   }

@@ -30,6 +30,11 @@ def _epi2(spec, u0, dt, steps, ctx=None, max_basis=12):
 
 
 def _both(monkeypatch, env, spec, u0, dt, steps=2):
+    # the step residual through the element-tile kernel in both runs: the strip residual
+    # (k_e2_phi_strip_fw<.., 2>) sums its face terms in another order than the tile kernel, and this
+    # file pins the JVP kernels bit for bit (the residual kernels are pinned to the oracle in
+    # test_gpu_euler2d.py and against each other below)
+    monkeypatch.setenv("EXPDG_E2_RHS_TILE", "1")
     out = []
     for v in ("1", "0"):
         monkeypatch.setenv(env, v)
@@ -91,6 +96,7 @@ def test_face_warps_on_slab_partitions_bit_identical(monkeypatch, kind, env):
     layer = u0.size // axis
     ranges = slab_ranges(axis, 3)
     res = []
+    monkeypatch.setenv("EXPDG_E2_RHS_TILE", "1")
     for v in ("1", "0"):
         monkeypatch.setenv(env, v)
 
@@ -104,3 +110,25 @@ def test_face_warps_on_slab_partitions_bit_identical(monkeypatch, kind, env):
         assert a[2] == b[2] == "completed"
         assert a[1] == b[1]
         assert np.array_equal(a[0], b[0])
+
+
+@pytest.mark.parametrize("order,nx,ny,flux", [(4, 12, 7, "lf"), (4, 11, 1, "roe"), (1, 40, 3, "lf"), (2, 9, 4, "roe"),
+                                              (3, 8, 8, "lf"), (5, 7, 3, "roe"), (7, 3, 4, "lf"), (8, 2, 3, "roe")])
+def test_strip_residual_matches_tile_kernel(monkeypatch, order, nx, ny, flux):
+    # R(x) and the frozen primitives it leaves for the JVPs: the strip kernel (MODE 2, face warps)
+    # against the element-tile kernel, through full_rhs and through one EPI2 step
+    rng = np.random.default_rng(10 * order + nx)
+    spec = pkg.OperatorSpec("euler2d", order, nx, ny, box=(0, 1, 0, 2, 0, 1), euler_flux=flux)
+    u0 = random_state(rng, nx * ny, (order + 1) ** 2)
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("EXPDG_E2_RHS_TILE", v)
+        c = pkg.Context(0, orth="dcgs2", fused=False)
+        op = pkg.Operator(c, spec)
+        rhs = to_host(op.full_rhs(to_dev(u0)))
+        r = pkg.integrate(c, op, to_dev(u0), "epi2", 2e-4, 4e-4, tol=1e-10, max_basis=12, orth_length=12)
+        out.append((rhs, to_host(r.u), list(r.iters_per_step), r.status))
+    (ra, ua, ia, sa), (rb, ub, ib, sb) = out
+    assert sa == sb == "completed" and ia == ib
+    assert np.max(np.abs(ra - rb)) <= 1e-13 * np.max(np.abs(rb))
+    assert np.max(np.abs(ua - ub)) <= 1e-13 * np.max(np.abs(ub))
