@@ -920,12 +920,18 @@ struct E3MarchFW {
   static constexpr bool OK = B::OK && SMEM <= 232448 - 3072;
 };
 
-template <int NP>
+// MODE 0: the linear operator (the phi cycle's JVP).  MODE 2, standalone only: the full right-hand
+// side R(x) (oracle/src/euler.cpp, Euler3DOperator: nonlinear volume fluxes, full LF face fluxes),
+// which also writes the frozen primitives of x for the step's JVPs and raises fst->domain_flag on
+// an inadmissible state -- the residual of every step (expdg_op_full_rhs, launch_residual).
+template <int NP, int MODE>
 __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
     k_e3_phi_march_fw(E3P<NP> P, PhiState* st, double* base, double* partials, BArgs b, const double* xin,
-                      double* yout) {
-  // st == nullptr: the standalone operator application y = L x (expdg_op_apply_linear), x / y the
-  // caller's vectors, no augmentation tail, no reductions
+                      double* yout, PhiState* fst, double* frozen) {
+  // st == nullptr: the standalone operator application y = L x / y = R(x) (expdg_op_apply_linear,
+  // expdg_op_full_rhs), x / y the caller's vectors, no augmentation tail, no reductions
+  if (MODE == 2 && fst && fst->stopped) return;
+  bool bad = false;
   using S = E3MarchFW<NP>;
   constexpr int NN = S::NN, NF = S::NF, BLK = S::BLK, TX = S::TX, TY = S::TY, NBUF = S::NBUF, N = NP - 1;
   extern __shared__ __align__(128) double smem[];
@@ -1016,11 +1022,11 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
           double* dst = ring + (size_t)sl * S::BUFD;
           const bool with_b = b1 && q >= 1 && q <= nz;
           const uint32_t rowb = (uint32_t)tx * BLK * 8;
-          mbar_arrive_expect_tx(&full[sl], (2u + (with_b ? 1u : 0u)) * (uint32_t)ty * rowb);
+          mbar_arrive_expect_tx(&full[sl], ((MODE == 2 ? 1u : 2u) + (with_b ? 1u : 0u)) * (uint32_t)ty * rowb);
           for (int ly = 0; ly < ty; ++ly) {
             const size_t e = pbase + (size_t)(iy0 + ly) * nx + ix0;
             bulk_g2s(dst + (size_t)ly * TX * BLK, srcx + e * BLK, rowb, &full[sl]);
-            bulk_g2s(dst + S::PL + (size_t)ly * TX * BLK, srct + e * BLK, rowb, &full[sl]);
+            if (MODE != 2) bulk_g2s(dst + S::PL + (size_t)ly * TX * BLK, srct + e * BLK, rowb, &full[sl]);
             if (with_b) {
               const size_t eb = ((size_t)(q - 1) * ny + iy0 + ly) * nx + ix0;
               bulk_g2s(dst + 2 * S::PL + (size_t)ly * TX * BLK, b1 + eb * BLK, rowb, &full[sl]);
@@ -1039,14 +1045,18 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
             for (int ly = 0; ly < ty; ++ly) {
               const size_t row = pbase + (size_t)(iy0 + ly) * nx;
               bulk_prefetch_l2(x + (row + gw) * BLK, eb);
-              bulk_prefetch_l2(P.ut + (row + gw) * BLK, eb);
               bulk_prefetch_l2(x + (row + ge) * BLK, eb);
-              bulk_prefetch_l2(P.ut + (row + ge) * BLK, eb);
+              if (MODE != 2) {
+                bulk_prefetch_l2(P.ut + (row + gw) * BLK, eb);
+                bulk_prefetch_l2(P.ut + (row + ge) * BLK, eb);
+              }
             }
             bulk_prefetch_l2(x + (pbase + (size_t)gs * nx + ix0) * BLK, rowb);
-            bulk_prefetch_l2(P.ut + (pbase + (size_t)gs * nx + ix0) * BLK, rowb);
             bulk_prefetch_l2(x + (pbase + (size_t)gn * nx + ix0) * BLK, rowb);
-            bulk_prefetch_l2(P.ut + (pbase + (size_t)gn * nx + ix0) * BLK, rowb);
+            if (MODE != 2) {
+              bulk_prefetch_l2(P.ut + (pbase + (size_t)gs * nx + ix0) * BLK, rowb);
+              bulk_prefetch_l2(P.ut + (pbase + (size_t)gn * nx + ix0) * BLK, rowb);
+            }
           }
         }
       }
@@ -1084,7 +1094,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < 5; ++c) {
             qq[c] = pl[e * BLK + c * NN + nd] * xs;
-            tt[c] = pl[S::PL + e * BLK + c * NN + nd];
+            tt[c] = MODE == 2 ? 0.0 : pl[S::PL + e * BLK + c * NN + nd];
           }
         };
         auto from_gmem = [&](int gx, int gy, int nd, double(&qq)[5], double(&tt)[5]) {
@@ -1092,13 +1102,12 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < 5; ++c) {
             qq[c] = x[(e * 5 + c) * NN + nd] * xs;
-            tt[c] = __ldg(P.ut + (e * 5 + c) * NN + nd);
+            tt[c] = MODE == 2 ? 0.0 : __ldg(P.ut + (e * 5 + c) * NN + nd);
           }
         };
         for (int f = ft; f < total; f += S::FTH) {
           double qa[5], ta[5], qb[5], tb[5], fl[5];
           double* dst;
-          bool bad = false;
           if (f < NFX) {  // x-face column fc between tile columns fc - 1 (low) and fc (high)
             const int fc = f / (TY * NF), rem = f - fc * TY * NF, fy = rem / NF, fn = rem - fy * NF;
             if (fc > tx || fy >= ty) continue;
@@ -1107,7 +1116,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
             else from_ring(cur, fy * TX + fc - 1, nlo, qa, ta);
             if (fc == tx) from_gmem(ix0 + tx == nx ? 0 : ix0 + tx, iy0 + fy, nhi, qb, tb);
             else from_ring(cur, fy * TX + fc, nhi, qb, tb);
-            face3(0, 0, P.gamma, qa, qb, ta, tb, fl, bad);
+            face3(MODE, 0, P.gamma, qa, qb, ta, tb, fl, bad);
             dst = fxf + fc * S::FXC + (fy * NF + fn) * 5;
           } else if (f < NFX + NFY) {  // y-face row fc between tile rows fc - 1 and fc
             const int g = f - NFX, fc = g / (TX * NF), rem = g - fc * TX * NF, fxl = rem / NF, fn = rem - fxl * NF;
@@ -1118,7 +1127,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
             else from_ring(cur, (fc - 1) * TX + fxl, nlo, qa, ta);
             if (fc == ty) from_gmem(ix0 + fxl, iy0 + ty == ny ? 0 : iy0 + ty, nhi, qb, tb);
             else from_ring(cur, fc * TX + fxl, nhi, qb, tb);
-            face3(0, 1, P.gamma, qa, qb, ta, tb, fl, bad);
+            face3(MODE, 1, P.gamma, qa, qb, ta, tb, fl, bad);
             dst = fyf + fc * S::FYR + (fxl * NF + fn) * 5;
           } else {  // z-faces: above this plane, or below it on the tile's first plane
             const int g = f - NFX - NFY;
@@ -1128,7 +1137,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
             if (el % TX >= tx || el / TX >= ty) continue;
             from_ring(top ? cur : lo, el, (N * NP) * NP + fn, qa, ta);
             from_ring(top ? hi : cur, el, fn, qb, tb);
-            face3(0, 2, P.gamma, qa, qb, ta, tb, fl, bad);
+            face3(MODE, 2, P.gamma, qa, qb, ta, tb, fl, bad);
             dst = (top ? fz_top : fz_bot) + (el * NF + fn) * 5;
           }
 #pragma unroll
@@ -1182,24 +1191,41 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
         double* sf = sf0 + (it & 1) * S::SF;
         // ---- volume fluxes of this node
         if (active) {
-          double qv[5], tv[5];
+          double qv[5], fl[5];
 #pragma unroll
-          for (int c = 0; c < 5; ++c) {
-            qv[c] = cur[le * BLK + c * NN + node] * xs;
-            tv[c] = cur[S::PL + le * BLK + c * NN + node];
+          for (int c = 0; c < 5; ++c) qv[c] = cur[le * BLK + c * NN + node] * xs;
+          if (MODE == 2) {
+            if (!admissible5(qv, P.gamma)) bad = true;
+            const Prim3 pq = prim3_of(qv, P.gamma);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              flux3_dir(qv, pq, d, fl);
+#pragma unroll
+              for (int c = 0; c < 5; ++c) sf[(d * 5 + c) * S::CONS + tid] = fl[c];
+            }
+            if (frozen) {  // (u, v, w, H, a) of the state for this step's JVPs
+              const double fv[5] = {pq.u[0], pq.u[1], pq.u[2], pq.H, pq.a};
+              const size_t e = ((size_t)z * ny + iy) * nx + ix;
+#pragma unroll
+              for (int c = 0; c < 5; ++c) frozen[(e * 5 + c) * NN + node] = fv[c];
+            }
+          } else {
+            double tv[5];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) tv[c] = cur[S::PL + le * BLK + c * NN + node];
+            const Prim3 tp = prim3_frozen(tv);
+            double Pv, Qv;
+            jac3_pre(tp, P.gamma, qv, Pv, Qv);
+            jac3_dir<0>(tp, Pv, Qv, qv, fl);
+#pragma unroll
+            for (int c = 0; c < 5; ++c) sf[(0 * 5 + c) * S::CONS + tid] = fl[c];
+            jac3_dir<1>(tp, Pv, Qv, qv, fl);
+#pragma unroll
+            for (int c = 0; c < 5; ++c) sf[(1 * 5 + c) * S::CONS + tid] = fl[c];
+            jac3_dir<2>(tp, Pv, Qv, qv, fl);
+#pragma unroll
+            for (int c = 0; c < 5; ++c) sf[(2 * 5 + c) * S::CONS + tid] = fl[c];
           }
-          const Prim3 tp = prim3_frozen(tv);
-          double Pv, Qv, fl[5];
-          jac3_pre(tp, P.gamma, qv, Pv, Qv);
-          jac3_dir<0>(tp, Pv, Qv, qv, fl);
-#pragma unroll
-          for (int c = 0; c < 5; ++c) sf[(0 * 5 + c) * S::CONS + tid] = fl[c];
-          jac3_dir<1>(tp, Pv, Qv, qv, fl);
-#pragma unroll
-          for (int c = 0; c < 5; ++c) sf[(1 * 5 + c) * S::CONS + tid] = fl[c];
-          jac3_dir<2>(tp, Pv, Qv, qv, fl);
-#pragma unroll
-          for (int c = 0; c < 5; ++c) sf[(2 * 5 + c) * S::CONS + tid] = fl[c];
         }
         strip_sync<S::CONS>();  // volume fluxes of plane z complete; every thread is past plane z - 1
         if (tid == 0 && prev_slot >= 0) {
@@ -1277,6 +1303,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
       mbar_arrive(&fempty[(it - 1) & 1]);
     }
   }
+  if (MODE == 2 && bad && fst) fst->domain_flag = 1;
   __syncthreads();
   if (!st) return;
   if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
@@ -1320,6 +1347,7 @@ class Euler3D : public OpDevice {
   // the plain march with face warps (EXPDG_E3_FW=0: the single-role march)
   static constexpr bool kFwOk = E3March<NP>::OK && E3MarchFW<NP>::OK;
   bool use_fw = kFwOk;
+  bool rhs_march = true;  // EXPDG_E3_RHS_TILE=1: the element-tile kernel for R(x) (residual, full_rhs)
   // the z-march also takes the DCGS2 pass-1 dots (EXPDG_E3_DOTS=0: off) on meshes of whole
   // tiles (the dot warps read the tile's elements as one contiguous block)
   static constexpr bool kDotFits = E3March<NP>::OK && E3March<NP, true>::FITS;
@@ -1406,9 +1434,14 @@ class Euler3D : public OpDevice {
       whole_tiles = d.nx % SM::TX == 0 && d.ny % SM::TY == 0;
       if (const char* v = std::getenv("EXPDG_E3_FW")) use_fw = use_fw && v[0] != '0';
     if (const char* v = std::getenv("EXPDG_E3_DBG")) P.dbg = std::atoi(v);
+    if (const char* v = std::getenv("EXPDG_E3_RHS_TILE")) rhs_march = v[0] != '1';
       if constexpr (kFwOk)
-        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      {
+        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         E3MarchFW<NP>::SMEM));
+        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        E3MarchFW<NP>::SMEM));
+      }
       if constexpr (kDotFits) {
         using SD = E3March<NP, true>;
         EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march<NP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1440,8 +1473,8 @@ class Euler3D : public OpDevice {
         }
         if constexpr (kFwOk) {
           if (use_fw) {
-            k_e3_phi_march_fw<NP><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
-                params(frozen), st, base, partials, b, nullptr, nullptr);
+            k_e3_phi_march_fw<NP, 0><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+                params(frozen), st, base, partials, b, nullptr, nullptr, nullptr, nullptr);
             return;
           }
         }
@@ -1456,8 +1489,13 @@ class Euler3D : public OpDevice {
     if (P.part) exchange(s, x, hb_(0), hb_(1));
     if constexpr (kFwOk) {
       if (which == 0 && use_march && use_fw && x != y) {  // y = L x through the z-march JVP (the phi cycle's kernel)
-        k_e3_phi_march_fw<NP><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
-            params(frozen), nullptr, nullptr, nullptr, BArgs{}, x, y);
+        k_e3_phi_march_fw<NP, 0><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+            params(frozen), nullptr, nullptr, nullptr, BArgs{}, x, y, nullptr, nullptr);
+        return;
+      }
+      if (which == 2 && use_march && use_fw && rhs_march && x != y) {  // y = R(x)
+        k_e3_phi_march_fw<NP, 2><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+            params(frozen), nullptr, nullptr, nullptr, BArgs{}, x, y, nullptr, nullptr);
         return;
       }
     }
@@ -1465,7 +1503,15 @@ class Euler3D : public OpDevice {
   }
   void launch_residual(cudaStream_t s, const double* u, double* r, PhiState* st, double*) override {
     if (P.part) exchange(s, u, hb_(0), hb_(1));
-    k_e3_apply<NP><<<grid, 256, 0, s>>>(params(nullptr), 2, u, r, st, frozen);
+    bool done = false;
+    if constexpr (kFwOk) {
+      if (use_march && use_fw && rhs_march && u != r) {
+        k_e3_phi_march_fw<NP, 2><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+            params(nullptr), nullptr, nullptr, nullptr, BArgs{}, u, r, st, frozen);
+        done = true;
+      }
+    }
+    if (!done) k_e3_apply<NP><<<grid, 256, 0, s>>>(params(nullptr), 2, u, r, st, frozen);
     if (P.part) exchange(s, frozen, hb_(2), hb_(3));  // frozen halo for this step's JVPs
   }
 };

@@ -33,8 +33,9 @@ def _both(monkeypatch, env, spec, u0, dt, steps=2):
     # the step residual through the element-tile kernel in both runs: the strip residual
     # (k_e2_phi_strip_fw<.., 2>) sums its face terms in another order than the tile kernel, and this
     # file pins the JVP kernels bit for bit (the residual kernels are pinned to the oracle in
-    # test_gpu_euler2d.py and against each other below)
+    # test_gpu_euler2d.py / test_gpu_extensions.py and against each other below)
     monkeypatch.setenv("EXPDG_E2_RHS_TILE", "1")
+    monkeypatch.setenv("EXPDG_E3_RHS_TILE", "1")
     out = []
     for v in ("1", "0"):
         monkeypatch.setenv(env, v)
@@ -97,6 +98,7 @@ def test_face_warps_on_slab_partitions_bit_identical(monkeypatch, kind, env):
     ranges = slab_ranges(axis, 3)
     res = []
     monkeypatch.setenv("EXPDG_E2_RHS_TILE", "1")
+    monkeypatch.setenv("EXPDG_E3_RHS_TILE", "1")
     for v in ("1", "0"):
         monkeypatch.setenv(env, v)
 
@@ -132,3 +134,44 @@ def test_strip_residual_matches_tile_kernel(monkeypatch, order, nx, ny, flux):
     assert sa == sb == "completed" and ia == ib
     assert np.max(np.abs(ra - rb)) <= 1e-13 * np.max(np.abs(rb))
     assert np.max(np.abs(ua - ub)) <= 1e-13 * np.max(np.abs(ub))
+
+
+@pytest.mark.parametrize("order,dims", [(3, (4, 4, 5)), (3, (5, 3, 4)), (3, (2, 2, 1)), (1, (9, 10, 3)), (1, (8, 16, 2))])
+def test_march_residual_matches_tile_kernel(monkeypatch, order, dims):
+    # the 3D counterpart: k_e3_phi_march_fw<.., 2> against k_e3_apply (mode 2)
+    nx, ny, nz = dims
+    rng = np.random.default_rng(order + nx + nz)
+    spec = pkg.OperatorSpec("euler3d", order, nx, ny, nz, box=(0, 1, 0, 2, 0, 1.5), euler_flux="lf")
+    u0 = random_state5(rng, nx * ny * nz, (order + 1) ** 3)
+    out = []
+    for v in ("0", "1"):
+        monkeypatch.setenv("EXPDG_E3_RHS_TILE", v)
+        c = pkg.Context(0, orth="dcgs2", fused=False)
+        op = pkg.Operator(c, spec)
+        rhs = to_host(op.full_rhs(to_dev(u0)))
+        r = pkg.integrate(c, op, to_dev(u0), "epi2", 2e-4, 4e-4, tol=1e-10, max_basis=12, orth_length=12)
+        out.append((rhs, to_host(r.u), list(r.iters_per_step), r.status))
+    (ra, ua, ia, sa), (rb, ub, ib, sb) = out
+    assert sa == sb == "completed" and ia == ib
+    assert np.max(np.abs(ra - rb)) <= 1e-13 * np.max(np.abs(rb))
+    assert np.max(np.abs(ua - ub)) <= 1e-13 * np.max(np.abs(ub))
+
+
+@pytest.mark.parametrize("kind", ["euler2d", "euler3d"])
+def test_strip_residual_reports_inadmissible_state(kind):
+    # a negative density reaches the domain flag through the MODE 2 kernels like through the tile
+    # kernels: integrate turns it into blew_up (proj/src/integrators.cpp:179-193)
+    rng = np.random.default_rng(2)
+    if kind == "euler2d":
+        spec = pkg.OperatorSpec("euler2d", 4, 7, 3, box=(0, 1, 0, 2, 0, 1), euler_flux="lf")
+        u0 = random_state(rng, 21, 25)
+    else:
+        spec = pkg.OperatorSpec("euler3d", 3, 3, 2, 3, box=(0, 1, 0, 2, 0, 1.5), euler_flux="lf")
+        u0 = random_state5(rng, 18, 64)
+    c = pkg.Context(0, fused=False)
+    op = pkg.Operator(c, spec)
+    good = pkg.integrate(c, op, to_dev(u0), "epi2", 2e-4, 2e-4, tol=1e-10, max_basis=12, orth_length=12)
+    assert good.status == "completed"
+    u0[7] = -1.0  # density of node 7 of element 0
+    bad = pkg.integrate(c, op, to_dev(u0), "epi2", 2e-4, 2e-4, tol=1e-10, max_basis=12, orth_length=12)
+    assert bad.status == "blew_up" and bad.blow_up_step == 1
