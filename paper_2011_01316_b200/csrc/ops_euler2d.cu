@@ -989,19 +989,23 @@ struct E2StripFW {
   static_assert(NBUF >= 4, "the face warps run up to two rows ahead of the node warps");
 };
 
-// MODE 0: the linear operator (the phi cycle's JVP).  MODE 2, standalone only: the full right-hand
+// MODE 0: the linear operator (the phi cycle's JVP).  Standalone only: MODE 2, the full right-hand
 // side R(x) (proj/src/euler.cpp:249-297: nonlinear volume fluxes, full LF / Roe face fluxes, no
 // frozen state), which also writes the frozen primitives of x for the step's JVPs (`frozen`) and
 // raises fst->domain_flag on an inadmissible state -- the residual of every step
-// (expdg_op_full_rhs, launch_residual).
-template <int NP, bool ROE, int CW, int MODE>
+// (expdg_op_full_rhs, launch_residual); MODE 1, the nonlinear remainder N(x) = R(x) - L x of the
+// split (expdg_op_apply_nonlinear, the EXPRB stages).
+template <int NP, bool ROE, int CW, int MODE, bool SOLO>
 __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>::PER_SM)
     k_e2_phi_strip_fw(E2P<NP> P, PhiState* st, double* base, double* partials, BArgs b, const double* xin,
                       double* yout, PhiState* fst, double* frozen) {
-  // st == nullptr: the standalone operator application y = L x / y = R(x) (expdg_op_apply_linear,
-  // expdg_op_full_rhs), x / y the caller's vectors, no augmentation tail, no reductions
+  // SOLO: the standalone operator application y = L x / N(x) / R(x) (expdg_op_apply_linear, ..),
+  // x / y the caller's vectors, no augmentation tail, no reductions (st is null).  A compile-time
+  // switch: the phi-cycle instantiation runs at 96 registers and a run-time one cost it spills
+  // (0.860 -> 0.935 ms per launch at C4).
+  static_assert(SOLO || MODE == 0, "the phi cycle applies the linear operator");
   constexpr int NARR = MODE == 2 ? 1 : 2;  // ring arrays in use: x (+ the frozen primitives)
-  if (MODE == 2 && fst && fst->stopped) return;
+  if (MODE != 0 && fst && fst->stopped) return;
   bool bad = false;
   using S = E2StripFW<NP, CW>;
   constexpr int NN = S::NN, W = S::W, BLK = S::BLK, NBUF = S::NBUF, N = NP - 1;
@@ -1019,9 +1023,9 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
   __shared__ double s_red[1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    s_go = st ? apply_go(st, base) : 1;
+    s_go = SOLO ? 1 : apply_go(st, base);
     if (s_go) {
-      if (st) {
+      if constexpr (!SOLO) {
         s_j = st->j;
         if (blockIdx.x == 0) {
           if (apply_stage(st, base) == 1) st->dots_fused = 0;
@@ -1055,8 +1059,8 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
   for (int q = tid; q < NP; q += blockDim.x) s_wq[q] = P.w[q];
   __syncthreads();
   if (!s_go) return;
-  const double* x = st ? base + (size_t)s_j * s_ld : xin;
-  double* y = st ? base + (size_t)(s_j + 1) * s_ld : yout;
+  const double* x = SOLO ? xin : base + (size_t)s_j * s_ld;
+  double* y = SOLO ? yout : base + (size_t)(s_j + 1) * s_ld;
   const double xs = s_xs, dt = s_dt;
   const int nx = P.nx, ny = P.ny;
   const int nstrips = (nx + W - 1) / W;
@@ -1221,24 +1225,31 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
           double qv[4], fx[4], fy[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) qv[c] = cur[(le + 1) * BLK + c * NN + node] * xs;
-          if (MODE == 2) {
+          if constexpr (MODE != 2) {
+            double tv[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tv[c] = cur[S::ROWD + (le + 1) * BLK + c * NN + node];
+            const Prim tp = prim_frozen(tv);
+            jac_apply_xy(tp, P.gamma, qv, fx, fy);
+          }
+          if constexpr (MODE != 0) {  // F(q) (MODE 2), F(q) - A(q~) q (MODE 1), as the tile kernel (e2_tile)
             if (!admissible4(qv, P.gamma)) bad = true;
             const Prim pq = prim_of(qv, P.gamma);
-            flux_dir(qv, pq, 0, fx);
-            flux_dir(qv, pq, 1, fy);
-            if (frozen) {  // (u, v, H, a | sqrt(rho)) of the state for this step's JVPs
+            double Fx[4], Fy[4];
+            flux_dir(qv, pq, 0, Fx);
+            flux_dir(qv, pq, 1, Fy);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              fx[c] = MODE == 1 ? Fx[c] - fx[c] : Fx[c];
+              fy[c] = MODE == 1 ? Fy[c] - fy[c] : Fy[c];
+            }
+            if (MODE == 2 && frozen) {  // (u, v, H, a | sqrt(rho)) of the state for this step's JVPs
               double fv[4];
               frozen_of<ROE>(qv, P.gamma, fv);
               const size_t e = (size_t)r * nx + ie;
 #pragma unroll
               for (int c = 0; c < 4; ++c) frozen[(e * 4 + c) * NN + node] = fv[c];
             }
-          } else {
-            double tv[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) tv[c] = cur[S::ROWD + (le + 1) * BLK + c * NN + node];
-            const Prim tp = prim_frozen(tv);
-            jac_apply_xy(tp, P.gamma, qv, fx, fy);
           }
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
@@ -1306,18 +1317,19 @@ __global__ void __launch_bounds__(E2StripFW<NP, CW>::THREADS, E2StripFW<NP, CW>:
       mbar_arrive(&fempty[(it - 1) & 1]);
     }
   }
-  if (MODE == 2 && bad && fst) fst->domain_flag = 1;
-  __syncthreads();
-  if (!st) return;
-  if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
-    const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
-    y[P.n + tid] = v;
-    if (st->tail_here) nacc = fma(v, v, nacc);
+  if (MODE != 0 && bad && fst) fst->domain_flag = 1;
+  if constexpr (!SOLO) {
+    __syncthreads();
+    if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
+      const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
+      y[P.n + tid] = v;
+      if (st->tail_here) nacc = fma(v, v, nacc);
+    }
+    const double tot = block_sum(nacc, s_buf);
+    if (tid == 0) s_red[0] = tot;
+    __syncthreads();
+    grid_reduce_last(s_red, 1, partials, 2 * kMaxSlots + 2, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
   }
-  const double tot = block_sum(nacc, s_buf);
-  if (tid == 0) s_red[0] = tot;
-  __syncthreads();
-  grid_reduce_last(s_red, 1, partials, 2 * kMaxSlots + 2, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
 // (u, v, H, a | sqrt(rho)) of q~ per node (proj/src/euler.cpp:15-24): the frozen
@@ -1370,11 +1382,32 @@ class Euler2D : public OpDevice {
     // the kernel is latency-bound, not DRAM-bound, and the lost CTAs cost more than the misses.
     const long long q = g / nstrips;
     if (fw_align && q >= 1 && P.ny % q == 0 && nstrips * q * 10 >= (long long)g * 8) g = (int)(nstrips * q);
+    if (st) {
+      if (roe)
+        k_e2_phi_strip_fw<NP, true, 4, 0, false><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, nullptr,
+                                                                                  nullptr, nullptr, nullptr);
+      else
+        k_e2_phi_strip_fw<NP, false, 4, 0, false><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, nullptr,
+                                                                                   nullptr, nullptr, nullptr);
+    } else {
+      if (roe)
+        k_e2_phi_strip_fw<NP, true, 4, 0, true><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, b, xin,
+                                                                                 yout, nullptr, nullptr);
+      else
+        k_e2_phi_strip_fw<NP, false, 4, 0, true><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, b, xin,
+                                                                                  yout, nullptr, nullptr);
+    }
+  }
+  // N(x) -> y through the strip kernel (MODE 1)
+  void launch_strip_nonlinear(cudaStream_t s, const E2P<NP>& p, const double* x, double* y) {
+    using SS = E2StripFW<NP, 4>;
+    const long long rows = (long long)((P.nx + SS::W - 1) / SS::W) * P.ny;
+    const int g = (int)std::max<long long>(1, std::min<long long>(rows, 148LL * fw2_per_sm));
     if (roe)
-      k_e2_phi_strip_fw<NP, true, 4, 0><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, xin, yout, nullptr,
-                                                                         nullptr);
+      k_e2_phi_strip_fw<NP, true, 4, 1, true><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, BArgs{}, x, y,
+                                                                         nullptr, nullptr);
     else
-      k_e2_phi_strip_fw<NP, false, 4, 0><<<g, SS::THREADS, SS::SMEM, s>>>(p, st, base, partials, b, xin, yout,
+      k_e2_phi_strip_fw<NP, false, 4, 1, true><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, BArgs{}, x, y,
                                                                           nullptr, nullptr);
   }
   // R(x) -> y through the strip kernel (MODE 2); frozen_out / fst may be null (expdg_op_full_rhs)
@@ -1384,10 +1417,10 @@ class Euler2D : public OpDevice {
     const long long rows = (long long)((P.nx + SS::W - 1) / SS::W) * P.ny;
     const int g = (int)std::max<long long>(1, std::min<long long>(rows, 148LL * fw2_per_sm));
     if (roe)
-      k_e2_phi_strip_fw<NP, true, 4, 2><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, BArgs{}, x, y,
+      k_e2_phi_strip_fw<NP, true, 4, 2, true><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, BArgs{}, x, y,
                                                                          fst, frozen_out);
     else
-      k_e2_phi_strip_fw<NP, false, 4, 2><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, BArgs{}, x, y,
+      k_e2_phi_strip_fw<NP, false, 4, 2, true><<<g, SS::THREADS, SS::SMEM, s>>>(p, nullptr, nullptr, nullptr, BArgs{}, x, y,
                                                                           fst, frozen_out);
   }
   template <int CW, bool DOT>
@@ -1501,18 +1534,26 @@ class Euler2D : public OpDevice {
     {  // the face-warp strip: attributes and occupancy here, never on the launch path (a runtime
        // call that synchronises the device must not run while another rank's collective spins)
       using SF = E2StripFW<NP, 4>;
-      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SF::SMEM));
-      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SF::SMEM));
-      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SF::SMEM));
-      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       SF::SMEM));
-      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw_per_sm, k_e2_phi_strip_fw<NP, false, 4, 0>,
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SF::SMEM));
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SF::SMEM));
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, false, 4, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SF::SMEM));
+      EXPDG_CUDA(cudaFuncSetAttribute(k_e2_phi_strip_fw<NP, true, 4, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SF::SMEM));
+      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw_per_sm, k_e2_phi_strip_fw<NP, false, 4, 0, false>,
                                                                SF::THREADS, SF::SMEM));
       fw_per_sm = std::max(1, fw_per_sm);
-      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw2_per_sm, k_e2_phi_strip_fw<NP, false, 4, 2>,
+      EXPDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fw2_per_sm, k_e2_phi_strip_fw<NP, false, 4, 2, true>,
                                                                SF::THREADS, SF::SMEM));
       fw2_per_sm = std::max(1, fw2_per_sm);
     }
@@ -1549,6 +1590,10 @@ class Euler2D : public OpDevice {
     }
     if (which == 2 && use_strip && use_fw && rhs_strip && x != y) {  // y = R(x)
       launch_strip_rhs(s, p, x, y, nullptr, nullptr);
+      return;
+    }
+    if (which == 1 && use_strip && use_fw && rhs_strip && x != y) {  // y = N(x) = R(x) - L x
+      launch_strip_nonlinear(s, p, x, y);
       return;
     }
     if (roe) k_e2_apply<NP, true><<<grid, 256, 0, s>>>(p, which, x, y, nullptr, nullptr);

@@ -920,17 +920,20 @@ struct E3MarchFW {
   static constexpr bool OK = B::OK && SMEM <= 232448 - 3072;
 };
 
-// MODE 0: the linear operator (the phi cycle's JVP).  MODE 2, standalone only: the full right-hand
+// MODE 0: the linear operator (the phi cycle's JVP).  Standalone only: MODE 2, the full right-hand
 // side R(x) (oracle/src/euler.cpp, Euler3DOperator: nonlinear volume fluxes, full LF face fluxes),
 // which also writes the frozen primitives of x for the step's JVPs and raises fst->domain_flag on
-// an inadmissible state -- the residual of every step (expdg_op_full_rhs, launch_residual).
-template <int NP, int MODE>
+// an inadmissible state -- the residual of every step (expdg_op_full_rhs, launch_residual);
+// MODE 1, the nonlinear remainder N(x) = R(x) - L x (expdg_op_apply_nonlinear, the EXPRB stages).
+template <int NP, int MODE, bool SOLO>
 __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
     k_e3_phi_march_fw(E3P<NP> P, PhiState* st, double* base, double* partials, BArgs b, const double* xin,
                       double* yout, PhiState* fst, double* frozen) {
-  // st == nullptr: the standalone operator application y = L x / y = R(x) (expdg_op_apply_linear,
-  // expdg_op_full_rhs), x / y the caller's vectors, no augmentation tail, no reductions
-  if (MODE == 2 && fst && fst->stopped) return;
+  // SOLO: the standalone operator application y = L x / N(x) / R(x) (expdg_op_apply_linear, ..),
+  // x / y the caller's vectors, no augmentation tail, no reductions (st is null); a compile-time
+  // switch so that the phi-cycle instantiation keeps its registers
+  static_assert(SOLO || MODE == 0, "the phi cycle applies the linear operator");
+  if (MODE != 0 && fst && fst->stopped) return;
   bool bad = false;
   using S = E3MarchFW<NP>;
   constexpr int NN = S::NN, NF = S::NF, BLK = S::BLK, TX = S::TX, TY = S::TY, NBUF = S::NBUF, N = NP - 1;
@@ -947,9 +950,9 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
   __shared__ double s_red[1];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    s_go = st ? apply_go(st, base) : 1;
+    s_go = SOLO ? 1 : apply_go(st, base);
     if (s_go) {
-      if (st) {
+      if constexpr (!SOLO) {
         s_j = st->j;
         if (blockIdx.x == 0) {
           if (apply_stage(st, base) == 1) st->dots_fused = 0;
@@ -981,8 +984,8 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
   }
   __syncthreads();
   if (!s_go) return;
-  const double* x = st ? base + (size_t)s_j * s_ld : xin;
-  double* y = st ? base + (size_t)(s_j + 1) * s_ld : yout;
+  const double* x = SOLO ? xin : base + (size_t)s_j * s_ld;
+  double* y = SOLO ? yout : base + (size_t)(s_j + 1) * s_ld;
   const double xs = s_xs, dt = s_dt;
   const int nx = P.nx, ny = P.ny, nz = P.nz;
   const int ntx = (nx + TX - 1) / TX, nty = (ny + TY - 1) / TY;
@@ -1194,22 +1197,7 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
           double qv[5], fl[5];
 #pragma unroll
           for (int c = 0; c < 5; ++c) qv[c] = cur[le * BLK + c * NN + node] * xs;
-          if (MODE == 2) {
-            if (!admissible5(qv, P.gamma)) bad = true;
-            const Prim3 pq = prim3_of(qv, P.gamma);
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              flux3_dir(qv, pq, d, fl);
-#pragma unroll
-              for (int c = 0; c < 5; ++c) sf[(d * 5 + c) * S::CONS + tid] = fl[c];
-            }
-            if (frozen) {  // (u, v, w, H, a) of the state for this step's JVPs
-              const double fv[5] = {pq.u[0], pq.u[1], pq.u[2], pq.H, pq.a};
-              const size_t e = ((size_t)z * ny + iy) * nx + ix;
-#pragma unroll
-              for (int c = 0; c < 5; ++c) frozen[(e * 5 + c) * NN + node] = fv[c];
-            }
-          } else {
+          if constexpr (MODE == 0) {  // one direction at a time: 5 live flux values, not 15
             double tv[5];
 #pragma unroll
             for (int c = 0; c < 5; ++c) tv[c] = cur[S::PL + le * BLK + c * NN + node];
@@ -1225,6 +1213,33 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
             jac3_dir<2>(tp, Pv, Qv, qv, fl);
 #pragma unroll
             for (int c = 0; c < 5; ++c) sf[(2 * 5 + c) * S::CONS + tid] = fl[c];
+          } else {  // F(q) (MODE 2), F(q) - A(q~) q (MODE 1), as the tile kernel (e3_tile)
+            double lin[3][5];
+            if constexpr (MODE == 1) {
+              double tv[5];
+#pragma unroll
+              for (int c = 0; c < 5; ++c) tv[c] = cur[S::PL + le * BLK + c * NN + node];
+              const Prim3 tp = prim3_frozen(tv);
+              double Pv, Qv;
+              jac3_pre(tp, P.gamma, qv, Pv, Qv);
+              jac3_dir<0>(tp, Pv, Qv, qv, lin[0]);
+              jac3_dir<1>(tp, Pv, Qv, qv, lin[1]);
+              jac3_dir<2>(tp, Pv, Qv, qv, lin[2]);
+            }
+            if (!admissible5(qv, P.gamma)) bad = true;
+            const Prim3 pq = prim3_of(qv, P.gamma);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              flux3_dir(qv, pq, d, fl);
+#pragma unroll
+              for (int c = 0; c < 5; ++c) sf[(d * 5 + c) * S::CONS + tid] = MODE == 1 ? fl[c] - lin[d][c] : fl[c];
+            }
+            if (MODE == 2 && frozen) {  // (u, v, w, H, a) of the state for this step's JVPs
+              const double fv[5] = {pq.u[0], pq.u[1], pq.u[2], pq.H, pq.a};
+              const size_t e = ((size_t)z * ny + iy) * nx + ix;
+#pragma unroll
+              for (int c = 0; c < 5; ++c) frozen[(e * 5 + c) * NN + node] = fv[c];
+            }
           }
         }
         strip_sync<S::CONS>();  // volume fluxes of plane z complete; every thread is past plane z - 1
@@ -1303,18 +1318,19 @@ __global__ void __launch_bounds__(E3MarchFW<NP>::THREADS, 1)
       mbar_arrive(&fempty[(it - 1) & 1]);
     }
   }
-  if (MODE == 2 && bad && fst) fst->domain_flag = 1;
-  __syncthreads();
-  if (!st) return;
-  if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
-    const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
-    y[P.n + tid] = v;
-    if (st->tail_here) nacc = fma(v, v, nacc);
+  if (MODE != 0 && bad && fst) fst->domain_flag = 1;
+  if constexpr (!SOLO) {
+    __syncthreads();
+    if (blockIdx.x == 0 && tid < kTailPad) {  // replicated tail, counted on rank 0
+      const double v = (tid + 1 < b.p) ? dt * s_xt[tid + 1] : 0.0;
+      y[P.n + tid] = v;
+      if (st->tail_here) nacc = fma(v, v, nacc);
+    }
+    const double tot = block_sum(nacc, s_buf);
+    if (tid == 0) s_red[0] = tot;
+    __syncthreads();
+    grid_reduce_last(s_red, 1, partials, 2 * kMaxSlots + 2, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
   }
-  const double tot = block_sum(nacc, s_buf);
-  if (tid == 0) s_red[0] = tot;
-  __syncthreads();
-  grid_reduce_last(s_red, 1, partials, 2 * kMaxSlots + 2, &st->ticket[4], [&](int, double v) { st->rs().nrmA = v; });
 }
 
 __global__ void k_e3_freeze(const double* __restrict__ q, long long nelem, int nn, double gamma,
@@ -1437,9 +1453,13 @@ class Euler3D : public OpDevice {
     if (const char* v = std::getenv("EXPDG_E3_RHS_TILE")) rhs_march = v[0] != '1';
       if constexpr (kFwOk)
       {
-        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP, 0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         E3MarchFW<NP>::SMEM));
-        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        E3MarchFW<NP>::SMEM));
+        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        E3MarchFW<NP>::SMEM));
+        EXPDG_CUDA(cudaFuncSetAttribute(k_e3_phi_march_fw<NP, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         E3MarchFW<NP>::SMEM));
       }
       if constexpr (kDotFits) {
@@ -1473,7 +1493,7 @@ class Euler3D : public OpDevice {
         }
         if constexpr (kFwOk) {
           if (use_fw) {
-            k_e3_phi_march_fw<NP, 0><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+            k_e3_phi_march_fw<NP, 0, false><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
                 params(frozen), st, base, partials, b, nullptr, nullptr, nullptr, nullptr);
             return;
           }
@@ -1489,12 +1509,17 @@ class Euler3D : public OpDevice {
     if (P.part) exchange(s, x, hb_(0), hb_(1));
     if constexpr (kFwOk) {
       if (which == 0 && use_march && use_fw && x != y) {  // y = L x through the z-march JVP (the phi cycle's kernel)
-        k_e3_phi_march_fw<NP, 0><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+        k_e3_phi_march_fw<NP, 0, true><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
             params(frozen), nullptr, nullptr, nullptr, BArgs{}, x, y, nullptr, nullptr);
         return;
       }
       if (which == 2 && use_march && use_fw && rhs_march && x != y) {  // y = R(x)
-        k_e3_phi_march_fw<NP, 2><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+        k_e3_phi_march_fw<NP, 2, true><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+            params(frozen), nullptr, nullptr, nullptr, BArgs{}, x, y, nullptr, nullptr);
+        return;
+      }
+      if (which == 1 && use_march && use_fw && rhs_march && x != y) {  // y = N(x) = R(x) - L x
+        k_e3_phi_march_fw<NP, 1, true><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
             params(frozen), nullptr, nullptr, nullptr, BArgs{}, x, y, nullptr, nullptr);
         return;
       }
@@ -1506,7 +1531,7 @@ class Euler3D : public OpDevice {
     bool done = false;
     if constexpr (kFwOk) {
       if (use_march && use_fw && rhs_march && u != r) {
-        k_e3_phi_march_fw<NP, 2><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
+        k_e3_phi_march_fw<NP, 2, true><<<march_grid, E3MarchFW<NP>::THREADS, E3MarchFW<NP>::SMEM, s>>>(
             params(nullptr), nullptr, nullptr, nullptr, BArgs{}, u, r, st, frozen);
         done = true;
       }

@@ -128,11 +128,15 @@ def test_strip_residual_matches_tile_kernel(monkeypatch, order, nx, ny, flux):
         c = pkg.Context(0, orth="dcgs2", fused=False)
         op = pkg.Operator(c, spec)
         rhs = to_host(op.full_rhs(to_dev(u0)))
-        r = pkg.integrate(c, op, to_dev(u0), "epi2", 2e-4, 4e-4, tol=1e-10, max_basis=12, orth_length=12)
-        out.append((rhs, to_host(r.u), list(r.iters_per_step), r.status))
-    (ra, ua, ia, sa), (rb, ub, ib, sb) = out
+        op.linearize(to_dev(u0))
+        x = 1.0 + 0.1 * np.cos(np.arange(u0.size))
+        nl = to_host(op.apply_nonlinear(to_dev(u0 * x)))  # MODE 1: N at a state away from the frozen one
+        r = pkg.integrate(c, op, to_dev(u0), "exprb32", 2e-4, 4e-4, tol=1e-10, max_basis=12, orth_length=12)
+        out.append((rhs, to_host(r.u), list(r.iters_per_step), r.status, nl))
+    (ra, ua, ia, sa, na), (rb, ub, ib, sb, nb) = out
     assert sa == sb == "completed" and ia == ib
     assert np.max(np.abs(ra - rb)) <= 1e-13 * np.max(np.abs(rb))
+    assert np.max(np.abs(na - nb)) <= 1e-13 * np.max(np.abs(rb))
     assert np.max(np.abs(ua - ub)) <= 1e-13 * np.max(np.abs(ub))
 
 
@@ -149,11 +153,15 @@ def test_march_residual_matches_tile_kernel(monkeypatch, order, dims):
         c = pkg.Context(0, orth="dcgs2", fused=False)
         op = pkg.Operator(c, spec)
         rhs = to_host(op.full_rhs(to_dev(u0)))
-        r = pkg.integrate(c, op, to_dev(u0), "epi2", 2e-4, 4e-4, tol=1e-10, max_basis=12, orth_length=12)
-        out.append((rhs, to_host(r.u), list(r.iters_per_step), r.status))
-    (ra, ua, ia, sa), (rb, ub, ib, sb) = out
+        op.linearize(to_dev(u0))
+        x = 1.0 + 0.1 * np.cos(np.arange(u0.size))
+        nl = to_host(op.apply_nonlinear(to_dev(u0 * x)))  # MODE 1: N at a state away from the frozen one
+        r = pkg.integrate(c, op, to_dev(u0), "exprb32", 2e-4, 4e-4, tol=1e-10, max_basis=12, orth_length=12)
+        out.append((rhs, to_host(r.u), list(r.iters_per_step), r.status, nl))
+    (ra, ua, ia, sa, na), (rb, ub, ib, sb, nb) = out
     assert sa == sb == "completed" and ia == ib
     assert np.max(np.abs(ra - rb)) <= 1e-13 * np.max(np.abs(rb))
+    assert np.max(np.abs(na - nb)) <= 1e-13 * np.max(np.abs(rb))
     assert np.max(np.abs(ua - ub)) <= 1e-13 * np.max(np.abs(ub))
 
 
