@@ -170,7 +170,7 @@ int expdg_ctx_comm(const expdg_ctx* ctx, int* rank, int* size); /* 0, 1 without 
  *         64-byte CUDA IPC handle), the handles are all-gathered (rank order), every rank calls
  *         expdg_ctx_attach_peer.
  *   Threads of one process, one device (tests): expdg_peer_group_create + expdg_ctx_attach_peer_local.
- * Every device-side wait for a peer is bounded (EXPDG_PEER_TIMEOUT_MS, default 20000): a peer that
+ * Every device-side wait for a peer is bounded (EXPDG_PEER_TIMEOUT_MS, default 60000; 0 = unbounded): a peer that
  * never arrives ends expdg_phi_combination / expdg_integrate with EXPDG_E_COMM instead of hanging
  * the GPU; the results of that call are invalid. */
 typedef struct expdg_peer_group expdg_peer_group;

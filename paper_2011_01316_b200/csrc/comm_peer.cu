@@ -55,7 +55,7 @@ struct PeerView {
   unsigned long long* peer[kPeerMax];
   int rank, size;
   long long halo_cap;
-  unsigned long long wait_ns;  // bound of every wait for a peer (EXPDG_PEER_TIMEOUT_MS, default 20 s)
+  unsigned long long wait_ns;  // bound of every wait for a peer (EXPDG_PEER_TIMEOUT_MS, default 60 s; 0: none)
 };
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
@@ -195,9 +195,11 @@ class PeerComm : public Comm {
   PeerComm(const PeerView& view, std::shared_ptr<void> k, HostBarrier* b) : v(view), keep(std::move(k)), hb(b) {
     rank = v.rank;
     size = v.size;
-    long long ms = 20000;
-    if (const char* e = std::getenv("EXPDG_PEER_TIMEOUT_MS")) ms = std::max(1LL, std::atoll(e));
-    v.wait_ns = (unsigned long long)ms * 1000000ull;
+    // 60 s: far above any skew between ranks that entered the same call (the collectives of one
+    // Krylov cycle are microseconds apart), short enough that a dead peer ends the run; 0 = unbounded
+    long long ms = 60000;
+    if (const char* e = std::getenv("EXPDG_PEER_TIMEOUT_MS")) ms = std::max(0LL, std::atoll(e));
+    v.wait_ns = ms == 0 ? ~0ull : (unsigned long long)ms * 1000000ull;
   }
   bool graph_capturable() const override { return true; }
   void host_barrier() override {
