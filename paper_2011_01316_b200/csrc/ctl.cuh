@@ -317,7 +317,7 @@ __device__ __forceinline__ void set_window(PhiState* st, int j) {
 // ||u - V a||, breakdown test of proj/src/phi.cpp:104-108 one cycle late) and write
 // column j provisionally from a, b, <u,w> and H.  Thread 0 of k_ctl.
 // Returns 1 on breakdown (mc = j), else 0.
-static __device__ int dcgs_finish(PhiState* st) {
+static __device__ int dcgs_finish(PhiState* st, double* Hst) {
   const int j = st->j;
   const double nd = (double)st->n;
   // stage-1 JVP 32n + dots pass 8n(j + 2) (with the dots in the JVP sweep, dots_fused: u and w
@@ -329,7 +329,7 @@ static __device__ int dcgs_finish(PhiState* st) {
   st->pl_ready = st->pl_look ? j + 1 : -1;
   double beta = 1.0;
   // distinct PhiState arrays: restrict lets the loads of the loops below be issued ahead
-  double* __restrict__ Hm = st->H;
+  double* __restrict__ Hm = Hst;
   const double* __restrict__ da = st->dc_a;
   const double* __restrict__ db = st->dc_b;
   const double* __restrict__ dg = st->dc_g;
@@ -338,13 +338,13 @@ static __device__ int dcgs_finish(PhiState* st) {
 #pragma unroll 4
     for (int l = 0; l < j; ++l) Hm[l * kMaxBasis + (j - 1)] += da[l];
     if (beta <= 1e-14 * fmax(st->pre_prev, 1e-300)) {
-      st->H[j * kMaxBasis + (j - 1)] = 0.0;
+      Hst[j * kMaxBasis + (j - 1)] = 0.0;
       st->mc = j;
       st->breakdown = 1;
       st->pl_ready = -1;
       return 1;
     }
-    st->H[j * kMaxBasis + (j - 1)] = beta;
+    Hst[j * kMaxBasis + (j - 1)] = beta;
     st->scale[j] = 1.0 / sqrt(st->red.nrmU);  // V_j = slot_j / ||slot_j||
   }
   const double ib = 1.0 / beta;
@@ -362,7 +362,7 @@ static __device__ int dcgs_finish(PhiState* st) {
   // beta); the next cycle's reorthogonalisation adds the remainder
   const double gj = j >= 1 ? beta * st->dc_a[j - 1] : 0.0;
   const double hj = st->dc_gp - gj * ib;
-  if (store) st->H[j * kMaxBasis + j] = hj;
+  if (store) Hst[j * kMaxBasis + j] = hj;
   hh = fma(hj, hj, hh);
   st->scale[j + 1] = ib;                                   // u_{j+1} = slot_{j+1} / beta
   st->pre_prev = sqrt(st->red.nrmW * ib * ib + hh);        // ||dt A V_j|| (incl. the augmentation)
@@ -385,8 +385,11 @@ __device__ __forceinline__ void set_pipe(PhiState* st) {
   st->pl_direct = !(pipe && (a == ACT_EXTEND || a == ACT_AVNORM) && st->pl_ready == st->j && !restart);
 }
 
+// Hg: the Hessenberg storage when `st` is a copy of the state's header only (k_ctl: the header in
+// shared memory, H left in global memory); null: st->H.
 __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W, double* Wsm, int ws_cap,
-                                         cudaGraphConditionalHandle cond, int use_graph) {
+                                         cudaGraphConditionalHandle cond, int use_graph, double* Hg = nullptr) {
+  double* const Hst = Hg ? Hg : st->H;
   __shared__ int s_phase, s_exit, s_zeroH, s_done;
   const int tid = threadIdx.x;
   // CGS2 / IOP column j of H from the two passes' sums (proj/src/phi.cpp:96-104), one entry per
@@ -397,7 +400,7 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
     for (int i = st->j0 + tid; i <= j; i += blockDim.x) {
       const double sci = st->scale[i];
       const double h1 = sci * st->red.dotA[i];
-      st->H[i * kMaxBasis + j] = full ? h1 + sci * st->red.dotB[i] : h1;
+      Hst[i * kMaxBasis + j] = full ? h1 + sci * st->red.dotB[i] : h1;
     }
   }
   if (tid == 0) {
@@ -414,7 +417,7 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
           break;
         case ACT_EXTEND: {
           if (st->dcgs) {
-            if (dcgs_finish(st)) {
+            if (dcgs_finish(st, Hst)) {
               phase = PH_POST;  // breakdown in column j-1: no avnorm
             } else {
               st->iterations++;
@@ -440,12 +443,12 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
           const double pre_norm = sqrt(st->red.nrmA);
           const double hnext = sqrt(st->red.nrmC);
           st->pre_norm = pre_norm;
-          st->H[(j + 1) * kMaxBasis + j] = hnext;
+          Hst[(j + 1) * kMaxBasis + j] = hnext;
           const int mc = j + 1;
           st->mc = mc;
           st->iterations++;
           if (hnext <= 1e-14 * fmax(pre_norm, 1e-300)) {
-            st->H[mc * kMaxBasis + (mc - 1)] = 0.0;
+            Hst[mc * kMaxBasis + (mc - 1)] = 0.0;
             st->breakdown = 1;
             phase = PH_POST;
           } else {
@@ -462,7 +465,7 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
         }
         case ACT_AVNORM:
           if (st->dcgs) {  // the avnorm cycle extends column mc provisionally as well
-            if (dcgs_finish(st)) {
+            if (dcgs_finish(st, Hst)) {
               st->avnorm = 0.0;  // breakdown in column mc-1 (the reference computes no avnorm)
             } else {
               st->iterations++;
@@ -514,7 +517,7 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
       for (int idx = tid; idx < N * N; idx += blockDim.x) {
         const int i = idx / N, j = idx % N;
         double v = 0.0;
-        if (i <= mc && j < mc) v = st->H[i * kMaxBasis + j];
+        if (i <= mc && j < mc) v = Hst[i * kMaxBasis + j];
         if (i == mc + 1 && j == mc) v = 1.0;
         Wx[idx] = h * v;
       }
@@ -640,7 +643,7 @@ __device__ __forceinline__ void ctl_body(PhiState* st, double* slot0, double* W,
   }
   if (s_zeroH) {
     const int rows = st->mmax + 1;
-    for (int idx = tid; idx < rows * kMaxBasis; idx += blockDim.x) st->H[idx] = 0.0;
+    for (int idx = tid; idx < rows * kMaxBasis; idx += blockDim.x) Hst[idx] = 0.0;
   }
   if (tid == 0) {
     st->phase = s_phase;

@@ -330,16 +330,27 @@ void device_expm(cudaStream_t s, double* work, int N, double* out) { k_expm<<<1,
 // The controller; the expm workspace (9 (mmax+2)^2 doubles) lives in dynamic shared memory
 // when it fits (ws_cap > 0), else in the global `W`: the LU solve and the matrix products
 // of an expm at N = 42 take ~0.35 ms out of L2 and a fraction of it out of shared memory.
-constexpr int kCtlWsMax = 26000;  // doubles of dynamic shared memory (203 KB)
+// The controller works on a copy of the state's header (everything before H, 13 KB) in shared
+// memory: its thread-0 bookkeeping is a chain of dependent accesses through the state pointer,
+// ~300-cycle L2 round trips each out of global memory (k_ctl took 20-26 us per cycle: 6 % of a C3
+// step).  H stays in global memory (a column per cycle, the whole matrix only at the decisions).
+constexpr int kCtlWsMax = 24500;  // doubles of dynamic shared memory for the expm workspace (191 KB)
+constexpr int kCtlHdrDoubles = (int)((kPhiHOff + 15) / 16 * 2);
 __global__ void __launch_bounds__(256) k_ctl(PhiState* st, double* slot0, double* W,
                                              cudaGraphConditionalHandle cond, int use_graph, int ws_cap) {
   extern __shared__ __align__(16) double ctl_ws[];
-  ctl_body(st, slot0, W, ctl_ws, ws_cap, cond, use_graph);
+  PhiState* ss = reinterpret_cast<PhiState*>(ctl_ws);
+  state_copy(reinterpret_cast<unsigned char*>(ss), reinterpret_cast<const unsigned char*>(st), 0);
+  __syncthreads();
+  ctl_body(ss, slot0, W, ctl_ws + kCtlHdrDoubles, ws_cap, cond, use_graph, st->H);
+  __syncthreads();
+  state_copy(reinterpret_cast<unsigned char*>(st), reinterpret_cast<const unsigned char*>(ss), 0);
 }
 static int ctl_ws_doubles(int mmax) {
   const long long need = 9LL * (mmax + 2) * (mmax + 2);
   return (mmax >= 0 && need <= kCtlWsMax) ? (int)need : 0;
 }
+static size_t ctl_smem_bytes(int mmax) { return sizeof(double) * ((size_t)kCtlHdrDoubles + ctl_ws_doubles(mmax)); }
 
 // Sets action = START / DONE after the init reduction (separate tiny kernel so the
 // decision sees the fully reduced norms).
@@ -412,7 +423,8 @@ Engine::Engine(int dev) : device(dev) {
   if (const char* v = std::getenv("EXPDG_ORTH"))
     use_dcgs = std::strcmp(v, "cgs2") == 0 ? 0 : (std::strcmp(v, "dcgs2") == 0 ? 2 : 1);
   dcgs_init_attrs(maxsm);
-  EXPDG_CUDA(cudaFuncSetAttribute(k_ctl, cudaFuncAttributeMaxDynamicSharedMemorySize, kCtlWsMax * 8));
+  EXPDG_CUDA(cudaFuncSetAttribute(k_ctl, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(double) * (kCtlWsMax + kCtlHdrDoubles)));
 }
 
 Engine::~Engine() {
@@ -621,7 +633,7 @@ void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraph
       reduce(s);
       ++body_launches;
     }
-    k_ctl<<<1, 256, (size_t)ctl_ws_doubles(mmax) * 8, s>>>(st, slot(0), ework, h, use_graph, ctl_ws_doubles(mmax));
+    k_ctl<<<1, 256, ctl_smem_bytes(mmax), s>>>(st, slot(0), ework, h, use_graph, ctl_ws_doubles(mmax));
     ++body_launches;
     return;
   }
@@ -642,7 +654,7 @@ void Engine::launch_body(cudaStream_t s, OpDevice& op, const BArgs& b, cudaGraph
     reduce(s);
     ++body_launches;
   }
-  k_ctl<<<1, 256, (size_t)ctl_ws_doubles(mmax) * 8, s>>>(st, slot(0), ework, h, use_graph, ctl_ws_doubles(mmax));
+  k_ctl<<<1, 256, ctl_smem_bytes(mmax), s>>>(st, slot(0), ework, h, use_graph, ctl_ws_doubles(mmax));
   ++body_launches;
 }
 
