@@ -10,7 +10,7 @@ timeout 900 python -m pytest tests -m gpu -x -q > $o/${tag}_gputests.log 2>&1; t
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > $o/${tag}_smoke.log 2>&1; tail -1 $o/${tag}_smoke.log
 timeout 600 python bench.py --impl reference > $o/${tag}_bench_reference_arm.json 2>$o/${tag}_err.log
 timeout 600 python bench.py > $o/${tag}_bench_c4_default.json 2>>$o/${tag}_err.log
-timeout 600 python bench.py --steps 10 --warmup 5 > $o/${tag}_bench_c4.json 2>>$o/${tag}_err.log
+timeout 600 python bench.py --steps 20 --warmup 5 > $o/${tag}_bench_c4.json 2>>$o/${tag}_err.log
 timeout 600 python bench.py --config C3 --steps 10 --warmup 5 > $o/${tag}_bench_c3.json 2>>$o/${tag}_err.log
 timeout 600 python bench.py --config C5 --steps 5 --warmup 3 > $o/${tag}_bench_c5.json 2>>$o/${tag}_err.log
 timeout 300 python tools/c1_profile.py > $o/${tag}_c1_profile.log 2>&1
