@@ -990,17 +990,39 @@ __global__ void __launch_bounds__(kClusterThreads, 1)
     ++round;
   };
   // this CTA's <V_{i0+i}, y> for i < k, one warp per vector (the tail counts on rank 0)
+  // (two vectors per warp and pass: their FMA chains and shuffle reductions interleave; each
+  // vector's sum keeps its order, so the totals are bit-identical to one vector per pass)
   auto local_dots = [&](int i0, int k, const double* y) {
-    for (int i = wid; i < k; i += T / 32) {
+    constexpr int NW = kClusterThreads / 32;
+    for (int i = wid; i < k; i += 2 * NW) {
+      const bool two = i + NW < k;
       const double* v = V + (size_t)(i0 + i) * lds;
-      double p0 = 0.0, p1 = 0.0;
+      const double* w = V + (size_t)(i0 + (two ? i + NW : i)) * lds;
+      double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
       for (int d = lane; d < nloc; d += 64) {
-        p0 = fma(v[d], y[d], p0);
-        if (d + 32 < nloc) p1 = fma(v[d + 32], y[d + 32], p1);
+        const double y0 = y[d];
+        p0 = fma(v[d], y0, p0);
+        q0 = fma(w[d], y0, q0);
+        if (d + 32 < nloc) {
+          const double y1 = y[d + 32];
+          p1 = fma(v[d + 32], y1, p1);
+          q1 = fma(w[d + 32], y1, q1);
+        }
       }
-      if (s_tailhere && lane < kTailPad) p0 = fma(v[tail_at + lane], y[tail_at + lane], p0);
-      const double p = warp_sum(p0 + p1);
-      if (lane == 0) s_mine[i] = p;
+      if (s_tailhere && lane < kTailPad) {
+        p0 = fma(v[tail_at + lane], y[tail_at + lane], p0);
+        q0 = fma(w[tail_at + lane], y[tail_at + lane], q0);
+      }
+      double p = p0 + p1, q = q0 + q1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        p += __shfl_xor_sync(0xffffffffu, p, o);
+        q += __shfl_xor_sync(0xffffffffu, q, o);
+      }
+      if (lane == 0) {
+        s_mine[i] = p;
+        if (two) s_mine[i + NW] = q;
+      }
     }
     __syncthreads();
   };
